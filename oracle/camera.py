@@ -1,0 +1,170 @@
+"""Single-lens and plenoptic camera models on slice-collapsed volumes (paper §2.6, §3).
+
+Conventions (readings Z1-Z13):
+
+* angular plane = main lens; s <-> x^r, t <-> y^r of the camera-aligned
+  (rotated) volume; slice n sits z_n = D_scene + (n - (Nz-1)/2) Dz^r in front of the
+  lens (object z increases away from the camera, Z13), X^{0q} = R_f o T_{z_n};
+* single-lens detector D behind the lens: X^{0d} = T_{-D};
+* plenoptic: array plane X^{0a} = T_{-D_mu_m}; lenslet mu (centre c_mu,
+  focal f_mu, detector b = D_d_mu behind the array):
+  X^{0mu} = T_{-D_mu_m} o R_{f_mu}(c_mu)^{-1} o T_{-b}  (P:1016 writes X^{0a} o R_mu o T_Ddmu);
+* mask M_mu: array cell j is open for lenslet mu iff its centre lies in
+  [c_mu - fill*pitch/2, c_mu + fill*pitch/2) (rasterised support; Z9/Z10);
+  M = sum_mu M_mu;
+* slice collapse: w^n_k = Dz^r x^r_n for every view k;
+* normalisation: the literal building blocks f^p = B f^q / V^p and
+  y = sqrt(V^d) sum_k f^d_k (reading Z7):
+    single-lens:  y = (sqrt(V^d)/V^d) sum_k sum_n B^{d q_n}_k Dz x^r_n
+    plenoptic, factored order eqn,plenoptic,factor:
+      a_k = (1/V^a) sum_n B^{a q_n}_k Dz x^r_n
+      y   = sum_k sum_mu (sqrt(V^mu)/V^mu) B^{mu a}_k M_mu a_k
+* memory layout of a plane field: array [t, s] (s fastest); the separable
+  product (B_s (x) B_t) f acts as  B_t @ F @ B_s^T.
+
+The plenoptic S3 operator per axis S_k = sum_mu B^{mu a}_k M_mu is formed literally
+(one transport per lenslet) -- the oracle does not use the adjoint symmetry; its
+adjoint is the literal transpose of every factor.
+"""
+import math
+
+import numpy as np
+import scipy.sparse as sp
+
+from .optics import compose, invert, lens, translate
+from .transport import Plane, angular_centres, basis_volume, transport_dense, transport_sparse
+
+SINGLE, PLENOPTIC = 0, 1
+
+
+class CameraModel:
+    """Camera c acting on its rotated volume x^r (shape (nz, ny, nx), voxel sizes vox_r)."""
+
+    def __init__(self, cam, dims, vox_r, dense=False):
+        self.cam = cam
+        self.nx, self.ny, self.nz = dims
+        self.vox_r = vox_r
+        self.type = cam["type"]
+        self.basis = cam["basis"]
+        self.ks, self.kt = cam["k_s"], cam["k_t"]
+        self.d0 = (cam["ap_s"] / cam["k_s"], cam["ap_t"] / cam["k_t"])
+        self.sk = (angular_centres(self.ks, self.d0[0]), angular_centres(self.kt, self.d0[1]))
+        self.dz = vox_r[2]
+        self.z = [cam["d_scene"] + (n - (self.nz - 1) * 0.5) * self.dz for n in range(self.nz)]
+        build = transport_dense if dense else (lambda *a: transport_sparse(*a))
+        self._dense = dense
+        n_src = (self.nx, self.ny)
+        fm = cam["f_main"]
+        self.slice_planes = [[Plane(n_src[ax], vox_r[ax], compose(lens(fm), translate(z))) for z in self.z]
+                             for ax in range(2)]
+        det_n = (cam["n_s"], cam["n_t"])
+        det_d = (cam["px_s"], cam["px_t"])
+        if self.type == SINGLE:
+            self.det_planes = [Plane(det_n[ax], det_d[ax], translate(-cam["d_det"])) for ax in range(2)]
+            dst = self.det_planes
+            vd = basis_volume(dst[0], self.d0[0]) * basis_volume(dst[1], self.d0[1])
+            self.scale_s1 = self.dz * math.sqrt(vd) / vd
+            self.scale_s3 = None
+        else:
+            nl = (cam["nl_s"], cam["nl_t"])
+            na = cam["n_a"]
+            self.pitch = tuple(det_n[ax] * det_d[ax] / nl[ax] for ax in range(2))
+            self.array_planes = [Plane(nl[ax] * na, self.pitch[ax] / na, translate(-cam["d_mu_m"]))
+                                 for ax in range(2)]
+            b = cam["d_d_mu"]
+            self.lenslet_planes = []
+            self.masks = []
+            for ax in range(2):
+                planes, masks = [], []
+                ac = self.array_planes[ax].centres()
+                for mu in range(nl[ax]):
+                    c_mu = (mu - (nl[ax] - 1) * 0.5) * self.pitch[ax]
+                    X0 = compose(translate(-cam["d_mu_m"]), compose(invert(lens(cam["f_mu"], c_mu)), translate(-b)))
+                    planes.append(Plane(det_n[ax], det_d[ax], X0))
+                    half = 0.5 * cam["fill"] * self.pitch[ax]
+                    masks.append(((ac >= c_mu - half) & (ac < c_mu + half)).astype(np.float64))
+                self.lenslet_planes.append(planes)
+                self.masks.append(masks)
+            dst = self.array_planes
+            va = basis_volume(dst[0], self.d0[0]) * basis_volume(dst[1], self.d0[1])
+            vmu = basis_volume(self.lenslet_planes[0][0], self.d0[0]) * \
+                basis_volume(self.lenslet_planes[1][0], self.d0[1])
+            self.scale_s1 = self.dz / va
+            self.scale_s3 = math.sqrt(vmu) / vmu
+        # S1: slice n -> array (plenoptic) or detector (single), per axis, per k_axis, per n
+        self.S1 = [[[build(self.slice_planes[ax][n], dst[ax], self.sk[ax][k], self.d0[ax], self.basis)
+                     for n in range(self.nz)] for k in range(len(self.sk[ax]))] for ax in range(2)]
+        # S3: array -> detector through every lenslet, masked: S_k = sum_mu B^{mu a}_k M_mu
+        if self.type == PLENOPTIC:
+            self.S3 = []
+            for ax in range(2):
+                per_k = []
+                for k in range(len(self.sk[ax])):
+                    acc = None
+                    for mu, pl in enumerate(self.lenslet_planes[ax]):
+                        B = build(self.array_planes[ax], pl, self.sk[ax][k], self.d0[ax], self.basis)
+                        term = B @ (np.diag(self.masks[ax][mu]) if dense else sp.diags(self.masks[ax][mu]))
+                        acc = term if acc is None else acc + term
+                    per_k.append(acc if dense else sp.csr_matrix(acc))
+                self.S3.append(per_k)
+
+    @property
+    def n_pix(self):
+        return self.cam["n_s"] * self.cam["n_t"]
+
+    # ---- matrix-free fp64 forward / adjoint (literal factored order, literal transposes) ----
+    def forward(self, xr):
+        xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)
+        y = np.zeros((self.cam["n_t"], self.cam["n_s"]))
+        for ks in range(self.ks):
+            for kt in range(self.kt):
+                acc = np.zeros((self.S1[1][kt][0].shape[0], self.S1[0][ks][0].shape[0]))
+                for n in range(self.nz):
+                    acc += self.S1[1][kt][n] @ (xr[n] @ self.S1[0][ks][n].T)
+                acc *= self.scale_s1
+                if self.type == PLENOPTIC:
+                    y += self.scale_s3 * (self.S3[1][kt] @ (acc @ self.S3[0][ks].T))
+                else:
+                    y += acc
+        return y
+
+    def adjoint(self, y):
+        y = np.asarray(y, np.float64).reshape(self.cam["n_t"], self.cam["n_s"])
+        g = np.zeros((self.nz, self.ny, self.nx))
+        for ks in range(self.ks):
+            for kt in range(self.kt):
+                if self.type == PLENOPTIC:
+                    a = self.scale_s3 * (self.S3[1][kt].T @ (y @ self.S3[0][ks]))
+                else:
+                    a = y
+                for n in range(self.nz):
+                    g[n] += self.scale_s1 * (self.S1[1][kt][n].T @ (a @ self.S1[0][ks][n]))
+        return g
+
+    def array_fields(self, xr):
+        """Plenoptic intermediate a_k (K, n_at, n_as) of the factored chain (for S1-stage parity)."""
+        xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)
+        out = []
+        for kt in range(self.kt):
+            for ks in range(self.ks):
+                acc = 0.0
+                for n in range(self.nz):
+                    acc = acc + self.S1[1][kt][n] @ (xr[n] @ self.S1[0][ks][n].T)
+                out.append(self.scale_s1 * acc)
+        return np.stack(out)
+
+    def dense(self):
+        """Explicit A (n_pix x n_vox) acting on x^r; tiny inputs only."""
+        def d(m):
+            return m if isinstance(m, np.ndarray) else m.toarray()
+        n_vox_slice = self.nx * self.ny
+        A = np.zeros((self.n_pix, self.nz * n_vox_slice))
+        for ks in range(self.ks):
+            for kt in range(self.kt):
+                S = self.scale_s3 * np.kron(d(self.S3[1][kt]), d(self.S3[0][ks])) \
+                    if self.type == PLENOPTIC else None
+                for n in range(self.nz):
+                    B = self.scale_s1 * np.kron(d(self.S1[1][kt][n]), d(self.S1[0][ks][n]))
+                    blk = B if S is None else S @ B
+                    A[:, n * n_vox_slice:(n + 1) * n_vox_slice] += blk
+        return A
