@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark: A+A^T pairs/s of the plenoptic light-transport system model (arXiv 1812.03358).
+
+One step = one pair: A_forward for every camera of the config, then A_adjoint for every camera
+accumulated into one gradient volume (rotation passes included, plan build excluded) --
+BASELINE.json's metric on its 128^3 two-camera config (configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--path collapsed|per_view]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: cameras x detector-row tiles)
+
+Timing: W untimed steps, then K steps; between steps L2 is flushed (a 256 MiB write); each step is
+bracketed by CUDA events on the launching stream (the flush is outside the events); the whole loop is
+bracketed by a barrier + synchronize; rank 0 prints ONE JSON line with the max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "128^3 two-camera"
+METRIC = "A+A^T pairs/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="collapsed", choices=["collapsed", "per_view"])
+    ap.add_argument("--config", default=WORKLOAD)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ helpers
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+    except Exception:
+        return {}
+
+
+def cpu_baseline(cfg, n_views_sample=None):
+    """Oracle (fp64, as it stands) timed on this host: camera 0 forward + adjoint on a view sample,
+    scaled linearly in K and by the number of cameras; rotation timed separately."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle.camera import CameraModel
+    from oracle.rotation import Rotation
+    from workloads import flame_volume, uniform_vector
+    vol = cfg["volume"]
+    dims = (vol["nx"], vol["ny"], vol["nz"])
+    vox = (vol["dx"], vol["dy"], vol["dz"])
+    with threadpool_limits(limits=1):
+        cam = CameraModel(cfg["cameras"][0], dims, vox)
+        K = cam.ks * cam.kt
+        views = [(ks, kt) for kt in range(cam.kt) for ks in range(cam.ks)]
+        if n_views_sample:
+            views = views[:n_views_sample]
+        x = flame_volume(vol).astype(np.float64)
+        r = uniform_vector(cam.n_pix, 1).astype(np.float64)
+        t0 = time.perf_counter()
+        cam.forward(x, views=views)
+        cam.adjoint(r, views=views)
+        t_cam = (time.perf_counter() - t0) * K / len(views)
+        t_rot = 0.0
+        for c in cfg["cameras"][1:]:
+            rot = Rotation(c["R"], dims, vox)
+            t0 = time.perf_counter()
+            rot.adjoint(rot.forward(x))
+            t_rot += time.perf_counter() - t0
+    t_pair = t_cam * len(cfg["cameras"]) + t_rot
+    return dict(value=1.0 / t_pair, unit="pairs/s", cores=1, kind="oracle",
+                sample="camera 0 fwd+adj over %d of %d views, scaled x%d views and x%d cameras, + measured "
+                       "rotation fwd+adj of the posed cameras; single thread (scipy.sparse fp64)"
+                       % (len(views), K, K // len(views), len(cfg["cameras"])),
+                seconds_measured=round(t_cam * len(views) / K + t_rot, 2))
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    """The oracle as the reference arm (tier rule): bounded samples of the same workload on host cores."""
+    if rank != 0:
+        return
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle.system import SystemOperator
+    from workloads import flame_volume, make_config, uniform_vector
+    cfg = make_config(args.config)
+    t_build = time.perf_counter()
+    ops = [SystemOperator(cfg["volume"], c) for c in cfg["cameras"]]
+    t_build = time.perf_counter() - t_build
+    x = flame_volume(cfg["volume"]).astype(np.float64)
+    rs = [uniform_vector(op.n_pix, 1).astype(np.float64) for op in ops]
+    K = ops[0].camera.ks * ops[0].camera.kt
+    per = []
+    with threadpool_limits(limits=1):
+        for it in range(args.warmup + args.steps):
+            k = it % K
+            view = [(k % ops[0].camera.ks, k // ops[0].camera.ks)]
+            t0 = time.perf_counter()
+            for op, r in zip(ops, rs):
+                xr = op.rot.forward(x)
+                op.camera.forward(xr, views=view)
+                op.rot.adjoint(op.camera.adjoint(r, views=view))
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                per.append(dt)
+    # one step = one view of the pair; a full pair is K views (cost linear in K)
+    t_pair = (sum(per) / len(per)) * K
+    value = 1.0 / t_pair
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_pair, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "step": "one view of an A+A^T pair per timed step, x%d views" % K},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "oracle",
+                             "sample": "per step: 1 of %d views of every camera's fwd+adj with rotation; "
+                                       "oracle build %.1fs excluded" % (K, t_build)},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ our arm
+def shard(cfg, rank, world):
+    """(camera, row0, row1) work items of this rank: cameras round-robin; with more ranks than cameras each
+    camera's detector rows are split into contiguous tiles."""
+    n_cam = len(cfg["cameras"])
+    if world <= n_cam:
+        return [(c, 0, cfg["cameras"][c]["n_t"]) for c in range(n_cam) if c % world == rank]
+    per = world // n_cam
+    c = rank % n_cam
+    tile = rank // n_cam
+    if tile >= per:
+        return []
+    nt = cfg["cameras"][c]["n_t"]
+    r0 = nt * tile // per
+    r1 = nt * (tile + 1) // per
+    return [(c, r0, r1)]
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_03358_b200 import lfm
+    from workloads import flame_volume, make_config, uniform_vector
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = make_config(args.config)
+    path = lfm.COLLAPSED if args.path == "collapsed" else lfm.PER_VIEW
+    plan = lfm.Plan(cfg, device=local_rank)
+    ws = plan.workspace()
+    items = shard(cfg, rank, world)
+    if world > 1 and any(r0 != 0 or r1 != cfg["cameras"][c]["n_t"] for c, r0, r1 in items):
+        # row tiles: each rank computes its full camera (row-restricted kernels are future work); the
+        # measured time is then an upper bound of the row-sharded step.
+        pass
+    n_vox = plan.infos[0]["n_vox"]
+    x = torch.as_tensor(flame_volume(cfg["volume"]), device=dev).reshape(-1)
+    ys = {c: torch.empty(plan.infos[c]["n_pix"], device=dev) for c, _, _ in items}
+    rs = {c: torch.as_tensor(uniform_vector(plan.infos[c]["n_pix"], 1 + c), device=dev) for c, _, _ in items}
+    g = torch.empty(n_vox, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(x_in, g_out):
+        n = 0
+        for c, _, _ in items:
+            lfm.A_forward(plan, c, x_in, ys[c], ws, path=path)
+            n += lfm.last_launch_count()
+        first = True
+        for c, _, _ in items:
+            lfm.A_adjoint(plan, c, rs[c], g_out, ws, accumulate=not first, path=path)
+            n += lfm.last_launch_count()
+            first = False
+        if not items:
+            g_out.zero_()
+        if world > 1:
+            dist.all_reduce(g_out)
+            n += 1
+        launches[0] = n
+
+    # dominant kernel: the separable transport of an unrotated camera (one sep_kernel launch per call)
+    dom_cam = next((c for c, _, _ in items if plan.infos[c]["rot_passes"] == 0), None)
+
+    for _ in range(args.warmup):
+        step(x, g)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step(x, g)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sorted(a.elapsed_time(b) for a, b in ev)
+    ms_mean = sum(ms) / len(ms)
+    # dominant-kernel timing on the same stream, inside timed steps of the same shape
+    dom = None
+    if dom_cam is not None:
+        fwd_ms, adj_ms = [], []
+        for i in range(max(3, args.steps // 2)):
+            flush.zero_()
+            a, b, c_, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            a.record(stream)
+            lfm.A_forward(plan, dom_cam, x, ys[dom_cam], ws, path=path)
+            b.record(stream)
+            flush.zero_()
+            c_.record(stream)
+            lfm.A_adjoint(plan, dom_cam, rs[dom_cam], g, ws, path=path)
+            d.record(stream)
+            torch.cuda.synchronize()
+            fwd_ms.append(a.elapsed_time(b))
+            adj_ms.append(c_.elapsed_time(d))
+        inf = plan.infos[dom_cam]
+        fma = inf["fma_alg"][1 if path == lfm.COLLAPSED else 0]
+        dom = dict(fwd_ms=sum(fwd_ms) / len(fwd_ms), adj_ms=sum(adj_ms) / len(adj_ms), fma=fma)
+    sm = clocks.stop()
+    # e2e: through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        gh = torch.empty(n_vox, dtype=torch.float32).pin_memory()
+        xd = torch.empty_like(x)
+        for _ in range(2):
+            xd.copy_(xh, non_blocking=True)
+            step(xd, g)
+            gh.copy_(g, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            xd.copy_(xh, non_blocking=True)
+            step(xd, g)
+            gh.copy_(g, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = dict(ms=e2e_ms, h2d=xh.numel() * 4, d2h=gh.numel() * 4)
+    # max over ranks
+    t = torch.tensor([ms_mean, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_mean, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12   # TFLOP/s, DESIGN.md §roofline
+    roof = None
+    if dom is not None:
+        achieved = 2.0 * dom["fma"] / (dom["fwd_ms"] * 1e-3) / 1e12
+        tr = ncu_traffic().get("dominant_kernel_dram_bytes_per_launch")
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": tr,
+                "kernel": "sep_kernel (%s forward, camera %d)" % (args.path, dom_cam),
+                "kernel_ms": dom["fwd_ms"], "adjoint_kernel_ms": dom["adj_ms"],
+                "adjoint_achieved": 2.0 * dom["fma"] / (dom["adj_ms"] * 1e-3) / 1e12,
+                "peak_note": "FP32 FMA: 148 SM x 128 lanes x 2 flop x %.0f MHz (sm_max_mhz, MEASURED_PEAKS.json)"
+                             % sm_max}
+    pair_bytes = sum(plan.infos[c]["bytes_alg"][1 if path == lfm.COLLAPSED else 0] * 2 for c in range(plan.n_cam))
+    value = 1e3 / ms_mean
+    line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_mean, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "volume": "%d^3 flame phantom" % cfg["volume"]["nx"],
+                       "cameras": len(cfg["cameras"]), "detector": "%dx%d" % (cfg["cameras"][0]["n_s"],
+                                                                                cfg["cameras"][0]["n_t"]),
+                       "views": "%dx%d pillbox" % (cfg["cameras"][0]["k_s"], cfg["cameras"][0]["k_t"]),
+                       "path": args.path, "parallelism": "cameras x detector-row tiles over %d rank(s)" % world,
+                       "l2": "256 MiB write between steps, outside the per-step CUDA events"},
+            "hbm_gbs_alg": pair_bytes / (ms_mean * 1e-3) / 1e9,
+            "hbm_frac_of_measured": pair_bytes / (ms_mean * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
+            "roofline": roof, "clocks": sm, "gpu_launches": launches[0] * args.steps}
+    if e2e:
+        line["e2e"] = {"value": 1e3 / e2e_ms, "unit": "pairs/s", "h2d_bytes_per_step": e2e["h2d"],
+                       "d2h_bytes_per_step": e2e["d2h"]}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as exc:  # the baseline is a report, never a reason to lose the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "pairs/s", "cores": 1, "kind": "oracle",
+                                    "sample": "failed: %s" % exc}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

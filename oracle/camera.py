@@ -113,32 +113,34 @@ class CameraModel:
         return self.cam["n_s"] * self.cam["n_t"]
 
     # ---- matrix-free fp64 forward / adjoint (literal factored order, literal transposes) ----
-    def forward(self, xr):
+    def _views(self, views):
+        return [(ks, kt) for kt in range(self.kt) for ks in range(self.ks)] if views is None else views
+
+    def forward(self, xr, views=None):
+        """y = A x^r; `views` (list of (k_s, k_t)) restricts the sum over k to a sample (bench timing)."""
         xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)
         y = np.zeros((self.cam["n_t"], self.cam["n_s"]))
-        for ks in range(self.ks):
-            for kt in range(self.kt):
-                acc = np.zeros((self.S1[1][kt][0].shape[0], self.S1[0][ks][0].shape[0]))
-                for n in range(self.nz):
-                    acc += self.S1[1][kt][n] @ (xr[n] @ self.S1[0][ks][n].T)
-                acc *= self.scale_s1
-                if self.type == PLENOPTIC:
-                    y += self.scale_s3 * (self.S3[1][kt] @ (acc @ self.S3[0][ks].T))
-                else:
-                    y += acc
+        for ks, kt in self._views(views):
+            acc = np.zeros((self.S1[1][kt][0].shape[0], self.S1[0][ks][0].shape[0]))
+            for n in range(self.nz):
+                acc += self.S1[1][kt][n] @ (xr[n] @ self.S1[0][ks][n].T)
+            acc *= self.scale_s1
+            if self.type == PLENOPTIC:
+                y += self.scale_s3 * (self.S3[1][kt] @ (acc @ self.S3[0][ks].T))
+            else:
+                y += acc
         return y
 
-    def adjoint(self, y):
+    def adjoint(self, y, views=None):
         y = np.asarray(y, np.float64).reshape(self.cam["n_t"], self.cam["n_s"])
         g = np.zeros((self.nz, self.ny, self.nx))
-        for ks in range(self.ks):
-            for kt in range(self.kt):
-                if self.type == PLENOPTIC:
-                    a = self.scale_s3 * (self.S3[1][kt].T @ (y @ self.S3[0][ks]))
-                else:
-                    a = y
-                for n in range(self.nz):
-                    g[n] += self.scale_s1 * (self.S1[1][kt][n].T @ (a @ self.S1[0][ks][n]))
+        for ks, kt in self._views(views):
+            if self.type == PLENOPTIC:
+                a = self.scale_s3 * (self.S3[1][kt].T @ (y @ self.S3[0][ks]))
+            else:
+                a = y
+            for n in range(self.nz):
+                g[n] += self.scale_s1 * (self.S1[1][kt][n].T @ (a @ self.S1[0][ks][n]))
         return g
 
     def array_fields(self, xr):

@@ -1,0 +1,487 @@
+// liblfm C ABI (include/lfm.h): argument validation, workspace layout, and the composition of
+// kernels into the paper's operators.  Every step of the hot path runs in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lfm_internal.h"
+#include "lfm_kernels.h"
+
+namespace lfm {
+lfm_status cuda_check(cudaError_t e, const char* what, std::string& err);
+}
+
+using namespace lfm;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_last_launches = 0;
+
+lfm_status fail(lfm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct WsLayout {
+  size_t r0, r1, f, s, s2, z, p, total;
+};
+
+WsLayout layout(const lfm_plan_s* p) {
+  size_t V = 0, F = 0, S = 0, Z = 0;
+  for (const CameraPlan& c : p->cams) {
+    V = std::max(V, (size_t)c.info.n_vox * 4);
+    F = std::max(F, c.ws_fields);
+    Z = std::max(Z, c.ws_z);
+    S = std::max(S, (size_t)std::max<long long>(c.info.n_pix, c.info.n_vox) * 4);
+  }
+  WsLayout L;
+  L.r0 = 0;
+  L.r1 = L.r0 + al256(V);
+  L.f = L.r1 + al256(V);
+  L.s = L.f + al256(F);
+  L.s2 = L.s + al256(S);
+  L.z = L.s2 + al256(S);
+  L.p = L.z + al256(Z);
+  L.total = L.p + al256(4096 * 8 * 4);
+  return L;
+}
+
+struct Ws {
+  float *r0, *r1, *f, *s, *s2, *z;
+  double* p;
+};
+
+lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
+  WsLayout L = layout(p);
+  if (!ws) return fail(LFM_E_INVALID, "workspace pointer is NULL");
+  if (ws_bytes < L.total) return fail(LFM_E_INVALID, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  if (((uintptr_t)ws & 255) != 0) return fail(LFM_E_INVALID, "workspace must be 256-byte aligned");
+  char* b = (char*)ws;
+  w.r0 = (float*)(b + L.r0);
+  w.r1 = (float*)(b + L.r1);
+  w.f = (float*)(b + L.f);
+  w.s = (float*)(b + L.s);
+  w.s2 = (float*)(b + L.s2);
+  w.z = (float*)(b + L.z);
+  w.p = (double*)(b + L.p);
+  return LFM_OK;
+}
+
+lfm_status check_cam(const lfm_plan_s* p, int cam, bool need_device = true) {
+  if (!p) return fail(LFM_E_INVALID, "plan is NULL");
+  if (cam < 0 || cam >= (int)p->cams.size()) return fail(LFM_E_INVALID, "camera index out of range");
+  if (need_device && p->device < 0) return fail(LFM_E_INVALID, "host-only plan (created with cuda_device = -1)");
+  return LFM_OK;
+}
+
+#define TRY(expr)                         \
+  do {                                    \
+    std::string _e;                       \
+    lfm_status _s = (expr);               \
+    (void)_e;                             \
+    if (_s != LFM_OK) return _s;          \
+  } while (0)
+
+// Rotation forward: returns the buffer holding x^r (x itself if the pose is the identity).
+lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, int accumulate, const Ws& w,
+                      void* stream, const float** xr) {
+  int act[3], na = 0;
+  for (int q = 0; q < 3; ++q)
+    if (cp.rot[q].active) act[na++] = q;
+  const float* cur = x;
+  std::string err;
+  for (int i = 0; i < na; ++i) {
+    bool last = i == na - 1;
+    float* dst = (last && final_out) ? final_out : ((cur == w.r0) ? w.r1 : w.r0);
+    lfm_status st = launch_shear(cp.rot[act[i]], 0, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
+                                 (last && final_out) ? accumulate : 0, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+    cur = dst;
+  }
+  if (na == 0 && final_out) {
+    lfm_status st = k_copy_scale(x, final_out, cp.info.n_vox, 1.f, accumulate, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+    cur = final_out;
+  }
+  *xr = cur;
+  return LFM_OK;
+}
+
+// Rotation adjoint E^zT E^xT E^yT applied to `in`, written (or accumulated) into `out`.
+lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int accumulate, const Ws& w, void* stream) {
+  int act[3], na = 0;
+  for (int q = 2; q >= 0; --q)
+    if (cp.rot[q].active) act[na++] = q;
+  std::string err;
+  if (na == 0) {
+    lfm_status st = k_copy_scale(in, out, cp.info.n_vox, 1.f, accumulate, stream, err);
+    return st == LFM_OK ? st : fail(st, err);
+  }
+  const float* cur = in;
+  for (int i = 0; i < na; ++i) {
+    bool last = i == na - 1;
+    float* dst = last ? out : ((cur == w.r0) ? w.r1 : w.r0);
+    lfm_status st = launch_shear(cp.rot[act[i]], 1, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
+                                 last ? accumulate : 0, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+    cur = dst;
+  }
+  return LFM_OK;
+}
+
+lfm_status sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int acc, void* stream) {
+  std::string err;
+  lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err);
+  return st == LFM_OK ? st : fail(st, err);
+}
+
+lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y, const Ws& w, void* stream) {
+  const float* xr;
+  TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
+  const bool plen = cp.info.type == LFM_PLENOPTIC;
+  if (path == LFM_PATH_COLLAPSED) return sep(cp.fwd_c, xr, y, 0, 1, 0, stream);
+  if (plen) {
+    TRY(sep(cp.fwd_s1, xr, w.f, 0, cp.info.n_views, 0, stream));
+    return sep(cp.fwd_s3, w.f, y, 0, 1, 0, stream);
+  }
+  return sep(cp.fwd_s1, xr, y, 0, 1, 0, stream);
+}
+
+lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x, int accumulate, const Ws& w,
+                        void* stream) {
+  const bool rot = cp.info.rot_passes != 0;
+  float* target = rot ? w.r0 : x;
+  int acc = rot ? 0 : accumulate;
+  const bool plen = cp.info.type == LFM_PLENOPTIC;
+  if (path == LFM_PATH_COLLAPSED) {
+    TRY(sep(cp.adj_c1, y, w.z, 0, cp.info.nz, 0, stream));
+    TRY(sep(cp.adj_c2, w.z, target, 0, cp.info.nz, acc, stream));
+  } else if (plen) {
+    TRY(sep(cp.adj_s3, y, w.f, 0, cp.info.n_views, 0, stream));
+    TRY(sep(cp.adj_s1, w.f, target, 0, cp.info.nz, acc, stream));
+  } else {
+    TRY(sep(cp.adj_s1, y, target, 0, cp.info.nz, acc, stream));
+  }
+  if (rot) {
+    // the adjoint passes ping-pong between r1 and r0; start from r0
+    int act[3], na = 0;
+    for (int q = 2; q >= 0; --q)
+      if (cp.rot[q].active) act[na++] = q;
+    const float* cur = w.r0;
+    std::string err;
+    for (int i = 0; i < na; ++i) {
+      bool last = i == na - 1;
+      float* dst = last ? x : ((cur == w.r0) ? w.r1 : w.r0);
+      lfm_status st = launch_shear(cp.rot[act[i]], 1, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
+                                   last ? accumulate : 0, stream, err);
+      if (st != LFM_OK) return fail(st, err);
+      cur = dst;
+    }
+  }
+  return LFM_OK;
+}
+
+lfm_status check_path(int path) {
+  if (path != LFM_PATH_PER_VIEW && path != LFM_PATH_COLLAPSED) return fail(LFM_E_INVALID, "unknown path");
+  return LFM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lfm_last_error(void) { return g_err.c_str(); }
+const char* lfm_version(void) { return "liblfm 0.1 (sm_100a)"; }
+int lfm_last_launch_count(void) { return g_last_launches; }
+
+lfm_status lfm_plan_create(const lfm_geometry* g, int cuda_device, lfm_plan* out) {
+  if (!out) return fail(LFM_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!g || g->n_cam <= 0 || !g->cam) return fail(LFM_E_INVALID, "geometry has no cameras");
+  lfm_plan_s* p = new lfm_plan_s;
+  p->device = cuda_device;
+  p->vol = g->vol;
+  p->cams.resize(g->n_cam);
+  for (int c = 0; c < g->n_cam; ++c) {
+    std::string err;
+    lfm_status st = build_camera(g->vol, g->cam[c], p->cams[c], err);
+    if (st != LFM_OK) {
+      delete p;
+      return fail(st, "camera " + std::to_string(c) + ": " + err);
+    }
+  }
+  WsLayout L = layout(p);
+  for (CameraPlan& c : p->cams) c.info.ws_bytes = L.total;
+  if (cuda_device >= 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    std::string err;
+    lfm_status st = cuda_check(cudaSetDevice(cuda_device), "cudaSetDevice", err);
+    for (int c = 0; st == LFM_OK && c < g->n_cam; ++c) {
+      st = upload_camera(p->cams[c], err);
+      if (st != LFM_OK) err = "camera " + std::to_string(c) + ": " + err;
+    }
+    cudaSetDevice(prev);
+    if (st != LFM_OK) {
+      for (CameraPlan& c : p->cams) free_camera(c);
+      delete p;
+      return fail(st, err);
+    }
+  }
+  *out = p;
+  return LFM_OK;
+}
+
+lfm_status lfm_plan_destroy(lfm_plan p) {
+  if (!p) return LFM_OK;
+  if (p->device >= 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    for (CameraPlan& c : p->cams) free_camera(c);
+    cudaSetDevice(prev);
+  }
+  delete p;
+  return LFM_OK;
+}
+
+lfm_status lfm_plan_info(lfm_plan p, int cam, lfm_info* out) {
+  lfm_status st = check_cam(p, cam, false);
+  if (st != LFM_OK) return st;
+  if (!out) return fail(LFM_E_INVALID, "out is NULL");
+  *out = p->cams[cam].info;
+  return LFM_OK;
+}
+
+lfm_status lfm_plan_export_table(lfm_plan p, int cam, int table_id, int axis, int index, void* host_dst,
+                                 size_t bytes, size_t* bytes_needed) {
+  lfm_status st = check_cam(p, cam, false);
+  if (st != LFM_OK) return st;
+  const CameraPlan& cp = p->cams[cam];
+  const void* srcp = nullptr;
+  size_t need = 0;
+  std::vector<char> tmp;
+  if (table_id == LFM_TAB_SCALARS) {
+    srcp = cp.scal;
+    need = sizeof(cp.scal);
+  } else if (table_id == LFM_TAB_ROT_MLO || table_id == LFM_TAB_ROT_W64) {
+    if (index < 0 || index > 2) return fail(LFM_E_INVALID, "shear pass index must be 0 (z), 1 (x), 2 (y)");
+    const ShearPass& sp = cp.rot[index];
+    if (!sp.active) {
+      need = 0;
+    } else if (table_id == LFM_TAB_ROT_MLO) {
+      srcp = sp.mlo[0].data();
+      need = sp.mlo[0].size() * 4;
+    } else {
+      srcp = sp.w64[0].data();
+      need = sp.w64[0].size() * 8;
+    }
+  } else {
+    if (axis < 0 || axis > 1) return fail(LFM_E_INVALID, "axis must be 0 (s) or 1 (t)");
+    const BandFamily* f = nullptr;
+    int group = table_id / 3, kind = table_id % 3;
+    switch (group) {
+      case 0: f = &cp.s1f[axis]; break;
+      case 1: f = &cp.s1a[axis]; break;
+      case 2: f = &cp.s3f[axis]; break;
+      case 3: f = &cp.s3a[axis]; break;
+      case 4: f = &cp.cf[axis]; break;
+      default: return fail(LFM_E_INVALID, "unknown table id");
+    }
+    if (index < 0 || index >= f->n_tables) return fail(LFM_E_INVALID, "table index out of range");
+    size_t r0 = (size_t)index * f->n_rows;
+    if (kind == 0) { srcp = f->start.data() + r0; need = (size_t)f->n_rows * 4; }
+    else if (kind == 1) { srcp = f->len.data() + r0; need = (size_t)f->n_rows * 4; }
+    else { srcp = f->w64.data() + r0 * f->taps; need = (size_t)f->n_rows * f->taps * 8; }
+  }
+  if (bytes_needed) *bytes_needed = need;
+  if (!host_dst) return LFM_OK;
+  if (bytes != need) return fail(LFM_E_INVALID, "export size mismatch: need " + std::to_string(need));
+  if (need) std::memcpy(host_dst, srcp, need);
+  return LFM_OK;
+}
+
+lfm_status lfm_lf_transport(lfm_plan p, int cam, int dst_plane, int src_plane, const float* src, float* dst,
+                            void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if (!src || !dst) return fail(LFM_E_INVALID, "src/dst is NULL");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  const CameraPlan& cp = p->cams[cam];
+  const int nz = cp.info.nz, K = cp.info.n_views;
+  const bool plen = cp.info.type == LFM_PLENOPTIC;
+  const int A = nz, D = nz + 1;
+  auto is_slice = [&](int q) { return q >= 0 && q < nz; };
+  if (plen) {
+    if (dst_plane == A && is_slice(src_plane)) st = sep(cp.xp_s1f, src, dst, src_plane * K, K, 0, stream);
+    else if (is_slice(dst_plane) && src_plane == A) st = sep(cp.xp_s1a, src, dst, dst_plane * K, K, 0, stream);
+    else if (dst_plane == D && src_plane == A) st = sep(cp.xp_s3f, src, dst, 0, K, 0, stream);
+    else if (dst_plane == A && src_plane == D) st = sep(cp.xp_s3a, src, dst, 0, K, 0, stream);
+    else return fail(LFM_E_MISMATCH, "unsupported plane pair for a plenoptic camera");
+  } else {
+    if (dst_plane == D && is_slice(src_plane)) st = sep(cp.xp_s1f, src, dst, src_plane * K, K, 0, stream);
+    else if (is_slice(dst_plane) && src_plane == D) st = sep(cp.xp_s1a, src, dst, dst_plane * K, K, 0, stream);
+    else return fail(LFM_E_MISMATCH, "unsupported plane pair for a single-lens camera");
+  }
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* out, int accumulate, void* ws,
+                          size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if (!in || !out || in == out) return fail(LFM_E_INVALID, "in/out NULL or aliased");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  const CameraPlan& cp = p->cams[cam];
+  if (dir == LFM_FWD) {
+    const float* xr;
+    st = rotate_fwd(cp, in, out, accumulate, w, stream, &xr);
+  } else if (dir == LFM_ADJ) {
+    st = rotate_adj(cp, in, out, accumulate, w, stream);
+  } else {
+    return fail(LFM_E_INVALID, "dir must be LFM_FWD or LFM_ADJ");
+  }
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y, void* ws, size_t ws_bytes,
+                         void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if ((st = check_path(path)) != LFM_OK) return st;
+  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  st = forward_impl(p->cams[cam], path, x, y, w, stream);
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_A_adjoint(lfm_plan p, int cam, int path, const float* y, float* x, int accumulate, void* ws,
+                         size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if ((st = check_path(path)) != LFM_OK) return st;
+  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  st = adjoint_impl(p->cams[cam], path, y, x, accumulate, w, stream);
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_pwls_stats(lfm_plan p, int cam, const float* Ax, const float* y, const float* w_, double* stats3,
+                          void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if (!Ax || !y || !w_ || !stats3) return fail(LFM_E_INVALID, "NULL argument");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  std::string err;
+  st = k_stats(Ax, y, w_, p->cams[cam].info.n_pix, w.p, stats3, stream, err);
+  g_last_launches = g_launches;
+  return st == LFM_OK ? st : fail(st, err);
+}
+
+lfm_status lfm_pwls_gains(lfm_plan p, const double* stats, double* gamma, int* flag, void* stream) {
+  g_launches = 0;
+  if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
+  if (!stats || !gamma) return fail(LFM_E_INVALID, "NULL argument");
+  std::string err;
+  lfm_status st = k_gains(stats, (int)p->cams.size(), gamma, flag, stream, err);
+  g_last_launches = g_launches;
+  return st == LFM_OK ? st : fail(st, err);
+}
+
+lfm_status lfm_pwls_grad(lfm_plan p, int path, int cam0, int cam1, const float* x, const float* const* y,
+                         const float* const* wts, const float* const* Ax, const double* gamma, float beta, float nu,
+                         int include_reg, float* grad, double* cost, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
+  if (cam0 < 0 || cam1 > (int)p->cams.size() || cam0 > cam1) return fail(LFM_E_INVALID, "bad camera range");
+  if (!x || !grad || (cam1 > cam0 && (!y || !wts || !Ax || !gamma))) return fail(LFM_E_INVALID, "NULL argument");
+  lfm_status st = check_path(path);
+  if (st != LFM_OK) return st;
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  std::string err;
+  const long long nvox = (long long)p->vol.nx * p->vol.ny * p->vol.nz;
+  if (cam1 == cam0) {
+    if ((st = k_fill(grad, nvox, 0.f, stream, err)) != LFM_OK) return fail(st, err);
+    if (cost) cudaMemsetAsync(cost, 0, sizeof(double), (cudaStream_t)stream);
+  }
+  for (int c = cam0; c < cam1; ++c) {
+    const CameraPlan& cp = p->cams[c];
+    if (!y[c] || !wts[c] || !Ax[c]) return fail(LFM_E_INVALID, "NULL per-camera pointer");
+    st = k_residual(Ax[c], y[c], wts[c], gamma, c, w.s, cp.info.n_pix, w.p, cost, c > cam0, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+    if ((st = adjoint_impl(cp, path, w.s, grad, c > cam0, w, stream)) != LFM_OK) return st;
+  }
+  if (include_reg) {
+    st = k_reg26(x, grad, p->vol.nx, p->vol.ny, p->vol.nz, beta, nu, w.p, cost ? cost + 1 : nullptr, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+  } else if (cost) {
+    cudaMemsetAsync(cost + 1, 0, sizeof(double), (cudaStream_t)stream);
+  }
+  g_last_launches = g_launches;
+  return cuda_check(cudaGetLastError(), "pwls_grad", err) == LFM_OK ? LFM_OK : fail(LFM_E_CUDA, err);
+}
+
+lfm_status lfm_majoriser(lfm_plan p, int path, int cam0, int cam1, const float* const* wts, float beta, int mode,
+                         float* d, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
+  if (cam0 < 0 || cam1 > (int)p->cams.size() || cam0 > cam1) return fail(LFM_E_INVALID, "bad camera range");
+  if (!d || ((mode & LFM_MAJ_SUM) && cam1 > cam0 && !wts)) return fail(LFM_E_INVALID, "NULL argument");
+  lfm_status st = check_path(path);
+  if (st != LFM_OK) return st;
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  std::string err;
+  const long long nvox = (long long)p->vol.nx * p->vol.ny * p->vol.nz;
+  if (mode & LFM_MAJ_SUM) {
+    if (cam1 == cam0 && (st = k_fill(d, nvox, 0.f, stream, err)) != LFM_OK) return fail(st, err);
+    for (int c = cam0; c < cam1; ++c) {
+      const CameraPlan& cp = p->cams[c];
+      if (!wts[c]) return fail(LFM_E_INVALID, "NULL weight pointer");
+      if ((st = k_fill(w.s, nvox, 1.f, stream, err)) != LFM_OK) return fail(st, err);
+      if ((st = forward_impl(cp, path, w.s, w.s2, w, stream)) != LFM_OK) return st;
+      if ((st = k_mul(w.s2, wts[c], w.s2, cp.info.n_pix, stream, err)) != LFM_OK) return fail(st, err);
+      if ((st = adjoint_impl(cp, path, w.s2, d, c > cam0, w, stream)) != LFM_OK) return st;
+    }
+  }
+  if (mode & LFM_MAJ_FINISH) {
+    if ((st = k_majoriser_finish(d, nvox, 36.f * beta, stream, err)) != LFM_OK) return fail(st, err);
+  }
+  g_last_launches = g_launches;
+  return LFM_OK;
+}
+
+lfm_status lfm_fista_update(lfm_plan p, float* x, float* z, const float* grad, const float* d, double t_old,
+                            double t_new, void* stream) {
+  g_launches = 0;
+  if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
+  if (!x || !z || !grad || !d) return fail(LFM_E_INVALID, "NULL argument");
+  if (!(t_new > 0)) return fail(LFM_E_INVALID, "t_new must be > 0");
+  std::string err;
+  const long long nvox = (long long)p->vol.nx * p->vol.ny * p->vol.nz;
+  lfm_status st = k_fista(x, z, grad, d, nvox, (float)((t_old - 1.0) / t_new), stream, err);
+  g_last_launches = g_launches;
+  return st == LFM_OK ? st : fail(st, err);
+}
+
+}  // extern "C"

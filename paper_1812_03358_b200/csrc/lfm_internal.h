@@ -1,0 +1,119 @@
+// Internal structures of liblfm: host plan (fp64 build, fp32 device tables) and kernel launch
+// descriptors.  Not part of the public ABI (include/lfm.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/lfm.h"
+
+namespace lfm {
+
+// One separable axis of an affine ray map (s,u) -> (m00 s + m01 u + o0, m10 s + m11 u + o1), §2.1.
+struct Affine {
+  double m00, m01, m10, m11, o0, o1;
+};
+
+// One axis of an optical plane: n cells of width delta centred on c0, and X^{0p}.
+struct Plane {
+  int n;
+  double delta;
+  Affine X0;
+  double c0;
+};
+
+// A family of banded 1D operator tables sharing the row count and padded tap count.
+// Table m, row r: band start (first source cell), band length, taps weights (fp64 on the host,
+// fp32 on the device; entries beyond `len` are zero).
+// The device uses the ELL form: per row the exact non-zero list (count, source index, weight), padded
+// to `ell` entries, stored [table][entry][row] so that lanes on consecutive rows coalesce.
+struct BandFamily {
+  int n_tables = 0, n_rows = 0, n_src = 0, taps = 0;
+  std::vector<int32_t> start, len;
+  std::vector<double> w64;
+  int ell = 0;                       // padded entries per row (multiple of 4)
+  std::vector<int32_t> cnt, eidx;    // [table][row], [table][entry][row]
+  std::vector<double> ew64;          // [table][entry][row]
+  int32_t* d_cnt = nullptr;
+  int32_t* d_idx = nullptr;
+  float* d_w = nullptr;
+};
+
+// One summand of a separable banded sum: source plane at src_base + src_off, s/t table indices.
+struct Term {
+  long long src_off;
+  int s_tab;
+  int t_tab;
+  float scale;
+  int pad;
+};
+
+// Per (table, output tile): first source cell and width of the staged footprint (width 0 = empty).
+struct Footprint {
+  int32_t lo, width;
+};
+
+// out[b] = out_scale * sum_{terms of b} scale * (B_s[s_tab] (x) B_t[t_tab]) src   (t-pass, s-pass)
+struct SepOp {
+  const BandFamily* fs = nullptr;  // rows = output s cells
+  const BandFamily* ft = nullptr;  // rows = output t cells
+  int n_os = 0, n_ot = 0, n_is = 0, n_it = 0, n_out = 0;
+  float out_scale = 1.f;
+  int ts = 64, tt = 32;            // output tile
+  int fs_max = 0, ft_max = 0;      // max source footprint per tile (s, t)
+  std::vector<Term> terms;
+  std::vector<int32_t> offs;       // n_out + 1
+  Term* d_terms = nullptr;
+  int32_t* d_offs = nullptr;
+  int ntx = 0, nty = 0;            // output tiles along s, t
+  Footprint* d_fp_s = nullptr;     // [s-table][tile_x]
+  Footprint* d_fp_t = nullptr;     // [t-table][tile_y]
+  double fma_alg = 0;              // sum over terms of nnz work (algorithmic)
+};
+
+// One shear pass of the rotation (eqn,rot,toeplitz): per line, first offset m_lo and taps weights.
+struct ShearPass {
+  int active = 0;
+  int axis = 0;  // 0 = z-pass, 1 = x-pass, 2 = y-pass
+  double c1 = 0, c2 = 0;
+  int taps = 0, n_lines = 0;
+  std::vector<int32_t> mlo[2];     // [fwd, adj]
+  std::vector<double> w64[2];
+  int32_t* d_mlo[2] = {nullptr, nullptr};
+  float* d_w[2] = {nullptr, nullptr};
+};
+
+struct CameraPlan {
+  lfm_camera cam;
+  lfm_info info;
+  BandFamily s1f[2], s1a[2], s3f[2], s3a[2], cf[2], ca[2];
+  // A_forward / A_adjoint ops, per path
+  SepOp fwd_s1, fwd_s3, adj_s3, adj_s1;   // per-view path
+  SepOp fwd_c, adj_c1, adj_c2;            // collapsed path (adjoint in two passes: t then s)
+  BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint
+  // lf_transport ops (output b = n*K + k for slice-indexed families)
+  SepOp xp_s1f, xp_s1a, xp_s3f, xp_s3a;
+  ShearPass rot[3];                       // application order z, x, y (x^r = E^y E^x E^z x)
+  double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
+  size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
+};
+
+}  // namespace lfm
+
+struct lfm_plan_s {
+  int device = 0;
+  lfm_volume vol;
+  std::vector<lfm::CameraPlan> cams;
+};
+
+namespace lfm {
+// plan.cpp (host fp64)
+void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width);
+lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& out, std::string& err);
+// kernels.cu
+lfm_status upload_camera(CameraPlan& cp, std::string& err);
+void free_camera(CameraPlan& cp);
+lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
+                      void* stream, std::string& err);
+}  // namespace lfm

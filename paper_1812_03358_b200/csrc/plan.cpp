@@ -1,0 +1,831 @@
+// liblfm plan builder: host fp64, compiled with -ffp-contract=off (no FMA contraction) so the
+// integer band tables follow a documented expression order (reading Z21).
+//
+// What it computes, per camera (P = PAPER.md line):
+//  * optics chain per axis (§2.1): T_d, R_f(c), composition, inverse;
+//  * rotation Theta = D S_z S_x S_y (eqn,rot,decomp P:1127-1135) in closed form, relabelled
+//    voxel sizes Delta/D, and per-line shear tables (eqn,rot,toeplitz P:1186-1198);
+//  * per (axis, angular index, slice) the 1D transport factors of eqn,xport,int
+//    as banded tables: weights = (1/|b_q|) int_{cell j} Trap(s - c_i) ds, the closed form of the
+//    missing tab,pillbox / tab,dirac, evaluated in fp64, rounded once to fp32;
+//  * adjoint tables from the opposite transport B^{qp} (closed form from the other side), used as
+//    the scaled forward operation;
+//  * the lenslet stage S_k = sum_mu B^{mu a}_k M_mu with rasterised square apertures (P:915-927,
+//    P:1011-1024), and the K-collapsed composite C_n = sum_k S_k B^{a q_n}_k (exact re-association).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lfm_internal.h"
+
+namespace lfm {
+
+static Affine translate(double d) { return {1.0, d, 0.0, 1.0, 0.0, 0.0}; }
+static Affine lens(double f, double c) { return {1.0, 0.0, -1.0 / f, 1.0, 0.0, c / f}; }
+
+static Affine compose(const Affine& a, const Affine& b) {  // a o b
+  Affine r;
+  r.m00 = a.m00 * b.m00 + a.m01 * b.m10;
+  r.m01 = a.m00 * b.m01 + a.m01 * b.m11;
+  r.m10 = a.m10 * b.m00 + a.m11 * b.m10;
+  r.m11 = a.m10 * b.m01 + a.m11 * b.m11;
+  r.o0 = a.m00 * b.o0 + a.m01 * b.o1 + a.o0;
+  r.o1 = a.m10 * b.o0 + a.m11 * b.o1 + a.o1;
+  return r;
+}
+
+static bool invert(const Affine& a, Affine& out) {
+  double det = a.m00 * a.m11 - a.m01 * a.m10;
+  if (std::fabs(det) <= 1e-12) return false;
+  double i00 = a.m11 / det;
+  double i01 = -a.m01 / det;
+  double i10 = -a.m10 / det;
+  double i11 = a.m00 / det;
+  out.m00 = i00; out.m01 = i01; out.m10 = i10; out.m11 = i11;
+  out.o0 = -(i00 * a.o0 + i01 * a.o1);
+  out.o1 = -(i10 * a.o0 + i11 * a.o1);
+  return true;
+}
+
+static double centre(const Plane& p, int i) { return p.c0 + ((double)i - (p.n - 1) * 0.5) * p.delta; }
+
+struct Kernel1D {  // one row family of a transport q -> p at angular centre s_k
+  double lam, mu, nu, W, w, H, bq_abs;
+  double sk;
+};
+
+// s_p = lam*s_q + mu*s_0 + nu (substituting u -> s_0 in eqn,xport,ip); trapezoid (W, w, H).
+static lfm_status make_kernel(const Plane& src, const Plane& dst, double s_k, double d0, int basis,
+                              Kernel1D& k, std::string& err) {
+  Affine inv;
+  if (!invert(dst.X0, inv)) { err = "singular X^{0p} block"; return LFM_E_SINGULAR; }
+  Affine Xpq = compose(inv, src.X0);  // X^{pq} = (X^{0p})^{-1} o X^{0q}
+  double P = Xpq.m00, Q = Xpq.m01, o_pq = Xpq.o0;
+  double a_q = src.X0.m00, b_q = src.X0.m01, o_q = src.X0.o0;
+  if (b_q == 0.0) { err = "source plane on the angular plane (b_q = 0)"; return LFM_E_DEGENERATE; }
+  k.lam = P - Q * a_q / b_q;
+  k.mu = Q / b_q;
+  k.nu = o_pq - Q * o_q / b_q;
+  if (k.lam == 0.0) { err = "destination conjugate to the angular plane (lambda = 0)"; return LFM_E_DEGENERATE; }
+  double al = std::fabs(k.lam);
+  double dp = dst.delta;
+  if (basis == LFM_DIRAC) {
+    k.W = dp / (2.0 * al);
+    k.w = dp / (2.0 * al);
+    k.H = d0;
+  } else {
+    double am = std::fabs(k.mu);
+    k.W = (d0 * am + dp) / (2.0 * al);
+    k.w = std::fabs(d0 * am - dp) / (2.0 * al);
+    k.H = (am == 0.0) ? d0 : std::min(d0, dp / am);
+  }
+  k.bq_abs = std::fabs(b_q);
+  k.sk = s_k;
+  return LFM_OK;
+}
+
+static double trap_value(double x, double W, double w, double H) {
+  double ax = std::fabs(x);
+  if (ax <= w) return H;
+  if (ax < W) return H * (W - ax) / (W - w);
+  return 0.0;
+}
+
+// Exact integral of the trapezoid over [lo, hi]: midpoint rule on each linear piece.
+static double trap_integral(double lo, double hi, double W, double w, double H) {
+  const double p0s[3] = {-W, -w, w};
+  const double p1s[3] = {-w, w, W};
+  double total = 0.0;
+  for (int q = 0; q < 3; ++q) {
+    double p0 = p0s[q], p1 = p1s[q];
+    if (p1 <= p0) continue;
+    double l = std::max(lo, p0);
+    double h = std::min(hi, p1);
+    if (h > l) total += (h - l) * trap_value(0.5 * (l + h), W, w, H);
+  }
+  return total;
+}
+
+// Row i of the transport: centre c_i on the source plane and the analytic band (reading Z21).
+static void row_band(const Plane& src, const Plane& dst, const Kernel1D& k, int i, double& c, int& lo, int& hi) {
+  c = (centre(dst, i) - k.nu - k.mu * k.sk) / k.lam;
+  double dq = src.delta;
+  double s0 = src.c0 + (0.0 - (src.n - 1) * 0.5) * dq;
+  double flo = std::floor((c - k.W - s0 - 0.5 * dq) / dq) + 1.0;
+  double fhi = std::ceil((c + k.W - s0 + 0.5 * dq) / dq) - 1.0;
+  flo = std::max(flo, 0.0);
+  fhi = std::min(fhi, (double)(src.n - 1));
+  if (fhi < flo) { lo = 0; hi = -1; return; }
+  lo = (int)flo;
+  hi = (int)fhi;
+}
+
+static double entry(const Plane& src, const Kernel1D& k, double c, int j) {
+  double sj = centre(src, j);
+  return trap_integral(sj - 0.5 * src.delta - c, sj + 0.5 * src.delta - c, k.W, k.w, k.H) / k.bq_abs;
+}
+
+// A sparse row: band [lo, lo+len) with weights (zeros allowed inside).
+struct Row {
+  int lo = 0, len = 0;
+  std::vector<double> w;
+};
+
+static lfm_status transport_rows(const Plane& src, const Plane& dst, double s_k, double d0, int basis,
+                                 std::vector<Row>& rows, std::string& err) {
+  Kernel1D k;
+  lfm_status st = make_kernel(src, dst, s_k, d0, basis, k, err);
+  if (st != LFM_OK) return st;
+  rows.assign(dst.n, Row());
+  for (int i = 0; i < dst.n; ++i) {
+    double c;
+    int lo, hi;
+    row_band(src, dst, k, i, c, lo, hi);
+    Row& r = rows[i];
+    if (hi < lo) continue;
+    r.lo = lo;
+    r.len = hi - lo + 1;
+    r.w.resize(r.len);
+    for (int j = lo; j <= hi; ++j) r.w[j - lo] = entry(src, k, c, j);
+  }
+  return LFM_OK;
+}
+
+static double basis_volume(const Plane& p, double d0) { return p.delta * d0 / std::fabs(p.X0.m01); }
+
+// Append a table (n_rows rows) to a family; taps is fixed later (max len).
+static void family_init(BandFamily& f, int n_tables, int n_rows, int n_src) {
+  f.n_tables = n_tables;
+  f.n_rows = n_rows;
+  f.n_src = n_src;
+  f.taps = 0;
+  f.start.assign((size_t)n_tables * n_rows, 0);
+  f.len.assign((size_t)n_tables * n_rows, 0);
+}
+
+// Build the ELL form (exact non-zero list per row) from the band rows.
+static void build_ell(BandFamily& f) {
+  int mx = 1;
+  f.cnt.assign((size_t)f.n_tables * f.n_rows, 0);
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int r = 0; r < f.n_rows; ++r) {
+      size_t idx = (size_t)m * f.n_rows + r;
+      int c = 0;
+      for (int q = 0; q < f.len[idx]; ++q) c += f.w64[idx * f.taps + q] != 0.0;
+      f.cnt[idx] = c;
+      mx = std::max(mx, c);
+    }
+  f.ell = (mx + 3) / 4 * 4;
+  size_t per = (size_t)f.ell * f.n_rows;
+  f.eidx.assign((size_t)f.n_tables * per, 0);
+  f.ew64.assign((size_t)f.n_tables * per, 0.0);
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int r = 0; r < f.n_rows; ++r) {
+      size_t idx = (size_t)m * f.n_rows + r;
+      int e = 0;
+      int first = f.len[idx] ? f.start[idx] : 0;
+      for (int q = 0; q < f.len[idx]; ++q) {
+        double w = f.w64[idx * f.taps + q];
+        if (w == 0.0) continue;
+        f.eidx[m * per + (size_t)e * f.n_rows + r] = f.start[idx] + q;
+        f.ew64[m * per + (size_t)e * f.n_rows + r] = w;
+        ++e;
+      }
+      for (; e < f.ell; ++e) f.eidx[m * per + (size_t)e * f.n_rows + r] = first;  // zero-weight padding
+    }
+}
+
+struct FamilyBuilder {
+  BandFamily& f;
+  std::vector<std::vector<Row>> tabs;
+  explicit FamilyBuilder(BandFamily& fam) : f(fam) {}
+  void finish() {
+    int taps = 1;
+    for (auto& t : tabs)
+      for (auto& r : t) taps = std::max(taps, r.len);
+    f.taps = taps;
+    f.w64.assign((size_t)f.n_tables * f.n_rows * taps, 0.0);
+    for (int m = 0; m < f.n_tables; ++m)
+      for (int r = 0; r < f.n_rows; ++r) {
+        const Row& row = tabs[m][r];
+        size_t idx = (size_t)m * f.n_rows + r;
+        f.start[idx] = row.len ? row.lo : 0;
+        f.len[idx] = row.len;
+        for (int q = 0; q < row.len; ++q) f.w64[idx * taps + q] = row.w[q];
+      }
+    tabs.clear();
+    build_ell(f);
+  }
+};
+
+static void make_identity(BandFamily& f, int n) {
+  family_init(f, 1, n, n);
+  FamilyBuilder b(f);
+  b.tabs.resize(1);
+  b.tabs[0].assign(n, Row());
+  for (int r = 0; r < n; ++r) {
+    b.tabs[0][r].lo = r;
+    b.tabs[0][r].len = 1;
+    b.tabs[0][r].w.assign(1, 1.0);
+  }
+  b.finish();
+}
+
+// ------------------------------------------------------------------------------------------
+// Rotation (eqn,rot,decomp): closed form, same expression order as DESIGN.md.
+struct Decomp {
+  double D[3];
+  double a_yx, a_yz, a_xy, a_xz, a_zx, a_zy;
+};
+
+static lfm_status decompose(const double* T, Decomp& d, std::string& err) {
+  double Txx = T[0], Txy = T[1], Txz = T[2], Tyx = T[3], Tyy = T[4], Tyz = T[5], Tzx = T[6], Tzy = T[7], Tzz = T[8];
+  double Dy = Tyy;
+  if (std::fabs(Dy) < 1e-6) { err = "rotation: D_y ~ 0 (>= 45 deg needs a quarter-turn permutation)"; return LFM_E_DEGENERATE; }
+  d.a_yx = Tyx / Dy;
+  d.a_yz = Tyz / Dy;
+  double Dx = Txx - Txy * d.a_yx;
+  if (std::fabs(Dx) < 1e-6) { err = "rotation: D_x ~ 0"; return LFM_E_DEGENERATE; }
+  d.a_xy = Txy / Dx;
+  d.a_xz = Txz / Dx - d.a_xy * d.a_yz;
+  double m_xx = 1.0 + d.a_xy * d.a_yx;
+  double m_xz = d.a_xz + d.a_xy * d.a_yz;
+  double alpha = Tzx - d.a_yx * Tzy;
+  double beta = m_xx * Tzy - d.a_xy * Tzx;
+  double Dz = Tzz - alpha * m_xz - beta * d.a_yz;
+  if (std::fabs(Dz) < 1e-6) { err = "rotation: D_z ~ 0"; return LFM_E_DEGENERATE; }
+  d.a_zx = alpha / Dz;
+  d.a_zy = beta / Dz;
+  d.D[0] = Dx;
+  d.D[1] = Dy;
+  d.D[2] = Dz;
+  return LFM_OK;
+}
+
+// (1/D)(Lambda_D * U_wa * U_wb)(d): exact piecewise polynomial via antiderivatives of Lambda.
+static double lam1(double t, double D) {
+  if (t <= -D) return 0.0;
+  if (t <= 0.0) return 0.5 * (t + D) * (t + D);
+  if (t < D) return D * D - 0.5 * (D - t) * (D - t);
+  return D * D;
+}
+static double lam2(double t, double D) {
+  if (t <= -D) return 0.0;
+  if (t <= 0.0) return (t + D) * (t + D) * (t + D) / 6.0;
+  if (t < D) return D * D * t + (D - t) * (D - t) * (D - t) / 6.0;
+  return D * D * t;
+}
+static double shear_weight(double d, double D, double wa, double wb) {
+  double tiny = 1e-9 * D;
+  double a = std::fabs(wa), b = std::fabs(wb);
+  bool ha = a > tiny, hb = b > tiny;
+  if (!ha && !hb) return std::max(0.0, D - std::fabs(d)) / D;
+  if (ha != hb) {
+    double w = ha ? a : b;
+    return (lam1(d + 0.5 * w, D) - lam1(d - 0.5 * w, D)) / (w * D);
+  }
+  double lo = std::min(a, b), hi = std::max(a, b);
+  double v = (lam2(d + 0.5 * (lo + hi), D) - lam2(d + 0.5 * (hi - lo), D) - lam2(d - 0.5 * (hi - lo), D) +
+              lam2(d - 0.5 * (lo + hi), D)) / (lo * hi * D);
+  return std::max(v, 0.0);
+}
+
+static void build_shear(ShearPass& sp, int axis, double c1, double c2, const int dims[3], const double vox[3]) {
+  sp.axis = axis;
+  sp.c1 = c1;
+  sp.c2 = c2;
+  sp.active = (c1 != 0.0 || c2 != 0.0);
+  if (!sp.active) return;
+  // axis 0: z-pass, lines (x,y), sigma = c1 x + c2 y, widths c1 dx, c2 dy, D = dz
+  // axis 1: x-pass, lines (y,z), sigma = c1 y + c2 z, widths c1 dy, c2 dz, D = dx
+  // axis 2: y-pass, lines (x,z), sigma = c1 x + c2 z, widths c1 dx, c2 dz, D = dy
+  int a1, a2, al;
+  if (axis == 0) { a1 = 0; a2 = 1; al = 2; }
+  else if (axis == 1) { a1 = 1; a2 = 2; al = 0; }
+  else { a1 = 0; a2 = 2; al = 1; }
+  int n1 = dims[a1], n2 = dims[a2];
+  double D = vox[al];
+  double wa = c1 * vox[a1], wb = c2 * vox[a2];
+  double reach = D + 0.5 * (std::fabs(wa) + std::fabs(wb));
+  sp.n_lines = n1 * n2;
+  int taps = 1;
+  std::vector<int> lo_f(sp.n_lines), lo_a(sp.n_lines), hi_f(sp.n_lines), hi_a(sp.n_lines);
+  for (int i2 = 0; i2 < n2; ++i2)
+    for (int i1 = 0; i1 < n1; ++i1) {
+      int line = i1 + n1 * i2;
+      double p1 = ((double)i1 - (n1 - 1) * 0.5) * vox[a1];
+      double p2 = ((double)i2 - (n2 - 1) * 0.5) * vox[a2];
+      double sig = c1 * p1 + c2 * p2;
+      for (int dir = 0; dir < 2; ++dir) {
+        double s = dir == 0 ? sig : -sig;  // E(a,b)^T = E(-a,-b)
+        int lo = (int)std::floor((s - reach) / D) + 1;
+        int hi = (int)std::ceil((s + reach) / D) - 1;
+        (dir == 0 ? lo_f : lo_a)[line] = lo;
+        (dir == 0 ? hi_f : hi_a)[line] = hi;
+        taps = std::max(taps, hi - lo + 1);
+      }
+    }
+  int pad = taps <= 4 ? 4 : (taps <= 8 ? 8 : 16);
+  sp.taps = pad;
+  for (int dir = 0; dir < 2; ++dir) {
+    sp.mlo[dir].assign(sp.n_lines, 0);
+    sp.w64[dir].assign((size_t)sp.n_lines * pad, 0.0);
+    for (int i2 = 0; i2 < n2; ++i2)
+      for (int i1 = 0; i1 < n1; ++i1) {
+        int line = i1 + n1 * i2;
+        double p1 = ((double)i1 - (n1 - 1) * 0.5) * vox[a1];
+        double p2 = ((double)i2 - (n2 - 1) * 0.5) * vox[a2];
+        double s = c1 * p1 + c2 * p2;
+        if (dir) s = -s;
+        int lo = (dir == 0 ? lo_f : lo_a)[line];
+        int hi = (dir == 0 ? hi_f : hi_a)[line];
+        sp.mlo[dir][line] = lo;
+        for (int m = lo; m <= hi; ++m) sp.w64[dir][(size_t)line * pad + (m - lo)] = shear_weight(m * D - s, D, wa, wb);
+      }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Footprint of table `tab` over output tile t: [lo, lo+width) of source cells (ELL entries).
+void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width) {
+  size_t per = (size_t)f.ell * f.n_rows;
+  int mn = 1 << 30, mxv = -1;
+  for (int r = t * tile; r < std::min(f.n_rows, (t + 1) * tile); ++r) {
+    int c = f.cnt[(size_t)tab * f.n_rows + r];
+    for (int e = 0; e < c; ++e) {
+      int j = f.eidx[tab * per + (size_t)e * f.n_rows + r];
+      mn = std::min(mn, j);
+      mxv = std::max(mxv, j);
+    }
+  }
+  if (mxv < 0) { lo = 0; width = 0; return; }
+  lo = mn;
+  width = mxv - mn + 1;
+}
+
+static void fill_sep_geometry(SepOp& op) {
+  const BandFamily& fs = *op.fs;
+  const BandFamily& ft = *op.ft;
+  op.fs_max = 1;
+  op.ft_max = 1;
+  std::vector<char> seen_s(fs.n_tables, 0), seen_t(ft.n_tables, 0);
+  double fma = 0;
+  int ntx = (fs.n_rows + op.ts - 1) / op.ts, nty = (ft.n_rows + op.tt - 1) / op.tt;
+  std::vector<double> used_s(fs.n_tables, 0), sum_s(fs.n_tables, 0), sum_t(ft.n_tables, 0);
+  for (const Term& t : op.terms) {
+    if (!seen_s[t.s_tab]) {
+      seen_s[t.s_tab] = 1;
+      int glo = 1 << 30, ghi = -1;
+      for (int x = 0; x < ntx; ++x) {
+        int lo, w;
+        ell_footprint(fs, t.s_tab, op.ts, x, lo, w);
+        op.fs_max = std::max(op.fs_max, w);
+        if (w) { glo = std::min(glo, lo); ghi = std::max(ghi, lo + w); }
+      }
+      used_s[t.s_tab] = ghi > glo ? ghi - glo : 0;
+      for (int r = 0; r < fs.n_rows; ++r) sum_s[t.s_tab] += fs.cnt[(size_t)t.s_tab * fs.n_rows + r];
+    }
+    if (!seen_t[t.t_tab]) {
+      seen_t[t.t_tab] = 1;
+      for (int y = 0; y < nty; ++y) {
+        int lo, w;
+        ell_footprint(ft, t.t_tab, op.tt, y, lo, w);
+        op.ft_max = std::max(op.ft_max, w);
+      }
+      for (int r = 0; r < ft.n_rows; ++r) sum_t[t.t_tab] += ft.cnt[(size_t)t.t_tab * ft.n_rows + r];
+    }
+    // algorithmic FMAs (non-zeros only): t-pass over the used source s range, then the s-pass
+    fma += sum_t[t.t_tab] * used_s[t.s_tab] + sum_s[t.s_tab] * ft.n_rows;
+  }
+  op.fma_alg = fma;
+}
+
+static void sep_init(SepOp& op, const BandFamily* fs, const BandFamily* ft, int n_is, int n_it, int n_out,
+                     float out_scale) {
+  op.fs = fs;
+  op.ft = ft;
+  op.n_os = fs->n_rows;
+  op.n_ot = ft->n_rows;
+  op.n_is = n_is;
+  op.n_it = n_it;
+  op.n_out = n_out;
+  op.out_scale = out_scale;
+  op.terms.clear();
+  op.offs.assign(1, 0);
+}
+static void sep_add(SepOp& op, long long off, int s_tab, int t_tab, float scale) {
+  op.terms.push_back(Term{off, s_tab, t_tab, scale, 0});
+}
+static void sep_close_output(SepOp& op) { op.offs.push_back((int32_t)op.terms.size()); }
+
+// Choose the largest output tile whose staged source footprint fits the shared-memory budget.
+static size_t sep_smem(const SepOp& op) {
+  size_t fsp = (size_t)op.fs_max + 1;
+  return ((size_t)op.ft_max * fsp + (size_t)op.tt * fsp) * 4 + (size_t)op.tt * op.ft->ell * 8 + (size_t)op.tt * 4;
+}
+static bool sep_choose_tile(SepOp& op) {
+  const int cand[][2] = {{64, 32}, {64, 16}, {32, 32}, {32, 16}, {16, 16}};
+  const size_t budget = 200 * 1024;
+  for (auto& c : cand) {
+    op.ts = c[0];
+    op.tt = c[1];
+    fill_sep_geometry(op);
+    if (sep_smem(op) <= budget) return true;
+  }
+  return false;
+}
+
+// ------------------------------------------------------------------------------------------
+lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& cp, std::string& err) {
+  cp.cam = cam;
+  lfm_info& info = cp.info;
+  std::memset(&info, 0, sizeof(info));
+  if (vol.nx <= 0 || vol.ny <= 0 || vol.nz <= 0 || !(vol.dx > 0) || !(vol.dy > 0) || !(vol.dz > 0)) {
+    err = "invalid volume";
+    return LFM_E_INVALID;
+  }
+  if (cam.k_s <= 0 || cam.k_t <= 0 || cam.n_s <= 0 || cam.n_t <= 0 || !(cam.px_s > 0) || !(cam.px_t > 0) ||
+      !(cam.ap_s > 0) || !(cam.ap_t > 0) || (cam.basis != LFM_PILLBOX && cam.basis != LFM_DIRAC)) {
+    err = "invalid camera parameters";
+    return LFM_E_INVALID;
+  }
+  if (cam.f_main == 0.0) { err = "zero main-lens focal length"; return LFM_E_SINGULAR; }
+  const bool plen = cam.type == LFM_PLENOPTIC;
+  if (plen) {
+    if (cam.nl_s <= 0 || cam.nl_t <= 0 || cam.n_a <= 0 || !(cam.fill > 0) || cam.fill > 1.0) {
+      err = "invalid plenoptic parameters (nl, n_a > 0, 0 < fill <= 1)";
+      return LFM_E_INVALID;
+    }
+    if (cam.f_mu == 0.0) { err = "zero lenslet focal length"; return LFM_E_SINGULAR; }
+  } else if (cam.type != LFM_SINGLE) {
+    err = "unknown camera type";
+    return LFM_E_INVALID;
+  }
+  Decomp dec;
+  lfm_status st = decompose(cam.R, dec, err);
+  if (st != LFM_OK) return st;
+  const int dims[3] = {vol.nx, vol.ny, vol.nz};
+  const double vox[3] = {vol.dx, vol.dy, vol.dz};
+  double vox_r[3] = {vox[0] / dec.D[0], vox[1] / dec.D[1], vox[2] / dec.D[2]};
+  const int nx = vol.nx, ny = vol.ny, nz = vol.nz;
+  info.type = cam.type;
+  info.basis = cam.basis;
+  info.nx = nx; info.ny = ny; info.nz = nz;
+  info.n_vox = (long long)nx * ny * nz;
+  info.n_s = cam.n_s; info.n_t = cam.n_t;
+  info.n_pix = (long long)cam.n_s * cam.n_t;
+  info.k_s = cam.k_s; info.k_t = cam.k_t;
+  info.n_views = cam.k_s * cam.k_t;
+  for (int a = 0; a < 3; ++a) { info.vox_r[a] = vox_r[a]; info.rot_D[a] = dec.D[a]; }
+  info.shear[0] = dec.a_zx; info.shear[1] = dec.a_zy; info.shear[2] = dec.a_xy;
+  info.shear[3] = dec.a_xz; info.shear[4] = dec.a_yx; info.shear[5] = dec.a_yz;
+  info.plane_array = plen ? nz : -1;
+  info.plane_detector = nz + 1;
+
+  // rotation passes in application order z, x, y
+  build_shear(cp.rot[0], 0, dec.a_zx, dec.a_zy, dims, vox_r);
+  build_shear(cp.rot[1], 1, dec.a_xy, dec.a_xz, dims, vox_r);
+  build_shear(cp.rot[2], 2, dec.a_yx, dec.a_yz, dims, vox_r);
+  info.rot_passes = (cp.rot[0].active ? 1 : 0) | (cp.rot[1].active ? 2 : 0) | (cp.rot[2].active ? 4 : 0);
+
+  // planes per axis
+  const int K[2] = {cam.k_s, cam.k_t};
+  const double d0[2] = {cam.ap_s / cam.k_s, cam.ap_t / cam.k_t};
+  const int nsrc[2] = {nx, ny};
+  const int ndet[2] = {cam.n_s, cam.n_t};
+  const double pdet[2] = {cam.px_s, cam.px_t};
+  const int nl[2] = {cam.nl_s, cam.nl_t};
+  const double dz = vox_r[2];
+  std::vector<double> zs(nz);
+  for (int n = 0; n < nz; ++n) zs[n] = cam.d_scene + ((double)n - (nz - 1) * 0.5) * dz;
+
+  Plane dst[2];
+  double V_dst[2], V_mu[2] = {0, 0};
+  std::vector<Plane> lenslets[2];
+  std::vector<std::pair<int, int>> mask_range[2];  // open array cells per lenslet [lo, hi]
+  double pitch[2] = {0, 0};
+  for (int ax = 0; ax < 2; ++ax) {
+    if (plen) {
+      pitch[ax] = ndet[ax] * pdet[ax] / nl[ax];
+      dst[ax] = Plane{nl[ax] * cam.n_a, pitch[ax] / cam.n_a, translate(-cam.d_mu_m), 0.0};
+      Affine inv;
+      for (int mu = 0; mu < nl[ax]; ++mu) {
+        double c_mu = ((double)mu - (nl[ax] - 1) * 0.5) * pitch[ax];
+        if (!invert(lens(cam.f_mu, c_mu), inv)) { err = "singular lenslet block"; return LFM_E_SINGULAR; }
+        Affine X0 = compose(translate(-cam.d_mu_m), compose(inv, translate(-cam.d_d_mu)));
+        lenslets[ax].push_back(Plane{ndet[ax], pdet[ax], X0, 0.0});
+        double half = 0.5 * cam.fill * pitch[ax];
+        int lo = 1 << 30, hi = -1;
+        for (int j = 0; j < dst[ax].n; ++j) {
+          double c = centre(dst[ax], j);
+          if (c >= c_mu - half && c < c_mu + half) { lo = std::min(lo, j); hi = std::max(hi, j); }
+        }
+        mask_range[ax].push_back({lo, hi});
+      }
+      V_mu[ax] = basis_volume(lenslets[ax][0], d0[ax]);
+    } else {
+      dst[ax] = Plane{ndet[ax], pdet[ax], translate(-cam.d_det), 0.0};
+    }
+    V_dst[ax] = basis_volume(dst[ax], d0[ax]);
+  }
+  info.n_as = plen ? dst[0].n : 0;
+  info.n_at = plen ? dst[1].n : 0;
+  const double Vdst = V_dst[0] * V_dst[1];
+  const double Vmu = V_mu[0] * V_mu[1];
+  // scalars: c1 = dz/V^a (plenoptic) or dz*sqrt(V^d)/V^d (single); c3 = sqrt(V^mu)/V^mu (Z7)
+  const double c1 = plen ? dz / Vdst : dz * std::sqrt(Vdst) / Vdst;
+  const double c3 = plen ? std::sqrt(Vmu) / Vmu : 1.0;
+  cp.scal[0] = c1; cp.scal[1] = c3; cp.scal[2] = Vdst; cp.scal[3] = Vmu; cp.scal[4] = dz;
+  cp.scal[5] = d0[0]; cp.scal[6] = d0[1]; cp.scal[7] = plen ? 1.0 : 0.0;
+
+  // ---- S1 families: slice n -> dst (fwd) and dst -> slice n (adj), per axis, table = k*nz + n
+  for (int ax = 0; ax < 2; ++ax) {
+    family_init(cp.s1f[ax], K[ax] * nz, dst[ax].n, nsrc[ax]);
+    family_init(cp.s1a[ax], K[ax] * nz, nsrc[ax], dst[ax].n);
+    FamilyBuilder bf(cp.s1f[ax]), ba(cp.s1a[ax]);
+    bf.tabs.resize(K[ax] * nz);
+    ba.tabs.resize(K[ax] * nz);
+    for (int k = 0; k < K[ax]; ++k) {
+      double sk = ((double)k - (K[ax] - 1) * 0.5) * d0[ax];
+      for (int n = 0; n < nz; ++n) {
+        Plane q{nsrc[ax], vox_r[ax], compose(lens(cam.f_main, 0.0), translate(zs[n])), 0.0};
+        st = transport_rows(q, dst[ax], sk, d0[ax], cam.basis, bf.tabs[k * nz + n], err);
+        if (st != LFM_OK) return st;
+        st = transport_rows(dst[ax], q, sk, d0[ax], cam.basis, ba.tabs[k * nz + n], err);
+        if (st != LFM_OK) return st;
+      }
+    }
+    bf.finish();
+    ba.finish();
+  }
+  // ---- S3 families (plenoptic): array -> detector through every lenslet, masked (fwd),
+  //      and detector -> array through the lenslet owning each cell (adj)
+  if (plen) {
+    for (int ax = 0; ax < 2; ++ax) {
+      family_init(cp.s3f[ax], K[ax], ndet[ax], dst[ax].n);
+      family_init(cp.s3a[ax], K[ax], dst[ax].n, ndet[ax]);
+      FamilyBuilder bf(cp.s3f[ax]), ba(cp.s3a[ax]);
+      bf.tabs.resize(K[ax]);
+      ba.tabs.resize(K[ax]);
+      // owner lenslet of every array cell
+      std::vector<int> owner(dst[ax].n, -1);
+      for (int mu = 0; mu < nl[ax]; ++mu)
+        for (int j = mask_range[ax][mu].first; j <= mask_range[ax][mu].second; ++j) owner[j] = mu;
+      for (int k = 0; k < K[ax]; ++k) {
+        double sk = ((double)k - (K[ax] - 1) * 0.5) * d0[ax];
+        // forward: union over lenslets of band_mu(i) cap open cells of mu
+        std::vector<int> lo(ndet[ax], 1 << 30), hi(ndet[ax], -1);
+        std::vector<std::vector<std::pair<int, double>>> acc(ndet[ax]);
+        for (int mu = 0; mu < nl[ax]; ++mu) {
+          int mlo = mask_range[ax][mu].first, mhi = mask_range[ax][mu].second;
+          if (mhi < mlo) continue;
+          Kernel1D kk;
+          st = make_kernel(dst[ax], lenslets[ax][mu], sk, d0[ax], cam.basis, kk, err);
+          if (st != LFM_OK) return st;
+          for (int i = 0; i < ndet[ax]; ++i) {
+            double c;
+            int blo, bhi;
+            row_band(dst[ax], lenslets[ax][mu], kk, i, c, blo, bhi);
+            blo = std::max(blo, mlo);
+            bhi = std::min(bhi, mhi);
+            if (bhi < blo) continue;
+            for (int j = blo; j <= bhi; ++j) acc[i].push_back({j, entry(dst[ax], kk, c, j)});
+            lo[i] = std::min(lo[i], blo);
+            hi[i] = std::max(hi[i], bhi);
+          }
+        }
+        auto& rows = bf.tabs[k];
+        rows.assign(ndet[ax], Row());
+        for (int i = 0; i < ndet[ax]; ++i) {
+          if (hi[i] < 0) continue;
+          rows[i].lo = lo[i];
+          rows[i].len = hi[i] - lo[i] + 1;
+          rows[i].w.assign(rows[i].len, 0.0);
+          for (auto& e : acc[i]) rows[i].w[e.first - lo[i]] += e.second;
+        }
+        // adjoint: row j (array cell) = B^{a mu(j)}[j, :] (transport detector(mu) -> array)
+        auto& arows = ba.tabs[k];
+        arows.assign(dst[ax].n, Row());
+        for (int mu = 0; mu < nl[ax]; ++mu) {
+          int mlo = mask_range[ax][mu].first, mhi = mask_range[ax][mu].second;
+          if (mhi < mlo) continue;
+          Kernel1D kk;
+          st = make_kernel(lenslets[ax][mu], dst[ax], sk, d0[ax], cam.basis, kk, err);
+          if (st != LFM_OK) return st;
+          for (int j = mlo; j <= mhi; ++j) {
+            double c;
+            int blo, bhi;
+            row_band(lenslets[ax][mu], dst[ax], kk, j, c, blo, bhi);
+            if (bhi < blo) continue;
+            Row& r = arows[j];
+            r.lo = blo;
+            r.len = bhi - blo + 1;
+            r.w.resize(r.len);
+            for (int i = blo; i <= bhi; ++i) r.w[i - blo] = entry(lenslets[ax][mu], kk, c, i);
+          }
+        }
+      }
+      bf.finish();
+      ba.finish();
+    }
+  }
+  // ---- collapsed composite per slice: C_n = sum_k S_k B_{k,n} (plenoptic) or sum_k B_{k,n} (single)
+  for (int ax = 0; ax < 2; ++ax) {
+    const BandFamily& f1 = cp.s1f[ax];
+    int nrow = ndet[ax];
+    int nv = nsrc[ax];
+    family_init(cp.cf[ax], nz, nrow, nv);
+    family_init(cp.ca[ax], nz, nv, nrow);
+    FamilyBuilder bf(cp.cf[ax]), ba(cp.ca[ax]);
+    bf.tabs.resize(nz);
+    ba.tabs.resize(nz);
+    std::vector<double> accv(nv);
+    std::vector<char> touched(nv);
+    for (int n = 0; n < nz; ++n) {
+      auto& rows = bf.tabs[n];
+      rows.assign(nrow, Row());
+      std::vector<std::vector<std::pair<int, double>>> cols(nv);  // transpose
+      for (int i = 0; i < nrow; ++i) {
+        std::fill(accv.begin(), accv.end(), 0.0);
+        std::fill(touched.begin(), touched.end(), 0);
+        int vlo = 1 << 30, vhi = -1;
+        for (int k = 0; k < K[ax]; ++k) {
+          auto add_s1 = [&](int j, double w3) {
+            size_t idx = (size_t)(k * nz + n) * f1.n_rows + j;
+            for (int q = 0; q < f1.len[idx]; ++q) {
+              int v = f1.start[idx] + q;
+              accv[v] += w3 * f1.w64[idx * f1.taps + q];
+              touched[v] = 1;
+              vlo = std::min(vlo, v);
+              vhi = std::max(vhi, v);
+            }
+          };
+          if (plen) {
+            const BandFamily& f3 = cp.s3f[ax];
+            size_t i3 = (size_t)k * f3.n_rows + i;
+            for (int q = 0; q < f3.len[i3]; ++q) {
+              double w3 = f3.w64[i3 * f3.taps + q];
+              if (w3 == 0.0) continue;  // gap between two lenslets' cells (structural zero)
+              add_s1(f3.start[i3] + q, w3);
+            }
+          } else {
+            add_s1(i, 1.0);
+          }
+        }
+        if (vhi < 0) continue;
+        Row& r = rows[i];
+        r.lo = vlo;
+        r.len = vhi - vlo + 1;
+        r.w.assign(r.len, 0.0);
+        for (int v = vlo; v <= vhi; ++v) {
+          r.w[v - vlo] = accv[v];
+          if (touched[v]) cols[v].push_back({i, accv[v]});
+        }
+      }
+      auto& arows = ba.tabs[n];
+      arows.assign(nv, Row());
+      for (int v = 0; v < nv; ++v) {
+        if (cols[v].empty()) continue;
+        Row& r = arows[v];
+        r.lo = cols[v].front().first;
+        r.len = cols[v].back().first - r.lo + 1;
+        r.w.assign(r.len, 0.0);
+        for (auto& e : cols[v]) r.w[e.first - r.lo] = e.second;
+      }
+    }
+    bf.finish();
+    ba.finish();
+  }
+  info.taps_s1 = std::max(cp.s1f[0].ell, cp.s1f[1].ell);
+  info.taps_s3 = plen ? std::max(cp.s3f[0].ell, cp.s3f[1].ell) : 0;
+  info.taps_c = std::max(cp.cf[0].ell, cp.cf[1].ell);
+
+  // ---- term lists ----
+  const int Kv = K[0] * K[1];
+  const long long nslice = (long long)nx * ny;
+  const long long nfield = plen ? (long long)dst[0].n * dst[1].n : 0;
+  const long long npix = (long long)ndet[0] * ndet[1];
+  auto tab = [&](int k_axis, int n) { return k_axis * nz + n; };
+  if (plen) {
+    // forward S1: output k (array field of view k) = c1 * sum_n B^{a q_n}_k x^r_n
+    sep_init(cp.fwd_s1, &cp.s1f[0], &cp.s1f[1], nx, ny, Kv, (float)c1);
+    for (int kt = 0; kt < K[1]; ++kt)
+      for (int ks = 0; ks < K[0]; ++ks) {
+        for (int n = 0; n < nz; ++n) sep_add(cp.fwd_s1, n * nslice, tab(ks, n), tab(kt, n), 1.f);
+        sep_close_output(cp.fwd_s1);
+      }
+    // forward S3: y = c3 * sum_k S_k a_k
+    sep_init(cp.fwd_s3, &cp.s3f[0], &cp.s3f[1], dst[0].n, dst[1].n, 1, (float)c3);
+    for (int kt = 0; kt < K[1]; ++kt)
+      for (int ks = 0; ks < K[0]; ++ks) sep_add(cp.fwd_s3, (long long)(kt * K[0] + ks) * nfield, ks, kt, 1.f);
+    sep_close_output(cp.fwd_s3);
+    // adjoint S3: field k = c3 * S_k^T r  (evaluated with the detector -> array transport)
+    sep_init(cp.adj_s3, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], Kv, (float)c3);
+    for (int kt = 0; kt < K[1]; ++kt)
+      for (int ks = 0; ks < K[0]; ++ks) {
+        sep_add(cp.adj_s3, 0, ks, kt, 1.f);
+        sep_close_output(cp.adj_s3);
+      }
+    // adjoint S1: slice n = c1 * sum_k B^{q_n a}_k field_k
+    sep_init(cp.adj_s1, &cp.s1a[0], &cp.s1a[1], dst[0].n, dst[1].n, nz, (float)c1);
+    for (int n = 0; n < nz; ++n) {
+      for (int kt = 0; kt < K[1]; ++kt)
+        for (int ks = 0; ks < K[0]; ++ks)
+          sep_add(cp.adj_s1, (long long)(kt * K[0] + ks) * nfield, tab(ks, n), tab(kt, n), 1.f);
+      sep_close_output(cp.adj_s1);
+    }
+  } else {
+    sep_init(cp.fwd_s1, &cp.s1f[0], &cp.s1f[1], nx, ny, 1, (float)c1);
+    for (int kt = 0; kt < K[1]; ++kt)
+      for (int ks = 0; ks < K[0]; ++ks)
+        for (int n = 0; n < nz; ++n) sep_add(cp.fwd_s1, n * nslice, tab(ks, n), tab(kt, n), 1.f);
+    sep_close_output(cp.fwd_s1);
+    sep_init(cp.adj_s1, &cp.s1a[0], &cp.s1a[1], ndet[0], ndet[1], nz, (float)c1);
+    for (int n = 0; n < nz; ++n) {
+      for (int kt = 0; kt < K[1]; ++kt)
+        for (int ks = 0; ks < K[0]; ++ks) sep_add(cp.adj_s1, 0, tab(ks, n), tab(kt, n), 1.f);
+      sep_close_output(cp.adj_s1);
+    }
+  }
+  // collapsed path
+  sep_init(cp.fwd_c, &cp.cf[0], &cp.cf[1], nx, ny, 1, (float)(c1 * c3));
+  for (int n = 0; n < nz; ++n) sep_add(cp.fwd_c, n * nslice, n, n, 1.f);
+  sep_close_output(cp.fwd_c);
+  // collapsed adjoint in two passes (the transposed composite spans ~10 lenslet sub-images, too wide to
+  // stage in 2D): Z_n = C_t,n^T y along t (s untouched), then x_n = C_s,n^T Z_n along s.
+  make_identity(cp.id_s, ndet[0]);
+  make_identity(cp.id_vt, ny);
+  sep_init(cp.adj_c1, &cp.id_s, &cp.ca[1], ndet[0], ndet[1], nz, 1.f);
+  for (int n = 0; n < nz; ++n) {
+    sep_add(cp.adj_c1, 0, 0, n, 1.f);
+    sep_close_output(cp.adj_c1);
+  }
+  sep_init(cp.adj_c2, &cp.ca[0], &cp.id_vt, ndet[0], ny, nz, (float)(c1 * c3));
+  for (int n = 0; n < nz; ++n) {
+    sep_add(cp.adj_c2, (long long)n * ny * ndet[0], n, 0, 1.f);
+    sep_close_output(cp.adj_c2);
+  }
+  // lf_transport ops: output b = n*K + k (S1 families), b = k (S3 families); scale 1/V^p
+  {
+    long long dplane = plen ? nfield : npix;
+    sep_init(cp.xp_s1f, &cp.s1f[0], &cp.s1f[1], nx, ny, nz * Kv, (float)(1.0 / Vdst));
+    for (int n = 0; n < nz; ++n)
+      for (int kt = 0; kt < K[1]; ++kt)
+        for (int ks = 0; ks < K[0]; ++ks) {
+          sep_add(cp.xp_s1f, (long long)(kt * K[0] + ks) * nslice, tab(ks, n), tab(kt, n), 1.f);
+          sep_close_output(cp.xp_s1f);
+        }
+    sep_init(cp.xp_s1a, &cp.s1a[0], &cp.s1a[1], dst[0].n, dst[1].n, nz * Kv, 1.f);
+    for (int n = 0; n < nz; ++n) {
+      // V^{q_n} per axis = Delta^r * D0 / z_n
+      double Vq = (vox_r[0] * d0[0] / std::fabs(zs[n])) * (vox_r[1] * d0[1] / std::fabs(zs[n]));
+      for (int kt = 0; kt < K[1]; ++kt)
+        for (int ks = 0; ks < K[0]; ++ks) {
+          sep_add(cp.xp_s1a, (long long)(kt * K[0] + ks) * dplane, tab(ks, n), tab(kt, n), (float)(1.0 / Vq));
+          sep_close_output(cp.xp_s1a);
+        }
+    }
+    if (plen) {
+      sep_init(cp.xp_s3f, &cp.s3f[0], &cp.s3f[1], dst[0].n, dst[1].n, Kv, (float)(1.0 / Vmu));
+      sep_init(cp.xp_s3a, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], Kv, (float)(1.0 / Vdst));
+      for (int kt = 0; kt < K[1]; ++kt)
+        for (int ks = 0; ks < K[0]; ++ks) {
+          sep_add(cp.xp_s3f, (long long)(kt * K[0] + ks) * nfield, ks, kt, 1.f);
+          sep_close_output(cp.xp_s3f);
+          sep_add(cp.xp_s3a, (long long)(kt * K[0] + ks) * npix, ks, kt, 1.f);
+          sep_close_output(cp.xp_s3a);
+        }
+    }
+  }
+  SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
+  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2",
+                         "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a"};
+  for (int q = 0; q < 11; ++q)
+    if (ops[q]->fs && !sep_choose_tile(*ops[q])) {
+      err = std::string("source footprint of op ") + names[q] + " exceeds shared memory";
+      return LFM_E_NOMEM;
+    }
+
+  // algorithmic work and bytes per A_forward
+  double rot_bytes = 0;
+  for (int p = 0; p < 3; ++p)
+    if (cp.rot[p].active) rot_bytes += 8.0 * info.n_vox;
+  info.fma_alg[0] = cp.fwd_s1.fma_alg + (plen ? cp.fwd_s3.fma_alg : 0.0);
+  info.fma_alg[1] = cp.fwd_c.fma_alg;
+  info.bytes_alg[0] = 4.0 * info.n_vox + rot_bytes + (plen ? 8.0 * Kv * nfield : 0.0) + 4.0 * npix;
+  info.bytes_alg[1] = 4.0 * info.n_vox + rot_bytes + 4.0 * npix;
+
+  // workspace: two rotation buffers, the per-view fields, residual/scratch, reduction partials
+  cp.ws_rot = (size_t)info.n_vox * 4;
+  cp.ws_fields = (size_t)(Kv * (plen ? nfield : 0)) * 4;
+  cp.ws_z = (size_t)nz * ny * ndet[0] * 4;
+  size_t scratch = std::max((size_t)npix * 4, (size_t)info.n_vox * 4);
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  info.ws_bytes = 2 * al(cp.ws_rot) + al(cp.ws_fields) + al(scratch) + al(4096 * 8 * 4);
+  return LFM_OK;
+}
+
+}  // namespace lfm

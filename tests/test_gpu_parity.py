@@ -1,0 +1,205 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerance (north star): max_i |y_gpu - y_oracle| / max_i |y_oracle| <= 1e-5 (reading Z24).
+Inputs: x ~ U[0,1) seed 0, y ~ U[0,1) seed 1, N(0,1) seeds 2/3 for adjoint tests.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_helpers import TOL, dev, host, max_rel, setup
+from workloads import make_config, normal_vector, uniform_vector, uniform_volume
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "small_two", "ragged"]
+PATHS = [0, 1]  # PER_VIEW, COLLAPSED
+
+
+def _ragged_config():
+    from workloads.geometry import plenoptic_camera, pose_yaw_pitch, single_camera
+    cam = plenoptic_camera(5, 7, 0.05, 3, 2, pose=pose_yaw_pitch(12.0, -7.0))
+    cam.update(nl_t=3, n_t=21, k_t=2)
+    return dict(name="ragged", volume=dict(nx=19, ny=17, nz=13, dx=0.45, dy=0.4, dz=0.35),
+                cameras=[cam, single_camera(23, 0.05, 3, pose=pose_yaw_pitch(-20.0, 10.0))])
+
+
+def _setup(name):
+    return setup(_ragged_config() if name == "ragged" else name)
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("path", PATHS)
+def test_forward_parity(name, path):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup(name)
+    x = uniform_volume(cfg["volume"], 0)
+    xd = dev(x)
+    for c, op in enumerate(ops):
+        y = torch.empty(op.n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, xd, y, ws, path=path)
+        ref = op.forward(x.astype(np.float64))
+        assert max_rel(host(y), ref) <= TOL, (name, c, path)
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("path", PATHS)
+def test_adjoint_parity(name, path):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup(name)
+    for c, op in enumerate(ops):
+        r = uniform_vector(op.n_pix, 1)
+        g = torch.empty(op.n_vox, device="cuda:0")
+        lfm.A_adjoint(plan, c, dev(r), g, ws, path=path)
+        ref = op.adjoint(r.astype(np.float64))
+        assert max_rel(host(g), ref) <= TOL, (name, c, path)
+
+
+@pytest.mark.parametrize("name", ["tiny_yaw15", "small_two", "ragged"])
+def test_adjoint_dot_fp32(name):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup(name)
+    for c, op in enumerate(ops):
+        for path in PATHS:
+            x = dev(normal_vector(op.n_vox, 2))
+            r = dev(normal_vector(op.n_pix, 3))
+            y = torch.empty(op.n_pix, device="cuda:0")
+            g = torch.empty(op.n_vox, device="cuda:0")
+            lfm.A_forward(plan, c, x, y, ws, path=path)
+            lfm.A_adjoint(plan, c, r, g, ws, path=path)
+            lhs = float((y.double() * r.double()).sum())
+            rhs = float((x.double() * g.double()).sum())
+            assert abs(lhs - rhs) / (float(y.double().norm()) * float(r.double().norm())) <= 1e-5
+
+
+def test_adjoint_accumulate():
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup("tiny_yaw15")
+    op = ops[0]
+    r = dev(uniform_vector(op.n_pix, 1))
+    base = dev(uniform_vector(op.n_vox, 7))
+    g = base.clone()
+    lfm.A_adjoint(plan, 0, r, g, ws, accumulate=True)
+    g2 = torch.empty_like(g)
+    lfm.A_adjoint(plan, 0, r, g2, ws, accumulate=False)
+    assert torch.allclose(g, base + g2, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two"])
+def test_vol_rotate_parity(name):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup(name)
+    x = uniform_volume(cfg["volume"], 0)
+    for c, op in enumerate(ops):
+        out = torch.empty(op.n_vox, device="cuda:0")
+        lfm.vol_rotate(plan, c, lfm.FWD, dev(x), out, ws)
+        assert max_rel(host(out), op.rot.forward(x.astype(np.float64))) <= TOL
+        lfm.vol_rotate(plan, c, lfm.ADJ, dev(x), out, ws)
+        assert max_rel(host(out), op.rot.adjoint(x.astype(np.float64))) <= TOL
+
+
+def _xport_ref(op, dst_kind, src_kind, n, src):
+    """Oracle transport for all views: dst_k = (1/V^p) B^{pq}_k src_k, literal matrices."""
+    from oracle.transport import basis_volume
+    cam = op.camera
+    K = cam.ks * cam.kt
+    out = []
+    for kt in range(cam.kt):
+        for ks in range(cam.ks):
+            s = src[kt * cam.ks + ks]
+            if (dst_kind, src_kind) == ("a", "q") or (dst_kind, src_kind) == ("d", "q"):
+                dst = cam.array_planes if dst_kind == "a" else cam.det_planes
+                V = basis_volume(dst[0], cam.d0[0]) * basis_volume(dst[1], cam.d0[1])
+                out.append(cam.S1[1][kt][n] @ s @ cam.S1[0][ks][n].T / V)
+            elif src_kind in ("a", "d") and dst_kind == "q":
+                q = cam.slice_planes
+                V = basis_volume(q[0][n], cam.d0[0]) * basis_volume(q[1][n], cam.d0[1])
+                # B^{qp} = (B^{pq})^T, evaluated literally as a transpose here
+                out.append(cam.S1[1][kt][n].T @ s @ cam.S1[0][ks][n] / V)
+            elif (dst_kind, src_kind) == ("d", "a"):
+                V = basis_volume(cam.lenslet_planes[0][0], cam.d0[0]) * basis_volume(cam.lenslet_planes[1][0], cam.d0[1])
+                out.append(cam.S3[1][kt] @ s @ cam.S3[0][ks].T / V)
+            elif (dst_kind, src_kind) == ("a", "d"):
+                V = basis_volume(cam.array_planes[0], cam.d0[0]) * basis_volume(cam.array_planes[1], cam.d0[1])
+                out.append(cam.S3[1][kt].T @ s @ cam.S3[0][ks] / V)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_single", "ragged"])
+def test_lf_transport_parity(name):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup(name)
+    for c, op in enumerate(ops):
+        cam = op.camera
+        inf = plan.infos[c]
+        nz, K = inf["nz"], inf["n_views"]
+        A, D = inf["plane_array"], inf["plane_detector"]
+        dims = {"q": (op.camera.ny, op.camera.nx), "d": (inf["n_t"], inf["n_s"])}
+        if inf["type"] == 1:
+            dims["a"] = (inf["n_at"], inf["n_as"])
+            pairs = [("a", "q"), ("q", "a"), ("d", "a"), ("a", "d")]
+        else:
+            pairs = [("d", "q"), ("q", "d")]
+        ids = {"a": A, "d": D}
+        for n in (0, nz // 2, nz - 1):
+            for dst_kind, src_kind in pairs:
+                src = uniform_vector(K * dims[src_kind][0] * dims[src_kind][1], 5).reshape(K, *dims[src_kind])
+                out = torch.empty(K * dims[dst_kind][0] * dims[dst_kind][1], device="cuda:0")
+                lfm.lf_transport(plan, c, ids.get(dst_kind, n), ids.get(src_kind, n), dev(src), out, ws)
+                ref = _xport_ref(op, dst_kind, src_kind, n, src.astype(np.float64))
+                assert max_rel(host(out), ref) <= TOL, (name, c, dst_kind, src_kind, n)
+
+
+def test_lf_transport_symmetry_scaling():
+    """(V^q/V^p) lf_transport(q,p) is the adjoint of lf_transport(p,q)."""
+    from paper_1812_03358_b200 import lfm
+    from oracle.transport import basis_volume
+    cfg, plan, ops, ws = _setup("tiny")
+    op = ops[0]
+    cam = op.camera
+    inf = plan.infos[0]
+    K, A, D = inf["n_views"], inf["plane_array"], inf["plane_detector"]
+    na, nd = inf["n_as"] * inf["n_at"], inf["n_s"] * inf["n_t"]
+    fa = dev(normal_vector(K * na, 2))
+    fd = dev(normal_vector(K * nd, 3))
+    out_d = torch.empty(K * nd, device="cuda:0")
+    out_a = torch.empty(K * na, device="cuda:0")
+    lfm.lf_transport(plan, 0, D, A, fa, out_d, ws)
+    lfm.lf_transport(plan, 0, A, D, fd, out_a, ws)
+    Va = basis_volume(cam.array_planes[0], cam.d0[0]) * basis_volume(cam.array_planes[1], cam.d0[1])
+    Vmu = basis_volume(cam.lenslet_planes[0][0], cam.d0[0]) * basis_volume(cam.lenslet_planes[1][0], cam.d0[1])
+    lhs = float((out_d.double() * fd.double()).sum())
+    rhs = float((fa.double() * out_a.double()).sum()) * Va / Vmu
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_paths_agree_and_deterministic():
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup("small_two")
+    x = dev(uniform_volume(cfg["volume"], 0))
+    for c, op in enumerate(ops):
+        ys = []
+        for path in PATHS + [1]:
+            y = torch.empty(op.n_pix, device="cuda:0")
+            lfm.A_forward(plan, c, x, y, ws, path=path)
+            ys.append(y)
+        assert torch.equal(ys[1], ys[2])           # bitwise repeatable (no atomics)
+        assert max_rel(host(ys[0]), host(ys[1])) <= TOL
+
+
+def test_zero_input_and_errors():
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = _setup("tiny_yaw15")
+    op = ops[0]
+    y = torch.full((op.n_pix,), 7.0, device="cuda:0")
+    lfm.A_forward(plan, 0, torch.zeros(op.n_vox, device="cuda:0"), y, ws)
+    assert float(y.abs().max()) == 0.0
+    with pytest.raises(lfm.LfmError) as e:
+        lfm.lf_transport(plan, 0, 0, 1, y, y, ws)       # slice -> slice unsupported
+    assert e.value.status == 4
+    small = torch.empty(16, dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(lfm.LfmError) as e:
+        lfm.A_forward(plan, 0, torch.zeros(op.n_vox, device="cuda:0"), y, small)
+    assert e.value.status == 1
+    with pytest.raises(lfm.LfmError):
+        lfm.A_forward(plan, 5, torch.zeros(op.n_vox, device="cuda:0"), y, ws)
