@@ -11,6 +11,7 @@
 // shear_kernel: one pass of the three-pass rotation (eqn,rot,toeplitz P:1186-1198).
 // PWLS kernels: deterministic fp64 two-level reductions, residual, 26-neighbour regulariser,
 //   FISTA update (eqn,pls P:299-317, Appendix A).
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,24 +46,35 @@ static lfm_status dev_upload(T** dst, const void* src, size_t bytes, std::string
 
 static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) {
   if (f.n_tables == 0) return LFM_OK;
-  std::vector<float> w32(f.ew64.size());
-  for (size_t i = 0; i < w32.size(); ++i) w32[i] = (float)f.ew64[i];  // one rounding fp64 -> fp32
-  lfm_status st = dev_upload(&f.d_cnt, f.cnt.data(), f.cnt.size() * sizeof(int32_t), err);
+  // device ELL layout [table][entry][pitch] with pitch = rows rounded up to 4 (16-byte cp.async rows)
+  const int pitch = (f.n_rows + 3) / 4 * 4;
+  const size_t per_h = (size_t)f.ell * f.n_rows, per_d = (size_t)f.ell * pitch;
+  std::vector<float> w32((size_t)f.n_tables * per_d, 0.f);
+  std::vector<int32_t> ix((size_t)f.n_tables * per_d, 0), cn((size_t)f.n_tables * pitch, 0);
+  for (int m = 0; m < f.n_tables; ++m) {
+    for (int r = 0; r < f.n_rows; ++r) cn[(size_t)m * pitch + r] = f.cnt[(size_t)m * f.n_rows + r];
+    for (int k = 0; k < f.ell; ++k)
+      for (int r = 0; r < f.n_rows; ++r) {
+        w32[m * per_d + (size_t)k * pitch + r] = (float)f.ew64[m * per_h + (size_t)k * f.n_rows + r];  // one rounding
+        ix[m * per_d + (size_t)k * pitch + r] = f.eidx[m * per_h + (size_t)k * f.n_rows + r];
+      }
+  }
+  lfm_status st = dev_upload(&f.d_cnt, cn.data(), cn.size() * sizeof(int32_t), err);
   if (st != LFM_OK) return st;
-  if ((st = dev_upload(&f.d_idx, f.eidx.data(), f.eidx.size() * sizeof(int32_t), err)) != LFM_OK) return st;
-  bytes += f.cnt.size() * 4 + f.eidx.size() * 4 + w32.size() * 4;
-  return dev_upload(&f.d_w, w32.data(), w32.size() * sizeof(float), err);
-}
-
-static void footprints(const BandFamily& f, int tile, std::vector<Footprint>& fp, int& ntiles) {
-  ntiles = (f.n_rows + tile - 1) / tile;
-  fp.assign((size_t)f.n_tables * ntiles, Footprint{0, 0});
-  for (int m = 0; m < f.n_tables; ++m)
-    for (int t = 0; t < ntiles; ++t) {
-      int lo, w;
-      ell_footprint(f, m, tile, t, lo, w);
-      fp[(size_t)m * ntiles + t] = Footprint{lo, w};
-    }
+  if ((st = dev_upload(&f.d_idx, ix.data(), ix.size() * sizeof(int32_t), err)) != LFM_OK) return st;
+  if ((st = dev_upload(&f.d_w, w32.data(), w32.size() * sizeof(float), err)) != LFM_OK) return st;
+  std::vector<int32_t> g4((size_t)f.n_tables * f.n_groups * 4);
+  for (size_t i = 0; i < (size_t)f.n_tables * f.n_groups; ++i) {
+    g4[4 * i] = f.g_j0[i];
+    g4[4 * i + 1] = f.g_w[i];
+    g4[4 * i + 2] = f.g_off[i];
+    g4[4 * i + 3] = 0;
+  }
+  std::vector<float> gw(f.g_w64.size() + 4);
+  for (size_t i = 0; i < f.g_w64.size(); ++i) gw[i] = (float)f.g_w64[i];
+  if ((st = dev_upload(&f.d_g, g4.data(), g4.size() * 4, err)) != LFM_OK) return st;
+  bytes += cn.size() * 4 + ix.size() * 4 + w32.size() * 4 + g4.size() * 4 + gw.size() * 4;
+  return dev_upload(&f.d_gw, gw.data(), gw.size() * 4, err);
 }
 
 static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
@@ -71,13 +83,28 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
   if (st != LFM_OK) return st;
   st = dev_upload(&op.d_offs, op.offs.data(), op.offs.size() * sizeof(int32_t), err);
   if (st != LFM_OK) return st;
-  std::vector<Footprint> fs, ft;
-  footprints(*op.fs, op.ts, fs, op.ntx);
-  footprints(*op.ft, op.tt, ft, op.nty);
-  st = dev_upload(&op.d_fp_s, fs.data(), fs.size() * sizeof(Footprint), err);
+  const BandFamily& fs = *op.fs;
+  const BandFamily& ft = *op.ft;
+  op.ntx = (fs.n_rows + op.ts - 1) / op.ts;
+  op.nty = (ft.n_rows + op.tt - 1) / op.tt;
+  std::vector<Footprint> vs((size_t)fs.n_tables * op.ntx);
+  std::vector<TileT> vt((size_t)ft.n_tables * op.nty);
+  for (int m = 0; m < fs.n_tables; ++m)
+    for (int x = 0; x < op.ntx; ++x) {
+      int lo, w;
+      ell_footprint(fs, m, op.ts, x, lo, w);
+      vs[(size_t)m * op.ntx + x] = Footprint{lo, w};
+    }
+  for (int m = 0; m < ft.n_tables; ++m)
+    for (int y = 0; y < op.nty; ++y) {
+      int lo, w, wo, wl;
+      g4_tile(ft, m, op.tt, y, lo, w, wo, wl);
+      vt[(size_t)m * op.nty + y] = TileT{lo, w, wo, wl};
+    }
+  st = dev_upload(&op.d_fp_s, vs.data(), vs.size() * sizeof(Footprint), err);
   if (st != LFM_OK) return st;
-  bytes += op.terms.size() * sizeof(Term) + (fs.size() + ft.size()) * sizeof(Footprint);
-  return dev_upload(&op.d_fp_t, ft.data(), ft.size() * sizeof(Footprint), err);
+  bytes += op.terms.size() * sizeof(Term) + vs.size() * sizeof(Footprint) + vt.size() * sizeof(TileT);
+  return dev_upload(&op.d_fp_t, vt.data(), vt.size() * sizeof(TileT), err);
 }
 
 lfm_status upload_camera(CameraPlan& cp, std::string& err) {
@@ -119,8 +146,8 @@ void free_camera(CameraPlan& cp) {
     for (BandFamily* f : {&cp.s1f[ax], &cp.s1a[ax], &cp.s3f[ax], &cp.s3a[ax], &cp.cf[ax], &cp.ca[ax]})
       fams.push_back(f);
   for (BandFamily* f : fams) {
-    dfree(f->d_cnt); dfree(f->d_idx); dfree(f->d_w);
-    f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr;
+    dfree(f->d_cnt); dfree(f->d_idx); dfree(f->d_w); dfree(f->d_g); dfree(f->d_gw);
+    f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
@@ -138,7 +165,13 @@ void free_camera(CameraPlan& cp) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Separable banded sum (ELL tables)
+// Separable banded sum, v2.
+//   pass 1 (s direction, gather): U[r][c] = sum_k ws[c][k] * X[r][idx_s[c][k]] for the staged source
+//          rows r of the tile's t footprint and the tile's output columns c (ELL s table);
+//   pass 2 (t direction, the large pass): out[4g+q][c] += sum_p wt[g][p][q] * U[j0_g + p][c] with the
+//          weights of a group of 4 output rows shared by a whole warp (G4 t table) and 4 columns per
+//          thread: one broadcast LDS.128 of weights + one LDS.128 of U feed 16 FFMAs.
+//   `nb` terms (slices / views) are staged per barrier.
 struct SepArgs {
   const float* src;
   float* out;
@@ -148,176 +181,298 @@ struct SepArgs {
   const int32_t* s_cnt;
   const int32_t* s_idx;
   const float* s_w;
-  const int32_t* t_cnt;
-  const int32_t* t_idx;
-  const float* t_w;
+  const int4* t_g;
+  const float* t_gw;
   const Footprint* fp_s;
-  const Footprint* fp_t;
-  int s_ell, t_ell;
+  const TileT* fp_t;
+  int s_ell, t_ngroups;
   int ntx, nty;
   int n_os, n_ot, n_is, n_it;
-  int fsp;   // smem row pitch of the staged source / T1 tiles
-  int ftm;   // max staged rows
+  int fsp, ftm, wtm, nb;
+  int nbuf;     // 2: double-buffered chunks, 1: a single chunk per output
+  int s_ident;  // s table is the identity: pass 1 is a copy (source rows staged straight into U)
   float out_scale;
   int accumulate;
 };
 
-constexpr int SEP_THREADS = 256;
+// Shared-memory layout of one staged term (floats); must match sep_smem() in plan.cpp.
+struct SlotLayout {
+  int xs, sw, si, sc, wt, gd, per;
+};
+__host__ __device__ inline SlotLayout slot_layout(int ftm, int fsp, int stage, int s_ell, int ts, int wtm, int ng) {
+  SlotLayout L;
+  L.xs = 0;
+  int x = stage ? (ftm * fsp + 3) / 4 * 4 : 0;
+  L.sw = x;
+  L.si = L.sw + s_ell * ts;
+  L.sc = L.si + s_ell * ts;
+  L.wt = L.sc + ts;
+  L.gd = L.wt + (wtm + 3) / 4 * 4;
+  L.per = L.gd + 4 * ng;
+  return L;
+}
 
-// TAPS_S > 0: s entries held in registers (<= TAPS_S per row); TAPS_S == 0: runtime loop from L1.
-template <int TS, int TT, int TAPS_S>
-__global__ void __launch_bounds__(SEP_THREADS) sep_kernel(SepArgs a) {
-  extern __shared__ float smem[];
-  constexpr int ROW_STEP = SEP_THREADS / TS;       // rows between a thread's outputs
-  constexpr int R = TS * TT / SEP_THREADS;          // outputs per thread
-  static_assert(R >= 1 && TS * TT % SEP_THREADS == 0, "tile must be a multiple of the block");
+// Per-term header cached in shared memory for the chunk.
+struct TermHdr {
+  long long src_off;
+  float scale;
+  int fs_lo, fs_w, ft_lo, ft_w, woff, s_tab, t_tab;
+};
+
+// TS x TT output tile, NT threads, CW columns per thread in pass 2 (4 or 8); STAGE = stage the source
+// footprint in smem (else pass 1 reads L1/L2); TAPS > 0: a column's s entries (<= TAPS) live in
+// registers, TAPS == 0: runtime count.  Chunks of nb terms are staged with cp.async into a double
+// buffer (headers, tables, weights, source footprint) so the loads of chunk i+1 overlap chunk i.
+template <int TS, int TT, int NT, int CW, bool STAGE, int TAPS>
+__global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
+  constexpr int NQ = TS / CW;          // column blocks per tile
+  constexpr int GSTEP = NT / NQ;
+  constexpr int NG = TT / 4;           // row groups per tile
+  constexpr int GP = NG / GSTEP;       // groups per thread
+  constexpr int CPT = NT / TS;         // threads per column in pass 1
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % TS == 0 && (CW == 4 || CW == 8), "tile/thread mismatch");
+  extern __shared__ __align__(16) float smem[];
+  __shared__ TermHdr hdr[2][8];
   const int tid = threadIdx.x;
   const int tx = blockIdx.x, ty = blockIdx.y, b = blockIdx.z;
   const int os0 = tx * TS, ot0 = ty * TT;
-  float* stage = smem;                               // [ftm][fsp]
-  float* t1 = stage + (size_t)a.ftm * a.fsp;         // [TT][fsp]
-  float* tw = t1 + (size_t)TT * a.fsp;               // [TT][t_ell]
-  int* tix = (int*)(tw + TT * a.t_ell);              // [TT][t_ell]
-  int* tcn = tix + TT * a.t_ell;                     // [TT]
-  // zero-fill once so padded (zero-weight) taps only ever read finite values
-  for (int e = tid; e < (a.ftm + TT) * a.fsp; e += SEP_THREADS) smem[e] = 0.f;
+  const SlotLayout L = slot_layout(a.ftm, a.fsp, STAGE && !a.s_ident, a.s_ell, TS, a.wtm, NG);
+  const int nbuf = a.nbuf;
+  float* bufs[2] = {smem, smem + (nbuf - 1) * a.nb * L.per};
+  float* Ubase = smem + nbuf * a.nb * L.per;   // [nbuf][nb][ftm][TS]
+  const int quad = tid % NQ, gsub = tid / NQ;
+  const int pc = tid % TS, pr0 = tid / TS;
+  const int pitch = (a.n_os + 3) / 4 * 4;      // ELL row pitch on the device
+  const bool col_ok = os0 + pc < a.n_os;
 
-  const int my_s = tid % TS;
-  const int my_t0 = tid / TS;
-  const int os = os0 + my_s;
-  const bool s_ok = os < a.n_os;
-  float acc[R], acc_hi[R];
+  float acc[GP][4][CW], hi[GP][4][CW];
 #pragma unroll
-  for (int r = 0; r < R; ++r) { acc[r] = 0.f; acc_hi[r] = 0.f; }
+  for (int j = 0; j < GP; ++j)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) { acc[j][r][c] = 0.f; hi[j][r][c] = 0.f; }
 
   const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  int since_flush = 0;
-  for (int e = e0; e < e1; ++e) {
-    const Term term = a.terms[e];
-    const Footprint fs = a.fp_s[(size_t)term.s_tab * a.ntx + tx];
-    const Footprint ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
-    if (fs.width == 0 || ft.width == 0) continue;    // CTA-uniform: no contribution to this tile
-    __syncthreads();                                  // previous term finished with smem
-    const float* src = a.src + term.src_off;
-    // stage the source footprint rows [ft.lo, ft.lo+ft.width) x cols [fs.lo, fs.lo+fs.width)
-    const int nst = ft.width * fs.width;
-    for (int q = tid; q < nst; q += SEP_THREADS) {
-      int r = q / fs.width, c = q - r * fs.width;
-      int row = ft.lo + r, col = fs.lo + c;
-      float v = 0.f;
-      if (row < a.n_it && col < a.n_is) v = __ldg(src + (size_t)row * a.n_is + col);
-      stage[r * a.fsp + c] = v;
-    }
-    // this tile's t-rows: counts, footprint-relative source rows, weights
-    {
-      const size_t tb = (size_t)term.t_tab * a.t_ell * a.n_ot;
-      for (int q = tid; q < TT * a.t_ell; q += SEP_THREADS) {
-        int tt = q / a.t_ell, k = q - tt * a.t_ell;
-        int row = ot0 + tt;
-        float w = 0.f;
-        int ix = 0;
-        if (row < a.n_ot) {
-          w = __ldg(a.t_w + tb + (size_t)k * a.n_ot + row);
-          ix = min(max(__ldg(a.t_idx + tb + (size_t)k * a.n_ot + row) - ft.lo, 0), ft.width - 1);
-        }
-        tw[q] = w;
-        tix[q] = ix;
+  const int nchunks = (e1 - e0 + a.nb - 1) / a.nb;
+
+  // Stage chunk ci into buffer side `sd`: headers (synchronously, tiny) + async copies.
+  auto stage_chunk = [&](int ci, int sd) {
+    const int e = e0 + ci * a.nb;
+    const int nterm = min(a.nb, e1 - e);
+    float* buf = bufs[sd];
+    for (int sl = 0; sl < nterm; ++sl) {
+      const Term term = a.terms[e + sl];
+      const Footprint fs = a.fp_s[(size_t)term.s_tab * a.ntx + tx];
+      const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
+      if (tid == 0) {
+        TermHdr h;
+        h.src_off = term.src_off;
+        h.scale = term.scale;
+        h.fs_lo = fs.lo;
+        h.fs_w = (fs.width == 0 || ft.width == 0) ? 0 : fs.width;
+        h.ft_lo = ft.lo;
+        h.ft_w = ft.width;
+        h.woff = ft.woff;
+        h.s_tab = term.s_tab;
+        h.t_tab = term.t_tab;
+        hdr[sd][sl] = h;
       }
-      for (int tt = tid; tt < TT; tt += SEP_THREADS) {
-        int row = ot0 + tt;
-        tcn[tt] = row < a.n_ot ? __ldg(a.t_cnt + (size_t)term.t_tab * a.n_ot + row) : 0;
-      }
-    }
-    __syncthreads();
-    // t-pass (minor direction first): t1[tt][c] = sum_k tw[tt][k] * stage[tix[tt][k]][c]
-    const int nt1 = TT * fs.width;
-    for (int q = tid; q < nt1; q += SEP_THREADS) {
-      int tt = q / fs.width, c = q - tt * fs.width;
-      const float* wr = tw + tt * a.t_ell;
-      const int* ir = tix + tt * a.t_ell;
-      const int cn = tcn[tt];
-      float v = 0.f;
-      for (int k = 0; k < cn; ++k) v = fmaf(wr[k], stage[ir[k] * a.fsp + c], v);
-      t1[tt * a.fsp + c] = v;
-    }
-    __syncthreads();
-    // s-pass: my column os, rows my_t0 + r*ROW_STEP, exact non-zero list (padded to the warp max)
-    {
-      const size_t sb = (size_t)term.s_tab * a.s_ell * a.n_os;
-      const int cnt = s_ok ? __ldg(a.s_cnt + (size_t)term.s_tab * a.n_os + os) : 0;
-      const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
-      if constexpr (TAPS_S > 0) {
-        float w[TAPS_S];
-        int ix[TAPS_S];
-#pragma unroll
-        for (int k = 0; k < TAPS_S; ++k) {
-          w[k] = 0.f;
-          ix[k] = 0;
-          if (k < cmax && s_ok) {
-            w[k] = __ldg(a.s_w + sb + (size_t)k * a.n_os + os) * term.scale;
-            ix[k] = min(max(__ldg(a.s_idx + sb + (size_t)k * a.n_os + os) - fs.lo, 0), fs.width - 1);
+      if (fs.width == 0 || ft.width == 0) continue;
+      float* slot = buf + sl * L.per;
+      if (a.s_ident) {
+        // U[r][c] = src[ft.lo + r][os0 + c]: 16-byte pieces where aligned, else 4-byte
+        float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
+        const float* src = a.src + term.src_off + os0;
+        const bool al16 = ((a.n_is & 3) == 0) && ((term.src_off & 3) == 0);
+        const int ncol = min(TS, a.n_is - os0);
+        if (al16 && ncol == TS) {
+          for (int q = tid; q < ft.width * (TS / 4); q += NT) {
+            const int r = q / (TS / 4), c4 = q - r * (TS / 4);
+            __pipeline_memcpy_async(U + r * TS + 4 * c4, src + (size_t)(ft.lo + r) * a.n_is + 4 * c4, 16);
+          }
+        } else {
+          for (int q = tid; q < ft.width * TS; q += NT) {
+            const int r = q / TS, c = q - r * TS;
+            if (c < ncol) __pipeline_memcpy_async(U + r * TS + c, src + (size_t)(ft.lo + r) * a.n_is + c, 4);
+            else U[r * TS + c] = 0.f;
           }
         }
+      } else if (STAGE) {
+        const float* src = a.src + term.src_off + fs.lo;
+        const int n = ft.width * fs.width;
+        for (int q = tid; q < n; q += NT) {
+          const int r = q / fs.width, c = q - r * fs.width;
+          const int row = min(ft.lo + r, a.n_it - 1);
+          __pipeline_memcpy_async(slot + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
+        }
+      }
+      const size_t sb = (size_t)term.s_tab * a.s_ell * pitch + os0;
+      for (int q = tid; q < a.s_ell * (TS / 4); q += NT) {
+        const int k = q / (TS / 4), c4 = q - k * (TS / 4);
+        if (os0 + 4 * c4 >= pitch) continue;
+        __pipeline_memcpy_async(slot + L.sw + k * TS + 4 * c4, a.s_w + sb + (size_t)k * pitch + 4 * c4, 16);
+        __pipeline_memcpy_async(slot + L.si + k * TS + 4 * c4, a.s_idx + sb + (size_t)k * pitch + 4 * c4, 16);
+      }
+      for (int c4 = tid; c4 < TS / 4; c4 += NT)
+        if (os0 + 4 * c4 < pitch)
+          __pipeline_memcpy_async(slot + L.sc + 4 * c4, a.s_cnt + (size_t)term.s_tab * pitch + os0 + 4 * c4, 16);
+      for (int q = tid; q < ft.wlen / 4; q += NT)
+        __pipeline_memcpy_async(slot + L.wt + 4 * q, a.t_gw + ft.woff + 4 * q, 16);
+      const int g0 = ty * NG;
+      for (int q = tid; q < NG; q += NT)
+        if (g0 + q < a.t_ngroups)
+          __pipeline_memcpy_async(slot + L.gd + 4 * q, a.t_g + (size_t)term.t_tab * a.t_ngroups + g0 + q, 16);
+    }
+    __pipeline_commit();
+  };
+
+  if (nchunks > 0) stage_chunk(0, 0);
+  int chunks = 0;
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int sd = ci & 1;
+    const int nterm = min(a.nb, e1 - (e0 + ci * a.nb));
+    float* buf = bufs[sd];
+    if (ci + 1 < nchunks) {
+      stage_chunk(ci + 1, sd ^ 1);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncthreads();
+    // ---- pass 1 (s gather): U[r][c] = sum_k w_c[k] * X[r][idx_c[k]], two independent rows per step
+    for (int sl = 0; sl < nterm && !a.s_ident; ++sl) {
+      const TermHdr h = hdr[sd][sl];
+      if (h.fs_w == 0) continue;
+      const float* slot = buf + sl * L.per;
+      float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
+      const int cnt = col_ok ? reinterpret_cast<const int*>(slot + L.sc)[pc] : 0;
+      const float* SW = slot + L.sw;
+      const int* SI = reinterpret_cast<const int*>(slot + L.si);
+      const float* gsrc = a.src + h.src_off + h.fs_lo;
+      if constexpr (TAPS > 0) {
+        float w[TAPS];
+        int ix[TAPS];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float* tr = t1 + (my_t0 + r * ROW_STEP) * a.fsp;
-          float v = 0.f;
+        for (int k = 0; k < TAPS; ++k) {
+          w[k] = k < cnt ? SW[k * TS + pc] * h.scale : 0.f;
+          ix[k] = k < cnt ? min(max(SI[k * TS + pc] - h.fs_lo, 0), h.fs_w - 1) : 0;
+        }
+        for (int r = pr0; r < h.ft_w; r += 2 * CPT) {
+          const int r2 = r + CPT;
+          const bool two = r2 < h.ft_w;
+          float v = 0.f, v2 = 0.f;
+          if (STAGE) {
+            const float* xr = slot + L.xs + r * a.fsp;
+            const float* xr2 = slot + L.xs + (two ? r2 : r) * a.fsp;
 #pragma unroll
-          for (int k = 0; k < TAPS_S; ++k)
-            if (k < cmax) v = fmaf(w[k], tr[ix[k]], v);
-          acc[r] += v;
+            for (int k = 0; k < TAPS; ++k) {
+              if (k >= cnt) break;
+              v = fmaf(w[k], xr[ix[k]], v);
+              v2 = fmaf(w[k], xr2[ix[k]], v2);
+            }
+          } else {
+            const int row = min(h.ft_lo + r, a.n_it - 1), row2 = min(h.ft_lo + (two ? r2 : r), a.n_it - 1);
+            const float* xr = gsrc + (size_t)row * a.n_is;
+            const float* xr2 = gsrc + (size_t)row2 * a.n_is;
+#pragma unroll
+            for (int k = 0; k < TAPS; ++k) {
+              if (k >= cnt) break;
+              v = fmaf(w[k], __ldg(xr + ix[k]), v);
+              v2 = fmaf(w[k], __ldg(xr2 + ix[k]), v2);
+            }
+          }
+          U[r * TS + pc] = v;
+          if (two) U[r2 * TS + pc] = v2;
         }
       } else {
-        for (int k = 0; k < cmax; ++k) {
-          float wk = 0.f;
-          int ik = 0;
-          if (s_ok) {
-            wk = __ldg(a.s_w + sb + (size_t)k * a.n_os + os) * term.scale;
-            ik = min(max(__ldg(a.s_idx + sb + (size_t)k * a.n_os + os) - fs.lo, 0), fs.width - 1);
+        for (int r = pr0; r < h.ft_w; r += CPT) {
+          float v = 0.f;
+          const float* xr = STAGE ? slot + L.xs + r * a.fsp
+                                  : gsrc + (size_t)min(h.ft_lo + r, a.n_it - 1) * a.n_is;
+          for (int k = 0; k < cnt; ++k) {
+            const int ik = min(max(SI[k * TS + pc] - h.fs_lo, 0), h.fs_w - 1);
+            v = fmaf(SW[k * TS + pc], STAGE ? xr[ik] : __ldg(xr + ik), v);
           }
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = fmaf(wk, t1[(my_t0 + r * ROW_STEP) * a.fsp + ik], acc[r]);
+          U[r * TS + pc] = v * h.scale;
         }
       }
     }
-    if (++since_flush == 16) {  // blocked accumulation (keeps long positive sums accurate)
+    __syncthreads();
+    // ---- pass 2 (t direction): groups of 4 output rows x CW columns per thread, warp-uniform weights
+    for (int sl = 0; sl < nterm; ++sl) {
+      const TermHdr h = hdr[sd][sl];
+      if (h.fs_w == 0) continue;
+      const float* slot = buf + sl * L.per;
+      const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
+      const int4* GD = reinterpret_cast<const int4*>(slot + L.gd);
 #pragma unroll
-      for (int r = 0; r < R; ++r) { acc_hi[r] += acc[r]; acc[r] = 0.f; }
-      since_flush = 0;
+      for (int j = 0; j < GP; ++j) {
+        const int gl = gsub + j * GSTEP;
+        if (ty * NG + gl >= a.t_ngroups) continue;
+        const int4 gd = GD[gl];
+        const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.woff));
+        const float* up = U + (gd.x - h.ft_lo) * TS + quad * CW;
+#pragma unroll 2
+        for (int p = 0; p < gd.y; ++p) {
+          const float4 w4 = wp[p];
+          const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int cb = 0; cb < CW; cb += 4) {
+            const float4 u4 = *reinterpret_cast<const float4*>(up + p * TS + cb);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              acc[j][r][cb + 0] = fmaf(wr[r], u4.x, acc[j][r][cb + 0]);
+              acc[j][r][cb + 1] = fmaf(wr[r], u4.y, acc[j][r][cb + 1]);
+              acc[j][r][cb + 2] = fmaf(wr[r], u4.z, acc[j][r][cb + 2]);
+              acc[j][r][cb + 3] = fmaf(wr[r], u4.w, acc[j][r][cb + 3]);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // chunk done with U and its buffer before they are refilled
+    if (++chunks == 4) {  // blocked accumulation (keeps long positive sums accurate)
+      chunks = 0;
+#pragma unroll
+      for (int j = 0; j < GP; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < CW; ++c) { hi[j][r][c] += acc[j][r][c]; acc[j][r][c] = 0.f; }
     }
   }
-  if (!s_ok) return;
   float* outb = a.out + (size_t)b * a.out_stride;
+  const int col = os0 + quad * CW;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    int row = ot0 + my_t0 + r * ROW_STEP;
-    if (row >= a.n_ot) continue;
-    float v = a.out_scale * (acc_hi[r] + acc[r]);
-    float* p = outb + (size_t)row * a.n_os + os;
-    *p = a.accumulate ? *p + v : v;
+  for (int j = 0; j < GP; ++j) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+      if (row >= a.n_ot) continue;
+      float* p = outb + (size_t)row * a.n_os + col;
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        if (col + c >= a.n_os) continue;
+        const float v = a.out_scale * (hi[j][r][c] + acc[j][r][c]);
+        p[c] = a.accumulate ? p[c] + v : v;
+      }
+    }
   }
 }
 
-template <int TS, int TT, int TAPS_S>
+template <int TS, int TT, int NT, int CW, bool STAGE, int TAPS>
 static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
-  auto kern = sep_kernel<TS, TT, TAPS_S>;
+  auto kern = sep_kernel<TS, TT, NT, CW, STAGE, TAPS>;
   static bool configured = false;  // per instantiation
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(sep_kernel)", err);
     configured = true;
   }
-  kern<<<grid, SEP_THREADS, smem, s>>>(a);
+  kern<<<grid, NT, smem, s>>>(a);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "sep_kernel launch", err);
-}
-
-template <int TS, int TT>
-static lfm_status launch_sep_taps(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
-  if (a.s_ell <= 4) return launch_sep_t<TS, TT, 4>(a, grid, smem, s, err);
-  if (a.s_ell <= 8) return launch_sep_t<TS, TT, 8>(a, grid, smem, s, err);
-  if (a.s_ell <= 16) return launch_sep_t<TS, TT, 16>(a, grid, smem, s, err);
-  return launch_sep_t<TS, TT, 0>(a, grid, smem, s, err);
 }
 
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
@@ -332,32 +487,47 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.s_cnt = op.fs->d_cnt;
   a.s_idx = op.fs->d_idx;
   a.s_w = op.fs->d_w;
-  a.t_cnt = op.ft->d_cnt;
-  a.t_idx = op.ft->d_idx;
-  a.t_w = op.ft->d_w;
+  a.t_g = reinterpret_cast<const int4*>(op.ft->d_g);
+  a.t_gw = op.ft->d_gw;
   a.fp_s = op.d_fp_s;
   a.fp_t = op.d_fp_t;
   a.s_ell = op.fs->ell;
-  a.t_ell = op.ft->ell;
+  a.t_ngroups = op.ft->n_groups;
   a.ntx = op.ntx;
   a.nty = op.nty;
   a.n_os = op.n_os;
   a.n_ot = op.n_ot;
   a.n_is = op.n_is;
   a.n_it = op.n_it;
-  a.fsp = op.fs_max + 1;  // +1: odd pitch spreads t-pass rows over banks
+  a.fsp = op.fs_max + 1;
   a.ftm = op.ft_max;
+  a.wtm = op.wt_max;
+  a.s_ident = op.s_ident;
+  {
+    int maxt = 0;
+    for (size_t q = 0; q + 1 < op.offs.size(); ++q) maxt = std::max(maxt, op.offs[q + 1] - op.offs[q]);
+    a.nbuf = maxt > op.nb ? 2 : 1;
+  }
+  a.nb = op.nb;
   a.out_scale = op.out_scale;
   a.accumulate = accumulate;
-  size_t smem = ((size_t)a.ftm * a.fsp + (size_t)op.tt * a.fsp) * 4 + (size_t)op.tt * a.t_ell * 8 + (size_t)op.tt * 4;
+  const size_t smem = sep_smem(op, op.nb);
   dim3 grid(op.ntx, op.nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
-  const int ts = op.ts, tt = op.tt;
-  if (ts == 64 && tt == 32) return launch_sep_taps<64, 32>(a, grid, smem, s, err);
-  if (ts == 64 && tt == 16) return launch_sep_taps<64, 16>(a, grid, smem, s, err);
-  if (ts == 32 && tt == 32) return launch_sep_taps<32, 32>(a, grid, smem, s, err);
-  if (ts == 32 && tt == 16) return launch_sep_taps<32, 16>(a, grid, smem, s, err);
-  if (ts == 16 && tt == 16) return launch_sep_taps<16, 16>(a, grid, smem, s, err);
+#define LFM_SEP_CASE(TS_, TT_, NT_, CW_)                                                              \
+  if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) {                                                \
+    if (a.s_ell <= 8)                                                                                \
+      return op.stage ? launch_sep_t<TS_, TT_, NT_, CW_, true, 8>(a, grid, smem, s, err)             \
+                      : launch_sep_t<TS_, TT_, NT_, CW_, false, 8>(a, grid, smem, s, err);           \
+    return op.stage ? launch_sep_t<TS_, TT_, NT_, CW_, true, 0>(a, grid, smem, s, err)               \
+                    : launch_sep_t<TS_, TT_, NT_, CW_, false, 0>(a, grid, smem, s, err);             \
+  }
+  LFM_SEP_CASE(128, 64, 256, 8)
+  LFM_SEP_CASE(128, 32, 128, 8)
+  LFM_SEP_CASE(64, 64, 128, 8)
+  LFM_SEP_CASE(64, 32, 64, 8)
+  LFM_SEP_CASE(32, 32, 64, 4)
+#undef LFM_SEP_CASE
   err = "unsupported sep tile";
   return LFM_E_INVALID;
 }

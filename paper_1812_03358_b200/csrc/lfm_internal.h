@@ -38,6 +38,13 @@ struct BandFamily {
   int32_t* d_cnt = nullptr;
   int32_t* d_idx = nullptr;
   float* d_w = nullptr;
+  // G4 form (rows grouped by 4): per group the union window [j0, j0+W) of source cells and W x 4
+  // dense weights (row-interleaved), used when the family is the t side of an op (warp-uniform).
+  int n_groups = 0, gmax = 0;
+  std::vector<int32_t> g_j0, g_w, g_off;  // [table][group]
+  std::vector<double> g_w64;              // flat, per table contiguous
+  int32_t* d_g = nullptr;                 // int4 per [table][group]: j0, W, off, 0
+  float* d_gw = nullptr;
 };
 
 // One summand of a separable banded sum: source plane at src_base + src_off, s/t table indices.
@@ -53,6 +60,10 @@ struct Term {
 struct Footprint {
   int32_t lo, width;
 };
+// Per (t-table, output tile_y): footprint plus the tile's block of G4 weights.
+struct TileT {
+  int32_t lo, width, woff, wlen;
+};
 
 // out[b] = out_scale * sum_{terms of b} scale * (B_s[s_tab] (x) B_t[t_tab]) src   (t-pass, s-pass)
 struct SepOp {
@@ -60,15 +71,19 @@ struct SepOp {
   const BandFamily* ft = nullptr;  // rows = output t cells
   int n_os = 0, n_ot = 0, n_is = 0, n_it = 0, n_out = 0;
   float out_scale = 1.f;
-  int ts = 64, tt = 32;            // output tile
+  int ts = 128, tt = 64, nt = 256;  // output tile, threads per CTA
   int fs_max = 0, ft_max = 0;      // max source footprint per tile (s, t)
   std::vector<Term> terms;
   std::vector<int32_t> offs;       // n_out + 1
   Term* d_terms = nullptr;
   int32_t* d_offs = nullptr;
   int ntx = 0, nty = 0;            // output tiles along s, t
+  int nb = 1;                      // terms staged per barrier
+  int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
+  int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
+  int wt_max = 0;                  // max G4 weight floats of one t tile
   Footprint* d_fp_s = nullptr;     // [s-table][tile_x]
-  Footprint* d_fp_t = nullptr;     // [t-table][tile_y]
+  TileT* d_fp_t = nullptr;         // [t-table][tile_y]
   double fma_alg = 0;              // sum over terms of nnz work (algorithmic)
 };
 
@@ -110,6 +125,8 @@ struct lfm_plan_s {
 namespace lfm {
 // plan.cpp (host fp64)
 void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width);
+void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen);
+size_t sep_smem(const SepOp& op, int nb);
 lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& out, std::string& err);
 // kernels.cu
 lfm_status upload_camera(CameraPlan& cp, std::string& err);

@@ -14,6 +14,8 @@
 //    P:1011-1024), and the K-collapsed composite C_n = sum_k S_k B^{a q_n}_k (exact re-association).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -195,6 +197,63 @@ static void build_ell(BandFamily& f) {
       }
       for (; e < f.ell; ++e) f.eidx[m * per + (size_t)e * f.n_rows + r] = first;  // zero-weight padding
     }
+  // G4 form: groups of 4 consecutive rows, union window of their bands, dense row-interleaved weights
+  f.n_groups = (f.n_rows + 3) / 4;
+  size_t ng = (size_t)f.n_tables * f.n_groups;
+  f.g_j0.assign(ng, 0);
+  f.g_w.assign(ng, 0);
+  f.g_off.assign(ng, 0);
+  f.g_w64.clear();
+  f.gmax = 0;
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int g = 0; g < f.n_groups; ++g) {
+      int lo = 1 << 30, hi = -1;
+      for (int q = 0; q < 4; ++q) {
+        int r = 4 * g + q;
+        if (r >= f.n_rows) break;
+        size_t idx = (size_t)m * f.n_rows + r;
+        if (!f.len[idx]) continue;
+        lo = std::min(lo, (int)f.start[idx]);
+        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
+      }
+      size_t gi = (size_t)m * f.n_groups + g;
+      f.g_off[gi] = (int)f.g_w64.size();
+      if (hi < 0) continue;
+      int W = hi - lo;
+      f.g_j0[gi] = lo;
+      f.g_w[gi] = W;
+      f.gmax = std::max(f.gmax, W);
+      size_t base = f.g_w64.size();
+      f.g_w64.resize(base + (size_t)W * 4, 0.0);
+      for (int q = 0; q < 4; ++q) {
+        int r = 4 * g + q;
+        if (r >= f.n_rows) break;
+        size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e) {
+          int j = f.start[idx] + e;
+          f.g_w64[base + (size_t)(j - lo) * 4 + q] = f.w64[idx * f.taps + e];
+        }
+      }
+    }
+}
+
+// Union window of the G4 groups of output tile t (rows [t*tile, (t+1)*tile)), and its weight block.
+void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen) {
+  int g0 = t * tile / 4, g1 = std::min(f.n_groups, (t + 1) * tile / 4);
+  int mn = 1 << 30, mx = -1;
+  for (int g = g0; g < g1; ++g) {
+    size_t gi = (size_t)tab * f.n_groups + g;
+    if (!f.g_w[gi]) continue;
+    mn = std::min(mn, (int)f.g_j0[gi]);
+    mx = std::max(mx, (int)(f.g_j0[gi] + f.g_w[gi]));
+  }
+  woff = g0 < f.n_groups ? f.g_off[(size_t)tab * f.n_groups + g0] : 0;
+  int end = (g1 < f.n_groups) ? f.g_off[(size_t)tab * f.n_groups + g1]
+                              : (tab + 1 < f.n_tables ? f.g_off[(size_t)(tab + 1) * f.n_groups] : (int)f.g_w64.size());
+  wlen = end - woff;
+  if (mx < 0) { lo = 0; width = 0; return; }
+  lo = mn;
+  width = mx - mn;
 }
 
 struct FamilyBuilder {
@@ -370,34 +429,36 @@ static void fill_sep_geometry(SepOp& op) {
   const BandFamily& ft = *op.ft;
   op.fs_max = 1;
   op.ft_max = 1;
+  op.wt_max = 4;
   std::vector<char> seen_s(fs.n_tables, 0), seen_t(ft.n_tables, 0);
   double fma = 0;
   int ntx = (fs.n_rows + op.ts - 1) / op.ts, nty = (ft.n_rows + op.tt - 1) / op.tt;
-  std::vector<double> used_s(fs.n_tables, 0), sum_s(fs.n_tables, 0), sum_t(ft.n_tables, 0);
+  std::vector<double> sum_s(fs.n_tables, 0), sum_t(ft.n_tables, 0), used_t(ft.n_tables, 0);
   for (const Term& t : op.terms) {
     if (!seen_s[t.s_tab]) {
       seen_s[t.s_tab] = 1;
-      int glo = 1 << 30, ghi = -1;
       for (int x = 0; x < ntx; ++x) {
         int lo, w;
         ell_footprint(fs, t.s_tab, op.ts, x, lo, w);
         op.fs_max = std::max(op.fs_max, w);
-        if (w) { glo = std::min(glo, lo); ghi = std::max(ghi, lo + w); }
       }
-      used_s[t.s_tab] = ghi > glo ? ghi - glo : 0;
       for (int r = 0; r < fs.n_rows; ++r) sum_s[t.s_tab] += fs.cnt[(size_t)t.s_tab * fs.n_rows + r];
     }
     if (!seen_t[t.t_tab]) {
       seen_t[t.t_tab] = 1;
+      int glo = 1 << 30, ghi = -1;
       for (int y = 0; y < nty; ++y) {
-        int lo, w;
-        ell_footprint(ft, t.t_tab, op.tt, y, lo, w);
+        int lo, w, wo, wl;
+        g4_tile(ft, t.t_tab, op.tt, y, lo, w, wo, wl);
         op.ft_max = std::max(op.ft_max, w);
+        op.wt_max = std::max(op.wt_max, wl);
+        if (w) { glo = std::min(glo, lo); ghi = std::max(ghi, lo + w); }
       }
+      used_t[t.t_tab] = ghi > glo ? ghi - glo : 0;
       for (int r = 0; r < ft.n_rows; ++r) sum_t[t.t_tab] += ft.cnt[(size_t)t.t_tab * ft.n_rows + r];
     }
-    // algorithmic FMAs (non-zeros only): t-pass over the used source s range, then the s-pass
-    fma += sum_t[t.t_tab] * used_s[t.s_tab] + sum_s[t.s_tab] * ft.n_rows;
+    // algorithmic FMAs (non-zeros only) of the s-then-t evaluation the kernel performs
+    fma += used_t[t.t_tab] * sum_s[t.s_tab] + sum_t[t.t_tab] * fs.n_rows;
   }
   op.fma_alg = fma;
 }
@@ -412,6 +473,7 @@ static void sep_init(SepOp& op, const BandFamily* fs, const BandFamily* ft, int 
   op.n_it = n_it;
   op.n_out = n_out;
   op.out_scale = out_scale;
+  op.s_ident = 0;
   op.terms.clear();
   op.offs.assign(1, 0);
 }
@@ -420,21 +482,83 @@ static void sep_add(SepOp& op, long long off, int s_tab, int t_tab, float scale)
 }
 static void sep_close_output(SepOp& op) { op.offs.push_back((int32_t)op.terms.size()); }
 
-// Choose the largest output tile whose staged source footprint fits the shared-memory budget.
-static size_t sep_smem(const SepOp& op) {
+// Shared memory of one stage of `nb` terms (must match kernels.cu).
+size_t sep_smem(const SepOp& op, int nb) {
+  // double-buffered slots (source footprint, pass-1 ELL rows, counts, pass-2 weights, group
+  // descriptors) + double-buffered U tiles; must match slot_layout() in kernels.cu
   size_t fsp = (size_t)op.fs_max + 1;
-  return ((size_t)op.ft_max * fsp + (size_t)op.tt * fsp) * 4 + (size_t)op.tt * op.ft->ell * 8 + (size_t)op.tt * 4;
+  size_t x = (op.stage && !op.s_ident) ? ((size_t)op.ft_max * fsp + 3) / 4 * 4 : 0;
+  size_t per = x + 2 * (size_t)op.fs->ell * op.ts + op.ts + ((size_t)op.wt_max + 3) / 4 * 4 + 4 * (op.tt / 4);
+  size_t maxt = 0;
+  for (size_t b = 0; b + 1 < op.offs.size(); ++b) maxt = std::max(maxt, (size_t)(op.offs[b + 1] - op.offs[b]));
+  size_t nbuf = maxt > (size_t)nb ? 2 : 1;  // one chunk per output: no double buffer needed
+  return (nbuf * per * nb + nbuf * (size_t)nb * op.ft_max * op.ts) * 4;
 }
-static bool sep_choose_tile(SepOp& op) {
-  const int cand[][2] = {{64, 32}, {64, 16}, {32, 32}, {32, 16}, {16, 16}};
-  const size_t budget = 200 * 1024;
-  for (auto& c : cand) {
-    op.ts = c[0];
-    op.tt = c[1];
-    fill_sep_geometry(op);
-    if (sep_smem(op) <= budget) return true;
+// Estimated time of an op for a tile choice: L2->SM traffic of the staged footprints and the FMA issue
+// slots of both passes, with a crude occupancy factor (a sampled cost model).
+static double sep_cost(const SepOp& op, int nt, size_t smem) {
+  const BandFamily& fs = *op.fs;
+  const BandFamily& ft = *op.ft;
+  size_t nterms = op.terms.size();
+  size_t step = std::max<size_t>(1, nterms / 64);
+  double bytes = 0, slots = 0;
+  int ntx = (fs.n_rows + op.ts - 1) / op.ts, nty = (ft.n_rows + op.tt - 1) / op.tt;
+  for (size_t e = 0; e < nterms; e += step) {
+    const Term& t = op.terms[e];
+    std::vector<int> flo(ntx), fw(ntx);
+    for (int x = 0; x < ntx; ++x) ell_footprint(fs, t.s_tab, op.ts, x, flo[x], fw[x]);
+    for (int y = 0; y < nty; ++y) {
+      int lo, w, wo, wl;
+      g4_tile(ft, t.t_tab, op.tt, y, lo, w, wo, wl);
+      if (!w) continue;
+      for (int x = 0; x < ntx; ++x) {
+        if (!fw[x]) continue;
+        if (op.s_ident) {
+          bytes += 4.0 * (double)w * op.ts + 4.0 * wl;
+          slots += (double)wl * op.ts;
+        } else {
+          bytes += 4.0 * (op.stage ? (double)w * fw[x] : (double)w * op.ts * fs.ell) + 4.0 * wl;
+          slots += 5.0 * (double)w * op.ts * fs.ell + (double)wl * op.ts;  // pass 1 (~5 instr/FMA) + pass 2
+        }
+      }
+    }
   }
-  return false;
+  double scale = (double)nterms / ((nterms + step - 1) / step);
+  int ctas = std::max<size_t>(1, (228 * 1024) / std::max<size_t>(smem + 1024, 1));
+  ctas = std::min(ctas, 2048 / nt);
+  double occ = std::min(1.0, ctas * nt / 512.0) * (ctas < 2 ? 0.7 : 1.0);
+  return scale * (bytes / 6e12 + slots / (30e12 * occ));
+}
+
+static bool sep_choose_tile(SepOp& op) {
+  const int cand[][3] = {{128, 64, 256}, {128, 32, 128}, {64, 64, 128}, {64, 32, 64}, {32, 32, 64}};
+  double best = 1e300;
+  int bts = 0, btt = 0, bst = 0, bnb = 0, bnt = 0;
+  for (auto& c : cand) {
+    for (int stage : {1, 0}) {
+      if (op.s_ident && stage == 0) continue;
+      op.ts = c[0];
+      op.tt = c[1];
+      op.stage = stage;
+      fill_sep_geometry(op);
+      for (int nb : {4, 2, 1}) {
+        if (nb > 1 && op.terms.size() < (size_t)op.n_out * 2) continue;  // single-term outputs: nb = 1
+        size_t smem = sep_smem(op, nb);
+        if (smem > (size_t)210 * 1024) continue;
+        double cost = sep_cost(op, c[2], smem) * (nb == 1 && op.terms.size() >= (size_t)op.n_out * 2 ? 1.15 : 1.0);
+        if (cost < best) { best = cost; bts = c[0]; btt = c[1]; bst = stage; bnb = nb; bnt = c[2]; }
+        break;  // largest nb that fits
+      }
+    }
+  }
+  if (!bts) return false;
+  op.ts = bts;
+  op.tt = btt;
+  op.stage = bst;
+  op.nb = bnb;
+  op.nt = bnt;
+  fill_sep_geometry(op);
+  return true;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -698,9 +822,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     bf.finish();
     ba.finish();
   }
-  info.taps_s1 = std::max(cp.s1f[0].ell, cp.s1f[1].ell);
-  info.taps_s3 = plen ? std::max(cp.s3f[0].ell, cp.s3f[1].ell) : 0;
-  info.taps_c = std::max(cp.cf[0].ell, cp.cf[1].ell);
+  info.taps_s1 = std::max(cp.s1f[0].ell, cp.s1f[1].gmax);
+  info.taps_s3 = plen ? std::max(cp.s3f[0].ell, cp.s3f[1].gmax) : 0;
+  info.taps_c = std::max(cp.cf[0].ell, cp.cf[1].gmax);
 
   // ---- term lists ----
   const int Kv = K[0] * K[1];
@@ -758,6 +882,7 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   make_identity(cp.id_s, ndet[0]);
   make_identity(cp.id_vt, ny);
   sep_init(cp.adj_c1, &cp.id_s, &cp.ca[1], ndet[0], ndet[1], nz, 1.f);
+  cp.adj_c1.s_ident = 1;
   for (int n = 0; n < nz; ++n) {
     sep_add(cp.adj_c1, 0, 0, n, 1.f);
     sep_close_output(cp.adj_c1);
@@ -803,11 +928,18 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
   const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2",
                          "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a"};
-  for (int q = 0; q < 11; ++q)
-    if (ops[q]->fs && !sep_choose_tile(*ops[q])) {
+  const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
+  for (int q = 0; q < 11; ++q) {
+    if (!ops[q]->fs) continue;
+    if (!sep_choose_tile(*ops[q])) {
       err = std::string("source footprint of op ") + names[q] + " exceeds shared memory";
       return LFM_E_NOMEM;
     }
+    if (dbg)
+      std::fprintf(stderr, "[lfm] %-7s nt %3d tile %3dx%-3d nb %d stage %d fs %4d ft %4d wt %5d ell_s %3d gmax_t %3d smem %6zu fma %.3g\n",
+                   names[q], ops[q]->nt, ops[q]->ts, ops[q]->tt, ops[q]->nb, ops[q]->stage, ops[q]->fs_max, ops[q]->ft_max,
+                   ops[q]->wt_max, ops[q]->fs->ell, ops[q]->ft->gmax, sep_smem(*ops[q], ops[q]->nb), ops[q]->fma_alg);
+  }
 
   // algorithmic work and bytes per A_forward
   double rot_bytes = 0;
