@@ -87,13 +87,12 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
   const BandFamily& ft = *op.ft;
   op.ntx = (fs.n_rows + op.ts - 1) / op.ts;
   op.nty = (ft.n_rows + op.tt - 1) / op.tt;
-  std::vector<Footprint> vs((size_t)fs.n_tables * op.ntx);
-  std::vector<TileT> vt((size_t)ft.n_tables * op.nty);
+  std::vector<TileT> vs((size_t)fs.n_tables * op.ntx), vt((size_t)ft.n_tables * op.nty);
   for (int m = 0; m < fs.n_tables; ++m)
     for (int x = 0; x < op.ntx; ++x) {
-      int lo, w;
-      ell_footprint(fs, m, op.ts, x, lo, w);
-      vs[(size_t)m * op.ntx + x] = Footprint{lo, w};
+      int lo, w, wo, wl;
+      g4_tile(fs, m, op.ts, x, lo, w, wo, wl);
+      vs[(size_t)m * op.ntx + x] = TileT{lo, w, wo, wl};
     }
   for (int m = 0; m < ft.n_tables; ++m)
     for (int y = 0; y < op.nty; ++y) {
@@ -101,9 +100,9 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
       g4_tile(ft, m, op.tt, y, lo, w, wo, wl);
       vt[(size_t)m * op.nty + y] = TileT{lo, w, wo, wl};
     }
-  st = dev_upload(&op.d_fp_s, vs.data(), vs.size() * sizeof(Footprint), err);
+  st = dev_upload(&op.d_fp_s, vs.data(), vs.size() * sizeof(TileT), err);
   if (st != LFM_OK) return st;
-  bytes += op.terms.size() * sizeof(Term) + vs.size() * sizeof(Footprint) + vt.size() * sizeof(TileT);
+  bytes += op.terms.size() * sizeof(Term) + (vs.size() + vt.size()) * sizeof(TileT);
   return dev_upload(&op.d_fp_t, vt.data(), vt.size() * sizeof(TileT), err);
 }
 
@@ -165,130 +164,121 @@ void free_camera(CameraPlan& cp) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Separable banded sum, v2.
-//   pass 1 (s direction, gather): U[r][c] = sum_k ws[c][k] * X[r][idx_s[c][k]] for the staged source
-//          rows r of the tile's t footprint and the tile's output columns c (ELL s table);
-//   pass 2 (t direction, the large pass): out[4g+q][c] += sum_p wt[g][p][q] * U[j0_g + p][c] with the
-//          weights of a group of 4 output rows shared by a whole warp (G4 t table) and 4 columns per
-//          thread: one broadcast LDS.128 of weights + one LDS.128 of U feed 16 FFMAs.
-//   `nb` terms (slices / views) are staged per barrier.
+// Separable banded sum.  For every term (one slice / view / transport) of an output tile:
+//   pass 1 (s direction): U[r][4g+q] = sum_p Ws_g[p][q] * X[r][j0_g + p]   (G4 s table: groups of 4
+//          output columns share a window of source columns; one LDS.128 of weights feeds 4 FFMAs
+//          per staged source row handled by the thread);
+//   pass 2 (t direction, the large pass): out[4g+q][c] += sum_p Wt_g[p][q] * U[j0_g + p][c] with the
+//          weights of a group of 4 output rows shared by the whole warp (broadcast) and 4 columns
+//          per thread: one LDS.128 of weights + one LDS.128 of U feed 16 FFMAs.
+// Chunks of nb terms (headers, source footprint, weights, group descriptors) are staged with cp.async
+// into a double buffer, so the loads of chunk i+1 overlap the two passes of chunk i.  One thread owns
+// each output element: no atomics; results are bitwise reproducible.
 struct SepArgs {
   const float* src;
   float* out;
   long long out_stride;
   const Term* terms;
   const int32_t* offs;  // already offset by b0
-  const int32_t* s_cnt;
-  const int32_t* s_idx;
-  const float* s_w;
+  const int4* s_g;
+  const float* s_gw;
   const int4* t_g;
   const float* t_gw;
-  const Footprint* fp_s;
+  const TileT* fp_s;
   const TileT* fp_t;
-  int s_ell, t_ngroups;
+  int s_ngroups, t_ngroups;
   int ntx, nty;
   int n_os, n_ot, n_is, n_it;
-  int fsp, ftm, wtm, nb;
-  int nbuf;     // 2: double-buffered chunks, 1: a single chunk per output
+  int fsp, ftm, wsm, wtm, nb, nbuf;
   int s_ident;  // s table is the identity: pass 1 is a copy (source rows staged straight into U)
   float out_scale;
   int accumulate;
 };
 
-// Shared-memory layout of one staged term (floats); must match sep_smem() in plan.cpp.
 struct SlotLayout {
-  int xs, sw, si, sc, wt, gd, per;
+  int xs, ws, gs, wt, gt, per;
 };
-__host__ __device__ inline SlotLayout slot_layout(int ftm, int fsp, int stage, int s_ell, int ts, int wtm, int ng) {
+__host__ __device__ inline SlotLayout slot_layout(int ftm, int fsp, bool xs, int wsm, int ts, int wtm, int tt,
+                                                  int gstep) {
   SlotLayout L;
   L.xs = 0;
-  int x = stage ? (ftm * fsp + 3) / 4 * 4 : 0;
-  L.sw = x;
-  L.si = L.sw + s_ell * ts;
-  L.sc = L.si + s_ell * ts;
-  L.wt = L.sc + ts;
-  L.gd = L.wt + (wtm + 3) / 4 * 4;
-  L.per = L.gd + 4 * ng;
+  L.ws = xs ? ((ftm + gstep) * fsp + 3) / 4 * 4 : 0;
+  L.gs = L.ws + (wsm + 3) / 4 * 4;
+  L.wt = L.gs + ts;            // ts/4 int4
+  L.gt = L.wt + (wtm + 3) / 4 * 4;
+  L.per = L.gt + tt;           // tt/4 int4
   return L;
 }
 
-// Per-term header cached in shared memory for the chunk.
 struct TermHdr {
   long long src_off;
   float scale;
-  int fs_lo, fs_w, ft_lo, ft_w, woff, s_tab, t_tab;
+  int fs_lo, fs_w, ws_off, ft_lo, ft_w, wt_off, s_tab, t_tab;
 };
 
-// TS x TT output tile, NT threads, CW columns per thread in pass 2 (4 or 8); STAGE = stage the source
-// footprint in smem (else pass 1 reads L1/L2); TAPS > 0: a column's s entries (<= TAPS) live in
-// registers, TAPS == 0: runtime count.  Chunks of nb terms are staged with cp.async into a double
-// buffer (headers, tables, weights, source footprint) so the loads of chunk i+1 overlap chunk i.
-template <int TS, int TT, int NT, int CW, bool STAGE, int TAPS>
+template <int TS, int TT, int NT, bool STAGE>
 __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
-  constexpr int NQ = TS / CW;          // column blocks per tile
-  constexpr int GSTEP = NT / NQ;
+  constexpr int NQ = TS / 4;           // 4-column groups per tile (pass 1 groups, pass 2 quads)
+  constexpr int GSTEP = NT / NQ;       // pass 2: row groups in flight; pass 1: row stride
   constexpr int NG = TT / 4;           // row groups per tile
-  constexpr int GP = NG / GSTEP;       // groups per thread
-  constexpr int CPT = NT / TS;         // threads per column in pass 1
-  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % TS == 0 && (CW == 4 || CW == 8), "tile/thread mismatch");
+  constexpr int GP = NG / GSTEP;       // row groups per thread in pass 2
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
   extern __shared__ __align__(16) float smem[];
   __shared__ TermHdr hdr[2][8];
   const int tid = threadIdx.x;
   const int tx = blockIdx.x, ty = blockIdx.y, b = blockIdx.z;
   const int os0 = tx * TS, ot0 = ty * TT;
-  const SlotLayout L = slot_layout(a.ftm, a.fsp, STAGE && !a.s_ident, a.s_ell, TS, a.wtm, NG);
+  const SlotLayout L = slot_layout(a.ftm, a.fsp, STAGE && !a.s_ident, a.wsm, TS, a.wtm, TT, GSTEP);
+  const int urows = a.ftm + GSTEP;  // U tile rows (padded)
   const int nbuf = a.nbuf;
   float* bufs[2] = {smem, smem + (nbuf - 1) * a.nb * L.per};
   float* Ubase = smem + nbuf * a.nb * L.per;   // [nbuf][nb][ftm][TS]
   const int quad = tid % NQ, gsub = tid / NQ;
-  const int pc = tid % TS, pr0 = tid / TS;
-  const int pitch = (a.n_os + 3) / 4 * 4;      // ELL row pitch on the device
-  const bool col_ok = os0 + pc < a.n_os;
 
-  float acc[GP][4][CW], hi[GP][4][CW];
+  float acc[GP][4][4], hi[GP][4][4];
 #pragma unroll
   for (int j = 0; j < GP; ++j)
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int c = 0; c < CW; ++c) { acc[j][r][c] = 0.f; hi[j][r][c] = 0.f; }
+      for (int c = 0; c < 4; ++c) { acc[j][r][c] = 0.f; hi[j][r][c] = 0.f; }
 
   const int e0 = a.offs[b], e1 = a.offs[b + 1];
   const int nchunks = (e1 - e0 + a.nb - 1) / a.nb;
 
-  // Stage chunk ci into buffer side `sd`: headers (synchronously, tiny) + async copies.
   auto stage_chunk = [&](int ci, int sd) {
     const int e = e0 + ci * a.nb;
     const int nterm = min(a.nb, e1 - e);
     float* buf = bufs[sd];
     for (int sl = 0; sl < nterm; ++sl) {
       const Term term = a.terms[e + sl];
-      const Footprint fs = a.fp_s[(size_t)term.s_tab * a.ntx + tx];
+      const TileT fs = a.fp_s[(size_t)term.s_tab * a.ntx + tx];
       const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
+      const bool live = fs.width != 0 && ft.width != 0;
       if (tid == 0) {
         TermHdr h;
         h.src_off = term.src_off;
         h.scale = term.scale;
         h.fs_lo = fs.lo;
-        h.fs_w = (fs.width == 0 || ft.width == 0) ? 0 : fs.width;
+        h.fs_w = live ? fs.width : 0;
+        h.ws_off = fs.woff;
         h.ft_lo = ft.lo;
         h.ft_w = ft.width;
-        h.woff = ft.woff;
+        h.wt_off = ft.woff;
         h.s_tab = term.s_tab;
         h.t_tab = term.t_tab;
         hdr[sd][sl] = h;
       }
-      if (fs.width == 0 || ft.width == 0) continue;
+      if (!live) continue;
       float* slot = buf + sl * L.per;
       if (a.s_ident) {
-        // U[r][c] = src[ft.lo + r][os0 + c]: 16-byte pieces where aligned, else 4-byte
-        float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
+        // U[r][c] = src[ft.lo + r][os0 + c]
+        float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const float* src = a.src + term.src_off + os0;
-        const bool al16 = ((a.n_is & 3) == 0) && ((term.src_off & 3) == 0);
         const int ncol = min(TS, a.n_is - os0);
-        if (al16 && ncol == TS) {
-          for (int q = tid; q < ft.width * (TS / 4); q += NT) {
-            const int r = q / (TS / 4), c4 = q - r * (TS / 4);
+        if (((a.n_is & 3) == 0) && ((term.src_off & 3) == 0) && ncol == TS) {
+          for (int q = tid; q < ft.width * NQ; q += NT) {
+            const int r = q / NQ, c4 = q - r * NQ;
             __pipeline_memcpy_async(U + r * TS + 4 * c4, src + (size_t)(ft.lo + r) * a.n_is + 4 * c4, 16);
           }
         } else {
@@ -298,31 +288,34 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
             else U[r * TS + c] = 0.f;
           }
         }
-      } else if (STAGE) {
-        const float* src = a.src + term.src_off + fs.lo;
-        const int n = ft.width * fs.width;
-        for (int q = tid; q < n; q += NT) {
-          const int r = q / fs.width, c = q - r * fs.width;
-          const int row = min(ft.lo + r, a.n_it - 1);
-          __pipeline_memcpy_async(slot + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
+      } else {
+        if (STAGE) {
+          const float* src = a.src + term.src_off + fs.lo;
+          const int n = ft.width * fs.width;
+          for (int q = tid; q < n; q += NT) {
+            const int r = q / fs.width, c = q - r * fs.width;
+            __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)(ft.lo + r) * a.n_is + c, 4);
+          }
+        }
+        for (int q = tid; q < fs.wlen / 4; q += NT)
+          __pipeline_memcpy_async(slot + L.ws + 4 * q, a.s_gw + fs.woff + 4 * q, 16);
+        const int g0 = tx * NQ;
+        for (int q = tid; q < NQ; q += NT) {
+          if (g0 + q < a.s_ngroups)
+            __pipeline_memcpy_async(slot + L.gs + 4 * q, a.s_g + (size_t)term.s_tab * a.s_ngroups + g0 + q, 16);
+          else
+            reinterpret_cast<int4*>(slot + L.gs)[q] = make_int4(0, 0, 0, 0);
         }
       }
-      const size_t sb = (size_t)term.s_tab * a.s_ell * pitch + os0;
-      for (int q = tid; q < a.s_ell * (TS / 4); q += NT) {
-        const int k = q / (TS / 4), c4 = q - k * (TS / 4);
-        if (os0 + 4 * c4 >= pitch) continue;
-        __pipeline_memcpy_async(slot + L.sw + k * TS + 4 * c4, a.s_w + sb + (size_t)k * pitch + 4 * c4, 16);
-        __pipeline_memcpy_async(slot + L.si + k * TS + 4 * c4, a.s_idx + sb + (size_t)k * pitch + 4 * c4, 16);
-      }
-      for (int c4 = tid; c4 < TS / 4; c4 += NT)
-        if (os0 + 4 * c4 < pitch)
-          __pipeline_memcpy_async(slot + L.sc + 4 * c4, a.s_cnt + (size_t)term.s_tab * pitch + os0 + 4 * c4, 16);
       for (int q = tid; q < ft.wlen / 4; q += NT)
         __pipeline_memcpy_async(slot + L.wt + 4 * q, a.t_gw + ft.woff + 4 * q, 16);
       const int g0 = ty * NG;
-      for (int q = tid; q < NG; q += NT)
+      for (int q = tid; q < NG; q += NT) {
         if (g0 + q < a.t_ngroups)
-          __pipeline_memcpy_async(slot + L.gd + 4 * q, a.t_g + (size_t)term.t_tab * a.t_ngroups + g0 + q, 16);
+          __pipeline_memcpy_async(slot + L.gt + 4 * q, a.t_g + (size_t)term.t_tab * a.t_ngroups + g0 + q, 16);
+        else
+          reinterpret_cast<int4*>(slot + L.gt)[q] = make_int4(0, 0, 0, 0);
+      }
     }
     __pipeline_commit();
   };
@@ -340,94 +333,71 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       __pipeline_wait_prior(0);
     }
     __syncthreads();
-    // ---- pass 1 (s gather): U[r][c] = sum_k w_c[k] * X[r][idx_c[k]], two independent rows per step
-    for (int sl = 0; sl < nterm && !a.s_ident; ++sl) {
-      const TermHdr h = hdr[sd][sl];
-      if (h.fs_w == 0) continue;
-      const float* slot = buf + sl * L.per;
-      float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
-      const int cnt = col_ok ? reinterpret_cast<const int*>(slot + L.sc)[pc] : 0;
-      const float* SW = slot + L.sw;
-      const int* SI = reinterpret_cast<const int*>(slot + L.si);
-      const float* gsrc = a.src + h.src_off + h.fs_lo;
-      if constexpr (TAPS > 0) {
-        float w[TAPS];
-        int ix[TAPS];
-#pragma unroll
-        for (int k = 0; k < TAPS; ++k) {
-          w[k] = k < cnt ? SW[k * TS + pc] * h.scale : 0.f;
-          ix[k] = k < cnt ? min(max(SI[k * TS + pc] - h.fs_lo, 0), h.fs_w - 1) : 0;
-        }
-        for (int r = pr0; r < h.ft_w; r += 2 * CPT) {
-          const int r2 = r + CPT;
-          const bool two = r2 < h.ft_w;
-          float v = 0.f, v2 = 0.f;
-          if (STAGE) {
-            const float* xr = slot + L.xs + r * a.fsp;
-            const float* xr2 = slot + L.xs + (two ? r2 : r) * a.fsp;
-#pragma unroll
-            for (int k = 0; k < TAPS; ++k) {
-              if (k >= cnt) break;
-              v = fmaf(w[k], xr[ix[k]], v);
-              v2 = fmaf(w[k], xr2[ix[k]], v2);
-            }
-          } else {
-            const int row = min(h.ft_lo + r, a.n_it - 1), row2 = min(h.ft_lo + (two ? r2 : r), a.n_it - 1);
-            const float* xr = gsrc + (size_t)row * a.n_is;
-            const float* xr2 = gsrc + (size_t)row2 * a.n_is;
-#pragma unroll
-            for (int k = 0; k < TAPS; ++k) {
-              if (k >= cnt) break;
-              v = fmaf(w[k], __ldg(xr + ix[k]), v);
-              v2 = fmaf(w[k], __ldg(xr2 + ix[k]), v2);
-            }
+    // ---- pass 1 (s direction, G4): thread = (column group `quad`, rows gsub, gsub+GSTEP, ...)
+    if (!a.s_ident) {
+      for (int sl = 0; sl < nterm; ++sl) {
+        const TermHdr h = hdr[sd][sl];
+        if (h.fs_w == 0) continue;
+        const float* slot = buf + sl * L.per;
+        float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
+        const int4 gd = reinterpret_cast<const int4*>(slot + L.gs)[quad];
+        const float4* wp0 = reinterpret_cast<const float4*>(slot + L.ws + (gd.z - h.ws_off));
+        const float* xs = STAGE ? slot + L.xs + (gd.x - h.fs_lo)
+                                : a.src + h.src_off + (size_t)h.ft_lo * a.n_is + gd.x;
+        const int pitch = STAGE ? a.fsp : a.n_is;
+        // two rows per step (r0, r0 + GSTEP); staged rows are padded so the second row is always
+        // addressable (its U row, beyond the footprint, is never read by pass 2)
+        for (int r0 = gsub; r0 < h.ft_w; r0 += 2 * GSTEP) {
+          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+          const float* x0 = xs + (size_t)r0 * pitch;
+          const float* x1 = x0 + (size_t)GSTEP * pitch;
+          const bool second = STAGE || r0 + GSTEP < h.ft_w;
+          const float4* wp = wp0;
+#pragma unroll 4
+          for (int p = 0; p < gd.y; ++p) {
+            const float4 w4 = *wp++;
+            const float a0 = STAGE ? *x0 : __ldg(x0);
+            const float a1 = STAGE ? *x1 : (second ? __ldg(x1) : 0.f);
+            ++x0;
+            ++x1;
+            v0.x = fmaf(w4.x, a0, v0.x); v0.y = fmaf(w4.y, a0, v0.y);
+            v0.z = fmaf(w4.z, a0, v0.z); v0.w = fmaf(w4.w, a0, v0.w);
+            v1.x = fmaf(w4.x, a1, v1.x); v1.y = fmaf(w4.y, a1, v1.y);
+            v1.z = fmaf(w4.z, a1, v1.z); v1.w = fmaf(w4.w, a1, v1.w);
           }
-          U[r * TS + pc] = v;
-          if (two) U[r2 * TS + pc] = v2;
-        }
-      } else {
-        for (int r = pr0; r < h.ft_w; r += CPT) {
-          float v = 0.f;
-          const float* xr = STAGE ? slot + L.xs + r * a.fsp
-                                  : gsrc + (size_t)min(h.ft_lo + r, a.n_it - 1) * a.n_is;
-          for (int k = 0; k < cnt; ++k) {
-            const int ik = min(max(SI[k * TS + pc] - h.fs_lo, 0), h.fs_w - 1);
-            v = fmaf(SW[k * TS + pc], STAGE ? xr[ik] : __ldg(xr + ik), v);
-          }
-          U[r * TS + pc] = v * h.scale;
+          v0.x *= h.scale; v0.y *= h.scale; v0.z *= h.scale; v0.w *= h.scale;
+          v1.x *= h.scale; v1.y *= h.scale; v1.z *= h.scale; v1.w *= h.scale;
+          *reinterpret_cast<float4*>(U + r0 * TS + 4 * quad) = v0;
+          if (STAGE || second) *reinterpret_cast<float4*>(U + (r0 + GSTEP) * TS + 4 * quad) = v1;
         }
       }
     }
     __syncthreads();
-    // ---- pass 2 (t direction): groups of 4 output rows x CW columns per thread, warp-uniform weights
+    // ---- pass 2 (t direction, G4): groups of 4 output rows x 4 columns per thread
     for (int sl = 0; sl < nterm; ++sl) {
       const TermHdr h = hdr[sd][sl];
       if (h.fs_w == 0) continue;
       const float* slot = buf + sl * L.per;
-      const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * a.ftm * TS;
-      const int4* GD = reinterpret_cast<const int4*>(slot + L.gd);
+      const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
+      const int4* GD = reinterpret_cast<const int4*>(slot + L.gt);
 #pragma unroll
       for (int j = 0; j < GP; ++j) {
-        const int gl = gsub + j * GSTEP;
-        if (ty * NG + gl >= a.t_ngroups) continue;
-        const int4 gd = GD[gl];
-        const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.woff));
-        const float* up = U + (gd.x - h.ft_lo) * TS + quad * CW;
-#pragma unroll 2
+        const int4 gd = GD[gsub + j * GSTEP];
+        const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.wt_off));
+        const float4* up = reinterpret_cast<const float4*>(U + (gd.x - h.ft_lo) * TS + quad * 4);
+#pragma unroll 4
         for (int p = 0; p < gd.y; ++p) {
-          const float4 w4 = wp[p];
-          const float wr[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-          for (int cb = 0; cb < CW; cb += 4) {
-            const float4 u4 = *reinterpret_cast<const float4*>(up + p * TS + cb);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              acc[j][r][cb + 0] = fmaf(wr[r], u4.x, acc[j][r][cb + 0]);
-              acc[j][r][cb + 1] = fmaf(wr[r], u4.y, acc[j][r][cb + 1]);
-              acc[j][r][cb + 2] = fmaf(wr[r], u4.z, acc[j][r][cb + 2]);
-              acc[j][r][cb + 3] = fmaf(wr[r], u4.w, acc[j][r][cb + 3]);
-            }
-          }
+          const float4 w4 = *wp++;
+          const float4 u4 = *up;
+          up += TS / 4;
+          acc[j][0][0] = fmaf(w4.x, u4.x, acc[j][0][0]); acc[j][0][1] = fmaf(w4.x, u4.y, acc[j][0][1]);
+          acc[j][0][2] = fmaf(w4.x, u4.z, acc[j][0][2]); acc[j][0][3] = fmaf(w4.x, u4.w, acc[j][0][3]);
+          acc[j][1][0] = fmaf(w4.y, u4.x, acc[j][1][0]); acc[j][1][1] = fmaf(w4.y, u4.y, acc[j][1][1]);
+          acc[j][1][2] = fmaf(w4.y, u4.z, acc[j][1][2]); acc[j][1][3] = fmaf(w4.y, u4.w, acc[j][1][3]);
+          acc[j][2][0] = fmaf(w4.z, u4.x, acc[j][2][0]); acc[j][2][1] = fmaf(w4.z, u4.y, acc[j][2][1]);
+          acc[j][2][2] = fmaf(w4.z, u4.z, acc[j][2][2]); acc[j][2][3] = fmaf(w4.z, u4.w, acc[j][2][3]);
+          acc[j][3][0] = fmaf(w4.w, u4.x, acc[j][3][0]); acc[j][3][1] = fmaf(w4.w, u4.y, acc[j][3][1]);
+          acc[j][3][2] = fmaf(w4.w, u4.z, acc[j][3][2]); acc[j][3][3] = fmaf(w4.w, u4.w, acc[j][3][3]);
         }
       }
     }
@@ -439,11 +409,12 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < CW; ++c) { hi[j][r][c] += acc[j][r][c]; acc[j][r][c] = 0.f; }
+          for (int c = 0; c < 4; ++c) { hi[j][r][c] += acc[j][r][c]; acc[j][r][c] = 0.f; }
     }
   }
   float* outb = a.out + (size_t)b * a.out_stride;
-  const int col = os0 + quad * CW;
+  const int col = os0 + quad * 4;
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
 #pragma unroll
@@ -451,19 +422,30 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
       if (row >= a.n_ot) continue;
       float* p = outb + (size_t)row * a.n_os + col;
+      float v[4];
 #pragma unroll
-      for (int c = 0; c < CW; ++c) {
-        if (col + c >= a.n_os) continue;
-        const float v = a.out_scale * (hi[j][r][c] + acc[j][r][c]);
-        p[c] = a.accumulate ? p[c] + v : v;
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * (hi[j][r][c] + acc[j][r][c]);
+      if (vec) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (a.accumulate) {
+          const float4 q = *reinterpret_cast<float4*>(p);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(p) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          p[c] = a.accumulate ? p[c] + v[c] : v[c];
+        }
       }
     }
   }
 }
 
-template <int TS, int TT, int NT, int CW, bool STAGE, int TAPS>
+template <int TS, int TT, int NT, bool STAGE>
 static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
-  auto kern = sep_kernel<TS, TT, NT, CW, STAGE, TAPS>;
+  auto kern = sep_kernel<TS, TT, NT, STAGE>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -484,14 +466,13 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.out_stride = (long long)op.n_os * op.n_ot;
   a.terms = op.d_terms;
   a.offs = op.d_offs + b0;
-  a.s_cnt = op.fs->d_cnt;
-  a.s_idx = op.fs->d_idx;
-  a.s_w = op.fs->d_w;
+  a.s_g = reinterpret_cast<const int4*>(op.fs->d_g);
+  a.s_gw = op.fs->d_gw;
   a.t_g = reinterpret_cast<const int4*>(op.ft->d_g);
   a.t_gw = op.ft->d_gw;
   a.fp_s = op.d_fp_s;
   a.fp_t = op.d_fp_t;
-  a.s_ell = op.fs->ell;
+  a.s_ngroups = op.fs->n_groups;
   a.t_ngroups = op.ft->n_groups;
   a.ntx = op.ntx;
   a.nty = op.nty;
@@ -501,32 +482,25 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.n_it = op.n_it;
   a.fsp = op.fs_max + 1;
   a.ftm = op.ft_max;
+  a.wsm = op.ws_max;
   a.wtm = op.wt_max;
-  a.s_ident = op.s_ident;
-  {
-    int maxt = 0;
-    for (size_t q = 0; q + 1 < op.offs.size(); ++q) maxt = std::max(maxt, op.offs[q + 1] - op.offs[q]);
-    a.nbuf = maxt > op.nb ? 2 : 1;
-  }
   a.nb = op.nb;
+  a.nbuf = op.nbuf;
+  a.s_ident = op.s_ident;
   a.out_scale = op.out_scale;
   a.accumulate = accumulate;
   const size_t smem = sep_smem(op, op.nb);
   dim3 grid(op.ntx, op.nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
-#define LFM_SEP_CASE(TS_, TT_, NT_, CW_)                                                              \
-  if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) {                                                \
-    if (a.s_ell <= 8)                                                                                \
-      return op.stage ? launch_sep_t<TS_, TT_, NT_, CW_, true, 8>(a, grid, smem, s, err)             \
-                      : launch_sep_t<TS_, TT_, NT_, CW_, false, 8>(a, grid, smem, s, err);           \
-    return op.stage ? launch_sep_t<TS_, TT_, NT_, CW_, true, 0>(a, grid, smem, s, err)               \
-                    : launch_sep_t<TS_, TT_, NT_, CW_, false, 0>(a, grid, smem, s, err);             \
-  }
-  LFM_SEP_CASE(128, 64, 256, 8)
-  LFM_SEP_CASE(128, 32, 128, 8)
-  LFM_SEP_CASE(64, 64, 128, 8)
-  LFM_SEP_CASE(64, 32, 64, 8)
-  LFM_SEP_CASE(32, 32, 64, 4)
+#define LFM_SEP_CASE(TS_, TT_, NT_)                                                              \
+  if (op.ts == TS_ && op.tt == TT_)                                                             \
+    return op.stage ? launch_sep_t<TS_, TT_, NT_, true>(a, grid, smem, s, err)                  \
+                    : launch_sep_t<TS_, TT_, NT_, false>(a, grid, smem, s, err);
+  LFM_SEP_CASE(128, 64, 256)
+  LFM_SEP_CASE(128, 32, 256)
+  LFM_SEP_CASE(64, 64, 128)
+  LFM_SEP_CASE(64, 32, 128)
+  LFM_SEP_CASE(32, 32, 64)
 #undef LFM_SEP_CASE
   err = "unsupported sep tile";
   return LFM_E_INVALID;

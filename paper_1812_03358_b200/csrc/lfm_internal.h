@@ -82,7 +82,9 @@ struct SepOp {
   int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
   int wt_max = 0;                  // max G4 weight floats of one t tile
-  Footprint* d_fp_s = nullptr;     // [s-table][tile_x]
+  int ws_max = 0;                  // max G4 weight floats of one s tile
+  int nbuf = 2;                    // 2: double-buffered chunks, 1: one chunk per output
+  TileT* d_fp_s = nullptr;         // [s-table][tile_x]
   TileT* d_fp_t = nullptr;         // [t-table][tile_y]
   double fma_alg = 0;              // sum over terms of nnz work (algorithmic)
 };

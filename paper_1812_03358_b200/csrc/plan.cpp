@@ -430,6 +430,7 @@ static void fill_sep_geometry(SepOp& op) {
   op.fs_max = 1;
   op.ft_max = 1;
   op.wt_max = 4;
+  op.ws_max = 4;
   std::vector<char> seen_s(fs.n_tables, 0), seen_t(ft.n_tables, 0);
   double fma = 0;
   int ntx = (fs.n_rows + op.ts - 1) / op.ts, nty = (ft.n_rows + op.tt - 1) / op.tt;
@@ -438,9 +439,10 @@ static void fill_sep_geometry(SepOp& op) {
     if (!seen_s[t.s_tab]) {
       seen_s[t.s_tab] = 1;
       for (int x = 0; x < ntx; ++x) {
-        int lo, w;
-        ell_footprint(fs, t.s_tab, op.ts, x, lo, w);
+        int lo, w, wo, wl;
+        g4_tile(fs, t.s_tab, op.ts, x, lo, w, wo, wl);
         op.fs_max = std::max(op.fs_max, w);
+        op.ws_max = std::max(op.ws_max, wl);
       }
       for (int r = 0; r < fs.n_rows; ++r) sum_s[t.s_tab] += fs.cnt[(size_t)t.s_tab * fs.n_rows + r];
     }
@@ -461,6 +463,9 @@ static void fill_sep_geometry(SepOp& op) {
     fma += used_t[t.t_tab] * sum_s[t.s_tab] + sum_t[t.t_tab] * fs.n_rows;
   }
   op.fma_alg = fma;
+  size_t maxt = 0;
+  for (size_t b = 0; b + 1 < op.offs.size(); ++b) maxt = std::max(maxt, (size_t)(op.offs[b + 1] - op.offs[b]));
+  op.nbuf = maxt > (size_t)op.nb ? 2 : 1;
 }
 
 static void sep_init(SepOp& op, const BandFamily* fs, const BandFamily* ft, int n_is, int n_it, int n_out,
@@ -484,15 +489,19 @@ static void sep_close_output(SepOp& op) { op.offs.push_back((int32_t)op.terms.si
 
 // Shared memory of one stage of `nb` terms (must match kernels.cu).
 size_t sep_smem(const SepOp& op, int nb) {
-  // double-buffered slots (source footprint, pass-1 ELL rows, counts, pass-2 weights, group
-  // descriptors) + double-buffered U tiles; must match slot_layout() in kernels.cu
+  // per staged term: source footprint, s weights, s group descriptors, t weights, t group descriptors
+  // (must match slot_layout() in kernels.cu); double-buffered when an output has more than nb terms
+  auto r4 = [](size_t v) { return (v + 3) / 4 * 4; };
   size_t fsp = (size_t)op.fs_max + 1;
-  size_t x = (op.stage && !op.s_ident) ? ((size_t)op.ft_max * fsp + 3) / 4 * 4 : 0;
-  size_t per = x + 2 * (size_t)op.fs->ell * op.ts + op.ts + ((size_t)op.wt_max + 3) / 4 * 4 + 4 * (op.tt / 4);
+  // staged rows padded by one pass-1 row stride (the kernel reads two rows per step unconditionally)
+  size_t gstep = (size_t)op.nt / (op.ts / 4);
+  size_t x = (op.s_ident || !op.stage) ? 0 : r4(((size_t)op.ft_max + gstep) * fsp);
+  size_t per = x + r4(op.ws_max) + op.ts + r4(op.wt_max) + op.tt;
+  size_t urows = (size_t)op.ft_max + gstep;  // U rows padded likewise
   size_t maxt = 0;
   for (size_t b = 0; b + 1 < op.offs.size(); ++b) maxt = std::max(maxt, (size_t)(op.offs[b + 1] - op.offs[b]));
-  size_t nbuf = maxt > (size_t)nb ? 2 : 1;  // one chunk per output: no double buffer needed
-  return (nbuf * per * nb + nbuf * (size_t)nb * op.ft_max * op.ts) * 4;
+  size_t nbuf = maxt > (size_t)nb ? 2 : 1;
+  return (nbuf * per * nb + nbuf * (size_t)nb * urows * op.ts) * 4;
 }
 // Estimated time of an op for a tile choice: L2->SM traffic of the staged footprints and the FMA issue
 // slots of both passes, with a crude occupancy factor (a sampled cost model).
@@ -505,8 +514,11 @@ static double sep_cost(const SepOp& op, int nt, size_t smem) {
   int ntx = (fs.n_rows + op.ts - 1) / op.ts, nty = (ft.n_rows + op.tt - 1) / op.tt;
   for (size_t e = 0; e < nterms; e += step) {
     const Term& t = op.terms[e];
-    std::vector<int> flo(ntx), fw(ntx);
-    for (int x = 0; x < ntx; ++x) ell_footprint(fs, t.s_tab, op.ts, x, flo[x], fw[x]);
+    std::vector<int> flo(ntx), fw(ntx), fwl(ntx);
+    for (int x = 0; x < ntx; ++x) {
+      int wo;
+      g4_tile(fs, t.s_tab, op.ts, x, flo[x], fw[x], wo, fwl[x]);
+    }
     for (int y = 0; y < nty; ++y) {
       int lo, w, wo, wl;
       g4_tile(ft, t.t_tab, op.tt, y, lo, w, wo, wl);
@@ -517,21 +529,22 @@ static double sep_cost(const SepOp& op, int nt, size_t smem) {
           bytes += 4.0 * (double)w * op.ts + 4.0 * wl;
           slots += (double)wl * op.ts;
         } else {
-          bytes += 4.0 * (op.stage ? (double)w * fw[x] : (double)w * op.ts * fs.ell) + 4.0 * wl;
-          slots += 5.0 * (double)w * op.ts * fs.ell + (double)wl * op.ts;  // pass 1 (~5 instr/FMA) + pass 2
+          bytes += 4.0 * ((op.stage ? (double)w * fw[x] : 2.0 * w * fwl[x] / 4.0) + fwl[x] + wl);
+          slots += 1.3 * (double)w * fwl[x] * (op.stage ? 1.0 : 2.0) + (double)wl * op.ts;  // pass 1 + pass 2
         }
       }
     }
   }
   double scale = (double)nterms / ((nterms + step - 1) / step);
-  int ctas = std::max<size_t>(1, (228 * 1024) / std::max<size_t>(smem + 1024, 1));
+  int ctas = (int)std::max<size_t>(1, (228 * 1024) / (smem + 1024));
   ctas = std::min(ctas, 2048 / nt);
-  double occ = std::min(1.0, ctas * nt / 512.0) * (ctas < 2 ? 0.7 : 1.0);
+  ctas = std::min(ctas, 65536 / (nt * 96));          // ~96 registers per thread
+  double occ = std::min(1.0, ctas * nt / 1024.0);     // latency-bound below ~32 warps per SM (measured)
   return scale * (bytes / 6e12 + slots / (30e12 * occ));
 }
 
 static bool sep_choose_tile(SepOp& op) {
-  const int cand[][3] = {{128, 64, 256}, {128, 32, 128}, {64, 64, 128}, {64, 32, 64}, {32, 32, 64}};
+  const int cand[][3] = {{128, 64, 256}, {128, 32, 256}, {64, 64, 128}, {64, 32, 128}, {32, 32, 64}};
   double best = 1e300;
   int bts = 0, btt = 0, bst = 0, bnb = 0, bnt = 0;
   for (auto& c : cand) {
@@ -539,15 +552,15 @@ static bool sep_choose_tile(SepOp& op) {
       if (op.s_ident && stage == 0) continue;
       op.ts = c[0];
       op.tt = c[1];
+      op.nt = c[2];
       op.stage = stage;
       fill_sep_geometry(op);
       for (int nb : {4, 2, 1}) {
         if (nb > 1 && op.terms.size() < (size_t)op.n_out * 2) continue;  // single-term outputs: nb = 1
         size_t smem = sep_smem(op, nb);
         if (smem > (size_t)210 * 1024) continue;
-        double cost = sep_cost(op, c[2], smem) * (nb == 1 && op.terms.size() >= (size_t)op.n_out * 2 ? 1.15 : 1.0);
+        double cost = sep_cost(op, c[2], smem) * (nb == 1 && op.terms.size() >= (size_t)op.n_out * 2 ? 1.1 : 1.0);
         if (cost < best) { best = cost; bts = c[0]; btt = c[1]; bst = stage; bnb = nb; bnt = c[2]; }
-        break;  // largest nb that fits
       }
     }
   }
@@ -935,10 +948,21 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
       err = std::string("source footprint of op ") + names[q] + " exceeds shared memory";
       return LFM_E_NOMEM;
     }
+    // tuning hook: LFM_FORCE_<op>=ts,tt,nt,nb,stage overrides the cost model (sweeps, tools/)
+    std::string env = std::string("LFM_FORCE_") + names[q];
+    if (const char* f = std::getenv(env.c_str())) {
+      int ts, tt, nt, nb, stg;
+      if (std::sscanf(f, "%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg) == 5) {
+        SepOp& op = *ops[q];
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg;
+        fill_sep_geometry(op);
+        if (sep_smem(op, nb) > (size_t)220 * 1024) { err = env + ": shared memory too large"; return LFM_E_INVALID; }
+      }
+    }
     if (dbg)
-      std::fprintf(stderr, "[lfm] %-7s nt %3d tile %3dx%-3d nb %d stage %d fs %4d ft %4d wt %5d ell_s %3d gmax_t %3d smem %6zu fma %.3g\n",
+      std::fprintf(stderr, "[lfm] %-7s nt %3d tile %3dx%-3d nb %d stage %d fs %4d ft %4d wt %5d gmax_s %3d gmax_t %3d smem %6zu fma %.3g\n",
                    names[q], ops[q]->nt, ops[q]->ts, ops[q]->tt, ops[q]->nb, ops[q]->stage, ops[q]->fs_max, ops[q]->ft_max,
-                   ops[q]->wt_max, ops[q]->fs->ell, ops[q]->ft->gmax, sep_smem(*ops[q], ops[q]->nb), ops[q]->fma_alg);
+                   ops[q]->wt_max, ops[q]->fs->gmax, ops[q]->ft->gmax, sep_smem(*ops[q], ops[q]->nb), ops[q]->fma_alg);
   }
 
   // algorithmic work and bytes per A_forward
