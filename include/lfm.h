@@ -157,6 +157,15 @@ lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y
 lfm_status lfm_A_adjoint(lfm_plan p, int cam, int path, const float* y, float* x, int accumulate,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* Detector-row sharding: rows [row0, row1) of y = A_c x (other rows of y may also
+ * be written with their correct values where an output tile straddles the range), and
+ * x (+)= A_c^T P y where P keeps only rows [row0, row1) of y (treated as zero elsewhere).  Summing
+ * lfm_A_adjoint_rows over a partition of the rows gives lfm_A_adjoint.  0 <= row0 < row1 <= n_t. */
+lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* x, float* y,
+                              void* ws, size_t ws_bytes, void* stream);
+lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
+                              int accumulate, void* ws, size_t ws_bytes, void* stream);
+
 /* --- PWLS with the camera gains minimised out (eqn,pls P:299-317; App. A) --------
  * Weights are absorbed (A~ = W^1/2 A, y~ = W^1/2 y); w = diag(W_c) >= 0.
  * Phase 1, per camera: stats3_dev[0..2] = [y'W(Ax), y'Wy, (Ax)'W(Ax)] in fp64 (deterministic

@@ -134,38 +134,42 @@ lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int acc
   return LFM_OK;
 }
 
-lfm_status sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int acc, void* stream) {
+lfm_status sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int acc, void* stream,
+               int out_r0 = 0, int out_r1 = -1, int win_r0 = 0, int win_r1 = -1) {
   std::string err;
-  lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err);
+  lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err, out_r0, out_r1, win_r0, win_r1);
   return st == LFM_OK ? st : fail(st, err);
 }
 
-lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y, const Ws& w, void* stream) {
+// y rows [r0, r1) of A_c x (r1 < 0: all rows).  Rows of partially covered tiles are computed as well.
+lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y, const Ws& w, void* stream,
+                        int r0 = 0, int r1 = -1) {
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
   const bool plen = cp.info.type == LFM_PLENOPTIC;
-  if (path == LFM_PATH_COLLAPSED) return sep(cp.fwd_c, xr, y, 0, 1, 0, stream);
+  if (path == LFM_PATH_COLLAPSED) return sep(cp.fwd_c, xr, y, 0, 1, 0, stream, r0, r1);
   if (plen) {
     TRY(sep(cp.fwd_s1, xr, w.f, 0, cp.info.n_views, 0, stream));
-    return sep(cp.fwd_s3, w.f, y, 0, 1, 0, stream);
+    return sep(cp.fwd_s3, w.f, y, 0, 1, 0, stream, r0, r1);
   }
-  return sep(cp.fwd_s1, xr, y, 0, 1, 0, stream);
+  return sep(cp.fwd_s1, xr, y, 0, 1, 0, stream, r0, r1);
 }
 
+// x (+)= A_c^T y restricted to the detector rows [r0, r1) of y (others treated as zero).
 lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x, int accumulate, const Ws& w,
-                        void* stream) {
+                        void* stream, int r0 = 0, int r1 = -1) {
   const bool rot = cp.info.rot_passes != 0;
   float* target = rot ? w.r0 : x;
   int acc = rot ? 0 : accumulate;
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
-    TRY(sep(cp.adj_c1, y, w.z, 0, cp.info.nz, 0, stream));
+    TRY(sep(cp.adj_c1, y, w.z, 0, cp.info.nz, 0, stream, 0, -1, r0, r1));
     TRY(sep(cp.adj_c2, w.z, target, 0, cp.info.nz, acc, stream));
   } else if (plen) {
-    TRY(sep(cp.adj_s3, y, w.f, 0, cp.info.n_views, 0, stream));
+    TRY(sep(cp.adj_s3, y, w.f, 0, cp.info.n_views, 0, stream, 0, -1, r0, r1));
     TRY(sep(cp.adj_s1, w.f, target, 0, cp.info.nz, acc, stream));
   } else {
-    TRY(sep(cp.adj_s1, y, target, 0, cp.info.nz, acc, stream));
+    TRY(sep(cp.adj_s1, y, target, 0, cp.info.nz, acc, stream, 0, -1, r0, r1));
   }
   if (rot) {
     // the adjoint passes ping-pong between r1 and r0; start from r0
@@ -355,32 +359,48 @@ lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* 
   return st;
 }
 
-lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y, void* ws, size_t ws_bytes,
-                         void* stream) {
+lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* x, float* y,
+                              void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
   if ((st = check_path(path)) != LFM_OK) return st;
   if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  if (row0 < 0 || row1 > p->cams[cam].info.n_t || row0 >= row1) return fail(LFM_E_INVALID, "bad detector row range");
   Ws w;
   if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
-  st = forward_impl(p->cams[cam], path, x, y, w, stream);
+  st = forward_impl(p->cams[cam], path, x, y, w, stream, row0, row1);
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y, void* ws, size_t ws_bytes,
+                         void* stream) {
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  return lfm_A_forward_rows(p, cam, path, 0, p->cams[cam].info.n_t, x, y, ws, ws_bytes, stream);
+}
+
+lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
+                              int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if ((st = check_path(path)) != LFM_OK) return st;
+  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  if (row0 < 0 || row1 > p->cams[cam].info.n_t || row0 >= row1) return fail(LFM_E_INVALID, "bad detector row range");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  st = adjoint_impl(p->cams[cam], path, y, x, accumulate, w, stream, row0, row1);
   g_last_launches = g_launches;
   return st;
 }
 
 lfm_status lfm_A_adjoint(lfm_plan p, int cam, int path, const float* y, float* x, int accumulate, void* ws,
                          size_t ws_bytes, void* stream) {
-  g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
-  if ((st = check_path(path)) != LFM_OK) return st;
-  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
-  Ws w;
-  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
-  st = adjoint_impl(p->cams[cam], path, y, x, accumulate, w, stream);
-  g_last_launches = g_launches;
-  return st;
+  return lfm_A_adjoint_rows(p, cam, path, 0, p->cams[cam].info.n_t, y, x, accumulate, ws, ws_bytes, stream);
 }
 
 lfm_status lfm_pwls_stats(lfm_plan p, int cam, const float* Ax, const float* y, const float* w_, double* stats3,

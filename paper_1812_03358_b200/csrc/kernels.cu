@@ -191,6 +191,8 @@ struct SepArgs {
   int n_os, n_ot, n_is, n_it;
   int fsp, ftm, wsm, wtm, nb, nbuf;
   int s_ident;  // s table is the identity: pass 1 is a copy (source rows staged straight into U)
+  int ty0;      // first output t tile of this launch (detector-row sharding)
+  int win_r0, win_r1;  // source rows outside [win_r0, win_r1) are treated as zero (adjoint row sharding)
   float out_scale;
   int accumulate;
 };
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
   extern __shared__ __align__(16) float smem[];
   __shared__ TermHdr hdr[2][8];
   const int tid = threadIdx.x;
-  const int tx = blockIdx.x, ty = blockIdx.y, b = blockIdx.z;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
   const int os0 = tx * TS, ot0 = ty * TT;
   const SlotLayout L = slot_layout(a.ftm, a.fsp, STAGE && !a.s_ident, a.wsm, TS, a.wtm, TT, GSTEP);
   const int urows = a.ftm + GSTEP;  // U tile rows (padded)
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       const Term term = a.terms[e + sl];
       const TileT fs = a.fp_s[(size_t)term.s_tab * a.ntx + tx];
       const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
-      const bool live = fs.width != 0 && ft.width != 0;
+      const bool live = fs.width != 0 && ft.width != 0 && ft.lo < a.win_r1 && ft.lo + ft.width > a.win_r0;
+      const bool windowed = ft.lo < a.win_r0 || ft.lo + ft.width > a.win_r1;
       if (tid == 0) {
         TermHdr h;
         h.src_off = term.src_off;
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const float* src = a.src + term.src_off + os0;
         const int ncol = min(TS, a.n_is - os0);
-        if (((a.n_is & 3) == 0) && ((term.src_off & 3) == 0) && ncol == TS) {
+        if (((a.n_is & 3) == 0) && ((term.src_off & 3) == 0) && ncol == TS && !windowed) {
           for (int q = tid; q < ft.width * NQ; q += NT) {
             const int r = q / NQ, c4 = q - r * NQ;
             __pipeline_memcpy_async(U + r * TS + 4 * c4, src + (size_t)(ft.lo + r) * a.n_is + 4 * c4, 16);
@@ -284,8 +287,11 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
         } else {
           for (int q = tid; q < ft.width * TS; q += NT) {
             const int r = q / TS, c = q - r * TS;
-            if (c < ncol) __pipeline_memcpy_async(U + r * TS + c, src + (size_t)(ft.lo + r) * a.n_is + c, 4);
-            else U[r * TS + c] = 0.f;
+            const int row = ft.lo + r;
+            if (c < ncol && row >= a.win_r0 && row < a.win_r1)
+              __pipeline_memcpy_async(U + r * TS + c, src + (size_t)row * a.n_is + c, 4);
+            else
+              U[r * TS + c] = 0.f;
           }
         }
       } else {
@@ -294,7 +300,11 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
           const int n = ft.width * fs.width;
           for (int q = tid; q < n; q += NT) {
             const int r = q / fs.width, c = q - r * fs.width;
-            __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)(ft.lo + r) * a.n_is + c, 4);
+            const int row = ft.lo + r;
+            if (!windowed || (row >= a.win_r0 && row < a.win_r1))
+              __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
+            else
+              slot[L.xs + r * a.fsp + c] = 0.f;
           }
         }
         for (int q = tid; q < fs.wlen / 4; q += NT)
@@ -351,12 +361,14 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
           float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
           const float* x0 = xs + (size_t)r0 * pitch;
           const float* x1 = x0 + (size_t)GSTEP * pitch;
-          const bool second = STAGE || r0 + GSTEP < h.ft_w;
+          const bool first_in = STAGE || (h.ft_lo + r0 >= a.win_r0 && h.ft_lo + r0 < a.win_r1);
+          const bool second = STAGE || (r0 + GSTEP < h.ft_w && h.ft_lo + r0 + GSTEP >= a.win_r0 &&
+                                        h.ft_lo + r0 + GSTEP < a.win_r1);
           const float4* wp = wp0;
 #pragma unroll 4
           for (int p = 0; p < gd.y; ++p) {
             const float4 w4 = *wp++;
-            const float a0 = STAGE ? *x0 : __ldg(x0);
+            const float a0 = STAGE ? *x0 : (first_in ? __ldg(x0) : 0.f);
             const float a1 = STAGE ? *x1 : (second ? __ldg(x1) : 0.f);
             ++x0;
             ++x1;
@@ -458,7 +470,7 @@ static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStr
 }
 
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
-                      void* stream, std::string& err) {
+                      void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1) {
   if (n_out <= 0) return LFM_OK;
   SepArgs a;
   a.src = src;
@@ -489,8 +501,16 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.s_ident = op.s_ident;
   a.out_scale = op.out_scale;
   a.accumulate = accumulate;
+  // output rows [out_r0, out_r1): whole tiles covering the range (rows of partial tiles are computed too)
+  const int r1 = out_r1 < 0 ? op.n_ot : std::min(out_r1, op.n_ot);
+  const int r0 = std::max(0, out_r0);
+  if (r1 <= r0) return LFM_OK;
+  a.ty0 = r0 / op.tt;
+  const int nty = (r1 + op.tt - 1) / op.tt - a.ty0;
+  a.win_r0 = std::max(0, win_r0);
+  a.win_r1 = win_r1 < 0 ? op.n_it : std::min(win_r1, op.n_it);
   const size_t smem = sep_smem(op, op.nb);
-  dim3 grid(op.ntx, op.nty, n_out);
+  dim3 grid(op.ntx, nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
 #define LFM_SEP_CASE(TS_, TT_, NT_)                                                              \
   if (op.ts == TS_ && op.tt == TT_)                                                             \

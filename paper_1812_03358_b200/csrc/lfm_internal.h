@@ -134,5 +134,6 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
 lfm_status upload_camera(CameraPlan& cp, std::string& err);
 void free_camera(CameraPlan& cp);
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
-                      void* stream, std::string& err);
+                      void* stream, std::string& err, int out_r0 = 0, int out_r1 = -1, int win_r0 = 0,
+                      int win_r1 = -1);
 }  // namespace lfm

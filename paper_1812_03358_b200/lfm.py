@@ -88,6 +88,8 @@ _SIGS = {
     "lfm_vol_rotate": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_forward": [_P, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
+    "lfm_A_forward_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _S, _P],
+    "lfm_A_adjoint_rows": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_pwls_stats": [_P, _I, _P, _P, _P, _P, _P, _S, _P],
     "lfm_pwls_gains": [_P, _P, _P, _P, _P],
     "lfm_pwls_grad": [_P, _I, _I, _I, _P, _PP, _PP, _PP, _P, _F, _F, _I, _P, _P, _P, _S, _P],
@@ -217,6 +219,16 @@ def A_forward(plan, cam, x, y, ws, path=COLLAPSED, stream=None):
 def A_adjoint(plan, cam, y, x, ws, accumulate=False, path=COLLAPSED, stream=None):
     _check(_lib.lfm_A_adjoint(plan.handle, cam, path, _ptr(y), _ptr(x), int(accumulate), _ptr(ws), ws.numel(),
                               _stream(stream)))
+
+
+def A_forward_rows(plan, cam, row0, row1, x, y, ws, path=COLLAPSED, stream=None):
+    _check(_lib.lfm_A_forward_rows(plan.handle, cam, path, row0, row1, _ptr(x), _ptr(y), _ptr(ws), ws.numel(),
+                                   _stream(stream)))
+
+
+def A_adjoint_rows(plan, cam, row0, row1, y, x, ws, accumulate=False, path=COLLAPSED, stream=None):
+    _check(_lib.lfm_A_adjoint_rows(plan.handle, cam, path, row0, row1, _ptr(y), _ptr(x), int(accumulate), _ptr(ws),
+                                   ws.numel(), _stream(stream)))
 
 
 def pwls_stats(plan, cam, Ax, y, w, stats3, ws, stream=None):

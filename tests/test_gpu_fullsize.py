@@ -1,0 +1,59 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (collapsed path,
+128^3 two-camera; also the 64^3 single-camera config), element by element against the fp64
+oracle; the 256^3 four-camera config is checked through properties that hold at any size (adjoint
+identity, agreement of the two evaluation orders) because the oracle there takes many minutes."""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_helpers import TOL, dev, host, max_rel
+from workloads import flame_volume, make_config, normal_vector, uniform_vector
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.mark.parametrize("name,paths", [("64^3 single", (0, 1)), ("128^3 two-camera", (1,))])
+def test_full_size_parity(name, paths):
+    from oracle.system import SystemOperator
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config(name)
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    x = flame_volume(cfg["volume"])
+    for c, cam in enumerate(cfg["cameras"]):
+        op = SystemOperator(cfg["volume"], cam)
+        y_ref = op.forward(x.astype(np.float64))
+        r = uniform_vector(op.n_pix, 1)
+        g_ref = op.adjoint(r.astype(np.float64))
+        for path in paths:
+            y = torch.empty(op.n_pix, device="cuda:0")
+            lfm.A_forward(plan, c, dev(x).reshape(-1), y, ws, path=path)
+            assert max_rel(host(y), y_ref) <= TOL, (name, c, path, "forward")
+            g = torch.empty(op.n_vox, device="cuda:0")
+            lfm.A_adjoint(plan, c, dev(r), g, ws, path=path)
+            assert max_rel(host(g), g_ref) <= TOL, (name, c, path, "adjoint")
+
+
+def test_256_four_camera_properties():
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config("256^3 four-camera")
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    n_vox = plan.infos[0]["n_vox"]
+    x = dev(normal_vector(n_vox, 2))
+    xf = dev(flame_volume(cfg["volume"])).reshape(-1)
+    for c in range(plan.n_cam):
+        n_pix = plan.infos[c]["n_pix"]
+        r = dev(normal_vector(n_pix, 3))
+        y = torch.empty(n_pix, device="cuda:0")
+        g = torch.empty(n_vox, device="cuda:0")
+        lfm.A_forward(plan, c, x, y, ws)
+        lfm.A_adjoint(plan, c, r, g, ws)
+        lhs = float((y.double() * r.double()).sum())
+        rhs = float((x.double() * g.double()).sum())
+        assert abs(lhs - rhs) / (float(y.double().norm()) * float(r.double().norm())) <= 1e-5
+        y1 = torch.empty(n_pix, device="cuda:0")
+        y0 = torch.empty(n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, xf, y1, ws, path=lfm.COLLAPSED)
+        lfm.A_forward(plan, c, xf, y0, ws, path=lfm.PER_VIEW)
+        assert max_rel(host(y0), host(y1)) <= TOL

@@ -1,0 +1,210 @@
+"""CPU checks of the C-ABI library (no GPU needed): it loads, exports every symbol include/lfm.h
+declares, and a host-only plan (cuda_device = -1) reproduces the oracle's index/geometry tables
+bit-exactly (north star: "bit-exactly on index/geometry tables") and its fp64 weights.
+
+The oracle computes its bands from its own closed form (oracle/transport.py); the plan computes
+them independently in C++ (paper_1812_03358_b200/csrc/plan.cpp); both follow the op order of
+DESIGN.md reading Z21."""
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from oracle.rotation import decompose, shear_matrix
+from oracle.system import build_system
+from oracle.transport import band, basis_volume
+from workloads import make_config
+from workloads.geometry import plenoptic_camera, pose_yaw, pose_yaw_pitch, single_camera
+
+lfm = pytest.importorskip("paper_1812_03358_b200.lfm")
+
+CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "small_two"]
+
+
+def ragged_config():
+    cam = plenoptic_camera(5, 7, 0.05, 3, 2, pose=pose_yaw_pitch(12.0, -7.0))
+    cam.update(nl_t=3, n_t=21, k_t=2)
+    return dict(name="ragged", volume=dict(nx=19, ny=17, nz=13, dx=0.45, dy=0.4, dz=0.35),
+                cameras=[cam, single_camera(23, 0.05, 3, pose=pose_yaw_pitch(-20.0, 10.0))])
+
+
+def _cfg(name):
+    return ragged_config() if name == "ragged" else make_config(name)
+
+
+def test_exports_every_header_symbol():
+    header = open(lfm.os.path.join(lfm._HERE, "..", "include", "lfm.h")).read()
+    names = sorted(set(re.findall(r"^\s*(?:lfm_status|int|const char\*)\s+(lfm_\w+)\s*\(", header, re.M)))
+    assert len(names) >= 16
+    lib = ctypes.CDLL(lfm.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(lfm.EXPORTED)
+    assert lfm.version().startswith("liblfm")
+
+
+def _oracle_s3_band(cam, ax, k):
+    """Union over lenslets of band_mu(i) cap open cells of mu (reading Z9/Z10)."""
+    n_det = cam.lenslet_planes[ax][0].n
+    lo = np.full(n_det, 1 << 30)
+    hi = np.full(n_det, -1)
+    for mu, pl in enumerate(cam.lenslet_planes[ax]):
+        open_cells = np.nonzero(cam.masks[ax][mu])[0]
+        if len(open_cells) == 0:
+            continue
+        blo, bhi = band(cam.array_planes[ax], pl, cam.sk[ax][k], cam.d0[ax], cam.basis)
+        blo = np.maximum(blo, open_cells[0])
+        bhi = np.minimum(bhi, open_cells[-1])
+        ok = bhi >= blo
+        lo = np.where(ok, np.minimum(lo, blo), lo)
+        hi = np.where(ok, np.maximum(hi, bhi), hi)
+    empty = hi < 0
+    return np.where(empty, 0, lo), np.where(empty, 0, hi - lo + 1)
+
+
+def _bands_equal(plan, c, tab, ax, idx, lo, hi):
+    st = plan.export_table(c, tab + "_START", ax, idx)
+    ln = plan.export_table(c, tab + "_LEN", ax, idx)
+    ln_o = np.where(hi >= lo, hi - lo + 1, 0)
+    st_o = np.where(hi >= lo, lo, 0)
+    assert np.array_equal(st, st_o) and np.array_equal(ln, ln_o), (tab, ax, idx)
+    return st, ln
+
+
+def _weights_match(plan, c, tab, ax, idx, dense, rel=1e-13):
+    st = plan.export_table(c, tab + "_START", ax, idx)
+    ln = plan.export_table(c, tab + "_LEN", ax, idx)
+    w = plan.export_table(c, tab + "_W64", ax, idx).reshape(len(st), -1)
+    rec = np.zeros_like(dense)
+    for i in range(len(st)):
+        rec[i, st[i]:st[i] + ln[i]] = w[i, :ln[i]]
+    scale = max(np.abs(dense).max(), 1e-300)
+    assert np.abs(rec - dense).max() <= rel * scale, (tab, ax, idx)
+
+
+@pytest.mark.parametrize("name", CONFIGS + ["ragged"])
+def test_band_tables_bit_exact(name):
+    cfg = _cfg(name)
+    plan = lfm.Plan(cfg, device=-1)
+    for c, op in enumerate(build_system(cfg)):
+        cam = op.camera
+        dst = cam.array_planes if cam.type == 1 else cam.det_planes
+        for ax in range(2):
+            for k in range(len(cam.sk[ax])):
+                for n in range(cam.nz):
+                    idx = k * cam.nz + n
+                    lo, hi = band(cam.slice_planes[ax][n], dst[ax], cam.sk[ax][k], cam.d0[ax], cam.basis)
+                    _bands_equal(plan, c, "S1F", ax, idx, lo, hi)
+                    _weights_match(plan, c, "S1F", ax, idx, cam.S1[ax][k][n].toarray())
+                    lo, hi = band(dst[ax], cam.slice_planes[ax][n], cam.sk[ax][k], cam.d0[ax], cam.basis)
+                    _bands_equal(plan, c, "S1A", ax, idx, lo, hi)
+                    # adjoint table = the transport in the other direction = transpose
+                    _weights_match(plan, c, "S1A", ax, idx, cam.S1[ax][k][n].toarray().T, rel=1e-10)
+                if cam.type == 1:
+                    st_o, ln_o = _oracle_s3_band(cam, ax, k)
+                    assert np.array_equal(plan.export_table(c, "S3F_START", ax, k), st_o)
+                    assert np.array_equal(plan.export_table(c, "S3F_LEN", ax, k), ln_o)
+                    _weights_match(plan, c, "S3F", ax, k, cam.S3[ax][k].toarray())
+                    _weights_match(plan, c, "S3A", ax, k, cam.S3[ax][k].toarray().T, rel=1e-10)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_single", "small_two", "ragged"])
+def test_collapsed_composite_tables(name):
+    """C_n = sum_k S_k B_{k,n} per axis (exact re-association over the tensor angular grid)."""
+    cfg = _cfg(name)
+    plan = lfm.Plan(cfg, device=-1)
+    for c, op in enumerate(build_system(cfg)):
+        cam = op.camera
+        for ax in range(2):
+            for n in range(cam.nz):
+                Cn = 0
+                for k in range(len(cam.sk[ax])):
+                    B = cam.S1[ax][k][n]
+                    Cn = Cn + ((cam.S3[ax][k] @ B) if cam.type == 1 else B)
+                Cn = Cn.toarray()
+                nz = Cn > 0
+                lo = np.where(nz.any(1), nz.argmax(1), 0)
+                hi = np.where(nz.any(1), Cn.shape[1] - 1 - nz[:, ::-1].argmax(1), -1)
+                _bands_equal(plan, c, "CF", ax, n, lo, hi)
+                _weights_match(plan, c, "CF", ax, n, Cn, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two"])
+def test_rotation_factors_and_shear_tables(name):
+    cfg = _cfg(name)
+    plan = lfm.Plan(cfg, device=-1)
+    vol = cfg["volume"]
+    dims = (vol["nx"], vol["ny"], vol["nz"])
+    vox = (vol["dx"], vol["dy"], vol["dz"])
+    for c, cam in enumerate(cfg["cameras"]):
+        inf = plan.info(c)
+        dec = decompose(cam["R"])
+        assert tuple(inf["rot_D"]) == dec["D"]                       # bit-exact fp64 geometry
+        assert tuple(inf["shear"]) == (dec["a_zx"], dec["a_zy"], dec["a_xy"], dec["a_xz"], dec["a_yx"], dec["a_yz"])
+        vox_r = tuple(v / d for v, d in zip(vox, dec["D"]))
+        assert tuple(inf["vox_r"]) == vox_r
+        coeffs = [(dec["a_zx"], dec["a_zy"]), (dec["a_xy"], dec["a_xz"]), (dec["a_yx"], dec["a_yz"])]
+        for p, axis in enumerate("zxy"):
+            E = shear_matrix(dims, vox_r, axis, *coeffs[p]).toarray()
+            mlo = plan.export_table(c, "ROT_MLO", 0, p)
+            if len(mlo) == 0:                                        # identity pass skipped
+                assert coeffs[p] == (0.0, 0.0)
+                continue
+            w = plan.export_table(c, "ROT_W64", 0, p).reshape(len(mlo), -1)
+            rec = np.zeros_like(E)
+            nx, ny, nz = dims
+            for flat in range(nx * ny * nz):
+                ix, iy, iz = flat % nx, (flat // nx) % ny, flat // (nx * ny)
+                line, pos, n, stride = {"z": (ix + nx * iy, iz, nz, nx * ny), "x": (iy + ny * iz, ix, nx, 1),
+                                        "y": (ix + nx * iz, iy, ny, nx)}[axis]
+                for q in range(w.shape[1]):
+                    j = pos + mlo[line] + q
+                    if 0 <= j < n and w[line, q] != 0.0:
+                        rec[flat, flat + (j - pos) * stride] = w[line, q]
+            assert np.abs(rec - E).max() <= 1e-12
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_scalars_match_oracle(name):
+    cfg = _cfg(name)
+    plan = lfm.Plan(cfg, device=-1)
+    for c, op in enumerate(build_system(cfg)):
+        sc = plan.export_table(c, "SCALARS", 0, 0)
+        cam = op.camera
+        assert sc[0] == pytest.approx(cam.scale_s1, rel=1e-14)
+        if cam.type == 1:
+            assert sc[1] == pytest.approx(cam.scale_s3, rel=1e-14)
+            assert sc[2] == pytest.approx(basis_volume(cam.array_planes[0], cam.d0[0]) *
+                                          basis_volume(cam.array_planes[1], cam.d0[1]), rel=1e-14)
+
+
+def test_error_statuses():
+    vol = dict(nx=8, ny=8, nz=8, dx=0.4, dy=0.4, dz=0.4)
+    cases = [
+        (plenoptic_camera(4, 8, 0.04, 2, 2, fill=1.5), 1),           # fill > 1
+        (plenoptic_camera(4, 8, 0.04, 2, 2, pose=pose_yaw(90.0)), 3),  # needs a quarter-turn permutation
+        (dict(single_camera(32, 0.04, 2), f_main=0.0), 2),           # zero focal length
+        (dict(single_camera(32, 0.04, 2), d_det=0.0), 3),            # detector on the angular plane
+        (dict(single_camera(32, 0.04, 2), k_s=0), 1),
+    ]
+    for cam, status in cases:
+        with pytest.raises(lfm.LfmError) as e:
+            lfm.Plan(dict(volume=vol, cameras=[cam]), device=-1)
+        assert e.value.status == status, (cam, e.value)
+        assert "camera 0" in str(e.value)
+    with pytest.raises(lfm.LfmError) as e:
+        lfm.Plan(dict(volume=vol, cameras=[]), device=-1)
+    assert e.value.status == 1
+
+
+def test_host_only_plan_rejects_apply_calls():
+    plan = lfm.Plan(make_config("tiny"), device=-1)
+    assert plan.info(0)["ws_bytes"] > 0
+    import torch
+    ws = torch.empty(plan.ws_bytes, dtype=torch.uint8)
+    x = torch.zeros(plan.info(0)["n_vox"])
+    y = torch.zeros(plan.info(0)["n_pix"])
+    with pytest.raises(lfm.LfmError) as e:
+        lfm.A_forward(plan, 0, x, y, ws, stream=0)
+    assert e.value.status == 1 and "host-only" in str(e.value)
