@@ -228,6 +228,7 @@ lfm_status lfm_plan_create(const lfm_geometry* g, int cuda_device, lfm_plan* out
     lfm_status st = cuda_check(cudaSetDevice(cuda_device), "cudaSetDevice", err);
     for (int c = 0; st == LFM_OK && c < g->n_cam; ++c) {
       st = upload_camera(p->cams[c], err);
+      if (st == LFM_OK) st = autotune_camera(p->cams[c], err);
       if (st != LFM_OK) err = "camera " + std::to_string(c) + ": " + err;
     }
     cudaSetDevice(prev);

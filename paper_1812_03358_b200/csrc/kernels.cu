@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -191,6 +193,7 @@ struct SepArgs {
   int n_os, n_ot, n_is, n_it;
   int fsp, ftm, wsm, wtm, nb, nbuf;
   int s_ident;  // s table is the identity: pass 1 is a copy (source rows staged straight into U)
+  int ug;       // identity s: pass 2 reads U rows straight from the source in global memory (no U tile)
   int ty0;      // first output t tile of this launch (detector-row sharding)
   int win_r0, win_r1;  // source rows outside [win_r0, win_r1) are treated as zero (adjoint row sharding)
   float out_scale;
@@ -274,7 +277,9 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       }
       if (!live) continue;
       float* slot = buf + sl * L.per;
-      if (a.s_ident) {
+      if (a.s_ident && a.ug) {
+        // pass 2 reads the source rows straight from L1/L2: nothing to stage
+      } else if (a.s_ident) {
         // U[r][c] = src[ft.lo + r][os0 + c]
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const float* src = a.src + term.src_off + os0;
@@ -392,16 +397,36 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       const float* slot = buf + sl * L.per;
       const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
       const int4* GD = reinterpret_cast<const int4*>(slot + L.gt);
+      const bool ug = a.s_ident && a.ug;
+      const int gcol = os0 + quad * 4;
+      const bool gvec = ug && ((a.n_is & 3) == 0) && ((h.src_off & 3) == 0) && gcol + 3 < a.n_is;
 #pragma unroll
       for (int j = 0; j < GP; ++j) {
         const int4 gd = GD[gsub + j * GSTEP];
         const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.wt_off));
         const float4* up = reinterpret_cast<const float4*>(U + (gd.x - h.ft_lo) * TS + quad * 4);
+        const float* gp = a.src + h.src_off + (size_t)gd.x * a.n_is + gcol;
+        int grow = gd.x;
 #pragma unroll 4
         for (int p = 0; p < gd.y; ++p) {
           const float4 w4 = *wp++;
-          const float4 u4 = *up;
-          up += TS / 4;
+          float4 u4;
+          if (!ug) {
+            u4 = *up;
+            up += TS / 4;
+          } else {
+            const bool rin = grow >= a.win_r0 && grow < a.win_r1;
+            if (gvec) {
+              u4 = rin ? __ldg(reinterpret_cast<const float4*>(gp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+              u4.x = (rin && gcol + 0 < a.n_is) ? __ldg(gp + 0) : 0.f;
+              u4.y = (rin && gcol + 1 < a.n_is) ? __ldg(gp + 1) : 0.f;
+              u4.z = (rin && gcol + 2 < a.n_is) ? __ldg(gp + 2) : 0.f;
+              u4.w = (rin && gcol + 3 < a.n_is) ? __ldg(gp + 3) : 0.f;
+            }
+            gp += a.n_is;
+            ++grow;
+          }
           acc[j][0][0] = fmaf(w4.x, u4.x, acc[j][0][0]); acc[j][0][1] = fmaf(w4.x, u4.y, acc[j][0][1]);
           acc[j][0][2] = fmaf(w4.x, u4.z, acc[j][0][2]); acc[j][0][3] = fmaf(w4.x, u4.w, acc[j][0][3]);
           acc[j][1][0] = fmaf(w4.y, u4.x, acc[j][1][0]); acc[j][1][1] = fmaf(w4.y, u4.y, acc[j][1][1]);
@@ -499,6 +524,7 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.nb = op.nb;
   a.nbuf = op.nbuf;
   a.s_ident = op.s_ident;
+  a.ug = op.s_ident && !op.stage;
   a.out_scale = op.out_scale;
   a.accumulate = accumulate;
   // output rows [out_r0, out_r1): whole tiles covering the range (rows of partial tiles are computed too)
@@ -785,4 +811,94 @@ lfm_status k_majoriser_finish(float* d, long long n, float add, void* s, std::st
   return cuda_check(cudaGetLastError(), "majoriser_finish", err);
 }
 
+}  // namespace lfm
+
+namespace lfm {
+// ------------------------------------------------------------------------------------------
+// Plan-time autotuning (host side of plan creation, excluded from timed work): every hot op of
+// A_forward / A_adjoint times each shared-memory-feasible (tile, threads, staging, nb) candidate on
+// zero-filled scratch buffers with CUDA events and keeps the fastest.  LFM_AUTOTUNE=0 disables it
+// (the cost-model choice is kept).
+static void free_sep_dev(SepOp& op) {
+  dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t);
+  op.d_terms = nullptr; op.d_offs = nullptr; op.d_fp_s = nullptr; op.d_fp_t = nullptr;
+}
+
+lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
+  const char* env = std::getenv("LFM_AUTOTUNE");
+  if (env && env[0] == '0') return LFM_OK;
+  SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2};
+  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2"};
+  const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
+  size_t src_n = 0, out_n = 0;
+  for (SepOp* op : ops) {
+    if (!op->fs) continue;
+    long long mx = 0;
+    for (const Term& t : op->terms) mx = std::max(mx, t.src_off);
+    src_n = std::max(src_n, (size_t)mx + (size_t)op->n_is * op->n_it + 16);
+    out_n = std::max(out_n, (size_t)std::min(op->n_out, 64) * op->n_os * op->n_ot + 16);
+  }
+  float *src = nullptr, *out = nullptr;
+  if (cudaMalloc(&src, src_n * 4) != cudaSuccess || cudaMalloc(&out, out_n * 4) != cudaSuccess) {
+    cudaGetLastError();
+    dfree(src);
+    if (dbg) std::fprintf(stderr, "[lfm] autotune skipped: no scratch memory\n");
+    return LFM_OK;
+  }
+  cudaMemset(src, 0, src_n * 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int cand[][3] = {{128, 64, 256}, {128, 32, 256}, {64, 64, 128}, {64, 32, 128}, {32, 32, 64}};
+  lfm_status st = LFM_OK;
+  for (int q = 0; q < 7 && st == LFM_OK; ++q) {
+    SepOp& op = *ops[q];
+    if (!op.fs) continue;
+    if (std::getenv((std::string("LFM_FORCE_") + names[q]).c_str())) continue;  // explicit override wins
+    const int n_out = std::min(op.n_out, 64);
+    const SepOp keep = op;  // cost-model choice (device pointers of `op` are replaced below)
+    int bts = keep.ts, btt = keep.tt, bnt = keep.nt, bnb = keep.nb, bst = keep.stage;
+    float best = 1e30f;
+    for (auto& c : cand) {
+      for (int stage : {1, 0}) {
+        for (int nb : {1, 2, 4}) {
+          if (nb > 1 && op.terms.size() < (size_t)op.n_out * 2) continue;
+          op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.stage = stage; op.nb = nb;
+          fill_sep_geometry(op);
+          if (sep_smem(op, nb) > (size_t)210 * 1024) continue;
+          free_sep_dev(op);
+          size_t bytes = 0;
+          if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+          float ms = 0, tot = 0;
+          bool ok = true;
+          for (int rep = 0; rep < 3 && ok; ++rep) {
+            cudaEventRecord(e0, 0);
+            ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+            cudaEventRecord(e1, 0);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) tot += ms;
+          }
+          if (!ok || cudaGetLastError() != cudaSuccess) continue;
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = nb; bst = stage; }
+        }
+        if (st != LFM_OK) break;
+      }
+      if (st != LFM_OK) break;
+    }
+    op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst;
+    fill_sep_geometry(op);
+    free_sep_dev(op);
+    size_t bytes = 0;
+    if (st == LFM_OK) st = upload_sep(op, bytes, err);
+    if (dbg)
+      std::fprintf(stderr, "[lfm] autotune %-7s -> tile %3dx%-3d nt %3d nb %d stage %d  (%.3f ms for %d outputs)\n",
+                   names[q], op.ts, op.tt, op.nt, op.nb, op.stage, best / 2, n_out);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  dfree(src);
+  dfree(out);
+  return st;
+}
 }  // namespace lfm

@@ -129,6 +129,9 @@ namespace lfm {
 void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width);
 void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen);
 size_t sep_smem(const SepOp& op, int nb);
+void fill_sep_geometry(SepOp& op);
+bool sep_choose_tile(SepOp& op);
+lfm_status autotune_camera(CameraPlan& cp, std::string& err);
 lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& out, std::string& err);
 // kernels.cu
 lfm_status upload_camera(CameraPlan& cp, std::string& err);

@@ -424,7 +424,7 @@ void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& 
   width = mxv - mn + 1;
 }
 
-static void fill_sep_geometry(SepOp& op) {
+void fill_sep_geometry(SepOp& op) {
   const BandFamily& fs = *op.fs;
   const BandFamily& ft = *op.ft;
   op.fs_max = 1;
@@ -501,7 +501,8 @@ size_t sep_smem(const SepOp& op, int nb) {
   size_t maxt = 0;
   for (size_t b = 0; b + 1 < op.offs.size(); ++b) maxt = std::max(maxt, (size_t)(op.offs[b + 1] - op.offs[b]));
   size_t nbuf = maxt > (size_t)nb ? 2 : 1;
-  return (nbuf * per * nb + nbuf * (size_t)nb * urows * op.ts) * 4;
+  const bool u_tile = !(op.s_ident && !op.stage);   // identity s read from global: no U tile
+  return (nbuf * per * nb + (u_tile ? nbuf * (size_t)nb * urows * op.ts : 0)) * 4;
 }
 // Estimated time of an op for a tile choice: L2->SM traffic of the staged footprints and the FMA issue
 // slots of both passes, with a crude occupancy factor (a sampled cost model).
@@ -526,11 +527,14 @@ static double sep_cost(const SepOp& op, int nt, size_t smem) {
       for (int x = 0; x < ntx; ++x) {
         if (!fw[x]) continue;
         if (op.s_ident) {
-          bytes += 4.0 * (double)w * op.ts + 4.0 * wl;
+          // staged: U tile; unstaged: pass 2 streams the rows from L1/L2 (~2x the L2 traffic of one staging)
+          bytes += 4.0 * (double)w * op.ts * (op.stage ? 1.0 : 6.0) + 4.0 * wl;
           slots += (double)wl * op.ts;
         } else {
-          bytes += 4.0 * ((op.stage ? (double)w * fw[x] : 2.0 * w * fwl[x] / 4.0) + fwl[x] + wl);
-          slots += 1.3 * (double)w * fwl[x] * (op.stage ? 1.0 : 2.0) + (double)wl * op.ts;  // pass 1 + pass 2
+          // unstaged pass 1 gathers scalar loads from L1/L2: latency-bound, counted 4x
+          // unstaged: gathered rows are shared through L1 by the TS/4 column groups of the CTA
+          bytes += 4.0 * ((op.stage ? (double)w * fw[x] : 2.0 * w * fwl[x] / 4.0 * (32.0 / op.ts)) + fwl[x] + wl);
+          slots += 1.3 * (double)w * fwl[x] * (op.stage ? 1.0 : 1.5) + (double)wl * op.ts;  // pass 1 + pass 2
         }
       }
     }
@@ -543,13 +547,12 @@ static double sep_cost(const SepOp& op, int nt, size_t smem) {
   return scale * (bytes / 6e12 + slots / (30e12 * occ));
 }
 
-static bool sep_choose_tile(SepOp& op) {
+bool sep_choose_tile(SepOp& op) {
   const int cand[][3] = {{128, 64, 256}, {128, 32, 256}, {64, 64, 128}, {64, 32, 128}, {32, 32, 64}};
   double best = 1e300;
   int bts = 0, btt = 0, bst = 0, bnb = 0, bnt = 0;
   for (auto& c : cand) {
     for (int stage : {1, 0}) {
-      if (op.s_ident && stage == 0) continue;
       op.ts = c[0];
       op.tt = c[1];
       op.nt = c[2];
