@@ -222,7 +222,7 @@ struct TermHdr {
 };
 
 template <int TS, int TT, int NT, bool STAGE>
-__global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
+__global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
   constexpr int NQ = TS / 4;           // 4-column groups per tile (pass 1 groups, pass 2 quads)
   constexpr int GSTEP = NT / NQ;       // pass 2: row groups in flight; pass 1: row stride
   constexpr int NG = TT / 4;           // row groups per tile
@@ -240,13 +240,13 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
   float* Ubase = smem + nbuf * a.nb * L.per;   // [nbuf][nb][ftm][TS]
   const int quad = tid % NQ, gsub = tid / NQ;
 
-  float acc[GP][4][4], hi[GP][4][4];
+  float acc[GP][4][4];
 #pragma unroll
   for (int j = 0; j < GP; ++j)
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) { acc[j][r][c] = 0.f; hi[j][r][c] = 0.f; }
+      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
 
   const int e0 = a.offs[b], e1 = a.offs[b + 1];
   const int nchunks = (e1 - e0 + a.nb - 1) / a.nb;
@@ -336,7 +336,6 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
   };
 
   if (nchunks > 0) stage_chunk(0, 0);
-  int chunks = 0;
   for (int ci = 0; ci < nchunks; ++ci) {
     const int sd = ci & 1;
     const int nterm = min(a.nb, e1 - (e0 + ci * a.nb));
@@ -439,15 +438,6 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       }
     }
     __syncthreads();  // chunk done with U and its buffer before they are refilled
-    if (++chunks == 4) {  // blocked accumulation (keeps long positive sums accurate)
-      chunks = 0;
-#pragma unroll
-      for (int j = 0; j < GP; ++j)
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) { hi[j][r][c] += acc[j][r][c]; acc[j][r][c] = 0.f; }
-    }
   }
   float* outb = a.out + (size_t)b * a.out_stride;
   const int col = os0 + quad * 4;
@@ -461,7 +451,7 @@ __global__ void __launch_bounds__(NT) sep_kernel(SepArgs a) {
       float* p = outb + (size_t)row * a.n_os + col;
       float v[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * (hi[j][r][c] + acc[j][r][c]);
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
       if (vec) {
         float4 o = make_float4(v[0], v[1], v[2], v[3]);
         if (a.accumulate) {
@@ -824,9 +814,30 @@ static void free_sep_dev(SepOp& op) {
   op.d_terms = nullptr; op.d_offs = nullptr; op.d_fp_s = nullptr; op.d_fp_t = nullptr;
 }
 
+// Optional result cache (LFM_TUNE_FILE): lines "<key> <op> ts tt nt nb stage"; a hit skips the timing
+// (used so that ncu captures see only the measured launches).
+static std::string tune_key(const CameraPlan& cp) {
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(&cp.cam);
+  unsigned long long h = 1469598103934665603ull;
+  for (size_t i = 0; i < sizeof(cp.cam); ++i) h = (h ^ b[i]) * 1099511628211ull;
+  char buf[96];
+  std::snprintf(buf, sizeof(buf), "%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
+  return buf;
+}
+
 lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   const char* env = std::getenv("LFM_AUTOTUNE");
   if (env && env[0] == '0') return LFM_OK;
+  const char* tfile = std::getenv("LFM_TUNE_FILE");
+  const std::string key = tune_key(cp);
+  std::vector<std::string> cached;
+  if (tfile) {
+    if (FILE* f = std::fopen(tfile, "r")) {
+      char line[256];
+      while (std::fgets(line, sizeof(line), f)) cached.push_back(line);
+      std::fclose(f);
+    }
+  }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2};
   const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2"};
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
@@ -855,6 +866,21 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     SepOp& op = *ops[q];
     if (!op.fs) continue;
     if (std::getenv((std::string("LFM_FORCE_") + names[q]).c_str())) continue;  // explicit override wins
+    bool hit = false;
+    for (const std::string& ln : cached) {
+      char k[128], o[32];
+      int ts, tt, nt, nb, stg;
+      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d", k, o, &ts, &tt, &nt, &nb, &stg) == 7 && key == k &&
+          std::string(o) == names[q]) {
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg;
+        fill_sep_geometry(op);
+        free_sep_dev(op);
+        size_t bytes = 0;
+        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+        hit = true;
+      }
+    }
+    if (hit || st != LFM_OK) continue;
     const int n_out = std::min(op.n_out, 64);
     const SepOp keep = op;  // cost-model choice (device pointers of `op` are replaced below)
     int bts = keep.ts, btt = keep.tt, bnt = keep.nt, bnb = keep.nb, bst = keep.stage;
@@ -894,6 +920,12 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> tile %3dx%-3d nt %3d nb %d stage %d  (%.3f ms for %d outputs)\n",
                    names[q], op.ts, op.tt, op.nt, op.nb, op.stage, best / 2, n_out);
+    if (tfile && st == LFM_OK) {
+      if (FILE* f = std::fopen(tfile, "a")) {
+        std::fprintf(f, "%s %s %d %d %d %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage);
+        std::fclose(f);
+      }
+    }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
