@@ -147,7 +147,13 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
   const bool plen = cp.info.type == LFM_PLENOPTIC;
-  if (path == LFM_PATH_COLLAPSED) return sep(cp.fwd_c, xr, y, 0, 1, 0, stream, r0, r1);
+  if (path == LFM_PATH_COLLAPSED) {
+    if (cp.fwd_split) {
+      TRY(sep(cp.fwd_c1, xr, w.z, 0, cp.info.nz, 0, stream));
+      return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1);
+    }
+    return sep(cp.fwd_c, xr, y, 0, 1, 0, stream, r0, r1);
+  }
   if (plen) {
     TRY(sep(cp.fwd_s1, xr, w.f, 0, cp.info.n_views, 0, stream));
     return sep(cp.fwd_s3, w.f, y, 0, 1, 0, stream, r0, r1);

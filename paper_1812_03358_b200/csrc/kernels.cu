@@ -65,8 +65,8 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
   if (st != LFM_OK) return st;
   if ((st = dev_upload(&f.d_idx, ix.data(), ix.size() * sizeof(int32_t), err)) != LFM_OK) return st;
   if ((st = dev_upload(&f.d_w, w32.data(), w32.size() * sizeof(float), err)) != LFM_OK) return st;
-  std::vector<int32_t> g4((size_t)f.n_tables * f.n_groups * 4);
-  for (size_t i = 0; i < (size_t)f.n_tables * f.n_groups; ++i) {
+  std::vector<int32_t> g4((size_t)f.n_tables * f.n_groups * 8);  // two int4 segments per group
+  for (size_t i = 0; i < (size_t)f.n_tables * f.n_groups * 2; ++i) {
     g4[4 * i] = f.g_j0[i];
     g4[4 * i + 1] = f.g_w[i];
     g4[4 * i + 2] = f.g_off[i];
@@ -119,7 +119,7 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
   for (BandFamily* f : {&cp.id_s, &cp.id_t, &cp.id_vt})
     if ((st = upload_family(*f, bytes, err)) != LFM_OK) return st;
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
   for (SepOp* op : ops)
     if ((st = upload_sep(*op, bytes, err)) != LFM_OK) return st;
   for (int p = 0; p < 3; ++p) {
@@ -151,7 +151,7 @@ void free_camera(CameraPlan& cp) {
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
   for (SepOp* op : ops) {
     dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t);
     op->d_terms = nullptr; op->d_offs = nullptr; op->d_fp_s = nullptr; op->d_fp_t = nullptr;
@@ -203,15 +203,17 @@ struct SepArgs {
 struct SlotLayout {
   int xs, ws, gs, wt, gt, per;
 };
+// per staged term: [source footprint X (mode 0)] [s weights] [s group descriptors: 2 int4 per group]
+// [t weights] [t group descriptors: 2 int4 per group]; must match sep_smem() in plan.cpp
 __host__ __device__ inline SlotLayout slot_layout(int ftm, int fsp, bool xs, int wsm, int ts, int wtm, int tt,
                                                   int gstep) {
   SlotLayout L;
   L.xs = 0;
   L.ws = xs ? ((ftm + gstep) * fsp + 3) / 4 * 4 : 0;
   L.gs = L.ws + (wsm + 3) / 4 * 4;
-  L.wt = L.gs + ts;            // ts/4 int4
+  L.wt = L.gs + 2 * ts;
   L.gt = L.wt + (wtm + 3) / 4 * 4;
-  L.per = L.gt + tt;           // tt/4 int4
+  L.per = L.gt + 2 * tt;
   return L;
 }
 
@@ -221,23 +223,40 @@ struct TermHdr {
   int fs_lo, fs_w, ws_off, ft_lo, ft_w, wt_off, s_tab, t_tab;
 };
 
-template <int TS, int TT, int NT, bool STAGE>
-__global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
+// 16 FFMAs: acc[r][c] += w[r] * u[c]
+__device__ __forceinline__ void fma4x4(float (&acc)[4][4], const float4 w4, const float4 u4) {
+  acc[0][0] = fmaf(w4.x, u4.x, acc[0][0]); acc[0][1] = fmaf(w4.x, u4.y, acc[0][1]);
+  acc[0][2] = fmaf(w4.x, u4.z, acc[0][2]); acc[0][3] = fmaf(w4.x, u4.w, acc[0][3]);
+  acc[1][0] = fmaf(w4.y, u4.x, acc[1][0]); acc[1][1] = fmaf(w4.y, u4.y, acc[1][1]);
+  acc[1][2] = fmaf(w4.y, u4.z, acc[1][2]); acc[1][3] = fmaf(w4.y, u4.w, acc[1][3]);
+  acc[2][0] = fmaf(w4.z, u4.x, acc[2][0]); acc[2][1] = fmaf(w4.z, u4.y, acc[2][1]);
+  acc[2][2] = fmaf(w4.z, u4.z, acc[2][2]); acc[2][3] = fmaf(w4.z, u4.w, acc[2][3]);
+  acc[3][0] = fmaf(w4.w, u4.x, acc[3][0]); acc[3][1] = fmaf(w4.w, u4.y, acc[3][1]);
+  acc[3][2] = fmaf(w4.w, u4.z, acc[3][2]); acc[3][3] = fmaf(w4.w, u4.w, acc[3][3]);
+}
+
+// MODE 0: source footprint staged in smem, pass 1 from smem;  MODE 1: pass 1 gathers from L1/L2;
+// MODE 2: identity s table, source rows staged straight into U;  MODE 3: identity s table, pass 2
+// streams the source rows from L1/L2 (no U tile).
+template <int TS, int TT, int NT, int MODE>
+__global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
   constexpr int NQ = TS / 4;           // 4-column groups per tile (pass 1 groups, pass 2 quads)
   constexpr int GSTEP = NT / NQ;       // pass 2: row groups in flight; pass 1: row stride
   constexpr int NG = TT / 4;           // row groups per tile
   constexpr int GP = NG / GSTEP;       // row groups per thread in pass 2
+  constexpr bool XS = MODE == 0;
+  constexpr bool IDENT = MODE >= 2;
   static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
   extern __shared__ __align__(16) float smem[];
   __shared__ TermHdr hdr[2][8];
   const int tid = threadIdx.x;
   const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
   const int os0 = tx * TS, ot0 = ty * TT;
-  const SlotLayout L = slot_layout(a.ftm, a.fsp, STAGE && !a.s_ident, a.wsm, TS, a.wtm, TT, GSTEP);
+  const SlotLayout L = slot_layout(a.ftm, a.fsp, XS, a.wsm, TS, a.wtm, TT, GSTEP);
   const int urows = a.ftm + GSTEP;  // U tile rows (padded)
   const int nbuf = a.nbuf;
   float* bufs[2] = {smem, smem + (nbuf - 1) * a.nb * L.per};
-  float* Ubase = smem + nbuf * a.nb * L.per;   // [nbuf][nb][ftm][TS]
+  float* Ubase = smem + nbuf * a.nb * L.per;   // [nbuf][nb][urows][TS]
   const int quad = tid % NQ, gsub = tid / NQ;
 
   float acc[GP][4][4];
@@ -277,9 +296,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
       }
       if (!live) continue;
       float* slot = buf + sl * L.per;
-      if (a.s_ident && a.ug) {
-        // pass 2 reads the source rows straight from L1/L2: nothing to stage
-      } else if (a.s_ident) {
+      if (MODE == 2) {
         // U[r][c] = src[ft.lo + r][os0 + c]
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const float* src = a.src + term.src_off + os0;
@@ -299,25 +316,26 @@ __global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
               U[r * TS + c] = 0.f;
           }
         }
-      } else {
-        if (STAGE) {
-          const float* src = a.src + term.src_off + fs.lo;
-          const int n = ft.width * fs.width;
-          for (int q = tid; q < n; q += NT) {
-            const int r = q / fs.width, c = q - r * fs.width;
-            const int row = ft.lo + r;
-            if (!windowed || (row >= a.win_r0 && row < a.win_r1))
-              __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
-            else
-              slot[L.xs + r * a.fsp + c] = 0.f;
-          }
+      }
+      if (XS) {
+        const float* src = a.src + term.src_off + fs.lo;
+        const int n = ft.width * fs.width;
+        for (int q = tid; q < n; q += NT) {
+          const int r = q / fs.width, c = q - r * fs.width;
+          const int row = ft.lo + r;
+          if (!windowed || (row >= a.win_r0 && row < a.win_r1))
+            __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
+          else
+            slot[L.xs + r * a.fsp + c] = 0.f;
         }
+      }
+      if (!IDENT) {
         for (int q = tid; q < fs.wlen / 4; q += NT)
           __pipeline_memcpy_async(slot + L.ws + 4 * q, a.s_gw + fs.woff + 4 * q, 16);
         const int g0 = tx * NQ;
-        for (int q = tid; q < NQ; q += NT) {
-          if (g0 + q < a.s_ngroups)
-            __pipeline_memcpy_async(slot + L.gs + 4 * q, a.s_g + (size_t)term.s_tab * a.s_ngroups + g0 + q, 16);
+        for (int q = tid; q < 2 * NQ; q += NT) {
+          if (g0 + q / 2 < a.s_ngroups)
+            __pipeline_memcpy_async(slot + L.gs + 4 * q, a.s_g + 2 * ((size_t)term.s_tab * a.s_ngroups + g0) + q, 16);
           else
             reinterpret_cast<int4*>(slot + L.gs)[q] = make_int4(0, 0, 0, 0);
         }
@@ -325,9 +343,9 @@ __global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
       for (int q = tid; q < ft.wlen / 4; q += NT)
         __pipeline_memcpy_async(slot + L.wt + 4 * q, a.t_gw + ft.woff + 4 * q, 16);
       const int g0 = ty * NG;
-      for (int q = tid; q < NG; q += NT) {
-        if (g0 + q < a.t_ngroups)
-          __pipeline_memcpy_async(slot + L.gt + 4 * q, a.t_g + (size_t)term.t_tab * a.t_ngroups + g0 + q, 16);
+      for (int q = tid; q < 2 * NG; q += NT) {
+        if (g0 + q / 2 < a.t_ngroups)
+          __pipeline_memcpy_async(slot + L.gt + 4 * q, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + g0) + q, 16);
         else
           reinterpret_cast<int4*>(slot + L.gt)[q] = make_int4(0, 0, 0, 0);
       }
@@ -347,93 +365,89 @@ __global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
       __pipeline_wait_prior(0);
     }
     __syncthreads();
-    // ---- pass 1 (s direction, G4): thread = (column group `quad`, rows gsub, gsub+GSTEP, ...)
-    if (!a.s_ident) {
+    // ---- pass 1 (s direction, G4 segments): thread = (column group `quad`, rows gsub, gsub+GSTEP, ...)
+    if (!IDENT) {
       for (int sl = 0; sl < nterm; ++sl) {
         const TermHdr h = hdr[sd][sl];
         if (h.fs_w == 0) continue;
         const float* slot = buf + sl * L.per;
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
-        const int4 gd = reinterpret_cast<const int4*>(slot + L.gs)[quad];
-        const float4* wp0 = reinterpret_cast<const float4*>(slot + L.ws + (gd.z - h.ws_off));
-        const float* xs = STAGE ? slot + L.xs + (gd.x - h.fs_lo)
-                                : a.src + h.src_off + (size_t)h.ft_lo * a.n_is + gd.x;
-        const int pitch = STAGE ? a.fsp : a.n_is;
-        // two rows per step (r0, r0 + GSTEP); staged rows are padded so the second row is always
-        // addressable (its U row, beyond the footprint, is never read by pass 2)
+        const int4* GS = reinterpret_cast<const int4*>(slot + L.gs);
+        const int4 sg0 = GS[2 * quad], sg1 = GS[2 * quad + 1];
+        const int pitch = XS ? a.fsp : a.n_is;
+        const float* xbase = XS ? slot + L.xs - h.fs_lo : a.src + h.src_off + (size_t)h.ft_lo * a.n_is;
+        // two rows per step; staged rows are padded so the second row is always addressable
         for (int r0 = gsub; r0 < h.ft_w; r0 += 2 * GSTEP) {
           float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-          const float* x0 = xs + (size_t)r0 * pitch;
-          const float* x1 = x0 + (size_t)GSTEP * pitch;
-          const bool first_in = STAGE || (h.ft_lo + r0 >= a.win_r0 && h.ft_lo + r0 < a.win_r1);
-          const bool second = STAGE || (r0 + GSTEP < h.ft_w && h.ft_lo + r0 + GSTEP >= a.win_r0 &&
-                                        h.ft_lo + r0 + GSTEP < a.win_r1);
-          const float4* wp = wp0;
+          const bool in0 = XS || (h.ft_lo + r0 >= a.win_r0 && h.ft_lo + r0 < a.win_r1);
+          const bool two = r0 + GSTEP < h.ft_w;
+          const bool in1 = XS || (two && h.ft_lo + r0 + GSTEP >= a.win_r0 && h.ft_lo + r0 + GSTEP < a.win_r1);
+#pragma unroll
+          for (int sgi = 0; sgi < 2; ++sgi) {
+            const int4 sg = sgi ? sg1 : sg0;
+            const float4* wp = reinterpret_cast<const float4*>(slot + L.ws + (sg.z - h.ws_off));
+            const float* x0 = xbase + (size_t)r0 * pitch + sg.x;
+            const float* x1 = x0 + (size_t)GSTEP * pitch;
 #pragma unroll 4
-          for (int p = 0; p < gd.y; ++p) {
-            const float4 w4 = *wp++;
-            const float a0 = STAGE ? *x0 : (first_in ? __ldg(x0) : 0.f);
-            const float a1 = STAGE ? *x1 : (second ? __ldg(x1) : 0.f);
-            ++x0;
-            ++x1;
-            v0.x = fmaf(w4.x, a0, v0.x); v0.y = fmaf(w4.y, a0, v0.y);
-            v0.z = fmaf(w4.z, a0, v0.z); v0.w = fmaf(w4.w, a0, v0.w);
-            v1.x = fmaf(w4.x, a1, v1.x); v1.y = fmaf(w4.y, a1, v1.y);
-            v1.z = fmaf(w4.z, a1, v1.z); v1.w = fmaf(w4.w, a1, v1.w);
+            for (int p = 0; p < sg.y; ++p) {
+              const float4 w4 = wp[p];
+              const float a0 = XS ? x0[p] : (in0 ? __ldg(x0 + p) : 0.f);
+              const float a1 = XS ? x1[p] : (in1 ? __ldg(x1 + p) : 0.f);
+              v0.x = fmaf(w4.x, a0, v0.x); v0.y = fmaf(w4.y, a0, v0.y);
+              v0.z = fmaf(w4.z, a0, v0.z); v0.w = fmaf(w4.w, a0, v0.w);
+              v1.x = fmaf(w4.x, a1, v1.x); v1.y = fmaf(w4.y, a1, v1.y);
+              v1.z = fmaf(w4.z, a1, v1.z); v1.w = fmaf(w4.w, a1, v1.w);
+            }
           }
           v0.x *= h.scale; v0.y *= h.scale; v0.z *= h.scale; v0.w *= h.scale;
           v1.x *= h.scale; v1.y *= h.scale; v1.z *= h.scale; v1.w *= h.scale;
           *reinterpret_cast<float4*>(U + r0 * TS + 4 * quad) = v0;
-          if (STAGE || second) *reinterpret_cast<float4*>(U + (r0 + GSTEP) * TS + 4 * quad) = v1;
+          if (XS || two) *reinterpret_cast<float4*>(U + (r0 + GSTEP) * TS + 4 * quad) = v1;
         }
       }
     }
-    __syncthreads();
-    // ---- pass 2 (t direction, G4): groups of 4 output rows x 4 columns per thread
+    if (MODE != 3) __syncthreads();
+    // ---- pass 2 (t direction, G4 segments): groups of 4 output rows x 4 columns per thread
     for (int sl = 0; sl < nterm; ++sl) {
       const TermHdr h = hdr[sd][sl];
       if (h.fs_w == 0) continue;
       const float* slot = buf + sl * L.per;
-      const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
       const int4* GD = reinterpret_cast<const int4*>(slot + L.gt);
-      const bool ug = a.s_ident && a.ug;
-      const int gcol = os0 + quad * 4;
-      const bool gvec = ug && ((a.n_is & 3) == 0) && ((h.src_off & 3) == 0) && gcol + 3 < a.n_is;
 #pragma unroll
       for (int j = 0; j < GP; ++j) {
-        const int4 gd = GD[gsub + j * GSTEP];
-        const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.wt_off));
-        const float4* up = reinterpret_cast<const float4*>(U + (gd.x - h.ft_lo) * TS + quad * 4);
-        const float* gp = a.src + h.src_off + (size_t)gd.x * a.n_is + gcol;
-        int grow = gd.x;
+        const int gl = gsub + j * GSTEP;
+#pragma unroll
+        for (int sgi = 0; sgi < 2; ++sgi) {
+          const int4 gd = GD[2 * gl + sgi];
+          const float4* wp = reinterpret_cast<const float4*>(slot + L.wt + (gd.z - h.wt_off));
+          if (MODE != 3) {
+            const float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
+            const float4* up = reinterpret_cast<const float4*>(U + (gd.x - h.ft_lo) * TS + quad * 4);
 #pragma unroll 4
-        for (int p = 0; p < gd.y; ++p) {
-          const float4 w4 = *wp++;
-          float4 u4;
-          if (!ug) {
-            u4 = *up;
-            up += TS / 4;
+            for (int p = 0; p < gd.y; ++p) fma4x4(acc[j], wp[p], up[p * (TS / 4)]);
           } else {
-            const bool rin = grow >= a.win_r0 && grow < a.win_r1;
-            if (gvec) {
-              u4 = rin ? __ldg(reinterpret_cast<const float4*>(gp)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-              u4.x = (rin && gcol + 0 < a.n_is) ? __ldg(gp + 0) : 0.f;
-              u4.y = (rin && gcol + 1 < a.n_is) ? __ldg(gp + 1) : 0.f;
-              u4.z = (rin && gcol + 2 < a.n_is) ? __ldg(gp + 2) : 0.f;
-              u4.w = (rin && gcol + 3 < a.n_is) ? __ldg(gp + 3) : 0.f;
+            const int gcol = os0 + quad * 4;
+            const bool gvec = ((a.n_is & 3) == 0) && ((h.src_off & 3) == 0) && gcol + 3 < a.n_is;
+            const float* gp = a.src + h.src_off + (size_t)gd.x * a.n_is + gcol;
+#pragma unroll 4
+            for (int p = 0; p < gd.y; ++p) {
+              const int row = gd.x + p;
+              const bool rin = row >= a.win_r0 && row < a.win_r1;
+              float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (rin) {
+                if (gvec) {
+                  u4 = __ldg(reinterpret_cast<const float4*>(gp + (size_t)p * a.n_is));
+                } else {
+                  const float* q = gp + (size_t)p * a.n_is;
+                  if (gcol + 0 < a.n_is) u4.x = __ldg(q + 0);
+                  if (gcol + 1 < a.n_is) u4.y = __ldg(q + 1);
+                  if (gcol + 2 < a.n_is) u4.z = __ldg(q + 2);
+                  if (gcol + 3 < a.n_is) u4.w = __ldg(q + 3);
+                }
+              }
+              fma4x4(acc[j], wp[p], u4);
             }
-            gp += a.n_is;
-            ++grow;
           }
-          acc[j][0][0] = fmaf(w4.x, u4.x, acc[j][0][0]); acc[j][0][1] = fmaf(w4.x, u4.y, acc[j][0][1]);
-          acc[j][0][2] = fmaf(w4.x, u4.z, acc[j][0][2]); acc[j][0][3] = fmaf(w4.x, u4.w, acc[j][0][3]);
-          acc[j][1][0] = fmaf(w4.y, u4.x, acc[j][1][0]); acc[j][1][1] = fmaf(w4.y, u4.y, acc[j][1][1]);
-          acc[j][1][2] = fmaf(w4.y, u4.z, acc[j][1][2]); acc[j][1][3] = fmaf(w4.y, u4.w, acc[j][1][3]);
-          acc[j][2][0] = fmaf(w4.z, u4.x, acc[j][2][0]); acc[j][2][1] = fmaf(w4.z, u4.y, acc[j][2][1]);
-          acc[j][2][2] = fmaf(w4.z, u4.z, acc[j][2][2]); acc[j][2][3] = fmaf(w4.z, u4.w, acc[j][2][3]);
-          acc[j][3][0] = fmaf(w4.w, u4.x, acc[j][3][0]); acc[j][3][1] = fmaf(w4.w, u4.y, acc[j][3][1]);
-          acc[j][3][2] = fmaf(w4.w, u4.z, acc[j][3][2]); acc[j][3][3] = fmaf(w4.w, u4.w, acc[j][3][3]);
         }
       }
     }
@@ -470,9 +484,9 @@ __global__ void __launch_bounds__(NT, 768 / NT) sep_kernel(SepArgs a) {
   }
 }
 
-template <int TS, int TT, int NT, bool STAGE>
+template <int TS, int TT, int NT, int MODE>
 static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
-  auto kern = sep_kernel<TS, TT, NT, STAGE>;
+  auto kern = sep_kernel<TS, TT, NT, MODE>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -482,6 +496,195 @@ static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStr
   kern<<<grid, NT, smem, s>>>(a);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "sep_kernel launch", err);
+}
+
+// ------------------------------------------------------------------------------------------
+// Streaming t-pass for ops whose s table is the identity (collapsed forward pass 2, adjoint pass 1):
+//   out[4g+q][c] (+)= scale * sum_terms sum_seg sum_p Wt_g[p][q] * src_e[j0 + p][os0 + c]
+// A producer warp streams, per term, the tile's source window rows (one cp.async.bulk per row),
+// the tile's weight block and group descriptors into a STAGES-deep ring of shared-memory slots,
+// completing on an mbarrier (expect_tx); NCW consumer warps wait on the slot's mbarrier, run the
+// 16-FFMA micro-kernel and release the slot on an "empty" mbarrier.  No CTA-wide barriers in the loop.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct StreamHdr {
+  float scale;
+  int ft_lo, ft_w, wt_off, live;
+};
+
+template <int TS, int TT, int NCW, int STAGES>
+__global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
+  constexpr int NCT = NCW * 32;        // consumer threads
+  constexpr int NQ = TS / 4;
+  constexpr int GSTEP = NCT / NQ;
+  constexpr int NG = TT / 4;
+  constexpr int GP = NG / GSTEP;
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NCT % NQ == 0, "tile/thread mismatch");
+  extern __shared__ __align__(16) float smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ StreamHdr hdr[STAGES];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int os0 = tx * TS, ot0 = ty * TT;
+  const int ustride = a.ftm * TS;                      // floats of the U slot
+  const int wstride = (a.wtm + 3) / 4 * 4;
+  const int slot_floats = ustride + wstride + 8 * NG;  // U | weights | 2 int4 descriptors per group
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCW) {
+    // ---------------- producer warp
+    const int ncol = min(TS, a.n_is - os0);
+    const uint32_t row_bytes = (uint32_t)ncol * 4;
+    for (int i = 0; i < e1 - e0; ++i) {
+      const int s = i % STAGES;
+      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+      const Term term = a.terms[e0 + i];
+      const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
+      float* slot = smem + (size_t)s * slot_floats;
+      const bool live = ft.width != 0;
+      const uint32_t bytes = live ? (uint32_t)ft.width * row_bytes + (uint32_t)ft.wlen * 4 + 32u * NG : 0u;
+      if (lane == 0) {
+        hdr[s] = StreamHdr{term.scale, ft.lo, ft.width, ft.woff, live ? 1 : 0};
+        mbar_arrive_expect_tx(&full[s], bytes);
+      }
+      __syncwarp();
+      if (live) {
+        const float* src = a.src + term.src_off + (size_t)ft.lo * a.n_is + os0;
+        for (int r = lane; r < ft.width; r += 32) bulk_g2s(slot + r * TS, src + (size_t)r * a.n_is, row_bytes, &full[s]);
+        if (lane == 0) {
+          bulk_g2s(slot + ustride, a.t_gw + ft.woff, (uint32_t)ft.wlen * 4, &full[s]);
+          bulk_g2s(slot + ustride + wstride, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG), 32u * NG,
+                   &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warps
+  const int quad = tid % NQ, gsub = tid / NQ;
+  float acc[GP][4][4];
+#pragma unroll
+  for (int j = 0; j < GP; ++j)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
+  for (int i = 0; i < e1 - e0; ++i) {
+    const int s = i % STAGES;
+    mbar_wait(&full[s], (i / STAGES) & 1);
+    const StreamHdr h = hdr[s];
+    if (h.live) {
+      const float* slot = smem + (size_t)s * slot_floats;
+      const float* W = slot + ustride;
+      const int4* GD = reinterpret_cast<const int4*>(slot + ustride + wstride);
+#pragma unroll
+      for (int j = 0; j < GP; ++j) {
+        const int gl = gsub + j * GSTEP;
+        float part[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) part[r][c] = 0.f;
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+          const int4 gd = GD[2 * gl + sg];
+          const float4* wp = reinterpret_cast<const float4*>(W + (gd.z - h.wt_off));
+          const float4* up = reinterpret_cast<const float4*>(slot + (gd.x - h.ft_lo) * TS + quad * 4);
+#pragma unroll 4
+          for (int p = 0; p < gd.y; ++p) fma4x4(part, wp[p], up[p * (TS / 4)]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[j][r][c] = fmaf(h.scale, part[r][c], acc[j][r][c]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  float* outb = a.out + (size_t)b * a.out_stride;
+  const int col = os0 + quad * 4;
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
+#pragma unroll
+  for (int j = 0; j < GP; ++j) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+      if (row >= a.n_ot) continue;
+      float* p = outb + (size_t)row * a.n_os + col;
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
+      if (vec) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (a.accumulate) {
+          const float4 q = *reinterpret_cast<float4*>(p);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(p) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          p[c] = a.accumulate ? p[c] + v[c] : v[c];
+        }
+      }
+    }
+  }
+}
+
+template <int TS, int TT, int NCW, int STAGES>
+static lfm_status launch_band_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
+  auto kern = band_t_kernel<TS, TT, NCW, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_t_kernel)", err);
+    configured = true;
+  }
+  kern<<<grid, (NCW + 1) * 32, smem, s>>>(a);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_t_kernel launch", err);
+}
+
+// shared memory of the streaming kernel (must match band_t_kernel's slot layout)
+size_t band_t_smem(const SepOp& op) {
+  size_t slot = (size_t)op.ft_max * op.ts + ((size_t)op.wt_max + 3) / 4 * 4 + 8 * (size_t)(op.tt / 4);
+  return slot * 4 * op.stages;
 }
 
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
@@ -525,13 +728,39 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   const int nty = (r1 + op.tt - 1) / op.tt - a.ty0;
   a.win_r0 = std::max(0, win_r0);
   a.win_r1 = win_r1 < 0 ? op.n_it : std::min(win_r1, op.n_it);
-  const size_t smem = sep_smem(op, op.nb);
   dim3 grid(op.ntx, nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
+  if (op.kind == 1) {
+    // streaming t-pass: identity s, whole windows, 16-byte aligned rows (checked at tuning time)
+    const size_t smem = band_t_smem(op);
+#define LFM_BT_CASE(TS_, TT_, NCW_)                                                                  \
+    if (op.ts == TS_ && op.tt == TT_) {                                                              \
+      switch (op.stages) {                                                                           \
+        case 2: return launch_band_t<TS_, TT_, NCW_, 2>(a, grid, smem, s, err);                      \
+        case 3: return launch_band_t<TS_, TT_, NCW_, 3>(a, grid, smem, s, err);                      \
+        default: return launch_band_t<TS_, TT_, NCW_, 4>(a, grid, smem, s, err);                     \
+      }                                                                                              \
+    }
+    LFM_BT_CASE(128, 64, 8)
+    LFM_BT_CASE(128, 32, 8)
+    LFM_BT_CASE(64, 64, 8)
+    LFM_BT_CASE(64, 32, 4)
+    LFM_BT_CASE(32, 32, 2)
+#undef LFM_BT_CASE
+    err = "unsupported band_t tile";
+    return LFM_E_INVALID;
+  }
+  const size_t smem = sep_smem(op, op.nb);
 #define LFM_SEP_CASE(TS_, TT_, NT_)                                                              \
-  if (op.ts == TS_ && op.tt == TT_)                                                             \
-    return op.stage ? launch_sep_t<TS_, TT_, NT_, true>(a, grid, smem, s, err)                  \
-                    : launch_sep_t<TS_, TT_, NT_, false>(a, grid, smem, s, err);
+  if (op.ts == TS_ && op.tt == TT_) {                                                           \
+    const int mode = op.s_ident ? (op.stage ? 2 : 3) : (op.stage ? 0 : 1);                      \
+    switch (mode) {                                                                             \
+      case 0: return launch_sep_t<TS_, TT_, NT_, 0>(a, grid, smem, s, err);                     \
+      case 1: return launch_sep_t<TS_, TT_, NT_, 1>(a, grid, smem, s, err);                     \
+      case 2: return launch_sep_t<TS_, TT_, NT_, 2>(a, grid, smem, s, err);                     \
+      default: return launch_sep_t<TS_, TT_, NT_, 3>(a, grid, smem, s, err);                    \
+    }                                                                                           \
+  }
   LFM_SEP_CASE(128, 64, 256)
   LFM_SEP_CASE(128, 32, 256)
   LFM_SEP_CASE(64, 64, 128)
@@ -838,8 +1067,11 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       std::fclose(f);
     }
   }
-  SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2};
-  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2"};
+  SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
+                  &cp.fwd_c1, &cp.fwd_c2};
+  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2", "fwd_c1", "fwd_c2"};
+  float op_best[9];
+  for (float& v : op_best) v = -1.f;
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
   size_t src_n = 0, out_n = 0;
   for (SepOp* op : ops) {
@@ -862,7 +1094,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   cudaEventCreate(&e1);
   const int cand[][3] = {{128, 64, 256}, {128, 32, 256}, {64, 64, 128}, {64, 32, 128}, {32, 32, 64}};
   lfm_status st = LFM_OK;
-  for (int q = 0; q < 7 && st == LFM_OK; ++q) {
+  for (int q = 0; q < 9 && st == LFM_OK; ++q) {
     SepOp& op = *ops[q];
     if (!op.fs) continue;
     if (std::getenv((std::string("LFM_FORCE_") + names[q]).c_str())) continue;  // explicit override wins
@@ -870,9 +1102,10 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     for (const std::string& ln : cached) {
       char k[128], o[32];
       int ts, tt, nt, nb, stg;
-      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d", k, o, &ts, &tt, &nt, &nb, &stg) == 7 && key == k &&
-          std::string(o) == names[q]) {
-        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg;
+      int kind = 0, stages = 2;
+      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages) >= 7 &&
+          key == k && std::string(o) == names[q]) {
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
         fill_sep_geometry(op);
         free_sep_dev(op);
         size_t bytes = 0;
@@ -885,6 +1118,36 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     const SepOp keep = op;  // cost-model choice (device pointers of `op` are replaced below)
     int bts = keep.ts, btt = keep.tt, bnt = keep.nt, bnb = keep.nb, bst = keep.stage;
     float best = 1e30f;
+    int bkind = keep.kind, bstages = keep.stages;
+    if (op.s_ident && (op.n_is % 4) == 0) {
+      for (auto& c : cand) {
+        for (int stages : {2, 3, 4}) {
+          op.kind = 1; op.ts = c[0]; op.tt = c[1]; op.stages = stages; op.nb = 1; op.stage = 1;
+          op.nt = c[0] == 32 ? 96 : (c[0] == 64 && c[1] == 32 ? 160 : 288);
+          fill_sep_geometry(op);
+          bool aligned = true;
+          for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
+          if (!aligned || band_t_smem(op) > (size_t)200 * 1024) continue;
+          free_sep_dev(op);
+          size_t bytes = 0;
+          if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+          float ms = 0, tot = 0;
+          bool ok = true;
+          for (int rep = 0; rep < 3 && ok; ++rep) {
+            cudaEventRecord(e0, 0);
+            ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+            cudaEventRecord(e1, 0);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) tot += ms;
+          }
+          if (!ok || cudaGetLastError() != cudaSuccess) continue;
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = op.nt; bnb = 1; bst = 1; bkind = 1; bstages = stages; }
+        }
+        if (st != LFM_OK) break;
+      }
+      op.kind = 0;
+    }
     for (auto& c : cand) {
       for (int stage : {1, 0}) {
         for (int nb : {1, 2, 4}) {
@@ -906,23 +1169,25 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
             if (rep > 0) tot += ms;
           }
           if (!ok || cudaGetLastError() != cudaSuccess) continue;
-          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = nb; bst = stage; }
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = nb; bst = stage; bkind = 0; }
         }
         if (st != LFM_OK) break;
       }
       if (st != LFM_OK) break;
     }
-    op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst;
+    op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst; op.kind = bkind; op.stages = bstages;
     fill_sep_geometry(op);
     free_sep_dev(op);
     size_t bytes = 0;
     if (st == LFM_OK) st = upload_sep(op, bytes, err);
+    op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
-      std::fprintf(stderr, "[lfm] autotune %-7s -> tile %3dx%-3d nt %3d nb %d stage %d  (%.3f ms for %d outputs)\n",
-                   names[q], op.ts, op.tt, op.nt, op.nb, op.stage, best / 2, n_out);
+      std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d (%.3f ms for %d outputs)\n",
+                   names[q], op.kind ? "band_t" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
-        std::fprintf(f, "%s %s %d %d %d %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage);
+        std::fprintf(f, "%s %s %d %d %d %d %d %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
+                     op.kind, op.stages);
         std::fclose(f);
       }
     }
@@ -931,6 +1196,10 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   cudaEventDestroy(e1);
   dfree(src);
   dfree(out);
+  // forward order: fused (fwd_c) or two passes (fwd_c1 + fwd_c2), whichever timed faster
+  if (op_best[4] > 0 && op_best[7] > 0 && op_best[8] > 0) cp.fwd_split = (op_best[7] + op_best[8]) < op_best[4];
+  if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
+  if (dbg) std::fprintf(stderr, "[lfm] collapsed forward: %s\n", cp.fwd_split ? "two passes" : "fused");
   return st;
 }
 }  // namespace lfm

@@ -81,6 +81,8 @@ struct SepOp {
   int nb = 1;                      // terms staged per barrier
   int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
+  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s)
+  int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile
   int nbuf = 2;                    // 2: double-buffered chunks, 1: one chunk per output
@@ -108,7 +110,9 @@ struct CameraPlan {
   // A_forward / A_adjoint ops, per path
   SepOp fwd_s1, fwd_s3, adj_s3, adj_s1;   // per-view path
   SepOp fwd_c, adj_c1, adj_c2;            // collapsed path (adjoint in two passes: t then s)
-  BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint
+  SepOp fwd_c1, fwd_c2;                   // collapsed forward in two passes: s (U_n for all n), then t
+  int fwd_split = 0;                      // 1: forward uses fwd_c1 + fwd_c2 (chosen by the autotuner)
+  BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint/forward
   // lf_transport ops (output b = n*K + k for slice-indexed families)
   SepOp xp_s1f, xp_s1a, xp_s3f, xp_s3a;
   ShearPass rot[3];                       // application order z, x, y (x^r = E^y E^x E^z x)
@@ -129,6 +133,7 @@ namespace lfm {
 void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width);
 void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen);
 size_t sep_smem(const SepOp& op, int nb);
+size_t band_t_smem(const SepOp& op);
 void fill_sep_geometry(SepOp& op);
 bool sep_choose_tile(SepOp& op);
 lfm_status autotune_camera(CameraPlan& cp, std::string& err);

@@ -197,14 +197,16 @@ static void build_ell(BandFamily& f) {
       }
       for (; e < f.ell; ++e) f.eidx[m * per + (size_t)e * f.n_rows + r] = first;  // zero-weight padding
     }
-  // G4 form: groups of 4 consecutive rows, union window of their bands, dense row-interleaved weights
+  // G4 form: groups of 4 consecutive rows; the union window of their bands is split at its longest
+  // all-zero run (if any) into at most two segments; dense row-interleaved weights per segment
   f.n_groups = (f.n_rows + 3) / 4;
   size_t ng = (size_t)f.n_tables * f.n_groups;
-  f.g_j0.assign(ng, 0);
-  f.g_w.assign(ng, 0);
-  f.g_off.assign(ng, 0);
+  f.g_j0.assign(2 * ng, 0);
+  f.g_w.assign(2 * ng, 0);
+  f.g_off.assign(2 * ng, 0);
   f.g_w64.clear();
   f.gmax = 0;
+  std::vector<double> dense;
   for (int m = 0; m < f.n_tables; ++m)
     for (int g = 0; g < f.n_groups; ++g) {
       int lo = 1 << 30, hi = -1;
@@ -217,23 +219,41 @@ static void build_ell(BandFamily& f) {
         hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
       }
       size_t gi = (size_t)m * f.n_groups + g;
-      f.g_off[gi] = (int)f.g_w64.size();
+      f.g_off[2 * gi] = f.g_off[2 * gi + 1] = (int)f.g_w64.size();
       if (hi < 0) continue;
-      int W = hi - lo;
-      f.g_j0[gi] = lo;
-      f.g_w[gi] = W;
-      f.gmax = std::max(f.gmax, W);
-      size_t base = f.g_w64.size();
-      f.g_w64.resize(base + (size_t)W * 4, 0.0);
+      const int W = hi - lo;
+      dense.assign((size_t)W * 4, 0.0);
       for (int q = 0; q < 4; ++q) {
         int r = 4 * g + q;
         if (r >= f.n_rows) break;
         size_t idx = (size_t)m * f.n_rows + r;
-        for (int e = 0; e < f.len[idx]; ++e) {
-          int j = f.start[idx] + e;
-          f.g_w64[base + (size_t)(j - lo) * 4 + q] = f.w64[idx * f.taps + e];
-        }
+        for (int e = 0; e < f.len[idx]; ++e)
+          dense[(size_t)(f.start[idx] + e - lo) * 4 + q] = f.w64[idx * f.taps + e];
       }
+      // longest run of all-zero columns strictly inside the window
+      int best_a = -1, best_len = 0;
+      for (int p = 0; p < W;) {
+        bool z = dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 && dense[4 * p + 3] == 0.0;
+        if (!z) { ++p; continue; }
+        int a = p;
+        while (p < W && dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 && dense[4 * p + 3] == 0.0) ++p;
+        if (a > 0 && p < W && p - a > best_len) { best_len = p - a; best_a = a; }
+      }
+      int segs[2][2] = {{0, W}, {0, 0}};  // [start, end) within the window
+      if (best_len > 0) {
+        segs[0][1] = best_a;
+        segs[1][0] = best_a + best_len;
+        segs[1][1] = W;
+      }
+      for (int sgi = 0; sgi < 2; ++sgi) {
+        int a = segs[sgi][0], b = segs[sgi][1];
+        f.g_j0[2 * gi + sgi] = lo + a;
+        f.g_w[2 * gi + sgi] = b - a;
+        f.g_off[2 * gi + sgi] = (int)f.g_w64.size();
+        for (int p = a; p < b; ++p)
+          for (int q = 0; q < 4; ++q) f.g_w64.push_back(dense[4 * p + q]);
+      }
+      f.gmax = std::max(f.gmax, W);
     }
 }
 
@@ -241,15 +261,16 @@ static void build_ell(BandFamily& f) {
 void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen) {
   int g0 = t * tile / 4, g1 = std::min(f.n_groups, (t + 1) * tile / 4);
   int mn = 1 << 30, mx = -1;
-  for (int g = g0; g < g1; ++g) {
-    size_t gi = (size_t)tab * f.n_groups + g;
-    if (!f.g_w[gi]) continue;
-    mn = std::min(mn, (int)f.g_j0[gi]);
-    mx = std::max(mx, (int)(f.g_j0[gi] + f.g_w[gi]));
-  }
-  woff = g0 < f.n_groups ? f.g_off[(size_t)tab * f.n_groups + g0] : 0;
-  int end = (g1 < f.n_groups) ? f.g_off[(size_t)tab * f.n_groups + g1]
-                              : (tab + 1 < f.n_tables ? f.g_off[(size_t)(tab + 1) * f.n_groups] : (int)f.g_w64.size());
+  for (int g = g0; g < g1; ++g)
+    for (int sgi = 0; sgi < 2; ++sgi) {
+      size_t gi = 2 * ((size_t)tab * f.n_groups + g) + sgi;
+      if (!f.g_w[gi]) continue;
+      mn = std::min(mn, (int)f.g_j0[gi]);
+      mx = std::max(mx, (int)(f.g_j0[gi] + f.g_w[gi]));
+    }
+  woff = g0 < f.n_groups ? f.g_off[2 * ((size_t)tab * f.n_groups + g0)] : 0;
+  int end = (g1 < f.n_groups) ? f.g_off[2 * ((size_t)tab * f.n_groups + g1)]
+                              : (tab + 1 < f.n_tables ? f.g_off[2 * ((size_t)(tab + 1) * f.n_groups)] : (int)f.g_w64.size());
   wlen = end - woff;
   if (mx < 0) { lo = 0; width = 0; return; }
   lo = mn;
@@ -496,7 +517,7 @@ size_t sep_smem(const SepOp& op, int nb) {
   // staged rows padded by one pass-1 row stride (the kernel reads two rows per step unconditionally)
   size_t gstep = (size_t)op.nt / (op.ts / 4);
   size_t x = (op.s_ident || !op.stage) ? 0 : r4(((size_t)op.ft_max + gstep) * fsp);
-  size_t per = x + r4(op.ws_max) + op.ts + r4(op.wt_max) + op.tt;
+  size_t per = x + r4(op.ws_max) + 2 * (size_t)op.ts + r4(op.wt_max) + 2 * (size_t)op.tt;
   size_t urows = (size_t)op.ft_max + gstep;  // U rows padded likewise
   size_t maxt = 0;
   for (size_t b = 0; b + 1 < op.offs.size(); ++b) maxt = std::max(maxt, (size_t)(op.offs[b + 1] - op.offs[b]));
@@ -903,6 +924,16 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     sep_add(cp.adj_c1, 0, 0, n, 1.f);
     sep_close_output(cp.adj_c1);
   }
+  // collapsed forward in two passes: U_n = X_n C_{s,n}^T (all slices, t identity), then y = sum_n C_{t,n} U_n
+  sep_init(cp.fwd_c1, &cp.cf[0], &cp.id_vt, nx, ny, nz, 1.f);
+  for (int n = 0; n < nz; ++n) {
+    sep_add(cp.fwd_c1, n * nslice, n, 0, 1.f);
+    sep_close_output(cp.fwd_c1);
+  }
+  sep_init(cp.fwd_c2, &cp.id_s, &cp.cf[1], ndet[0], ny, 1, (float)(c1 * c3));
+  cp.fwd_c2.s_ident = 1;
+  for (int n = 0; n < nz; ++n) sep_add(cp.fwd_c2, (long long)n * ny * ndet[0], 0, n, 1.f);
+  sep_close_output(cp.fwd_c2);
   sep_init(cp.adj_c2, &cp.ca[0], &cp.id_vt, ndet[0], ny, nz, (float)(c1 * c3));
   for (int n = 0; n < nz; ++n) {
     sep_add(cp.adj_c2, (long long)n * ny * ndet[0], n, 0, 1.f);
@@ -941,11 +972,11 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     }
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
   const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2",
-                         "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a"};
+                         "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a", "fwd_c1", "fwd_c2"};
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
-  for (int q = 0; q < 11; ++q) {
+  for (int q = 0; q < 13; ++q) {
     if (!ops[q]->fs) continue;
     if (!sep_choose_tile(*ops[q])) {
       err = std::string("source footprint of op ") + names[q] + " exceeds shared memory";
