@@ -575,19 +575,33 @@ __global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
       const Term term = a.terms[e0 + i];
       const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
       float* slot = smem + (size_t)s * slot_floats;
-      const bool live = ft.width != 0;
-      const uint32_t bytes = live ? (uint32_t)ft.width * row_bytes + (uint32_t)ft.wlen * 4 + 32u * NG : 0u;
+      // source rows outside [win_r0, win_r1) count as zero (adjoint detector-row sharding)
+      const int wlo = max(ft.lo, a.win_r0), whi = min(ft.lo + ft.width, a.win_r1);
+      const bool live = ft.width != 0 && whi > wlo;
+      const int ngt = min(NG, a.t_ngroups - ty * NG);  // descriptors that exist for this tile
+      const uint32_t bytes =
+          live ? (uint32_t)(whi - wlo) * row_bytes + (uint32_t)ft.wlen * 4 + 32u * ngt : 0u;
+      if (live && (wlo > ft.lo || whi < ft.lo + ft.width)) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = ft.lo; r < ft.lo + ft.width; ++r) {
+          if (r >= wlo && r < whi) continue;
+          for (int c = lane; c < TS / 4; c += 32) reinterpret_cast<float4*>(slot + (r - ft.lo) * TS)[c] = z;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      __syncwarp();
       if (lane == 0) {
         hdr[s] = StreamHdr{term.scale, ft.lo, ft.width, ft.woff, live ? 1 : 0};
         mbar_arrive_expect_tx(&full[s], bytes);
       }
       __syncwarp();
       if (live) {
-        const float* src = a.src + term.src_off + (size_t)ft.lo * a.n_is + os0;
-        for (int r = lane; r < ft.width; r += 32) bulk_g2s(slot + r * TS, src + (size_t)r * a.n_is, row_bytes, &full[s]);
+        const float* src = a.src + term.src_off + (size_t)wlo * a.n_is + os0;
+        float* dst = slot + (wlo - ft.lo) * TS;
+        for (int r = lane; r < whi - wlo; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.n_is, row_bytes, &full[s]);
         if (lane == 0) {
           bulk_g2s(slot + ustride, a.t_gw + ft.woff, (uint32_t)ft.wlen * 4, &full[s]);
-          bulk_g2s(slot + ustride + wstride, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG), 32u * NG,
+          bulk_g2s(slot + ustride + wstride, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG), 32u * ngt,
                    &full[s]);
         }
       }
@@ -614,6 +628,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
 #pragma unroll
       for (int j = 0; j < GP; ++j) {
         const int gl = gsub + j * GSTEP;
+        if (ty * NG + gl >= a.t_ngroups) continue;
         float part[4][4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -665,6 +680,94 @@ __global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
       }
     }
   }
+}
+
+// L2-gather t-pass for identity-s ops: no shared memory and no barriers.  Thread = (4 source columns,
+// GP groups of 4 output rows); per term and segment a branch-free loop over the segment's source rows
+// [gd.x, gd.x + gd.y) clipped once to the row window, loading u (16 B) and the 4 weights (16 B, L1-resident)
+// per row with a deep unroll so that many L2 requests are in flight per warp.
+template <int TS, int TT, int NT, int UNR>
+__global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
+  constexpr int NQ = TS / 4;
+  constexpr int GSTEP = NT / NQ;
+  constexpr int NG = TT / 4;
+  constexpr int GP = NG / GSTEP;
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
+  const int tid = threadIdx.x;
+  const int quad = tid % NQ, gsub = tid / NQ;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int os0 = tx * TS, ot0 = ty * TT;
+  const int col = os0 + quad * 4;
+  const bool col_ok = col < a.n_is;  // n_is % 4 == 0 (checked at tuning time): whole quads in or out
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  float acc[GP][4][4];
+#pragma unroll
+  for (int j = 0; j < GP; ++j)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
+  if (col_ok) {
+    for (int e = e0; e < e1; ++e) {
+      const Term term = a.terms[e];
+      const float* src = a.src + term.src_off + col;
+      const int4* GD = reinterpret_cast<const int4*>(a.t_g) + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG);
+#pragma unroll
+      for (int j = 0; j < GP; ++j) {
+        const int gl = gsub + j * GSTEP;
+        if (ty * NG + gl >= a.t_ngroups) continue;
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+          const int4 gd = __ldg(GD + 2 * gl + sg);
+          const int p0 = max(0, a.win_r0 - gd.x), p1 = min(gd.y, a.win_r1 - gd.x);
+          const float4* wp = reinterpret_cast<const float4*>(a.t_gw + gd.z);
+          const float* up = src + (size_t)gd.x * a.n_is;
+#pragma unroll UNR
+          for (int p = p0; p < p1; ++p)
+            fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.n_is)));
+        }
+      }
+    }
+  }
+  if (!col_ok) return;
+  float* outb = a.out + (size_t)b * a.out_stride;
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
+#pragma unroll
+  for (int j = 0; j < GP; ++j) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+      if (row >= a.n_ot) continue;
+      float* p = outb + (size_t)row * a.n_os + col;
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
+      if (vec) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (a.accumulate) {
+          const float4 q = *reinterpret_cast<float4*>(p);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(p) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          p[c] = a.accumulate ? p[c] + v[c] : v[c];
+        }
+      }
+    }
+  }
+}
+
+template <int TS, int TT, int NT>
+static lfm_status launch_band_g(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr) {
+  if (unr == 8)
+    band_g_kernel<TS, TT, NT, 8><<<grid, NT, 0, s>>>(a);
+  else
+    band_g_kernel<TS, TT, NT, 4><<<grid, NT, 0, s>>>(a);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_g_kernel launch", err);
 }
 
 template <int TS, int TT, int NCW, int STAGES>
@@ -748,6 +851,20 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     LFM_BT_CASE(32, 32, 2)
 #undef LFM_BT_CASE
     err = "unsupported band_t tile";
+    return LFM_E_INVALID;
+  }
+  if (op.kind == 2) {
+    // L2-gather t-pass: identity s, no shared memory
+#define LFM_BG_CASE(TS_, TT_, NT_) \
+    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_g<TS_, TT_, NT_>(a, grid, s, err, op.stages);
+    LFM_BG_CASE(128, 32, 256)
+    LFM_BG_CASE(128, 64, 256)
+    LFM_BG_CASE(128, 16, 128)
+    LFM_BG_CASE(64, 32, 128)
+    LFM_BG_CASE(64, 64, 256)
+    LFM_BG_CASE(32, 32, 64)
+#undef LFM_BG_CASE
+    err = "unsupported band_g tile";
     return LFM_E_INVALID;
   }
   const size_t smem = sep_smem(op, op.nb);
@@ -1050,7 +1167,8 @@ static std::string tune_key(const CameraPlan& cp) {
   unsigned long long h = 1469598103934665603ull;
   for (size_t i = 0; i < sizeof(cp.cam); ++i) h = (h ^ b[i]) * 1099511628211ull;
   char buf[96];
-  std::snprintf(buf, sizeof(buf), "%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
+  // v4: the line format carries kernel kind, pipeline stages and the timed ms; older caches are ignored
+  std::snprintf(buf, sizeof(buf), "v4_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
   return buf;
 }
 
@@ -1103,9 +1221,12 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       char k[128], o[32];
       int ts, tt, nt, nb, stg;
       int kind = 0, stages = 2;
-      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages) >= 7 &&
+      float ms = 0;
+      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d %f", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages,
+                      &ms) == 10 &&
           key == k && std::string(o) == names[q]) {
         op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
+        op_best[q] = ms;
         fill_sep_geometry(op);
         free_sep_dev(op);
         size_t bytes = 0;
@@ -1147,6 +1268,33 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         if (st != LFM_OK) break;
       }
       op.kind = 0;
+      const int gcand[][3] = {{128, 32, 256}, {128, 64, 256}, {128, 16, 128}, {64, 32, 128}, {64, 64, 256}, {32, 32, 64}};
+      for (auto& c : gcand) {
+        if (st != LFM_OK) break;
+        bool aligned = true;
+        for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
+        if (!aligned) break;
+        for (int unr : {4, 8}) {
+        op.kind = 2; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr;
+        fill_sep_geometry(op);
+        free_sep_dev(op);
+        size_t bytes = 0;
+        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+        float ms = 0, tot = 0;
+        bool ok = true;
+        for (int rep = 0; rep < 3 && ok; ++rep) {
+          cudaEventRecord(e0, 0);
+          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+          cudaEventRecord(e1, 0);
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (rep > 0) tot += ms;
+        }
+        if (!ok || cudaGetLastError() != cudaSuccess) continue;
+        if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 2; bstages = unr; }
+        }
+      }
+      op.kind = 0;
     }
     for (auto& c : cand) {
       for (int stage : {1, 0}) {
@@ -1183,11 +1331,11 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind ? "band_t" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
-        std::fprintf(f, "%s %s %d %d %d %d %d %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
-                     op.kind, op.stages);
+        std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
+                     op.kind, op.stages, op_best[q]);
         std::fclose(f);
       }
     }

@@ -45,6 +45,8 @@ struct BandFamily {
   std::vector<double> g_w64;              // flat, per table contiguous
   int32_t* d_g = nullptr;                 // int4 per [table][group]: j0, W, off, 0
   float* d_gw = nullptr;
+  // density statistics (LFM_DEBUG): non-zeros, G4 slot columns, columns with any non-zero
+  double st_nnz = 0, st_cols_g4 = 0, st_cols_nz = 0;
 };
 
 // One summand of a separable banded sum: source plane at src_base + src_off, s/t table indices.
@@ -81,7 +83,7 @@ struct SepOp {
   int nb = 1;                      // terms staged per barrier
   int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
-  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s)
+  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s), 2: band_g_kernel (L2 gather)
   int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile

@@ -254,6 +254,12 @@ static void build_ell(BandFamily& f) {
           for (int q = 0; q < 4; ++q) f.g_w64.push_back(dense[4 * p + q]);
       }
       f.gmax = std::max(f.gmax, W);
+      for (int p = 0; p < W; ++p) {
+        bool z = dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 && dense[4 * p + 3] == 0.0;
+        f.st_cols_nz += !z;
+        for (int q = 0; q < 4; ++q) f.st_nnz += dense[4 * p + q] != 0.0;
+      }
+      f.st_cols_g4 += segs[0][1] - segs[0][0] + segs[1][1] - segs[1][0];
     }
 }
 
@@ -976,6 +982,15 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2",
                          "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a", "fwd_c1", "fwd_c2"};
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
+  if (dbg) {
+    const BandFamily* fams[] = {&cp.s1f[0], &cp.s1f[1], &cp.s1a[0], &cp.s1a[1], &cp.s3f[0], &cp.s3f[1],
+                                &cp.s3a[0], &cp.s3a[1], &cp.cf[0],  &cp.cf[1],  &cp.ca[0],  &cp.ca[1]};
+    const char* fn[] = {"s1f0", "s1f1", "s1a0", "s1a1", "s3f0", "s3f1", "s3a0", "s3a1", "cf0", "cf1", "ca0", "ca1"};
+    for (int i = 0; i < 12; ++i)
+      if (fams[i]->st_cols_g4 > 0)
+        std::fprintf(stderr, "[lfm] family %-4s G4 density %.3f  (any-nonzero columns only: %.3f)\n", fn[i],
+                     fams[i]->st_nnz / (4 * fams[i]->st_cols_g4), fams[i]->st_nnz / (4 * fams[i]->st_cols_nz));
+  }
   for (int q = 0; q < 13; ++q) {
     if (!ops[q]->fs) continue;
     if (!sep_choose_tile(*ops[q])) {
@@ -985,12 +1000,20 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     // tuning hook: LFM_FORCE_<op>=ts,tt,nt,nb,stage overrides the cost model (sweeps, tools/)
     std::string env = std::string("LFM_FORCE_") + names[q];
     if (const char* f = std::getenv(env.c_str())) {
-      int ts, tt, nt, nb, stg;
-      if (std::sscanf(f, "%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg) == 5) {
+      // optional 6th/7th fields: kind (1 = streaming band_t kernel, identity-s ops only), stages
+      int ts, tt, nt, nb, stg, kind = 0, stages = 2;
+      if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages) >= 5) {
         SepOp& op = *ops[q];
-        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg;
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
         fill_sep_geometry(op);
-        if (sep_smem(op, nb) > (size_t)220 * 1024) { err = env + ": shared memory too large"; return LFM_E_INVALID; }
+        if (kind == 1 || kind == 2) {
+          bool ok = op.s_ident && op.n_is % 4 == 0 && (kind == 2 || band_t_smem(op) <= (size_t)200 * 1024);
+          for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
+          if (!ok) { err = env + ": band_t not applicable"; return LFM_E_INVALID; }
+        } else if (sep_smem(op, nb) > (size_t)220 * 1024) {
+          err = env + ": shared memory too large";
+          return LFM_E_INVALID;
+        }
       }
     }
     if (dbg)

@@ -12,7 +12,7 @@ from workloads import make_config, normal_vector, uniform_vector, uniform_volume
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "small_two", "ragged"]
+SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "small_two", "ragged"]
 PATHS = [0, 1]  # PER_VIEW, COLLAPSED
 
 

@@ -1,0 +1,88 @@
+"""GPU parity of the detector-row entry points (lfm_A_forward_rows / lfm_A_adjoint_rows, the calls the
+multi-GPU partition and bench.py use) and of every kernel variant the autotuner may pick for the
+streamed t-pass ops, forced one at a time through LFM_FORCE_<op> (so the parity does not depend on
+which variant wins the timing on a given box).  Oracle: fp64, element by element, tolerance 1e-5."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.system import build_system
+from tests.gpu_helpers import TOL, dev, host, max_rel, setup
+from workloads import make_config, uniform_vector, uniform_volume
+
+pytestmark = pytest.mark.gpu
+
+
+def _masked_rows(r, n_t, r0, r1):
+    rr = r.reshape(n_t, -1).copy()
+    rr[:r0] = 0.0
+    rr[r1:] = 0.0
+    return rr.ravel()
+
+
+@pytest.mark.parametrize("name", ["small_two", "tiny_multi"])
+@pytest.mark.parametrize("path", [0, 1])
+def test_rows_entry_points(name, path):
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = setup(name)
+    x = uniform_volume(cfg["volume"], 0)
+    for c, op in enumerate(ops):
+        n_t = cfg["cameras"][c]["n_t"]
+        cuts = [0, n_t // 3 + 1, (2 * n_t) // 3 - 1, n_t]   # ragged, not multiples of any tile
+        yref = op.forward(x.astype(np.float64)).reshape(n_t, -1)
+        y = torch.full((op.n_pix,), float("nan"), device="cuda:0")
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            lfm.A_forward_rows(plan, c, r0, r1, dev(x), y, ws, path=path)
+            got = host(y).reshape(n_t, -1)[r0:r1]
+            assert max_rel(got, yref[r0:r1]) <= TOL * np.abs(yref).max() / np.abs(yref[r0:r1]).max()
+        r = uniform_vector(op.n_pix, 1)
+        g = torch.empty(op.n_vox, device="cuda:0")
+        for i, (r0, r1) in enumerate(zip(cuts[:-1], cuts[1:])):
+            lfm.A_adjoint_rows(plan, c, r0, r1, dev(r), g, ws, accumulate=i > 0, path=path)
+            if i == 0:
+                part = op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))
+                assert max_rel(host(g), part) <= TOL
+        assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL
+
+
+# band_t: ts,tt,nt,nb,stage,kind=1,stages ; band_g: kind=2, last field = unroll ;
+# sep: MODE variants (stage 1 = staged U, 0 = U from L2)
+VARIANTS = {
+    "band_t_128x64_s4": "128,64,288,1,1,1,4",
+    "band_t_128x32_s2": "128,32,288,1,1,1,2",
+    "band_t_64x64_s3": "64,64,288,1,1,1,3",
+    "band_t_64x32_s2": "64,32,160,1,1,1,2",
+    "band_t_32x32_s4": "32,32,96,1,1,1,4",
+    "band_g_128x32_u8": "128,32,256,1,0,2,8",
+    "band_g_64x32_u4": "64,32,128,1,0,2,4",
+    "band_g_128x64_u4": "128,64,256,1,0,2,4",
+    "sep_128x64_staged": "128,64,256,1,1",
+    "sep_64x32_l2": "64,32,128,1,0",
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_forced_t_pass_variants(variant, monkeypatch):
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config("small_two")
+    monkeypatch.setenv("LFM_FORCE_fwd_c2", VARIANTS[variant])
+    monkeypatch.setenv("LFM_FORCE_adj_c1", VARIANTS[variant])
+    monkeypatch.setenv("LFM_FWD_SPLIT", "1")
+    monkeypatch.delenv("LFM_TUNE_FILE", raising=False)
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    ops = build_system(cfg)
+    x = uniform_volume(cfg["volume"], 0)
+    for c, op in enumerate(ops):
+        n_t = cfg["cameras"][c]["n_t"]
+        y = torch.empty(op.n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, dev(x), y, ws, path=1)
+        assert max_rel(host(y), op.forward(x.astype(np.float64))) <= TOL, (variant, c)
+        r = uniform_vector(op.n_pix, 1)
+        g = torch.empty(op.n_vox, device="cuda:0")
+        lfm.A_adjoint(plan, c, dev(r), g, ws, path=1)
+        assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL, (variant, c)
+        # windowed source rows (adjoint row sharding) through the same kernel
+        r0, r1 = n_t // 4 + 1, (3 * n_t) // 4
+        lfm.A_adjoint_rows(plan, c, r0, r1, dev(r), g, ws, path=1)
+        assert max_rel(host(g), op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))) <= TOL, (variant, c)

@@ -19,7 +19,7 @@ from workloads.geometry import plenoptic_camera, pose_yaw, pose_yaw_pitch, singl
 
 lfm = pytest.importorskip("paper_1812_03358_b200.lfm")
 
-CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "small_two"]
+CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "small_two"]
 
 
 def ragged_config():
@@ -109,7 +109,7 @@ def test_band_tables_bit_exact(name):
                     _weights_match(plan, c, "S3A", ax, k, cam.S3[ax][k].toarray().T, rel=1e-10)
 
 
-@pytest.mark.parametrize("name", ["tiny", "tiny_single", "small_two", "ragged"])
+@pytest.mark.parametrize("name", ["tiny", "tiny_single", "tiny_dirac", "small_two", "ragged"])
 def test_collapsed_composite_tables(name):
     """C_n = sum_k S_k B_{k,n} per axis (exact re-association over the tensor angular grid)."""
     cfg = _cfg(name)
