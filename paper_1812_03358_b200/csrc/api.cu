@@ -169,7 +169,7 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   int acc = rot ? 0 : accumulate;
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
-    TRY(sep(cp.adj_c1, y, w.z, 0, cp.info.nz, 0, stream, 0, -1, r0, r1));
+    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1));  // one output: all (vt, n) rows
     TRY(sep(cp.adj_c2, w.z, target, 0, cp.info.nz, acc, stream));
   } else if (plen) {
     TRY(sep(cp.adj_s3, y, w.f, 0, cp.info.n_views, 0, stream, 0, -1, r0, r1));

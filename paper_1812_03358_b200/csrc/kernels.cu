@@ -76,6 +76,14 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
   for (size_t i = 0; i < f.g_w64.size(); ++i) gw[i] = (float)f.g_w64[i];
   if ((st = dev_upload(&f.d_g, g4.data(), g4.size() * 4, err)) != LFM_OK) return st;
   bytes += cn.size() * 4 + ix.size() * 4 + w32.size() * 4 + g4.size() * 4 + gw.size() * 4;
+  if (f.want_mseg) {
+    std::vector<float> mw(f.m_w64.size() + 4);
+    for (size_t i = 0; i < f.m_w64.size(); ++i) mw[i] = (float)f.m_w64[i];  // one rounding, like every table
+    if ((st = dev_upload(&f.d_moff, f.m_off.data(), f.m_off.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_mseg, f.m_seg.data(), f.m_seg.size() * 4 + 16, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_mw, mw.data(), mw.size() * 4, err)) != LFM_OK) return st;
+    bytes += f.m_off.size() * 4 + f.m_seg.size() * 4 + mw.size() * 4;
+  }
   return dev_upload(&f.d_gw, gw.data(), gw.size() * 4, err);
 }
 
@@ -116,7 +124,7 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
     for (BandFamily* f : fams)
       if ((st = upload_family(*f, bytes, err)) != LFM_OK) return st;
   }
-  for (BandFamily* f : {&cp.id_s, &cp.id_t, &cp.id_vt})
+  for (BandFamily* f : {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n})
     if ((st = upload_family(*f, bytes, err)) != LFM_OK) return st;
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
@@ -142,13 +150,15 @@ static void dfree(void* p) {
 }
 
 void free_camera(CameraPlan& cp) {
-  std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt};
+  std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
   for (int ax = 0; ax < 2; ++ax)
     for (BandFamily* f : {&cp.s1f[ax], &cp.s1a[ax], &cp.s3f[ax], &cp.s3a[ax], &cp.cf[ax], &cp.ca[ax]})
       fams.push_back(f);
   for (BandFamily* f : fams) {
     dfree(f->d_cnt); dfree(f->d_idx); dfree(f->d_w); dfree(f->d_g); dfree(f->d_gw);
+    dfree(f->d_moff); dfree(f->d_mseg); dfree(f->d_mw);
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
+    f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
@@ -180,6 +190,11 @@ struct SepArgs {
   const float* src;
   float* out;
   long long out_stride;
+  long long src_pitch;  // floats between source rows
+  long long out_pitch;  // floats between output rows
+  const int32_t* t_moff;  // MSEG t family (band_m_kernel)
+  const int4* t_mseg;
+  const float* t_mw;
   const Term* terms;
   const int32_t* offs;  // already offset by b0
   const int4* s_g;
@@ -301,17 +316,17 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const float* src = a.src + term.src_off + os0;
         const int ncol = min(TS, a.n_is - os0);
-        if (((a.n_is & 3) == 0) && ((term.src_off & 3) == 0) && ncol == TS && !windowed) {
+        if (((a.n_is & 3) == 0) && ((a.src_pitch & 3) == 0) && ((term.src_off & 3) == 0) && ncol == TS && !windowed) {
           for (int q = tid; q < ft.width * NQ; q += NT) {
             const int r = q / NQ, c4 = q - r * NQ;
-            __pipeline_memcpy_async(U + r * TS + 4 * c4, src + (size_t)(ft.lo + r) * a.n_is + 4 * c4, 16);
+            __pipeline_memcpy_async(U + r * TS + 4 * c4, src + (size_t)(ft.lo + r) * a.src_pitch + 4 * c4, 16);
           }
         } else {
           for (int q = tid; q < ft.width * TS; q += NT) {
             const int r = q / TS, c = q - r * TS;
             const int row = ft.lo + r;
             if (c < ncol && row >= a.win_r0 && row < a.win_r1)
-              __pipeline_memcpy_async(U + r * TS + c, src + (size_t)row * a.n_is + c, 4);
+              __pipeline_memcpy_async(U + r * TS + c, src + (size_t)row * a.src_pitch + c, 4);
             else
               U[r * TS + c] = 0.f;
           }
@@ -324,7 +339,7 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
           const int r = q / fs.width, c = q - r * fs.width;
           const int row = ft.lo + r;
           if (!windowed || (row >= a.win_r0 && row < a.win_r1))
-            __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)row * a.n_is + c, 4);
+            __pipeline_memcpy_async(slot + L.xs + r * a.fsp + c, src + (size_t)row * a.src_pitch + c, 4);
           else
             slot[L.xs + r * a.fsp + c] = 0.f;
         }
@@ -374,8 +389,8 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
         float* U = Ubase + (size_t)((sd % nbuf) * a.nb + sl) * urows * TS;
         const int4* GS = reinterpret_cast<const int4*>(slot + L.gs);
         const int4 sg0 = GS[2 * quad], sg1 = GS[2 * quad + 1];
-        const int pitch = XS ? a.fsp : a.n_is;
-        const float* xbase = XS ? slot + L.xs - h.fs_lo : a.src + h.src_off + (size_t)h.ft_lo * a.n_is;
+        const long long pitch = XS ? a.fsp : a.src_pitch;
+        const float* xbase = XS ? slot + L.xs - h.fs_lo : a.src + h.src_off + (size_t)h.ft_lo * a.src_pitch;
         // two rows per step; staged rows are padded so the second row is always addressable
         for (int r0 = gsub; r0 < h.ft_w; r0 += 2 * GSTEP) {
           float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
@@ -427,8 +442,8 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
             for (int p = 0; p < gd.y; ++p) fma4x4(acc[j], wp[p], up[p * (TS / 4)]);
           } else {
             const int gcol = os0 + quad * 4;
-            const bool gvec = ((a.n_is & 3) == 0) && ((h.src_off & 3) == 0) && gcol + 3 < a.n_is;
-            const float* gp = a.src + h.src_off + (size_t)gd.x * a.n_is + gcol;
+            const bool gvec = ((a.n_is & 3) == 0) && ((a.src_pitch & 3) == 0) && ((h.src_off & 3) == 0) && gcol + 3 < a.n_is;
+            const float* gp = a.src + h.src_off + (size_t)gd.x * a.src_pitch + gcol;
 #pragma unroll 4
             for (int p = 0; p < gd.y; ++p) {
               const int row = gd.x + p;
@@ -436,9 +451,9 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
               float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f);
               if (rin) {
                 if (gvec) {
-                  u4 = __ldg(reinterpret_cast<const float4*>(gp + (size_t)p * a.n_is));
+                  u4 = __ldg(reinterpret_cast<const float4*>(gp + (size_t)p * a.src_pitch));
                 } else {
-                  const float* q = gp + (size_t)p * a.n_is;
+                  const float* q = gp + (size_t)p * a.src_pitch;
                   if (gcol + 0 < a.n_is) u4.x = __ldg(q + 0);
                   if (gcol + 1 < a.n_is) u4.y = __ldg(q + 1);
                   if (gcol + 2 < a.n_is) u4.z = __ldg(q + 2);
@@ -455,14 +470,14 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
   }
   float* outb = a.out + (size_t)b * a.out_stride;
   const int col = os0 + quad * 4;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
       if (row >= a.n_ot) continue;
-      float* p = outb + (size_t)row * a.n_os + col;
+      float* p = outb + (size_t)row * a.out_pitch + col;
       float v[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
@@ -596,9 +611,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
       }
       __syncwarp();
       if (live) {
-        const float* src = a.src + term.src_off + (size_t)wlo * a.n_is + os0;
+        const float* src = a.src + term.src_off + (size_t)wlo * a.src_pitch + os0;
         float* dst = slot + (wlo - ft.lo) * TS;
-        for (int r = lane; r < whi - wlo; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.n_is, row_bytes, &full[s]);
+        for (int r = lane; r < whi - wlo; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.src_pitch, row_bytes, &full[s]);
         if (lane == 0) {
           bulk_g2s(slot + ustride, a.t_gw + ft.woff, (uint32_t)ft.wlen * 4, &full[s]);
           bulk_g2s(slot + ustride + wstride, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG), 32u * ngt,
@@ -653,14 +668,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
   }
   float* outb = a.out + (size_t)b * a.out_stride;
   const int col = os0 + quad * 4;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
       if (row >= a.n_ot) continue;
-      float* p = outb + (size_t)row * a.n_os + col;
+      float* p = outb + (size_t)row * a.out_pitch + col;
       float v[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
@@ -721,24 +736,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
           const int4 gd = __ldg(GD + 2 * gl + sg);
           const int p0 = max(0, a.win_r0 - gd.x), p1 = min(gd.y, a.win_r1 - gd.x);
           const float4* wp = reinterpret_cast<const float4*>(a.t_gw + gd.z);
-          const float* up = src + (size_t)gd.x * a.n_is;
+          const float* up = src + (size_t)gd.x * a.src_pitch;
 #pragma unroll UNR
           for (int p = p0; p < p1; ++p)
-            fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.n_is)));
+            fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.src_pitch)));
         }
       }
     }
   }
   if (!col_ok) return;
   float* outb = a.out + (size_t)b * a.out_stride;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0);
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
       if (row >= a.n_ot) continue;
-      float* p = outb + (size_t)row * a.n_os + col;
+      float* p = outb + (size_t)row * a.out_pitch + col;
       float v[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
@@ -758,6 +773,90 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
       }
     }
   }
+}
+
+// L2-gather t-pass over the MSEG form of the t family (identity s): per group a CSR list of dense
+// segments (one per cluster of source rows), so the FMA slots follow the non-zeros (~95% for the
+// slice-interleaved adjoint family, vs ~36-52% with two segments).  Otherwise as band_g_kernel.
+template <int TS, int TT, int NT, int UNR>
+__global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
+  constexpr int NQ = TS / 4;
+  constexpr int GSTEP = NT / NQ;
+  constexpr int NG = TT / 4;
+  constexpr int GP = NG / GSTEP;
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
+  const int tid = threadIdx.x;
+  const int quad = tid % NQ, gsub = tid / NQ;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int os0 = tx * TS, ot0 = ty * TT;
+  const int col = os0 + quad * 4;
+  if (col >= a.n_is) return;  // n_is % 4 == 0 (checked at tuning time): whole quads in or out
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  float acc[GP][4][4];
+#pragma unroll
+  for (int j = 0; j < GP; ++j)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
+  for (int e = e0; e < e1; ++e) {
+    const Term term = a.terms[e];
+    const float* src = a.src + term.src_off + col;
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+      const int g = ty * NG + gsub + j * GSTEP;
+      if (g >= a.t_ngroups) continue;
+      const size_t gi = (size_t)term.t_tab * a.t_ngroups + g;
+      const int s0 = __ldg(a.t_moff + gi), s1 = __ldg(a.t_moff + gi + 1);
+      for (int sg = s0; sg < s1; ++sg) {
+        const int4 gd = __ldg(a.t_mseg + sg);
+        const int p0 = max(0, a.win_r0 - gd.x), p1 = min(gd.y, a.win_r1 - gd.x);
+        const float4* wp = reinterpret_cast<const float4*>(a.t_mw + gd.z);
+        const float* up = src + (size_t)gd.x * a.src_pitch;
+#pragma unroll UNR
+        for (int p = p0; p < p1; ++p)
+          fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.src_pitch)));
+      }
+    }
+  }
+  float* outb = a.out + (size_t)b * a.out_stride;
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+  for (int j = 0; j < GP; ++j) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+      if (row >= a.n_ot) continue;
+      float* p = outb + (size_t)row * a.out_pitch + col;
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
+      if (vec) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (a.accumulate) {
+          const float4 q = *reinterpret_cast<float4*>(p);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(p) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          p[c] = a.accumulate ? p[c] + v[c] : v[c];
+        }
+      }
+    }
+  }
+}
+
+template <int TS, int TT, int NT>
+static lfm_status launch_band_m(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr) {
+  if (unr == 8)
+    band_m_kernel<TS, TT, NT, 8><<<grid, NT, 0, s>>>(a);
+  else
+    band_m_kernel<TS, TT, NT, 4><<<grid, NT, 0, s>>>(a);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_m_kernel launch", err);
 }
 
 template <int TS, int TT, int NT>
@@ -796,7 +895,16 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   SepArgs a;
   a.src = src;
   a.out = out;
-  a.out_stride = (long long)op.n_os * op.n_ot;
+  if (b0 < 0 || n_out < 0 || b0 + n_out > op.n_out) {
+    err = "launch_sep: output range outside the op";
+    return LFM_E_INVALID;
+  }
+  a.out_stride = op.out_stride ? op.out_stride : (long long)op.n_os * op.n_ot;
+  a.src_pitch = op.src_pitch ? op.src_pitch : op.n_is;
+  a.out_pitch = op.out_pitch ? op.out_pitch : op.n_os;
+  a.t_moff = op.ft->d_moff;
+  a.t_mseg = reinterpret_cast<const int4*>(op.ft->d_mseg);
+  a.t_mw = op.ft->d_mw;
   a.terms = op.d_terms;
   a.offs = op.d_offs + b0;
   a.s_g = reinterpret_cast<const int4*>(op.fs->d_g);
@@ -865,6 +973,21 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     LFM_BG_CASE(32, 32, 64)
 #undef LFM_BG_CASE
     err = "unsupported band_g tile";
+    return LFM_E_INVALID;
+  }
+  if (op.kind == 3) {
+    // L2-gather t-pass over MSEG segments: identity s, no shared memory
+    if (!op.ft->d_moff) { err = "band_m: t family has no MSEG form"; return LFM_E_INVALID; }
+#define LFM_BM_CASE(TS_, TT_, NT_) \
+    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_m<TS_, TT_, NT_>(a, grid, s, err, op.stages);
+    LFM_BM_CASE(128, 32, 256)
+    LFM_BM_CASE(128, 16, 128)
+    LFM_BM_CASE(128, 8, 64)
+    LFM_BM_CASE(64, 32, 128)
+    LFM_BM_CASE(64, 16, 64)
+    LFM_BM_CASE(32, 32, 64)
+#undef LFM_BM_CASE
+    err = "unsupported band_m tile";
     return LFM_E_INVALID;
   }
   const size_t smem = sep_smem(op, op.nb);
@@ -1196,8 +1319,12 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     if (!op->fs) continue;
     long long mx = 0;
     for (const Term& t : op->terms) mx = std::max(mx, t.src_off);
-    src_n = std::max(src_n, (size_t)mx + (size_t)op->n_is * op->n_it + 16);
-    out_n = std::max(out_n, (size_t)std::min(op->n_out, 64) * op->n_os * op->n_ot + 16);
+    const long long sp = op->src_pitch ? op->src_pitch : op->n_is;
+    const long long opch = op->out_pitch ? op->out_pitch : op->n_os;
+    const long long ost = op->out_stride ? op->out_stride : (long long)op->n_os * op->n_ot;
+    src_n = std::max(src_n, (size_t)(mx + (long long)(op->n_it - 1) * sp + op->n_is + 16));
+    out_n = std::max(out_n, (size_t)((long long)(std::min(op->n_out, 64) - 1) * ost + (long long)(op->n_ot - 1) * opch +
+                                     op->n_os + 16));
   }
   float *src = nullptr, *out = nullptr;
   if (cudaMalloc(&src, src_n * 4) != cudaSuccess || cudaMalloc(&out, out_n * 4) != cudaSuccess) {
@@ -1295,6 +1422,33 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         }
       }
       op.kind = 0;
+      const int mcand[][3] = {{128, 32, 256}, {128, 16, 128}, {128, 8, 64}, {64, 32, 128}, {64, 16, 64}, {32, 32, 64}};
+      for (auto& c : mcand) {
+        if (st != LFM_OK || !op.ft->want_mseg) break;
+        bool aligned = true;
+        for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
+        if (!aligned) break;
+        for (int unr : {4, 8}) {
+          op.kind = 3; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr;
+          fill_sep_geometry(op);
+          free_sep_dev(op);
+          size_t bytes = 0;
+          if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+          float ms = 0, tot = 0;
+          bool ok = true;
+          for (int rep = 0; rep < 3 && ok; ++rep) {
+            cudaEventRecord(e0, 0);
+            ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+            cudaEventRecord(e1, 0);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) tot += ms;
+          }
+          if (!ok || cudaGetLastError() != cudaSuccess) continue;
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 3; bstages = unr; }
+        }
+      }
+      op.kind = 0;
     }
     for (auto& c : cand) {
       for (int stage : {1, 0}) {
@@ -1331,7 +1485,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
         std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,

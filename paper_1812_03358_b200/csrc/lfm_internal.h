@@ -45,8 +45,17 @@ struct BandFamily {
   std::vector<double> g_w64;              // flat, per table contiguous
   int32_t* d_g = nullptr;                 // int4 per [table][group]: j0, W, off, 0
   float* d_gw = nullptr;
+  // MSEG form (built when want_mseg): per group a CSR list of segments, split at every all-zero run of
+  // >= 2 source cells; segment = int4 {j0, W, off, 0}, weights W x 4 (row-interleaved) at off.
+  int want_mseg = 0;
+  std::vector<int32_t> m_off;              // [table*n_groups + g] .. +1 (size n_tables*n_groups + 1)
+  std::vector<int32_t> m_seg;              // 4 ints per segment
+  std::vector<double> m_w64;
+  int32_t* d_moff = nullptr;
+  int32_t* d_mseg = nullptr;
+  float* d_mw = nullptr;
   // density statistics (LFM_DEBUG): non-zeros, G4 slot columns, columns with any non-zero
-  double st_nnz = 0, st_cols_g4 = 0, st_cols_nz = 0;
+  double st_nnz = 0, st_cols_g4 = 0, st_cols_nz = 0, st_msegs = 0, st_cols_m = 0;
 };
 
 // One summand of a separable banded sum: source plane at src_base + src_off, s/t table indices.
@@ -83,7 +92,11 @@ struct SepOp {
   int nb = 1;                      // terms staged per barrier
   int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
-  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s), 2: band_g_kernel (L2 gather)
+  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s), 2: band_g_kernel (L2 gather),
+                                   // 3: band_m_kernel (L2 gather over MSEG segments of ft)
+  long long src_pitch = 0;         // floats between source rows (0: n_is)
+  long long out_pitch = 0;         // floats between output rows (0: n_os)
+  long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)
   int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile
@@ -115,6 +128,7 @@ struct CameraPlan {
   SepOp fwd_c1, fwd_c2;                   // collapsed forward in two passes: s (U_n for all n), then t
   int fwd_split = 0;                      // 1: forward uses fwd_c1 + fwd_c2 (chosen by the autotuner)
   BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint/forward
+  BandFamily ca1n, cf1n;                  // slice-interleaved collapsed t families (rows (vt,n) / sources (vt,n))
   // lf_transport ops (output b = n*K + k for slice-indexed families)
   SepOp xp_s1f, xp_s1a, xp_s3f, xp_s3a;
   ShearPass rot[3];                       // application order z, x, y (x^r = E^y E^x E^z x)

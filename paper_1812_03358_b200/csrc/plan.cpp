@@ -206,6 +206,9 @@ static void build_ell(BandFamily& f) {
   f.g_off.assign(2 * ng, 0);
   f.g_w64.clear();
   f.gmax = 0;
+  f.m_seg.clear();
+  f.m_w64.clear();
+  if (f.want_mseg) f.m_off.assign(ng + 1, 0);
   std::vector<double> dense;
   for (int m = 0; m < f.n_tables; ++m)
     for (int g = 0; g < f.n_groups; ++g) {
@@ -220,6 +223,7 @@ static void build_ell(BandFamily& f) {
       }
       size_t gi = (size_t)m * f.n_groups + g;
       f.g_off[2 * gi] = f.g_off[2 * gi + 1] = (int)f.g_w64.size();
+      if (f.want_mseg) f.m_off[gi] = (int)(f.m_seg.size() / 4);
       if (hi < 0) continue;
       const int W = hi - lo;
       dense.assign((size_t)W * 4, 0.0);
@@ -260,7 +264,38 @@ static void build_ell(BandFamily& f) {
         for (int q = 0; q < 4; ++q) f.st_nnz += dense[4 * p + q] != 0.0;
       }
       f.st_cols_g4 += segs[0][1] - segs[0][0] + segs[1][1] - segs[1][0];
+      // multi-segment form (MSEG): split the window at every all-zero run of >= 2 columns
+      {
+        int p = 0;
+        while (p < W) {
+          while (p < W && dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 &&
+                 dense[4 * p + 3] == 0.0)
+            ++p;
+          if (p >= W) break;
+          int a = p, last = p;
+          while (p < W) {
+            bool z = dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 && dense[4 * p + 3] == 0.0;
+            if (!z) { last = p; ++p; continue; }
+            int zs = p;
+            while (p < W && dense[4 * p] == 0.0 && dense[4 * p + 1] == 0.0 && dense[4 * p + 2] == 0.0 &&
+                   dense[4 * p + 3] == 0.0)
+              ++p;
+            if (p - zs >= 2 || p >= W) break;
+          }
+          f.st_msegs += 1;
+          f.st_cols_m += last - a + 1;
+          if (f.want_mseg) {
+            f.m_seg.push_back(lo + a);
+            f.m_seg.push_back(last - a + 1);
+            f.m_seg.push_back((int)f.m_w64.size());
+            f.m_seg.push_back(0);
+            for (int c = a; c <= last; ++c)
+              for (int q = 0; q < 4; ++q) f.m_w64.push_back(dense[4 * c + q]);
+          }
+        }
+      }
     }
+  if (f.want_mseg) f.m_off[ng] = (int)(f.m_seg.size() / 4);
 }
 
 // Union window of the G4 groups of output tile t (rows [t*tile, (t+1)*tile)), and its weight block.
@@ -305,6 +340,55 @@ struct FamilyBuilder {
     build_ell(f);
   }
 };
+
+// Slice-interleaved forms of a per-slice family f (n_tables = nz, rows r, sources j):
+//  rows_by_slice: one table, row (r, n) at r*nz + n = table n's row r (same sources).  Groups of 4 rows
+//                 are then 4 neighbouring slices of one output row, whose bands nearly coincide.
+//  cols_by_slice: one table, row r with sources (j, n) at j*nz + n = table n's entry (r, j): the sum over
+//                 slices becomes one long band over the interleaved source index.
+static void make_rows_by_slice(BandFamily& out, const BandFamily& f) {
+  const int nz = f.n_tables;
+  family_init(out, 1, f.n_rows * nz, f.n_src);
+  FamilyBuilder b(out);
+  b.tabs.resize(1);
+  b.tabs[0].assign((size_t)f.n_rows * nz, Row());
+  for (int r = 0; r < f.n_rows; ++r)
+    for (int n = 0; n < nz; ++n) {
+      size_t idx = (size_t)n * f.n_rows + r;
+      Row& row = b.tabs[0][(size_t)r * nz + n];
+      row.lo = f.start[idx];
+      row.len = f.len[idx];
+      row.w.assign(f.w64.begin() + idx * f.taps, f.w64.begin() + idx * f.taps + f.len[idx]);
+    }
+  b.finish();
+}
+
+static void make_cols_by_slice(BandFamily& out, const BandFamily& f) {
+  const int nz = f.n_tables;
+  family_init(out, 1, f.n_rows, f.n_src * nz);
+  FamilyBuilder b(out);
+  b.tabs.resize(1);
+  b.tabs[0].assign(f.n_rows, Row());
+  for (int r = 0; r < f.n_rows; ++r) {
+    int lo = 1 << 30, hi = -1;
+    for (int n = 0; n < nz; ++n) {
+      size_t idx = (size_t)n * f.n_rows + r;
+      if (!f.len[idx]) continue;
+      lo = std::min(lo, f.start[idx] * nz + n);
+      hi = std::max(hi, (f.start[idx] + f.len[idx] - 1) * nz + n);
+    }
+    Row& row = b.tabs[0][r];
+    if (hi < 0) continue;
+    row.lo = lo;
+    row.len = hi - lo + 1;
+    row.w.assign(row.len, 0.0);
+    for (int n = 0; n < nz; ++n) {
+      size_t idx = (size_t)n * f.n_rows + r;
+      for (int q = 0; q < f.len[idx]; ++q) row.w[(size_t)(f.start[idx] + q) * nz + n - lo] = f.w64[idx * f.taps + q];
+    }
+  }
+  b.finish();
+}
 
 static void make_identity(BandFamily& f, int n) {
   family_init(f, 1, n, n);
@@ -916,6 +1000,20 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
       sep_close_output(cp.adj_s1);
     }
   }
+  // slice-interleaved t families of the two-pass collapsed path, with their MSEG segment lists
+  cp.ca1n.want_mseg = 1;
+  make_rows_by_slice(cp.ca1n, cp.ca[1]);
+  cp.cf1n.want_mseg = 1;
+  make_cols_by_slice(cp.cf1n, cp.cf[1]);
+  if (std::getenv("LFM_DEBUG")) {
+    const BandFamily* fs[] = {&cp.ca1n, &cp.cf1n, &cp.ca[1], &cp.cf[1], &cp.ca[0], &cp.cf[0]};
+    const char* nm[] = {"ca1 rows-by-slice", "cf1 cols-by-slice", "ca1", "cf1", "ca0", "cf0"};
+    for (int i = 0; i < 6; ++i)
+      std::fprintf(stderr, "[lfm] %-18s G4 %.3f  MSEG %.3f  (%.2f segs/group, %.1f cols/seg)  gap-free %.3f\n", nm[i],
+                   fs[i]->st_nnz / (4 * fs[i]->st_cols_g4), fs[i]->st_nnz / (4 * fs[i]->st_cols_m),
+                   fs[i]->st_msegs / ((double)fs[i]->n_tables * fs[i]->n_groups), fs[i]->st_cols_m / fs[i]->st_msegs,
+                   fs[i]->st_nnz / (4 * fs[i]->st_cols_nz));
+  }
   // collapsed path
   sep_init(cp.fwd_c, &cp.cf[0], &cp.cf[1], nx, ny, 1, (float)(c1 * c3));
   for (int n = 0; n < nz; ++n) sep_add(cp.fwd_c, n * nslice, n, n, 1.f);
@@ -924,27 +1022,33 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   // stage in 2D): Z_n = C_t,n^T y along t (s untouched), then x_n = C_s,n^T Z_n along s.
   make_identity(cp.id_s, ndet[0]);
   make_identity(cp.id_vt, ny);
-  sep_init(cp.adj_c1, &cp.id_s, &cp.ca[1], ndet[0], ndet[1], nz, 1.f);
+  // The intermediate Z of both two-pass orders is slice-interleaved: row (vt, n) at (vt*nz + n)*ndet_s.
+  // adjoint pass t: one term over the rows-by-slice family (4 neighbouring slices of one voxel row per
+  // G4 group: nearly identical bands, so the MSEG segments are ~95% dense)
+  sep_init(cp.adj_c1, &cp.id_s, &cp.ca1n, ndet[0], ndet[1], 1, 1.f);
   cp.adj_c1.s_ident = 1;
+  sep_add(cp.adj_c1, 0, 0, 0, 1.f);
+  sep_close_output(cp.adj_c1);
+  // adjoint pass s: x_n = C_s,n^T Z_n, reading slice n's rows at pitch nz*ndet_s
+  sep_init(cp.adj_c2, &cp.ca[0], &cp.id_vt, ndet[0], ny, nz, (float)(c1 * c3));
+  cp.adj_c2.src_pitch = (long long)nz * ndet[0];
   for (int n = 0; n < nz; ++n) {
-    sep_add(cp.adj_c1, 0, 0, n, 1.f);
-    sep_close_output(cp.adj_c1);
+    sep_add(cp.adj_c2, (long long)n * ndet[0], n, 0, 1.f);
+    sep_close_output(cp.adj_c2);
   }
-  // collapsed forward in two passes: U_n = X_n C_{s,n}^T (all slices, t identity), then y = sum_n C_{t,n} U_n
+  // collapsed forward in two passes: U_n = X_n C_{s,n}^T (all slices, t identity, written interleaved),
+  // then y = C_t U over the cols-by-slice family: the slice sum is one long band per detector row
   sep_init(cp.fwd_c1, &cp.cf[0], &cp.id_vt, nx, ny, nz, 1.f);
+  cp.fwd_c1.out_pitch = (long long)nz * ndet[0];
+  cp.fwd_c1.out_stride = ndet[0];
   for (int n = 0; n < nz; ++n) {
     sep_add(cp.fwd_c1, n * nslice, n, 0, 1.f);
     sep_close_output(cp.fwd_c1);
   }
-  sep_init(cp.fwd_c2, &cp.id_s, &cp.cf[1], ndet[0], ny, 1, (float)(c1 * c3));
+  sep_init(cp.fwd_c2, &cp.id_s, &cp.cf1n, ndet[0], ny * nz, 1, (float)(c1 * c3));
   cp.fwd_c2.s_ident = 1;
-  for (int n = 0; n < nz; ++n) sep_add(cp.fwd_c2, (long long)n * ny * ndet[0], 0, n, 1.f);
+  sep_add(cp.fwd_c2, 0, 0, 0, 1.f);
   sep_close_output(cp.fwd_c2);
-  sep_init(cp.adj_c2, &cp.ca[0], &cp.id_vt, ndet[0], ny, nz, (float)(c1 * c3));
-  for (int n = 0; n < nz; ++n) {
-    sep_add(cp.adj_c2, (long long)n * ny * ndet[0], n, 0, 1.f);
-    sep_close_output(cp.adj_c2);
-  }
   // lf_transport ops: output b = n*K + k (S1 families), b = k (S3 families); scale 1/V^p
   {
     long long dplane = plen ? nfield : npix;
@@ -993,7 +1097,12 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   }
   for (int q = 0; q < 13; ++q) {
     if (!ops[q]->fs) continue;
-    if (!sep_choose_tile(*ops[q])) {
+    if (ops[q]->s_ident && ops[q]->ft->want_mseg && ops[q]->n_is % 4 == 0) {
+      // identity s over an MSEG t family: the L2-gather kernel needs no shared memory (autotuned later)
+      SepOp& op = *ops[q];
+      op.kind = 3; op.ts = 128; op.tt = 16; op.nt = 128; op.nb = 1; op.stage = 0; op.stages = 4;
+      fill_sep_geometry(op);
+    } else if (!sep_choose_tile(*ops[q])) {
       err = std::string("source footprint of op ") + names[q] + " exceeds shared memory";
       return LFM_E_NOMEM;
     }
@@ -1006,10 +1115,11 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
         SepOp& op = *ops[q];
         op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
         fill_sep_geometry(op);
-        if (kind == 1 || kind == 2) {
-          bool ok = op.s_ident && op.n_is % 4 == 0 && (kind == 2 || band_t_smem(op) <= (size_t)200 * 1024);
+        if (kind >= 1) {
+          bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
+                    (kind != 3 || op.ft->want_mseg);
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
-          if (!ok) { err = env + ": band_t not applicable"; return LFM_E_INVALID; }
+          if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
         } else if (sep_smem(op, nb) > (size_t)220 * 1024) {
           err = env + ": shared memory too large";
           return LFM_E_INVALID;

@@ -45,31 +45,35 @@ def test_rows_entry_points(name, path):
         assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL
 
 
-# band_t: ts,tt,nt,nb,stage,kind=1,stages ; band_g: kind=2, last field = unroll ;
-# sep: MODE variants (stage 1 = staged U, 0 = U from L2)
+# band_t: ts,tt,nt,nb,stage,kind=1,stages ; band_g (2-segment G4) kind=2 / band_m (MSEG) kind=3, last
+# field = unroll ; sep: MODE variants (stage 1 = staged U, 0 = U from L2)
 VARIANTS = {
-    "band_t_128x64_s4": "128,64,288,1,1,1,4",
-    "band_t_128x32_s2": "128,32,288,1,1,1,2",
-    "band_t_64x64_s3": "64,64,288,1,1,1,3",
-    "band_t_64x32_s2": "64,32,160,1,1,1,2",
-    "band_t_32x32_s4": "32,32,96,1,1,1,4",
+    "band_m_128x16_u4": "128,16,128,1,0,3,4",
+    "band_m_128x32_u8": "128,32,256,1,0,3,8",
+    "band_m_64x16_u8": "64,16,64,1,0,3,8",
+    "band_m_32x32_u4": "32,32,64,1,0,3,4",
     "band_g_128x32_u8": "128,32,256,1,0,2,8",
     "band_g_64x32_u4": "64,32,128,1,0,2,4",
-    "band_g_128x64_u4": "128,64,256,1,0,2,4",
-    "sep_128x64_staged": "128,64,256,1,1",
+    "band_t_128x32_s2": "128,32,288,1,1,1,2",
+    "band_t_32x32_s4": "32,32,96,1,1,1,4",
     "sep_64x32_l2": "64,32,128,1,0",
+    "sep_32x32_staged": "32,32,64,1,1",
 }
 
 
+@pytest.mark.parametrize("op_name", ["adj_c1", "fwd_c2"])
 @pytest.mark.parametrize("variant", list(VARIANTS))
-def test_forced_t_pass_variants(variant, monkeypatch):
+def test_forced_t_pass_variants(op_name, variant, monkeypatch):
     from paper_1812_03358_b200 import lfm
     cfg = make_config("small_two")
-    monkeypatch.setenv("LFM_FORCE_fwd_c2", VARIANTS[variant])
-    monkeypatch.setenv("LFM_FORCE_adj_c1", VARIANTS[variant])
+    monkeypatch.setenv("LFM_FORCE_" + op_name, VARIANTS[variant])
     monkeypatch.setenv("LFM_FWD_SPLIT", "1")
     monkeypatch.delenv("LFM_TUNE_FILE", raising=False)
-    plan = lfm.Plan(cfg, device=0)
+    try:
+        plan = lfm.Plan(cfg, device=0)
+    except lfm.LfmError as e:  # the variant's staged footprint does not fit this op's shared memory
+        assert "not applicable" in str(e) or "too large" in str(e), str(e)
+        pytest.skip(str(e))
     ws = plan.workspace()
     ops = build_system(cfg)
     x = uniform_volume(cfg["volume"], 0)
@@ -82,7 +86,11 @@ def test_forced_t_pass_variants(variant, monkeypatch):
         g = torch.empty(op.n_vox, device="cuda:0")
         lfm.A_adjoint(plan, c, dev(r), g, ws, path=1)
         assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL, (variant, c)
-        # windowed source rows (adjoint row sharding) through the same kernel
+        # windowed source rows (adjoint row sharding) and output rows (forward row sharding)
         r0, r1 = n_t // 4 + 1, (3 * n_t) // 4
         lfm.A_adjoint_rows(plan, c, r0, r1, dev(r), g, ws, path=1)
         assert max_rel(host(g), op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))) <= TOL, (variant, c)
+        y.fill_(float("nan"))
+        lfm.A_forward_rows(plan, c, r0, r1, dev(x), y, ws, path=1)
+        yref = op.forward(x.astype(np.float64)).reshape(n_t, -1)
+        assert max_rel(host(y).reshape(n_t, -1)[r0:r1], yref[r0:r1]) <= TOL * np.abs(yref).max() / np.abs(yref[r0:r1]).max()
