@@ -28,7 +28,7 @@ lfm_status fail(lfm_status s, const std::string& msg) {
 size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct WsLayout {
-  size_t r0, r1, f, s, s2, z, p, total;
+  size_t r0, r1, xt, f, s, s2, z, zt, p, total;
 };
 
 WsLayout layout(const lfm_plan_s* p) {
@@ -42,17 +42,19 @@ WsLayout layout(const lfm_plan_s* p) {
   WsLayout L;
   L.r0 = 0;
   L.r1 = L.r0 + al256(V);
-  L.f = L.r1 + al256(V);
+  L.xt = L.r1 + al256(V);
+  L.f = L.xt + al256(V);
   L.s = L.f + al256(F);
   L.s2 = L.s + al256(S);
   L.z = L.s2 + al256(S);
-  L.p = L.z + al256(Z);
+  L.zt = L.z + al256(Z);
+  L.p = L.zt + al256(Z);
   L.total = L.p + al256(4096 * 8 * 4);
   return L;
 }
 
 struct Ws {
-  float *r0, *r1, *f, *s, *s2, *z;
+  float *r0, *r1, *xt, *f, *s, *s2, *z, *zt;
   double* p;
 };
 
@@ -68,6 +70,8 @@ lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
   w.s = (float*)(b + L.s);
   w.s2 = (float*)(b + L.s2);
   w.z = (float*)(b + L.z);
+  w.xt = (float*)(b + L.xt);
+  w.zt = (float*)(b + L.zt);
   w.p = (double*)(b + L.p);
   return LFM_OK;
 }
@@ -149,7 +153,17 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
     if (cp.fwd_split) {
-      TRY(sep(cp.fwd_c1, xr, w.z, 0, cp.info.nz, 0, stream));
+      if (cp.fwd_t) {
+        // s pass as a t pass over the transposed slices, written back in the interleaved U layout
+        const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz;
+        const long long nslice = (long long)nx * ny;
+        std::string err;
+        lfm_status st = k_transpose(xr, w.xt, nz, ny, nx, nslice, nx, nslice, ny, stream, err);
+        if (st != LFM_OK) return fail(st, err);
+        TRY(sep(cp.fwd_p1, w.xt, w.z, 0, nz, 0, stream));
+      } else {
+        TRY(sep(cp.fwd_c1, xr, w.z, 0, cp.info.nz, 0, stream));
+      }
       return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1);
     }
     return sep(cp.fwd_c, xr, y, 0, 1, 0, stream, r0, r1);
@@ -170,7 +184,16 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
     TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1));  // one output: all (vt, n) rows
-    TRY(sep(cp.adj_c2, w.z, target, 0, cp.info.nz, acc, stream));
+    if (cp.adj_t) {
+      // Z_n -> ZT_n = [j][vt] per slice, then the s pass as a t pass with transposed output into x_n
+      const int ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
+      std::string err;
+      lfm_status st = k_transpose(w.z, w.zt, nz, ny, nd, nd, (long long)nz * nd, (long long)nd * ny, ny, stream, err);
+      if (st != LFM_OK) return fail(st, err);
+      TRY(sep(cp.adj_a2, w.zt, target, 0, nz, acc, stream));
+    } else {
+      TRY(sep(cp.adj_c2, w.z, target, 0, cp.info.nz, acc, stream));
+    }
   } else if (plen) {
     TRY(sep(cp.adj_s3, y, w.f, 0, cp.info.n_views, 0, stream, 0, -1, r0, r1));
     TRY(sep(cp.adj_s1, w.f, target, 0, cp.info.nz, acc, stream));

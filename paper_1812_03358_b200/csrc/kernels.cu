@@ -127,7 +127,7 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
   for (BandFamily* f : {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n})
     if ((st = upload_family(*f, bytes, err)) != LFM_OK) return st;
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
   for (SepOp* op : ops)
     if ((st = upload_sep(*op, bytes, err)) != LFM_OK) return st;
   for (int p = 0; p < 3; ++p) {
@@ -161,7 +161,7 @@ void free_camera(CameraPlan& cp) {
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
   for (SepOp* op : ops) {
     dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t);
     op->d_terms = nullptr; op->d_offs = nullptr; op->d_fp_s = nullptr; op->d_fp_t = nullptr;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
 // L2-gather t-pass over the MSEG form of the t family (identity s): per group a CSR list of dense
 // segments (one per cluster of source rows), so the FMA slots follow the non-zeros (~95% for the
 // slice-interleaved adjoint family, vs ~36-52% with two segments).  Otherwise as band_g_kernel.
-template <int TS, int TT, int NT, int UNR>
+template <int TS, int TT, int NT, int UNR, bool TOUT>
 __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
   constexpr int NQ = TS / 4;
   constexpr int GSTEP = NT / NQ;
@@ -820,6 +820,38 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
     }
   }
   float* outb = a.out + (size_t)b * a.out_stride;
+  if (TOUT) {
+    // transposed output: element (row, col) at outb[col * out_pitch + row]; 4 consecutive rows per store
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+      const int row0 = ot0 + 4 * (gsub + j * GSTEP);
+      if (row0 >= a.n_ot) continue;
+      const bool vec = row0 + 3 < a.n_ot && ((a.n_ot & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (col + c >= a.n_os) continue;
+        float* p = outb + (size_t)(col + c) * a.out_pitch + row0;
+        float v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = a.out_scale * acc[j][r][c];
+        if (vec) {
+          float4 o = make_float4(v[0], v[1], v[2], v[3]);
+          if (a.accumulate) {
+            const float4 q = *reinterpret_cast<float4*>(p);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(p) = o;
+        } else {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            if (row0 + r >= a.n_ot) continue;
+            p[r] = a.accumulate ? p[r] + v[r] : v[r];
+          }
+        }
+      }
+    }
+    return;
+  }
   const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
@@ -850,11 +882,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
 }
 
 template <int TS, int TT, int NT>
-static lfm_status launch_band_m(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr) {
-  if (unr == 8)
-    band_m_kernel<TS, TT, NT, 8><<<grid, NT, 0, s>>>(a);
-  else
-    band_m_kernel<TS, TT, NT, 4><<<grid, NT, 0, s>>>(a);
+static lfm_status launch_band_m(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
+  if (tout) {
+    if (unr == 8)
+      band_m_kernel<TS, TT, NT, 8, true><<<grid, NT, 0, s>>>(a);
+    else
+      band_m_kernel<TS, TT, NT, 4, true><<<grid, NT, 0, s>>>(a);
+  } else if (unr == 8) {
+    band_m_kernel<TS, TT, NT, 8, false><<<grid, NT, 0, s>>>(a);
+  } else {
+    band_m_kernel<TS, TT, NT, 4, false><<<grid, NT, 0, s>>>(a);
+  }
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_m_kernel launch", err);
 }
@@ -887,6 +925,40 @@ static lfm_status launch_band_t(const SepArgs& a, dim3 grid, size_t smem, cudaSt
 size_t band_t_smem(const SepOp& op) {
   size_t slot = (size_t)op.ft_max * op.ts + ((size_t)op.wt_max + 3) / 4 * 4 + 8 * (size_t)(op.tt / 4);
   return slot * 4 * op.stages;
+}
+
+// Batched transpose: out[b][c][r] = in[b][r][c] (r < R, c < C), 32x32 tiles through shared memory
+// (padded against bank conflicts), coalesced on both sides.  Used to move the collapsed path's
+// intermediates between row-major orders (pure data movement, no arithmetic).
+__global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int R,
+                                                        int C, long long in_bs, long long in_pitch, long long out_bs,
+                                                        long long out_pitch) {
+  __shared__ float tile[32][33];
+  const int b = blockIdx.z;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const float* ib = in + (size_t)b * in_bs;
+  float* ob = out + (size_t)b * out_bs;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int r = r0 + ty + k, c = c0 + tx;
+    if (r < R && c < C) tile[ty + k][tx] = ib[(size_t)r * in_pitch + c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int c = c0 + ty + k, r = r0 + tx;
+    if (r < R && c < C) ob[(size_t)c * out_pitch + r] = tile[tx][ty + k];
+  }
+}
+
+lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
+                       long long out_bs, long long out_pitch, void* stream, std::string& err) {
+  if (B <= 0 || R <= 0 || C <= 0) return LFM_OK;
+  dim3 grid((C + 31) / 32, (R + 31) / 32, B);
+  transpose_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, out, R, C, in_bs, in_pitch, out_bs, out_pitch);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "transpose_kernel launch", err);
 }
 
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
@@ -941,6 +1013,10 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.win_r1 = win_r1 < 0 ? op.n_it : std::min(win_r1, op.n_it);
   dim3 grid(op.ntx, nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
+  if (op.tout && op.kind != 3) {
+    err = "transposed output needs the band_m kernel";
+    return LFM_E_INVALID;
+  }
   if (op.kind == 1) {
     // streaming t-pass: identity s, whole windows, 16-byte aligned rows (checked at tuning time)
     const size_t smem = band_t_smem(op);
@@ -979,7 +1055,7 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     // L2-gather t-pass over MSEG segments: identity s, no shared memory
     if (!op.ft->d_moff) { err = "band_m: t family has no MSEG form"; return LFM_E_INVALID; }
 #define LFM_BM_CASE(TS_, TT_, NT_) \
-    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_m<TS_, TT_, NT_>(a, grid, s, err, op.stages);
+    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_m<TS_, TT_, NT_>(a, grid, s, err, op.stages, op.tout);
     LFM_BM_CASE(128, 32, 256)
     LFM_BM_CASE(128, 16, 128)
     LFM_BM_CASE(128, 8, 64)
@@ -1309,9 +1385,11 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     }
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.fwd_c1, &cp.fwd_c2};
-  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2", "fwd_c1", "fwd_c2"};
-  float op_best[9];
+                  &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
+  const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2", "fwd_c1", "fwd_c2",
+                         "fwd_p1", "adj_a2"};
+  constexpr int NQ_OPS = 11;
+  float op_best[NQ_OPS];
   for (float& v : op_best) v = -1.f;
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
   size_t src_n = 0, out_n = 0;
@@ -1322,9 +1400,9 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     const long long sp = op->src_pitch ? op->src_pitch : op->n_is;
     const long long opch = op->out_pitch ? op->out_pitch : op->n_os;
     const long long ost = op->out_stride ? op->out_stride : (long long)op->n_os * op->n_ot;
+    const long long nr = op->tout ? op->n_os : op->n_ot, nc = op->tout ? op->n_ot : op->n_os;
     src_n = std::max(src_n, (size_t)(mx + (long long)(op->n_it - 1) * sp + op->n_is + 16));
-    out_n = std::max(out_n, (size_t)((long long)(std::min(op->n_out, 64) - 1) * ost + (long long)(op->n_ot - 1) * opch +
-                                     op->n_os + 16));
+    out_n = std::max(out_n, (size_t)((long long)(std::min(op->n_out, 64) - 1) * ost + (nr - 1) * opch + nc + 16));
   }
   float *src = nullptr, *out = nullptr;
   if (cudaMalloc(&src, src_n * 4) != cudaSuccess || cudaMalloc(&out, out_n * 4) != cudaSuccess) {
@@ -1339,7 +1417,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   cudaEventCreate(&e1);
   const int cand[][3] = {{128, 64, 256}, {128, 32, 256}, {64, 64, 128}, {64, 32, 128}, {32, 32, 64}};
   lfm_status st = LFM_OK;
-  for (int q = 0; q < 9 && st == LFM_OK; ++q) {
+  for (int q = 0; q < NQ_OPS && st == LFM_OK; ++q) {
     SepOp& op = *ops[q];
     if (!op.fs) continue;
     if (std::getenv((std::string("LFM_FORCE_") + names[q]).c_str())) continue;  // explicit override wins
@@ -1369,6 +1447,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     int bkind = keep.kind, bstages = keep.stages;
     if (op.s_ident && (op.n_is % 4) == 0) {
       for (auto& c : cand) {
+        if (op.tout) break;  // transposed output: band_m only
         for (int stages : {2, 3, 4}) {
           op.kind = 1; op.ts = c[0]; op.tt = c[1]; op.stages = stages; op.nb = 1; op.stage = 1;
           op.nt = c[0] == 32 ? 96 : (c[0] == 64 && c[1] == 32 ? 160 : 288);
@@ -1397,7 +1476,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       op.kind = 0;
       const int gcand[][3] = {{128, 32, 256}, {128, 64, 256}, {128, 16, 128}, {64, 32, 128}, {64, 64, 256}, {32, 32, 64}};
       for (auto& c : gcand) {
-        if (st != LFM_OK) break;
+        if (st != LFM_OK || op.tout) break;
         bool aligned = true;
         for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
         if (!aligned) break;
@@ -1451,6 +1530,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       op.kind = 0;
     }
     for (auto& c : cand) {
+      if (op.tout) break;
       for (int stage : {1, 0}) {
         for (int nb : {1, 2, 4}) {
           if (nb > 1 && op.terms.size() < (size_t)op.n_out * 2) continue;
@@ -1494,14 +1574,47 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       }
     }
   }
+  // s passes of the two-pass path: direct (sep kernel) or transpose + band_m with transposed output
+  float t_x = -1.f, t_z = -1.f;
+  if (st == LFM_OK && (op_best[9] > 0 || op_best[10] > 0)) {
+    const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
+    const long long nslice = (long long)nx * ny;
+    auto time_it = [&](auto&& fn) {
+      float ms = 0, tot = 0;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(e0, 0);
+        fn();
+        cudaEventRecord(e1, 0);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0) tot += ms;
+      }
+      return tot;
+    };
+    std::string terr;
+    t_x = time_it([&] { k_transpose(src, out, nz, ny, nx, nslice, nx, nslice, ny, nullptr, terr); });
+    t_z = time_it([&] {
+      k_transpose(src, out, nz, ny, nd, nd, (long long)nz * nd, (long long)nd * ny, ny, nullptr, terr);
+    });
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   dfree(src);
   dfree(out);
-  // forward order: fused (fwd_c) or two passes (fwd_c1 + fwd_c2), whichever timed faster
-  if (op_best[4] > 0 && op_best[7] > 0 && op_best[8] > 0) cp.fwd_split = (op_best[7] + op_best[8]) < op_best[4];
+  if (op_best[9] > 0 && op_best[7] > 0 && t_x >= 0) cp.fwd_t = (t_x + op_best[9]) < op_best[7];
+  if (op_best[10] > 0 && op_best[6] > 0 && t_z >= 0) cp.adj_t = (t_z + op_best[10]) < op_best[6];
+  if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] == '1';
+  if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] == '1';
+  cp.fwd_t = cp.fwd_t && cp.fwd_p1.fs && cp.fwd_p1.kind == 3;  // transposed output exists only in band_m
+  cp.adj_t = cp.adj_t && cp.adj_a2.fs && cp.adj_a2.kind == 3;
+  const float fwd_s = cp.fwd_t ? t_x + op_best[9] : op_best[7];
+  // forward order: fused (fwd_c) or two passes (s pass + fwd_c2), whichever timed faster
+  if (op_best[4] > 0 && fwd_s > 0 && op_best[8] > 0) cp.fwd_split = (fwd_s + op_best[8]) < op_best[4];
   if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
-  if (dbg) std::fprintf(stderr, "[lfm] collapsed forward: %s\n", cp.fwd_split ? "two passes" : "fused");
+  if (dbg)
+    std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",
+                 cp.fwd_split ? "two passes" : "fused", cp.fwd_t ? "transposed" : "direct", t_x, t_z,
+                 cp.adj_t ? "transposed" : "direct");
   return st;
 }
 }  // namespace lfm

@@ -97,6 +97,7 @@ struct SepOp {
   long long src_pitch = 0;         // floats between source rows (0: n_is)
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)
+  int tout = 0;                    // band_m only: write element (row, col) at col * out_pitch + row
   int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile
@@ -127,6 +128,9 @@ struct CameraPlan {
   SepOp fwd_c, adj_c1, adj_c2;            // collapsed path (adjoint in two passes: t then s)
   SepOp fwd_c1, fwd_c2;                   // collapsed forward in two passes: s (U_n for all n), then t
   int fwd_split = 0;                      // 1: forward uses fwd_c1 + fwd_c2 (chosen by the autotuner)
+  SepOp fwd_p1, adj_a2;                   // transposed s passes (band_m with transposed output)
+  int fwd_t = 0;                          // 1: split forward's s pass = transpose x + fwd_p1 (autotuner)
+  int adj_t = 0;                          // 1: adjoint's s pass = transpose Z + adj_a2 (autotuner)
   BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint/forward
   BandFamily ca1n, cf1n;                  // slice-interleaved collapsed t families (rows (vt,n) / sources (vt,n))
   // lf_transport ops (output b = n*K + k for slice-indexed families)
@@ -160,4 +164,6 @@ void free_camera(CameraPlan& cp);
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0 = 0, int out_r1 = -1, int win_r0 = 0,
                       int win_r1 = -1);
+lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
+                       long long out_bs, long long out_pitch, void* stream, std::string& err);
 }  // namespace lfm

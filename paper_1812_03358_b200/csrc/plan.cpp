@@ -889,6 +889,8 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     int nv = nsrc[ax];
     family_init(cp.cf[ax], nz, nrow, nv);
     family_init(cp.ca[ax], nz, nv, nrow);
+    // s-axis composites also serve as t families of the transposed two-pass path (MSEG segments)
+    cp.cf[ax].want_mseg = cp.ca[ax].want_mseg = ax == 0;
     FamilyBuilder bf(cp.cf[ax]), ba(cp.ca[ax]);
     bf.tabs.resize(nz);
     ba.tabs.resize(nz);
@@ -1049,6 +1051,29 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   cp.fwd_c2.s_ident = 1;
   sep_add(cp.fwd_c2, 0, 0, 0, 1.f);
   sep_close_output(cp.fwd_c2);
+  // transposed variants of the s passes (t passes over transposed slices, written back transposed):
+  //  fwd_p1: U[(vt,n)][i_s] = sum_vx C_s,n[i_s][vx] xT_n[vx][vt]     (xT_n = x_n transposed, [vx][vt])
+  //  adj_a2: x_n[vt][vx]   = sum_j C_s,n^T[vx][j] ZT_n[j][vt]        (ZT_n = Z_n transposed, [j][vt])
+  if (ny % 4 == 0) {  // band_m reads whole 16-byte column quads of the transposed slices
+  sep_init(cp.fwd_p1, &cp.id_vt, &cp.cf[0], ny, nx, nz, 1.f);
+  cp.fwd_p1.s_ident = 1;
+  cp.fwd_p1.tout = 1;
+  cp.fwd_p1.out_pitch = (long long)nz * ndet[0];
+  cp.fwd_p1.out_stride = ndet[0];
+  for (int n = 0; n < nz; ++n) {
+    sep_add(cp.fwd_p1, n * nslice, 0, n, 1.f);
+    sep_close_output(cp.fwd_p1);
+  }
+  sep_init(cp.adj_a2, &cp.id_vt, &cp.ca[0], ny, ndet[0], nz, (float)(c1 * c3));
+  cp.adj_a2.s_ident = 1;
+  cp.adj_a2.tout = 1;
+  cp.adj_a2.out_pitch = nx;
+  cp.adj_a2.out_stride = nslice;
+  for (int n = 0; n < nz; ++n) {
+    sep_add(cp.adj_a2, (long long)n * ndet[0] * ny, 0, n, 1.f);
+    sep_close_output(cp.adj_a2);
+  }
+  }
   // lf_transport ops: output b = n*K + k (S1 families), b = k (S3 families); scale 1/V^p
   {
     long long dplane = plen ? nfield : npix;
@@ -1082,9 +1107,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     }
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
-                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2};
+                  &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
   const char* names[] = {"fwd_s1", "fwd_s3", "adj_s3", "adj_s1", "fwd_c", "adj_c1", "adj_c2",
-                         "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a", "fwd_c1", "fwd_c2"};
+                         "xp_s1f", "xp_s1a", "xp_s3f", "xp_s3a", "fwd_c1", "fwd_c2", "fwd_p1", "adj_a2"};
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
   if (dbg) {
     const BandFamily* fams[] = {&cp.s1f[0], &cp.s1f[1], &cp.s1a[0], &cp.s1a[1], &cp.s3f[0], &cp.s3f[1],
@@ -1095,7 +1120,7 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
         std::fprintf(stderr, "[lfm] family %-4s G4 density %.3f  (any-nonzero columns only: %.3f)\n", fn[i],
                      fams[i]->st_nnz / (4 * fams[i]->st_cols_g4), fams[i]->st_nnz / (4 * fams[i]->st_cols_nz));
   }
-  for (int q = 0; q < 13; ++q) {
+  for (int q = 0; q < 15; ++q) {
     if (!ops[q]->fs) continue;
     if (ops[q]->s_ident && ops[q]->ft->want_mseg && ops[q]->n_is % 4 == 0) {
       // identity s over an MSEG t family: the L2-gather kernel needs no shared memory (autotuned later)

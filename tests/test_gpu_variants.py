@@ -94,3 +94,33 @@ def test_forced_t_pass_variants(op_name, variant, monkeypatch):
         lfm.A_forward_rows(plan, c, r0, r1, dev(x), y, ws, path=1)
         yref = op.forward(x.astype(np.float64)).reshape(n_t, -1)
         assert max_rel(host(y).reshape(n_t, -1)[r0:r1], yref[r0:r1]) <= TOL * np.abs(yref).max() / np.abs(yref[r0:r1]).max()
+
+
+@pytest.mark.parametrize("name", ["small_two", "tiny_multi", "tiny_dirac"])
+@pytest.mark.parametrize("transposed", ["0", "1"])
+def test_s_pass_orders(name, transposed, monkeypatch):
+    """Both s-pass orders of the two-pass collapsed path (direct sep kernel, or transpose + band_m with
+    transposed output), forced, against the oracle: forward, adjoint and their row-range forms."""
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config(name)
+    monkeypatch.setenv("LFM_FWD_SPLIT", "1")
+    monkeypatch.setenv("LFM_FWD_T", transposed)
+    monkeypatch.setenv("LFM_ADJ_T", transposed)
+    monkeypatch.delenv("LFM_TUNE_FILE", raising=False)
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    ops = build_system(cfg)
+    x = uniform_volume(cfg["volume"], 0)
+    for c, op in enumerate(ops):
+        n_t = cfg["cameras"][c]["n_t"]
+        y = torch.empty(op.n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, dev(x), y, ws, path=1)
+        assert max_rel(host(y), op.forward(x.astype(np.float64))) <= TOL, (name, c)
+        r = uniform_vector(op.n_pix, 1)
+        g = torch.full((op.n_vox,), 0.5, device="cuda:0")
+        lfm.A_adjoint(plan, c, dev(r), g, ws, accumulate=True, path=1)
+        ref = 0.5 + op.adjoint(r.astype(np.float64))
+        assert max_rel(host(g), ref) <= TOL, (name, c)
+        r0, r1 = n_t // 3, n_t - 3
+        lfm.A_adjoint_rows(plan, c, r0, r1, dev(r), g, ws, path=1)
+        assert max_rel(host(g), op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))) <= TOL, (name, c)
