@@ -84,6 +84,14 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_mw, mw.data(), mw.size() * 4, err)) != LFM_OK) return st;
     bytes += f.m_off.size() * 4 + f.m_seg.size() * 4 + mw.size() * 4;
   }
+  if (!f.m8_off.empty()) {
+    std::vector<float> mw(f.m8_w64.size() + 8);
+    for (size_t i = 0; i < f.m8_w64.size(); ++i) mw[i] = (float)f.m8_w64[i];
+    if ((st = dev_upload(&f.d_m8off, f.m8_off.data(), f.m8_off.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_m8seg, f.m8_seg.data(), f.m8_seg.size() * 4 + 16, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_m8w, mw.data(), mw.size() * 4, err)) != LFM_OK) return st;
+    bytes += f.m8_off.size() * 4 + f.m8_seg.size() * 4 + mw.size() * 4;
+  }
   return dev_upload(&f.d_gw, gw.data(), gw.size() * 4, err);
 }
 
@@ -156,7 +164,8 @@ void free_camera(CameraPlan& cp) {
       fams.push_back(f);
   for (BandFamily* f : fams) {
     dfree(f->d_cnt); dfree(f->d_idx); dfree(f->d_w); dfree(f->d_g); dfree(f->d_gw);
-    dfree(f->d_moff); dfree(f->d_mseg); dfree(f->d_mw);
+    dfree(f->d_moff); dfree(f->d_mseg); dfree(f->d_mw); dfree(f->d_m8off); dfree(f->d_m8seg); dfree(f->d_m8w);
+    f->d_m8off = nullptr; f->d_m8seg = nullptr; f->d_m8w = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
@@ -778,11 +787,28 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
 // L2-gather t-pass over the MSEG form of the t family (identity s): per group a CSR list of dense
 // segments (one per cluster of source rows), so the FMA slots follow the non-zeros (~95% for the
 // slice-interleaved adjoint family, vs ~36-52% with two segments).  Otherwise as band_g_kernel.
-template <int TS, int TT, int NT, int UNR, bool TOUT>
-__global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
+template <int GR>
+__device__ __forceinline__ void fma_gr(float (&acc)[GR][4], const float* __restrict__ w, float4 u) {
+#pragma unroll
+  for (int q4 = 0; q4 < GR / 4; ++q4) {
+    const float4 w4 = __ldg(reinterpret_cast<const float4*>(w) + q4);
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      acc[4 * q4 + r][0] = fmaf(wv[r], u.x, acc[4 * q4 + r][0]);
+      acc[4 * q4 + r][1] = fmaf(wv[r], u.y, acc[4 * q4 + r][1]);
+      acc[4 * q4 + r][2] = fmaf(wv[r], u.z, acc[4 * q4 + r][2]);
+      acc[4 * q4 + r][3] = fmaf(wv[r], u.w, acc[4 * q4 + r][3]);
+    }
+  }
+}
+
+// GR = rows per MSEG group (4 or 8): each source load feeds GR x 4 FMAs.
+template <int TS, int TT, int NT, int UNR, bool TOUT, int GR>
+__global__ void __launch_bounds__(NT, (GR == 8 ? 512 : 1024) / NT) band_m_kernel(SepArgs a) {
   constexpr int NQ = TS / 4;
   constexpr int GSTEP = NT / NQ;
-  constexpr int NG = TT / 4;
+  constexpr int NG = TT / GR;
   constexpr int GP = NG / GSTEP;
   static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
   const int tid = threadIdx.x;
@@ -792,11 +818,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
   const int col = os0 + quad * 4;
   if (col >= a.n_is) return;  // n_is % 4 == 0 (checked at tuning time): whole quads in or out
   const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  float acc[GP][4][4];
+  const int ngroups = (a.n_ot + GR - 1) / GR;
+  float acc[GP][GR][4];
 #pragma unroll
   for (int j = 0; j < GP; ++j)
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < GR; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
   for (int e = e0; e < e1; ++e) {
@@ -805,17 +832,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
 #pragma unroll
     for (int j = 0; j < GP; ++j) {
       const int g = ty * NG + gsub + j * GSTEP;
-      if (g >= a.t_ngroups) continue;
-      const size_t gi = (size_t)term.t_tab * a.t_ngroups + g;
+      if (g >= ngroups) continue;
+      const size_t gi = (size_t)term.t_tab * ngroups + g;
       const int s0 = __ldg(a.t_moff + gi), s1 = __ldg(a.t_moff + gi + 1);
       for (int sg = s0; sg < s1; ++sg) {
         const int4 gd = __ldg(a.t_mseg + sg);
         const int p0 = max(0, a.win_r0 - gd.x), p1 = min(gd.y, a.win_r1 - gd.x);
-        const float4* wp = reinterpret_cast<const float4*>(a.t_mw + gd.z);
+        const float* wp = a.t_mw + gd.z;
         const float* up = src + (size_t)gd.x * a.src_pitch;
 #pragma unroll UNR
         for (int p = p0; p < p1; ++p)
-          fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.src_pitch)));
+          fma_gr<GR>(acc[j], wp + GR * p, __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.src_pitch)));
       }
     }
   }
@@ -824,28 +851,32 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
     // transposed output: element (row, col) at outb[col * out_pitch + row]; 4 consecutive rows per store
 #pragma unroll
     for (int j = 0; j < GP; ++j) {
-      const int row0 = ot0 + 4 * (gsub + j * GSTEP);
-      if (row0 >= a.n_ot) continue;
-      const bool vec = row0 + 3 < a.n_ot && ((a.n_ot & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (col + c >= a.n_os) continue;
-        float* p = outb + (size_t)(col + c) * a.out_pitch + row0;
-        float v[4];
+      for (int r4 = 0; r4 < GR / 4; ++r4) {
+        const int row0 = ot0 + GR * (gsub + j * GSTEP) + 4 * r4;
+        if (row0 >= a.n_ot) continue;
+        const bool vec =
+            row0 + 3 < a.n_ot && ((a.n_ot & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) v[r] = a.out_scale * acc[j][r][c];
-        if (vec) {
-          float4 o = make_float4(v[0], v[1], v[2], v[3]);
-          if (a.accumulate) {
-            const float4 q = *reinterpret_cast<float4*>(p);
-            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-          }
-          *reinterpret_cast<float4*>(p) = o;
-        } else {
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          float* p = outb + (size_t)(col + c) * a.out_pitch + row0;
+          float v[4];
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            if (row0 + r >= a.n_ot) continue;
-            p[r] = a.accumulate ? p[r] + v[r] : v[r];
+          for (int r = 0; r < 4; ++r) v[r] = a.out_scale * acc[j][4 * r4 + r][c];
+          if (vec) {
+            float4 o = make_float4(v[0], v[1], v[2], v[3]);
+            if (a.accumulate) {
+              const float4 q = *reinterpret_cast<float4*>(p);
+              o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+            }
+            *reinterpret_cast<float4*>(p) = o;
+          } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              if (row0 + r >= a.n_ot) continue;
+              p[r] = a.accumulate ? p[r] + v[r] : v[r];
+            }
           }
         }
       }
@@ -856,8 +887,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
 #pragma unroll
   for (int j = 0; j < GP; ++j) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+    for (int r = 0; r < GR; ++r) {
+      const int row = ot0 + GR * (gsub + j * GSTEP) + r;
       if (row >= a.n_ot) continue;
       float* p = outb + (size_t)row * a.out_pitch + col;
       float v[4];
@@ -882,16 +913,32 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_m_kernel(SepArgs a) {
 }
 
 template <int TS, int TT, int NT>
+static lfm_status launch_band_m8(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
+  if (tout) {
+    if (unr == 8)
+      band_m_kernel<TS, TT, NT, 8, true, 8><<<grid, NT, 0, s>>>(a);
+    else
+      band_m_kernel<TS, TT, NT, 4, true, 8><<<grid, NT, 0, s>>>(a);
+  } else if (unr == 8) {
+    band_m_kernel<TS, TT, NT, 8, false, 8><<<grid, NT, 0, s>>>(a);
+  } else {
+    band_m_kernel<TS, TT, NT, 4, false, 8><<<grid, NT, 0, s>>>(a);
+  }
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_m_kernel launch", err);
+}
+
+template <int TS, int TT, int NT>
 static lfm_status launch_band_m(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
   if (tout) {
     if (unr == 8)
-      band_m_kernel<TS, TT, NT, 8, true><<<grid, NT, 0, s>>>(a);
+      band_m_kernel<TS, TT, NT, 8, true, 4><<<grid, NT, 0, s>>>(a);
     else
-      band_m_kernel<TS, TT, NT, 4, true><<<grid, NT, 0, s>>>(a);
+      band_m_kernel<TS, TT, NT, 4, true, 4><<<grid, NT, 0, s>>>(a);
   } else if (unr == 8) {
-    band_m_kernel<TS, TT, NT, 8, false><<<grid, NT, 0, s>>>(a);
+    band_m_kernel<TS, TT, NT, 8, false, 4><<<grid, NT, 0, s>>>(a);
   } else {
-    band_m_kernel<TS, TT, NT, 4, false><<<grid, NT, 0, s>>>(a);
+    band_m_kernel<TS, TT, NT, 4, false, 4><<<grid, NT, 0, s>>>(a);
   }
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_m_kernel launch", err);
@@ -974,9 +1021,9 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.out_stride = op.out_stride ? op.out_stride : (long long)op.n_os * op.n_ot;
   a.src_pitch = op.src_pitch ? op.src_pitch : op.n_is;
   a.out_pitch = op.out_pitch ? op.out_pitch : op.n_os;
-  a.t_moff = op.ft->d_moff;
-  a.t_mseg = reinterpret_cast<const int4*>(op.ft->d_mseg);
-  a.t_mw = op.ft->d_mw;
+  a.t_moff = op.mgrp == 8 ? op.ft->d_m8off : op.ft->d_moff;
+  a.t_mseg = reinterpret_cast<const int4*>(op.mgrp == 8 ? op.ft->d_m8seg : op.ft->d_mseg);
+  a.t_mw = op.mgrp == 8 ? op.ft->d_m8w : op.ft->d_mw;
   a.terms = op.d_terms;
   a.offs = op.d_offs + b0;
   a.s_g = reinterpret_cast<const int4*>(op.fs->d_g);
@@ -1053,7 +1100,18 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   }
   if (op.kind == 3) {
     // L2-gather t-pass over MSEG segments: identity s, no shared memory
-    if (!op.ft->d_moff) { err = "band_m: t family has no MSEG form"; return LFM_E_INVALID; }
+    if (!(op.mgrp == 8 ? op.ft->d_m8off : op.ft->d_moff)) { err = "band_m: t family has no MSEG form"; return LFM_E_INVALID; }
+    if (op.mgrp == 8) {
+#define LFM_BM8_CASE(TS_, TT_, NT_) \
+      if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_m8<TS_, TT_, NT_>(a, grid, s, err, op.stages, op.tout);
+      LFM_BM8_CASE(128, 32, 128)
+      LFM_BM8_CASE(128, 16, 64)
+      LFM_BM8_CASE(128, 64, 256)
+      LFM_BM8_CASE(64, 32, 64)
+#undef LFM_BM8_CASE
+      err = "unsupported band_m (8-row groups) tile";
+      return LFM_E_INVALID;
+    }
 #define LFM_BM_CASE(TS_, TT_, NT_) \
     if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_m<TS_, TT_, NT_>(a, grid, s, err, op.stages, op.tout);
     LFM_BM_CASE(128, 32, 256)
@@ -1366,8 +1424,8 @@ static std::string tune_key(const CameraPlan& cp) {
   unsigned long long h = 1469598103934665603ull;
   for (size_t i = 0; i < sizeof(cp.cam); ++i) h = (h ^ b[i]) * 1099511628211ull;
   char buf[96];
-  // v4: the line format carries kernel kind, pipeline stages and the timed ms; older caches are ignored
-  std::snprintf(buf, sizeof(buf), "v4_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
+  // v5: the line format carries kernel kind, pipeline stages, the timed ms and MSEG group rows
+  std::snprintf(buf, sizeof(buf), "v5_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
   return buf;
 }
 
@@ -1427,10 +1485,11 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       int ts, tt, nt, nb, stg;
       int kind = 0, stages = 2;
       float ms = 0;
-      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d %f", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages,
-                      &ms) == 10 &&
+      int mg = 4;
+      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d %f %d", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages,
+                      &ms, &mg) == 11 &&
           key == k && std::string(o) == names[q]) {
-        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages; op.mgrp = mg;
         op_best[q] = ms;
         fill_sep_geometry(op);
         free_sep_dev(op);
@@ -1444,7 +1503,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     const SepOp keep = op;  // cost-model choice (device pointers of `op` are replaced below)
     int bts = keep.ts, btt = keep.tt, bnt = keep.nt, bnb = keep.nb, bst = keep.stage;
     float best = 1e30f;
-    int bkind = keep.kind, bstages = keep.stages;
+    int bkind = keep.kind, bstages = keep.stages, bmgrp = keep.mgrp;
     if (op.s_ident && (op.n_is % 4) == 0) {
       for (auto& c : cand) {
         if (op.tout) break;  // transposed output: band_m only
@@ -1501,14 +1560,17 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         }
       }
       op.kind = 0;
-      const int mcand[][3] = {{128, 32, 256}, {128, 16, 128}, {128, 8, 64}, {64, 32, 128}, {64, 16, 64}, {32, 32, 64}};
+      const int mcand[][4] = {{128, 32, 256, 4}, {128, 16, 128, 4}, {128, 8, 64, 4},  {64, 32, 128, 4},
+                              {64, 16, 64, 4},   {32, 32, 64, 4},   {128, 32, 128, 8}, {128, 16, 64, 8},
+                              {128, 64, 256, 8}, {64, 32, 64, 8}};
       for (auto& c : mcand) {
         if (st != LFM_OK || !op.ft->want_mseg) break;
+        if (c[3] == 8 && op.ft->m8_off.empty()) continue;
         bool aligned = true;
         for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
         if (!aligned) break;
         for (int unr : {4, 8}) {
-          op.kind = 3; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr;
+          op.kind = 3; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr; op.mgrp = c[3];
           fill_sep_geometry(op);
           free_sep_dev(op);
           size_t bytes = 0;
@@ -1524,7 +1586,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
             if (rep > 0) tot += ms;
           }
           if (!ok || cudaGetLastError() != cudaSuccess) continue;
-          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 3; bstages = unr; }
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 3; bstages = unr; bmgrp = c[3]; }
         }
       }
       op.kind = 0;
@@ -1557,19 +1619,19 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       }
       if (st != LFM_OK) break;
     }
-    op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst; op.kind = bkind; op.stages = bstages;
+    op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst; op.kind = bkind; op.stages = bstages; op.mgrp = bmgrp;
     fill_sep_geometry(op);
     free_sep_dev(op);
     size_t bytes = 0;
     if (st == LFM_OK) st = upload_sep(op, bytes, err);
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
-      std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, best / 2, n_out);
+      std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d grp %d (%.3f ms for %d outputs)\n",
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
-        std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
-                     op.kind, op.stages, op_best[q]);
+        std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
+                     op.kind, op.stages, op_best[q], op.mgrp);
         std::fclose(f);
       }
     }

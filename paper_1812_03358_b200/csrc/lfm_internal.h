@@ -54,6 +54,12 @@ struct BandFamily {
   int32_t* d_moff = nullptr;
   int32_t* d_mseg = nullptr;
   float* d_mw = nullptr;
+  // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
+  std::vector<int32_t> m8_off, m8_seg;
+  std::vector<double> m8_w64;
+  int32_t* d_m8off = nullptr;
+  int32_t* d_m8seg = nullptr;
+  float* d_m8w = nullptr;
   // density statistics (LFM_DEBUG): non-zeros, G4 slot columns, columns with any non-zero
   double st_nnz = 0, st_cols_g4 = 0, st_cols_nz = 0, st_msegs = 0, st_cols_m = 0;
 };
@@ -98,6 +104,7 @@ struct SepOp {
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)
   int tout = 0;                    // band_m only: write element (row, col) at col * out_pitch + row
+  int mgrp = 4;                    // band_m only: rows per MSEG group (4 or 8)
   int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile

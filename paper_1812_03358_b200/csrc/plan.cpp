@@ -341,6 +341,95 @@ struct FamilyBuilder {
   }
 };
 
+// MSEG form with groups of 8 rows (segments split at zero runs >= 2 source cells, weights 8 per cell).
+static void build_mseg8(BandFamily& f) {
+  const int G = 8;
+  const int ng = (f.n_rows + G - 1) / G;
+  f.m8_off.assign((size_t)f.n_tables * ng + 1, 0);
+  f.m8_seg.clear();
+  f.m8_w64.clear();
+  std::vector<double> dense;
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int g = 0; g < ng; ++g) {
+      f.m8_off[(size_t)m * ng + g] = (int)(f.m8_seg.size() / 4);
+      int lo = 1 << 30, hi = -1;
+      for (int r = G * g; r < std::min(f.n_rows, G * g + G); ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        if (!f.len[idx]) continue;
+        lo = std::min(lo, (int)f.start[idx]);
+        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
+      }
+      if (hi < 0) continue;
+      const int W = hi - lo;
+      dense.assign((size_t)W * G, 0.0);
+      for (int r = G * g; r < std::min(f.n_rows, G * g + G); ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e) dense[(size_t)(f.start[idx] + e - lo) * G + (r - G * g)] = f.w64[idx * f.taps + e];
+      }
+      auto zero = [&](int c) {
+        for (int q = 0; q < G; ++q)
+          if (dense[(size_t)c * G + q] != 0.0) return false;
+        return true;
+      };
+      int p = 0;
+      while (p < W) {
+        while (p < W && zero(p)) ++p;
+        if (p >= W) break;
+        int a = p, last = p;
+        while (p < W) {
+          if (!zero(p)) { last = p; ++p; continue; }
+          int zs = p;
+          while (p < W && zero(p)) ++p;
+          if (p - zs >= 2 || p >= W) break;
+        }
+        f.m8_seg.push_back(lo + a);
+        f.m8_seg.push_back(last - a + 1);
+        f.m8_seg.push_back((int)f.m8_w64.size());
+        f.m8_seg.push_back(0);
+        for (int c = a; c <= last; ++c)
+          for (int q = 0; q < G; ++q) f.m8_w64.push_back(dense[(size_t)c * G + q]);
+      }
+    }
+  f.m8_off[(size_t)f.n_tables * ng] = (int)(f.m8_seg.size() / 4);
+}
+
+// Debug statistic: density nnz / (G * MSEG columns) of groups of G rows (split at zero runs >= 2).
+static double mseg_density(const BandFamily& f, int G) {
+  double nnz = 0, cols = 0;
+  std::vector<char> any;
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int g0 = 0; g0 < f.n_rows; g0 += G) {
+      int lo = 1 << 30, hi = -1;
+      for (int r = g0; r < std::min(f.n_rows, g0 + G); ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        if (!f.len[idx]) continue;
+        lo = std::min(lo, (int)f.start[idx]);
+        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
+      }
+      if (hi < 0) continue;
+      any.assign(hi - lo, 0);
+      for (int r = g0; r < std::min(f.n_rows, g0 + G); ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e)
+          if (f.w64[idx * f.taps + e] != 0.0) { any[f.start[idx] + e - lo] = 1; nnz += 1; }
+      }
+      int p = 0, W = hi - lo;
+      while (p < W) {
+        while (p < W && !any[p]) ++p;
+        if (p >= W) break;
+        int a = p, last = p;
+        while (p < W) {
+          if (any[p]) { last = p; ++p; continue; }
+          int zs = p;
+          while (p < W && !any[p]) ++p;
+          if (p - zs >= 2 || p >= W) break;
+        }
+        cols += last - a + 1;
+      }
+    }
+  return nnz / (G * cols);
+}
+
 // Slice-interleaved forms of a per-slice family f (n_tables = nz, rows r, sources j):
 //  rows_by_slice: one table, row (r, n) at r*nz + n = table n's row r (same sources).  Groups of 4 rows
 //                 are then 4 neighbouring slices of one output row, whose bands nearly coincide.
@@ -1005,8 +1094,10 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
   // slice-interleaved t families of the two-pass collapsed path, with their MSEG segment lists
   cp.ca1n.want_mseg = 1;
   make_rows_by_slice(cp.ca1n, cp.ca[1]);
+  build_mseg8(cp.ca1n);
   cp.cf1n.want_mseg = 1;
   make_cols_by_slice(cp.cf1n, cp.cf[1]);
+  build_mseg8(cp.cf1n);
   if (std::getenv("LFM_DEBUG")) {
     const BandFamily* fs[] = {&cp.ca1n, &cp.cf1n, &cp.ca[1], &cp.cf[1], &cp.ca[0], &cp.cf[0]};
     const char* nm[] = {"ca1 rows-by-slice", "cf1 cols-by-slice", "ca1", "cf1", "ca0", "cf0"};
@@ -1015,6 +1106,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
                    fs[i]->st_nnz / (4 * fs[i]->st_cols_g4), fs[i]->st_nnz / (4 * fs[i]->st_cols_m),
                    fs[i]->st_msegs / ((double)fs[i]->n_tables * fs[i]->n_groups), fs[i]->st_cols_m / fs[i]->st_msegs,
                    fs[i]->st_nnz / (4 * fs[i]->st_cols_nz));
+    for (int G : {4, 8, 16})
+      std::fprintf(stderr, "[lfm] MSEG density with %2d-row groups: ca1n %.3f  cf1n %.3f  ca0 %.3f  cf0 %.3f\n", G,
+                   mseg_density(cp.ca1n, G), mseg_density(cp.cf1n, G), mseg_density(cp.ca[0], G), mseg_density(cp.cf[0], G));
   }
   // collapsed path
   sep_init(cp.fwd_c, &cp.cf[0], &cp.cf[1], nx, ny, 1, (float)(c1 * c3));
@@ -1135,14 +1229,14 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     std::string env = std::string("LFM_FORCE_") + names[q];
     if (const char* f = std::getenv(env.c_str())) {
       // optional 6th/7th fields: kind (1 = streaming band_t kernel, identity-s ops only), stages
-      int ts, tt, nt, nb, stg, kind = 0, stages = 2;
-      if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages) >= 5) {
+      int ts, tt, nt, nb, stg, kind = 0, stages = 2, mg = 4;
+      if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages, &mg) >= 5) {
         SepOp& op = *ops[q];
-        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages;
+        op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages; op.mgrp = mg;
         fill_sep_geometry(op);
         if (kind >= 1) {
           bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
-                    (kind != 3 || op.ft->want_mseg);
+                    (kind != 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty()));
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
           if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
         } else if (sep_smem(op, nb) > (size_t)220 * 1024) {

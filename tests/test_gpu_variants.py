@@ -52,6 +52,8 @@ VARIANTS = {
     "band_m_128x32_u8": "128,32,256,1,0,3,8",
     "band_m_64x16_u8": "64,16,64,1,0,3,8",
     "band_m_32x32_u4": "32,32,64,1,0,3,4",
+    "band_m8_128x32_u4": "128,32,128,1,0,3,4,8",
+    "band_m8_64x32_u8": "64,32,64,1,0,3,8,8",
     "band_g_128x32_u8": "128,32,256,1,0,2,8",
     "band_g_64x32_u4": "64,32,128,1,0,2,4",
     "band_t_128x32_s2": "128,32,288,1,1,1,2",
