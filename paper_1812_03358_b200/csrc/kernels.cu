@@ -84,6 +84,16 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_mw, mw.data(), mw.size() * 4, err)) != LFM_OK) return st;
     bytes += f.m_off.size() * 4 + f.m_seg.size() * 4 + mw.size() * 4;
   }
+  if (!f.f_off.empty()) {
+    std::vector<float> fw(f.f_w64.size() + 16);
+    for (size_t i = 0; i < f.f_w64.size(); ++i) fw[i] = (float)f.f_w64[i];
+    std::vector<int32_t> fr(f.f_row);
+    fr.resize(fr.size() + 8, 0);
+    if ((st = dev_upload(&f.d_foff, f.f_off.data(), f.f_off.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_frow, fr.data(), fr.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_fw, fw.data(), fw.size() * 4, err)) != LFM_OK) return st;
+    bytes += f.f_off.size() * 4 + fr.size() * 4 + fw.size() * 4;
+  }
   if (!f.m8_off.empty()) {
     std::vector<float> mw(f.m8_w64.size() + 8);
     for (size_t i = 0; i < f.m8_w64.size(); ++i) mw[i] = (float)f.m8_w64[i];
@@ -121,6 +131,66 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
   st = dev_upload(&op.d_fp_s, vs.data(), vs.size() * sizeof(TileT), err);
   if (st != LFM_OK) return st;
   bytes += op.terms.size() * sizeof(Term) + (vs.size() + vt.size()) * sizeof(TileT);
+  if (op.kind == 4) {
+    // band_s chunk lists: per (t-table, tile_y) the union of the tile's MSEG segments (gaps <= 2 rows
+    // merged), cut into chunks of <= op.chunk source rows, in increasing row order
+    const int ng = ft.n_groups, NG = op.tt / 4;
+    std::vector<int2> ch;
+    std::vector<int32_t> off((size_t)ft.n_tables * op.nty + 1, 0);
+    std::vector<std::pair<int, int>> iv;
+    for (int m = 0; m < ft.n_tables; ++m)
+      for (int y = 0; y < op.nty; ++y) {
+        off[(size_t)m * op.nty + y] = (int)ch.size();
+        iv.clear();
+        for (int g = y * NG; g < std::min(ng, y * NG + NG); ++g) {
+          size_t gi = (size_t)m * ng + g;
+          for (int sg = ft.m_off[gi]; sg < ft.m_off[gi + 1]; ++sg)
+            iv.push_back({ft.m_seg[4 * (size_t)sg], ft.m_seg[4 * (size_t)sg] + ft.m_seg[4 * (size_t)sg + 1]});
+        }
+        std::sort(iv.begin(), iv.end());
+        int a = -1, b = -1;
+        auto flush = [&]() {
+          for (int lo = a; lo < b; lo += op.chunk) ch.push_back(make_int2(lo, std::min(op.chunk, b - lo)));
+        };
+        for (auto& v : iv) {
+          if (a < 0) { a = v.first; b = v.second; continue; }
+          if (v.first <= b + 2) { b = std::max(b, v.second); continue; }
+          flush();
+          a = v.first; b = v.second;
+        }
+        if (a >= 0) flush();
+      }
+    off.back() = (int)ch.size();
+    // per (chunk, group): the group's weights for the chunk's rows form one contiguous float4 range
+    // (segment weight blocks are stored back to back in row order)
+    std::vector<int2> cw(ch.size() * NG + 1, make_int2(0, 0));
+    for (int m = 0; m < ft.n_tables; ++m)
+      for (int y = 0; y < op.nty; ++y)
+        for (int c = off[(size_t)m * op.nty + y]; c < off[(size_t)m * op.nty + y + 1]; ++c) {
+          const int cs = ch[c].x, ce = ch[c].x + ch[c].y;
+          for (int k = 0; k < NG; ++k) {
+            const int g = y * NG + k;
+            if (g >= ng) continue;
+            size_t gi = (size_t)m * ng + g;
+            int f0 = -1, f1 = -1;
+            for (int sg = ft.m_off[gi]; sg < ft.m_off[gi + 1]; ++sg) {
+              const int j0 = ft.m_seg[4 * (size_t)sg], w = ft.m_seg[4 * (size_t)sg + 1], wo = ft.m_seg[4 * (size_t)sg + 2];
+              const int a0 = std::max(j0, cs), a1 = std::min(j0 + w, ce);
+              if (a0 >= a1) continue;
+              if (f0 < 0) f0 = wo / 4 + (a0 - j0);
+              f1 = wo / 4 + (a1 - j0);
+            }
+            if (f0 >= 0) cw[(size_t)c * NG + k] = make_int2(f0, f1 - f0);
+          }
+        }
+    ch.push_back(make_int2(0, 0));
+    if ((st = dev_upload(&op.d_chunks, reinterpret_cast<int32_t*>(ch.data()), ch.size() * sizeof(int2), err)) != LFM_OK)
+      return st;
+    if ((st = dev_upload(&op.d_chunk_w, reinterpret_cast<int32_t*>(cw.data()), cw.size() * sizeof(int2), err)) != LFM_OK)
+      return st;
+    if ((st = dev_upload(&op.d_chunk_off, off.data(), off.size() * 4, err)) != LFM_OK) return st;
+    bytes += ch.size() * sizeof(int2) + off.size() * 4;
+  }
   return dev_upload(&op.d_fp_t, vt.data(), vt.size() * sizeof(TileT), err);
 }
 
@@ -166,14 +236,18 @@ void free_camera(CameraPlan& cp) {
     dfree(f->d_cnt); dfree(f->d_idx); dfree(f->d_w); dfree(f->d_g); dfree(f->d_gw);
     dfree(f->d_moff); dfree(f->d_mseg); dfree(f->d_mw); dfree(f->d_m8off); dfree(f->d_m8seg); dfree(f->d_m8w);
     f->d_m8off = nullptr; f->d_m8seg = nullptr; f->d_m8w = nullptr;
+    dfree(f->d_foff); dfree(f->d_frow); dfree(f->d_fw);
+    f->d_foff = nullptr; f->d_frow = nullptr; f->d_fw = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
   for (SepOp* op : ops) {
-    dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t);
+    dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t); dfree(op->d_chunks);
+    dfree(op->d_chunk_off); dfree(op->d_chunk_w);
     op->d_terms = nullptr; op->d_offs = nullptr; op->d_fp_s = nullptr; op->d_fp_t = nullptr;
+    op->d_chunks = nullptr; op->d_chunk_off = nullptr; op->d_chunk_w = nullptr;
   }
   for (int p = 0; p < 3; ++p)
     for (int d = 0; d < 2; ++d) {
@@ -201,6 +275,12 @@ struct SepArgs {
   long long out_stride;
   long long src_pitch;  // floats between source rows
   long long out_pitch;  // floats between output rows
+  const int2* chunks;     // band_s_kernel chunk lists
+  const int32_t* chunk_off;
+  const int2* chunk_w;
+  const int32_t* t_foff;  // flat MSEG entries (band_f_kernel)
+  const int4* t_frow;
+  const float4* t_fw;
   const int32_t* t_moff;  // MSEG t family (band_m_kernel)
   const int4* t_mseg;
   const float* t_mw;
@@ -912,6 +992,295 @@ __global__ void __launch_bounds__(NT, (GR == 8 ? 512 : 1024) / NT) band_m_kernel
   }
 }
 
+// Streaming MSEG t-pass for identity-s ops (TS = 128 columns, one consumer warp per group of 4 output
+// rows, NG groups per CTA, plus one producer warp).  The producer streams the union of the tile's
+// segment rows, chunk by chunk (cp.async.bulk per source row, completion on an mbarrier), into a
+// STAGES-deep ring; every consumer warp walks its own sorted segment list alongside the chunks, so each
+// source row is read from L2 once per CTA and shared by all NG groups through shared memory.
+template <int NG, int K, int STAGES>
+__global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
+  constexpr int TS = 128;
+  constexpr int SLOT = K * TS + NG * K * 4;  // U rows, then per group K weight float4s
+  extern __shared__ __align__(16) float smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int os0 = tx * TS;
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NG) {
+    // ---------------- producer warp: all chunks of all terms, in order
+    const int ncol = min(TS, a.n_is - os0);
+    const uint32_t row_bytes = (uint32_t)ncol * 4;
+    int it = 0;
+    for (int e = e0; e < e1; ++e) {
+      const Term term = a.terms[e];
+      const int c0 = a.chunk_off[(size_t)term.t_tab * a.nty + ty], c1 = a.chunk_off[(size_t)term.t_tab * a.nty + ty + 1];
+      for (int c = c0; c < c1; ++c, ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        const int2 ck = a.chunks[c];
+        float* slot = smem + (size_t)s * SLOT;
+        const int wlo = max(ck.x, a.win_r0), whi = min(ck.x + ck.y, a.win_r1);
+        const int nrow = max(0, whi - wlo);
+        const int2 cw = lane < NG ? a.chunk_w[(size_t)c * NG + lane] : make_int2(0, 0);
+        uint32_t wbytes = (uint32_t)cw.y * 16;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wbytes += __shfl_xor_sync(0xffffffffu, wbytes, o);
+        if (nrow < ck.y) {  // rows outside the source window read as zero
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int r = 0; r < ck.y; ++r) {
+            const int row = ck.x + r;
+            if (row >= wlo && row < whi) continue;
+            for (int q = lane; q < TS / 4; q += 32) reinterpret_cast<float4*>(slot + r * TS)[q] = z;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * row_bytes + wbytes);
+        __syncwarp();
+        const float* src = a.src + term.src_off + (size_t)wlo * a.src_pitch + os0;
+        float* dst = slot + (wlo - ck.x) * TS;
+        for (int r = lane; r < nrow; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.src_pitch, row_bytes, &full[s]);
+        if (cw.y > 0) bulk_g2s(slot + K * TS + lane * K * 4, a.t_mw + 4 * (size_t)cw.x, (uint32_t)cw.y * 16, &full[s]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warp `warp` = group ty*NG + warp
+  const int g = ty * NG + warp;
+  const bool gvalid = g < a.t_ngroups;
+  float acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+  int it = 0;
+  for (int e = e0; e < e1; ++e) {
+    const Term term = a.terms[e];
+    const int c0 = a.chunk_off[(size_t)term.t_tab * a.nty + ty], c1 = a.chunk_off[(size_t)term.t_tab * a.nty + ty + 1];
+    const size_t gi = (size_t)term.t_tab * a.t_ngroups + g;
+    int si = gvalid ? __ldg(a.t_moff + gi) : 0;
+    const int s_end = gvalid ? __ldg(a.t_moff + gi + 1) : 0;
+    int4 sd = si < s_end ? __ldg(a.t_mseg + si) : make_int4(0, 0, 0, 0);
+    for (int c = c0; c < c1; ++c, ++it) {
+      const int s = it % STAGES;
+      const int2 ck = a.chunks[c];
+      const int wf0 = a.chunk_w[(size_t)c * NG + warp].x;  // first weight float4 of this group in the slot
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      const float* slot = smem + (size_t)s * SLOT;
+      const float4* wsl = reinterpret_cast<const float4*>(slot + K * TS + warp * K * 4);
+      const int cend = ck.x + ck.y;
+      while (si < s_end && sd.x < cend) {
+        const int pa = max(sd.x, ck.x), pb = min(sd.x + sd.y, cend);
+        const float4* wp = wsl + (sd.z / 4 - sd.x - wf0);
+        const float* up = slot + lane * 4 - ck.x * TS;
+#pragma unroll 4
+        for (int p = pa; p < pb; ++p) fma4x4(acc, wp[p], *reinterpret_cast<const float4*>(up + p * TS));
+        if (sd.x + sd.y > cend) break;  // segment continues in the next chunk
+        ++si;
+        if (si < s_end) sd = __ldg(a.t_mseg + si);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  if (!gvalid) return;
+  const int col = os0 + lane * 4;
+  if (col >= a.n_os) return;
+  float* outb = a.out + (size_t)b * a.out_stride;
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int row = 4 * g + r;
+    if (row >= a.n_ot) continue;
+    float* p = outb + (size_t)row * a.out_pitch + col;
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[r][c];
+    if (vec) {
+      float4 o = make_float4(v[0], v[1], v[2], v[3]);
+      if (a.accumulate) {
+        const float4 q = *reinterpret_cast<float4*>(p);
+        o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+      }
+      *reinterpret_cast<float4*>(p) = o;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (col + c >= a.n_os) continue;
+        p[c] = a.accumulate ? p[c] + v[c] : v[c];
+      }
+    }
+  }
+}
+
+template <int NG, int K, int STAGES>
+static lfm_status launch_band_s(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err) {
+  auto kern = band_s_kernel<NG, K, STAGES>;
+  const size_t smem = (size_t)STAGES * (K * 128 + NG * K * 4) * 4;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_s_kernel)", err);
+    configured = true;
+  }
+  kern<<<grid, (NG + 1) * 32, smem, s>>>(a);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_s_kernel launch", err);
+}
+
+// Flat L2-gather t-pass (identity s): per group of 4 output rows a padded list of entries
+// (source row, 4 weights); the loop runs over blocks of 4 entries with the rows fetched as one int4,
+// so 4 x (16-byte source load + 16-byte weight load) per block are independent and the unroll keeps
+// UNR blocks of loads in flight.  Rows outside [win_r0, win_r1) contribute zero (predicated loads).
+template <int TS, int TT, int NT, int UNR, bool TOUT>
+__global__ void __launch_bounds__(NT, 1024 / NT) band_f_kernel(SepArgs a) {
+  constexpr int NQ = TS / 4;
+  constexpr int GSTEP = NT / NQ;
+  constexpr int NG = TT / 4;
+  constexpr int GP = NG / GSTEP;
+  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
+  const int tid = threadIdx.x;
+  const int quad = tid % NQ, gsub = tid / NQ;
+  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int os0 = tx * TS, ot0 = ty * TT;
+  const int col = os0 + quad * 4;
+  if (col >= a.n_is) return;
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  const bool windowed = a.win_r0 > 0 || a.win_r1 < a.n_it;
+  float acc[GP][4][4];
+#pragma unroll
+  for (int j = 0; j < GP; ++j)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
+  for (int e = e0; e < e1; ++e) {
+    const Term term = a.terms[e];
+    const float* src = a.src + term.src_off + col;
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+      const int g = ty * NG + gsub + j * GSTEP;
+      if (g >= a.t_ngroups) continue;
+      const size_t gi = (size_t)term.t_tab * a.t_ngroups + g;
+      const int q0 = __ldg(a.t_foff + gi) / 4, q1 = __ldg(a.t_foff + gi + 1) / 4;
+      if (!windowed) {
+#pragma unroll UNR
+        for (int q = q0; q < q1; ++q) {
+          const int4 rw = __ldg(a.t_frow + q);
+          const float4 u0 = __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.x * a.src_pitch));
+          const float4 u1 = __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.y * a.src_pitch));
+          const float4 u2 = __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.z * a.src_pitch));
+          const float4 u3 = __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.w * a.src_pitch));
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 0), u0);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 1), u1);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 2), u2);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 3), u3);
+        }
+      } else {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll UNR
+        for (int q = q0; q < q1; ++q) {
+          const int4 rw = __ldg(a.t_frow + q);
+          const bool i0 = rw.x >= a.win_r0 && rw.x < a.win_r1, i1 = rw.y >= a.win_r0 && rw.y < a.win_r1;
+          const bool i2 = rw.z >= a.win_r0 && rw.z < a.win_r1, i3 = rw.w >= a.win_r0 && rw.w < a.win_r1;
+          const float4 u0 = i0 ? __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.x * a.src_pitch)) : z;
+          const float4 u1 = i1 ? __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.y * a.src_pitch)) : z;
+          const float4 u2 = i2 ? __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.z * a.src_pitch)) : z;
+          const float4 u3 = i3 ? __ldg(reinterpret_cast<const float4*>(src + (size_t)rw.w * a.src_pitch)) : z;
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 0), u0);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 1), u1);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 2), u2);
+          fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 3), u3);
+        }
+      }
+    }
+  }
+  float* outb = a.out + (size_t)b * a.out_stride;
+  if (TOUT) {
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+      const int row0 = ot0 + 4 * (gsub + j * GSTEP);
+      if (row0 >= a.n_ot) continue;
+      const bool vec = row0 + 3 < a.n_ot && ((a.n_ot & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (col + c >= a.n_os) continue;
+        float* p = outb + (size_t)(col + c) * a.out_pitch + row0;
+        float v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = a.out_scale * acc[j][r][c];
+        if (vec) {
+          float4 o = make_float4(v[0], v[1], v[2], v[3]);
+          if (a.accumulate) {
+            const float4 q = *reinterpret_cast<float4*>(p);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4*>(p) = o;
+        } else {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            if (row0 + r >= a.n_ot) continue;
+            p[r] = a.accumulate ? p[r] + v[r] : v[r];
+          }
+        }
+      }
+    }
+    return;
+  }
+  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+  for (int j = 0; j < GP; ++j) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
+      if (row >= a.n_ot) continue;
+      float* p = outb + (size_t)row * a.out_pitch + col;
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
+      if (vec) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (a.accumulate) {
+          const float4 q = *reinterpret_cast<float4*>(p);
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(p) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (col + c >= a.n_os) continue;
+          p[c] = a.accumulate ? p[c] + v[c] : v[c];
+        }
+      }
+    }
+  }
+}
+
+template <int TS, int TT, int NT>
+static lfm_status launch_band_f(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
+  if (tout) {
+    if (unr == 2)
+      band_f_kernel<TS, TT, NT, 2, true><<<grid, NT, 0, s>>>(a);
+    else
+      band_f_kernel<TS, TT, NT, 1, true><<<grid, NT, 0, s>>>(a);
+  } else if (unr == 2) {
+    band_f_kernel<TS, TT, NT, 2, false><<<grid, NT, 0, s>>>(a);
+  } else {
+    band_f_kernel<TS, TT, NT, 1, false><<<grid, NT, 0, s>>>(a);
+  }
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_f_kernel launch", err);
+}
+
 template <int TS, int TT, int NT>
 static lfm_status launch_band_m8(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
   if (tout) {
@@ -1021,6 +1390,12 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.out_stride = op.out_stride ? op.out_stride : (long long)op.n_os * op.n_ot;
   a.src_pitch = op.src_pitch ? op.src_pitch : op.n_is;
   a.out_pitch = op.out_pitch ? op.out_pitch : op.n_os;
+  a.chunks = reinterpret_cast<const int2*>(op.d_chunks);
+  a.chunk_w = reinterpret_cast<const int2*>(op.d_chunk_w);
+  a.chunk_off = op.d_chunk_off;
+  a.t_foff = op.ft->d_foff;
+  a.t_frow = reinterpret_cast<const int4*>(op.ft->d_frow);
+  a.t_fw = reinterpret_cast<const float4*>(op.ft->d_fw);
   a.t_moff = op.mgrp == 8 ? op.ft->d_m8off : op.ft->d_moff;
   a.t_mseg = reinterpret_cast<const int4*>(op.mgrp == 8 ? op.ft->d_m8seg : op.ft->d_mseg);
   a.t_mw = op.mgrp == 8 ? op.ft->d_m8w : op.ft->d_mw;
@@ -1060,8 +1435,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.win_r1 = win_r1 < 0 ? op.n_it : std::min(win_r1, op.n_it);
   dim3 grid(op.ntx, nty, n_out);
   cudaStream_t s = (cudaStream_t)stream;
-  if (op.tout && op.kind != 3) {
-    err = "transposed output needs the band_m kernel";
+  if (op.tout && op.kind != 3 && op.kind != 5) {
+    err = "transposed output needs the band_m or band_f kernel";
     return LFM_E_INVALID;
   }
   if (op.kind == 1) {
@@ -1096,6 +1471,34 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     LFM_BG_CASE(32, 32, 64)
 #undef LFM_BG_CASE
     err = "unsupported band_g tile";
+    return LFM_E_INVALID;
+  }
+  if (op.kind == 5) {
+    if (!op.ft->d_foff) { err = "band_f: t family has no flat MSEG form"; return LFM_E_INVALID; }
+#define LFM_BF_CASE(TS_, TT_, NT_) \
+    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_f<TS_, TT_, NT_>(a, grid, s, err, op.stages, op.tout);
+    LFM_BF_CASE(128, 32, 256)
+    LFM_BF_CASE(128, 16, 128)
+    LFM_BF_CASE(128, 8, 64)
+    LFM_BF_CASE(64, 32, 128)
+    LFM_BF_CASE(64, 16, 64)
+#undef LFM_BF_CASE
+    err = "unsupported band_f tile";
+    return LFM_E_INVALID;
+  }
+  if (op.kind == 4) {
+    // streamed MSEG t-pass: TS = 128, tt = 4 * NG; unit term scales (checked at tuning time)
+    if (!op.d_chunks) { err = "band_s: chunk lists missing"; return LFM_E_INVALID; }
+#define LFM_BS_CASE(NG_, K_, ST_) \
+    if (op.tt == 4 * NG_ && op.chunk == K_ && op.stages == ST_) return launch_band_s<NG_, K_, ST_>(a, grid, s, err);
+    LFM_BS_CASE(4, 32, 4)
+    LFM_BS_CASE(8, 32, 4)
+    LFM_BS_CASE(4, 64, 3)
+    LFM_BS_CASE(8, 64, 3)
+    LFM_BS_CASE(16, 32, 4)
+    LFM_BS_CASE(8, 16, 6)
+#undef LFM_BS_CASE
+    err = "unsupported band_s configuration";
     return LFM_E_INVALID;
   }
   if (op.kind == 3) {
@@ -1413,8 +1816,10 @@ namespace lfm {
 // zero-filled scratch buffers with CUDA events and keeps the fastest.  LFM_AUTOTUNE=0 disables it
 // (the cost-model choice is kept).
 static void free_sep_dev(SepOp& op) {
-  dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t);
+  dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t); dfree(op.d_chunks); dfree(op.d_chunk_off);
+  dfree(op.d_chunk_w);
   op.d_terms = nullptr; op.d_offs = nullptr; op.d_fp_s = nullptr; op.d_fp_t = nullptr;
+  op.d_chunks = nullptr; op.d_chunk_off = nullptr; op.d_chunk_w = nullptr;
 }
 
 // Optional result cache (LFM_TUNE_FILE): lines "<key> <op> ts tt nt nb stage"; a hit skips the timing
@@ -1425,7 +1830,7 @@ static std::string tune_key(const CameraPlan& cp) {
   for (size_t i = 0; i < sizeof(cp.cam); ++i) h = (h ^ b[i]) * 1099511628211ull;
   char buf[96];
   // v5: the line format carries kernel kind, pipeline stages, the timed ms and MSEG group rows
-  std::snprintf(buf, sizeof(buf), "v5_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
+  std::snprintf(buf, sizeof(buf), "v6_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
   return buf;
 }
 
@@ -1450,6 +1855,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   float op_best[NQ_OPS];
   for (float& v : op_best) v = -1.f;
   const bool dbg = std::getenv("LFM_DEBUG") != nullptr;
+  const bool dbg_all = std::getenv("LFM_DEBUG_TUNE") != nullptr;  // every candidate's time
   size_t src_n = 0, out_n = 0;
   for (SepOp* op : ops) {
     if (!op->fs) continue;
@@ -1485,11 +1891,12 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       int ts, tt, nt, nb, stg;
       int kind = 0, stages = 2;
       float ms = 0;
-      int mg = 4;
-      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d %f %d", k, o, &ts, &tt, &nt, &nb, &stg, &kind, &stages,
-                      &ms, &mg) == 11 &&
+      int mg = 4, chk = 32;
+      if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d %d %d %d %d %f %d %d", k, o, &ts, &tt, &nt, &nb, &stg, &kind,
+                      &stages, &ms, &mg, &chk) == 12 &&
           key == k && std::string(o) == names[q]) {
         op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages; op.mgrp = mg;
+        op.chunk = chk;
         op_best[q] = ms;
         fill_sep_geometry(op);
         free_sep_dev(op);
@@ -1503,7 +1910,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     const SepOp keep = op;  // cost-model choice (device pointers of `op` are replaced below)
     int bts = keep.ts, btt = keep.tt, bnt = keep.nt, bnb = keep.nb, bst = keep.stage;
     float best = 1e30f;
-    int bkind = keep.kind, bstages = keep.stages, bmgrp = keep.mgrp;
+    int bkind = keep.kind, bstages = keep.stages, bmgrp = keep.mgrp, bchunk = keep.chunk;
     if (op.s_ident && (op.n_is % 4) == 0) {
       for (auto& c : cand) {
         if (op.tout) break;  // transposed output: band_m only
@@ -1586,7 +1993,71 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
             if (rep > 0) tot += ms;
           }
           if (!ok || cudaGetLastError() != cudaSuccess) continue;
+          if (dbg_all)
+            std::fprintf(stderr, "[lfm]   %-7s band_m %3dx%-3d nt %3d unroll %d grp %d: %.3f ms\n", names[q], c[0], c[1], c[2],
+                         unr, c[3], tot / 2);
           if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 3; bstages = unr; bmgrp = c[3]; }
+        }
+      }
+      op.kind = 0;
+      const int fcand[][3] = {{128, 32, 256}, {128, 16, 128}, {128, 8, 64}, {64, 32, 128}, {64, 16, 64}};
+      for (auto& c : fcand) {
+        if (st != LFM_OK || !op.ft->want_mseg) break;
+        bool aligned = true;
+        for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
+        if (!aligned) break;
+        for (int unr : {1, 2}) {
+          op.kind = 5; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr; op.mgrp = 4;
+          fill_sep_geometry(op);
+          free_sep_dev(op);
+          size_t bytes = 0;
+          if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+          float ms = 0, tot = 0;
+          bool ok = true;
+          for (int rep = 0; rep < 3 && ok; ++rep) {
+            cudaEventRecord(e0, 0);
+            ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+            cudaEventRecord(e1, 0);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) tot += ms;
+          }
+          if (!ok || cudaGetLastError() != cudaSuccess) continue;
+          if (dbg_all)
+            std::fprintf(stderr, "[lfm]   %-7s band_f %3dx%-3d nt %3d unroll %d: %.3f ms\n", names[q], c[0], c[1], c[2], unr,
+                         tot / 2);
+          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 5; bstages = unr; bmgrp = 4; }
+        }
+      }
+      op.kind = 0;
+      // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)
+      bool unit = true;
+      for (const Term& t : op.terms) unit &= t.scale == 1.f && (t.src_off % 4) == 0;
+      const int scand[][3] = {{4, 32, 4}, {8, 32, 4}, {4, 64, 3}, {8, 64, 3}, {16, 32, 4}, {8, 16, 6}};
+      for (auto& c : scand) {
+        if (st != LFM_OK || !op.ft->want_mseg || op.tout || !unit) break;
+        op.kind = 4; op.ts = 128; op.tt = 4 * c[0]; op.nt = (c[0] + 1) * 32; op.chunk = c[1]; op.stages = c[2];
+        op.nb = 1; op.stage = 0; op.mgrp = 4;
+        fill_sep_geometry(op);
+        free_sep_dev(op);
+        size_t bytes = 0;
+        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+        float ms = 0, tot = 0;
+        bool ok = true;
+        for (int rep = 0; rep < 3 && ok; ++rep) {
+          cudaEventRecord(e0, 0);
+          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+          cudaEventRecord(e1, 0);
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (rep > 0) tot += ms;
+        }
+        if (!ok || cudaGetLastError() != cudaSuccess) continue;
+        if (dbg_all)
+          std::fprintf(stderr, "[lfm]   %-7s band_s NG %2d chunk %2d stages %d: %.3f ms\n", names[q], c[0], c[1], c[2], tot / 2);
+        if (tot < best) {
+          best = tot; bts = 128; btt = 4 * c[0]; bnt = (c[0] + 1) * 32; bnb = 1; bst = 0; bkind = 4; bstages = c[2];
+          bmgrp = 4; bchunk = c[1];
         }
       }
       op.kind = 0;
@@ -1620,6 +2091,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       if (st != LFM_OK) break;
     }
     op.ts = bts; op.tt = btt; op.nt = bnt; op.nb = bnb; op.stage = bst; op.kind = bkind; op.stages = bstages; op.mgrp = bmgrp;
+    op.chunk = bchunk;
     fill_sep_geometry(op);
     free_sep_dev(op);
     size_t bytes = 0;
@@ -1627,11 +2099,11 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d grp %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
-        std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb, op.stage,
-                     op.kind, op.stages, op_best[q], op.mgrp);
+        std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb,
+                     op.stage, op.kind, op.stages, op_best[q], op.mgrp, op.chunk);
         std::fclose(f);
       }
     }

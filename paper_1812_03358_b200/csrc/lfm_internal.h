@@ -54,6 +54,13 @@ struct BandFamily {
   int32_t* d_moff = nullptr;
   int32_t* d_mseg = nullptr;
   float* d_mw = nullptr;
+  // flat form of the MSEG lists (built with want_mseg): per group a list of (source row, 4 weights)
+  // entries padded to a multiple of 4 with zero weights, so the kernel loop has no segment structure
+  std::vector<int32_t> f_off, f_row;       // f_off: [table*n_groups + g] .. +1 in entries
+  std::vector<double> f_w64;               // 4 per entry
+  int32_t* d_foff = nullptr;
+  int32_t* d_frow = nullptr;
+  float* d_fw = nullptr;
   // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
   std::vector<int32_t> m8_off, m8_seg;
   std::vector<double> m8_w64;
@@ -100,11 +107,17 @@ struct SepOp {
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
   int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s), 2: band_g_kernel (L2 gather),
                                    // 3: band_m_kernel (L2 gather over MSEG segments of ft)
+                                   // 4: band_s_kernel (MSEG segments, source rows streamed through smem)
+                                   // 5: band_f_kernel (flat MSEG entry lists, L2 gather, deep unroll)
   long long src_pitch = 0;         // floats between source rows (0: n_is)
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)
   int tout = 0;                    // band_m only: write element (row, col) at col * out_pitch + row
   int mgrp = 4;                    // band_m only: rows per MSEG group (4 or 8)
+  int chunk = 32;                  // band_s only: source rows per streamed chunk
+  int32_t* d_chunks = nullptr;     // band_s: per (t-table, tile_y) list of {first row, rows} chunk pairs
+  int32_t* d_chunk_off = nullptr;  //         offsets into d_chunks, size n_tables * nty + 1
+  int32_t* d_chunk_w = nullptr;    //         per (chunk, group of the tile): {first weight float4, count}
   int stages = 2;                  // band_t pipeline depth
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile

@@ -295,7 +295,30 @@ static void build_ell(BandFamily& f) {
         }
       }
     }
-  if (f.want_mseg) f.m_off[ng] = (int)(f.m_seg.size() / 4);
+  if (f.want_mseg) {
+    f.m_off[ng] = (int)(f.m_seg.size() / 4);
+    // flat form: one entry per MSEG column, each group padded to a multiple of 4 entries
+    f.f_off.assign(ng + 1, 0);
+    f.f_row.clear();
+    f.f_w64.clear();
+    for (size_t gi = 0; gi < ng; ++gi) {
+      f.f_off[gi] = (int)f.f_row.size();
+      int last = 0;
+      for (int sg = f.m_off[gi]; sg < f.m_off[gi + 1]; ++sg) {
+        const int j0 = f.m_seg[4 * (size_t)sg], w = f.m_seg[4 * (size_t)sg + 1], wo = f.m_seg[4 * (size_t)sg + 2];
+        for (int p = 0; p < w; ++p) {
+          f.f_row.push_back(j0 + p);
+          for (int q = 0; q < 4; ++q) f.f_w64.push_back(f.m_w64[wo + 4 * (size_t)p + q]);
+          last = j0 + p;
+        }
+      }
+      while (f.f_row.size() % 4) {
+        f.f_row.push_back(last);
+        for (int q = 0; q < 4; ++q) f.f_w64.push_back(0.0);
+      }
+    }
+    f.f_off[ng] = (int)f.f_row.size();
+  }
 }
 
 // Union window of the G4 groups of output tile t (rows [t*tile, (t+1)*tile)), and its weight block.
@@ -1229,14 +1252,17 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     std::string env = std::string("LFM_FORCE_") + names[q];
     if (const char* f = std::getenv(env.c_str())) {
       // optional 6th/7th fields: kind (1 = streaming band_t kernel, identity-s ops only), stages
-      int ts, tt, nt, nb, stg, kind = 0, stages = 2, mg = 4;
-      if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages, &mg) >= 5) {
+      int ts, tt, nt, nb, stg, kind = 0, stages = 2, mg = 4, chk = 32;
+      if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages, &mg, &chk) >= 5) {
         SepOp& op = *ops[q];
         op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages; op.mgrp = mg;
+        op.chunk = chk;
         fill_sep_geometry(op);
         if (kind >= 1) {
           bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
-                    (kind != 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty()));
+                    (kind < 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty())) &&
+                    (kind != 4 || (ts == 128 && !op.tout)) && (kind != 5 || !op.ft->f_off.empty());
+          for (const Term& t : op.terms) ok &= kind != 4 || t.scale == 1.f;
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
           if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
         } else if (sep_smem(op, nb) > (size_t)220 * 1024) {
