@@ -102,6 +102,8 @@ typedef struct {
   size_t table_bytes;       /* device bytes of this camera's tables */
   double fma_alg[2];        /* algorithmic FMAs (plan nnz) per A_forward per path [per_view, collapsed] */
   double bytes_alg[2];      /* algorithmic HBM bytes per A_forward per path */
+  double fma_stage[2];      /* algorithmic FMAs (non-zeros x columns) of one launch of stage
+                               LFM_STAGE_FWD_T / LFM_STAGE_ADJ_T (lfm_A_stage) */
 } lfm_info;
 
 /* Table ids for lfm_plan_export_table (bit-exact comparison with the oracle in tests).
@@ -165,6 +167,18 @@ lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1,
                               void* ws, size_t ws_bytes, void* stream);
 lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
                               int accumulate, void* ws, size_t ws_bytes, void* stream);
+
+/* Single stages of the collapsed two-pass path (NEXT-1), for measuring
+ * the dominant kernels in isolation.  Each stage is ONE kernel launch and reads / writes the
+ * slice-interleaved intermediate Z that the workspace holds after a full call:
+ *   LFM_STAGE_FWD_T: y = sum over (vt, n) of C_t[i_t][(vt, n)] Z[(vt, n)][:]  (Z from the last
+ *                    lfm_A_forward of this camera with this workspace; `in` unused, `out` = y);
+ *   LFM_STAGE_ADJ_T: Z[(vt, n)][:] = sum over i_t of C_t,n^T[vt][i_t] y[i_t][:]  (`in` = y; `out` unused,
+ *                    Z is left in the workspace).
+ * Status LFM_E_INVALID if the camera's collapsed path is not in its two-pass form. */
+enum { LFM_STAGE_FWD_T = 0, LFM_STAGE_ADJ_T = 1 };
+lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* out, void* ws, size_t ws_bytes,
+                       void* stream);
 
 /* --- PWLS with the camera gains minimised out (eqn,pls P:299-317; App. A) --------
  * Weights are absorbed (A~ = W^1/2 A, y~ = W^1/2 y); w = diag(W_c) >= 0.

@@ -404,6 +404,28 @@ lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1,
   return st;
 }
 
+lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* out, void* ws, size_t ws_bytes,
+                       void* stream) {
+  g_launches = 0;
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  const CameraPlan& cp = p->cams[cam];
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  if (stage == LFM_STAGE_FWD_T) {
+    if (!cp.fwd_split) return fail(LFM_E_INVALID, "collapsed forward of this camera is not in two-pass form");
+    if (!out) return fail(LFM_E_INVALID, "out is NULL");
+    st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream);
+  } else if (stage == LFM_STAGE_ADJ_T) {
+    if (!in) return fail(LFM_E_INVALID, "in is NULL");
+    st = sep(cp.adj_c1, in, w.z, 0, 1, 0, stream);
+  } else {
+    return fail(LFM_E_INVALID, "unknown stage");
+  }
+  g_last_launches = g_launches;
+  return st;
+}
+
 lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y, void* ws, size_t ws_bytes,
                          void* stream) {
   lfm_status st = check_cam(p, cam);

@@ -2110,7 +2110,15 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   }
   // s passes of the two-pass path: direct (sep kernel) or transpose + band_m with transposed output
   float t_x = -1.f, t_z = -1.f;
-  if (st == LFM_OK && (op_best[9] > 0 || op_best[10] > 0)) {
+  int cached_decision[3] = {-1, -1, -1};
+  for (const std::string& ln : cached) {
+    char k[128], o[32];
+    int d0, d1, d2;
+    if (std::sscanf(ln.c_str(), "%127s %31s %d %d %d", k, o, &d0, &d1, &d2) == 5 && key == k && std::string(o) == "decide") {
+      cached_decision[0] = d0; cached_decision[1] = d1; cached_decision[2] = d2;
+    }
+  }
+  if (st == LFM_OK && cached_decision[0] < 0 && (op_best[9] > 0 || op_best[10] > 0)) {
     const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
     const long long nslice = (long long)nx * ny;
     auto time_it = [&](auto&& fn) {
@@ -2137,13 +2145,26 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   dfree(out);
   if (op_best[9] > 0 && op_best[7] > 0 && t_x >= 0) cp.fwd_t = (t_x + op_best[9]) < op_best[7];
   if (op_best[10] > 0 && op_best[6] > 0 && t_z >= 0) cp.adj_t = (t_z + op_best[10]) < op_best[6];
+  if (cached_decision[0] >= 0) {
+    cp.fwd_split = cached_decision[0];
+    cp.fwd_t = cached_decision[1];
+    cp.adj_t = cached_decision[2];
+  } else if (tfile) {
+    if (FILE* f = std::fopen(tfile, "a")) {
+      const float fwd_s0 = cp.fwd_t ? t_x + op_best[9] : op_best[7];
+      const int split = (op_best[4] > 0 && fwd_s0 > 0 && op_best[8] > 0) ? (fwd_s0 + op_best[8]) < op_best[4] : cp.fwd_split;
+      std::fprintf(f, "%s decide %d %d %d\n", key.c_str(), split, cp.fwd_t, cp.adj_t);
+      std::fclose(f);
+    }
+  }
   if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] == '1';
   if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] == '1';
-  cp.fwd_t = cp.fwd_t && cp.fwd_p1.fs && cp.fwd_p1.kind == 3;  // transposed output exists only in band_m
-  cp.adj_t = cp.adj_t && cp.adj_a2.fs && cp.adj_a2.kind == 3;
+  // transposed output exists only in band_m / band_f
+  cp.fwd_t = cp.fwd_t && cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5);
+  cp.adj_t = cp.adj_t && cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5);
   const float fwd_s = cp.fwd_t ? t_x + op_best[9] : op_best[7];
   // forward order: fused (fwd_c) or two passes (s pass + fwd_c2), whichever timed faster
-  if (op_best[4] > 0 && fwd_s > 0 && op_best[8] > 0) cp.fwd_split = (fwd_s + op_best[8]) < op_best[4];
+  if (cached_decision[0] < 0 && op_best[4] > 0 && fwd_s > 0 && op_best[8] > 0) cp.fwd_split = (fwd_s + op_best[8]) < op_best[4];
   if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
   if (dbg)
     std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",

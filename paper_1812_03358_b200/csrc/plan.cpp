@@ -1283,6 +1283,13 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
     if (cp.rot[p].active) rot_bytes += 8.0 * info.n_vox;
   info.fma_alg[0] = cp.fwd_s1.fma_alg + (plen ? cp.fwd_s3.fma_alg : 0.0);
   info.fma_alg[1] = cp.fwd_c.fma_alg;
+  {
+    double nnz_f = 0, nnz_a = 0;
+    for (size_t i = 0; i < cp.cf1n.cnt.size(); ++i) nnz_f += cp.cf1n.cnt[i];
+    for (size_t i = 0; i < cp.ca1n.cnt.size(); ++i) nnz_a += cp.ca1n.cnt[i];
+    info.fma_stage[0] = nnz_f * ndet[0];
+    info.fma_stage[1] = nnz_a * ndet[0];
+  }
   info.bytes_alg[0] = 4.0 * info.n_vox + rot_bytes + (plen ? 8.0 * Kv * nfield : 0.0) + 4.0 * npix;
   info.bytes_alg[1] = 4.0 * info.n_vox + rot_bytes + 4.0 * npix;
 

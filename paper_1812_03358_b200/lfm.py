@@ -59,7 +59,8 @@ class Info(ctypes.Structure):
                 ("vox_r", ctypes.c_double * 3), ("rot_D", ctypes.c_double * 3), ("shear", ctypes.c_double * 6),
                 ("rot_passes", ctypes.c_int), ("taps_s1", ctypes.c_int), ("taps_s3", ctypes.c_int),
                 ("taps_c", ctypes.c_int), ("ws_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
-                ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2)]
+                ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
+                ("fma_stage", ctypes.c_double * 2)]
 
     def as_dict(self):
         out = {}
@@ -90,6 +91,7 @@ _SIGS = {
     "lfm_A_adjoint": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_forward_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint_rows": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _S, _P],
+    "lfm_A_stage": [_P, _I, _I, _P, _P, _P, _S, _P],
     "lfm_pwls_stats": [_P, _I, _P, _P, _P, _P, _P, _S, _P],
     "lfm_pwls_gains": [_P, _P, _P, _P, _P],
     "lfm_pwls_grad": [_P, _I, _I, _I, _P, _PP, _PP, _PP, _P, _F, _F, _I, _P, _P, _P, _S, _P],
@@ -224,6 +226,14 @@ def A_adjoint(plan, cam, y, x, ws, accumulate=False, path=COLLAPSED, stream=None
 def A_forward_rows(plan, cam, row0, row1, x, y, ws, path=COLLAPSED, stream=None):
     _check(_lib.lfm_A_forward_rows(plan.handle, cam, path, row0, row1, _ptr(x), _ptr(y), _ptr(ws), ws.numel(),
                                    _stream(stream)))
+
+
+STAGE_FWD_T, STAGE_ADJ_T = 0, 1
+
+
+def A_stage(plan, cam, stage, inp, out, ws, stream=None):
+    """One kernel of the collapsed two-pass path on the workspace intermediate (include/lfm.h)."""
+    _check(_lib.lfm_A_stage(plan.handle, cam, stage, _ptr(inp), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def A_adjoint_rows(plan, cam, row0, row1, y, x, ws, accumulate=False, path=COLLAPSED, stream=None):

@@ -132,3 +132,28 @@ def test_s_pass_orders(name, transposed, monkeypatch):
         r0, r1 = n_t // 3, n_t - 3
         lfm.A_adjoint_rows(plan, c, r0, r1, dev(r), g, ws, path=1)
         assert max_rel(host(g), op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))) <= TOL, (name, c)
+
+
+def test_stage_entry_points():
+    """lfm_A_stage runs exactly one launch of the forward / adjoint t pass on the workspace intermediate:
+    FWD_T after a forward reproduces that forward's y bit for bit; bad stage ids and NULLs fail."""
+    from paper_1812_03358_b200 import lfm
+    cfg, plan, ops, ws = setup("small_two")
+    x = dev(uniform_volume(cfg["volume"], 0))
+    for c, op in enumerate(ops):
+        y = torch.empty(op.n_pix, device="cuda:0")
+        try:
+            lfm.A_forward(plan, c, x, y, ws, path=1)
+            y2 = torch.full_like(y, float("nan"))
+            lfm.A_stage(plan, c, lfm.STAGE_FWD_T, None, y2, ws)
+        except lfm.LfmError as e:
+            assert "two-pass" in str(e)
+            continue
+        assert lfm.last_launch_count() == 1
+        assert torch.equal(y, y2)
+        lfm.A_stage(plan, c, lfm.STAGE_ADJ_T, dev(uniform_vector(op.n_pix, 1)), None, ws)
+        assert lfm.last_launch_count() == 1
+        with pytest.raises(lfm.LfmError):
+            lfm.A_stage(plan, c, 7, None, y2, ws)
+        with pytest.raises(lfm.LfmError):
+            lfm.A_stage(plan, c, lfm.STAGE_ADJ_T, None, None, ws)
