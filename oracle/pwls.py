@@ -108,14 +108,46 @@ def majoriser(ops, ws, beta, shape):
     return np.maximum(d.reshape(shape) + MAJORISER_C * beta, 1e-12)
 
 
-def fista(ops, ys, ws, beta, nu, shape, iters, d=None, callback=None):
+def subset_views(k_s, k_t, n_subsets, m):
+    """View subset S_m of the angular plane (sec,subset P:383-386): the K = k_s k_t views ordered
+    lexicographically with k_s varying fastest (reading R5: k = k_t k_s_count + k_s, the storage order of
+    P:85-87), every n_subsets-th one starting at m.  Returned as (k_s, k_t) pairs."""
+    return [(k % k_s, k // k_s) for k in range(k_s * k_t) if k % n_subsets == m]
+
+
+def gradient_subset(x, ops, ys, ws, beta, nu, n_subsets, m):
+    """View-subset approximation of the profiled gradient, eqn,subset in reading Z19:
+    y^_c = (K_c/|S|) sum_{k in S} A_ck x;  gains from y^_c (eqn,optimal,gain with A_c x -> y^_c);
+    g = sum_c (K_c/|S|) sum_{k in S} A_ck^T W_c (y^_c - g_c y_c) + grad R + nu."""
+    x = np.asarray(x, np.float64)
+    Ax, sc, views = [], [], []
+    for op in ops:
+        cam = op.camera
+        v = subset_views(cam.ks, cam.kt, n_subsets, m)
+        s = cam.ks * cam.kt / len(v)
+        views.append(v)
+        sc.append(s)
+        Ax.append(s * op.forward(x, v))
+    gam = gains([stats(a, y, w) for a, y, w in zip(Ax, ys, ws)])
+    g = np.zeros(x.size)
+    for op, a, y, w, gc, s, v in zip(ops, Ax, ys, ws, gam, sc, views):
+        r = np.asarray(w, np.float64).ravel() * (a - gc * np.asarray(y, np.float64).ravel())
+        g += s * op.adjoint(r, v)
+    return g.reshape(x.shape) + reg_grad(x, beta) + nu
+
+
+def fista(ops, ys, ws, beta, nu, shape, iters, d=None, callback=None, n_subsets=1):
     if d is None:
         d = majoriser(ops, ws, beta, shape)
     x = np.zeros(shape)
     z = np.zeros(shape)
     t = 1.0
     for it in range(iters):
-        g = gradient(z, ops, ys, ws, beta, nu)
+        # n_subsets > 1: ordered-subsets acceleration, subset it mod n_subsets at iteration it (sec,subset)
+        if n_subsets > 1:
+            g = gradient_subset(z, ops, ys, ws, beta, nu, n_subsets, it % n_subsets)
+        else:
+            g = gradient(z, ops, ys, ws, beta, nu)
         x_new = np.maximum(0.0, z - g / d)
         t_new = 0.5 * (1.0 + np.sqrt(1.0 + 4.0 * t * t))
         z = x_new + ((t - 1.0) / t_new) * (x_new - x)

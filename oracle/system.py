@@ -20,11 +20,16 @@ class SystemOperator:
         self.n_vox = dims[0] * dims[1] * dims[2]
         self.n_pix = cam["n_s"] * cam["n_t"]
 
-    def forward(self, x):
-        return self.camera.forward(self.rot.forward(x)).ravel()
+    def forward(self, x, views=None):
+        """y = A_c x; `views` (list of (k_s, k_t)) restricts the sum over the angular plane (eqn,subset)."""
+        return self.camera.forward(self.rot.forward(x), views).ravel()
 
-    def adjoint(self, y):
-        return self.rot.adjoint(self.camera.adjoint(y)).ravel()
+    def adjoint(self, y, views=None):
+        return self.rot.adjoint(self.camera.adjoint(y, views)).ravel()
+
+    @property
+    def n_views(self):
+        return self.camera.ks * self.camera.kt
 
     def dense(self):
         return self.camera.dense() @ self.rot.dense()
