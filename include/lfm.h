@@ -78,6 +78,9 @@ typedef struct {
   lfm_volume vol;
   int n_cam;
   const lfm_camera* cam;    /* n_cam entries, copied by lfm_plan_create */
+  int n_subsets;            /* view subsets for the ordered-subsets gradient (sec,subset P:360-388):
+                               0 or 1 = none; M > 1 builds, per camera, subset m = every M-th view of the
+                               lexicographically ordered angular plane starting at m (k = k_t*K_s + k_s) */
 } lfm_geometry;
 
 typedef struct lfm_plan_s* lfm_plan;
@@ -168,6 +171,17 @@ lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1,
 lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
                               int accumulate, void* ws, size_t ws_bytes, void* stream);
 
+/* View-subset operators (sec,subset, eqn,subset P:366-379, reading Z19): with S_m the plan's subset m,
+ *   y = (K/|S_m|) sum_{k in S_m} A_ck x           (lfm_A_forward_subset)
+ *   x (+)= (K/|S_m|) sum_{k in S_m} A_ck^T y      (lfm_A_adjoint_subset)
+ * evaluated on the per-view path (the K-collapse needs the full angular sum).  0 <= subset < n_subsets of the
+ * plan (LFM_E_INVALID otherwise, also when the plan has no subsets).  Same buffers and workspace as
+ * lfm_A_forward / lfm_A_adjoint. */
+lfm_status lfm_A_forward_subset(lfm_plan p, int cam, int subset, const float* x, float* y, void* ws, size_t ws_bytes,
+                                void* stream);
+lfm_status lfm_A_adjoint_subset(lfm_plan p, int cam, int subset, const float* y, float* x, int accumulate, void* ws,
+                                size_t ws_bytes, void* stream);
+
 /* Single stages of the collapsed two-pass path (NEXT-1), for measuring
  * the dominant kernels in isolation.  Each stage is ONE kernel launch and reads / writes the
  * slice-interleaved intermediate Z that the workspace holds after a full call:
@@ -194,8 +208,11 @@ lfm_status lfm_pwls_gains(lfm_plan p, const double* stats_dev, double* gamma_dev
 /* Phase 2: grad = sum_c A_c^T W_c (A_c x - gamma_c y_c) + beta * sum_{l in N_j}(x_j - x_l) + nu
  * over the cameras [cam0, cam1) of this rank (a multi-GPU caller all-reduces grad afterwards and
  * adds the regulariser on one rank only: include_reg).  cost_dev (nullable): fp64 [2] =
- * [sum_c 1/2||.||^2_W, nu*sum x + R(x)].  Ax[c], y[c], w[c] are device pointers per camera. */
-lfm_status lfm_pwls_grad(lfm_plan p, int path, int cam0, int cam1, const float* x,
+ * [sum_c 1/2||.||^2_W, nu*sum x + R(x)].  Ax[c], y[c], w[c] are device pointers per camera.
+ * subset >= 0: the view-subset gradient of eqn,subset (reading Z19): A_c^T is replaced by
+ * (K/|S|) sum_{k in S} A_ck^T and Ax[c] must be the subset prediction of lfm_A_forward_subset; `path`
+ * is then ignored.  subset < 0: the exact gradient on `path`. */
+lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, const float* x,
                          const float* const* y, const float* const* w, const float* const* Ax,
                          const double* gamma_dev, float beta, float nu, int include_reg,
                          float* grad, double* cost_dev, void* ws, size_t ws_bytes, void* stream);

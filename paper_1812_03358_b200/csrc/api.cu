@@ -232,6 +232,34 @@ const char* lfm_last_error(void) { return g_err.c_str(); }
 const char* lfm_version(void) { return "liblfm 0.1 (sm_100a)"; }
 int lfm_last_launch_count(void) { return g_last_launches; }
 
+// View-subset forward / adjoint (per-view path over the subset's ops, then rotation as usual).
+lfm_status forward_subset_impl(const CameraPlan& cp, int m, const float* x, float* y, const Ws& w, void* stream) {
+  const ViewOps& vo = cp.subs[m];
+  const float* xr;
+  TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
+  if (cp.info.type == LFM_PLENOPTIC) {
+    TRY(sep(vo.fwd_s1, xr, w.f, 0, vo.n_views, 0, stream));
+    return sep(vo.fwd_s3, w.f, y, 0, 1, 0, stream);
+  }
+  return sep(vo.fwd_s1, xr, y, 0, 1, 0, stream);
+}
+
+lfm_status adjoint_subset_impl(const CameraPlan& cp, int m, const float* y, float* x, int accumulate, const Ws& w,
+                               void* stream) {
+  const ViewOps& vo = cp.subs[m];
+  const bool rot = cp.info.rot_passes != 0;
+  float* target = rot ? w.r0 : x;
+  const int acc = rot ? 0 : accumulate;
+  if (cp.info.type == LFM_PLENOPTIC) {
+    TRY(sep(vo.adj_s3, y, w.f, 0, vo.n_views, 0, stream));
+    TRY(sep(vo.adj_s1, w.f, target, 0, cp.info.nz, acc, stream));
+  } else {
+    TRY(sep(vo.adj_s1, y, target, 0, cp.info.nz, acc, stream));
+  }
+  if (rot) TRY(rotate_adj(cp, w.r0, x, accumulate, w, stream));
+  return LFM_OK;
+}
+
 lfm_status lfm_plan_create(const lfm_geometry* g, int cuda_device, lfm_plan* out) {
   if (!out) return fail(LFM_E_INVALID, "out is NULL");
   *out = nullptr;
@@ -239,10 +267,11 @@ lfm_status lfm_plan_create(const lfm_geometry* g, int cuda_device, lfm_plan* out
   lfm_plan_s* p = new lfm_plan_s;
   p->device = cuda_device;
   p->vol = g->vol;
+  p->n_subsets = g->n_subsets > 1 ? g->n_subsets : 0;
   p->cams.resize(g->n_cam);
   for (int c = 0; c < g->n_cam; ++c) {
     std::string err;
-    lfm_status st = build_camera(g->vol, g->cam[c], p->cams[c], err);
+    lfm_status st = build_camera(g->vol, g->cam[c], g->n_subsets, p->cams[c], err);
     if (st != LFM_OK) {
       delete p;
       return fail(st, "camera " + std::to_string(c) + ": " + err);
@@ -258,6 +287,7 @@ lfm_status lfm_plan_create(const lfm_geometry* g, int cuda_device, lfm_plan* out
     for (int c = 0; st == LFM_OK && c < g->n_cam; ++c) {
       st = upload_camera(p->cams[c], err);
       if (st == LFM_OK) st = autotune_camera(p->cams[c], err);
+      if (st == LFM_OK) st = prepare_subsets(p->cams[c], err);
       if (st != LFM_OK) err = "camera " + std::to_string(c) + ": " + err;
     }
     cudaSetDevice(prev);
@@ -426,6 +456,40 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
   return st;
 }
 
+static lfm_status check_subset(lfm_plan p, int cam, int subset) {
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  if (subset < 0 || subset >= (int)p->cams[cam].subs.size())
+    return fail(LFM_E_INVALID, "subset index outside the plan's n_subsets");
+  return LFM_OK;
+}
+
+lfm_status lfm_A_forward_subset(lfm_plan p, int cam, int subset, const float* x, float* y, void* ws, size_t ws_bytes,
+                                void* stream) {
+  g_launches = 0;
+  lfm_status st = check_subset(p, cam, subset);
+  if (st != LFM_OK) return st;
+  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  st = forward_subset_impl(p->cams[cam], subset, x, y, w, stream);
+  g_last_launches = g_launches;
+  return st;
+}
+
+lfm_status lfm_A_adjoint_subset(lfm_plan p, int cam, int subset, const float* y, float* x, int accumulate, void* ws,
+                                size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  lfm_status st = check_subset(p, cam, subset);
+  if (st != LFM_OK) return st;
+  if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
+  Ws w;
+  if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
+  st = adjoint_subset_impl(p->cams[cam], subset, y, x, accumulate, w, stream);
+  g_last_launches = g_launches;
+  return st;
+}
+
 lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y, void* ws, size_t ws_bytes,
                          void* stream) {
   lfm_status st = check_cam(p, cam);
@@ -479,15 +543,16 @@ lfm_status lfm_pwls_gains(lfm_plan p, const double* stats, double* gamma, int* f
   return st == LFM_OK ? st : fail(st, err);
 }
 
-lfm_status lfm_pwls_grad(lfm_plan p, int path, int cam0, int cam1, const float* x, const float* const* y,
+lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, const float* x, const float* const* y,
                          const float* const* wts, const float* const* Ax, const double* gamma, float beta, float nu,
                          int include_reg, float* grad, double* cost, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
   if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
   if (cam0 < 0 || cam1 > (int)p->cams.size() || cam0 > cam1) return fail(LFM_E_INVALID, "bad camera range");
   if (!x || !grad || (cam1 > cam0 && (!y || !wts || !Ax || !gamma))) return fail(LFM_E_INVALID, "NULL argument");
-  lfm_status st = check_path(path);
+  lfm_status st = subset < 0 ? check_path(path) : LFM_OK;
   if (st != LFM_OK) return st;
+  if (subset >= 0 && subset >= p->n_subsets) return fail(LFM_E_INVALID, "subset index outside the plan's n_subsets");
   Ws w;
   if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
   std::string err;
@@ -501,7 +566,9 @@ lfm_status lfm_pwls_grad(lfm_plan p, int path, int cam0, int cam1, const float* 
     if (!y[c] || !wts[c] || !Ax[c]) return fail(LFM_E_INVALID, "NULL per-camera pointer");
     st = k_residual(Ax[c], y[c], wts[c], gamma, c, w.s, cp.info.n_pix, w.p, cost, c > cam0, stream, err);
     if (st != LFM_OK) return fail(st, err);
-    if ((st = adjoint_impl(cp, path, w.s, grad, c > cam0, w, stream)) != LFM_OK) return st;
+    st = subset < 0 ? adjoint_impl(cp, path, w.s, grad, c > cam0, w, stream)
+                    : adjoint_subset_impl(cp, subset, w.s, grad, c > cam0, w, stream);
+    if (st != LFM_OK) return st;
   }
   if (include_reg) {
     st = k_reg26(x, grad, p->vol.nx, p->vol.ny, p->vol.nz, beta, nu, w.p, cost ? cost + 1 : nullptr, stream, err);

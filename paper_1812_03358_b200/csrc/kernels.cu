@@ -227,6 +227,27 @@ static void dfree(void* p) {
   if (p) cudaFree(p);
 }
 
+// Subset ops reuse the tile configuration the autotuner chose for the full per-view op (same tables,
+// fewer terms per output, so the staged footprints and shared memory only shrink).
+lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
+  size_t bytes = 0;
+  for (ViewOps& vo : cp.subs) {
+    SepOp* pairs[][2] = {{&vo.fwd_s1, &cp.fwd_s1}, {&vo.fwd_s3, &cp.fwd_s3}, {&vo.adj_s3, &cp.adj_s3},
+                         {&vo.adj_s1, &cp.adj_s1}};
+    for (auto& pr : pairs) {
+      SepOp& op = *pr[0];
+      const SepOp& full = *pr[1];
+      if (!op.fs) continue;
+      op.ts = full.ts; op.tt = full.tt; op.nt = full.nt; op.nb = full.nb; op.stage = full.stage;
+      op.kind = full.kind; op.stages = full.stages; op.mgrp = full.mgrp; op.chunk = full.chunk;
+      fill_sep_geometry(op);
+      lfm_status st = upload_sep(op, bytes, err);
+      if (st != LFM_OK) return st;
+    }
+  }
+  return LFM_OK;
+}
+
 void free_camera(CameraPlan& cp) {
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
   for (int ax = 0; ax < 2; ++ax)
@@ -243,7 +264,10 @@ void free_camera(CameraPlan& cp) {
   }
   SepOp* ops[] = {&cp.fwd_s1, &cp.fwd_s3, &cp.adj_s3, &cp.adj_s1, &cp.fwd_c, &cp.adj_c1, &cp.adj_c2,
                   &cp.xp_s1f, &cp.xp_s1a, &cp.xp_s3f, &cp.xp_s3a, &cp.fwd_c1, &cp.fwd_c2, &cp.fwd_p1, &cp.adj_a2};
-  for (SepOp* op : ops) {
+  std::vector<SepOp*> all(std::begin(ops), std::end(ops));
+  for (ViewOps& vo : cp.subs)
+    for (SepOp* op : {&vo.fwd_s1, &vo.fwd_s3, &vo.adj_s3, &vo.adj_s1}) all.push_back(op);
+  for (SepOp* op : all) {
     dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t); dfree(op->d_chunks);
     dfree(op->d_chunk_off); dfree(op->d_chunk_w);
     op->d_terms = nullptr; op->d_offs = nullptr; op->d_fp_s = nullptr; op->d_fp_t = nullptr;

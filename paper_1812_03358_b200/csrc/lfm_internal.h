@@ -139,6 +139,12 @@ struct ShearPass {
   float* d_w[2] = {nullptr, nullptr};
 };
 
+// Per-view ops restricted to one view subset (sec,subset): compact field slots j <-> views S[j].
+struct ViewOps {
+  SepOp fwd_s1, fwd_s3, adj_s3, adj_s1;
+  int n_views = 0;
+};
+
 struct CameraPlan {
   lfm_camera cam;
   lfm_info info;
@@ -156,6 +162,7 @@ struct CameraPlan {
   // lf_transport ops (output b = n*K + k for slice-indexed families)
   SepOp xp_s1f, xp_s1a, xp_s3f, xp_s3a;
   ShearPass rot[3];                       // application order z, x, y (x^r = E^y E^x E^z x)
+  std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
 };
@@ -164,6 +171,7 @@ struct CameraPlan {
 
 struct lfm_plan_s {
   int device = 0;
+  int n_subsets = 0;
   lfm_volume vol;
   std::vector<lfm::CameraPlan> cams;
 };
@@ -177,7 +185,9 @@ size_t band_t_smem(const SepOp& op);
 void fill_sep_geometry(SepOp& op);
 bool sep_choose_tile(SepOp& op);
 lfm_status autotune_camera(CameraPlan& cp, std::string& err);
-lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& out, std::string& err);
+lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subsets, CameraPlan& out,
+                        std::string& err);
+lfm_status prepare_subsets(CameraPlan& cp, std::string& err);
 // kernels.cu
 lfm_status upload_camera(CameraPlan& cp, std::string& err);
 void free_camera(CameraPlan& cp);

@@ -801,7 +801,8 @@ bool sep_choose_tile(SepOp& op) {
 }
 
 // ------------------------------------------------------------------------------------------
-lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan& cp, std::string& err) {
+lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subsets, CameraPlan& cp,
+                        std::string& err) {
   cp.cam = cam;
   lfm_info& info = cp.info;
   std::memset(&info, 0, sizeof(info));
@@ -1112,6 +1113,52 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, CameraPlan
       for (int kt = 0; kt < K[1]; ++kt)
         for (int ks = 0; ks < K[0]; ++ks) sep_add(cp.adj_s1, 0, tab(ks, n), tab(kt, n), 1.f);
       sep_close_output(cp.adj_s1);
+    }
+  }
+  // view-subset ops (sec,subset): subset m = views k = kt*K_s + ks with k mod M == m, compact field slots,
+  // the K/|S| factor of eqn,subset folded into the final op's scale
+  cp.subs.clear();
+  if (n_subsets > 1) {
+    if (n_subsets > Kv) { err = "n_subsets exceeds the number of views"; return LFM_E_INVALID; }
+    cp.subs.resize(n_subsets);
+    for (int m = 0; m < n_subsets; ++m) {
+      ViewOps& vo = cp.subs[m];
+      std::vector<int> S;
+      for (int k = m; k < Kv; k += n_subsets) S.push_back(k);
+      vo.n_views = (int)S.size();
+      const double sc = (double)Kv / S.size();
+      if (plen) {
+        sep_init(vo.fwd_s1, &cp.s1f[0], &cp.s1f[1], nx, ny, vo.n_views, (float)c1);
+        for (int k : S) {
+          const int ks = k % K[0], kt = k / K[0];
+          for (int n = 0; n < nz; ++n) sep_add(vo.fwd_s1, n * nslice, tab(ks, n), tab(kt, n), 1.f);
+          sep_close_output(vo.fwd_s1);
+        }
+        sep_init(vo.fwd_s3, &cp.s3f[0], &cp.s3f[1], dst[0].n, dst[1].n, 1, (float)(c3 * sc));
+        for (size_t j = 0; j < S.size(); ++j) sep_add(vo.fwd_s3, (long long)j * nfield, S[j] % K[0], S[j] / K[0], 1.f);
+        sep_close_output(vo.fwd_s3);
+        sep_init(vo.adj_s3, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], vo.n_views, (float)c3);
+        for (int k : S) {
+          sep_add(vo.adj_s3, 0, k % K[0], k / K[0], 1.f);
+          sep_close_output(vo.adj_s3);
+        }
+        sep_init(vo.adj_s1, &cp.s1a[0], &cp.s1a[1], dst[0].n, dst[1].n, nz, (float)(c1 * sc));
+        for (int n = 0; n < nz; ++n) {
+          for (size_t j = 0; j < S.size(); ++j)
+            sep_add(vo.adj_s1, (long long)j * nfield, tab(S[j] % K[0], n), tab(S[j] / K[0], n), 1.f);
+          sep_close_output(vo.adj_s1);
+        }
+      } else {
+        sep_init(vo.fwd_s1, &cp.s1f[0], &cp.s1f[1], nx, ny, 1, (float)(c1 * sc));
+        for (int k : S)
+          for (int n = 0; n < nz; ++n) sep_add(vo.fwd_s1, n * nslice, tab(k % K[0], n), tab(k / K[0], n), 1.f);
+        sep_close_output(vo.fwd_s1);
+        sep_init(vo.adj_s1, &cp.s1a[0], &cp.s1a[1], ndet[0], ndet[1], nz, (float)(c1 * sc));
+        for (int n = 0; n < nz; ++n) {
+          for (int k : S) sep_add(vo.adj_s1, 0, tab(k % K[0], n), tab(k / K[0], n), 1.f);
+          sep_close_output(vo.adj_s1);
+        }
+      }
     }
   }
   // slice-interleaved t families of the two-pass collapsed path, with their MSEG segment lists

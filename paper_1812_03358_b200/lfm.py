@@ -47,7 +47,7 @@ class Camera(ctypes.Structure):
 
 
 class Geometry(ctypes.Structure):
-    _fields_ = [("vol", Volume), ("n_cam", ctypes.c_int), ("cam", ctypes.POINTER(Camera))]
+    _fields_ = [("vol", Volume), ("n_cam", ctypes.c_int), ("cam", ctypes.POINTER(Camera)), ("n_subsets", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -92,9 +92,11 @@ _SIGS = {
     "lfm_A_forward_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint_rows": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_stage": [_P, _I, _I, _P, _P, _P, _S, _P],
+    "lfm_A_forward_subset": [_P, _I, _I, _P, _P, _P, _S, _P],
+    "lfm_A_adjoint_subset": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_pwls_stats": [_P, _I, _P, _P, _P, _P, _P, _S, _P],
     "lfm_pwls_gains": [_P, _P, _P, _P, _P],
-    "lfm_pwls_grad": [_P, _I, _I, _I, _P, _PP, _PP, _PP, _P, _F, _F, _I, _P, _P, _P, _S, _P],
+    "lfm_pwls_grad": [_P, _I, _I, _I, _I, _P, _PP, _PP, _PP, _P, _F, _F, _I, _P, _P, _P, _S, _P],
     "lfm_majoriser": [_P, _I, _I, _I, _PP, _F, _I, _P, _P, _S, _P],
     "lfm_fista_update": [_P, _P, _P, _P, _P, _D, _D, _P],
     "lfm_last_launch_count": [],
@@ -153,11 +155,13 @@ def _camera_struct(c):
 class Plan:
     """Owns an lfm_plan built from a workloads-style config dict {volume, cameras}."""
 
-    def __init__(self, config, device=0):
+    def __init__(self, config, device=0, n_subsets=0):
         vol = config["volume"]
         cams = config["cameras"]
         arr = (Camera * len(cams))(*[_camera_struct(c) for c in cams])
-        g = Geometry(Volume(vol["nx"], vol["ny"], vol["nz"], vol["dx"], vol["dy"], vol["dz"]), len(cams), arr)
+        g = Geometry(Volume(vol["nx"], vol["ny"], vol["nz"], vol["dx"], vol["dy"], vol["dz"]), len(cams), arr,
+                     int(n_subsets))
+        self.n_subsets = int(n_subsets) if n_subsets > 1 else 0
         h = _P()
         _check(_lib.lfm_plan_create(ctypes.byref(g), int(device), ctypes.byref(h)))
         self._h = h
@@ -228,6 +232,16 @@ def A_forward_rows(plan, cam, row0, row1, x, y, ws, path=COLLAPSED, stream=None)
                                    _stream(stream)))
 
 
+def A_forward_subset(plan, cam, subset, x, y, ws, stream=None):
+    """y = (K/|S_m|) sum_{k in S_m} A_ck x over the plan's view subset m (include/lfm.h)."""
+    _check(_lib.lfm_A_forward_subset(plan.handle, cam, subset, _ptr(x), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def A_adjoint_subset(plan, cam, subset, y, x, ws, accumulate=False, stream=None):
+    _check(_lib.lfm_A_adjoint_subset(plan.handle, cam, subset, _ptr(y), _ptr(x), int(accumulate), _ptr(ws), ws.numel(),
+                                     _stream(stream)))
+
+
 STAGE_FWD_T, STAGE_ADJ_T = 0, 1
 
 
@@ -258,10 +272,10 @@ def _ptr_array(ts, n):
 
 
 def pwls_grad(plan, x, ys, ws_, Axs, gamma, beta, nu, grad, ws, cam0=0, cam1=None, include_reg=True, cost=None,
-              path=COLLAPSED, stream=None):
+              path=COLLAPSED, stream=None, subset=-1):
     n = plan.n_cam
     cam1 = n if cam1 is None else cam1
-    _check(_lib.lfm_pwls_grad(plan.handle, path, cam0, cam1, _ptr(x), _ptr_array(ys, n), _ptr_array(ws_, n),
+    _check(_lib.lfm_pwls_grad(plan.handle, path, int(subset), cam0, cam1, _ptr(x), _ptr_array(ys, n), _ptr_array(ws_, n),
                               _ptr_array(Axs, n), _ptr(gamma), float(beta), float(nu), int(include_reg), _ptr(grad),
                               _ptr(cost), _ptr(ws), ws.numel(), _stream(stream)))
 

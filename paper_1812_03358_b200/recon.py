@@ -1,7 +1,8 @@
 """PWLS reconstruction driver (paper §5, Appendix A) over the C ABI: orchestration only.
 
 Per FISTA iteration (reading Z18; tab,alg P:349 is missing):
-  1. Ax_c = A_c z               (lfm_A_forward, every camera of this rank)
+  1. Ax_c = A_c z               (lfm_A_forward, every camera of this rank; with ordered subsets
+                                 (sec,subset) the subset prediction lfm_A_forward_subset instead)
   2. s_c = [y'WAx, y'Wy, Ax'WAx] (lfm_pwls_stats)  -> all-reduce over ranks (multi-GPU)
   3. gamma = gains(s)           (lfm_pwls_gains, on device; gamma_1 = 1)
   4. grad = sum_c A_c^T W_c (A_c z - gamma_c y_c) (+ grad R + nu on rank 0)  (lfm_pwls_grad)
@@ -49,28 +50,37 @@ class PWLS:
         lfm.majoriser(self.plan, self.wts, self.beta, self.d, self.ws, 0, 0, mode=lfm.MAJ_FINISH, path=self.path)
         return self.d
 
-    def gradient(self, x, with_cost=False):
+    def gradient(self, x, with_cost=False, subset=-1):
+        """Exact profiled gradient (subset < 0) or the view-subset approximation eqn,subset with
+        the plan's subset `subset`: prediction, gains and backprojection all over that subset (reading Z19)."""
         self.stats.zero_()
         for c in range(self.cam0, self.cam1):
-            lfm.A_forward(self.plan, c, x, self.Ax[c], self.ws, path=self.path)
+            if subset < 0:
+                lfm.A_forward(self.plan, c, x, self.Ax[c], self.ws, path=self.path)
+            else:
+                lfm.A_forward_subset(self.plan, c, subset, x, self.Ax[c], self.ws)
             lfm.pwls_stats(self.plan, c, self.Ax[c], self.ys[c], self.wts[c], self.stats[3 * c:3 * c + 3], self.ws)
         self._allreduce(self.stats)
         lfm.pwls_gains(self.plan, self.stats, self.gamma, self.flag)
         lfm.pwls_grad(self.plan, x, self.ys, self.wts, self.Ax, self.gamma, self.beta, self.nu, self.grad, self.ws,
                       self.cam0, self.cam1, include_reg=self.rank0, cost=self.cost if with_cost else None,
-                      path=self.path)
+                      path=self.path, subset=subset)
         self._allreduce(self.grad)
         if with_cost:
             self._allreduce(self.cost)
         return self.grad
 
-    def fista(self, iters, x=None, callback=None):
+    def fista(self, iters, x=None, callback=None, subsets=False):
+        """FISTA (reading Z18); subsets=True: ordered subsets, iteration it uses the plan's subset
+        it mod n_subsets (sec,subset P:360-388)."""
+        if subsets and not self.plan.n_subsets:
+            raise ValueError("the plan was built without view subsets (Plan(..., n_subsets=M))")
         d = self.majoriser()
         x = torch.zeros(self.n_vox, device=self.grad.device) if x is None else x
         z = x.clone()
         t = 1.0
         for it in range(iters):
-            g = self.gradient(z)
+            g = self.gradient(z, subset=it % self.plan.n_subsets if subsets else -1)
             t_new = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t * t))
             lfm.fista_update(self.plan, x, z, g, d, t, t_new)
             t = t_new
