@@ -161,26 +161,24 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
         if (a >= 0) flush();
       }
     off.back() = (int)ch.size();
-    // per (chunk, group): the group's weights for the chunk's rows form one contiguous float4 range
-    // (segment weight blocks are stored back to back in row order)
+    // per (chunk, group): the range [e_lo, e_hi) of the group's flat entries whose source rows fall in the
+    // chunk (flat entries are in increasing row order within a group)
     std::vector<int2> cw(ch.size() * NG + 1, make_int2(0, 0));
     for (int m = 0; m < ft.n_tables; ++m)
       for (int y = 0; y < op.nty; ++y)
-        for (int c = off[(size_t)m * op.nty + y]; c < off[(size_t)m * op.nty + y + 1]; ++c) {
-          const int cs = ch[c].x, ce = ch[c].x + ch[c].y;
-          for (int k = 0; k < NG; ++k) {
-            const int g = y * NG + k;
-            if (g >= ng) continue;
-            size_t gi = (size_t)m * ng + g;
-            int f0 = -1, f1 = -1;
-            for (int sg = ft.m_off[gi]; sg < ft.m_off[gi + 1]; ++sg) {
-              const int j0 = ft.m_seg[4 * (size_t)sg], w = ft.m_seg[4 * (size_t)sg + 1], wo = ft.m_seg[4 * (size_t)sg + 2];
-              const int a0 = std::max(j0, cs), a1 = std::min(j0 + w, ce);
-              if (a0 >= a1) continue;
-              if (f0 < 0) f0 = wo / 4 + (a0 - j0);
-              f1 = wo / 4 + (a1 - j0);
-            }
-            if (f0 >= 0) cw[(size_t)c * NG + k] = make_int2(f0, f1 - f0);
+        for (int k = 0; k < NG; ++k) {
+          const int g = y * NG + k;
+          if (g >= ng) continue;
+          const size_t gi = (size_t)m * ng + g;
+          int e = ft.f_off[gi];
+          const int e_end = ft.f_off[gi + 1];
+          for (int c = off[(size_t)m * op.nty + y]; c < off[(size_t)m * op.nty + y + 1]; ++c) {
+            const int cs = ch[c].x, ce = ch[c].x + ch[c].y;
+            while (e < e_end && ft.f_row[e] < cs) ++e;
+            int e2 = e;
+            while (e2 < e_end && ft.f_row[e2] < ce) ++e2;
+            cw[(size_t)c * NG + k] = make_int2(e, e2);
+            e = e2;
           }
         }
     ch.push_back(make_int2(0, 0));
@@ -1024,7 +1022,7 @@ __global__ void __launch_bounds__(NT, (GR == 8 ? 512 : 1024) / NT) band_m_kernel
 template <int NG, int K, int STAGES>
 __global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
   constexpr int TS = 128;
-  constexpr int SLOT = K * TS + NG * K * 4;  // U rows, then per group K weight float4s
+  constexpr int SLOT = K * TS;  // the chunk's source rows
   extern __shared__ __align__(16) float smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1054,10 +1052,7 @@ __global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
         float* slot = smem + (size_t)s * SLOT;
         const int wlo = max(ck.x, a.win_r0), whi = min(ck.x + ck.y, a.win_r1);
         const int nrow = max(0, whi - wlo);
-        const int2 cw = lane < NG ? a.chunk_w[(size_t)c * NG + lane] : make_int2(0, 0);
-        uint32_t wbytes = (uint32_t)cw.y * 16;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wbytes += __shfl_xor_sync(0xffffffffu, wbytes, o);
+
         if (nrow < ck.y) {  // rows outside the source window read as zero
           const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int r = 0; r < ck.y; ++r) {
@@ -1068,19 +1063,19 @@ __global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * row_bytes + wbytes);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * row_bytes);
         __syncwarp();
         const float* src = a.src + term.src_off + (size_t)wlo * a.src_pitch + os0;
         float* dst = slot + (wlo - ck.x) * TS;
         for (int r = lane; r < nrow; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.src_pitch, row_bytes, &full[s]);
-        if (cw.y > 0) bulk_g2s(slot + K * TS + lane * K * 4, a.t_mw + 4 * (size_t)cw.x, (uint32_t)cw.y * 16, &full[s]);
       }
     }
     return;
   }
-  // ---------------- consumer warp `warp` = group ty*NG + warp
+  // ---------------- consumer warp `warp` = group ty*NG + warp: its flat entries of each chunk
   const int g = ty * NG + warp;
   const bool gvalid = g < a.t_ngroups;
+  const int* frow = reinterpret_cast<const int*>(a.t_frow);
   float acc[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -1090,28 +1085,15 @@ __global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
   for (int e = e0; e < e1; ++e) {
     const Term term = a.terms[e];
     const int c0 = a.chunk_off[(size_t)term.t_tab * a.nty + ty], c1 = a.chunk_off[(size_t)term.t_tab * a.nty + ty + 1];
-    const size_t gi = (size_t)term.t_tab * a.t_ngroups + g;
-    int si = gvalid ? __ldg(a.t_moff + gi) : 0;
-    const int s_end = gvalid ? __ldg(a.t_moff + gi + 1) : 0;
-    int4 sd = si < s_end ? __ldg(a.t_mseg + si) : make_int4(0, 0, 0, 0);
     for (int c = c0; c < c1; ++c, ++it) {
       const int s = it % STAGES;
       const int2 ck = a.chunks[c];
-      const int wf0 = a.chunk_w[(size_t)c * NG + warp].x;  // first weight float4 of this group in the slot
+      const int2 er = a.chunk_w[(size_t)c * NG + warp];
       mbar_wait(&full[s], (it / STAGES) & 1);
-      const float* slot = smem + (size_t)s * SLOT;
-      const float4* wsl = reinterpret_cast<const float4*>(slot + K * TS + warp * K * 4);
-      const int cend = ck.x + ck.y;
-      while (si < s_end && sd.x < cend) {
-        const int pa = max(sd.x, ck.x), pb = min(sd.x + sd.y, cend);
-        const float4* wp = wsl + (sd.z / 4 - sd.x - wf0);
-        const float* up = slot + lane * 4 - ck.x * TS;
+      const float* up = smem + (size_t)s * SLOT + lane * 4 - ck.x * TS;
 #pragma unroll 4
-        for (int p = pa; p < pb; ++p) fma4x4(acc, wp[p], *reinterpret_cast<const float4*>(up + p * TS));
-        if (sd.x + sd.y > cend) break;  // segment continues in the next chunk
-        ++si;
-        if (si < s_end) sd = __ldg(a.t_mseg + si);
-      }
+      for (int q = er.x; q < er.y; ++q)
+        fma4x4(acc, __ldg(a.t_fw + q), *reinterpret_cast<const float4*>(up + __ldg(frow + q) * TS));
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -1149,7 +1131,7 @@ __global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
 template <int NG, int K, int STAGES>
 static lfm_status launch_band_s(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err) {
   auto kern = band_s_kernel<NG, K, STAGES>;
-  const size_t smem = (size_t)STAGES * (K * 128 + NG * K * 4) * 4;
+  const size_t smem = (size_t)STAGES * K * 128 * 4;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
