@@ -19,6 +19,10 @@ passes permute the axes):
 
 (1/Dz) Lambda * U is the paper's "piecewise quadratic" g^z integrated over the source
 cell.  Every pass keeps the grid dims with zeros outside (crop, Z14).
+
+Poses beyond 45 degrees (NEXT-4): Theta = P Theta' with P the closest of the 24 cube
+rotations (reading R7); P is applied first as an exact index relabelling x_P(q) = x(P q), then the
+three shears of Theta'.
 """
 import numpy as np
 import scipy.sparse as sp
@@ -136,11 +140,61 @@ def shear_matrix(dims, vox, axis, c1, c2):
     return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
 
 
+def _proper_signed_permutations():
+    """The 24 rotations of the cube (signed permutation matrices with det +1), identity first."""
+    import itertools
+    out = [np.eye(3)]
+    for perm in itertools.permutations(range(3)):
+        for signs in itertools.product((1.0, -1.0), repeat=3):
+            P = np.zeros((3, 3))
+            for r in range(3):
+                P[r, perm[r]] = signs[r]
+            if np.linalg.det(P) > 0.5 and not np.array_equal(P, np.eye(3)):
+                out.append(P)
+    return out
+
+
+def quarter_turn(R):
+    """NEXT-4 reading R7: Theta = P Theta' with P the cube rotation closest to Theta (largest trace of
+    P^T Theta; ties keep the earlier candidate, identity first), so the residual Theta' is within the
+    range the three-shear decomposition handles (P:1117-1119 restrict the decomposition to < 45 deg)."""
+    T = np.asarray(R, np.float64).reshape(3, 3)
+    best, bestv = None, -np.inf
+    for P in _proper_signed_permutations():
+        v = np.trace(P.T @ T)
+        if v > bestv + 1e-12:
+            best, bestv = P, v
+    return best, best.T @ T
+
+
+def permutation_matrix(P, dims, vox):
+    """Sparse relabelling x_P(q) = x(P q) on a grid symmetric about the origin (exact for a signed
+    permutation when the permuted axes have equal cell counts and sizes)."""
+    nx, ny, nz = dims
+    n = (nx, ny, nz)
+    for b in range(3):
+        a = int(np.argmax(np.abs(P[b])))
+        if n[a] != n[b] or abs(vox[a] - vox[b]) > 1e-12 * vox[b]:
+            raise NotDecomposable("quarter-turn permutation needs equal dims and voxel sizes on the permuted axes")
+    I = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1).reshape(-1, 3)
+    src = np.zeros_like(I)
+    for b in range(3):
+        a = int(np.argmax(np.abs(P[b])))
+        src[:, b] = I[:, a] if P[b, a] > 0 else n[b] - 1 - I[:, a]
+    rows = I[:, 0] + nx * (I[:, 1] + ny * I[:, 2])
+    cols = src[:, 0] + nx * (src[:, 1] + ny * src[:, 2])
+    N = nx * ny * nz
+    return sp.csr_matrix((np.ones(N), (rows, cols)), shape=(N, N))
+
+
 class Rotation:
-    """x^r = E^y E^x E^z x on the relabelled grid (voxel sizes Delta/D)."""
+    """x^r = E^y E^x E^z P_perm x on the relabelled grid (voxel sizes Delta/D); P_perm is the exact
+    quarter-turn relabelling of reading R7 (identity for poses within 45 degrees)."""
 
     def __init__(self, R, dims, vox):
-        self.dec = decompose(R)
+        self.P, Tres = quarter_turn(R)
+        self.Pm = None if np.array_equal(self.P, np.eye(3)) else permutation_matrix(self.P, dims, vox)
+        self.dec = decompose(Tres.ravel())
         D = self.dec["D"]
         self.dims = dims
         self.vox_r = (vox[0] / D[0], vox[1] / D[1], vox[2] / D[2])
@@ -151,11 +205,19 @@ class Rotation:
 
     def forward(self, x):
         v = np.asarray(x, np.float64).ravel()
+        if self.Pm is not None:
+            v = self.Pm @ v
         return (self.Ey @ (self.Ex @ (self.Ez @ v))).reshape(self.dims[2], self.dims[1], self.dims[0])
 
     def adjoint(self, xr):
         v = np.asarray(xr, np.float64).ravel()
-        return (self.Ez.T @ (self.Ex.T @ (self.Ey.T @ v))).reshape(self.dims[2], self.dims[1], self.dims[0])
+        v = self.Ez.T @ (self.Ex.T @ (self.Ey.T @ v))
+        if self.Pm is not None:
+            v = self.Pm.T @ v
+        return v.reshape(self.dims[2], self.dims[1], self.dims[0])
 
     def dense(self):
-        return (self.Ey @ self.Ex @ self.Ez).toarray()
+        M = self.Ey @ self.Ex @ self.Ez
+        if self.Pm is not None:
+            M = M @ self.Pm
+        return M.toarray()

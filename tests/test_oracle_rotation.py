@@ -57,6 +57,41 @@ def test_quarter_turn_rejected():
         decompose(pose_yaw(90.0))
 
 
+def test_quarter_turn_choice():
+    """Reading R7: P is a proper cube rotation, P Theta' reproduces Theta, and the residual angle is the
+    smallest over the 24 candidates (<= 45 deg for single-axis poses; identity below 45 deg)."""
+    from oracle.rotation import _proper_signed_permutations, quarter_turn
+    assert len(_proper_signed_permutations()) == 24
+    for pose, resid in ((pose_yaw(30.0), 30.0), (pose_yaw(50.0), 40.0), (pose_yaw(120.0), 30.0),
+                        (pose_pitch(100.0), 10.0), (pose_yaw(-135.0), 45.0), (pose_yaw(90.0), 0.0)):
+        P, T = quarter_turn(pose)
+        assert abs(np.linalg.det(P) - 1.0) < 1e-15 and set(np.abs(P).ravel()) <= {0.0, 1.0}
+        assert np.abs(P @ T - np.asarray(pose).reshape(3, 3)).max() < 1e-15
+        ang = np.degrees(np.arccos(np.clip((np.trace(T) - 1) / 2, -1, 1)))
+        assert ang == pytest.approx(resid, abs=1e-9)
+    assert np.array_equal(quarter_turn(pose_yaw(30.0))[0], np.eye(3))
+
+
+def test_quarter_turn_is_exact_relabelling():
+    """A 90-degree yaw is a pure permutation of the voxels: x^r equals the point samples of the rotated
+    blob exactly (p = Theta p^r), and the adjoint is its transpose."""
+    n, d = 12, 0.4
+    c = (np.arange(n) - (n - 1) / 2) * d
+    x = _gauss_cell_average((c, c, c))
+    for pose in (pose_yaw(90.0), pose_yaw(-90.0), pose_pitch(90.0), pose_yaw(180.0)):
+        rot = Rotation(pose, (n, n, n), (d, d, d))
+        ref = _gauss_cell_average((c, c, c), R=pose)
+        assert np.abs(rot.forward(x) - ref).max() < 1e-12
+        rng = np.random.default_rng(1)
+        a, b = rng.normal(size=(n, n, n)), rng.normal(size=(n, n, n))
+        assert abs(np.sum(rot.forward(a) * b) - np.sum(a * rot.adjoint(b))) < 1e-12 * np.linalg.norm(a) * np.linalg.norm(b)
+
+
+def test_quarter_turn_needs_equal_axes():
+    with pytest.raises(NotDecomposable):
+        Rotation(pose_yaw(90.0), (8, 8, 10), (0.4, 0.4, 0.4))
+
+
 @pytest.mark.parametrize("wa,wb", [(0.0, 0.0), (0.35, 0.0), (0.0, 0.8), (0.3, 0.55), (0.9, 0.9), (1.7, 0.2)])
 def test_shear_kernel_vs_quadrature(wa, wb):
     """E entry = 1/(Dx Dy Dz) int int Lambda_Dz(d - a xi - b eta) over the cell (brute force)."""
@@ -101,7 +136,8 @@ def _gauss_cell_average(centres, R=None):
     return np.exp(-0.5 * np.sum(((P - BLOB_C) / BLOB_S) ** 2, -1))
 
 
-@pytest.mark.parametrize("pose", [pose_yaw(20.0), pose_yaw(30.0), pose_pitch(25.0), pose_yaw_pitch(20.0, 15.0)])
+@pytest.mark.parametrize("pose", [pose_yaw(20.0), pose_yaw(30.0), pose_pitch(25.0), pose_yaw_pitch(20.0, 15.0),
+                                  pose_yaw(120.0), pose_pitch(-100.0), pose_yaw_pitch(70.0, 50.0)])
 def test_rotation_fidelity_blob(pose):
     n, d = 40, 0.4
     c = (np.arange(n) - (n - 1) / 2) * d
