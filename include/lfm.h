@@ -99,7 +99,10 @@ typedef struct {
   double vox_r[3];          /* rotated voxel sizes Delta/D */
   double rot_D[3];          /* D_Theta */
   double shear[6];          /* a_zx a_zy a_xy a_xz a_yx a_yz (eqn,rot,decomp) */
-  int rot_passes;           /* bitmask of non-identity shear passes: 1=z 2=x 4=y */
+  int rot_passes;           /* bitmask of non-identity rotation stages: 1=z 2=x 4=y shear passes, 8=quarter-turn
+                               relabelling applied first (poses beyond 45 deg, reading R7) */
+  int rot_perm[9];          /* that relabelling P (signed permutation, row-major; identity if bit 8 is clear):
+                               Theta = P D S_z S_x S_y */
   int taps_s1, taps_s3, taps_c;  /* padded band widths of the S1, S3 and collapsed tables */
   size_t ws_bytes;          /* workspace needed by every apply call on this camera */
   size_t table_bytes;       /* device bytes of this camera's tables */

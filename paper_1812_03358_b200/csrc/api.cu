@@ -91,10 +91,13 @@ lfm_status check_cam(const lfm_plan_s* p, int cam, bool need_device = true) {
     if (_s != LFM_OK) return _s;          \
   } while (0)
 
-// Rotation forward: returns the buffer holding x^r (x itself if the pose is the identity).
+// Rotation forward: returns the buffer holding x^r (x itself if the pose is the identity).  Stages in
+// order: the quarter-turn relabelling (if any, reading R7), then the active shear passes z, x, y;
+// intermediate results ping-pong between w.r0 and w.r1, the last one goes to final_out if given.
 lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, int accumulate, const Ws& w,
                       void* stream, const float** xr) {
-  int act[3], na = 0;
+  int act[4], na = 0;
+  if (cp.has_perm) act[na++] = -1;
   for (int q = 0; q < 3; ++q)
     if (cp.rot[q].active) act[na++] = q;
   const float* cur = x;
@@ -102,8 +105,11 @@ lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, in
   for (int i = 0; i < na; ++i) {
     bool last = i == na - 1;
     float* dst = (last && final_out) ? final_out : ((cur == w.r0) ? w.r1 : w.r0);
-    lfm_status st = launch_shear(cp.rot[act[i]], 0, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
-                                 (last && final_out) ? accumulate : 0, stream, err);
+    const int acc = (last && final_out) ? accumulate : 0;
+    lfm_status st = act[i] < 0 ? k_permute(cur, dst, cp.info.nx, cp.info.ny, cp.info.nz, cp.perm_axis[0],
+                                           cp.perm_sign[0], acc, stream, err)
+                               : launch_shear(cp.rot[act[i]], 0, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz, acc,
+                                              stream, err);
     if (st != LFM_OK) return fail(st, err);
     cur = dst;
   }
@@ -116,11 +122,13 @@ lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, in
   return LFM_OK;
 }
 
-// Rotation adjoint E^zT E^xT E^yT applied to `in`, written (or accumulated) into `out`.
+// Rotation adjoint E^zT E^xT E^yT, then the inverse relabelling P^T, applied to `in`, written (or
+// accumulated) into `out`.  `in` may be w.r0 or w.r1 (the ping-pong never writes the buffer it reads).
 lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int accumulate, const Ws& w, void* stream) {
-  int act[3], na = 0;
+  int act[4], na = 0;
   for (int q = 2; q >= 0; --q)
     if (cp.rot[q].active) act[na++] = q;
+  if (cp.has_perm) act[na++] = -1;
   std::string err;
   if (na == 0) {
     lfm_status st = k_copy_scale(in, out, cp.info.n_vox, 1.f, accumulate, stream, err);
@@ -130,8 +138,11 @@ lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int acc
   for (int i = 0; i < na; ++i) {
     bool last = i == na - 1;
     float* dst = last ? out : ((cur == w.r0) ? w.r1 : w.r0);
-    lfm_status st = launch_shear(cp.rot[act[i]], 1, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
-                                 last ? accumulate : 0, stream, err);
+    const int acc = last ? accumulate : 0;
+    lfm_status st = act[i] < 0 ? k_permute(cur, dst, cp.info.nx, cp.info.ny, cp.info.nz, cp.perm_axis[1],
+                                           cp.perm_sign[1], acc, stream, err)
+                               : launch_shear(cp.rot[act[i]], 1, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz, acc,
+                                              stream, err);
     if (st != LFM_OK) return fail(st, err);
     cur = dst;
   }
@@ -200,22 +211,7 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   } else {
     TRY(sep(cp.adj_s1, y, target, 0, cp.info.nz, acc, stream, 0, -1, r0, r1));
   }
-  if (rot) {
-    // the adjoint passes ping-pong between r1 and r0; start from r0
-    int act[3], na = 0;
-    for (int q = 2; q >= 0; --q)
-      if (cp.rot[q].active) act[na++] = q;
-    const float* cur = w.r0;
-    std::string err;
-    for (int i = 0; i < na; ++i) {
-      bool last = i == na - 1;
-      float* dst = last ? x : ((cur == w.r0) ? w.r1 : w.r0);
-      lfm_status st = launch_shear(cp.rot[act[i]], 1, cur, dst, cp.info.nx, cp.info.ny, cp.info.nz,
-                                   last ? accumulate : 0, stream, err);
-      if (st != LFM_OK) return fail(st, err);
-      cur = dst;
-    }
-  }
+  if (rot) TRY(rotate_adj(cp, w.r0, x, accumulate, w, stream));
   return LFM_OK;
 }
 

@@ -1383,6 +1383,40 @@ lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long lo
   return cuda_check(cudaGetLastError(), "transpose_kernel launch", err);
 }
 
+// Quarter-turn relabelling (reading R7): out[I] (+)= in[src(I)] with src_b = I_{axis[b]} or
+// n_b - 1 - I_{axis[b]} (sign[b] < 0); exact, pure data movement (8 bytes per voxel).
+struct PermMap {
+  int axis[3], sign[3];
+};
+
+__global__ void permute_kernel(const float* __restrict__ in, float* __restrict__ out, int nx, int ny, int nz, PermMap m,
+                               int accumulate) {
+  const long long n = (long long)nx * ny * nz;
+  const int dims[3] = {nx, ny, nz};
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n; v += (long long)gridDim.x * blockDim.x) {
+    const int I[3] = {(int)(v % nx), (int)((v / nx) % ny), (int)(v / ((long long)nx * ny))};
+    int S[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int i = I[m.axis[b]];
+      S[b] = m.sign[b] > 0 ? i : dims[b] - 1 - i;
+    }
+    const float val = __ldg(in + S[0] + (long long)nx * (S[1] + (long long)ny * S[2]));
+    out[v] = accumulate ? out[v] + val : val;
+  }
+}
+
+lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
+                     int accumulate, void* stream, std::string& err) {
+  PermMap m;
+  for (int b = 0; b < 3; ++b) { m.axis[b] = axis[b]; m.sign[b] = sign[b]; }
+  const long long n = (long long)nx * ny * nz;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  permute_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(in, out, nx, ny, nz, m, accumulate);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "permute_kernel launch", err);
+}
+
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1) {
   if (n_out <= 0) return LFM_OK;

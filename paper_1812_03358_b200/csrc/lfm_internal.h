@@ -162,6 +162,8 @@ struct CameraPlan {
   // lf_transport ops (output b = n*K + k for slice-indexed families)
   SepOp xp_s1f, xp_s1a, xp_s3f, xp_s3a;
   ShearPass rot[3];                       // application order z, x, y (x^r = E^y E^x E^z x)
+  int has_perm = 0;                       // quarter-turn relabelling applied before the shears (reading R7)
+  int perm_axis[2][3], perm_sign[2][3];   // [fwd: P, adj: P^T] source axis and sign per output axis
   std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
@@ -196,4 +198,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
                       int win_r1 = -1);
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
+lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
+                     int accumulate, void* stream, std::string& err);
 }  // namespace lfm

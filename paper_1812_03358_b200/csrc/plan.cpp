@@ -827,11 +827,59 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     err = "unknown camera type";
     return LFM_E_INVALID;
   }
-  Decomp dec;
-  lfm_status st = decompose(cam.R, dec, err);
-  if (st != LFM_OK) return st;
+  // reading R7: Theta = P Theta' with P the cube rotation of largest trace(P^T Theta) (identity first, then
+  // permutations in lexicographic order x sign patterns (+,+,+), (+,+,-), ...; ties keep the earlier one)
   const int dims[3] = {vol.nx, vol.ny, vol.nz};
   const double vox[3] = {vol.dx, vol.dy, vol.dz};
+  double Tres[9];
+  {
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    double best = -1e300;
+    int bp[3] = {0, 1, 2}, bs[3] = {1, 1, 1};
+    auto consider = [&](const int* pm, const int* sg) {
+      double tr = 0;  // trace(P^T T) = sum_r s_r T[r][pm[r]]
+      for (int r = 0; r < 3; ++r) tr += sg[r] * cam.R[3 * r + pm[r]];
+      if (tr > best + 1e-12) {
+        best = tr;
+        for (int r = 0; r < 3; ++r) { bp[r] = pm[r]; bs[r] = sg[r]; }
+      }
+    };
+    const int id[3] = {0, 1, 2}, one[3] = {1, 1, 1};
+    consider(id, one);
+    for (int q = 0; q < 6; ++q)
+      for (int m = 0; m < 8; ++m) {
+        const int sg[3] = {(m & 4) ? -1 : 1, (m & 2) ? -1 : 1, (m & 1) ? -1 : 1};
+        // det of a signed permutation = sign(perm) * s0 s1 s2
+        const int par = (q == 0 || q == 3 || q == 4) ? 1 : -1;
+        if (par * sg[0] * sg[1] * sg[2] != 1) continue;
+        if (q == 0 && m == 0) continue;  // identity already considered
+        consider(perms[q], sg);
+      }
+    // Tres = P^T T: row a of P^T T = sum_r P[r][a] T[r][.] -> P[r][bp[r]] = bs[r]
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Tres[3 * bp[r] + c] = bs[r] * cam.R[3 * r + c];
+    cp.has_perm = !(bp[0] == 0 && bp[1] == 1 && bp[2] == 2 && bs[0] == 1 && bs[1] == 1 && bs[2] == 1);
+    for (int k = 0; k < 9; ++k) info.rot_perm[k] = 0;
+    for (int r = 0; r < 3; ++r) info.rot_perm[3 * r + bp[r]] = bs[r];
+    if (cp.has_perm) {
+      for (int b = 0; b < 3; ++b) {
+        const int a = bp[b];
+        if (dims[a] != dims[b] || std::fabs(vox[a] - vox[b]) > 1e-12 * vox[b]) {
+          err = "pose needs a quarter-turn relabelling, which needs equal dims and voxel sizes on the permuted axes";
+          return LFM_E_DEGENERATE;
+        }
+        // forward x_P(q) = x(P q): source axis of output axis b is bp[b] with sign bs[b];
+        // adjoint (P^T): output axis bp[b] reads source axis b with the same sign
+        cp.perm_axis[0][b] = bp[b];
+        cp.perm_sign[0][b] = bs[b];
+        cp.perm_axis[1][bp[b]] = b;
+        cp.perm_sign[1][bp[b]] = bs[b];
+      }
+    }
+  }
+  Decomp dec;
+  lfm_status st = decompose(Tres, dec, err);
+  if (st != LFM_OK) return st;
   double vox_r[3] = {vox[0] / dec.D[0], vox[1] / dec.D[1], vox[2] / dec.D[2]};
   const int nx = vol.nx, ny = vol.ny, nz = vol.nz;
   info.type = cam.type;
@@ -852,7 +900,8 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   build_shear(cp.rot[0], 0, dec.a_zx, dec.a_zy, dims, vox_r);
   build_shear(cp.rot[1], 1, dec.a_xy, dec.a_xz, dims, vox_r);
   build_shear(cp.rot[2], 2, dec.a_yx, dec.a_yz, dims, vox_r);
-  info.rot_passes = (cp.rot[0].active ? 1 : 0) | (cp.rot[1].active ? 2 : 0) | (cp.rot[2].active ? 4 : 0);
+  info.rot_passes = (cp.rot[0].active ? 1 : 0) | (cp.rot[1].active ? 2 : 0) | (cp.rot[2].active ? 4 : 0) |
+                    (cp.has_perm ? 8 : 0);
 
   // planes per axis
   const int K[2] = {cam.k_s, cam.k_t};

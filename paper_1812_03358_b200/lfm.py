@@ -57,7 +57,7 @@ class Info(ctypes.Structure):
                 ("n_views", ctypes.c_int), ("n_as", ctypes.c_int), ("n_at", ctypes.c_int),
                 ("plane_array", ctypes.c_int), ("plane_detector", ctypes.c_int),
                 ("vox_r", ctypes.c_double * 3), ("rot_D", ctypes.c_double * 3), ("shear", ctypes.c_double * 6),
-                ("rot_passes", ctypes.c_int), ("taps_s1", ctypes.c_int), ("taps_s3", ctypes.c_int),
+                ("rot_passes", ctypes.c_int), ("rot_perm", ctypes.c_int * 9), ("taps_s1", ctypes.c_int), ("taps_s3", ctypes.c_int),
                 ("taps_c", ctypes.c_int), ("ws_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
                 ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
                 ("fma_stage", ctypes.c_double * 2)]

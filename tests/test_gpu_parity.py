@@ -12,7 +12,7 @@ from workloads import make_config, normal_vector, uniform_vector, uniform_volume
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "small_two", "ragged"]
+SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "ragged"]
 PATHS = [0, 1]  # PER_VIEW, COLLAPSED
 
 
@@ -85,7 +85,7 @@ def test_adjoint_accumulate():
     assert torch.allclose(g, base + g2, rtol=1e-6, atol=1e-7)
 
 
-@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two"])
+@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two", "tiny_turn"])
 def test_vol_rotate_parity(name):
     from paper_1812_03358_b200 import lfm
     cfg, plan, ops, ws = _setup(name)

@@ -19,7 +19,7 @@ from workloads.geometry import plenoptic_camera, pose_yaw, pose_yaw_pitch, singl
 
 lfm = pytest.importorskip("paper_1812_03358_b200.lfm")
 
-CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "small_two"]
+CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two"]
 
 
 def ragged_config():
@@ -130,8 +130,9 @@ def test_collapsed_composite_tables(name):
                 _weights_match(plan, c, "CF", ax, n, Cn, rel=1e-12)
 
 
-@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two"])
+@pytest.mark.parametrize("name", ["tiny_yaw15", "ragged", "small_two", "tiny_turn"])
 def test_rotation_factors_and_shear_tables(name):
+    from oracle.rotation import quarter_turn
     cfg = _cfg(name)
     plan = lfm.Plan(cfg, device=-1)
     vol = cfg["volume"]
@@ -139,7 +140,10 @@ def test_rotation_factors_and_shear_tables(name):
     vox = (vol["dx"], vol["dy"], vol["dz"])
     for c, cam in enumerate(cfg["cameras"]):
         inf = plan.info(c)
-        dec = decompose(cam["R"])
+        P, T = quarter_turn(cam["R"])                                 # reading R7
+        assert inf["rot_perm"] == [int(v) for v in P.ravel()]
+        assert bool(inf["rot_passes"] & 8) == (not np.array_equal(P, np.eye(3)))
+        dec = decompose(T.ravel())
         assert tuple(inf["rot_D"]) == dec["D"]                       # bit-exact fp64 geometry
         assert tuple(inf["shear"]) == (dec["a_zx"], dec["a_zy"], dec["a_xy"], dec["a_xz"], dec["a_yx"], dec["a_yz"])
         vox_r = tuple(v / d for v, d in zip(vox, dec["D"]))
@@ -183,7 +187,6 @@ def test_error_statuses():
     vol = dict(nx=8, ny=8, nz=8, dx=0.4, dy=0.4, dz=0.4)
     cases = [
         (plenoptic_camera(4, 8, 0.04, 2, 2, fill=1.5), 1),           # fill > 1
-        (plenoptic_camera(4, 8, 0.04, 2, 2, pose=pose_yaw(90.0)), 3),  # needs a quarter-turn permutation
         (dict(single_camera(32, 0.04, 2), f_main=0.0), 2),           # zero focal length
         (dict(single_camera(32, 0.04, 2), d_det=0.0), 3),            # detector on the angular plane
         (dict(single_camera(32, 0.04, 2), k_s=0), 1),
@@ -193,6 +196,12 @@ def test_error_statuses():
             lfm.Plan(dict(volume=vol, cameras=[cam]), device=-1)
         assert e.value.status == status, (cam, e.value)
         assert "camera 0" in str(e.value)
+    # a quarter turn is an exact relabelling only between equal axes (reading R7)
+    vol2 = dict(nx=8, ny=8, nz=10, dx=0.4, dy=0.4, dz=0.4)
+    with pytest.raises(lfm.LfmError) as e:
+        lfm.Plan(dict(volume=vol2, cameras=[plenoptic_camera(4, 8, 0.04, 2, 2, pose=pose_yaw(90.0))]), device=-1)
+    assert e.value.status == 3 and "quarter-turn" in str(e.value)
+    lfm.Plan(dict(volume=vol, cameras=[plenoptic_camera(4, 8, 0.04, 2, 2, pose=pose_yaw(90.0))]), device=-1)
     with pytest.raises(lfm.LfmError) as e:
         lfm.Plan(dict(volume=vol, cameras=[]), device=-1)
     assert e.value.status == 1

@@ -19,7 +19,7 @@ from oracle.system import SystemOperator, build_system
 from workloads import make_config, normal_vector, uniform_volume
 from workloads.geometry import plenoptic_camera, single_camera
 
-TINY = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_dirac"]
+TINY = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_dirac", "tiny_turn"]
 
 
 @pytest.mark.parametrize("name", TINY)

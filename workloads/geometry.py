@@ -92,6 +92,11 @@ def make_config(name):
         return dict(name=name, volume=volume(16, 0.4),
                     cameras=[plenoptic_camera(4, 8, 0.04, 2, 2, basis=DIRAC),
                              single_camera(32, 0.04, 2, pose=pose_yaw(15.0), basis=DIRAC)])
+    if name == "tiny_turn":  # poses beyond 45 degrees (NEXT-4, reading R7): quarter-turn relabelling + shears
+        return dict(name=name, volume=volume(16, 0.4),
+                    cameras=[plenoptic_camera(4, 8, 0.04, 2, 2, pose=pose_yaw(120.0)),
+                             single_camera(32, 0.04, 2, pose=pose_yaw_pitch(70.0, 50.0)),
+                             single_camera(32, 0.04, 2, pose=pose_yaw(-90.0))])
     if name == "small_two":  # a 32^3 two-camera case: several tiles + ragged edges, oracle in seconds
         return dict(name=name, volume=volume(32, 0.4),
                     cameras=[plenoptic_camera(8, 8, 0.04, 4, 4),
@@ -112,5 +117,5 @@ def make_config(name):
     raise KeyError(name)
 
 
-CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "small_two",
+CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two",
            "64^3 single", "128^3 two-camera", "256^3 four-camera"]
