@@ -94,6 +94,16 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_fw, fw.data(), fw.size() * 4, err)) != LFM_OK) return st;
     bytes += f.f_off.size() * 4 + fr.size() * 4 + fw.size() * 4;
   }
+  if (!f.x_off.empty()) {
+    std::vector<int32_t> xk(f.x_k);
+    xk.push_back(0);
+    std::vector<float> xa(f.x_a);
+    xa.resize(xa.size() + 256, 0.f);
+    if ((st = dev_upload(&f.d_xoff, f.x_off.data(), f.x_off.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_xk, xk.data(), xk.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_xa, xa.data(), xa.size() * 4, err)) != LFM_OK) return st;
+    bytes += f.x_off.size() * 4 + xk.size() * 4 + xa.size() * 4;
+  }
   if (!f.m8_off.empty()) {
     std::vector<float> mw(f.m8_w64.size() + 8);
     for (size_t i = 0; i < f.m8_w64.size(); ++i) mw[i] = (float)f.m8_w64[i];
@@ -257,6 +267,8 @@ void free_camera(CameraPlan& cp) {
     f->d_m8off = nullptr; f->d_m8seg = nullptr; f->d_m8w = nullptr;
     dfree(f->d_foff); dfree(f->d_frow); dfree(f->d_fw);
     f->d_foff = nullptr; f->d_frow = nullptr; f->d_fw = nullptr;
+    dfree(f->d_xoff); dfree(f->d_xk); dfree(f->d_xa);
+    f->d_xoff = nullptr; f->d_xk = nullptr; f->d_xa = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
@@ -300,6 +312,9 @@ struct SepArgs {
   const int2* chunks;     // band_s_kernel chunk lists
   const int32_t* chunk_off;
   const int2* chunk_w;
+  const int32_t* t_xoff;  // tensor-core blocks (band_x_kernel)
+  const int32_t* t_xk;
+  const float4* t_xa;
   const int32_t* t_foff;  // flat MSEG entries (band_f_kernel)
   const int4* t_frow;
   const float4* t_fw;
@@ -1271,6 +1286,127 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_f_kernel(SepArgs a) {
   }
 }
 
+// Tensor-core t pass (identity s, one output row tile of 16 rows per warp-group): out = C U with C sparse,
+// evaluated as block-sparse dense products on the legacy tensor path (mma.sync m16n8k8, tf32 in, fp32
+// accumulate) in 3xTF32 form, C U = C_hi U_hi + C_hi U_lo + C_lo U_hi (+ O(2^-22)), which keeps fp32-level
+// accuracy.  The weights arrive pre-split in fragment order (build_mma); the source values are split in
+// registers (cvt.rna.tf32).  CTA = NW warps on one 16-row tile, each warp 64 columns (8 n8 tiles).
+__device__ __forceinline__ uint32_t tf32_rna(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) band_x_kernel(SepArgs a) {
+  // Column map: n-index g of n8 tile j is column c0 + 8 g + j, so a lane's B values of one source row are
+  // 8 consecutive floats (two 16-byte loads) and its accumulators cover 16 consecutive columns.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int ty = blockIdx.y + a.ty0, b = blockIdx.z;
+  const int c0 = (blockIdx.x * NW + warp) * 64;  // this warp's first column
+  if (c0 >= a.n_is) return;
+  const int e0 = a.offs[b], e1 = a.offs[b + 1];
+  const int ntile = (a.n_ot + 15) / 16;
+  float acc[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+  const int cl = c0 + 8 * g;                               // this lane's 8 source columns
+  const bool cfull = cl + 8 <= a.n_is && ((a.src_pitch & 3) == 0);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = e0; e < e1; ++e) {
+    const Term term = a.terms[e];
+    const float* src = a.src + term.src_off + cl;
+    const bool vec = cfull && ((term.src_off & 3) == 0);
+    const size_t ti = (size_t)term.t_tab * ntile + ty;
+    const int q0 = __ldg(a.t_xoff + ti), q1 = __ldg(a.t_xoff + ti + 1);
+#pragma unroll 2
+    for (int q = q0; q < q1; ++q) {
+      const int k0 = __ldg(a.t_xk + q);
+      const float4 ah = __ldg(a.t_xa + 2 * ((size_t)q * 32 + lane));
+      const float4 al = __ldg(a.t_xa + 2 * ((size_t)q * 32 + lane) + 1);
+      const uint32_t Ah[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z), __float_as_uint(ah.w)};
+      const uint32_t Al[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z), __float_as_uint(al.w)};
+      const int ka = k0 + tq, kb = k0 + tq + 4;
+      const bool ina = ka >= a.win_r0 && ka < a.win_r1, inb = kb >= a.win_r0 && kb < a.win_r1;
+      const float* pa = src + (size_t)ka * a.src_pitch;
+      const float* pb = src + (size_t)kb * a.src_pitch;
+      float bv0[8], bv1[8];
+      if (vec) {
+        const float4 u0 = ina ? __ldg(reinterpret_cast<const float4*>(pa)) : z;
+        const float4 u1 = ina ? __ldg(reinterpret_cast<const float4*>(pa) + 1) : z;
+        const float4 u2 = inb ? __ldg(reinterpret_cast<const float4*>(pb)) : z;
+        const float4 u3 = inb ? __ldg(reinterpret_cast<const float4*>(pb) + 1) : z;
+        bv0[0] = u0.x; bv0[1] = u0.y; bv0[2] = u0.z; bv0[3] = u0.w; bv0[4] = u1.x; bv0[5] = u1.y; bv0[6] = u1.z; bv0[7] = u1.w;
+        bv1[0] = u2.x; bv1[1] = u2.y; bv1[2] = u2.z; bv1[3] = u2.w; bv1[4] = u3.x; bv1[5] = u3.y; bv1[6] = u3.z; bv1[7] = u3.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool cin = cl + j < a.n_is;
+          bv0[j] = (ina && cin) ? __ldg(pa + j) : 0.f;
+          bv1[j] = (inb && cin) ? __ldg(pb + j) : 0.f;
+        }
+      }
+      // 3xTF32 split of the source: hi = truncation to tf32 (exact), lo = the exact fp32 remainder; the three
+      // products are issued tile-interleaved so consecutive MMAs never share an accumulator
+      uint32_t h0[8], h1[8], l0[8], l1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h0[j] = __float_as_uint(bv0[j]) & 0xffffe000u;
+        h1[j] = __float_as_uint(bv1[j]) & 0xffffe000u;
+        l0[j] = __float_as_uint(bv0[j] - __uint_as_float(h0[j]));
+        l1[j] = __float_as_uint(bv1[j] - __uint_as_float(h1[j]));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Al, h0[j], h1[j]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Ah, l0[j], l1[j]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Ah, h0[j], h1[j]);
+    }
+  }
+  // C fragment of tile j: (row g, n 2tq / 2tq+1) and (row g+8, ...) -> columns c0 + 16 tq + j and
+  // c0 + 16 tq + 8 + j: a lane's 16 consecutive columns per row
+  float* outb = a.out + (size_t)b * a.out_stride;
+  const int r0 = 16 * ty + g;
+  const int cw = c0 + 16 * tq;
+  const bool ovec = cw + 16 <= a.n_os && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int row = r0 + 8 * h;
+    if (row >= a.n_ot) continue;
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = a.out_scale * acc[j][2 * h];
+      v[8 + j] = a.out_scale * acc[j][2 * h + 1];
+    }
+    float* p = outb + (size_t)row * a.out_pitch + cw;
+    if (ovec) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float4 o = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        if (a.accumulate) {
+          const float4 qv = reinterpret_cast<float4*>(p)[k];
+          o.x += qv.x; o.y += qv.y; o.z += qv.z; o.w += qv.w;
+        }
+        reinterpret_cast<float4*>(p)[k] = o;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (cw + k < a.n_os) p[k] = a.accumulate ? p[k] + v[k] : v[k];
+    }
+  }
+}
+
 template <int TS, int TT, int NT>
 static lfm_status launch_band_f(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
   if (tout) {
@@ -1433,6 +1569,9 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.chunks = reinterpret_cast<const int2*>(op.d_chunks);
   a.chunk_w = reinterpret_cast<const int2*>(op.d_chunk_w);
   a.chunk_off = op.d_chunk_off;
+  a.t_xoff = op.ft->d_xoff;
+  a.t_xk = op.ft->d_xk;
+  a.t_xa = reinterpret_cast<const float4*>(op.ft->d_xa);
   a.t_foff = op.ft->d_foff;
   a.t_frow = reinterpret_cast<const int4*>(op.ft->d_frow);
   a.t_fw = reinterpret_cast<const float4*>(op.ft->d_fw);
@@ -1512,6 +1651,19 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 #undef LFM_BG_CASE
     err = "unsupported band_g tile";
     return LFM_E_INVALID;
+  }
+  if (op.kind == 7) {
+    if (!op.ft->d_xoff || op.tout) { err = "band_x: needs the tensor-core form and normal output"; return LFM_E_INVALID; }
+    // grid: x = column groups of NW*64, y = 16-row tiles
+    const int nw = op.nt / 32;
+    dim3 gx((op.n_is + nw * 64 - 1) / (nw * 64), (r1 + 15) / 16 - r0 / 16, n_out);
+    a.ty0 = r0 / 16;
+    if (nw == 4) band_x_kernel<4><<<gx, 128, 0, s>>>(a);
+    else if (nw == 2) band_x_kernel<2><<<gx, 64, 0, s>>>(a);
+    else if (nw == 8) band_x_kernel<8><<<gx, 256, 0, s>>>(a);
+    else { err = "unsupported band_x warps"; return LFM_E_INVALID; }
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "band_x_kernel launch", err);
   }
   if (op.kind == 5) {
     if (!op.ft->d_foff) { err = "band_f: t family has no flat MSEG form"; return LFM_E_INVALID; }
@@ -2070,6 +2222,32 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         }
       }
       op.kind = 0;
+      // band_x: tensor cores (one-table MMA form, unit scales, normal output)
+      for (int nt : {64, 128, 256}) {
+        if (st != LFM_OK || op.ft->x_off.empty() || op.tout) break;
+        bool unit = true;
+        for (const Term& t : op.terms) unit &= t.scale == 1.f;
+        if (!unit) break;
+        op.kind = 7; op.ts = 64 * (nt / 32); op.tt = 16; op.nt = nt; op.nb = 1; op.stage = 0; op.stages = 1; op.mgrp = 4;
+        fill_sep_geometry(op);
+        free_sep_dev(op);
+        size_t bytes = 0;
+        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+        float ms = 0, tot = 0;
+        bool ok = true;
+        for (int rep = 0; rep < 3 && ok; ++rep) {
+          cudaEventRecord(e0, 0);
+          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+          cudaEventRecord(e1, 0);
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (rep > 0) tot += ms;
+        }
+        if (!ok || cudaGetLastError() != cudaSuccess) continue;
+        if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_x nt %3d: %.3f ms\n", names[q], nt, tot / 2);
+        if (tot < best) { best = tot; bts = op.ts; btt = 16; bnt = nt; bnb = 1; bst = 0; bkind = 7; bstages = 1; bmgrp = 4; }
+      }
+      op.kind = 0;
       // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)
       bool unit = true;
       for (const Term& t : op.terms) unit &= t.scale == 1.f && (t.src_off % 4) == 0;
@@ -2139,7 +2317,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d grp %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : op.kind == 7 ? "band_x" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
         std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb,

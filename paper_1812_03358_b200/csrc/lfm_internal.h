@@ -61,6 +61,14 @@ struct BandFamily {
   int32_t* d_foff = nullptr;
   int32_t* d_frow = nullptr;
   float* d_fw = nullptr;
+  // tensor-core form (band_x): per tile of 16 rows, the union of the rows' supports cut into blocks of 8
+  // source cells; per block the 16x8 weights split into tf32 hi + lo parts in mma.m16n8k8 A-fragment order
+  // (per lane: hi[4], lo[4])
+  std::vector<int32_t> x_off, x_k;         // x_off[tile] .. +1 into blocks; x_k[block] = first source cell
+  std::vector<float> x_a;                  // 256 floats per block
+  int32_t* d_xoff = nullptr;
+  int32_t* d_xk = nullptr;
+  float* d_xa = nullptr;
   // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
   std::vector<int32_t> m8_off, m8_seg;
   std::vector<double> m8_w64;
@@ -109,6 +117,7 @@ struct SepOp {
                                    // 3: band_m_kernel (L2 gather over MSEG segments of ft)
                                    // 4: band_s_kernel (MSEG segments, source rows streamed through smem)
                                    // 5: band_f_kernel (flat MSEG entry lists, L2 gather, deep unroll)
+                                   // 7: band_x_kernel (tensor cores: mma.sync m16n8k8 3xTF32 over 16-row blocks)
   long long src_pitch = 0;         // floats between source rows (0: n_is)
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)

@@ -364,6 +364,81 @@ struct FamilyBuilder {
   }
 };
 
+// tf32 value of an fp32 (round to nearest, ties away from zero, 10 explicit mantissa bits; the low 13 bits
+// cleared), as cvt.rna.tf32.f32 does on the device.
+static float tf32_round(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u += 0x1000u;
+  u &= 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// Tensor-core form of a one-table family (band_x): tiles of 16 rows; the union of the rows' non-zero
+// source cells split at zero runs >= 8 cells into runs, each covered by blocks of 8 cells; per block the
+// fp32 weights (one rounding from fp64) split as w = hi + lo + O(2^-22 w) with hi, lo tf32, laid out per
+// lane of mma.m16n8k8 (row-major A: a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]).
+static void build_mma(BandFamily& f) {
+  const int nt = (f.n_rows + 15) / 16;
+  f.x_off.assign((size_t)f.n_tables * nt + 1, 0);
+  f.x_k.clear();
+  f.x_a.clear();
+  std::vector<char> any;
+  std::vector<float> A;
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int t = 0; t < nt; ++t) {
+      f.x_off[(size_t)m * nt + t] = (int)f.x_k.size();
+      const int r0 = 16 * t, r1 = std::min(f.n_rows, r0 + 16);
+      int lo = 1 << 30, hi = -1;
+      for (int r = r0; r < r1; ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        if (!f.len[idx]) continue;
+        lo = std::min(lo, (int)f.start[idx]);
+        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
+      }
+      if (hi < 0) continue;
+      any.assign(hi - lo, 0);
+      for (int r = r0; r < r1; ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e)
+          if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e - lo] = 1;
+      }
+      auto weight = [&](int r, int k) -> float {  // fp32 weight of row r at source k (0 outside the band)
+        if (r >= r1) return 0.f;
+        size_t idx = (size_t)m * f.n_rows + r;
+        const int e = k - f.start[idx];
+        if (e < 0 || e >= f.len[idx]) return 0.f;
+        return (float)f.w64[idx * f.taps + e];
+      };
+      int p = 0;
+      const int W = hi - lo;
+      while (p < W) {
+        while (p < W && !any[p]) ++p;
+        if (p >= W) break;
+        int a = p, last = p;
+        while (p < W) {
+          if (any[p]) { last = p; ++p; continue; }
+          int zs = p;
+          while (p < W && !any[p]) ++p;
+          if (p - zs >= 8 || p >= W) break;
+        }
+        for (int k0 = lo + a; k0 <= lo + last; k0 += 8) {
+          f.x_k.push_back(k0);
+          for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane / 4, tq = lane % 4;
+            const float v[4] = {weight(r0 + g, k0 + tq), weight(r0 + g + 8, k0 + tq), weight(r0 + g, k0 + tq + 4),
+                                weight(r0 + g + 8, k0 + tq + 4)};
+            for (int q = 0; q < 4; ++q) f.x_a.push_back(tf32_round(v[q]));
+            for (int q = 0; q < 4; ++q) f.x_a.push_back(tf32_round(v[q] - tf32_round(v[q])));
+          }
+        }
+      }
+    }
+  f.x_off[(size_t)f.n_tables * nt] = (int)f.x_k.size();
+}
+
 // MSEG form with groups of 8 rows (segments split at zero runs >= 2 source cells, weights 8 per cell).
 static void build_mseg8(BandFamily& f) {
   const int G = 8;
@@ -1214,9 +1289,11 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   cp.ca1n.want_mseg = 1;
   make_rows_by_slice(cp.ca1n, cp.ca[1]);
   build_mseg8(cp.ca1n);
+  build_mma(cp.ca1n);
   cp.cf1n.want_mseg = 1;
   make_cols_by_slice(cp.cf1n, cp.cf[1]);
   build_mseg8(cp.cf1n);
+  build_mma(cp.cf1n);
   if (std::getenv("LFM_DEBUG")) {
     const BandFamily* fs[] = {&cp.ca1n, &cp.cf1n, &cp.ca[1], &cp.cf[1], &cp.ca[0], &cp.cf[0]};
     const char* nm[] = {"ca1 rows-by-slice", "cf1 cols-by-slice", "ca1", "cf1", "ca0", "cf0"};
@@ -1357,8 +1434,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
         if (kind >= 1) {
           bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
                     (kind < 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty())) &&
-                    (kind != 4 || (ts == 128 && !op.tout)) && (kind != 5 || !op.ft->f_off.empty());
-          for (const Term& t : op.terms) ok &= kind != 4 || t.scale == 1.f;
+                    (kind != 4 || (ts == 128 && !op.tout)) && (kind != 5 || !op.ft->f_off.empty()) &&
+                    (kind != 7 || (!op.ft->x_off.empty() && !op.tout));
+          for (const Term& t : op.terms) ok &= (kind != 4 && kind != 7) || t.scale == 1.f;
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
           if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
         } else if (sep_smem(op, nb) > (size_t)220 * 1024) {
