@@ -1302,25 +1302,31 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) band_x_kernel(SepArgs a) {
-  // Column map: n-index g of n8 tile j is column c0 + 8 g + j, so a lane's B values of one source row are
-  // 8 consecutive floats (two 16-byte loads) and its accumulators cover 16 consecutive columns.
+template <int NW, int NJ, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) band_x_kernel(SepArgs a) {
+  // Column map: n-index g of n8 tile j is column c0 + NJ g + j, so a lane's B values of one source row are
+  // NJ consecutive floats and its accumulators cover 2 NJ consecutive columns.
+  constexpr int WC = 8 * NJ;  // columns per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const int ty = blockIdx.y + a.ty0, b = blockIdx.z;
-  const int c0 = (blockIdx.x * NW + warp) * 64;  // this warp's first column
+  const int c0 = (blockIdx.x * NW + warp) * WC;  // this warp's first column
   if (c0 >= a.n_is) return;
   const int e0 = a.offs[b], e1 = a.offs[b + 1];
   const int ntile = (a.n_ot + 15) / 16;
-  float acc[8][4];
+  // The tensor-core accumulator adds with truncation, so a long chain of MMAs into one accumulator drifts
+  // (~N ulp for N MMAs, all in one direction for same-sign data).  The MMAs therefore accumulate only
+  // XBLK blocks at a time (1: every block, with fresh accumulators); each partial sum is then added to `acc`
+  // with a round-to-nearest FADD.
+  constexpr int XBLK = 1;
+  float acc[NJ][4], part[NJ][4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < NJ; ++j)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
-  const int cl = c0 + 8 * g;                               // this lane's 8 source columns
-  const bool cfull = cl + 8 <= a.n_is && ((a.src_pitch & 3) == 0);
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < 4; ++q) acc[j][q] = part[j][q] = 0.f;
+  int nblk = 0;
+  const int cl = c0 + NJ * g;                              // this lane's NJ source columns
+  const bool cfull = cl + NJ <= a.n_is && ((a.src_pitch & 3) == 0);
   for (int e = e0; e < e1; ++e) {
     const Term term = a.terms[e];
     const float* src = a.src + term.src_off + cl;
@@ -1338,17 +1344,18 @@ __global__ void __launch_bounds__(NW * 32) band_x_kernel(SepArgs a) {
       const bool ina = ka >= a.win_r0 && ka < a.win_r1, inb = kb >= a.win_r0 && kb < a.win_r1;
       const float* pa = src + (size_t)ka * a.src_pitch;
       const float* pb = src + (size_t)kb * a.src_pitch;
-      float bv0[8], bv1[8];
+      float bv0[NJ], bv1[NJ];
       if (vec) {
-        const float4 u0 = ina ? __ldg(reinterpret_cast<const float4*>(pa)) : z;
-        const float4 u1 = ina ? __ldg(reinterpret_cast<const float4*>(pa) + 1) : z;
-        const float4 u2 = inb ? __ldg(reinterpret_cast<const float4*>(pb)) : z;
-        const float4 u3 = inb ? __ldg(reinterpret_cast<const float4*>(pb) + 1) : z;
-        bv0[0] = u0.x; bv0[1] = u0.y; bv0[2] = u0.z; bv0[3] = u0.w; bv0[4] = u1.x; bv0[5] = u1.y; bv0[6] = u1.z; bv0[7] = u1.w;
-        bv1[0] = u2.x; bv1[1] = u2.y; bv1[2] = u2.z; bv1[3] = u2.w; bv1[4] = u3.x; bv1[5] = u3.y; bv1[6] = u3.z; bv1[7] = u3.w;
+#pragma unroll
+        for (int v = 0; v < NJ / 4; ++v) {
+          const float4 u0 = ina ? __ldg(reinterpret_cast<const float4*>(pa) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 u1 = inb ? __ldg(reinterpret_cast<const float4*>(pb) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          bv0[4 * v] = u0.x; bv0[4 * v + 1] = u0.y; bv0[4 * v + 2] = u0.z; bv0[4 * v + 3] = u0.w;
+          bv1[4 * v] = u1.x; bv1[4 * v + 1] = u1.y; bv1[4 * v + 2] = u1.z; bv1[4 * v + 3] = u1.w;
+        }
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           const bool cin = cl + j < a.n_is;
           bv0[j] = (ina && cin) ? __ldg(pa + j) : 0.f;
           bv1[j] = (inb && cin) ? __ldg(pb + j) : 0.f;
@@ -1356,42 +1363,78 @@ __global__ void __launch_bounds__(NW * 32) band_x_kernel(SepArgs a) {
       }
       // 3xTF32 split of the source: hi = truncation to tf32 (exact), lo = the exact fp32 remainder; the three
       // products are issued tile-interleaved so consecutive MMAs never share an accumulator
-      uint32_t h0[8], h1[8], l0[8], l1[8];
+      uint32_t h0[NJ], h1[NJ], l0[NJ], l1[NJ];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         h0[j] = __float_as_uint(bv0[j]) & 0xffffe000u;
         h1[j] = __float_as_uint(bv1[j]) & 0xffffe000u;
         l0[j] = __float_as_uint(bv0[j] - __uint_as_float(h0[j]));
         l1[j] = __float_as_uint(bv1[j] - __uint_as_float(h1[j]));
       }
+      if (XBLK == 1) {
+        // fresh tensor-core accumulators per block, in groups of 4 tiles (few live registers), then RN adds
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Al, h0[j], h1[j]);
+        for (int j0 = 0; j0 < NJ; j0 += 4) {
+          float pp[4][4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Ah, l0[j], l1[j]);
+          for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mma_tf32(acc[j], Ah, h0[j], h1[j]);
+            for (int c = 0; c < 4; ++c) pp[j][c] = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Al, h0[j0 + j], h1[j0 + j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Ah, l0[j0 + j], l1[j0 + j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Ah, h0[j0 + j], h1[j0 + j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[j0 + j][c] += pp[j][c];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Al, h0[j], h1[j]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Ah, l0[j], l1[j]);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Ah, h0[j], h1[j]);
+        if (++nblk == XBLK) {
+          nblk = 0;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              acc[j][c] += part[j][c];
+              part[j][c] = 0.f;
+            }
+        }
+      }
     }
   }
-  // C fragment of tile j: (row g, n 2tq / 2tq+1) and (row g+8, ...) -> columns c0 + 16 tq + j and
-  // c0 + 16 tq + 8 + j: a lane's 16 consecutive columns per row
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] += part[j][c];
+  // C fragment of tile j: (row g, n 2tq / 2tq+1) and (row g+8, ...) -> columns c0 + 2 NJ tq + j and
+  // c0 + 2 NJ tq + NJ + j: a lane's 2 NJ consecutive columns per row
   float* outb = a.out + (size_t)b * a.out_stride;
   const int r0 = 16 * ty + g;
-  const int cw = c0 + 16 * tq;
-  const bool ovec = cw + 16 <= a.n_os && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
+  const int cw = c0 + 2 * NJ * tq;
+  const bool ovec = cw + 2 * NJ <= a.n_os && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int row = r0 + 8 * h;
     if (row >= a.n_ot) continue;
-    float v[16];
+    float v[2 * NJ];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       v[j] = a.out_scale * acc[j][2 * h];
-      v[8 + j] = a.out_scale * acc[j][2 * h + 1];
+      v[NJ + j] = a.out_scale * acc[j][2 * h + 1];
     }
     float* p = outb + (size_t)row * a.out_pitch + cw;
     if (ovec) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < NJ / 2; ++k) {
         float4 o = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
         if (a.accumulate) {
           const float4 qv = reinterpret_cast<float4*>(p)[k];
@@ -1401,7 +1444,7 @@ __global__ void __launch_bounds__(NW * 32) band_x_kernel(SepArgs a) {
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
+      for (int k = 0; k < 2 * NJ; ++k)
         if (cw + k < a.n_os) p[k] = a.accumulate ? p[k] + v[k] : v[k];
     }
   }
@@ -1654,14 +1697,18 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   }
   if (op.kind == 7) {
     if (!op.ft->d_xoff || op.tout) { err = "band_x: needs the tensor-core form and normal output"; return LFM_E_INVALID; }
-    // grid: x = column groups of NW*64, y = 16-row tiles
+    // grid: x = column groups of ts (= warps x 8 NJ), y = 16-row tiles; op.stages = NJ (n8 tiles per warp)
     const int nw = op.nt / 32;
-    dim3 gx((op.n_is + nw * 64 - 1) / (nw * 64), (r1 + 15) / 16 - r0 / 16, n_out);
+    dim3 gx((op.n_is + op.ts - 1) / op.ts, (r1 + 15) / 16 - r0 / 16, n_out);
     a.ty0 = r0 / 16;
-    if (nw == 4) band_x_kernel<4><<<gx, 128, 0, s>>>(a);
-    else if (nw == 2) band_x_kernel<2><<<gx, 64, 0, s>>>(a);
-    else if (nw == 8) band_x_kernel<8><<<gx, 256, 0, s>>>(a);
-    else { err = "unsupported band_x warps"; return LFM_E_INVALID; }
+    if (op.ts != nw * 8 * op.stages) { err = "band_x: ts must be warps x 8 x NJ"; return LFM_E_INVALID; }
+    // minimum resident CTAs per SM: ~128 registers per thread for NJ 8, ~80 for NJ 4
+    if (op.stages == 8 && nw == 4) band_x_kernel<4, 8, 4><<<gx, 128, 0, s>>>(a);
+    else if (op.stages == 8 && nw == 2) band_x_kernel<2, 8, 8><<<gx, 64, 0, s>>>(a);
+    else if (op.stages == 4 && nw == 4) band_x_kernel<4, 4, 6><<<gx, 128, 0, s>>>(a);
+    else if (op.stages == 4 && nw == 8) band_x_kernel<8, 4, 3><<<gx, 256, 0, s>>>(a);
+    else if (op.stages == 4 && nw == 2) band_x_kernel<2, 4, 12><<<gx, 64, 0, s>>>(a);
+    else { err = "unsupported band_x configuration"; return LFM_E_INVALID; }
     ++g_launches;
     return cuda_check(cudaGetLastError(), "band_x_kernel launch", err);
   }
@@ -2223,12 +2270,15 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       }
       op.kind = 0;
       // band_x: tensor cores (one-table MMA form, unit scales, normal output)
-      for (int nt : {64, 128, 256}) {
+      const int xcand[][2] = {{128, 8}, {64, 8}, {128, 4}, {256, 4}, {64, 4}};  // threads, NJ
+      for (auto& xc : xcand) {
+        const int nt = xc[0], nj = xc[1];
         if (st != LFM_OK || op.ft->x_off.empty() || op.tout) break;
         bool unit = true;
         for (const Term& t : op.terms) unit &= t.scale == 1.f;
         if (!unit) break;
-        op.kind = 7; op.ts = 64 * (nt / 32); op.tt = 16; op.nt = nt; op.nb = 1; op.stage = 0; op.stages = 1; op.mgrp = 4;
+        op.kind = 7; op.ts = (nt / 32) * 8 * nj; op.tt = 16; op.nt = nt; op.nb = 1; op.stage = 0; op.stages = nj;
+        op.mgrp = 4;
         fill_sep_geometry(op);
         free_sep_dev(op);
         size_t bytes = 0;
@@ -2244,8 +2294,8 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
           if (rep > 0) tot += ms;
         }
         if (!ok || cudaGetLastError() != cudaSuccess) continue;
-        if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_x nt %3d: %.3f ms\n", names[q], nt, tot / 2);
-        if (tot < best) { best = tot; bts = op.ts; btt = 16; bnt = nt; bnb = 1; bst = 0; bkind = 7; bstages = 1; bmgrp = 4; }
+        if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_x nt %3d NJ %d: %.3f ms\n", names[q], nt, nj, tot / 2);
+        if (tot < best) { best = tot; bts = op.ts; btt = 16; bnt = nt; bnb = 1; bst = 0; bkind = 7; bstages = nj; bmgrp = 4; }
       }
       op.kind = 0;
       // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)

@@ -377,7 +377,7 @@ static float tf32_round(float v) {
 }
 
 // Tensor-core form of a one-table family (band_x): tiles of 16 rows; the union of the rows' non-zero
-// source cells split at zero runs >= 8 cells into runs, each covered by blocks of 8 cells; per block the
+// source cells covered by the fewest blocks of 8 consecutive cells; per block the
 // fp32 weights (one rounding from fp64) split as w = hi + lo + O(2^-22 w) with hi, lo tf32, laid out per
 // lane of mma.m16n8k8 (row-major A: a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]).
 static void build_mma(BandFamily& f) {
@@ -412,19 +412,15 @@ static void build_mma(BandFamily& f) {
         if (e < 0 || e >= f.len[idx]) return 0.f;
         return (float)f.w64[idx * f.taps + e];
       };
-      int p = 0;
+      // fewest blocks of 8 consecutive source cells covering every non-zero column: greedy interval cover
+      // (a block starts at the first non-zero column not yet covered)
       const int W = hi - lo;
-      while (p < W) {
-        while (p < W && !any[p]) ++p;
-        if (p >= W) break;
-        int a = p, last = p;
-        while (p < W) {
-          if (any[p]) { last = p; ++p; continue; }
-          int zs = p;
-          while (p < W && !any[p]) ++p;
-          if (p - zs >= 8 || p >= W) break;
-        }
-        for (int k0 = lo + a; k0 <= lo + last; k0 += 8) {
+      std::vector<int> starts;
+      for (int p = 0; p < W; ++p)
+        if (any[p] && (starts.empty() || p >= starts.back() + 8)) starts.push_back(p);
+      for (int a0 : starts) {
+        {
+          const int k0 = lo + a0;
           f.x_k.push_back(k0);
           for (int lane = 0; lane < 32; ++lane) {
             const int g = lane / 4, tq = lane % 4;
@@ -1302,6 +1298,12 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
                    fs[i]->st_nnz / (4 * fs[i]->st_cols_g4), fs[i]->st_nnz / (4 * fs[i]->st_cols_m),
                    fs[i]->st_msegs / ((double)fs[i]->n_tables * fs[i]->n_groups), fs[i]->st_cols_m / fs[i]->st_msegs,
                    fs[i]->st_nnz / (4 * fs[i]->st_cols_nz));
+    for (const BandFamily* f : {&cp.ca1n, &cp.cf1n}) {
+      double nnz = 0;
+      for (int v : f->cnt) nnz += v;
+      std::fprintf(stderr, "[lfm] tensor-core form: %zu blocks of 16x8, density %.3f\n", f->x_k.size(),
+                   nnz / (128.0 * f->x_k.size()));
+    }
     for (int G : {4, 8, 16})
       std::fprintf(stderr, "[lfm] MSEG density with %2d-row groups: ca1n %.3f  cf1n %.3f  ca0 %.3f  cf0 %.3f\n", G,
                    mseg_density(cp.ca1n, G), mseg_density(cp.cf1n, G), mseg_density(cp.ca[0], G), mseg_density(cp.cf[0], G));
