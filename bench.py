@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--config", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-per-view", action="store_true", help="skip the per-view path reference timing")
     return ap.parse_args()
 
 
@@ -314,6 +315,30 @@ def run_ours(args, rank, world, local_rank):
             kname = "%s A_forward, camera %d" % (args.path, dom_cam)
         dom = dict(fwd_ms=sum(fwd_ms) / len(fwd_ms), adj_ms=sum(adj_ms) / len(adj_ms), fma=fma_f, fma_adj=fma_a,
                    name=kname)
+    # the paper's own evaluation order (per-view factored chain) on the same
+    # workload, for reference: device time of one forward and one adjoint per camera
+    per_view = None
+    if world == 1 and path == lfm.COLLAPSED and not args.no_per_view:
+        fv, av = [], []
+        for c in range(plan.n_cam):
+            lfm.A_forward(plan, c, x, ys[c], ws, path=lfm.PER_VIEW)
+            tf, ta = [], []
+            for _ in range(3):
+                a_, b_, c_, d_ = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+                flush.zero_()
+                a_.record(stream)
+                lfm.A_forward(plan, c, x, ys[c], ws, path=lfm.PER_VIEW)
+                b_.record(stream)
+                flush.zero_()
+                c_.record(stream)
+                lfm.A_adjoint(plan, c, rs[c], g, ws, path=lfm.PER_VIEW)
+                d_.record(stream)
+                torch.cuda.synchronize()
+                tf.append(a_.elapsed_time(b_))
+                ta.append(c_.elapsed_time(d_))
+            fv.append(sorted(tf)[1])
+            av.append(sorted(ta)[1])
+        per_view = {"fwd_ms": fv, "adj_ms": av, "pairs_per_s": 1e3 / (sum(fv) + sum(av))}
     sm = clocks.stop()
     # e2e: through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -394,6 +419,8 @@ def run_ours(args, rank, world, local_rank):
             "hbm_gbs_alg": pair_bytes / (ms_mean * 1e-3) / 1e9,
             "hbm_frac_of_measured": pair_bytes / (ms_mean * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
             "roofline": roof, "clocks": sm, "gpu_launches": launches[0] * args.steps}
+    if per_view is not None:
+        line["per_view_path"] = per_view
     if e2e:
         line["e2e"] = {"value": 1e3 / e2e_ms, "unit": "pairs/s", "h2d_bytes_per_step": e2e["h2d"],
                        "d2h_bytes_per_step": e2e["d2h"]}

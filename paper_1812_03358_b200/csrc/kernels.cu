@@ -1207,9 +1207,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_f_kernel(SepArgs a) {
           fma4x4(acc[j], __ldg(a.t_fw + 4 * q + 3), u3);
         }
       } else {
+        // row window (adjoint detector-row sharding): entries are in increasing row order within the group,
+        // so only the blocks of 4 entries that straddle or lie inside [win_r0, win_r1) are visited
+        const int* fr = reinterpret_cast<const int*>(a.t_frow);
+        int lo = q0, hi = q1;  // first block whose last row >= win_r0, first block whose first row >= win_r1
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(fr + 4 * mid + 3) < a.win_r0) lo = mid + 1; else hi = mid;
+        }
+        int lo2 = lo, hi2 = q1;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (__ldg(fr + 4 * mid) < a.win_r1) lo2 = mid + 1; else hi2 = mid;
+        }
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll UNR
-        for (int q = q0; q < q1; ++q) {
+        for (int q = lo; q < lo2; ++q) {
           const int4 rw = __ldg(a.t_frow + q);
           const bool i0 = rw.x >= a.win_r0 && rw.x < a.win_r1, i1 = rw.y >= a.win_r0 && rw.y < a.win_r1;
           const bool i2 = rw.z >= a.win_r0 && rw.z < a.win_r1, i3 = rw.w >= a.win_r0 && rw.w < a.win_r1;
