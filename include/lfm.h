@@ -110,6 +110,9 @@ typedef struct {
   double bytes_alg[2];      /* algorithmic HBM bytes per A_forward per path */
   double fma_stage[2];      /* algorithmic FMAs (non-zeros x columns) of one launch of stage
                                LFM_STAGE_FWD_T / LFM_STAGE_ADJ_T (lfm_A_stage) */
+  double mma_stage[2];      /* tensor-core MACs one launch of those stages issues when it runs on the tcgen05
+                               kernel (3 products x dense 128 x 16 blocks x columns) */
+  int kind_stage[2];        /* kernel the autotuner chose for those stages (8 = tcgen05 band_u, 5 = band_f, ...) */
 } lfm_info;
 
 /* Table ids for lfm_plan_export_table (bit-exact comparison with the oracle in tests).

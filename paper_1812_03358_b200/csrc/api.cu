@@ -315,6 +315,8 @@ lfm_status lfm_plan_info(lfm_plan p, int cam, lfm_info* out) {
   if (st != LFM_OK) return st;
   if (!out) return fail(LFM_E_INVALID, "out is NULL");
   *out = p->cams[cam].info;
+  out->kind_stage[0] = p->cams[cam].fwd_c2.kind;
+  out->kind_stage[1] = p->cams[cam].adj_c1.kind;
   return LFM_OK;
 }
 

@@ -1,0 +1,225 @@
+// band_u: the identity-s t pass  out[r][c] = scale * sum_k C[r][k] src[k][c]  (C a banded 1D operator from
+// the plan, src row-major with pitch) on the 5th-generation tensor cores (tcgen05, kind::tf32, 3xTF32).
+//
+// C is cut into tiles of 128 rows; the union of a tile's non-zero source rows is covered by blocks of 16
+// consecutive source rows (build_umma in plan.cpp).  Per block the plan stores the 128 x 16 weights as two
+// tf32 images (hi = rn(w), lo = rn(w - hi)) laid out exactly as the tensor core reads them from shared memory
+// (K-major, 64-byte swizzle).  One work item = (row tile, 256 output columns); a CTA runs items persistently:
+//
+//   warp 0      producer: per block one bulk copy of the weight images (16 KB) and 8 TMA tiles of the source
+//               (16 rows x 32 columns each, 128B/32B-atom swizzle = UMMA MN-major layout type 1)
+//   warps 2-3   split: the tensor core truncates fp32 to tf32, so src = hi + lo with hi = the raw tile and
+//               lo = src - trunc(src) (exact), written beside it
+//   warp 1      MMA issuer: per block and 8-row k-step  D += C_lo S_hi + C_hi S_lo + C_hi S_hi  (M128 N256 K8)
+//   warps 4-11  drain + epilogue: the TMEM accumulator adds by truncation (measured,
+//               tools/microbench/tc_probe.cu), so a chain of MMAs drifts low by ~2^-24 per add; every `group`
+//               blocks the MMA warp switches to the other of two TMEM accumulators and these warps add the
+//               finished one into fp32 registers (round to nearest), then write the item's output rows.
+#pragma once
+#include <cuda.h>
+
+#include "tc_sm100.h"
+
+namespace lfm {
+
+struct UArgs {
+  const float* A;         // weight images: block b at A + 4096 b (hi 2048 floats, then lo 2048 floats)
+  const int32_t* blk_off; // per row tile: first block .. (row tiles of the table, n_tiles + 1 entries)
+  const int32_t* blk_k0;  // per block: first source row (plan coordinates)
+  float* out;
+  long long out_pitch;
+  int n_rows, n_cols;     // output rows (table rows) and columns
+  int mt0, n_mt, n_nt;    // row tiles [mt0, mt0 + n_mt), column tiles of 256
+  int k_shift;            // source row of TMA coordinate 0 (the row window start)
+  int group;              // blocks per TMEM accumulator before it is drained
+  float scale;
+  int accumulate;
+};
+
+constexpr int U_STAGES = 4;
+constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
+constexpr int U_THREADS = 384;
+constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 1024 + 256;
+
+__global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map, UArgs a) {
+  using namespace tc;
+  extern __shared__ uint8_t u_smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)u_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + U_STAGES * U_STAGE_BYTES);
+  uint64_t* full = bars;                  // TMA landed (tx count)
+  uint64_t* conv = bars + U_STAGES;       // lo split written (64 arrivals)
+  uint64_t* empty = bars + 2 * U_STAGES;  // MMAs of the stage done (commit)
+  uint64_t* tfull = bars + 3 * U_STAGES;  // accumulator ready (commit), 2
+  uint64_t* tempty = tfull + 2;           // accumulator drained (8 warps), 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < U_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    fence_barrier_init();
+    prefetch_tma_desc(&src_map);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_items = a.n_mt * a.n_nt;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int mt = a.mt0 + it / a.n_nt, nt = it % a.n_nt;
+        const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+        const bool rev = (mt & 1) != 0;
+        for (int j = b0; j < b1; ++j) {
+          const int b = rev ? b0 + b1 - 1 - j : j;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = sm + s * U_STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[s], 32768);
+          bulk_g2s(st, a.A + (size_t)b * 4096, 16384, &full[s]);
+          const int k = __ldg(a.blk_k0 + b) - a.k_shift;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) tma_load_2d(st + 16384 + g * 2048, &src_map, nt * 256 + g * 32, k, &full[s]);
+          if (++s == U_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_tf32(128, 256, 0, 1);
+      int s = 0;
+      uint32_t ph = 0;
+      int buf = 0;
+      uint32_t tph[2] = {0, 0};
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int mt = a.mt0 + it / a.n_nt;
+        const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+        for (int g0 = b0; g0 < b1; g0 += a.group) {
+          mbar_wait(&tempty[buf], tph[buf] ^ 1);
+          tph[buf] ^= 1;
+          tc_fence_after();
+          const uint32_t d = tmem + buf * 256;
+          const int g1 = min(b1, g0 + a.group);
+          for (int j = g0; j < g1; ++j) {
+            mbar_wait(&conv[s], ph);
+            tc_fence_after();
+            const uint32_t st = smem_u32(sm + s * U_STAGE_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint64_t ahi = smem_desc(st + 32 * kk, 16, 512, 4);
+              const uint64_t alo = smem_desc(st + 8192 + 32 * kk, 16, 512, 4);
+              const uint64_t bhi = smem_desc(st + 16384 + 1024 * kk, 2048, 512, 1);
+              const uint64_t blo = smem_desc(st + 32768 + 1024 * kk, 2048, 512, 1);
+              mma_tf32_ss(d, alo, bhi, IDESC, (j != g0 || kk != 0) ? 1u : 0u);
+#ifndef BAND_U_TWO_PRODUCTS
+              mma_tf32_ss(d, ahi, blo, IDESC, 1u);
+#endif
+              mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
+            }
+            tc_commit(&empty[s]);
+            if (++s == U_STAGES) { s = 0; ph ^= 1; }
+          }
+          tc_commit(&tfull[buf]);
+          buf ^= 1;
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // lo split: 16 KB source tile = 1024 float4, 64 threads x 16
+    const int t = threadIdx.x - 64;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int mt = a.mt0 + it / a.n_nt;
+      const int nb = __ldg(a.blk_off + mt + 1) - __ldg(a.blk_off + mt);
+      for (int b = 0; b < nb; ++b) {
+        mbar_wait(&full[s], ph);
+        const float4* src = reinterpret_cast<const float4*>(sm + s * U_STAGE_BYTES + 16384);
+        float4* lo = reinterpret_cast<float4*>(sm + s * U_STAGE_BYTES + 32768);
+#ifndef BAND_U_NO_SPLIT
+#pragma unroll 4
+        for (int i = 0; i < 16; ++i) {
+          const float4 u = src[t + 64 * i];
+          float4 l;
+          l.x = u.x - __uint_as_float(__float_as_uint(u.x) & 0xffffe000u);
+          l.y = u.y - __uint_as_float(__float_as_uint(u.y) & 0xffffe000u);
+          l.z = u.z - __uint_as_float(__float_as_uint(u.z) & 0xffffe000u);
+          l.w = u.w - __uint_as_float(__float_as_uint(u.w) & 0xffffe000u);
+          lo[t + 64 * i] = l;
+        }
+#endif
+        fence_proxy_async_smem();
+        mbar_arrive(&conv[s]);
+        if (++s == U_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (its row quarter), columns half h
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    int buf = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int mt = a.mt0 + it / a.n_nt, nt = it % a.n_nt;
+      const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+      float acc[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+      for (int g0 = b0; g0 < b1; g0 += a.group) {
+        mbar_wait(&tfull[buf], tph[buf]);
+        tph[buf] ^= 1;
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + h * 128;
+#pragma unroll
+        for (int c = 0; c < 128; c += 16) {
+          float v[16];
+          tmem_ld16(base + c, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        buf ^= 1;
+      }
+      const int row = mt * 128 + 32 * q + lane;
+      const int c0 = nt * 256 + h * 128;
+#ifdef BAND_U_NO_EPI_WRITE
+      if (row < 0) {
+#else
+      if (row < a.n_rows) {
+#endif
+        float* o = a.out + (size_t)row * a.out_pitch + c0;
+        if (c0 + 128 <= a.n_cols && ((a.out_pitch & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0)) {
+#pragma unroll
+          for (int c = 0; c < 128; c += 4) {
+            float4 v = make_float4(a.scale * acc[c], a.scale * acc[c + 1], a.scale * acc[c + 2], a.scale * acc[c + 3]);
+            if (a.accumulate) {
+              const float4 p = *reinterpret_cast<const float4*>(o + c);
+              v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+            }
+            *reinterpret_cast<float4*>(o + c) = v;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c0 + c < a.n_cols) o[c] = a.accumulate ? o[c] + a.scale * acc[c] : a.scale * acc[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace lfm

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "band_u.cuh"
 #include "lfm_internal.h"
 #include "lfm_kernels.h"
 
@@ -103,6 +104,14 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_xk, xk.data(), xk.size() * 4, err)) != LFM_OK) return st;
     if ((st = dev_upload(&f.d_xa, xa.data(), xa.size() * 4, err)) != LFM_OK) return st;
     bytes += f.x_off.size() * 4 + xk.size() * 4 + xa.size() * 4;
+  }
+  if (!f.u_off.empty()) {
+    std::vector<int32_t> uk(f.u_k0);
+    uk.push_back(0);
+    if ((st = dev_upload(&f.d_uoff, f.u_off.data(), f.u_off.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_uk0, uk.data(), uk.size() * 4, err)) != LFM_OK) return st;
+    if ((st = dev_upload(&f.d_ua, f.u_a.data(), f.u_a.size() * 4, err)) != LFM_OK) return st;
+    bytes += f.u_off.size() * 4 + uk.size() * 4 + f.u_a.size() * 4;
   }
   if (!f.m8_off.empty()) {
     std::vector<float> mw(f.m8_w64.size() + 8);
@@ -269,6 +278,8 @@ void free_camera(CameraPlan& cp) {
     f->d_foff = nullptr; f->d_frow = nullptr; f->d_fw = nullptr;
     dfree(f->d_xoff); dfree(f->d_xk); dfree(f->d_xa);
     f->d_xoff = nullptr; f->d_xk = nullptr; f->d_xa = nullptr;
+    dfree(f->d_uoff); dfree(f->d_uk0); dfree(f->d_ua);
+    f->d_uoff = nullptr; f->d_uk0 = nullptr; f->d_ua = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
@@ -1609,6 +1620,52 @@ lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const 
   return cuda_check(cudaGetLastError(), "permute_kernel launch", err);
 }
 
+// ---------------------------------------------------------------------------------------------- band_u host side
+// TMA descriptor of a row-major fp32 source (rows x cols, pitch in floats): 32-column x 16-row boxes with the
+// 128-byte / 32-byte-atom swizzle that the tcgen05 MN-major operand (layout type 1) expects.  Rows and columns
+// outside the map read as zero (the row window of a sharded adjoint).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static lfm_status encode_src_map(CUtensorMap* map, const float* base, int cols, int rows, long long pitch,
+                                 std::string& err) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr) != cudaSuccess ||
+        !encode) {
+      cudaGetLastError();
+      err = "band_u: cuTensorMapEncodeTiled unavailable";
+      return LFM_E_CUDA;
+    }
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 3)) {
+    err = "band_u: source rows must be 16-byte aligned";
+    return LFM_E_INVALID;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)pitch * 4};
+  cuuint32_t box[2] = {32, 16}, es[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "band_u: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return LFM_E_CUDA;
+  }
+  return LFM_OK;
+}
+static int g_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1) {
   if (n_out <= 0) return LFM_OK;
@@ -1707,6 +1764,49 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 #undef LFM_BG_CASE
     err = "unsupported band_g tile";
     return LFM_E_INVALID;
+  }
+  if (op.kind == 8) {
+    // tcgen05 t pass (band_u.cuh): one table, one unit-scale term per output, normal output, 16-byte rows
+    if (!op.ft->d_uoff || op.tout || n_out != 1) { err = "band_u: needs the tcgen05 form, one output, normal output"; return LFM_E_INVALID; }
+    const Term& term = op.terms[op.offs[b0]];
+    const float* base = src + term.src_off + (long long)a.win_r0 * a.src_pitch;
+    const int win_rows = a.win_r1 - a.win_r0;
+    if (win_rows <= 0) {  // empty source window: the output is zero (or unchanged)
+      if (!accumulate)
+        for (int r = r0; r < r1; ++r)
+          if (cudaMemsetAsync(out + (long long)b0 * a.out_stride + (long long)r * a.out_pitch, 0, (size_t)op.n_os * 4, s) != cudaSuccess)
+            return cuda_check(cudaGetLastError(), "band_u memset", err);
+      return LFM_OK;
+    }
+    CUtensorMap map;
+    lfm_status st = encode_src_map(&map, base, op.n_is, win_rows, a.src_pitch, err);
+    if (st != LFM_OK) return st;
+    static int smem_set = 0;
+    if (!smem_set) {
+      if (cudaFuncSetAttribute(band_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
+        return cuda_check(cudaGetLastError(), "band_u smem attribute", err);
+      smem_set = 1;
+    }
+    UArgs u;
+    const int n_mt = (op.n_ot + 127) / 128;
+    u.A = op.ft->d_ua;
+    u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
+    u.blk_k0 = op.ft->d_uk0;
+    u.out = out + (long long)b0 * a.out_stride;
+    u.out_pitch = a.out_pitch;
+    u.n_rows = op.n_ot;
+    u.n_cols = op.n_os;
+    u.mt0 = r0 / 128;
+    u.n_mt = (r1 + 127) / 128 - u.mt0;
+    u.n_nt = (op.n_os + 255) / 256;
+    u.k_shift = a.win_r0;
+    u.group = op.stages > 0 ? op.stages : 4;
+    u.scale = op.out_scale * term.scale;
+    u.accumulate = accumulate;
+    const int grid_u = std::min(u.n_mt * u.n_nt, g_num_sms());
+    band_u_kernel<<<grid_u, U_THREADS, U_SMEM, s>>>(map, u);
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "band_u_kernel launch", err);
   }
   if (op.kind == 7) {
     if (!op.ft->d_xoff || op.tout) { err = "band_x: needs the tensor-core form and normal output"; return LFM_E_INVALID; }
@@ -2311,6 +2411,32 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         if (tot < best) { best = tot; bts = op.ts; btt = 16; bnt = nt; bnb = 1; bst = 0; bkind = 7; bstages = nj; bmgrp = 4; }
       }
       op.kind = 0;
+      // band_u: tcgen05 (one output, one term, normal output, 16-byte source rows); stages = drain group
+      for (int grp : {4}) {
+        const long long sp = op.src_pitch ? op.src_pitch : op.n_is;
+        if (st != LFM_OK || op.ft->u_off.empty() || op.tout || op.n_out != 1 || op.terms.size() != 1 ||
+            (sp & 3) || (op.terms[0].src_off & 3) || std::getenv("LFM_NO_TC"))
+          break;
+        op.kind = 8; op.ts = 256; op.tt = 128; op.nt = U_THREADS; op.nb = 1; op.stage = 0; op.stages = grp; op.mgrp = 4;
+        fill_sep_geometry(op);
+        free_sep_dev(op);
+        size_t bytes = 0;
+        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
+        float ms = 0, tot = 0;
+        bool ok = true;
+        for (int rep = 0; rep < 3 && ok; ++rep) {
+          cudaEventRecord(e0, 0);
+          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
+          cudaEventRecord(e1, 0);
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (rep > 0) tot += ms;
+        }
+        if (!ok || cudaGetLastError() != cudaSuccess) continue;
+        if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_u group %d: %.3f ms\n", names[q], grp, tot / 2);
+        if (tot < best) { best = tot; bts = 256; btt = 128; bnt = U_THREADS; bnb = 1; bst = 0; bkind = 8; bstages = grp; bmgrp = 4; }
+      }
+      op.kind = 0;
       // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)
       bool unit = true;
       for (const Term& t : op.terms) unit &= t.scale == 1.f && (t.src_off % 4) == 0;
@@ -2380,7 +2506,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d grp %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : op.kind == 7 ? "band_x" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
+                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : op.kind == 7 ? "band_x" : op.kind == 8 ? "band_u" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
         std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb,

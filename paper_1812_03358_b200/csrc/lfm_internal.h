@@ -69,6 +69,13 @@ struct BandFamily {
   int32_t* d_xoff = nullptr;
   int32_t* d_xk = nullptr;
   float* d_xa = nullptr;
+  // tcgen05 form (band_u): per tile of 128 rows the union of the rows' supports cut into blocks of 16 source
+  // cells; per block two 128 x 16 tf32 weight images (hi, lo) in the shared-memory layout the MMA reads
+  std::vector<int32_t> u_off, u_k0;        // u_off[table * n_tiles + tile] .. +1 into blocks; u_k0[block]
+  std::vector<float> u_a;                  // 4096 floats per block
+  int32_t* d_uoff = nullptr;
+  int32_t* d_uk0 = nullptr;
+  float* d_ua = nullptr;
   // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
   std::vector<int32_t> m8_off, m8_seg;
   std::vector<double> m8_w64;
@@ -118,6 +125,7 @@ struct SepOp {
                                    // 4: band_s_kernel (MSEG segments, source rows streamed through smem)
                                    // 5: band_f_kernel (flat MSEG entry lists, L2 gather, deep unroll)
                                    // 7: band_x_kernel (tensor cores: mma.sync m16n8k8 3xTF32 over 16-row blocks)
+                                   // 8: band_u_kernel (tcgen05 kind::tf32 3xTF32, 128-row tiles, TMA, TMEM)
   long long src_pitch = 0;         // floats between source rows (0: n_is)
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)

@@ -435,6 +435,61 @@ static void build_mma(BandFamily& f) {
   f.x_off[(size_t)f.n_tables * nt] = (int)f.x_k.size();
 }
 
+// tcgen05 form of a one-table family (band_u, band_u.cuh): tiles of 128 rows; the union of the rows'
+// non-zero source cells covered by the fewest blocks of 16 consecutive cells (greedy); per block the fp32
+// weights (one rounding from fp64) split as w = hi + lo + O(2^-22 w), hi = rn_tf32(w), lo = rn_tf32(w - hi),
+// each a 128 x 16 image in the tensor core's K-major 64-byte-swizzled shared-memory layout: element (m, k) at
+// byte m*64 + k*4 with bits [4,6) XOR bits [7,9).
+static void build_umma(BandFamily& f) {
+  const int nt = (f.n_rows + 127) / 128;
+  f.u_off.assign((size_t)f.n_tables * nt + 1, 0);
+  f.u_k0.clear();
+  f.u_a.clear();
+  std::vector<char> any;
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int t = 0; t < nt; ++t) {
+      f.u_off[(size_t)m * nt + t] = (int)f.u_k0.size();
+      const int r0 = 128 * t, r1 = std::min(f.n_rows, r0 + 128);
+      int lo = 1 << 30, hi = -1;
+      for (int r = r0; r < r1; ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        if (!f.len[idx]) continue;
+        lo = std::min(lo, (int)f.start[idx]);
+        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
+      }
+      if (hi < 0) continue;
+      any.assign(hi - lo, 0);
+      for (int r = r0; r < r1; ++r) {
+        size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e)
+          if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e - lo] = 1;
+      }
+      std::vector<int> starts;
+      for (int p = 0; p < hi - lo; ++p)
+        if (any[p] && (starts.empty() || p >= starts.back() + 16)) starts.push_back(p);
+      for (int a0 : starts) {
+        const int k0 = lo + a0;
+        f.u_k0.push_back(k0);
+        const size_t base = f.u_a.size();
+        f.u_a.resize(base + 4096, 0.f);
+        for (int r = r0; r < r1; ++r) {
+          size_t idx = (size_t)m * f.n_rows + r;
+          for (int k = 0; k < 16; ++k) {
+            const int e = k0 + k - f.start[idx];
+            if (e < 0 || e >= f.len[idx]) continue;
+            const float w = (float)f.w64[idx * f.taps + e];
+            const float wh = tf32_round(w), wl = tf32_round(w - wh);
+            uint32_t off = (uint32_t)((r - r0) * 64 + k * 4);
+            off ^= ((off >> 7) & 3u) << 4;
+            f.u_a[base + off / 4] = wh;
+            f.u_a[base + 2048 + off / 4] = wl;
+          }
+        }
+      }
+    }
+  f.u_off[(size_t)f.n_tables * nt] = (int)f.u_k0.size();
+}
+
 // MSEG form with groups of 8 rows (segments split at zero runs >= 2 source cells, weights 8 per cell).
 static void build_mseg8(BandFamily& f) {
   const int G = 8;
@@ -1286,10 +1341,12 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   make_rows_by_slice(cp.ca1n, cp.ca[1]);
   build_mseg8(cp.ca1n);
   build_mma(cp.ca1n);
+  build_umma(cp.ca1n);
   cp.cf1n.want_mseg = 1;
   make_cols_by_slice(cp.cf1n, cp.cf[1]);
   build_mseg8(cp.cf1n);
   build_mma(cp.cf1n);
+  build_umma(cp.cf1n);
   if (std::getenv("LFM_DEBUG")) {
     const BandFamily* fs[] = {&cp.ca1n, &cp.cf1n, &cp.ca[1], &cp.cf[1], &cp.ca[0], &cp.cf[0]};
     const char* nm[] = {"ca1 rows-by-slice", "cf1 cols-by-slice", "ca1", "cf1", "ca0", "cf0"};
@@ -1437,7 +1494,8 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
           bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
                     (kind < 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty())) &&
                     (kind != 4 || (ts == 128 && !op.tout)) && (kind != 5 || !op.ft->f_off.empty()) &&
-                    (kind != 7 || (!op.ft->x_off.empty() && !op.tout));
+                    (kind != 7 || (!op.ft->x_off.empty() && !op.tout)) &&
+                    (kind != 8 || (!op.ft->u_off.empty() && !op.tout && op.n_out == 1 && op.terms.size() == 1));
           for (const Term& t : op.terms) ok &= (kind != 4 && kind != 7) || t.scale == 1.f;
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
           if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
@@ -1465,6 +1523,8 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     for (size_t i = 0; i < cp.ca1n.cnt.size(); ++i) nnz_a += cp.ca1n.cnt[i];
     info.fma_stage[0] = nnz_f * ndet[0];
     info.fma_stage[1] = nnz_a * ndet[0];
+    info.mma_stage[0] = 3.0 * 128 * 16 * (double)cp.cf1n.u_k0.size() * ndet[0];
+    info.mma_stage[1] = 3.0 * 128 * 16 * (double)cp.ca1n.u_k0.size() * ndet[0];
   }
   info.bytes_alg[0] = 4.0 * info.n_vox + rot_bytes + (plen ? 8.0 * Kv * nfield : 0.0) + 4.0 * npix;
   info.bytes_alg[1] = 4.0 * info.n_vox + rot_bytes + 4.0 * npix;

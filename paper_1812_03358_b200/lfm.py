@@ -60,7 +60,8 @@ class Info(ctypes.Structure):
                 ("rot_passes", ctypes.c_int), ("rot_perm", ctypes.c_int * 9), ("taps_s1", ctypes.c_int), ("taps_s3", ctypes.c_int),
                 ("taps_c", ctypes.c_int), ("ws_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
                 ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
-                ("fma_stage", ctypes.c_double * 2)]
+                ("fma_stage", ctypes.c_double * 2), ("mma_stage", ctypes.c_double * 2),
+                ("kind_stage", ctypes.c_int * 2)]
 
     def as_dict(self):
         out = {}

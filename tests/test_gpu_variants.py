@@ -47,7 +47,7 @@ def test_rows_entry_points(name, path):
 
 # band_t: ts,tt,nt,nb,stage,kind=1,stages ; band_g (2-segment G4) kind=2 / band_m (MSEG) kind=3 with
 # unroll and MSEG group rows ; band_s (streamed MSEG) kind=4 with stages, 4, chunk rows ; band_f (flat
-# MSEG entries) kind=5 with unroll ; band_x (tensor cores, 3xTF32) kind=7, stages = NJ n8 tiles per warp, ts = warps x 8 NJ, tt = 16 ; sep: MODE variants (stage 1 = staged U, 0 = U from L2)
+# MSEG entries) kind=5 with unroll ; band_u (tcgen05 3xTF32, 128-row tiles) kind=8, stages = drain group ; band_x (tensor cores, 3xTF32) kind=7, stages = NJ n8 tiles per warp, ts = warps x 8 NJ, tt = 16 ; sep: MODE variants (stage 1 = staged U, 0 = U from L2)
 VARIANTS = {
     "band_m_128x16_u4": "128,16,128,1,0,3,4",
     "band_m_128x32_u8": "128,32,256,1,0,3,8",
@@ -62,6 +62,8 @@ VARIANTS = {
     "band_x_nt128_nj8": "256,16,128,1,0,7,8",
     "band_x_nt128_nj4": "128,16,128,1,0,7,4",
     "band_x_nt256_nj4": "256,16,256,1,0,7,4",
+    "band_u_g4": "256,128,384,1,0,8,4",
+    "band_u_g1": "256,128,384,1,0,8,1",
     "band_s_ng8_k64": "128,32,288,1,0,4,3,4,64",
     "band_s_ng8_k16": "128,32,288,1,0,4,6,4,16",
     "band_g_128x32_u8": "128,32,256,1,0,2,8",
