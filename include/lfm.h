@@ -15,6 +15,8 @@
  *  - Layouts: a volume is x fastest, then y, then z (nx*ny*nz floats, eqn,voxel P:1036-1044);
  *    a light-field plane is s fastest then t; multi-view fields are view-major with
  *    view index k = k_t*K_s + k_s; a detector image is n_t rows of n_s pixels.
+ *  - Data buffers must be 16-byte aligned (the tensor-core t passes move rows by TMA);
+ *    cudaMalloc and PyTorch allocations are.  A misaligned buffer gives LFM_E_INVALID.
  *  - Outputs are overwritten unless an `accumulate` argument is non-zero.
  *  - Errors: every call returns an lfm_status and never throws; lfm_last_error() gives a
  *    thread-local message naming the failing camera, axis or block.

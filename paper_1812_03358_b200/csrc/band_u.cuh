@@ -39,13 +39,16 @@ struct UArgs {
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
 constexpr int U_THREADS = 384;
-constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 1024 + 256;
+constexpr int U_STAGE_OUT = 4096;  // per epilogue warp: 32 rows x 32 columns fp32, 128-byte swizzle (TMA store)
+constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 8 * U_STAGE_OUT + 1024 + 256;
 
-__global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map, UArgs a) {
+__global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
+                                                              const __grid_constant__ CUtensorMap out_map, UArgs a) {
   using namespace tc;
   extern __shared__ uint8_t u_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)u_smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + U_STAGES * U_STAGE_BYTES);
+  uint8_t* sout = sm + U_STAGES * U_STAGE_BYTES;  // epilogue staging, 8 x 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * U_STAGE_OUT);
   uint64_t* full = bars;                  // TMA landed (tx count)
   uint64_t* conv = bars + U_STAGES;       // lo split written (64 arrivals)
   uint64_t* empty = bars + 2 * U_STAGES;  // MMAs of the stage done (commit)
@@ -65,6 +68,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     }
     fence_barrier_init();
     prefetch_tma_desc(&src_map);
+    prefetch_tma_desc(&out_map);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -191,31 +195,32 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         if (lane == 0) mbar_arrive(&tempty[buf]);
         buf ^= 1;
       }
-      const int row = mt * 128 + 32 * q + lane;
-      const int c0 = nt * 256 + h * 128;
-#ifdef BAND_U_NO_EPI_WRITE
-      if (row < 0) {
-#else
-      if (row < a.n_rows) {
-#endif
-        float* o = a.out + (size_t)row * a.out_pitch + c0;
-        if (c0 + 128 <= a.n_cols && ((a.out_pitch & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0)) {
+      // output: per 32-column chunk the warp's 32 x 32 block goes through its swizzled staging buffer and one
+      // TMA store (or TMA add when accumulating); rows / columns outside the output are clipped by the TMA unit
+      uint8_t* stg = sout + (warp - 4) * U_STAGE_OUT;
+      const int r0 = mt * 128 + 32 * q, c0 = nt * 256 + h * 128;
 #pragma unroll
-          for (int c = 0; c < 128; c += 4) {
-            float4 v = make_float4(a.scale * acc[c], a.scale * acc[c + 1], a.scale * acc[c + 2], a.scale * acc[c + 3]);
-            if (a.accumulate) {
-              const float4 p = *reinterpret_cast<const float4*>(o + c);
-              v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
-            }
-            *reinterpret_cast<float4*>(o + c) = v;
-          }
-        } else {
+      for (int c = 0; c < 128; c += 32) {
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c0 + c < a.n_cols) o[c] = a.accumulate ? o[c] + a.scale * acc[c] : a.scale * acc[c];
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = make_float4(a.scale * acc[c + 4 * j], a.scale * acc[c + 4 * j + 1], a.scale * acc[c + 4 * j + 2],
+                                       a.scale * acc[c + 4 * j + 3]);
+          *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+#ifndef BAND_U_NO_EPI_WRITE
+        if (lane == 0) {
+          if (a.accumulate) tma_add_2d(&out_map, c0 + c, r0, stg);
+          else tma_store_2d(&out_map, c0 + c, r0, stg);
+          bulk_commit();
+        }
+#endif
       }
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();

@@ -1621,14 +1621,15 @@ lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const 
 }
 
 // ---------------------------------------------------------------------------------------------- band_u host side
-// TMA descriptor of a row-major fp32 source (rows x cols, pitch in floats): 32-column x 16-row boxes with the
-// 128-byte / 32-byte-atom swizzle that the tcgen05 MN-major operand (layout type 1) expects.  Rows and columns
-// outside the map read as zero (the row window of a sharded adjoint).
+// TMA descriptor of a row-major fp32 matrix (rows x cols, pitch in floats).  band_u reads its source in
+// 32-column x 16-row boxes with the 128-byte / 32-byte-atom swizzle that the tcgen05 MN-major operand (layout
+// type 1) expects (rows and columns outside the map read as zero: the row window of a sharded adjoint), and
+// writes its output in 32 x 32 boxes with the 128-byte swizzle (writes outside the map are clipped).
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static lfm_status encode_src_map(CUtensorMap* map, const float* base, int cols, int rows, long long pitch,
-                                 std::string& err) {
+static lfm_status encode_map(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
+                             int box_r, CUtensorMapSwizzle swz, std::string& err) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -1640,15 +1641,15 @@ static lfm_status encode_src_map(CUtensorMap* map, const float* base, int cols, 
     }
   }
   if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 3)) {
-    err = "band_u: source rows must be 16-byte aligned";
+    err = "band_u: buffers and their rows must be 16-byte aligned";
     return LFM_E_INVALID;
   }
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t gstr[1] = {(cuuint64_t)pitch * 4};
-  cuuint32_t box[2] = {32, 16}, es[2] = {1, 1};
+  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r}, es[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, es,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     err = "band_u: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return LFM_E_CUDA;
@@ -1778,8 +1779,11 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
             return cuda_check(cudaGetLastError(), "band_u memset", err);
       return LFM_OK;
     }
-    CUtensorMap map;
-    lfm_status st = encode_src_map(&map, base, op.n_is, win_rows, a.src_pitch, err);
+    CUtensorMap map, omap;
+    lfm_status st = encode_map(&map, base, op.n_is, win_rows, a.src_pitch, 32, 16, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, err);
+    if (st != LFM_OK) return st;
+    st = encode_map(&omap, out + (long long)b0 * a.out_stride, op.n_os, op.n_ot, a.out_pitch, 32, 32,
+                    CU_TENSOR_MAP_SWIZZLE_128B, err);
     if (st != LFM_OK) return st;
     static int smem_set = 0;
     if (!smem_set) {
@@ -1804,7 +1808,7 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.scale = op.out_scale * term.scale;
     u.accumulate = accumulate;
     const int grid_u = std::min(u.n_mt * u.n_nt, g_num_sms());
-    band_u_kernel<<<grid_u, U_THREADS, U_SMEM, s>>>(map, u);
+    band_u_kernel<<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
     ++g_launches;
     return cuda_check(cudaGetLastError(), "band_u_kernel launch", err);
   }

@@ -124,12 +124,21 @@ int main(int argc, char** argv) {
                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) { printf("encode failed %d\n", (int)cr); return 1; }
+    CUtensorMap omap;
+    {
+      cuuint64_t od[2] = {(cuuint64_t)p.N, (cuuint64_t)p.R};
+      cuuint64_t os[1] = {(cuuint64_t)p.N * 4};
+      cuuint32_t ob[2] = {32, 32};
+      cr = encode(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dout, od, os, ob, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) { printf("encode out failed %d\n", (int)cr); return 1; }
+    }
     UArgs a;
     a.A = dA; a.blk_off = doff; a.blk_k0 = dk0; a.out = dout; a.out_pitch = p.N; a.n_rows = p.R; a.n_cols = p.N;
     a.mt0 = 0; a.n_mt = n_mt; a.n_nt = (p.N + 255) / 256; a.k_shift = 0; a.group = cs.group; a.scale = 1.f;
     a.accumulate = 0;
     const int grid = std::min(nsm, n_mt * a.n_nt);
-    band_u_kernel<<<grid, U_THREADS, U_SMEM>>>(map, a);
+    band_u_kernel<<<grid, U_THREADS, U_SMEM>>>(map, omap, a);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
     cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost);
@@ -151,7 +160,7 @@ int main(int argc, char** argv) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      for (int i = 0; i < cs.reps; ++i) band_u_kernel<<<grid, U_THREADS, U_SMEM>>>(map, a);
+      for (int i = 0; i < cs.reps; ++i) band_u_kernel<<<grid, U_THREADS, U_SMEM>>>(map, omap, a);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
