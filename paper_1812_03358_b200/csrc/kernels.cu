@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "band_u.cuh"
+#include "spass.cuh"
 #include "lfm_internal.h"
 #include "lfm_kernels.h"
 
@@ -236,8 +237,86 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
       bytes += sp.mlo[d].size() * 4 + w32.size() * 4;
     }
   }
+  // adjoint direct s pass: per (slice, 16-column tile) of ca[0] the union of the rows' non-zero source cells
+  {
+    const BandFamily& f = cp.ca[0];
+    const int nt = (f.n_rows + SPA_VX - 1) / SPA_VX;
+    cp.spa_fp.assign((size_t)f.n_tables * nt * 2, 0);
+    cp.spa_wmax = 1;
+    const size_t per = (size_t)f.ell * f.n_rows;
+    for (int m = 0; m < f.n_tables; ++m)
+      for (int t = 0; t < nt; ++t) {
+        int lo = 1 << 30, hi = -1;
+        for (int r = t * SPA_VX; r < std::min(f.n_rows, t * SPA_VX + SPA_VX); ++r)
+          for (int e = 0; e < f.cnt[(size_t)m * f.n_rows + r]; ++e) {
+            const int j = f.eidx[m * per + (size_t)e * f.n_rows + r];
+            lo = std::min(lo, j);
+            hi = std::max(hi, j + 1);
+          }
+        if (hi < 0) lo = hi = 0;
+        cp.spa_fp[2 * ((size_t)m * nt + t)] = lo;
+        cp.spa_fp[2 * ((size_t)m * nt + t) + 1] = hi - lo;
+        cp.spa_wmax = std::max(cp.spa_wmax, hi - lo);
+      }
+    if ((st = dev_upload(&cp.d_spa_fp, cp.spa_fp.data(), cp.spa_fp.size() * 4, err)) != LFM_OK) return st;
+    bytes += cp.spa_fp.size() * 4;
+  }
   cp.info.table_bytes = bytes;
   return LFM_OK;
+}
+
+lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err) {
+  const BandFamily& f = cp.cf[0];
+  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = f.n_rows;
+  const int pitch = (f.n_rows + 3) / 4 * 4;
+  dim3 grid((nd + 255) / 256, nz, (ny + SPF_VTG - 1) / SPF_VTG);
+  const size_t smem = (size_t)SPF_VTG * nx * 4;
+  if (smem > 48 * 1024) { err = "spass_fwd: volume rows too long"; return LFM_E_INVALID; }
+  spass_fwd_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x, U, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell, pitch);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "spass_fwd_kernel launch", err);
+}
+
+lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err) {
+  const BandFamily& f = cp.ca[0];
+  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = f.n_src;
+  const int pitch = (f.n_rows + 3) / 4 * 4;
+  const int tmax = f.ell;
+  const size_t smem = ((size_t)SPA_VT * (SPA_CH + 1) + SPA_VT * (SPA_VX + 1) + 2 * SPA_VX * tmax) * 4;
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    if (smem > 200 * 1024 ||
+        cudaFuncSetAttribute(spass_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      err = "spass_adj: tap table exceeds shared memory";
+      return LFM_E_INVALID;
+    }
+    smem_set = smem;
+  }
+  if (std::getenv("LFM_SPA_ROW") == nullptr || std::getenv("LFM_SPA_ROW")[0] != '0') {
+    const size_t rsm = (size_t)8 * (nd + nd / 16 + 4) * 4;
+    static size_t rsm_set = 48 * 1024;
+    if (rsm > rsm_set) {
+      if (rsm > 200 * 1024 ||
+          cudaFuncSetAttribute(spass_adj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) != cudaSuccess) {
+        cudaGetLastError();
+        err = "spass_adj: detector rows exceed shared memory";
+        return LFM_E_INVALID;
+      }
+      rsm_set = rsm;
+    }
+    dim3 g2((ny + 7) / 8, nz);
+    spass_adj_row_kernel<<<g2, 256, rsm, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
+                                                                pitch, cp.adj_a2.out_scale, accumulate);
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "spass_adj_row_kernel launch", err);
+  }
+  dim3 grid((nx + SPA_VX - 1) / SPA_VX, nz);
+  spass_adj_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w,
+                                                             reinterpret_cast<const int2*>(cp.d_spa_fp), nx, ny, nz, nd,
+                                                             f.ell, pitch, tmax, cp.adj_a2.out_scale, accumulate);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "spass_adj_kernel launch", err);
 }
 
 static void dfree(void* p) {
@@ -266,6 +345,8 @@ lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
 }
 
 void free_camera(CameraPlan& cp) {
+  dfree(cp.d_spa_fp);
+  cp.d_spa_fp = nullptr;
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
   for (int ax = 0; ax < 2; ++ax)
     for (BandFamily* f : {&cp.s1f[ax], &cp.s1a[ax], &cp.s3f[ax], &cp.s3a[ax], &cp.cf[ax], &cp.ca[ax]})
@@ -2556,31 +2637,72 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   dfree(out);
   if (op_best[9] > 0 && op_best[7] > 0 && t_x >= 0) cp.fwd_t = (t_x + op_best[9]) < op_best[7];
   if (op_best[10] > 0 && op_best[6] > 0 && t_z >= 0) cp.adj_t = (t_z + op_best[10]) < op_best[6];
+  // transposed output exists only in band_m / band_f
+  cp.fwd_t = cp.fwd_t && cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5);
+  cp.adj_t = cp.adj_t && cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5);
+  float fwd_s = cp.fwd_t ? t_x + op_best[9] : op_best[7];
+  // direct s passes (spass.cuh, mode 2): timed against the choice above, kept when faster
+  if (st == LFM_OK && cached_decision[0] < 0) {
+    float* sb = nullptr;
+    float* ob = nullptr;
+    const size_t big = std::max((size_t)cp.info.ny * cp.info.nz * cp.adj_c1.n_os, (size_t)cp.info.n_vox) * 4;
+    if (cudaMalloc(&sb, big) == cudaSuccess && cudaMalloc(&ob, big) == cudaSuccess) {
+      cudaMemset(sb, 0, big);
+      cudaEvent_t f0, f1;
+      cudaEventCreate(&f0);
+      cudaEventCreate(&f1);
+      auto time2 = [&](auto&& fn) {
+        float ms = 0, tot = 0;
+        bool ok = true;
+        for (int rep = 0; rep < 3; ++rep) {
+          cudaEventRecord(f0, 0);
+          ok &= fn() == LFM_OK;
+          cudaEventRecord(f1, 0);
+          cudaEventSynchronize(f1);
+          cudaEventElapsedTime(&ms, f0, f1);
+          if (rep > 0) tot += ms;
+        }
+        return ok ? tot : -1.f;
+      };
+      std::string terr;
+      const float t_sf = time2([&] { return k_spass_fwd(cp, sb, ob, nullptr, terr); });
+      const float t_sa = time2([&] { return k_spass_adj(cp, sb, ob, 0, nullptr, terr); });
+      const float adj_s = cp.adj_t ? t_z + op_best[10] : op_best[6];
+      if (dbg)
+        std::fprintf(stderr, "[lfm] direct s passes: fwd %.3f ms (vs %.3f), adj %.3f ms (vs %.3f) x2\n", t_sf, fwd_s, t_sa, adj_s);
+      if (t_sf > 0 && (fwd_s <= 0 || t_sf < fwd_s)) { cp.fwd_t = 2; fwd_s = t_sf; }
+      if (t_sa > 0 && (adj_s <= 0 || t_sa < adj_s)) cp.adj_t = 2;
+      cudaEventDestroy(f0);
+      cudaEventDestroy(f1);
+    }
+    cudaGetLastError();
+    dfree(sb);
+    dfree(ob);
+  }
+  // forward order: fused (fwd_c) or two passes (s pass + fwd_c2), whichever timed faster
+  if (cached_decision[0] < 0 && op_best[4] > 0 && fwd_s > 0 && op_best[8] > 0) cp.fwd_split = (fwd_s + op_best[8]) < op_best[4];
   if (cached_decision[0] >= 0) {
     cp.fwd_split = cached_decision[0];
     cp.fwd_t = cached_decision[1];
     cp.adj_t = cached_decision[2];
   } else if (tfile) {
     if (FILE* f = std::fopen(tfile, "a")) {
-      const float fwd_s0 = cp.fwd_t ? t_x + op_best[9] : op_best[7];
-      const int split = (op_best[4] > 0 && fwd_s0 > 0 && op_best[8] > 0) ? (fwd_s0 + op_best[8]) < op_best[4] : cp.fwd_split;
-      std::fprintf(f, "%s decide %d %d %d\n", key.c_str(), split, cp.fwd_t, cp.adj_t);
+      std::fprintf(f, "%s decide %d %d %d\n", key.c_str(), cp.fwd_split, cp.fwd_t, cp.adj_t);
       std::fclose(f);
     }
   }
-  if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] == '1';
-  if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] == '1';
-  // transposed output exists only in band_m / band_f
-  cp.fwd_t = cp.fwd_t && cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5);
-  cp.adj_t = cp.adj_t && cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5);
-  const float fwd_s = cp.fwd_t ? t_x + op_best[9] : op_best[7];
-  // forward order: fused (fwd_c) or two passes (s pass + fwd_c2), whichever timed faster
-  if (cached_decision[0] < 0 && op_best[4] > 0 && fwd_s > 0 && op_best[8] > 0) cp.fwd_split = (fwd_s + op_best[8]) < op_best[4];
+  // overrides: LFM_FWD_T / LFM_ADJ_T = 0 direct sep, 1 transpose + band_m/band_f, 2 direct s-pass kernels
+  if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] - '0';
+  if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] - '0';
+  if (cp.fwd_t == 1 && !(cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5))) cp.fwd_t = 0;
+  if (cp.adj_t == 1 && !(cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5))) cp.adj_t = 0;
+  if (cp.fwd_t < 0 || cp.fwd_t > 2) cp.fwd_t = 0;
+  if (cp.adj_t < 0 || cp.adj_t > 2) cp.adj_t = 0;
   if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
+  static const char* smode[] = {"direct sep", "transposed", "spass"};
   if (dbg)
     std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",
-                 cp.fwd_split ? "two passes" : "fused", cp.fwd_t ? "transposed" : "direct", t_x, t_z,
-                 cp.adj_t ? "transposed" : "direct");
+                 cp.fwd_split ? "two passes" : "fused", smode[cp.fwd_t], t_x, t_z, smode[cp.adj_t]);
   return st;
 }
 }  // namespace lfm

@@ -172,8 +172,8 @@ struct CameraPlan {
   SepOp fwd_c1, fwd_c2;                   // collapsed forward in two passes: s (U_n for all n), then t
   int fwd_split = 0;                      // 1: forward uses fwd_c1 + fwd_c2 (chosen by the autotuner)
   SepOp fwd_p1, adj_a2;                   // transposed s passes (band_m with transposed output)
-  int fwd_t = 0;                          // 1: split forward's s pass = transpose x + fwd_p1 (autotuner)
-  int adj_t = 0;                          // 1: adjoint's s pass = transpose Z + adj_a2 (autotuner)
+  int fwd_t = 0;                          // 1: split forward's s pass = transpose x + fwd_p1, 2: spass_fwd (autotuner)
+  int adj_t = 0;                          // 1: adjoint's s pass = transpose Z + adj_a2, 2: spass_adj (autotuner)
   BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint/forward
   BandFamily ca1n, cf1n;                  // slice-interleaved collapsed t families (rows (vt,n) / sources (vt,n))
   // lf_transport ops (output b = n*K + k for slice-indexed families)
@@ -183,6 +183,10 @@ struct CameraPlan {
   int perm_axis[2][3], perm_sign[2][3];   // [fwd: P, adj: P^T] source axis and sign per output axis
   std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
+  // direct s passes (spass.cuh): adjoint footprints {first s, width} per (slice, 16-column tile) of ca[0]
+  std::vector<int32_t> spa_fp;
+  int spa_wmax = 0;
+  int32_t* d_spa_fp = nullptr;
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
 };
 
@@ -215,6 +219,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
                       int win_r1 = -1);
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
+lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
+lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);
 }  // namespace lfm
