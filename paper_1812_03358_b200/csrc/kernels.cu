@@ -237,30 +237,6 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
       bytes += sp.mlo[d].size() * 4 + w32.size() * 4;
     }
   }
-  // adjoint direct s pass: per (slice, 16-column tile) of ca[0] the union of the rows' non-zero source cells
-  {
-    const BandFamily& f = cp.ca[0];
-    const int nt = (f.n_rows + SPA_VX - 1) / SPA_VX;
-    cp.spa_fp.assign((size_t)f.n_tables * nt * 2, 0);
-    cp.spa_wmax = 1;
-    const size_t per = (size_t)f.ell * f.n_rows;
-    for (int m = 0; m < f.n_tables; ++m)
-      for (int t = 0; t < nt; ++t) {
-        int lo = 1 << 30, hi = -1;
-        for (int r = t * SPA_VX; r < std::min(f.n_rows, t * SPA_VX + SPA_VX); ++r)
-          for (int e = 0; e < f.cnt[(size_t)m * f.n_rows + r]; ++e) {
-            const int j = f.eidx[m * per + (size_t)e * f.n_rows + r];
-            lo = std::min(lo, j);
-            hi = std::max(hi, j + 1);
-          }
-        if (hi < 0) lo = hi = 0;
-        cp.spa_fp[2 * ((size_t)m * nt + t)] = lo;
-        cp.spa_fp[2 * ((size_t)m * nt + t) + 1] = hi - lo;
-        cp.spa_wmax = std::max(cp.spa_wmax, hi - lo);
-      }
-    if ((st = dev_upload(&cp.d_spa_fp, cp.spa_fp.data(), cp.spa_fp.size() * 4, err)) != LFM_OK) return st;
-    bytes += cp.spa_fp.size() * 4;
-  }
   cp.info.table_bytes = bytes;
   return LFM_OK;
 }
@@ -281,40 +257,27 @@ lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   const BandFamily& f = cp.ca[0];
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = f.n_src;
   const int pitch = (f.n_rows + 3) / 4 * 4;
-  const int tmax = f.ell;
-  const size_t smem = ((size_t)SPA_VT * (SPA_CH + 1) + SPA_VT * (SPA_VX + 1) + 2 * SPA_VX * tmax) * 4;
-  static size_t smem_set = 48 * 1024;
-  if (smem > smem_set) {
-    if (smem > 200 * 1024 ||
-        cudaFuncSetAttribute(spass_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+  const int vta = cp.spa_vta == 4 ? 4 : 8;
+  const size_t smem = (size_t)vta * (nd + (nd >> 4) + 4) * 4;
+  static size_t smem_set[2] = {48 * 1024, 48 * 1024};
+  size_t& ss = smem_set[vta == 8];
+  if (smem > ss) {
+    cudaError_t e = vta == 8 ? cudaFuncSetAttribute(spass_adj_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(spass_adj_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 200 * 1024 || e != cudaSuccess) {
       cudaGetLastError();
-      err = "spass_adj: tap table exceeds shared memory";
+      err = "spass_adj: detector rows exceed shared memory";
       return LFM_E_INVALID;
     }
-    smem_set = smem;
+    ss = smem;
   }
-  if (std::getenv("LFM_SPA_ROW") == nullptr || std::getenv("LFM_SPA_ROW")[0] != '0') {
-    const size_t rsm = (size_t)8 * (nd + nd / 16 + 4) * 4;
-    static size_t rsm_set = 48 * 1024;
-    if (rsm > rsm_set) {
-      if (rsm > 200 * 1024 ||
-          cudaFuncSetAttribute(spass_adj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) != cudaSuccess) {
-        cudaGetLastError();
-        err = "spass_adj: detector rows exceed shared memory";
-        return LFM_E_INVALID;
-      }
-      rsm_set = rsm;
-    }
-    dim3 g2((ny + 7) / 8, nz);
-    spass_adj_row_kernel<<<g2, 256, rsm, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
-                                                                pitch, cp.adj_a2.out_scale, accumulate);
-    ++g_launches;
-    return cuda_check(cudaGetLastError(), "spass_adj_row_kernel launch", err);
-  }
-  dim3 grid((nx + SPA_VX - 1) / SPA_VX, nz);
-  spass_adj_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w,
-                                                             reinterpret_cast<const int2*>(cp.d_spa_fp), nx, ny, nz, nd,
-                                                             f.ell, pitch, tmax, cp.adj_a2.out_scale, accumulate);
+  dim3 grid((ny + vta - 1) / vta, nz);
+  if (vta == 8)
+    spass_adj_kernel<8><<<grid, 128, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
+                                                                  pitch, cp.adj_a2.out_scale, accumulate);
+  else
+    spass_adj_kernel<4><<<grid, 128, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
+                                                                  pitch, cp.adj_a2.out_scale, accumulate);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "spass_adj_kernel launch", err);
 }
@@ -345,8 +308,7 @@ lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
 }
 
 void free_camera(CameraPlan& cp) {
-  dfree(cp.d_spa_fp);
-  cp.d_spa_fp = nullptr;
+
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
   for (int ax = 0; ax < 2; ++ax)
     for (BandFamily* f : {&cp.s1f[ax], &cp.s1a[ax], &cp.s3f[ax], &cp.s3a[ax], &cp.cf[ax], &cp.ca[ax]})
@@ -2666,7 +2628,12 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       };
       std::string terr;
       const float t_sf = time2([&] { return k_spass_fwd(cp, sb, ob, nullptr, terr); });
-      const float t_sa = time2([&] { return k_spass_adj(cp, sb, ob, 0, nullptr, terr); });
+      cp.spa_vta = 4;
+      const float t_sa4 = time2([&] { return k_spass_adj(cp, sb, ob, 0, nullptr, terr); });
+      cp.spa_vta = 8;
+      const float t_sa8 = time2([&] { return k_spass_adj(cp, sb, ob, 0, nullptr, terr); });
+      cp.spa_vta = (t_sa4 > 0 && (t_sa8 <= 0 || t_sa4 < t_sa8)) ? 4 : 8;
+      const float t_sa = cp.spa_vta == 4 ? t_sa4 : t_sa8;
       const float adj_s = cp.adj_t ? t_z + op_best[10] : op_best[6];
       if (dbg)
         std::fprintf(stderr, "[lfm] direct s passes: fwd %.3f ms (vs %.3f), adj %.3f ms (vs %.3f) x2\n", t_sf, fwd_s, t_sa, adj_s);

@@ -183,10 +183,7 @@ struct CameraPlan {
   int perm_axis[2][3], perm_sign[2][3];   // [fwd: P, adj: P^T] source axis and sign per output axis
   std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
-  // direct s passes (spass.cuh): adjoint footprints {first s, width} per (slice, 16-column tile) of ca[0]
-  std::vector<int32_t> spa_fp;
-  int spa_wmax = 0;
-  int32_t* d_spa_fp = nullptr;
+  int spa_vta = 8;                        // voxel rows per CTA of the direct adjoint s pass (4 or 8, autotuned)
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
 };
 
