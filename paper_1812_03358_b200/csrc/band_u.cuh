@@ -34,6 +34,8 @@ struct UArgs {
   int group;              // blocks per TMEM accumulator before it is drained
   float scale;
   int accumulate;
+  int tile_mode;          // 0: tile = 128 consecutive rows; 1: 2 rows-of-slices (vt) x 64 slices, rows vt*nz + n
+  int tm_nz;              // nz for tile_mode 1
 };
 
 constexpr int U_STAGES = 4;
@@ -198,7 +200,9 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       // output: per 32-column chunk the warp's 32 x 32 block goes through its swizzled staging buffer and one
       // TMA store (or TMA add when accumulating); rows / columns outside the output are clipped by the TMA unit
       uint8_t* stg = sout + (warp - 4) * U_STAGE_OUT;
-      const int r0 = mt * 128 + 32 * q, c0 = nt * 256 + h * 128;
+      const int r0 = a.tile_mode == 0 ? mt * 128 + 32 * q
+                                       : (2 * (mt / (a.tm_nz >> 6)) + (q >> 1)) * a.tm_nz + 64 * (mt % (a.tm_nz >> 6)) + 32 * (q & 1);
+      const int c0 = nt * 256 + h * 128;
 #pragma unroll
       for (int c = 0; c < 128; c += 32) {
         if (lane == 0) bulk_wait_read0();

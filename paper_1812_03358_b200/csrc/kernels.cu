@@ -255,9 +255,9 @@ lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* str
 
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err) {
   const BandFamily& f = cp.ca[0];
-  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = f.n_src;
+  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;  // Z rows: detector columns
   const int pitch = (f.n_rows + 3) / 4 * 4;
-  const int vta = cp.spa_vta == 4 ? 4 : 8;
+  const int vta = std::getenv("LFM_SPA_VTA") ? (std::atoi(std::getenv("LFM_SPA_VTA")) == 4 ? 4 : 8) : (cp.spa_vta == 4 ? 4 : 8);
   const size_t smem = (size_t)vta * (nd + (nd >> 4) + 4) * 4;
   static size_t smem_set[2] = {48 * 1024, 48 * 1024};
   size_t& ss = smem_set[vta == 8];
@@ -274,10 +274,10 @@ lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   dim3 grid((ny + vta - 1) / vta, nz);
   if (vta == 8)
     spass_adj_kernel<8><<<grid, 128, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
-                                                                  pitch, cp.adj_a2.out_scale, accumulate);
+                                                                  pitch, cp.adj_c2.out_scale, accumulate);
   else
     spass_adj_kernel<4><<<grid, 128, smem, (cudaStream_t)stream>>>(Z, out, f.d_cnt, f.d_idx, f.d_w, nx, ny, nz, nd, f.ell,
-                                                                  pitch, cp.adj_a2.out_scale, accumulate);
+                                                                  pitch, cp.adj_c2.out_scale, accumulate);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "spass_adj_kernel launch", err);
 }
@@ -1620,9 +1620,51 @@ __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict_
   }
 }
 
+// 64 x 64 tiles with 16-byte accesses on both sides (rows and pitches multiples of 4 floats, 16-byte aligned
+// bases): 4 KB in flight per warp instead of 512 B.
+__global__ void __launch_bounds__(256) transpose64_kernel(const float* __restrict__ in, float* __restrict__ out, int R,
+                                                          int C, long long in_bs, long long in_pitch, long long out_bs,
+                                                          long long out_pitch) {
+  __shared__ float tile[64][65];
+  const int b = blockIdx.z;
+  const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
+  const float* ib = in + (size_t)b * in_bs;
+  float* ob = out + (size_t)b * out_bs;
+  const int t = threadIdx.x;
+  const int lc = 4 * (t & 15), lr = t >> 4;
+  float4 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = r0 + lr + 16 * k, c = c0 + lc;
+    v[k] = (r < R && c < C) ? __ldg(reinterpret_cast<const float4*>(ib + (size_t)r * in_pitch + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float* d = &tile[lr + 16 * k][lc];
+    d[0] = v[k].x; d[1] = v[k].y; d[2] = v[k].z; d[3] = v[k].w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = c0 + lr + 16 * k, r = r0 + lc;
+    if (r < R && c < C) {
+      const float4 o = make_float4(tile[lc][lr + 16 * k], tile[lc + 1][lr + 16 * k], tile[lc + 2][lr + 16 * k],
+                                   tile[lc + 3][lr + 16 * k]);
+      *reinterpret_cast<float4*>(ob + (size_t)c * out_pitch + r) = o;
+    }
+  }
+}
+
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err) {
   if (B <= 0 || R <= 0 || C <= 0) return LFM_OK;
+  if (R % 4 == 0 && C % 4 == 0 && in_bs % 4 == 0 && in_pitch % 4 == 0 && out_bs % 4 == 0 && out_pitch % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    dim3 g64((C + 63) / 64, (R + 63) / 64, B);
+    transpose64_kernel<<<g64, 256, 0, (cudaStream_t)stream>>>(in, out, R, C, in_bs, in_pitch, out_bs, out_pitch);
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "transpose64_kernel launch", err);
+  }
   dim3 grid((C + 31) / 32, (R + 31) / 32, B);
   transpose_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, out, R, C, in_bs, in_pitch, out_bs, out_pitch);
   ++g_launches;
@@ -1850,6 +1892,9 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.group = op.stages > 0 ? op.stages : 4;
     u.scale = op.out_scale * term.scale;
     u.accumulate = accumulate;
+    u.tile_mode = op.ft->u_mode;
+    u.tm_nz = op.ft->u_nz;
+    if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
     const int grid_u = std::min(u.n_mt * u.n_nt, g_num_sms());
     band_u_kernel<<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
     ++g_launches;

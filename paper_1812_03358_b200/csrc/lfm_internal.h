@@ -72,6 +72,7 @@ struct BandFamily {
   // tcgen05 form (band_u): per tile of 128 rows the union of the rows' supports cut into blocks of 16 source
   // cells; per block two 128 x 16 tf32 weight images (hi, lo) in the shared-memory layout the MMA reads
   std::vector<int32_t> u_off, u_k0;        // u_off[table * n_tiles + tile] .. +1 into blocks; u_k0[block]
+  int u_mode = 0, u_nz = 0;                // tile composition (build_umma): 0 = 128 rows, 1 = 2 vt x 64 slices
   std::vector<float> u_a;                  // 4096 floats per block
   int32_t* d_uoff = nullptr;
   int32_t* d_uk0 = nullptr;

@@ -1,7 +1,7 @@
 # ncu --set full of the direct s-pass kernels (forced), one launch each
 mkdir -p gpurun_out
 export LFM_FWD_T=2 LFM_ADJ_T=2 LFM_FWD_SPLIT=1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spass -c 3 -f -o gpurun_out/prof_spass \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:spass_fwd -c 1 -f -o gpurun_out/prof_spass \
   python -c "
 import sys; sys.path.insert(0,'.')
 import torch
