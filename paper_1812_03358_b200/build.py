@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["kernels.cu", "api.cu"]
 SOURCES_CPP = ["plan.cpp"]
-HEADERS = ["lfm_internal.h", "lfm_kernels.h", "band_u.cuh", "tc_sm100.h", "spass.cuh"]
+HEADERS = ["lfm_internal.h", "lfm_kernels.h", "band_u.cuh", "tc_sm100.h", "spass.cuh", "band_v.cuh"]
 
 
 def _inputs():

@@ -164,10 +164,10 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
     if (cp.fwd_split) {
-      if (cp.fwd_t == 2) {
-        // direct s pass (spass_fwd_kernel): slices -> interleaved U
+      if (cp.fwd_t == 2 || cp.fwd_t == 3) {
+        // direct s pass (spass_fwd_kernel, or band_v on the tensor cores): slices -> interleaved U
         std::string err;
-        lfm_status st = k_spass_fwd(cp, xr, w.z, stream, err);
+        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, xr, w.z, stream, err) : k_spass_fwd(cp, xr, w.z, stream, err);
         if (st != LFM_OK) return fail(st, err);
       } else if (cp.fwd_t) {
         // s pass as a t pass over the transposed slices, written back in the interleaved U layout
@@ -200,10 +200,11 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED) {
     TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1));  // one output: all (vt, n) rows
-    if (cp.adj_t == 2) {
-      // direct s pass (spass_adj_kernel) on Z
+    if (cp.adj_t == 2 || cp.adj_t == 3) {
+      // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
-      lfm_status st = k_spass_adj(cp, w.z, target, acc, stream, err);
+      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, w.z, target, acc, stream, err)
+                                    : k_spass_adj(cp, w.z, target, acc, stream, err);
       if (st != LFM_OK) return fail(st, err);
     } else if (cp.adj_t) {
       // Z_n -> ZT_n = [j][vt] per slice, then the s pass as a t pass with transposed output into x_n

@@ -1,0 +1,250 @@
+// band_v: the s passes of the two-pass collapsed path on the tcgen05 tensor cores (kind::tf32, 3xTF32),
+// the data as the MMA's A operand (M = 128 voxel rows vt of one slice), a banded s composite as B:
+//
+//   forward (DIR 0)  U[vt][n][s]   = sum_vx x[n][vt][vx] Cf_n[s][vx]        N = 256 detector columns s, K = vx
+//   adjoint (DIR 1)  x[n][vt][vx] (+)= scale sum_s Z[vt][n][s] Ca_n[vx][s]   N = 16 voxel columns vx,  K = s
+//
+// One work item = (slice n, row tile of 128 vt, N-tile); its K range (the union of the N-tile's supports) is
+// covered by blocks of 16 (build_vmma, kernels.cu) with per block the N x 16 weights pre-split into tf32 hi/lo
+// images in the K-major 64-byte-swizzled layout.  Per block the producer bulk-copies the images and loads the
+// data tile [128 vt][16 k] with one 3D TMA (64-byte swizzle = the same UMMA layout), the split warps write
+// A_lo = A - trunc(A), the MMA thread issues per 8-wide k-step  D += A_hi B_lo + A_lo B_hi + A_hi B_hi
+// (M128 N K8), and every `group` blocks the TMEM accumulator is drained into fp32 registers (the accumulator
+// truncates, see band_u.cuh).  The epilogue writes through shared memory and 3D TMA stores (U: boxes of
+// 32 s x 32 vt; x: 8 vx x 32 vt), or TMA reduce-adds when accumulating.  Warp roles as in band_u.
+#pragma once
+#include <cuda.h>
+
+#include "tc_sm100.h"
+
+namespace lfm {
+
+struct VArgs {
+  const float* B;          // weight images: block b at B + b * 32 * N floats (hi N x 16, then lo N x 16)
+  const int32_t* blk_off;  // per item key (n * n_nt + nt): blocks [off, off+1)
+  const int32_t* blk_k0;   // per block: first k (vx forward, s adjoint)
+  int nz, n_mt, n_nt;      // items = nz * n_mt * n_nt (item = (n * n_mt + mt) * n_nt + nt)
+  int group;               // blocks per TMEM accumulator before it is drained
+  float scale;
+  int accumulate;
+};
+
+constexpr int V_STAGES = 4;
+constexpr int V_THREADS = 384;
+
+template <int N>
+struct VCfg {
+  static constexpr int A_BYTES = 128 * 16 * 4;        // data tile [128][16] fp32 (8 KB)
+  static constexpr int B_BYTES = N * 16 * 4;          // one weight image [N][16]
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
+  static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
+  static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
+  static constexpr int OUT = 32 * OC * 4;             // staging per warp
+  static constexpr size_t SMEM = (size_t)V_STAGES * STAGE + 8 * OUT + 1024 + 256;
+  static constexpr int TCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
+};
+
+template <int N, int DIR>
+__global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
+                                                              const __grid_constant__ CUtensorMap out_map, VArgs a) {
+  using namespace tc;
+  using C = VCfg<N>;
+  extern __shared__ uint8_t v_smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sout = sm + V_STAGES * C::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * C::OUT);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + V_STAGES;
+  uint64_t* empty = bars + 2 * V_STAGES;
+  uint64_t* tfull = bars + 3 * V_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < V_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    fence_barrier_init();
+    prefetch_tma_desc(&a_map);
+    prefetch_tma_desc(&out_map);
+  }
+  if (warp == 1) tmem_alloc<C::TCOLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_items = a.nz * a.n_mt * a.n_nt;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int nt = it % a.n_nt, mt = (it / a.n_nt) % a.n_mt, n = it / (a.n_nt * a.n_mt);
+        const int key = n * a.n_nt + nt;
+        const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+        for (int b = b0; b < b1; ++b) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = sm + s * C::STAGE;
+          mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
+          bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 32 * N, 2 * C::B_BYTES, &full[s]);
+          const int k = __ldg(a.blk_k0 + b);
+          if (DIR == 0) tma_load_3d(st, &a_map, k, mt * 128, n, &full[s]);   // map (vx, vt, n)
+          else tma_load_3d(st, &a_map, k, n, mt * 128, &full[s]);            // map (s, n, vt)
+          if (++s == V_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int buf = 0;
+      uint32_t tph[2] = {0, 0};
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int nt = it % a.n_nt, n = it / (a.n_nt * a.n_mt);
+        const int key = n * a.n_nt + nt;
+        const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+        for (int g0 = b0; g0 < b1; g0 += a.group) {
+          mbar_wait(&tempty[buf], tph[buf] ^ 1);
+          tph[buf] ^= 1;
+          tc_fence_after();
+          const uint32_t d = tmem + buf * N;
+          const int g1 = min(b1, g0 + a.group);
+          for (int j = g0; j < g1; ++j) {
+            mbar_wait(&conv[s], ph);
+            tc_fence_after();
+            const uint32_t st = smem_u32(sm + s * C::STAGE);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint64_t ahi = smem_desc(st + 32 * kk, 16, 512, 4);
+              const uint64_t alo = smem_desc(st + C::A_BYTES + 32 * kk, 16, 512, 4);
+              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + 32 * kk, 16, 512, 4);
+              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + 32 * kk, 16, 512, 4);
+              mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kk != 0) ? 1u : 0u);
+              mma_tf32_ss(d, alo, bhi, IDESC, 1u);
+              mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
+            }
+            tc_commit(&empty[s]);
+            if (++s == V_STAGES) { s = 0; ph ^= 1; }
+          }
+          tc_commit(&tfull[buf]);
+          buf ^= 1;
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // lo split of the data tile: 8 KB = 512 float4, 64 threads x 8
+    const int t = threadIdx.x - 64;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int nt = it % a.n_nt, n = it / (a.n_nt * a.n_mt);
+      const int key = n * a.n_nt + nt;
+      const int nb = __ldg(a.blk_off + key + 1) - __ldg(a.blk_off + key);
+      for (int b = 0; b < nb; ++b) {
+        mbar_wait(&full[s], ph);
+        const float4* src = reinterpret_cast<const float4*>(sm + s * C::STAGE);
+        float4* lo = reinterpret_cast<float4*>(sm + s * C::STAGE + C::A_BYTES);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 u = src[t + 64 * i];
+          float4 l;
+          l.x = u.x - __uint_as_float(__float_as_uint(u.x) & 0xffffe000u);
+          l.y = u.y - __uint_as_float(__float_as_uint(u.y) & 0xffffe000u);
+          l.z = u.z - __uint_as_float(__float_as_uint(u.z) & 0xffffe000u);
+          l.w = u.w - __uint_as_float(__float_as_uint(u.w) & 0xffffe000u);
+          lo[t + 64 * i] = l;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&conv[s]);
+        if (++s == V_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (voxel rows), columns [h EC, (h+1) EC)
+    constexpr int EC = C::EC, OC = C::OC;
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    uint8_t* stg = sout + (warp - 4) * C::OUT;
+    int buf = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int nt = it % a.n_nt, mt = (it / a.n_nt) % a.n_mt, n = it / (a.n_nt * a.n_mt);
+      const int key = n * a.n_nt + nt;
+      const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+      float acc[EC];
+#pragma unroll
+      for (int c = 0; c < EC; ++c) acc[c] = 0.f;
+      for (int g0 = b0; g0 < b1; g0 += a.group) {
+        mbar_wait(&tfull[buf], tph[buf]);
+        tph[buf] ^= 1;
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * N + h * EC;
+        if constexpr (EC >= 16) {
+#pragma unroll
+          for (int c = 0; c < EC; c += 16) {
+            float v[16];
+            tmem_ld16(base + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+          }
+        } else {
+          float v[EC];
+          tmem_ld_n<EC>(base, v);
+#pragma unroll
+          for (int i = 0; i < EC; ++i) acc[i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        buf ^= 1;
+      }
+      const int vt0 = mt * 128 + 32 * q, c0 = nt * N + h * EC;
+#pragma unroll
+      for (int c = 0; c < EC; c += OC) {
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const float4 v = make_float4(a.scale * acc[c + 4 * jj], a.scale * acc[c + 4 * jj + 1],
+                                         a.scale * acc[c + 4 * jj + 2], a.scale * acc[c + 4 * jj + 3]);
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((jj ^ (lane & 7)) << 4)) = v;
+          }
+        } else {  // OC-float rows, no swizzle
+#pragma unroll
+          for (int jj = 0; jj < OC; jj += 4) {
+            const float4 v = make_float4(a.scale * acc[c + jj], a.scale * acc[c + jj + 1], a.scale * acc[c + jj + 2],
+                                         a.scale * acc[c + jj + 3]);
+            *reinterpret_cast<float4*>(stg + lane * OC * 4 + jj * 4) = v;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (DIR == 0) {  // U map (s, n, vt)
+            if (a.accumulate) tma_add_3d(&out_map, c0 + c, n, vt0, stg);
+            else tma_store_3d(&out_map, c0 + c, n, vt0, stg);
+          } else {  // x map (vx, vt, n)
+            if (a.accumulate) tma_add_3d(&out_map, c0 + c, vt0, n, stg);
+            else tma_store_3d(&out_map, c0 + c, vt0, n, stg);
+          }
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<C::TCOLS>(tmem);
+}
+
+}  // namespace lfm

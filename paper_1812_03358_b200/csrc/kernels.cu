@@ -17,10 +17,12 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
 #include "band_u.cuh"
+#include "band_v.cuh"
 #include "spass.cuh"
 #include "lfm_internal.h"
 #include "lfm_kernels.h"
@@ -28,6 +30,7 @@
 namespace lfm {
 
 thread_local int g_launches = 0;
+static int g_num_sms();
 
 lfm_status cuda_check(cudaError_t e, const char* what, std::string& err) {
   if (e == cudaSuccess) return LFM_OK;
@@ -46,6 +49,17 @@ static lfm_status dev_upload(T** dst, const void* src, size_t bytes, std::string
     return LFM_E_NOMEM;
   }
   return cuda_check(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "upload", err);
+}
+
+// tf32 value of an fp32 (round to nearest, ties away, low 13 bits cleared), as cvt.rna.tf32.f32
+static float tf32_host(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u += 0x1000u;
+  u &= 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
 }
 
 static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) {
@@ -237,6 +251,76 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
       bytes += sp.mlo[d].size() * 4 + w32.size() * 4;
     }
   }
+  // tcgen05 s passes (band_v.cuh): forward items (slice n, 256 detector columns), K = vx, from cf[0];
+  // adjoint items (slice n, 16 voxel columns), K = s, from ca[0].  Weights rounded once to fp32, then split
+  // hi = rn_tf32(w), lo = rn_tf32(w - hi); image element (row r, k) at byte r*64 + k*4, bits [4,6) ^= [7,9).
+  {
+    auto build = [&](const BandFamily& f, int N, CameraPlan::VTab& T) {
+      T.N = N;
+      T.n_nt = (f.n_rows + N - 1) / N;
+      T.off.assign((size_t)f.n_tables * T.n_nt + 1, 0);
+      T.k0.clear();
+      T.img.clear();
+      std::vector<char> any(f.n_src + 16);
+      for (int m = 0; m < f.n_tables; ++m)
+        for (int t = 0; t < T.n_nt; ++t) {
+          T.off[(size_t)m * T.n_nt + t] = (int)T.k0.size();
+          std::fill(any.begin(), any.end(), 0);
+          const int r0 = t * N, r1 = std::min(f.n_rows, r0 + N);
+          for (int r = r0; r < r1; ++r) {
+            const size_t idx = (size_t)m * f.n_rows + r;
+            for (int e = 0; e < f.len[idx]; ++e)
+              if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e] = 1;
+          }
+          int last = -(1 << 30);
+          for (int kn = 0; kn < f.n_src; ++kn) {
+            if (!any[kn] || kn < last + 16) continue;
+            const int k = kn & ~3;  // TMA: the innermost box coordinate must sit on a 16-byte boundary
+            last = k;
+            T.k0.push_back(k);
+            const size_t base = T.img.size();
+            T.img.resize(base + (size_t)32 * N, 0.f);
+            for (int r = r0; r < r1; ++r) {
+              const size_t idx = (size_t)m * f.n_rows + r;
+              for (int kk = 0; kk < 16; ++kk) {
+                const int e = k + kk - f.start[idx];
+                if (e < 0 || e >= f.len[idx]) continue;
+                const float w = (float)f.w64[idx * f.taps + e];
+                const float wh = tf32_host(w), wl = tf32_host(w - wh);
+                uint32_t o = (uint32_t)((r - r0) * 64 + kk * 4);
+                o ^= ((o >> 7) & 3u) << 4;
+                T.img[base + o / 4] = wh;
+                T.img[base + (size_t)16 * N + o / 4] = wl;
+              }
+            }
+          }
+        }
+      T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
+    };
+    build(cp.cf[0], 256, cp.vf);
+    build(cp.ca[0], 16, cp.va);
+    if (std::getenv("LFM_DEBUG"))
+      for (const CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
+        int mx = 0, mn = 1 << 30;
+        for (size_t i = 0; i + 1 < T->off.size(); ++i) {
+          mx = std::max(mx, T->off[i + 1] - T->off[i]);
+          mn = std::min(mn, T->off[i + 1] - T->off[i]);
+        }
+        int kmin = 1 << 30, kmax = -1;
+        for (int k : T->k0) { kmin = std::min(kmin, k); kmax = std::max(kmax, k); }
+        std::fprintf(stderr, "[lfm] band_v N %d: items %zu blocks %zu (min %d max %d per item) k0 in [%d, %d]\n", T->N,
+                     T->off.size() - 1, T->k0.size(), mn, mx, kmin, kmax);
+      }
+    for (CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
+      std::vector<int32_t> k0(T->k0);
+      k0.push_back(0);
+      if ((st = dev_upload(&T->d_off, T->off.data(), T->off.size() * 4, err)) != LFM_OK) return st;
+      if ((st = dev_upload(&T->d_k0, k0.data(), k0.size() * 4, err)) != LFM_OK) return st;
+      if (!T->img.empty() && (st = dev_upload(&T->d_img, T->img.data(), T->img.size() * 4, err)) != LFM_OK) return st;
+      bytes += T->off.size() * 4 + k0.size() * 4 + T->img.size() * 4;
+      std::vector<float>().swap(T->img);  // host copy not needed after upload
+    }
+  }
   cp.info.table_bytes = bytes;
   return LFM_OK;
 }
@@ -282,6 +366,91 @@ lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   return cuda_check(cudaGetLastError(), "spass_adj_kernel launch", err);
 }
 
+// ---------------------------------------------------------------------------------------------- band_v host side
+typedef CUresult (*EncodeTiledFnV)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static lfm_status encode3(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
+                          const int box[3], CUtensorMapSwizzle swz, std::string& err) {
+  static EncodeTiledFnV encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr) != cudaSuccess || !encode) {
+      cudaGetLastError();
+      err = "band_v: cuTensorMapEncodeTiled unavailable";
+      return LFM_E_CUDA;
+    }
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (strides[0] & 15) || (strides[1] & 15)) {
+    err = "band_v: buffers and their rows must be 16-byte aligned";
+    return LFM_E_INVALID;
+  }
+  cuuint64_t gd[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+  cuuint64_t gs[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
+  cuuint32_t bx[3] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2]}, es[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gd, gs, bx, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "band_v: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return LFM_E_CUDA;
+  }
+  return LFM_OK;
+}
+
+template <int N, int DIR>
+static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
+                                float scale, int accumulate, void* stream, std::string& err) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(band_v_kernel<N, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VCfg<N>::SMEM) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
+    attr = true;
+  }
+  VArgs v;
+  v.B = T.d_img;
+  v.blk_off = T.d_off;
+  v.blk_k0 = T.d_k0;
+  v.nz = nz;
+  v.n_mt = (ny + 127) / 128;
+  v.n_nt = T.n_nt;
+  v.group = 4;
+  v.scale = scale;
+  v.accumulate = accumulate;
+  const int items = v.nz * v.n_mt * v.n_nt;
+  band_v_kernel<N, DIR><<<std::min(items, g_num_sms()), V_THREADS, VCfg<N>::SMEM, (cudaStream_t)stream>>>(am, om, v);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
+}
+
+lfm_status k_vpass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err) {
+  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
+  if (!cp.vf.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
+  CUtensorMap am, om;
+  const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
+  const int ab[3] = {16, 128, 1};
+  lfm_status st = encode3(&am, x, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err);
+  if (st != LFM_OK) return st;
+  const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+  const int ob[3] = {32, 1, 32};
+  if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
+  return launch_band_v<256, 0>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err);
+}
+
+lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err) {
+  const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
+  if (!cp.va.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
+  CUtensorMap am, om;
+  const long long ad[3] = {nd, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+  const int ab[3] = {16, 1, 128};
+  lfm_status st = encode3(&am, Z, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err);
+  if (st != LFM_OK) return st;
+  const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
+  const int ob[3] = {8, 32, 1};
+  if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
+  return launch_band_v<16, 1>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err);
+}
+
+
 static void dfree(void* p) {
   if (p) cudaFree(p);
 }
@@ -308,6 +477,10 @@ lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
 }
 
 void free_camera(CameraPlan& cp) {
+  for (CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
+    dfree(T->d_off); dfree(T->d_k0); dfree(T->d_img);
+    T->d_off = nullptr; T->d_k0 = nullptr; T->d_img = nullptr;
+  }
 
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
   for (int ax = 0; ax < 2; ++ax)
@@ -2679,11 +2852,16 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       const float t_sa8 = time2([&] { return k_spass_adj(cp, sb, ob, 0, nullptr, terr); });
       cp.spa_vta = (t_sa4 > 0 && (t_sa8 <= 0 || t_sa4 < t_sa8)) ? 4 : 8;
       const float t_sa = cp.spa_vta == 4 ? t_sa4 : t_sa8;
-      const float adj_s = cp.adj_t ? t_z + op_best[10] : op_best[6];
+      float adj_s = cp.adj_t ? t_z + op_best[10] : op_best[6];
+      const float t_vf = std::getenv("LFM_NO_VF") ? -1.f : time2([&] { return k_vpass_fwd(cp, sb, ob, nullptr, terr); });
+      const float t_va = std::getenv("LFM_NO_VA") ? -1.f : time2([&] { return k_vpass_adj(cp, sb, ob, 0, nullptr, terr); });
       if (dbg)
-        std::fprintf(stderr, "[lfm] direct s passes: fwd %.3f ms (vs %.3f), adj %.3f ms (vs %.3f) x2\n", t_sf, fwd_s, t_sa, adj_s);
+        std::fprintf(stderr, "[lfm] direct s passes: fwd %.3f / tc %.3f ms (vs %.3f), adj %.3f / tc %.3f ms (vs %.3f) x2\n",
+                     t_sf, t_vf, fwd_s, t_sa, t_va, adj_s);
       if (t_sf > 0 && (fwd_s <= 0 || t_sf < fwd_s)) { cp.fwd_t = 2; fwd_s = t_sf; }
-      if (t_sa > 0 && (adj_s <= 0 || t_sa < adj_s)) cp.adj_t = 2;
+      if (t_sa > 0 && (adj_s <= 0 || t_sa < adj_s)) { cp.adj_t = 2; adj_s = t_sa; }
+      if (t_vf > 0 && (fwd_s <= 0 || t_vf < fwd_s)) { cp.fwd_t = 3; fwd_s = t_vf; }
+      if (t_va > 0 && (adj_s <= 0 || t_va < adj_s)) { cp.adj_t = 3; adj_s = t_va; }
       cudaEventDestroy(f0);
       cudaEventDestroy(f1);
     }
@@ -2708,10 +2886,14 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] - '0';
   if (cp.fwd_t == 1 && !(cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5))) cp.fwd_t = 0;
   if (cp.adj_t == 1 && !(cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5))) cp.adj_t = 0;
-  if (cp.fwd_t < 0 || cp.fwd_t > 2) cp.fwd_t = 0;
-  if (cp.adj_t < 0 || cp.adj_t > 2) cp.adj_t = 0;
+  // band_v moves rows by TMA: 16-byte row strides of the volume and of the detector intermediates
+  const bool tc_ok = cp.info.nx % 4 == 0 && cp.adj_c1.n_os % 4 == 0 && cp.cf[0].n_rows % 4 == 0;
+  if (cp.fwd_t == 3 && !tc_ok) cp.fwd_t = 2;
+  if (cp.adj_t == 3 && !tc_ok) cp.adj_t = 2;
+  if (cp.fwd_t < 0 || cp.fwd_t > 3) cp.fwd_t = 0;
+  if (cp.adj_t < 0 || cp.adj_t > 3) cp.adj_t = 0;
   if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
-  static const char* smode[] = {"direct sep", "transposed", "spass"};
+  static const char* smode[] = {"direct sep", "transposed", "spass", "tcgen05"};
   if (dbg)
     std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",
                  cp.fwd_split ? "two passes" : "fused", smode[cp.fwd_t], t_x, t_z, smode[cp.adj_t]);

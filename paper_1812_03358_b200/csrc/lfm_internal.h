@@ -173,8 +173,8 @@ struct CameraPlan {
   SepOp fwd_c1, fwd_c2;                   // collapsed forward in two passes: s (U_n for all n), then t
   int fwd_split = 0;                      // 1: forward uses fwd_c1 + fwd_c2 (chosen by the autotuner)
   SepOp fwd_p1, adj_a2;                   // transposed s passes (band_m with transposed output)
-  int fwd_t = 0;                          // 1: split forward's s pass = transpose x + fwd_p1, 2: spass_fwd (autotuner)
-  int adj_t = 0;                          // 1: adjoint's s pass = transpose Z + adj_a2, 2: spass_adj (autotuner)
+  int fwd_t = 0;                          // forward s pass: 0 sep, 1 transpose x + fwd_p1, 2 spass_fwd, 3 band_v (autotuner)
+  int adj_t = 0;                          // adjoint s pass: 0 sep, 1 transpose Z + adj_a2, 2 spass_adj, 3 band_v (autotuner)
   BandFamily id_s, id_t, id_vt;           // identity row maps used by the two-pass adjoint/forward
   BandFamily ca1n, cf1n;                  // slice-interleaved collapsed t families (rows (vt,n) / sources (vt,n))
   // lf_transport ops (output b = n*K + k for slice-indexed families)
@@ -185,6 +185,15 @@ struct CameraPlan {
   std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
   int spa_vta = 8;                        // voxel rows per CTA of the direct adjoint s pass (4 or 8, autotuned)
+  // tcgen05 s passes (band_v.cuh): per item (slice n, N-tile) the K blocks of 16 and the N x 16 hi/lo images
+  struct VTab {
+    int N = 0, n_nt = 0;
+    std::vector<int32_t> off, k0;
+    std::vector<float> img;
+    int32_t* d_off = nullptr;
+    int32_t* d_k0 = nullptr;
+    float* d_img = nullptr;
+  } vf, va;
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
 };
 
@@ -218,6 +227,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
 lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
+lfm_status k_vpass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
+lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);

@@ -111,10 +111,10 @@ def test_forced_t_pass_variants(op_name, variant, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["small_two", "tiny_multi", "tiny_dirac"])
-@pytest.mark.parametrize("transposed", ["0", "1", "2"])
+@pytest.mark.parametrize("transposed", ["0", "1", "2", "3"])
 def test_s_pass_orders(name, transposed, monkeypatch):
     """The three s-pass forms of the two-pass collapsed path (0: direct sep kernel, 1: transpose + band_m/band_f
-    with transposed output, 2: the direct s-pass kernels of spass.cuh), forced, against the oracle: forward,
+    with transposed output, 2: the direct s-pass kernels of spass.cuh, 3: the tcgen05 s passes of band_v.cuh), forced, against the oracle: forward,
     adjoint and their row-range forms."""
     from paper_1812_03358_b200 import lfm
     cfg = make_config(name)
