@@ -5,9 +5,10 @@
 //   adjoint (DIR 1)  x[n][vt][vx] (+)= scale sum_s Z[vt][n][s] Ca_n[vx][s]   N = 16 voxel columns vx,  K = s
 //
 // One work item = (slice n, row tile of 128 vt, N-tile); its K range (the union of the N-tile's supports) is
-// covered by blocks of 16 (build_vmma, kernels.cu) with per block the N x 16 weights pre-split into tf32 hi/lo
-// images in the K-major 64-byte-swizzled layout.  Per block the producer bulk-copies the images and loads the
-// data tile [128 vt][16 k] with one 3D TMA (64-byte swizzle = the same UMMA layout), the split warps write
+// covered by blocks of BK = 16 or 32 (upload_camera, kernels.cu) with per block the N x BK weights pre-split into
+// tf32 hi/lo images in the K-major swizzled layout (64-byte for BK 16, 128-byte for BK 32).  Per block the
+// producer bulk-copies the images and loads the data tile [128 vt][BK k] with one 3D TMA (same swizzle = the
+// same UMMA layout), the split warps write
 // A_lo = A - trunc(A), the MMA thread issues per 8-wide k-step  D += A_hi B_lo + A_lo B_hi + A_hi B_hi
 // (M128 N K8), and every `group` blocks the TMEM accumulator is drained into fp32 registers (the accumulator
 // truncates, see band_u.cuh).  The epilogue writes through shared memory and 3D TMA stores (U: boxes of
@@ -29,39 +30,41 @@ struct VArgs {
   int accumulate;
 };
 
-constexpr int V_STAGES = 4;
 constexpr int V_THREADS = 384;
 
-template <int N>
+template <int N, int BK>
 struct VCfg {
-  static constexpr int A_BYTES = 128 * 16 * 4;        // data tile [128][16] fp32 (8 KB)
-  static constexpr int B_BYTES = N * 16 * 4;          // one weight image [N][16]
+  static constexpr int A_BYTES = 128 * BK * 4;        // data tile [128][BK] fp32
+  static constexpr int B_BYTES = N * BK * 4;          // one weight image [N][BK]
+  static constexpr int STAGES = (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES);
+  static constexpr int LAYOUT = BK == 32 ? 2 : 4;     // UMMA K-major 128-byte (BK 32) or 64-byte (BK 16) swizzle
+  static constexpr int SBO = 8 * BK * 4;              // 8-row core-matrix group stride
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
   static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
   static constexpr int OUT = 32 * OC * 4;             // staging per warp
-  static constexpr size_t SMEM = (size_t)V_STAGES * STAGE + 8 * OUT + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * OUT + 1024 + 256;
   static constexpr int TCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
 };
 
-template <int N, int DIR>
+template <int N, int DIR, int BK>
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
                                                               const __grid_constant__ CUtensorMap out_map, VArgs a) {
   using namespace tc;
-  using C = VCfg<N>;
+  using C = VCfg<N, BK>;
   extern __shared__ uint8_t v_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sout = sm + V_STAGES * C::STAGE;
+  uint8_t* sout = sm + C::STAGES * C::STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * C::OUT);
   uint64_t* full = bars;
-  uint64_t* conv = bars + V_STAGES;
-  uint64_t* empty = bars + 2 * V_STAGES;
-  uint64_t* tfull = bars + 3 * V_STAGES;
+  uint64_t* conv = bars + C::STAGES;
+  uint64_t* empty = bars + 2 * C::STAGES;
+  uint64_t* tfull = bars + 3 * C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < V_STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], 64);
       mbar_init(&empty[s], 1);
@@ -93,11 +96,11 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
-          bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 32 * N, 2 * C::B_BYTES, &full[s]);
+          bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           const int k = __ldg(a.blk_k0 + b);
           if (DIR == 0) tma_load_3d(st, &a_map, k, mt * 128, n, &full[s]);   // map (vx, vt, n)
           else tma_load_3d(st, &a_map, k, n, mt * 128, &full[s]);            // map (s, n, vt)
-          if (++s == V_STAGES) { s = 0; ph ^= 1; }
+          if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -123,17 +126,17 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
             tc_fence_after();
             const uint32_t st = smem_u32(sm + s * C::STAGE);
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              const uint64_t ahi = smem_desc(st + 32 * kk, 16, 512, 4);
-              const uint64_t alo = smem_desc(st + C::A_BYTES + 32 * kk, 16, 512, 4);
-              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + 32 * kk, 16, 512, 4);
-              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + 32 * kk, 16, 512, 4);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ahi = smem_desc(st + 32 * kk, 16, C::SBO, C::LAYOUT);
+              const uint64_t alo = smem_desc(st + C::A_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
+              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
+              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
               mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kk != 0) ? 1u : 0u);
               mma_tf32_ss(d, alo, bhi, IDESC, 1u);
               mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
             }
             tc_commit(&empty[s]);
-            if (++s == V_STAGES) { s = 0; ph ^= 1; }
+            if (++s == C::STAGES) { s = 0; ph ^= 1; }
           }
           tc_commit(&tfull[buf]);
           buf ^= 1;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
       }
     }
   } else if (warp < 4) {
-    // lo split of the data tile: 8 KB = 512 float4, 64 threads x 8
+    // lo split of the data tile: 128 x BK floats, 64 threads
     const int t = threadIdx.x - 64;
     int s = 0;
     uint32_t ph = 0;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         const float4* src = reinterpret_cast<const float4*>(sm + s * C::STAGE);
         float4* lo = reinterpret_cast<float4*>(sm + s * C::STAGE + C::A_BYTES);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < BK / 2; ++i) {
           const float4 u = src[t + 64 * i];
           float4 l;
           l.x = u.x - __uint_as_float(__float_as_uint(u.x) & 0xffffe000u);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         }
         fence_proxy_async_smem();
         mbar_arrive(&conv[s]);
-        if (++s == V_STAGES) { s = 0; ph ^= 1; }
+        if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else {

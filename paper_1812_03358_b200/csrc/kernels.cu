@@ -255,13 +255,16 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
   // adjoint items (slice n, 16 voxel columns), K = s, from ca[0].  Weights rounded once to fp32, then split
   // hi = rn_tf32(w), lo = rn_tf32(w - hi); image element (row r, k) at byte r*64 + k*4, bits [4,6) ^= [7,9).
   {
-    auto build = [&](const BandFamily& f, int N, CameraPlan::VTab& T) {
+    auto build = [&](const BandFamily& f, int N, int BK, CameraPlan::VTab& T) {
       T.N = N;
+      T.BK = BK;
       T.n_nt = (f.n_rows + N - 1) / N;
       T.off.assign((size_t)f.n_tables * T.n_nt + 1, 0);
       T.k0.clear();
       T.img.clear();
-      std::vector<char> any(f.n_src + 16);
+      std::vector<char> any(f.n_src + 32);
+      const int row_bytes = BK * 4;
+      const uint32_t smask = BK == 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
       for (int m = 0; m < f.n_tables; ++m)
         for (int t = 0; t < T.n_nt; ++t) {
           T.off[(size_t)m * T.n_nt + t] = (int)T.k0.size();
@@ -274,31 +277,33 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
           }
           int last = -(1 << 30);
           for (int kn = 0; kn < f.n_src; ++kn) {
-            if (!any[kn] || kn < last + 16) continue;
+            if (!any[kn] || kn < last + BK) continue;
             const int k = kn & ~3;  // TMA: the innermost box coordinate must sit on a 16-byte boundary
             last = k;
             T.k0.push_back(k);
             const size_t base = T.img.size();
-            T.img.resize(base + (size_t)32 * N, 0.f);
+            T.img.resize(base + (size_t)2 * BK * N, 0.f);
             for (int r = r0; r < r1; ++r) {
               const size_t idx = (size_t)m * f.n_rows + r;
-              for (int kk = 0; kk < 16; ++kk) {
+              for (int kk = 0; kk < BK; ++kk) {
                 const int e = k + kk - f.start[idx];
                 if (e < 0 || e >= f.len[idx]) continue;
                 const float w = (float)f.w64[idx * f.taps + e];
                 const float wh = tf32_host(w), wl = tf32_host(w - wh);
-                uint32_t o = (uint32_t)((r - r0) * 64 + kk * 4);
-                o ^= ((o >> 7) & 3u) << 4;
+                uint32_t o = (uint32_t)((r - r0) * row_bytes + kk * 4);
+                o ^= ((o >> 7) & smask) << 4;
                 T.img[base + o / 4] = wh;
-                T.img[base + (size_t)16 * N + o / 4] = wl;
+                T.img[base + (size_t)BK * N + o / 4] = wl;
               }
             }
           }
         }
       T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
     };
-    build(cp.cf[0], 256, cp.vf);
-    build(cp.ca[0], 16, cp.va);
+    const int bk_f = std::getenv("LFM_VBK_F") ? std::atoi(std::getenv("LFM_VBK_F")) : 32;
+    const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
+    build(cp.cf[0], 256, bk_f == 16 ? 16 : 32, cp.vf);
+    build(cp.ca[0], 16, bk_a == 16 ? 16 : 32, cp.va);
     if (std::getenv("LFM_DEBUG"))
       for (const CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
         int mx = 0, mn = 1 << 30;
@@ -397,12 +402,12 @@ static lfm_status encode3(CUtensorMap* map, const float* base, const long long d
   return LFM_OK;
 }
 
-template <int N, int DIR>
+template <int N, int DIR, int BK>
 static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(band_v_kernel<N, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VCfg<N>::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(band_v_kernel<N, DIR, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VCfg<N, BK>::SMEM) != cudaSuccess)
       return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
     attr = true;
   }
@@ -417,7 +422,7 @@ static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am
   v.scale = scale;
   v.accumulate = accumulate;
   const int items = v.nz * v.n_mt * v.n_nt;
-  band_v_kernel<N, DIR><<<std::min(items, g_num_sms()), V_THREADS, VCfg<N>::SMEM, (cudaStream_t)stream>>>(am, om, v);
+  band_v_kernel<N, DIR, BK><<<std::min(items, g_num_sms()), V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
@@ -427,13 +432,14 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const float* x, float* U, void* str
   if (!cp.vf.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
-  const int ab[3] = {16, 128, 1};
-  lfm_status st = encode3(&am, x, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err);
+  const int ab[3] = {cp.vf.BK, 128, 1};
+  lfm_status st = encode3(&am, x, ad, as, ab, cp.vf.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
   const int ob[3] = {32, 1, 32};
   if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
-  return launch_band_v<256, 0>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err);
+  return cp.vf.BK == 32 ? launch_band_v<256, 0, 32>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err)
+                        : launch_band_v<256, 0, 16>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err);
 }
 
 lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err) {
@@ -441,13 +447,14 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   if (!cp.va.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const long long ad[3] = {nd, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
-  const int ab[3] = {16, 1, 128};
-  lfm_status st = encode3(&am, Z, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err);
+  const int ab[3] = {cp.va.BK, 1, 128};
+  lfm_status st = encode3(&am, Z, ad, as, ab, cp.va.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
   const int ob[3] = {8, 32, 1};
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
-  return launch_band_v<16, 1>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err);
+  return cp.va.BK == 32 ? launch_band_v<16, 1, 32>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err)
+                        : launch_band_v<16, 1, 16>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err);
 }
 
 

@@ -187,7 +187,7 @@ struct CameraPlan {
   int spa_vta = 8;                        // voxel rows per CTA of the direct adjoint s pass (4 or 8, autotuned)
   // tcgen05 s passes (band_v.cuh): per item (slice n, N-tile) the K blocks of 16 and the N x 16 hi/lo images
   struct VTab {
-    int N = 0, n_nt = 0;
+    int N = 0, n_nt = 0, BK = 16;
     std::vector<int32_t> off, k0;
     std::vector<float> img;
     int32_t* d_off = nullptr;
