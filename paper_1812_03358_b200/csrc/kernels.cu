@@ -303,7 +303,8 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
     const int bk_f = std::getenv("LFM_VBK_F") ? std::atoi(std::getenv("LFM_VBK_F")) : 32;
     const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
     build(cp.cf[0], 256, bk_f == 16 ? 16 : 32, cp.vf);
-    build(cp.ca[0], 16, bk_a == 16 ? 16 : 32, cp.va);
+    const int vn_a = std::getenv("LFM_VN_A") ? std::atoi(std::getenv("LFM_VN_A")) : 16;
+    build(cp.ca[0], vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : 32, cp.va);
     if (std::getenv("LFM_DEBUG"))
       for (const CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
         int mx = 0, mn = 1 << 30;
@@ -451,10 +452,14 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   lfm_status st = encode3(&am, Z, ad, as, ab, cp.va.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
-  const int ob[3] = {8, 32, 1};
+  const int ob[3] = {cp.va.N / 2, 32, 1};
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
-  return cp.va.BK == 32 ? launch_band_v<16, 1, 32>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err)
-                        : launch_band_v<16, 1, 16>(cp.va, am, om, nz, ny, cp.adj_c2.out_scale, accumulate, stream, err);
+  const float sc = cp.adj_c2.out_scale;
+  if (cp.va.N == 32)
+    return cp.va.BK == 32 ? launch_band_v<32, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
+                          : launch_band_v<32, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
+  return cp.va.BK == 32 ? launch_band_v<16, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
+                        : launch_band_v<16, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
 }
 
 
@@ -2173,34 +2178,32 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 }
 
 // ------------------------------------------------------------------------------------------
-// Shear pass: out[i] = sum_k w[line][k] * in[pos + mlo[line] + k along the pass axis]
+// Shear pass: out[i] = sum_k w[line][k] * in[pos + mlo[line] + k along the pass axis].  3D grid (x tiles of 32,
+// y tiles of 8, z): no 64-bit divisions; consecutive threads on consecutive x (coalesced rows).
 template <int TAPS>
 __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     const int32_t* __restrict__ mlo, const float* __restrict__ w,
                                                     int axis, int nx, int ny, int nz, int accumulate) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long nvox = (long long)nx * ny * nz;
-  if (idx >= nvox) return;
-  int ix = (int)(idx % nx);
-  long long r = idx / nx;
-  int iy = (int)(r % ny);
-  int iz = (int)(r / ny);
+  const int ix = blockIdx.x * 32 + threadIdx.x, iy = blockIdx.y * 8 + threadIdx.y, iz = blockIdx.z;
+  if (ix >= nx || iy >= ny) return;
+  const size_t idx = ((size_t)iz * ny + iy) * nx + ix;
   int line, pos, n;
-  long long stride;
-  if (axis == 0) { line = ix + nx * iy; pos = iz; n = nz; stride = (long long)nx * ny; }
+  size_t stride;
+  if (axis == 0) { line = ix + nx * iy; pos = iz; n = nz; stride = (size_t)nx * ny; }
   else if (axis == 1) { line = iy + ny * iz; pos = ix; n = nx; stride = 1; }
   else { line = ix + nx * iz; pos = iy; n = ny; stride = nx; }
   const int m0 = __ldg(mlo + line);
   const float* wl = w + (size_t)line * TAPS;
+  const float* src = in + idx - (size_t)pos * stride;  // start of this voxel's line
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < TAPS; k += 4) {
-    float4 w4 = __ldg(reinterpret_cast<const float4*>(wl + k));
-    float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wl + k));
+    const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      int j = pos + m0 + k + q;
-      if (j >= 0 && j < n) acc = fmaf(wk[q], __ldg(in + idx + (long long)(j - pos) * stride), acc);
+      const int j = pos + m0 + k + q;
+      if (j >= 0 && j < n) acc = fmaf(wk[q], __ldg(src + (size_t)j * stride), acc);
     }
   }
   out[idx] = accumulate ? out[idx] + acc : acc;
@@ -2208,15 +2211,14 @@ __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in
 
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
-  long long nvox = (long long)nx * ny * nz;
-  dim3 grid((unsigned)((nvox + 255) / 256));
+  dim3 grid((nx + 31) / 32, (ny + 7) / 8, nz), blk(32, 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (sp.taps == 4)
-    shear_kernel<4><<<grid, 256, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
+    shear_kernel<4><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
   else if (sp.taps == 8)
-    shear_kernel<8><<<grid, 256, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
+    shear_kernel<8><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
   else
-    shear_kernel<16><<<grid, 256, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
+    shear_kernel<16><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "shear_kernel launch", err);
 }

@@ -12,3 +12,6 @@ for st in fwd adj; do
   timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -f -o gpurun_out/prof_$st \
     python tools/prof_stage.py $st > gpurun_out/ncu_$st.log 2>&1; echo "NCU $st EXIT $?"
 done
+# the s passes (band_v, tcgen05): one forward and one adjoint launch
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:band_v -f \
+  -o gpurun_out/prof_spass python tools/prof_pair.py 0 > gpurun_out/ncu_spass.log 2>&1; echo "NCU spass EXIT $?"
