@@ -162,6 +162,11 @@ lfm_status lfm_lf_transport(lfm_plan p, int cam, int dst_plane, int src_plane, c
 lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* out,
                           int accumulate, void* ws, size_t ws_bytes, void* stream);
 
+/* dst += src over n floats (the sum over cameras of the backprojections, sum_c A_c^T r_c in the PWLS gradient
+ * eqn,pls P:299-317, when the cameras run concurrently on their own streams into private volumes).  dst and
+ * src must not alias; n >= 0. */
+lfm_status lfm_vol_accumulate(const float* src, float* dst, long long n, void* stream);
+
 /* y = A_c x (rotation, slice collapse, camera; §3.2).  x: n_vox, y: n_pix. */
 lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y,
                          void* ws, size_t ws_bytes, void* stream);

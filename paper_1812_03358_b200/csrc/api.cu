@@ -407,6 +407,17 @@ lfm_status lfm_lf_transport(lfm_plan p, int cam, int dst_plane, int src_plane, c
   return st;
 }
 
+lfm_status lfm_vol_accumulate(const float* src, float* dst, long long n, void* stream) {
+  g_launches = 0;
+  if (n < 0) return fail(LFM_E_INVALID, "n < 0");
+  if (n == 0) return LFM_OK;
+  if (!src || !dst || src == dst) return fail(LFM_E_INVALID, "src/dst NULL or aliased");
+  std::string err;
+  lfm_status st = k_copy_scale(src, dst, n, 1.f, 1, stream, err);
+  g_last_launches = g_launches;
+  return st == LFM_OK ? st : fail(st, err);
+}
+
 lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* out, int accumulate, void* ws,
                           size_t ws_bytes, void* stream) {
   g_launches = 0;

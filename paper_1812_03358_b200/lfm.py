@@ -88,6 +88,7 @@ _SIGS = {
     "lfm_plan_export_table": [_P, _I, _I, _I, _I, _P, _S, ctypes.POINTER(_S)],
     "lfm_lf_transport": [_P, _I, _I, _I, _P, _P, _P, _S, _P],
     "lfm_vol_rotate": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
+    "lfm_vol_accumulate": [_P, _P, ctypes.c_longlong, _P],
     "lfm_A_forward": [_P, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_forward_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _S, _P],
@@ -217,6 +218,11 @@ def lf_transport(plan, cam, dst_plane, src_plane, src, dst, ws, stream=None):
 def vol_rotate(plan, cam, direction, src, dst, ws, accumulate=False, stream=None):
     _check(_lib.lfm_vol_rotate(plan.handle, cam, direction, _ptr(src), _ptr(dst), int(accumulate), _ptr(ws),
                                ws.numel(), _stream(stream)))
+
+
+def vol_accumulate(src, dst, stream=None):
+    """dst += src (the camera sum of concurrent backprojections)."""
+    _check(_lib.lfm_vol_accumulate(_ptr(src), _ptr(dst), int(src.numel()), _stream(stream)))
 
 
 def A_forward(plan, cam, x, y, ws, path=COLLAPSED, stream=None):

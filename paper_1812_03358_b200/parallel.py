@@ -60,3 +60,39 @@ class PairRunner:
     def pair(self, x, ys, rs, g):
         self.forward(x, ys)
         self.adjoint(rs, g)
+
+
+class ConcurrentPair:
+    """The same pair with every item on its own CUDA stream and workspace (one process per GPU, items of
+    this rank only).  Forwards are independent.  Item 0's adjoint writes g; item i > 0 writes a private
+    volume g_i; after all items finish, the g_i are added into g in item order (deterministic: the same
+    summation order as the sequential PairRunner, g = ((A_0^T r_0) + A_1^T r_1) + ...).
+
+    run(i, fn) runs fn on item i's stream after the previous call's inputs are visible (injected: CUDA
+    streams on a GPU, plain calls on CPU); join() makes the main stream wait for every item;
+    accumulate(src, dst) adds on the main stream.
+    """
+
+    def __init__(self, items, forward_rows, adjoint_rows, accumulate, zero, run, join, private, allreduce=None):
+        self.items = items
+        self.forward_rows = forward_rows      # (i, c, r0, r1, x, y)
+        self.adjoint_rows = adjoint_rows      # (i, c, r0, r1, r, g_target)   overwrite
+        self.accumulate = accumulate          # (src, dst)                     dst += src
+        self.zero = zero
+        self.run = run                        # (i, fn)
+        self.join = join                      # ()
+        self.private = private                # private[i] for i >= 1: volume buffers
+        self.allreduce = allreduce
+
+    def pair(self, x, ys, rs, g):
+        for i, (c, r0, r1) in enumerate(self.items):
+            tgt = g if i == 0 else self.private[i]
+            self.run(i, lambda i=i, c=c, r0=r0, r1=r1, tgt=tgt: (self.forward_rows(i, c, r0, r1, x, ys[c]),
+                                                            self.adjoint_rows(i, c, r0, r1, rs[c], tgt)))
+        self.join()
+        if not self.items:
+            self.zero(g)
+        for i in range(1, len(self.items)):
+            self.accumulate(self.private[i], g)
+        if self.allreduce is not None:
+            self.allreduce(g)

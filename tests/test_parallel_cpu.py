@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1812_03358_b200.parallel import PairRunner, shard
+from paper_1812_03358_b200.parallel import ConcurrentPair, PairRunner, shard
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
@@ -24,7 +24,7 @@ def test_partition_covers_rows_once(world, rows):
         assert (s == 1).all()
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, mode="seq"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,7 +57,14 @@ def _worker(rank, world, port, out):
             g[:] = t.numpy()
 
         items = shard(n_rows, rank, world)
-        runner = PairRunner(items, fwd_rows, adj_rows, lambda g: g.fill(0.0), allreduce)
+        if mode == "seq":
+            runner = PairRunner(items, fwd_rows, adj_rows, lambda g: g.fill(0.0), allreduce)
+        else:  # per-item "streams" are plain calls on CPU; private volumes for items >= 1
+            private = [None] + [np.zeros(ops[0].n_vox) for _ in items[1:]]
+            runner = ConcurrentPair(items, lambda i, c, r0, r1, xv, y: fwd_rows(c, r0, r1, xv, y),
+                                    lambda i, c, r0, r1, r, tgt: adj_rows(c, r0, r1, r, tgt, False),
+                                    lambda src, dst: dst.__iadd__(src), lambda g: g.fill(0.0),
+                                    lambda i, fn: fn(), lambda: None, private, allreduce)
         ys = [np.full(op.n_pix, np.nan) for op in ops]
         g = np.zeros(ops[0].n_vox)
         runner.pair(x, ys, rs, g)
@@ -73,9 +80,49 @@ def _worker(rank, world, port, out):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_gloo_pair_equals_single_process(world):
-    port = 29500 + 7 * world + os.getpid() % 200
+@pytest.mark.parametrize("mode", ["seq", "conc"])
+def test_gloo_pair_equals_single_process(world, mode):
+    port = 29500 + 7 * world + (13 if mode == "conc" else 0) + os.getpid() % 200
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, out, mode), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
+
+
+def test_concurrent_pair_sums_in_item_order():
+    """ConcurrentPair on one process: every item's forward rows, and g = A_0^T r_0 + A_1^T r_1 + ... added
+    in item order -- bitwise the sequential PairRunner result."""
+    from oracle.system import build_system
+    from workloads import make_config, uniform_vector, uniform_volume
+    cfg = make_config("tiny_multi")
+    ops = build_system(cfg)
+    x = uniform_volume(cfg["volume"], 0).astype(np.float64).ravel()
+    rs = [uniform_vector(op.n_pix, 1 + c).astype(np.float64) for c, op in enumerate(ops)]
+    items = [(c, 0, cam["n_t"]) for c, cam in enumerate(cfg["cameras"])]
+    assert len(items) >= 2
+
+    def fwd(c, r0, r1, xv, y):
+        y[:] = ops[c].forward(xv)
+
+    def adj(c, r0, r1, r, g, acc):
+        v = ops[c].adjoint(r)
+        if acc:
+            g += v
+        else:
+            g[:] = v
+
+    ys1 = [np.zeros(op.n_pix) for op in ops]
+    g1 = np.zeros(ops[0].n_vox)
+    PairRunner(items, fwd, adj, lambda g: g.fill(0.0)).pair(x, ys1, rs, g1)
+    order = []
+    ys2 = [np.zeros(op.n_pix) for op in ops]
+    g2 = np.full(ops[0].n_vox, np.nan)
+    private = [None] + [np.full(ops[0].n_vox, np.nan) for _ in items[1:]]
+    ConcurrentPair(items, lambda i, c, r0, r1, xv, y: fwd(c, r0, r1, xv, y),
+                   lambda i, c, r0, r1, r, tgt: adj(c, r0, r1, r, tgt, False),
+                   lambda src, dst: (order.append(id(src)), dst.__iadd__(src)), lambda g: g.fill(0.0),
+                   lambda i, fn: fn(), lambda: None, private).pair(x, ys2, rs, g2)
+    assert order == [id(p) for p in private[1:]]
+    assert np.array_equal(g1, g2)
+    for a, b in zip(ys1, ys2):
+        assert np.array_equal(a, b)
