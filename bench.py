@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-per-view", action="store_true", help="skip the per-view path reference timing")
     ap.add_argument("--one-stream", action="store_true", help="run the rank's cameras one after another on one stream")
+    ap.add_argument("--no-graph", action="store_true", help="launch the timed pairs eagerly instead of as a CUDA graph")
     return ap.parse_args()
 
 
@@ -254,8 +255,9 @@ def run_ours(args, rank, world, local_rank):
                 fn()
 
         def join():
+            cur = torch.cuda.current_stream()
             for s_i in streams:
-                stream.wait_stream(s_i)
+                cur.wait_stream(s_i)
 
         def accumulate(src, dst):
             lfm.vol_accumulate(src, dst)
@@ -278,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
     def step(x_in, g_out):
         launches[0] = 0
         if start is not None:
-            start.record(stream)
+            start.record(torch.cuda.current_stream())
         runner.pair(x_in, ys, rs, g_out)
 
     # dominant kernel: the separable transport of an unrotated camera (one sep_kernel launch per call)
@@ -298,10 +300,23 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # the timed pair as one CUDA graph (captured once after the warm-up: the same kernels, tensor maps and
+    # stream fork/join, replayed without host launch overhead); --no-graph launches it eagerly every step
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(x, g)
+        n_graph_launches = launches[0]
+        graph.replay()
+        torch.cuda.synchronize()
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        step(x, g)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(x, g)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -470,7 +485,8 @@ def run_ours(args, rank, world, local_rank):
                        "views": "%dx%d pillbox" % (cfg["cameras"][0]["k_s"], cfg["cameras"][0]["k_t"]),
                        "path": args.path, "parallelism": "cameras x detector-row tiles over %d rank(s)%s" % (
                            world, ", concurrent per-camera streams" if len(items) > 1 and not args.one_stream else ""),
-                       "l2": "256 MiB write between steps, outside the per-step CUDA events"},
+                       "l2": "256 MiB write between steps, outside the per-step CUDA events",
+                       "launch": "eager" if args.no_graph else "one CUDA graph per pair (captured after warm-up)"},
             "hbm_gbs_alg": pair_bytes / (ms_mean * 1e-3) / 1e9,
             "hbm_frac_of_measured": pair_bytes / (ms_mean * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
             "roofline": roof, "clocks": sm, "gpu_launches": launches[0] * args.steps}
