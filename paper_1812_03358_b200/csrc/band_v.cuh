@@ -37,8 +37,12 @@ struct VCfg {
   static constexpr int A_BYTES = 128 * BK * 4;        // data tile [128][BK] fp32
   static constexpr int B_BYTES = N * BK * 4;          // one weight image [N][BK]
   static constexpr int STAGES = (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES);
-  static constexpr int LAYOUT = BK == 32 ? 2 : 4;     // UMMA K-major 128-byte (BK 32) or 64-byte (BK 16) swizzle
-  static constexpr int SBO = 8 * BK * 4;              // 8-row core-matrix group stride
+  static constexpr int SUB = BK < 32 ? BK : 32;      // sub-block width: one swizzle atom row (BK 64 = 2 sub-blocks)
+  static constexpr int KS = BK / SUB;
+  static constexpr int SUBA = 128 * SUB * 4;          // bytes of one data sub-tile [128][SUB]
+  static constexpr int SUBB = N * SUB * 4;            // bytes of one weight sub-image [N][SUB]
+  static constexpr int LAYOUT = SUB == 32 ? 2 : 4;    // UMMA K-major 128-byte (SUB 32) or 64-byte (SUB 16) swizzle
+  static constexpr int SBO = 8 * SUB * 4;             // 8-row core-matrix group stride
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
   static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
@@ -98,8 +102,11 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
           bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           const int k = __ldg(a.blk_k0 + b);
-          if (DIR == 0) tma_load_3d(st, &a_map, k, mt * 128, n, &full[s]);   // map (vx, vt, n)
-          else tma_load_3d(st, &a_map, k, n, mt * 128, &full[s]);            // map (s, n, vt)
+#pragma unroll
+          for (int j = 0; j < C::KS; ++j) {
+            if (DIR == 0) tma_load_3d(st + j * C::SUBA, &a_map, k + j * C::SUB, mt * 128, n, &full[s]);   // (vx, vt, n)
+            else tma_load_3d(st + j * C::SUBA, &a_map, k + j * C::SUB, n, mt * 128, &full[s]);            // (s, n, vt)
+          }
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -126,12 +133,14 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
             tc_fence_after();
             const uint32_t st = smem_u32(sm + s * C::STAGE);
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t ahi = smem_desc(st + 32 * kk, 16, C::SBO, C::LAYOUT);
-              const uint64_t alo = smem_desc(st + C::A_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
-              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
-              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + 32 * kk, 16, C::SBO, C::LAYOUT);
-              mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kk != 0) ? 1u : 0u);
+            for (int kq = 0; kq < BK / 8; ++kq) {
+              const int sj = kq / (C::SUB / 8), kk = kq % (C::SUB / 8);
+              const uint32_t ao = sj * C::SUBA + 32 * kk, bo = sj * C::SUBB + 32 * kk;
+              const uint64_t ahi = smem_desc(st + ao, 16, C::SBO, C::LAYOUT);
+              const uint64_t alo = smem_desc(st + C::A_BYTES + ao, 16, C::SBO, C::LAYOUT);
+              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + bo, 16, C::SBO, C::LAYOUT);
+              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + bo, 16, C::SBO, C::LAYOUT);
+              mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kq != 0) ? 1u : 0u);
               mma_tf32_ss(d, alo, bhi, IDESC, 1u);
               mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
             }

@@ -263,8 +263,7 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
       T.k0.clear();
       T.img.clear();
       std::vector<char> any(f.n_src + 32);
-      const int row_bytes = BK * 4;
-      const uint32_t smask = BK == 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
+      const uint32_t smask = BK >= 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
       for (int m = 0; m < f.n_tables; ++m)
         for (int t = 0; t < T.n_nt; ++t) {
           T.off[(size_t)m * T.n_nt + t] = (int)T.k0.size();
@@ -290,10 +289,12 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
                 if (e < 0 || e >= f.len[idx]) continue;
                 const float w = (float)f.w64[idx * f.taps + e];
                 const float wh = tf32_host(w), wl = tf32_host(w - wh);
-                uint32_t o = (uint32_t)((r - r0) * row_bytes + kk * 4);
+                const int sub = BK < 32 ? BK : 32, sj = kk / sub;  // sub-images of one swizzle-atom row each
+                uint32_t o = (uint32_t)((r - r0) * sub * 4 + (kk % sub) * 4);
                 o ^= ((o >> 7) & smask) << 4;
-                T.img[base + o / 4] = wh;
-                T.img[base + (size_t)BK * N + o / 4] = wl;
+                const size_t so = (size_t)sj * N * sub;
+                T.img[base + so + o / 4] = wh;
+                T.img[base + (size_t)BK * N + so + o / 4] = wl;
               }
             }
           }
@@ -304,7 +305,7 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
     const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
     build(cp.cf[0], 256, bk_f == 16 ? 16 : 32, cp.vf);
     const int vn_a = std::getenv("LFM_VN_A") ? std::atoi(std::getenv("LFM_VN_A")) : 16;
-    build(cp.ca[0], vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : 32, cp.va);
+    build(cp.ca[0], vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : bk_a == 64 ? 64 : 32, cp.va);
     if (std::getenv("LFM_DEBUG"))
       for (const CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
         int mx = 0, mn = 1 << 30;
@@ -448,8 +449,8 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   if (!cp.va.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const long long ad[3] = {nd, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
-  const int ab[3] = {cp.va.BK, 1, 128};
-  lfm_status st = encode3(&am, Z, ad, as, ab, cp.va.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
+  const int ab[3] = {cp.va.BK < 32 ? cp.va.BK : 32, 1, 128};
+  lfm_status st = encode3(&am, Z, ad, as, ab, cp.va.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
   const int ob[3] = {cp.va.N / 2, 32, 1};
@@ -458,6 +459,7 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   if (cp.va.N == 32)
     return cp.va.BK == 32 ? launch_band_v<32, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
                           : launch_band_v<32, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
+  if (cp.va.BK == 64) return launch_band_v<16, 1, 64>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
   return cp.va.BK == 32 ? launch_band_v<16, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
                         : launch_band_v<16, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
 }
