@@ -303,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
     # the timed pair as one CUDA graph (captured once after the warm-up: the same kernels, tensor maps and
     # stream fork/join, replayed without host launch overhead); --no-graph launches it eagerly every step
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and world == 1:  # multi-rank pairs hold an NCCL all-reduce: launched eagerly
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step(x, g)
@@ -486,7 +486,7 @@ def run_ours(args, rank, world, local_rank):
                        "path": args.path, "parallelism": "cameras x detector-row tiles over %d rank(s)%s" % (
                            world, ", concurrent per-camera streams" if len(items) > 1 and not args.one_stream else ""),
                        "l2": "256 MiB write between steps, outside the per-step CUDA events",
-                       "launch": "eager" if args.no_graph else "one CUDA graph per pair (captured after warm-up)"},
+                       "launch": "eager" if (args.no_graph or world > 1) else "one CUDA graph per pair (captured after warm-up)"},
             "hbm_gbs_alg": pair_bytes / (ms_mean * 1e-3) / 1e9,
             "hbm_frac_of_measured": pair_bytes / (ms_mean * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
             "roofline": roof, "clocks": sm, "gpu_launches": launches[0] * args.steps}
