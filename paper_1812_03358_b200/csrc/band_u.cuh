@@ -41,6 +41,9 @@ struct UArgs {
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
 constexpr int U_THREADS = 384;
+#ifndef U_SPLIT_BATCH
+#define U_SPLIT_BATCH 8  // float4 loads issued together by each split thread (16 per block)
+#endif
 constexpr int U_STAGE_OUT = 4096;  // per epilogue warp: 32 rows x 32 columns fp32, 128-byte swizzle (TMA store)
 constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 8 * U_STAGE_OUT + 1024 + 256;
 
@@ -153,15 +156,21 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         const float4* src = reinterpret_cast<const float4*>(sm + s * U_STAGE_BYTES + 16384);
         float4* lo = reinterpret_cast<float4*>(sm + s * U_STAGE_BYTES + 32768);
 #ifndef BAND_U_NO_SPLIT
-#pragma unroll 4
-        for (int i = 0; i < 16; ++i) {
-          const float4 u = src[t + 64 * i];
-          float4 l;
-          l.x = u.x - __uint_as_float(__float_as_uint(u.x) & 0xffffe000u);
-          l.y = u.y - __uint_as_float(__float_as_uint(u.y) & 0xffffe000u);
-          l.z = u.z - __uint_as_float(__float_as_uint(u.z) & 0xffffe000u);
-          l.w = u.w - __uint_as_float(__float_as_uint(u.w) & 0xffffe000u);
-          lo[t + 64 * i] = l;
+        // all 16 loads first (one shared-memory latency for the block), then the 16 stores
+#pragma unroll
+        for (int h = 0; h < 16 / U_SPLIT_BATCH; ++h) {
+          float4 u[U_SPLIT_BATCH];
+#pragma unroll
+          for (int i = 0; i < U_SPLIT_BATCH; ++i) u[i] = src[t + 64 * (U_SPLIT_BATCH * h + i)];
+#pragma unroll
+          for (int i = 0; i < U_SPLIT_BATCH; ++i) {
+            float4 l;
+            l.x = u[i].x - __uint_as_float(__float_as_uint(u[i].x) & 0xffffe000u);
+            l.y = u[i].y - __uint_as_float(__float_as_uint(u[i].y) & 0xffffe000u);
+            l.z = u[i].z - __uint_as_float(__float_as_uint(u[i].z) & 0xffffe000u);
+            l.w = u[i].w - __uint_as_float(__float_as_uint(u[i].w) & 0xffffe000u);
+            lo[t + 64 * (U_SPLIT_BATCH * h + i)] = l;
+          }
         }
 #endif
         fence_proxy_async_smem();

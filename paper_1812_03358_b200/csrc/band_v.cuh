@@ -165,15 +165,21 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         mbar_wait(&full[s], ph);
         const float4* src = reinterpret_cast<const float4*>(sm + s * C::STAGE);
         float4* lo = reinterpret_cast<float4*>(sm + s * C::STAGE + C::A_BYTES);
+        constexpr int NB = BK / 2, BAT = NB < 8 ? NB : 8;  // float4 per thread, loads issued together
 #pragma unroll
-        for (int i = 0; i < BK / 2; ++i) {
-          const float4 u = src[t + 64 * i];
-          float4 l;
-          l.x = u.x - __uint_as_float(__float_as_uint(u.x) & 0xffffe000u);
-          l.y = u.y - __uint_as_float(__float_as_uint(u.y) & 0xffffe000u);
-          l.z = u.z - __uint_as_float(__float_as_uint(u.z) & 0xffffe000u);
-          l.w = u.w - __uint_as_float(__float_as_uint(u.w) & 0xffffe000u);
-          lo[t + 64 * i] = l;
+        for (int h = 0; h < NB / BAT; ++h) {
+          float4 u[BAT];
+#pragma unroll
+          for (int i = 0; i < BAT; ++i) u[i] = src[t + 64 * (BAT * h + i)];
+#pragma unroll
+          for (int i = 0; i < BAT; ++i) {
+            float4 l;
+            l.x = u[i].x - __uint_as_float(__float_as_uint(u[i].x) & 0xffffe000u);
+            l.y = u[i].y - __uint_as_float(__float_as_uint(u[i].y) & 0xffffe000u);
+            l.z = u[i].z - __uint_as_float(__float_as_uint(u[i].z) & 0xffffe000u);
+            l.w = u[i].w - __uint_as_float(__float_as_uint(u[i].w) & 0xffffe000u);
+            lo[t + 64 * (BAT * h + i)] = l;
+          }
         }
         fence_proxy_async_smem();
         mbar_arrive(&conv[s]);
