@@ -36,7 +36,12 @@ template <int N, int BK>
 struct VCfg {
   static constexpr int A_BYTES = 128 * BK * 4;        // data tile [128][BK] fp32
   static constexpr int B_BYTES = N * BK * 4;          // one weight image [N][BK]
-  static constexpr int STAGES = (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : (200 * 1024) / (2 * A_BYTES + 2 * B_BYTES);
+  static constexpr int EC0 = N >= 256 ? 128 : N / 2;
+  static constexpr int OUT0 = 32 * (EC0 >= 32 ? 32 : EC0) * 4;
+  // staging buffers per epilogue warp: 2 (store i+1 overlaps store i) when the ring keeps >= 2 stages, else 1
+  static constexpr int NOB = (230912 - 16 * OUT0) / (2 * A_BYTES + 2 * B_BYTES) >= 2 ? 2 : 1;
+  static constexpr int RING = 230912 - 8 * NOB * OUT0;  // 227 KB minus alignment slack and barriers
+  static constexpr int STAGES = RING / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : RING / (2 * A_BYTES + 2 * B_BYTES);
   static constexpr int SUB = BK < 32 ? BK : 32;      // sub-block width: one swizzle atom row (BK 64 = 2 sub-blocks)
   static constexpr int KS = BK / SUB;
   static constexpr int SUBA = 128 * SUB * 4;          // bytes of one data sub-tile [128][SUB]
@@ -47,7 +52,8 @@ struct VCfg {
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
   static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
   static constexpr int OUT = 32 * OC * 4;             // staging per warp
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * OUT + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * NOB * OUT + 1024 + 512;
+  static_assert(STAGES >= 2, "band_v: stage too large");
   static constexpr int TCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
 };
 
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
   extern __shared__ uint8_t v_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sout = sm + C::STAGES * C::STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * C::OUT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * C::NOB * C::OUT);
   uint64_t* full = bars;
   uint64_t* conv = bars + C::STAGES;
   uint64_t* empty = bars + 2 * C::STAGES;
@@ -190,7 +196,8 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (voxel rows), columns [h EC, (h+1) EC)
     constexpr int EC = C::EC, OC = C::OC;
     const int q = warp & 3, h = (warp - 4) >> 2;
-    uint8_t* stg = sout + (warp - 4) * C::OUT;
+    uint8_t* stg0 = sout + (warp - 4) * C::NOB * C::OUT;
+    int ob = 0;  // staging buffer of the next store
     int buf = 0;
     uint32_t tph[2] = {0, 0};
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -227,7 +234,8 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
       const int vt0 = mt * 128 + 32 * q, c0 = nt * N + h * EC;
 #pragma unroll
       for (int c = 0; c < EC; c += OC) {
-        if (lane == 0) bulk_wait_read0();
+        uint8_t* stg = stg0 + ob * C::OUT;
+        if (lane == 0) bulk_wait_read<C::NOB - 1>();  // the store that last used this buffer has read it
         __syncwarp();
         if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
 #pragma unroll
@@ -256,6 +264,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           }
           bulk_commit();
         }
+        if (++ob == C::NOB) ob = 0;
       }
     }
     if (lane == 0) bulk_wait0();
