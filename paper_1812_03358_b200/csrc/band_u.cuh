@@ -31,12 +31,26 @@ struct UArgs {
   int n_rows, n_cols;     // output rows (table rows) and columns
   int mt0, n_mt, n_nt;    // row tiles [mt0, mt0 + n_mt), column tiles of 256
   int k_shift;            // source row of TMA coordinate 0 (the row window start)
+  int k_end;              // end of the source row window (k_shift + rows); blocks outside it are skipped
+  int windowed;           // 1: the window is narrower than the source (row-sharded adjoint)
   int group;              // blocks per TMEM accumulator before it is drained
   float scale;
   int accumulate;
   int tile_mode;          // 0: tile = 128 consecutive rows; 1: 2 rows-of-slices (vt) x 64 slices, rows vt*nz + n
   int tm_nz;              // nz for tile_mode 1
 };
+
+// blocks of row tile mt whose 16 source rows intersect the row window (all of them when not windowed)
+__device__ __forceinline__ bool u_live(const UArgs& a, int b) {
+  const int k = __ldg(a.blk_k0 + b);
+  return k + 16 > a.k_shift && k < a.k_end;
+}
+__device__ __forceinline__ int u_nlive(const UArgs& a, int b0, int b1) {
+  if (!a.windowed) return b1 - b0;
+  int n = 0;
+  for (int b = b0; b < b1; ++b) n += u_live(a, b);
+  return n;
+}
 
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
@@ -92,6 +106,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         const bool rev = (mt & 1) != 0;
         for (int j = b0; j < b1; ++j) {
           const int b = rev ? b0 + b1 - 1 - j : j;
+          if (a.windowed && !u_live(a, b)) continue;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * U_STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], 32768);
@@ -112,7 +127,8 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       uint32_t tph[2] = {0, 0};
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int mt = a.mt0 + it / a.n_nt;
-        const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+        const int nl = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
+        const int b0 = 0, b1 = nl;  // live blocks in producer order
         for (int g0 = b0; g0 < b1; g0 += a.group) {
           mbar_wait(&tempty[buf], tph[buf] ^ 1);
           tph[buf] ^= 1;
@@ -150,7 +166,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int mt = a.mt0 + it / a.n_nt;
-      const int nb = __ldg(a.blk_off + mt + 1) - __ldg(a.blk_off + mt);
+      const int nb = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
       for (int b = 0; b < nb; ++b) {
         mbar_wait(&full[s], ph);
         const float4* src = reinterpret_cast<const float4*>(sm + s * U_STAGE_BYTES + 16384);
@@ -185,7 +201,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     uint32_t tph[2] = {0, 0};
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int mt = a.mt0 + it / a.n_nt, nt = it % a.n_nt;
-      const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+      const int b0 = 0, b1 = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
       float acc[128];
 #pragma unroll
       for (int c = 0; c < 128; ++c) acc[c] = 0.f;

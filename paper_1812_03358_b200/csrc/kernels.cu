@@ -2076,6 +2076,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.n_mt = (r1 + 127) / 128 - u.mt0;
     u.n_nt = (op.n_os + 255) / 256;
     u.k_shift = a.win_r0;
+    u.k_end = a.win_r1;
+    u.windowed = a.win_r0 > 0 || a.win_r1 < op.n_it;
     u.group = op.stages > 0 ? op.stages : 4;
     u.scale = op.out_scale * term.scale;
     u.accumulate = accumulate;

@@ -135,7 +135,7 @@ int main(int argc, char** argv) {
     }
     UArgs a;
     a.A = dA; a.blk_off = doff; a.blk_k0 = dk0; a.out = dout; a.out_pitch = p.N; a.n_rows = p.R; a.n_cols = p.N;
-    a.mt0 = 0; a.n_mt = n_mt; a.n_nt = (p.N + 255) / 256; a.k_shift = 0; a.group = cs.group; a.scale = 1.f;
+    a.mt0 = 0; a.n_mt = n_mt; a.n_nt = (p.N + 255) / 256; a.k_shift = 0; a.k_end = p.K; a.windowed = 0; a.group = cs.group; a.scale = 1.f;
     a.accumulate = 0;
     a.tile_mode = 0;
     a.tm_nz = 0;
