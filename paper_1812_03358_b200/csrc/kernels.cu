@@ -2690,7 +2690,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       }
       op.kind = 0;
       // band_u: tcgen05 (one output, one term, normal output, 16-byte source rows); stages = drain group
-      for (int grp : {4}) {
+      for (int grp : {4, 8}) {
         const long long sp = op.src_pitch ? op.src_pitch : op.n_is;
         if (st != LFM_OK || op.ft->u_off.empty() || op.tout || op.n_out != 1 || op.terms.size() != 1 ||
             (sp & 3) || (op.terms[0].src_off & 3) || std::getenv("LFM_NO_TC"))

@@ -64,6 +64,7 @@ VARIANTS = {
     "band_x_nt256_nj4": "256,16,256,1,0,7,4",
     "band_u_g4": "256,128,384,1,0,8,4",
     "band_u_g1": "256,128,384,1,0,8,1",
+    "band_u_g8": "256,128,384,1,0,8,8",
     "band_s_ng8_k64": "128,32,288,1,0,4,3,4,64",
     "band_s_ng8_k16": "128,32,288,1,0,4,6,4,16",
     "band_g_128x32_u8": "128,32,256,1,0,2,8",
