@@ -2712,7 +2712,8 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         }
         if (!ok || cudaGetLastError() != cudaSuccess) continue;
         if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_u group %d: %.3f ms\n", names[q], grp, tot / 2);
-        if (tot < best) { best = tot; bts = 256; btt = 128; bnt = U_THREADS; bnb = 1; bst = 0; bkind = 8; bstages = grp; bmgrp = 4; }
+        // the second drain group must win by 2 % (ties otherwise flip between runs)
+        if (tot < (grp == 4 ? best : 0.98f * best)) { best = tot; bts = 256; btt = 128; bnt = U_THREADS; bnb = 1; bst = 0; bkind = 8; bstages = grp; bmgrp = 4; }
       }
       op.kind = 0;
       // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)
