@@ -374,10 +374,38 @@ lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
 }
 
 // ---------------------------------------------------------------------------------------------- band_v host side
+// Tensor-map cache (per host thread): the maps depend only on (base, dims, strides, box, swizzle), and the same
+// buffers come back every call, so an apply call re-encodes nothing after its first use (host launch overhead).
+struct TmapKey {
+  const void* base;
+  long long v[11];
+};
+struct TmapEntry {
+  TmapKey key;
+  CUtensorMap map;
+};
+static std::vector<TmapEntry>& tmap_cache() {
+  thread_local std::vector<TmapEntry> cache;
+  return cache;
+}
+static bool tmap_lookup(const TmapKey& k, CUtensorMap* out) {
+  for (const TmapEntry& e : tmap_cache())
+    if (e.key.base == k.base && std::memcmp(e.key.v, k.v, sizeof(k.v)) == 0) {
+      *out = e.map;
+      return true;
+    }
+  return false;
+}
+static void tmap_insert(const TmapKey& k, const CUtensorMap& m) {
+  std::vector<TmapEntry>& c = tmap_cache();
+  if (c.size() >= 64) c.erase(c.begin());  // bounded: oldest first
+  c.push_back({k, m});
+}
+
 typedef CUresult (*EncodeTiledFnV)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static lfm_status encode3(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
+static lfm_status encode3_raw(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
                           const int box[3], CUtensorMapSwizzle swz, std::string& err) {
   static EncodeTiledFnV encode = nullptr;
   if (!encode) {
@@ -402,6 +430,15 @@ static lfm_status encode3(CUtensorMap* map, const float* base, const long long d
     return LFM_E_CUDA;
   }
   return LFM_OK;
+}
+
+static lfm_status encode3(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
+                          const int box[3], CUtensorMapSwizzle swz, std::string& err) {
+  const TmapKey k = {base, {3, dims[0], dims[1], dims[2], strides[0], strides[1], box[0], box[1], box[2], (long long)swz, 0}};
+  if (tmap_lookup(k, map)) return LFM_OK;
+  lfm_status st = encode3_raw(map, base, dims, strides, box, swz, err);
+  if (st == LFM_OK) tmap_insert(k, *map);
+  return st;
 }
 
 template <int N, int DIR, int BK>
@@ -1900,8 +1937,18 @@ lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
+                                 int box_r, CUtensorMapSwizzle swz, std::string& err);
 static lfm_status encode_map(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
                              int box_r, CUtensorMapSwizzle swz, std::string& err) {
+  const TmapKey k = {base, {2, cols, rows, pitch, box_c, box_r, (long long)swz, 0, 0, 0, 0}};
+  if (tmap_lookup(k, map)) return LFM_OK;
+  lfm_status st = encode_map_raw(map, base, cols, rows, pitch, box_c, box_r, swz, err);
+  if (st == LFM_OK) tmap_insert(k, *map);
+  return st;
+}
+static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
+                                 int box_r, CUtensorMapSwizzle swz, std::string& err) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
