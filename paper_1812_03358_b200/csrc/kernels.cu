@@ -2229,40 +2229,84 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 }
 
 // ------------------------------------------------------------------------------------------
-// Shear pass: out[i] = sum_k w[line][k] * in[pos + mlo[line] + k along the pass axis].  3D grid (x tiles of 32,
-// y tiles of 8, z): no 64-bit divisions; consecutive threads on consecutive x (coalesced rows).
+// Shear pass: out[i] = sum_k w[line][k] * in[pos + mlo[line] + k along the pass axis].  3D grid: x tiles of 32
+// threads (coalesced rows), y tiles of 8, z chunks of SH_ZC; each thread walks SH_ZC voxels along z with the
+// table and data loads of all of them in flight together (the pass is latency-bound, 8 B of HBM per voxel).
+constexpr int SH_ZC = 8;
 template <int TAPS>
 __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     const int32_t* __restrict__ mlo, const float* __restrict__ w,
                                                     int axis, int nx, int ny, int nz, int accumulate) {
-  const int ix = blockIdx.x * 32 + threadIdx.x, iy = blockIdx.y * 8 + threadIdx.y, iz = blockIdx.z;
+  const int ix = blockIdx.x * 32 + threadIdx.x, iy = blockIdx.y * 8 + threadIdx.y, z0 = blockIdx.z * SH_ZC;
   if (ix >= nx || iy >= ny) return;
-  const size_t idx = ((size_t)iz * ny + iy) * nx + ix;
-  int line, pos, n;
-  size_t stride;
-  if (axis == 0) { line = ix + nx * iy; pos = iz; n = nz; stride = (size_t)nx * ny; }
-  else if (axis == 1) { line = iy + ny * iz; pos = ix; n = nx; stride = 1; }
-  else { line = ix + nx * iz; pos = iy; n = ny; stride = nx; }
-  const int m0 = __ldg(mlo + line);
-  const float* wl = w + (size_t)line * TAPS;
-  const float* src = in + idx - (size_t)pos * stride;  // start of this voxel's line
-  float acc = 0.f;
+  const size_t plane = (size_t)nx * ny;
+  float res[SH_ZC];
+  if (axis == 0) {
+    // z pass: one line (x, y) per thread, so the shift and the weights are loaded once and the input column is
+    // read as one sliding window of SH_ZC + TAPS - 1 values (each input value loaded once, not TAPS times)
+    const int line = ix + nx * iy;
+    const int m0 = __ldg(mlo + line);
+    float wk[TAPS];
 #pragma unroll
-  for (int k = 0; k < TAPS; k += 4) {
-    const float4 w4 = __ldg(reinterpret_cast<const float4*>(wl + k));
-    const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = pos + m0 + k + q;
-      if (j >= 0 && j < n) acc = fmaf(wk[q], __ldg(src + (size_t)j * stride), acc);
+    for (int k = 0; k < TAPS; k += 4) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4*>(w + (size_t)line * TAPS + k));
+      wk[k] = w4.x; wk[k + 1] = w4.y; wk[k + 2] = w4.z; wk[k + 3] = w4.w;
     }
+    const float* col = in + (size_t)iy * nx + ix;
+    float win[SH_ZC + TAPS - 1];
+#pragma unroll
+    for (int i = 0; i < SH_ZC + TAPS - 1; ++i) {
+      const int j = z0 + m0 + i;
+      win[i] = (j >= 0 && j < nz) ? __ldg(col + (size_t)j * plane) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < SH_ZC; ++q) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < TAPS; ++k) acc = fmaf(wk[k], win[q + k], acc);
+      res[q] = acc;
+    }
+  } else {
+#pragma unroll
+  for (int q = 0; q < SH_ZC; ++q) {
+    const int iz = z0 + q;
+    res[q] = 0.f;
+    if (iz >= nz) continue;
+    const size_t idx = (size_t)iz * plane + (size_t)iy * nx + ix;
+    int line, pos, n;
+    size_t stride;
+    if (axis == 0) { line = ix + nx * iy; pos = iz; n = nz; stride = plane; }
+    else if (axis == 1) { line = iy + ny * iz; pos = ix; n = nx; stride = 1; }
+    else { line = ix + nx * iz; pos = iy; n = ny; stride = nx; }
+    const int m0 = __ldg(mlo + line);
+    const float* wl = w + (size_t)line * TAPS;
+    const float* src = in + idx - (size_t)pos * stride;  // start of this voxel's line
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < TAPS; k += 4) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4*>(wl + k));
+      const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = pos + m0 + k + t;
+        if (j >= 0 && j < n) acc = fmaf(wk[t], __ldg(src + (size_t)j * stride), acc);
+      }
+    }
+    res[q] = acc;
   }
-  out[idx] = accumulate ? out[idx] + acc : acc;
+  }
+#pragma unroll
+  for (int q = 0; q < SH_ZC; ++q) {
+    const int iz = z0 + q;
+    if (iz >= nz) break;
+    const size_t idx = (size_t)iz * plane + (size_t)iy * nx + ix;
+    out[idx] = accumulate ? out[idx] + res[q] : res[q];
+  }
 }
 
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
-  dim3 grid((nx + 31) / 32, (ny + 7) / 8, nz), blk(32, 8);
+  dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + SH_ZC - 1) / SH_ZC), blk(32, 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (sp.taps == 4)
     shear_kernel<4><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
