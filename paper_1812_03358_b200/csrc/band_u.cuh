@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_tf32(128, 256, 0, 1);
+      const uint64_t dA0 = smem_desc(smem_u32(sm), 16, 512, 4);            // weights, K-major 64-byte swizzle
+      const uint64_t dB0 = smem_desc(smem_u32(sm) + 16384, 2048, 512, 1);  // source, MN-major 128B/32B-atom
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
@@ -138,13 +140,14 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
           for (int j = g0; j < g1; ++j) {
             mbar_wait(&conv[s], ph);
             tc_fence_after();
-            const uint32_t st = smem_u32(sm + s * U_STAGE_BYTES);
+            // descriptors = the stage-0 ones plus the start-address offset (16-byte units, low field; no carry)
+            const uint64_t so = (uint64_t)((s * U_STAGE_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
-              const uint64_t ahi = smem_desc(st + 32 * kk, 16, 512, 4);
-              const uint64_t alo = smem_desc(st + 8192 + 32 * kk, 16, 512, 4);
-              const uint64_t bhi = smem_desc(st + 16384 + 1024 * kk, 2048, 512, 1);
-              const uint64_t blo = smem_desc(st + 32768 + 1024 * kk, 2048, 512, 1);
+              const uint64_t ahi = dA0 + so + 2 * kk;
+              const uint64_t alo = dA0 + so + (8192 >> 4) + 2 * kk;
+              const uint64_t bhi = dB0 + so + 64 * kk;
+              const uint64_t blo = dB0 + so + (16384 >> 4) + 64 * kk;
               mma_tf32_ss(d, alo, bhi, IDESC, (j != g0 || kk != 0) ? 1u : 0u);
 #ifndef BAND_U_TWO_PRODUCTS
               mma_tf32_ss(d, ahi, blo, IDESC, 1u);

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
+      const uint64_t d0 = smem_desc(smem_u32(sm), 16, C::SBO, C::LAYOUT);  // all operands K-major, same swizzle
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
@@ -137,15 +138,15 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           for (int j = g0; j < g1; ++j) {
             mbar_wait(&conv[s], ph);
             tc_fence_after();
-            const uint32_t st = smem_u32(sm + s * C::STAGE);
+            const uint64_t so = (uint64_t)((s * C::STAGE) >> 4);  // stage offset in the descriptors' address field
 #pragma unroll
             for (int kq = 0; kq < BK / 8; ++kq) {
               const int sj = kq / (C::SUB / 8), kk = kq % (C::SUB / 8);
-              const uint32_t ao = sj * C::SUBA + 32 * kk, bo = sj * C::SUBB + 32 * kk;
-              const uint64_t ahi = smem_desc(st + ao, 16, C::SBO, C::LAYOUT);
-              const uint64_t alo = smem_desc(st + C::A_BYTES + ao, 16, C::SBO, C::LAYOUT);
-              const uint64_t bhi = smem_desc(st + 2 * C::A_BYTES + bo, 16, C::SBO, C::LAYOUT);
-              const uint64_t blo = smem_desc(st + 2 * C::A_BYTES + C::B_BYTES + bo, 16, C::SBO, C::LAYOUT);
+              const uint64_t ao = (uint64_t)((sj * C::SUBA + 32 * kk) >> 4), bo = (uint64_t)((sj * C::SUBB + 32 * kk) >> 4);
+              const uint64_t ahi = d0 + so + ao;
+              const uint64_t alo = d0 + so + (C::A_BYTES >> 4) + ao;
+              const uint64_t bhi = d0 + so + ((2 * C::A_BYTES) >> 4) + bo;
+              const uint64_t blo = d0 + so + ((2 * C::A_BYTES + C::B_BYTES) >> 4) + bo;
               mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kq != 0) ? 1u : 0u);
               mma_tf32_ss(d, alo, bhi, IDESC, 1u);
               mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
