@@ -10,7 +10,8 @@
 // producer bulk-copies the images and loads the data tile [128 vt][BK k] with one 3D TMA (same swizzle = the
 // same UMMA layout), the split warps write
 // A_lo = A - trunc(A), the MMA thread issues per 8-wide k-step  D += A_hi B_lo + A_lo B_hi + A_hi B_hi
-// (M128 N K8), and every `group` blocks the TMEM accumulator is drained into fp32 registers (the accumulator
+// (M128 N K8; for N <= 128 as two MMAs, A_hi [B_hi; B_lo] with N' = 2N and A_lo B_hi, the halves summed in the
+// drain), and every `group` blocks the TMEM accumulator is drained into fp32 registers (the accumulator
 // truncates, see band_u.cuh).  The epilogue writes through shared memory and 3D TMA stores (U: boxes of
 // 32 s x 32 vt; x: 8 vx x 32 vt), or TMA reduce-adds when accumulating.  Warp roles as in band_u.
 #pragma once
@@ -54,7 +55,15 @@ struct VCfg {
   static constexpr int OUT = 32 * OC * 4;             // staging per warp
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * NOB * OUT + 1024 + 512;
   static_assert(STAGES >= 2, "band_v: stage too large");
-  static constexpr int TCOLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
+#ifndef BAND_V_NO_MERGE
+  // merged products (N <= 128, one sub-block per stage): the hi and lo weight images are consecutive K-major
+  // row groups, so [B_hi; B_lo] is one N' = 2N operand and A_hi B_hi, A_hi B_lo come from one MMA (A_hi read once)
+  static constexpr bool MERGE = N <= 128 && KS == 1;
+#else
+  static constexpr bool MERGE = false;
+#endif
+  static constexpr int ACC = MERGE ? 2 * N : N;      // TMEM columns per accumulator
+  static constexpr int TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
 };
 
 template <int N, int DIR, int BK>
@@ -120,6 +129,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
+      constexpr uint32_t IDESC2 = idesc_tf32(128, C::MERGE ? 2 * N : N, 0, 0);
       const uint64_t d0 = smem_desc(smem_u32(sm), 16, C::SBO, C::LAYOUT);  // all operands K-major, same swizzle
       int s = 0;
       uint32_t ph = 0;
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           mbar_wait(&tempty[buf], tph[buf] ^ 1);
           tph[buf] ^= 1;
           tc_fence_after();
-          const uint32_t d = tmem + buf * N;
+          const uint32_t d = tmem + buf * C::ACC;
           const int g1 = min(b1, g0 + a.group);
           for (int j = g0; j < g1; ++j) {
             mbar_wait(&conv[s], ph);
@@ -147,9 +157,15 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
               const uint64_t alo = d0 + so + (C::A_BYTES >> 4) + ao;
               const uint64_t bhi = d0 + so + ((2 * C::A_BYTES) >> 4) + bo;
               const uint64_t blo = d0 + so + ((2 * C::A_BYTES + C::B_BYTES) >> 4) + bo;
-              mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kq != 0) ? 1u : 0u);
-              mma_tf32_ss(d, alo, bhi, IDESC, 1u);
-              mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
+              if constexpr (C::MERGE) {
+                // D[:, 0:N] += A_hi B_hi, D[:, N:2N] += A_hi B_lo (one MMA), then D[:, 0:N] += A_lo B_hi
+                mma_tf32_ss(d, ahi, bhi, IDESC2, (j != g0 || kq != 0) ? 1u : 0u);
+                mma_tf32_ss(d, alo, bhi, IDESC, 1u);
+              } else {
+                mma_tf32_ss(d, ahi, blo, IDESC, (j != g0 || kq != 0) ? 1u : 0u);
+                mma_tf32_ss(d, alo, bhi, IDESC, 1u);
+                mma_tf32_ss(d, ahi, bhi, IDESC, 1u);
+              }
             }
             tc_commit(&empty[s]);
             if (++s == C::STAGES) { s = 0; ph ^= 1; }
@@ -212,20 +228,23 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         mbar_wait(&tfull[buf], tph[buf]);
         tph[buf] ^= 1;
         tc_fence_after();
-        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * N + h * EC;
-        if constexpr (EC >= 16) {
+        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * C::ACC + h * EC;
 #pragma unroll
-          for (int c = 0; c < EC; c += 16) {
-            float v[16];
-            tmem_ld16(base + c, v);
+        for (int part = 0; part < (C::MERGE ? 2 : 1); ++part) {  // merged: the A_hi B_lo half at column + N
+          if constexpr (EC >= 16) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+            for (int c = 0; c < EC; c += 16) {
+              float v[16];
+              tmem_ld16(base + part * N + c, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+            }
+          } else {
+            float v[EC];
+            tmem_ld_n<EC>(base + part * N, v);
+#pragma unroll
+            for (int i = 0; i < EC; ++i) acc[i] += v[i];
           }
-        } else {
-          float v[EC];
-          tmem_ld_n<EC>(base, v);
-#pragma unroll
-          for (int i = 0; i < EC; ++i) acc[i] += v[i];
         }
         tc_fence_before();
         __syncwarp();
