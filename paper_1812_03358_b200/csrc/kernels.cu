@@ -2232,8 +2232,7 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 // Shear pass: out[i] = sum_k w[line][k] * in[pos + mlo[line] + k along the pass axis].  3D grid: x tiles of 32
 // threads (coalesced rows), y tiles of 8, z chunks of SH_ZC; each thread walks SH_ZC voxels along z with the
 // table and data loads of all of them in flight together (the pass is latency-bound, 8 B of HBM per voxel).
-constexpr int SH_ZC = 8;
-template <int TAPS>
+template <int TAPS, int SH_ZC>
 __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     const int32_t* __restrict__ mlo, const float* __restrict__ w,
                                                     int axis, int nx, int ny, int nz, int accumulate) {
@@ -2306,14 +2305,28 @@ __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in
 
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
-  dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + SH_ZC - 1) / SH_ZC), blk(32, 8);
+  // z chunk per thread: the z pass reads a sliding window of ZC + TAPS - 1 values per ZC outputs, so longer
+  // chunks cut its re-reads and its block count (B200 bench: 16 -> +1.5 % pairs/s, 32 -> +1.3 %, the rotation
+  // alone unchanged at ~20 us, so the gain is overlap with the other camera); the in-plane passes keep 8
+  static const int zc_z = std::getenv("LFM_SH_ZC") ? std::atoi(std::getenv("LFM_SH_ZC")) : 16;
+  const int zc = sp.axis == 0 && (zc_z == 16 || zc_z == 32) ? zc_z : 8;  // instantiated chunks only
+  dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + zc - 1) / zc), blk(32, 8);
   cudaStream_t s = (cudaStream_t)stream;
-  if (sp.taps == 4)
-    shear_kernel<4><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
-  else if (sp.taps == 8)
-    shear_kernel<8><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
-  else
-    shear_kernel<16><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate);
+#define LFM_SHEAR(T, Z) shear_kernel<T, Z><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate)
+  if (zc == 16) {
+    if (sp.taps == 4) LFM_SHEAR(4, 16);
+    else if (sp.taps == 8) LFM_SHEAR(8, 16);
+    else LFM_SHEAR(16, 16);
+  } else if (zc == 32) {
+    if (sp.taps == 4) LFM_SHEAR(4, 32);
+    else if (sp.taps == 8) LFM_SHEAR(8, 32);
+    else LFM_SHEAR(16, 32);
+  } else {
+    if (sp.taps == 4) LFM_SHEAR(4, 8);
+    else if (sp.taps == 8) LFM_SHEAR(8, 8);
+    else LFM_SHEAR(16, 8);
+  }
+#undef LFM_SHEAR
   ++g_launches;
   return cuda_check(cudaGetLastError(), "shear_kernel launch", err);
 }
