@@ -2303,6 +2303,59 @@ __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in
   }
 }
 
+// x pass (axis 1, the line runs along the contiguous axis, one shift m0 and one weight row per line): each thread
+// owns 4 consecutive x of one line, loads the aligned float4 window that covers them plus the taps
+// (ceil((TAPS + 6) / 4) LDG.128 instead of 4 TAPS scalar loads) and stores one float4.  Same FMA order as
+// shear_kernel (taps ascending; out-of-range taps contribute exact zeros), so the results are identical.
+template <int TAPS, int ZC>
+__global__ void __launch_bounds__(256) shear_x4_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                       const int32_t* __restrict__ mlo, const float* __restrict__ w,
+                                                       int nx, int ny, int nz, int accumulate) {
+  constexpr int NV4 = (TAPS + 6 + 3) / 4;
+  const int x4 = 4 * (blockIdx.x * 32 + threadIdx.x), iy = blockIdx.y * 8 + threadIdx.y, z0 = blockIdx.z * ZC;
+  if (x4 >= nx || iy >= ny) return;
+#pragma unroll 2
+  for (int q = 0; q < ZC; ++q) {
+    const int iz = z0 + q;
+    if (iz >= nz) break;
+    const int line = iy + ny * iz;
+    const int m0 = __ldg(mlo + line);
+    const int a = x4 + (m0 & ~3), r = m0 & 3;  // aligned window start (floor) and offset in it
+    const float* row = in + ((size_t)iz * ny + iy) * nx;
+    float v[4 * NV4];
+#pragma unroll
+    for (int i = 0; i < NV4; ++i) {
+      const int j = a + 4 * i;
+      const float4 t = (j >= 0 && j < nx) ? __ldg(reinterpret_cast<const float4*>(row + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+    }
+    float u[TAPS + 3];
+#pragma unroll
+    for (int j = 0; j < TAPS + 3; ++j) u[j] = r == 0 ? v[j] : r == 1 ? v[j + 1] : r == 2 ? v[j + 2] : v[j + 3];
+    float wk[TAPS];
+#pragma unroll
+    for (int k = 0; k < TAPS; k += 4) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4*>(w + (size_t)line * TAPS + k));
+      wk[k] = w4.x; wk[k + 1] = w4.y; wk[k + 2] = w4.z; wk[k + 3] = w4.w;
+    }
+    float res[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < TAPS; ++k) acc = fmaf(wk[k], u[i + k], acc);
+      res[i] = acc;
+    }
+    float4* o = reinterpret_cast<float4*>(out + ((size_t)iz * ny + iy) * nx + x4);
+    float4 r4 = make_float4(res[0], res[1], res[2], res[3]);
+    if (accumulate) {
+      const float4 p = *o;
+      r4.x += p.x; r4.y += p.y; r4.z += p.z; r4.w += p.w;
+    }
+    *o = r4;
+  }
+}
+
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
   // z chunk per thread: the z pass reads a sliding window of ZC + TAPS - 1 values per ZC outputs, so longer
@@ -2310,6 +2363,19 @@ lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* ou
   // alone unchanged at ~20 us, so the gain is overlap with the other camera); the in-plane passes keep 8
   static const int zc_z = std::getenv("LFM_SH_ZC") ? std::atoi(std::getenv("LFM_SH_ZC")) : 16;
   const int zc = sp.axis == 0 && (zc_z == 16 || zc_z == 32) ? zc_z : 8;  // instantiated chunks only
+  static const bool x4_off = std::getenv("LFM_SH_X4") && std::atoi(std::getenv("LFM_SH_X4")) == 0;
+  if (sp.axis == 1 && !x4_off && nx % 4 == 0 && ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+    dim3 grid4((nx / 4 + 31) / 32, (ny + 7) / 8, (nz + 7) / 8), blk4(32, 8);
+    cudaStream_t s4 = (cudaStream_t)stream;
+    if (sp.taps == 4)
+      shear_x4_kernel<4, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    else if (sp.taps == 8)
+      shear_x4_kernel<8, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    else
+      shear_x4_kernel<16, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "shear_x4_kernel launch", err);
+  }
   dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + zc - 1) / zc), blk(32, 8);
   cudaStream_t s = (cudaStream_t)stream;
 #define LFM_SHEAR(T, Z) shear_kernel<T, Z><<<grid, blk, 0, s>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], sp.axis, nx, ny, nz, accumulate)
