@@ -2314,7 +2314,7 @@ __global__ void __launch_bounds__(256) shear_x4_kernel(const float* __restrict__
   constexpr int NV4 = (TAPS + 6 + 3) / 4;
   const int x4 = 4 * (blockIdx.x * 32 + threadIdx.x), iy = blockIdx.y * 8 + threadIdx.y, z0 = blockIdx.z * ZC;
   if (x4 >= nx || iy >= ny) return;
-#pragma unroll 2
+#pragma unroll
   for (int q = 0; q < ZC; ++q) {
     const int iz = z0 + q;
     if (iz >= nz) break;
@@ -2363,16 +2363,23 @@ lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* ou
   // alone unchanged at ~20 us, so the gain is overlap with the other camera); the in-plane passes keep 8
   static const int zc_z = std::getenv("LFM_SH_ZC") ? std::atoi(std::getenv("LFM_SH_ZC")) : 16;
   const int zc = sp.axis == 0 && (zc_z == 16 || zc_z == 32) ? zc_z : 8;  // instantiated chunks only
-  static const bool x4_off = std::getenv("LFM_SH_X4") && std::atoi(std::getenv("LFM_SH_X4")) == 0;
-  if (sp.axis == 1 && !x4_off && nx % 4 == 0 && ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0) {
-    dim3 grid4((nx / 4 + 31) / 32, (ny + 7) / 8, (nz + 7) / 8), blk4(32, 8);
+  // LFM_SH_X4: 0 = scalar shear_kernel, 1 = x4 with 8 z per thread, 2 = 4 z, 3 = 16 z, 4 (default) = 2 z, 5 = 1 z
+  // (B200, 128^3 yaw camera, rotation fwd per direction: scalar 20.5 us, 16 z 22.6, 8 z 16.4, 4 z 13.2, 2 z 12.6,
+  // 1 z 12.4; bench 2081 / 2089 / 2141 / 2169 / 2183 / 2180 pairs/s)
+  static const int x4_mode = std::getenv("LFM_SH_X4") ? std::atoi(std::getenv("LFM_SH_X4")) : 4;
+  if (sp.axis == 1 && x4_mode > 0 && nx % 4 == 0 && ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+    const int zx = x4_mode == 2 ? 4 : x4_mode == 3 ? 16 : x4_mode == 4 ? 2 : x4_mode == 5 ? 1 : 8;
+    dim3 grid4((nx / 4 + 31) / 32, (ny + 7) / 8, (nz + zx - 1) / zx), blk4(32, 8);
     cudaStream_t s4 = (cudaStream_t)stream;
-    if (sp.taps == 4)
-      shear_x4_kernel<4, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
-    else if (sp.taps == 8)
-      shear_x4_kernel<8, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
-    else
-      shear_x4_kernel<16, 8><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+#define LFM_SHX4(T, Z) shear_x4_kernel<T, Z><<<grid4, blk4, 0, s4>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate)
+#define LFM_SHX4_T(Z) if (sp.taps == 4) LFM_SHX4(4, Z); else if (sp.taps == 8) LFM_SHX4(8, Z); else LFM_SHX4(16, Z)
+    if (zx == 4) { LFM_SHX4_T(4); }
+    else if (zx == 2) { LFM_SHX4_T(2); }
+    else if (zx == 1) { LFM_SHX4_T(1); }
+    else if (zx == 16) { LFM_SHX4_T(16); }
+    else { LFM_SHX4_T(8); }
+#undef LFM_SHX4_T
+#undef LFM_SHX4
     ++g_launches;
     return cuda_check(cudaGetLastError(), "shear_x4_kernel launch", err);
   }
