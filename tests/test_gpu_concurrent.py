@@ -19,6 +19,12 @@ def test_vol_accumulate():
     lfm.vol_accumulate(a, b)
     torch.cuda.synchronize()
     assert torch.equal(b.cpu(), ref)
+    # 4-byte offset views: the scalar kernel instead of the float4 one, same result
+    a1, b1 = a[1:], b[1:]
+    ref1 = (a1 + b1).cpu()
+    lfm.vol_accumulate(a1, b1)
+    torch.cuda.synchronize()
+    assert torch.equal(b1.cpu(), ref1)
     with pytest.raises(lfm.LfmError):
         lfm.vol_accumulate(a, a)
 
