@@ -224,7 +224,10 @@ lfm_status lfm_pwls_gains(lfm_plan p, const double* stats_dev, double* gamma_dev
  * [sum_c 1/2||.||^2_W, nu*sum x + R(x)].  Ax[c], y[c], w[c] are device pointers per camera.
  * subset >= 0: the view-subset gradient of eqn,subset (reading Z19): A_c^T is replaced by
  * (K/|S|) sum_{k in S} A_ck^T and Ax[c] must be the subset prediction of lfm_A_forward_subset; `path`
- * is then ignored.  subset < 0: the exact gradient on `path`. */
+ * is then ignored.  subset < 0: the exact gradient on `path`.
+ * Non-finite cost: when cost_dev is non-NULL (and `stream` is not capturing a graph) the call
+ * waits for the stream, reads the cost and returns LFM_E_NONFINITE if either part is NaN or infinite (grad and
+ * cost_dev are still written).  Pass cost_dev = NULL for a call that never synchronises. */
 lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, const float* x,
                          const float* const* y, const float* const* w, const float* const* Ax,
                          const double* gamma_dev, float beta, float nu, int include_reg,

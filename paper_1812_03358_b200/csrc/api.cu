@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -26,6 +27,21 @@ lfm_status fail(lfm_status s, const std::string& msg) {
 }
 
 size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Apply calls run on the plan's device: switch to it for the call (kernel attributes, SM counts and tensor maps
+// are per device) and restore the caller's current device afterwards.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const lfm_plan_s* p) {
+    if (!p || p->device < 0) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); return; }
+    if (cur != p->device && cudaSetDevice(p->device) == cudaSuccess) prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 struct WsLayout {
   size_t r0, r1, xt, f, s, s2, z, zt, p, total;
@@ -381,6 +397,7 @@ lfm_status lfm_plan_export_table(lfm_plan p, int cam, int table_id, int axis, in
 
 lfm_status lfm_lf_transport(lfm_plan p, int cam, int dst_plane, int src_plane, const float* src, float* dst,
                             void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -420,6 +437,7 @@ lfm_status lfm_vol_accumulate(const float* src, float* dst, long long n, void* s
 
 lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* out, int accumulate, void* ws,
                           size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -441,6 +459,7 @@ lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* 
 
 lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* x, float* y,
                               void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -456,6 +475,7 @@ lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1,
 
 lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* out, void* ws, size_t ws_bytes,
                        void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -486,6 +506,7 @@ static lfm_status check_subset(lfm_plan p, int cam, int subset) {
 
 lfm_status lfm_A_forward_subset(lfm_plan p, int cam, int subset, const float* x, float* y, void* ws, size_t ws_bytes,
                                 void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_subset(p, cam, subset);
   if (st != LFM_OK) return st;
@@ -499,6 +520,7 @@ lfm_status lfm_A_forward_subset(lfm_plan p, int cam, int subset, const float* x,
 
 lfm_status lfm_A_adjoint_subset(lfm_plan p, int cam, int subset, const float* y, float* x, int accumulate, void* ws,
                                 size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_subset(p, cam, subset);
   if (st != LFM_OK) return st;
@@ -519,6 +541,7 @@ lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y
 
 lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
                               int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -541,6 +564,7 @@ lfm_status lfm_A_adjoint(lfm_plan p, int cam, int path, const float* y, float* x
 
 lfm_status lfm_pwls_stats(lfm_plan p, int cam, const float* Ax, const float* y, const float* w_, double* stats3,
                           void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
@@ -554,6 +578,7 @@ lfm_status lfm_pwls_stats(lfm_plan p, int cam, const float* Ax, const float* y, 
 }
 
 lfm_status lfm_pwls_gains(lfm_plan p, const double* stats, double* gamma, int* flag, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
   if (!stats || !gamma) return fail(LFM_E_INVALID, "NULL argument");
@@ -566,6 +591,7 @@ lfm_status lfm_pwls_gains(lfm_plan p, const double* stats, double* gamma, int* f
 lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, const float* x, const float* const* y,
                          const float* const* wts, const float* const* Ax, const double* gamma, float beta, float nu,
                          int include_reg, float* grad, double* cost, void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
   if (cam0 < 0 || cam1 > (int)p->cams.size() || cam0 > cam1) return fail(LFM_E_INVALID, "bad camera range");
@@ -597,11 +623,31 @@ lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, c
     cudaMemsetAsync(cost + 1, 0, sizeof(double), (cudaStream_t)stream);
   }
   g_last_launches = g_launches;
-  return cuda_check(cudaGetLastError(), "pwls_grad", err) == LFM_OK ? LFM_OK : fail(LFM_E_CUDA, err);
+  if (cuda_check(cudaGetLastError(), "pwls_grad", err) != LFM_OK) return fail(LFM_E_CUDA, err);
+  // non-finite cost: when the cost is requested (and the stream is not being captured into a graph)
+  // the call waits for it and checks both parts
+  if (cost) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      double h[2] = {0.0, 0.0};
+      if (cuda_check(cudaMemcpyAsync(h, cost, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream), "cost copy", err) !=
+              LFM_OK ||
+          cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "cost sync", err) != LFM_OK)
+        return fail(LFM_E_CUDA, err);
+      if (!std::isfinite(h[0]) || !std::isfinite(h[1]))
+        return fail(LFM_E_NONFINITE, "non-finite cost: data term " + std::to_string(h[0]) + ", prior term " +
+                                         std::to_string(h[1]) + " (cameras " + std::to_string(cam0) + ".." +
+                                         std::to_string(cam1 - 1) + ")");
+    } else {
+      cudaGetLastError();
+    }
+  }
+  return LFM_OK;
 }
 
 lfm_status lfm_majoriser(lfm_plan p, int path, int cam0, int cam1, const float* const* wts, float beta, int mode,
                          float* d, void* ws, size_t ws_bytes, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
   if (cam0 < 0 || cam1 > (int)p->cams.size() || cam0 > cam1) return fail(LFM_E_INVALID, "bad camera range");
@@ -632,6 +678,7 @@ lfm_status lfm_majoriser(lfm_plan p, int path, int cam0, int cam1, const float* 
 
 lfm_status lfm_fista_update(lfm_plan p, float* x, float* z, const float* grad, const float* d, double t_old,
                             double t_new, void* stream) {
+  DevGuard dev_guard(p);
   g_launches = 0;
   if (!p || p->device < 0) return fail(LFM_E_INVALID, "plan is NULL or host-only");
   if (!x || !z || !grad || !d) return fail(LFM_E_INVALID, "NULL argument");

@@ -31,6 +31,13 @@ namespace lfm {
 
 thread_local int g_launches = 0;
 static int g_num_sms();
+// Kernel attributes (dynamic shared memory limits) belong to a device context: one-time flags are kept per device.
+constexpr int LFM_MAX_DEV = 64;
+static int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < LFM_MAX_DEV) ? d : 0;
+}
 
 lfm_status cuda_check(cudaError_t e, const char* what, std::string& err) {
   if (e == cudaSuccess) return LFM_OK;
@@ -350,8 +357,10 @@ lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int acc
   const int pitch = (f.n_rows + 3) / 4 * 4;
   const int vta = std::getenv("LFM_SPA_VTA") ? (std::atoi(std::getenv("LFM_SPA_VTA")) == 4 ? 4 : 8) : (cp.spa_vta == 4 ? 4 : 8);
   const size_t smem = (size_t)vta * (nd + (nd >> 4) + 4) * 4;
-  static size_t smem_set[2] = {48 * 1024, 48 * 1024};
-  size_t& ss = smem_set[vta == 8];
+  static size_t smem_set[LFM_MAX_DEV][2];
+  size_t& ss0 = smem_set[cur_dev()][vta == 8];
+  if (ss0 == 0) ss0 = 48 * 1024;
+  size_t& ss = ss0;
   if (smem > ss) {
     cudaError_t e = vta == 8 ? cudaFuncSetAttribute(spass_adj_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                              : cudaFuncSetAttribute(spass_adj_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -444,11 +453,12 @@ static lfm_status encode3(CUtensorMap* map, const float* base, const long long d
 template <int N, int DIR, int BK>
 static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[LFM_MAX_DEV];
+  const int dv = cur_dev();
+  if (!attr[dv]) {
     if (cudaFuncSetAttribute(band_v_kernel<N, DIR, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VCfg<N, BK>::SMEM) != cudaSuccess)
       return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
-    attr = true;
+    attr[dv] = true;
   }
   VArgs v;
   v.B = T.d_img;
@@ -906,7 +916,8 @@ __global__ void __launch_bounds__(NT, 640 / NT) sep_kernel(SepArgs a) {
 template <int TS, int TT, int NT, int MODE>
 static lfm_status launch_sep_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
   auto kern = sep_kernel<TS, TT, NT, MODE>;
-  static bool configured = false;  // per instantiation
+  static bool configured_dev[LFM_MAX_DEV];  // per instantiation and device
+  bool& configured = configured_dev[cur_dev()];
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(sep_kernel)", err);
@@ -1425,7 +1436,8 @@ template <int NG, int K, int STAGES>
 static lfm_status launch_band_s(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err) {
   auto kern = band_s_kernel<NG, K, STAGES>;
   const size_t smem = (size_t)STAGES * K * 128 * 4;
-  static bool configured = false;
+  static bool configured_dev[LFM_MAX_DEV];
+  bool& configured = configured_dev[cur_dev()];
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_s_kernel)", err);
@@ -1802,7 +1814,8 @@ static lfm_status launch_band_g(const SepArgs& a, dim3 grid, cudaStream_t s, std
 template <int TS, int TT, int NCW, int STAGES>
 static lfm_status launch_band_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
   auto kern = band_t_kernel<TS, TT, NCW, STAGES>;
-  static bool configured = false;
+  static bool configured_dev[LFM_MAX_DEV];
+  bool& configured = configured_dev[cur_dev()];
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_t_kernel)", err);
@@ -1976,10 +1989,10 @@ static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, 
   return LFM_OK;
 }
 static int g_num_sms() {
-  static int n = 0;
+  static int sms[LFM_MAX_DEV];
+  const int dev = cur_dev();
+  int& n = sms[dev];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
@@ -2104,14 +2117,15 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     st = encode_map(&omap, out + (long long)b0 * a.out_stride, op.n_os, op.n_ot, a.out_pitch, 32, 32,
                     CU_TENSOR_MAP_SWIZZLE_128B, err);
     if (st != LFM_OK) return st;
-    static int smem_set = 0;
-    if (!smem_set) {
+    static bool smem_set[LFM_MAX_DEV];
+    const int dv = cur_dev();
+    if (!smem_set[dv]) {
       if (cudaFuncSetAttribute(band_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
         return cuda_check(cudaGetLastError(), "band_u smem attribute", err);
-      smem_set = 1;
+      smem_set[dv] = true;
     }
     UArgs u;
-    const int n_mt = (op.n_ot + 127) / 128;
+    const int n_mt = op.ft->u_ntiles;
     u.A = op.ft->d_ua;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
     u.blk_k0 = op.ft->d_uk0;
@@ -2119,8 +2133,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.out_pitch = a.out_pitch;
     u.n_rows = op.n_ot;
     u.n_cols = op.n_os;
-    u.mt0 = r0 / 128;
-    u.n_mt = (r1 + 127) / 128 - u.mt0;
+    u.mt0 = op.ft->u_mode ? 0 : r0 / 128;
+    u.n_mt = op.ft->u_mode ? n_mt : (r1 + 127) / 128 - u.mt0;
     u.n_nt = (op.n_os + 255) / 256;
     u.k_shift = a.win_r0;
     u.k_end = a.win_r1;
@@ -2645,8 +2659,8 @@ namespace lfm {
 // ------------------------------------------------------------------------------------------
 // Plan-time autotuning (host side of plan creation, excluded from timed work): every hot op of
 // A_forward / A_adjoint times each shared-memory-feasible (tile, threads, staging, nb) candidate on
-// zero-filled scratch buffers with CUDA events and keeps the fastest.  LFM_AUTOTUNE=0 disables it
-// (the cost-model choice is kept).
+// zero-filled scratch buffers with CUDA events and keeps the fastest.  It runs only with LFM_AUTOTUNE=1; the
+// default is the fixed tcgen05 choice of tc_defaults (no timed launches at plan creation).
 static void free_sep_dev(SepOp& op) {
   dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t); dfree(op.d_chunks); dfree(op.d_chunk_off);
   dfree(op.d_chunk_w);
@@ -2657,18 +2671,77 @@ static void free_sep_dev(SepOp& op) {
 // Optional result cache (LFM_TUNE_FILE): lines "<key> <op> ts tt nt nb stage"; a hit skips the timing
 // (used so that ncu captures see only the measured launches).
 static std::string tune_key(const CameraPlan& cp) {
-  const unsigned char* b = reinterpret_cast<const unsigned char*>(&cp.cam);
+  // field by field (struct padding never enters the hash), plus the rotated voxel sizes, which fix every band
   unsigned long long h = 1469598103934665603ull;
-  for (size_t i = 0; i < sizeof(cp.cam); ++i) h = (h ^ b[i]) * 1099511628211ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  const lfm_camera& c = cp.cam;
+  const int iv[] = {c.type, c.basis, c.k_s, c.k_t, c.nl_s, c.nl_t, c.n_a, c.n_s, c.n_t};
+  const double dv[] = {c.f_main, c.ap_s, c.ap_t, c.d_scene, c.d_det, c.d_mu_m, c.d_d_mu, c.f_mu, c.fill, c.px_s, c.px_t};
+  mix(iv, sizeof(iv));
+  mix(dv, sizeof(dv));
+  mix(c.R, sizeof(c.R));
+  mix(cp.info.vox_r, sizeof(cp.info.vox_r));
   char buf[96];
-  // v5: the line format carries kernel kind, pipeline stages, the timed ms and MSEG group rows
-  std::snprintf(buf, sizeof(buf), "v6_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
+  // v7: keyed field by field with the rotated voxel sizes
+  std::snprintf(buf, sizeof(buf), "v7_%016llx_%dx%dx%d", h, cp.info.nx, cp.info.ny, cp.info.nz);
   return buf;
+}
+
+// Overrides and layout conditions applied to whichever choice was made (timed or default):
+// LFM_FWD_T / LFM_ADJ_T = 0 direct sep, 1 transpose + band_m/band_f, 2 direct s-pass kernels, 3 band_v.
+static void finish_choice(CameraPlan& cp, bool dbg, float t_x, float t_z) {
+  if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] - '0';
+  if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] - '0';
+  if (cp.fwd_t == 1 && !(cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5))) cp.fwd_t = 0;
+  if (cp.adj_t == 1 && !(cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5))) cp.adj_t = 0;
+  // band_v moves rows by TMA: 16-byte row strides of the volume and of the detector intermediates
+  const bool tc_ok = cp.info.nx % 4 == 0 && cp.adj_c1.n_os % 4 == 0 && cp.cf[0].n_rows % 4 == 0;
+  if (cp.fwd_t == 3 && !tc_ok) cp.fwd_t = 2;
+  if (cp.adj_t == 3 && !tc_ok) cp.adj_t = 2;
+  if (cp.fwd_t < 0 || cp.fwd_t > 3) cp.fwd_t = 0;
+  if (cp.adj_t < 0 || cp.adj_t > 3) cp.adj_t = 0;
+  if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
+  static const char* smode[] = {"direct sep", "transposed", "spass", "tcgen05"};
+  if (dbg)
+    std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",
+                 cp.fwd_split ? "two passes" : "fused", smode[cp.fwd_t], t_x, t_z, smode[cp.adj_t]);
+}
+
+// B200 default (no timing, LFM_AUTOTUNE unset or 0): the collapsed path in its two-pass form with the tcgen05
+// kernels wherever their layout conditions hold -- band_u for both t passes (fwd_c2, adj_c1; drain group 4)
+// and band_v for both s passes -- the choice the timed search makes on B200 at 64^3-256^3.
+// The other ops keep the cost model's tiles.  LFM_FORCE_<op> still wins.
+static lfm_status tc_defaults(CameraPlan& cp, std::string& err) {
+  for (auto pr : {std::make_pair(&cp.fwd_c2, "fwd_c2"), std::make_pair(&cp.adj_c1, "adj_c1")}) {
+    SepOp& op = *pr.first;
+    if (!op.fs || std::getenv((std::string("LFM_FORCE_") + pr.second).c_str())) continue;
+    const long long sp = op.src_pitch ? op.src_pitch : op.n_is;
+    if (op.ft->u_off.empty() || op.tout || op.n_out != 1 || op.terms.size() != 1 || (sp & 3) ||
+        (op.terms[0].src_off & 3) || std::getenv("LFM_NO_TC"))
+      continue;
+    op.kind = 8; op.ts = 256; op.tt = 128; op.nt = U_THREADS; op.nb = 1; op.stage = 0; op.stages = 4; op.mgrp = 4;
+    fill_sep_geometry(op);
+    free_sep_dev(op);
+    size_t bytes = 0;
+    lfm_status st = upload_sep(op, bytes, err);
+    if (st != LFM_OK) return st;
+  }
+  cp.fwd_split = 1;
+  cp.fwd_t = std::getenv("LFM_NO_VF") ? 2 : 3;
+  cp.adj_t = std::getenv("LFM_NO_VA") ? 2 : 3;
+  return LFM_OK;
 }
 
 lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   const char* env = std::getenv("LFM_AUTOTUNE");
-  if (env && env[0] == '0') return LFM_OK;
+  if (!env || env[0] != '1') {
+    lfm_status st = tc_defaults(cp, err);
+    finish_choice(cp, std::getenv("LFM_DEBUG") != nullptr, -1.f, -1.f);
+    return st;
+  }
   const char* tfile = std::getenv("LFM_TUNE_FILE");
   const std::string key = tune_key(cp);
   std::vector<std::string> cached;
@@ -3097,22 +3170,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       std::fclose(f);
     }
   }
-  // overrides: LFM_FWD_T / LFM_ADJ_T = 0 direct sep, 1 transpose + band_m/band_f, 2 direct s-pass kernels
-  if (const char* e = std::getenv("LFM_FWD_T")) cp.fwd_t = e[0] - '0';
-  if (const char* e = std::getenv("LFM_ADJ_T")) cp.adj_t = e[0] - '0';
-  if (cp.fwd_t == 1 && !(cp.fwd_p1.fs && (cp.fwd_p1.kind == 3 || cp.fwd_p1.kind == 5))) cp.fwd_t = 0;
-  if (cp.adj_t == 1 && !(cp.adj_a2.fs && (cp.adj_a2.kind == 3 || cp.adj_a2.kind == 5))) cp.adj_t = 0;
-  // band_v moves rows by TMA: 16-byte row strides of the volume and of the detector intermediates
-  const bool tc_ok = cp.info.nx % 4 == 0 && cp.adj_c1.n_os % 4 == 0 && cp.cf[0].n_rows % 4 == 0;
-  if (cp.fwd_t == 3 && !tc_ok) cp.fwd_t = 2;
-  if (cp.adj_t == 3 && !tc_ok) cp.adj_t = 2;
-  if (cp.fwd_t < 0 || cp.fwd_t > 3) cp.fwd_t = 0;
-  if (cp.adj_t < 0 || cp.adj_t > 3) cp.adj_t = 0;
-  if (const char* fs = std::getenv("LFM_FWD_SPLIT")) cp.fwd_split = fs[0] == '1';
-  static const char* smode[] = {"direct sep", "transposed", "spass", "tcgen05"};
-  if (dbg)
-    std::fprintf(stderr, "[lfm] collapsed forward: %s, s pass %s (transpose x %.3f, z %.3f ms x2); adjoint s pass %s\n",
-                 cp.fwd_split ? "two passes" : "fused", smode[cp.fwd_t], t_x, t_z, smode[cp.adj_t]);
+  finish_choice(cp, dbg, t_x, t_z);
   return st;
 }
 }  // namespace lfm

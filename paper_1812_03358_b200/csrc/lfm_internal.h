@@ -73,6 +73,7 @@ struct BandFamily {
   // cells; per block two 128 x 16 tf32 weight images (hi, lo) in the shared-memory layout the MMA reads
   std::vector<int32_t> u_off, u_k0;        // u_off[table * n_tiles + tile] .. +1 into blocks; u_k0[block]
   int u_mode = 0, u_nz = 0;                // tile composition (build_umma): 0 = 128 rows, 1 = 2 vt x 64 slices
+  int u_ntiles = 0;                        // row tiles per table: ceil(n_rows/128) (mode 0), ceil(ny/2)*nz/64 (mode 1)
   std::vector<float> u_a;                  // 4096 floats per block
   int32_t* d_uoff = nullptr;
   int32_t* d_uk0 = nullptr;

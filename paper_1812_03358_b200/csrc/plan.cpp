@@ -455,7 +455,9 @@ static int umma_row(const BandFamily& f, int t, int m) {
 }
 
 static void build_umma(BandFamily& f) {
-  const int nt = (f.n_rows + 127) / 128;
+  // mode 1 pairs voxel rows: an odd ny leaves a last tile with one voxel row (its other half reads as none)
+  const int nt = f.u_mode == 0 ? (f.n_rows + 127) / 128 : ((f.n_rows / f.u_nz + 1) / 2) * (f.u_nz / 64);
+  f.u_ntiles = nt;
   f.u_off.assign((size_t)f.n_tables * nt + 1, 0);
   f.u_k0.clear();
   f.u_a.clear();

@@ -63,3 +63,20 @@ def test_fista_trajectory():
     for a, b in zip(xs_gpu, xs_ref):
         assert max_rel(a, b) <= 1e-4
     assert (xs_gpu[-1] >= 0).all()
+
+
+def test_nonfinite_cost_status():
+    """a non-finite cost is an error -- lfm_pwls_grad returns LFM_E_NONFINITE when the cost is
+    requested; without a cost pointer the call stays asynchronous and returns LFM_OK."""
+    from paper_1812_03358_b200 import lfm
+    from paper_1812_03358_b200.recon import PWLS
+    cfg, plan, ops, ys, ws_, _ = _problem()
+    rec = PWLS(plan, [dev(y) for y in ys], [dev(w) for w in ws_], 0.01)
+    x = uniform_volume(cfg["volume"], 4).astype(np.float32)
+    x[3] = np.nan
+    with pytest.raises(lfm.LfmError) as e:
+        rec.gradient(dev(x), with_cost=True)
+    assert e.value.status == 6
+    rec.gradient(dev(x), with_cost=False)   # no cost requested: no check, no error
+    torch.cuda.synchronize()
+    assert np.isnan(host(rec.grad)).any()

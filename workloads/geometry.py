@@ -101,6 +101,10 @@ def make_config(name):
         return dict(name=name, volume=volume(32, 0.4),
                     cameras=[plenoptic_camera(8, 8, 0.04, 4, 4),
                              plenoptic_camera(8, 8, 0.04, 4, 4, pose=pose_yaw(30.0))])
+    if name == "odd_ny":  # nz % 64 == 0 (slice-pair tcgen05 tiles) with an odd number of voxel rows, ragged edges
+        return dict(name=name, volume=dict(nx=32, ny=33, nz=64, dx=0.4, dy=0.4, dz=0.4),
+                    cameras=[plenoptic_camera(16, 8, 0.04, 2, 2),
+                             plenoptic_camera(16, 8, 0.04, 2, 2, pose=pose_yaw(20.0))])
     if name == "64^3 single":  # configs[1]
         return dict(name=name, volume=volume(64, 0.4),
                     cameras=[plenoptic_camera(64, 16, 0.005, 16, 4)])
@@ -117,5 +121,5 @@ def make_config(name):
     raise KeyError(name)
 
 
-CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two",
+CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "odd_ny",
            "64^3 single", "128^3 two-camera", "256^3 four-camera"]
