@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--config", default=WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-recon", action="store_true", help="skip the 50-iteration reconstruction timing")
     ap.add_argument("--no-per-view", action="store_true", help="skip the per-view path reference timing")
     ap.add_argument("--one-stream", action="store_true", help="run the rank's cameras one after another on one stream")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed pairs eagerly instead of as a CUDA graph")
@@ -113,42 +114,112 @@ def ncu_traffic():
         return {}
 
 
-def cpu_baseline(cfg, n_views_sample=None):
-    """Oracle (fp64, as it stands) timed on this host: camera 0 forward + adjoint on a view sample,
-    scaled linearly in K and by the number of cameras; rotation timed separately."""
+def host_facts():
+    """CPU model, usable cores and BLAS thread pools of this host (BASELINE.md CPU-baseline plan)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    return model, cores, blas
+
+
+_POOL = {}
+
+
+def _pool_task(task):
+    """One (camera, view) forward + adjoint of the fp64 oracle, in a forked worker (the camera models are
+    inherited copy-on-write from the parent)."""
+    from threadpoolctl import threadpool_limits
+    c, view = task
+    cam, xr, r = _POOL["cams"][c], _POOL["xr"][c], _POOL["r"][c]
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        cam.forward(xr, views=[view])
+        cam.adjoint(r, views=[view])
+        return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, budget_s=25.0):
+    """The fp64 oracle (as it stands, scipy.sparse) on this host's cores, on a bounded sample of the pair:
+    (i) one thread: camera 0 forward + adjoint on one view, scaled by K views and the number of cameras, plus
+        the measured rotation forward + adjoint of the posed cameras;
+    (ii) every usable core: a process pool runs `cores` (camera, view) forward+adjoint tasks at once (one per
+        core, fork), the batch time scaled to the pair's n_cam x K tasks, plus the single-thread rotations.
+    Cost is linear in K; both numbers are extrapolated from their samples and labelled so."""
+    import multiprocessing as mp
+
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     from oracle.camera import CameraModel
     from oracle.rotation import Rotation
     from workloads import flame_volume, uniform_vector
+    model, cores, blas = host_facts()
     vol = cfg["volume"]
     dims = (vol["nx"], vol["ny"], vol["nz"])
     vox = (vol["dx"], vol["dy"], vol["dz"])
+    x = flame_volume(vol).astype(np.float64)
+    t_build = time.perf_counter()
+    rots = [Rotation(c["R"], dims, vox) for c in cfg["cameras"]]
+    cams = [CameraModel(c, dims, rot.vox_r) for c, rot in zip(cfg["cameras"], rots)]
+    t_build = time.perf_counter() - t_build
+    K = cams[0].ks * cams[0].kt
+    n_cam = len(cams)
     with threadpool_limits(limits=1):
-        cam = CameraModel(cfg["cameras"][0], dims, vox)
-        K = cam.ks * cam.kt
-        views = [(ks, kt) for kt in range(cam.kt) for ks in range(cam.ks)]
-        if n_views_sample:
-            views = views[:n_views_sample]
-        x = flame_volume(vol).astype(np.float64)
-        r = uniform_vector(cam.n_pix, 1).astype(np.float64)
-        t0 = time.perf_counter()
-        cam.forward(x, views=views)
-        cam.adjoint(r, views=views)
-        t_cam = (time.perf_counter() - t0) * K / len(views)
         t_rot = 0.0
-        for c in cfg["cameras"][1:]:
-            rot = Rotation(c["R"], dims, vox)
+        xr = []
+        for rot in rots:
             t0 = time.perf_counter()
-            rot.adjoint(rot.forward(x))
+            xr.append(rot.forward(x))
+            rot.adjoint(xr[-1])
             t_rot += time.perf_counter() - t0
-    t_pair = t_cam * len(cfg["cameras"]) + t_rot
-    return dict(value=1.0 / t_pair, unit="pairs/s", cores=1, kind="oracle",
-                sample="camera 0 fwd+adj over %d of %d views, scaled x%d views and x%d cameras, + measured "
-                       "rotation fwd+adj of the posed cameras; single thread (scipy.sparse fp64)"
-                       % (len(views), K, K // len(views), len(cfg["cameras"])),
-                seconds_measured=round(t_cam * len(views) / K + t_rot, 2))
+        rs = [uniform_vector(cam.n_pix, 1 + c).astype(np.float64) for c, cam in enumerate(cams)]
+        t0 = time.perf_counter()
+        cams[0].forward(xr[0], views=[(0, 0)])
+        cams[0].adjoint(rs[0], views=[(0, 0)])
+        t_view = time.perf_counter() - t0
+    t_pair1 = t_view * K * n_cam + t_rot
+    out = dict(value=1.0 / t_pair1, unit="pairs/s", cores=1, kind="oracle", cpu_model=model, blas=blas,
+               sample="one thread: camera 0 fwd+adj over 1 of %d views (%.2f s), x%d views x%d cameras, + measured "
+                      "rotation fwd+adj of every camera (%.2f s); oracle build %.1f s excluded; extrapolated"
+                      % (K, t_view, K, n_cam, t_rot, t_build))
+    n_tasks = min(cores, n_cam * K, max(1, int(budget_s / max(t_view, 1e-3)) * cores))
+    if cores > 1:
+        try:
+            _POOL.update(cams=cams, xr=xr, r=rs)
+            tasks = [(i % n_cam, ((i // n_cam) % cams[0].ks, (i // n_cam) // cams[0].ks % cams[0].kt))
+                     for i in range(n_tasks)]
+            ctx = mp.get_context("fork")
+            with ctx.Pool(cores) as pool:
+                pool.map(_pool_task, tasks[:cores])                       # warm the workers
+                t0 = time.perf_counter()
+                pool.map(_pool_task, tasks, chunksize=1)
+                t_batch = time.perf_counter() - t0
+            waves = math.ceil(n_cam * K / cores)
+            t_pair = t_batch * waves / math.ceil(n_tasks / cores) + t_rot
+            out["all_cores"] = dict(value=1.0 / t_pair, cores=cores, tasks_timed=n_tasks,
+                                    sample="process pool over (camera, view) fwd+adj tasks on %d cores: %d tasks in "
+                                           "%.2f s, scaled to the pair's %d tasks (%d waves), + single-thread "
+                                           "rotations; extrapolated" % (cores, n_tasks, t_batch, n_cam * K, waves))
+        except Exception as exc:
+            out["all_cores"] = {"value": None, "cores": cores, "sample": "failed: %s" % exc}
+        finally:
+            _POOL.clear()
+    return out
 
 
 # ------------------------------------------------------------------------------------ reference arm
@@ -191,15 +262,20 @@ def run_reference(args, rank, world):
                 per_rot.append(t_rot)
     # one step = one view of every camera's forward+adjoint (+ the rotations, once per pair); a full pair
     # is K views (cost linear in K)
+    step_s = [a + b for a, b in zip(per_view, per_rot)]
     t_pair = (sum(per_view) / len(per_view)) * K + sum(per_rot) / len(per_rot)
     value = 1.0 / t_pair
+    model, cores, blas = host_facts()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_pair, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(step_s) / len(step_s),
+            "pair_ms_extrapolated": 1e3 * t_pair, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "step": "one view of an A+A^T pair per timed step, x%d views" % K},
-            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "oracle",
-                             "sample": "per step: 1 of %d views of every camera's fwd+adj with rotation; "
-                                       "oracle build %.1fs excluded" % (K, t_build)},
+            "config": {"workload": args.config,
+                       "step": "one timed step = 1 view of every camera's fwd+adj with the rotations; value = pairs/s "
+                               "extrapolated to the pair's %d views (cost linear in K, P:406-408)" % K},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": 1, "kind": "oracle", "cpu_model": model,
+                             "blas": blas, "sample": "per step: 1 of %d views of every camera's fwd+adj with rotation, "
+                                                     "one thread; oracle build %.1fs excluded" % (K, t_build)},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -277,11 +353,11 @@ def run_ours(args, rank, world, local_rank):
         start = None
         runner = PairRunner(items, fwd_rows, adj_rows, lambda gv: gv.zero_(), allreduce if world > 1 else None)
 
-    def step(x_in, g_out):
+    def step(x_in, g_out, ys_=None, rs_=None):
         launches[0] = 0
         if start is not None:
             start.record(torch.cuda.current_stream())
-        runner.pair(x_in, ys, rs, g_out)
+        runner.pair(x_in, ys if ys_ is None else ys_, rs if rs_ is None else rs_, g_out)
 
     # dominant kernel: the separable transport of an unrotated camera (one sep_kernel launch per call)
     dom_cam = next((c for c, r0, r1 in items if plan.infos[c]["rot_passes"] == 0 and r0 == 0
@@ -323,42 +399,40 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     ms = sorted(a.elapsed_time(b) for a, b in ev)
     ms_mean = sum(ms) / len(ms)
+    ms_med = ms[len(ms) // 2] if len(ms) % 2 else 0.5 * (ms[len(ms) // 2 - 1] + ms[len(ms) // 2])
     # dominant-kernel timing on the same stream, inside timed steps of the same shape
     # The dominant kernel of the collapsed path is its forward t pass (one launch, lfm_A_stage FWD_T:
     # the slice sum over the interleaved intermediate); its adjoint counterpart is ADJ_T.  Each launch
     # is timed alone with events on the bench stream, after an L2 flush, inputs from a full call.
+    def timed(fn, reps=max(5, min(21, args.steps // 4)), prep=None):
+        """Median device time (ms) of fn() alone on the bench stream, L2 flushed before every launch."""
+        out = []
+        for _ in range(reps):
+            if prep is not None:
+                prep()
+            flush.zero_()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            fn()
+            b_.record(stream)
+            torch.cuda.synchronize()
+            out.append(a_.elapsed_time(b_))
+        out.sort()
+        return out[len(out) // 2]
+
     dom = None
     if dom_cam is not None:
-        fwd_ms, adj_ms = [], []
         staged = path == lfm.COLLAPSED
-        for i in range(max(3, args.steps // 2)):
-            a, b, c_, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-            if staged:
-                try:
-                    lfm.A_forward(plan, dom_cam, x, ys[dom_cam], ws, path=path)
-                    flush.zero_()
-                    a.record(stream)
-                    lfm.A_stage(plan, dom_cam, lfm.STAGE_FWD_T, None, ys[dom_cam], ws)
-                    b.record(stream)
-                    flush.zero_()
-                    c_.record(stream)
-                    lfm.A_stage(plan, dom_cam, lfm.STAGE_ADJ_T, rs[dom_cam], None, ws)
-                    d.record(stream)
-                except lfm.LfmError:  # fused collapsed forward: time the whole call instead
-                    staged = False
-            if not staged:
-                flush.zero_()
-                a.record(stream)
-                lfm.A_forward(plan, dom_cam, x, ys[dom_cam], ws, path=path)
-                b.record(stream)
-                flush.zero_()
-                c_.record(stream)
-                lfm.A_adjoint(plan, dom_cam, rs[dom_cam], g, ws, path=path)
-                d.record(stream)
-            torch.cuda.synchronize()
-            fwd_ms.append(a.elapsed_time(b))
-            adj_ms.append(c_.elapsed_time(d))
         inf = plan.infos[dom_cam]
+        try:
+            lfm.A_forward(plan, dom_cam, x, ys[dom_cam], ws, path=path)
+            fwd_ms = timed(lambda: lfm.A_stage(plan, dom_cam, lfm.STAGE_FWD_T, None, ys[dom_cam], ws))
+            adj_ms = timed(lambda: lfm.A_stage(plan, dom_cam, lfm.STAGE_ADJ_T, rs[dom_cam], None, ws))
+        except lfm.LfmError:  # fused collapsed forward: time the whole call instead
+            staged = False
+        if not staged:
+            fwd_ms = timed(lambda: lfm.A_forward(plan, dom_cam, x, ys[dom_cam], ws, path=path))
+            adj_ms = timed(lambda: lfm.A_adjoint(plan, dom_cam, rs[dom_cam], g, ws, path=path))
         kind = None
         if staged:
             fma_f, fma_a = inf["fma_stage"][0], inf["fma_stage"][1]
@@ -367,8 +441,59 @@ def run_ours(args, rank, world, local_rank):
         else:
             fma_f = fma_a = inf["fma_alg"][1 if path == lfm.COLLAPSED else 0]
             kname = "%s A_forward, camera %d" % (args.path, dom_cam)
-        dom = dict(fwd_ms=sum(fwd_ms) / len(fwd_ms), adj_ms=sum(adj_ms) / len(adj_ms), fma=fma_f, fma_adj=fma_a,
-                   name=kname, kind=kind, mma=inf["mma_stage"][0])
+        dom = dict(fwd_ms=fwd_ms, adj_ms=adj_ms, fma=fma_f, fma_adj=fma_a, name=kname, kind=kind, mma=inf["mma_stage"][0])
+
+    # every kernel of the pair timed alone (CUDA events, L2 flushed, median): device time, algorithmic HBM bytes
+    # -> GB/s and the fraction of the measured copy peak / the 8 TB/s spec, FMA rate where it counts
+    kernels = None
+    if world == 1 and path == lfm.COLLAPSED:
+        kernels = {}
+        c0 = 0
+        inf = plan.infos[c0]
+        nv, npx = inf["n_vox"], inf["n_pix"]
+        z_bytes = 4.0 * inf["ny"] * inf["nz"] * inf["n_s"]          # the slice-interleaved intermediate U / Z
+        tmp = torch.empty(nv, device=dev)
+
+        def add(name, ms_, nbytes, fma=None, what=""):
+            k = {"ms": ms_, "bytes": nbytes, "gbs": nbytes / (ms_ * 1e-3) / 1e9}
+            k["frac_measured"] = k["gbs"] / peaks.get("hbm_gbs", 6551.4)
+            k["frac_8tbs"] = k["gbs"] / 8000.0
+            if fma is not None:
+                k["tflops"] = 2.0 * fma / (ms_ * 1e-3) / 1e12
+            if what:
+                k["what"] = what
+            kernels[name] = k
+
+        peaks = measured_peaks()
+        rot_cam = next((c for c in range(plan.n_cam) if plan.infos[c]["rot_passes"]), None)
+        if rot_cam is not None:
+            npass = bin(plan.infos[rot_cam]["rot_passes"] & 7).count("1")
+            add("rotation_fwd", timed(lambda: lfm.vol_rotate(plan, rot_cam, lfm.FWD, x, tmp, ws)), 8.0 * nv * npass,
+                what="%d shear passes, camera %d: read + write per voxel per pass" % (npass, rot_cam))
+            add("rotation_adj", timed(lambda: lfm.vol_rotate(plan, rot_cam, lfm.ADJ, x, tmp, ws)), 8.0 * nv * npass)
+        if inf["kind_stage"][0] == 8:
+            add("s_pass_fwd (band_v)", timed(lambda: lfm.A_stage(plan, c0, lfm.STAGE_FWD_S, x, None, ws)),
+                4.0 * nv + z_bytes, fma=inf["fma_spass"][0], what="read x^r, write U")
+            lfm.A_stage(plan, c0, lfm.STAGE_FWD_S, x, None, ws)
+            add("t_pass_fwd (band_u)", timed(lambda: lfm.A_stage(plan, c0, lfm.STAGE_FWD_T, None, ys[c0], ws)),
+                z_bytes + 4.0 * npx, fma=inf["fma_stage"][0], what="read U, write y")
+            add("t_pass_adj (band_u)", timed(lambda: lfm.A_stage(plan, c0, lfm.STAGE_ADJ_T, rs[c0], None, ws)),
+                4.0 * npx + z_bytes, fma=inf["fma_stage"][1], what="read y, write Z")
+            add("s_pass_adj (band_v)", timed(lambda: lfm.A_stage(plan, c0, lfm.STAGE_ADJ_S, None, tmp, ws)),
+                z_bytes + 4.0 * nv, fma=inf["fma_spass"][1], what="read Z, write x^r")
+        stats = torch.zeros(3, dtype=torch.float64, device=dev)
+        wts = torch.ones(npx, device=dev)
+        add("pwls_stats", timed(lambda: lfm.pwls_stats(plan, c0, ys[c0], rs[c0], wts, stats, ws)), 12.0 * npx,
+            what="read Ax, y, w")
+        add("pwls_reg26 (+fill)", timed(lambda: lfm.pwls_grad(plan, x, [], [], [], None, 0.01, 0.0, tmp, ws, cam0=0,
+                                                              cam1=0, include_reg=True)), 16.0 * nv,
+            what="grad = 0, then grad += beta sum_26 (x_j - x_l) + nu: write, read x, read+write grad")
+        zz, dd, gg = torch.rand(nv, device=dev), torch.rand(nv, device=dev) + 1.0, torch.rand(nv, device=dev)
+        xx = torch.rand(nv, device=dev)
+        add("fista_update", timed(lambda: lfm.fista_update(plan, xx, zz, gg, dd, 1.0, 1.6)), 24.0 * nv,
+            what="read x, z, grad, d; write x, z")
+        add("vol_accumulate", timed(lambda: lfm.vol_accumulate(gg, tmp)), 12.0 * nv, what="dst += src")
+
     # the paper's own evaluation order (per-view factored chain) on the same
     # workload, for reference: device time of one forward and one adjoint per camera
     per_view = None
@@ -376,73 +501,117 @@ def run_ours(args, rank, world, local_rank):
         fv, av = [], []
         for c in range(plan.n_cam):
             lfm.A_forward(plan, c, x, ys[c], ws, path=lfm.PER_VIEW)
-            tf, ta = [], []
-            for _ in range(3):
-                a_, b_, c_, d_ = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-                flush.zero_()
-                a_.record(stream)
-                lfm.A_forward(plan, c, x, ys[c], ws, path=lfm.PER_VIEW)
-                b_.record(stream)
-                flush.zero_()
-                c_.record(stream)
-                lfm.A_adjoint(plan, c, rs[c], g, ws, path=lfm.PER_VIEW)
-                d_.record(stream)
-                torch.cuda.synchronize()
-                tf.append(a_.elapsed_time(b_))
-                ta.append(c_.elapsed_time(d_))
-            fv.append(sorted(tf)[1])
-            av.append(sorted(ta)[1])
+            fv.append(timed(lambda: lfm.A_forward(plan, c, x, ys[c], ws, path=lfm.PER_VIEW), reps=3))
+            av.append(timed(lambda: lfm.A_adjoint(plan, c, rs[c], g, ws, path=lfm.PER_VIEW), reps=3))
         per_view = {"fwd_ms": fv, "adj_ms": av, "pairs_per_s": 1e3 / (sum(fv) + sum(av))}
     sm = clocks.stop()
-    # e2e: through the public API with host buffers (pinned), copies inside the timed region
-    e2e = None
-    if not args.no_e2e:
-        # Each step copies its own input volume host->device and its gradient device->host (pinned buffers,
-        # two of each so step i+1's upload and step i's download overlap step i's / i+1's compute on a
-        # separate copy stream; events order the buffers).
-        xh = [x.cpu().pin_memory(), x.cpu().pin_memory()]
-        gh = [torch.empty(n_vox, dtype=torch.float32).pin_memory() for _ in range(2)]
-        xd = [torch.empty_like(x), torch.empty_like(x)]
-        gd = [torch.empty_like(g), torch.empty_like(g)]
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region.  "pair": every input
+    # of the pair crosses host -> device each step (x and every r_c) and every output device -> host (every y_c and
+    # g); "gradient": x in, g out, the detector data resident (a reconstruction's view).  Two sets of device and
+    # host buffers: step i+1's upload and step i's download run on a copy stream while step i / i+1 compute.
+    def run_e2e(n, full):
         cs = torch.cuda.Stream()
+        cams_ = sorted(ys)
+        hin = [dict(x=x.cpu().pin_memory(), r={c: rs[c].cpu().pin_memory() for c in cams_}) for _ in range(2)]
+        hout = [dict(y={c: torch.empty(ys[c].numel()).pin_memory() for c in cams_},
+                     g=torch.empty(n_vox).pin_memory()) for _ in range(2)]
+        dv = [dict(x=torch.empty_like(x), r={c: torch.empty_like(rs[c]) if full else rs[c] for c in cams_},
+                   y={c: torch.empty_like(ys[c]) for c in cams_}, g=torch.empty_like(g)) for _ in range(2)]
 
-        def run_e2e(n):
-            up = [torch.cuda.Event() for _ in range(n + 1)]
-            done = [torch.cuda.Event() for _ in range(n)]
-            cs.wait_stream(stream)  # nothing on the copy stream starts before the timed region opens
+        def upload(i):
+            b, h = dv[i % 2], hin[i % 2]
+            b["x"].copy_(h["x"], non_blocking=True)
+            if full:
+                for c in cams_:
+                    b["r"][c].copy_(h["r"][c], non_blocking=True)
+
+        def download(i):
+            b, h = dv[i % 2], hout[i % 2]
+            if full:
+                for c in cams_:
+                    h["y"][c].copy_(b["y"][c], non_blocking=True)
+            h["g"].copy_(b["g"], non_blocking=True)
+
+        up = [torch.cuda.Event() for _ in range(n + 1)]
+        done = [torch.cuda.Event() for _ in range(n)]
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            upload(0)
+            up[0].record(cs)
+        for i in range(n):
+            stream.wait_event(up[i])
+            b = dv[i % 2]
+            step(b["x"], b["g"], b["y"], b["r"])
+            done[i].record(stream)
             with torch.cuda.stream(cs):
-                xd[0].copy_(xh[0], non_blocking=True)
-                up[0].record(cs)
-            for i in range(n):
-                stream.wait_event(up[i])
-                step(xd[i % 2], gd[i % 2])
-                done[i].record(stream)
-                with torch.cuda.stream(cs):
-                    if i + 1 < n:
-                        if i >= 1:
-                            cs.wait_event(done[i - 1])  # xd[(i+1)%2] was step i-1's input
-                        xd[(i + 1) % 2].copy_(xh[(i + 1) % 2], non_blocking=True)
-                        up[i + 1].record(cs)
-                    cs.wait_event(done[i])
-                    gh[i % 2].copy_(gd[i % 2], non_blocking=True)
-            stream.wait_stream(cs)
+                if i + 1 < n:
+                    if i >= 1:
+                        cs.wait_event(done[i - 1])     # buffers (i+1)%2 were step i-1's
+                    upload(i + 1)
+                    up[i + 1].record(cs)
+                cs.wait_event(done[i])
+                download(i)
+        stream.wait_stream(cs)
+        full_in = x.numel() * 4 + (sum(rs[c].numel() for c in cams_) * 4 if full else 0)
+        full_out = n_vox * 4 + (sum(ys[c].numel() for c in cams_) * 4 if full else 0)
+        return full_in, full_out
 
-        run_e2e(3)
+    e2e = {}
+    if not args.no_e2e:
+        for kind_, full in (("pair", True), ("gradient", False)):
+            run_e2e(3, full)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bi, bo = run_e2e(args.steps, full)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e[kind_] = dict(ms=e0.elapsed_time(e1) / args.steps, h2d=bi, d2h=bo)
+
+    # the reconstruction config (BASELINE configs[4]): 50 FISTA iterations with per-camera gains on the 128^3
+    # two-camera geometry (SURVEY §8(d) recon row): data y_c = gamma_c A_c x_true, gamma = (1, 0.7), W = 1,
+    # beta = 0.01 median(d_data), nu = 0, x_0 = 0; device time of the whole run (eager launches, one host
+    # scalar per iteration) / 50
+    recon = None
+    if world == 1 and not args.no_recon and args.config == WORKLOAD:
+        from paper_1812_03358_b200.recon import PWLS
+        gam_true = [1.0, 0.7, 1.9, 1.3]
+        yd = [torch.empty(plan.infos[c]["n_pix"], device=dev) for c in range(plan.n_cam)]
+        for c in range(plan.n_cam):
+            lfm.A_forward(plan, c, x, yd[c], ws)
+            yd[c].mul_(gam_true[c] if c else 1.0)
+        wd = [torch.ones_like(v) for v in yd]
+        rec = PWLS(plan, yd, wd, 0.0)
+        d0 = rec.majoriser().clone()
+        rec.beta = 0.01 * float(d0.median())
+        iters = 50
+        rec.fista(2)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        run_e2e(args.steps)
+        rec.majoriser()
         e1.record(stream)
+        xr_ = rec.fista(iters)            # recomputes the majoriser first, then 50 iterations
+        e2.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.steps
-        e2e = dict(ms=e2e_ms, h2d=xh[0].numel() * 4, d2h=gh[0].numel() * 4)
+        t_maj, t_run = e0.elapsed_time(e1), e1.elapsed_time(e2)
+        rel = float((xr_ - x).norm() / x.norm())
+        recon = {"workload": "recon: 128^3 two-camera, 50 FISTA iterations, gains (1, 0.7), W = 1, beta = 0.01 "
+                             "median(d)", "ms_per_iteration": (t_run - t_maj) / iters, "iterations": iters,
+                 "ms_majoriser": t_maj, "ms_total": t_run, "iterations_per_s": 1e3 * iters / (t_run - t_maj),
+                 "rel_error_vs_truth_after_50": rel,
+                 "per_iteration": "A_c z + stats (every camera), gains, sum_c A_c^T W(A_c z - gamma y) + reg26, "
+                                  "FISTA update; majoriser (one extra forward+adjoint per camera) once per run"}
+
     # max over ranks
-    t = torch.tensor([ms_mean, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_med, ms_mean, e2e["pair"]["ms"] if e2e else 0.0, e2e["gradient"]["ms"] if e2e else 0.0],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_mean, e2e_ms = float(t[0]), float(t[1])
+    ms_med, ms_mean = float(t[0]), float(t[1])
     if rank != 0:
         return
     peaks = measured_peaks()
@@ -474,10 +643,24 @@ def run_ours(args, rank, world, local_rank):
                          "alu_equiv": {"peak": fp32_peak, "frac": achieved / fp32_peak,
                                        "what": "algorithmic flops / time vs the FP32 FMA roof the plain kernels face"},
                          "kernel": dom["name"] + " on tcgen05 (band_u)"})
-    pair_bytes = sum(plan.infos[c]["bytes_alg"][1 if path == lfm.COLLAPSED else 0] * 2 for c in range(plan.n_cam))
-    value = 1e3 / ms_mean
+    pi = 1 if path == lfm.COLLAPSED else 0
+    pair_bytes = sum(plan.infos[c]["bytes_alg"][pi] * 2 for c in range(plan.n_cam))
+    # the pair's binding roof (BASELINE.md roofline caveat): max(FMA_alg / FMA peak, bytes_alg / HBM peak) / time,
+    # FMA_alg = the plan's non-zero work of every camera's forward and adjoint (collapsed: both s and t passes)
+    if path == lfm.COLLAPSED:
+        pair_fma = sum(2.0 * (plan.infos[c]["fma_stage"][0] + plan.infos[c]["fma_spass"][0]) for c in range(plan.n_cam))
+    else:
+        pair_fma = sum(2.0 * plan.infos[c]["fma_alg"][0] for c in range(plan.n_cam))
+    t_fma = 2.0 * pair_fma / (fp32_peak * 1e12)
+    t_hbm = pair_bytes / (peaks.get("hbm_gbs", 6551.4) * 1e9)
+    pair_roof = {"binding": "fp32_fma" if t_fma >= t_hbm else "hbm", "fma_alg": pair_fma, "bytes_alg": pair_bytes,
+                 "floor_ms": 1e3 * max(t_fma, t_hbm), "frac": 1e3 * max(t_fma, t_hbm) / ms_med,
+                 "what": "max(FMA_alg / FP32 FMA peak, bytes_alg / measured HBM) / median pair time "
+                         "(BASELINE.md); FMA_alg counts plan non-zeros of every s and t pass"}
+    value = 1e3 / ms_med
     line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_mean, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_med, "ms_per_step_mean": ms_mean, "statistic": "median",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "volume": "%d^3 flame phantom" % cfg["volume"]["nx"],
                        "cameras": len(cfg["cameras"]), "detector": "%dx%d" % (cfg["cameras"][0]["n_s"],
@@ -487,14 +670,23 @@ def run_ours(args, rank, world, local_rank):
                            world, ", concurrent per-camera streams" if len(items) > 1 and not args.one_stream else ""),
                        "l2": "256 MiB write between steps, outside the per-step CUDA events",
                        "launch": "eager" if (args.no_graph or world > 1) else "one CUDA graph per pair (captured after warm-up)"},
-            "hbm_gbs_alg": pair_bytes / (ms_mean * 1e-3) / 1e9,
-            "hbm_frac_of_measured": pair_bytes / (ms_mean * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
+            "hbm_gbs_alg": pair_bytes / (ms_med * 1e-3) / 1e9,
+            "hbm_frac_of_measured": pair_bytes / (ms_med * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
+            "pair_roofline": pair_roof,
             "roofline": roof, "clocks": sm, "gpu_launches": launches[0] * args.steps}
+    if kernels:
+        line["kernels"] = kernels
     if per_view is not None:
         line["per_view_path"] = per_view
     if e2e:
-        line["e2e"] = {"value": 1e3 / e2e_ms, "unit": "pairs/s", "h2d_bytes_per_step": e2e["h2d"],
-                       "d2h_bytes_per_step": e2e["d2h"]}
+        line["e2e"] = {"value": 1e3 / float(t[2]), "unit": "pairs/s", "h2d_bytes_per_step": e2e["pair"]["h2d"],
+                       "d2h_bytes_per_step": e2e["pair"]["d2h"],
+                       "what": "every input (x, r_c) in and every output (y_c, g) out per pair, pinned host buffers"}
+        line["e2e_gradient"] = {"value": 1e3 / float(t[3]), "unit": "pairs/s",
+                                "h2d_bytes_per_step": e2e["gradient"]["h2d"], "d2h_bytes_per_step": e2e["gradient"]["d2h"],
+                                "what": "x in, g out; detector data resident"}
+    if recon is not None:
+        line["recon"] = recon
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg)

@@ -115,6 +115,10 @@ typedef struct {
   double mma_stage[2];      /* tensor-core MACs one launch of those stages issues when it runs on the tcgen05
                                kernel (3 products x dense 128 x 16 blocks x columns) */
   int kind_stage[2];        /* kernel the autotuner chose for those stages (8 = tcgen05 band_u, 5 = band_f, ...) */
+  double fma_spass[2];      /* algorithmic FMAs of one launch of LFM_STAGE_FWD_S / LFM_STAGE_ADJ_S (the collapsed
+                               path's s passes: non-zeros of C_s,n summed over slices x ny voxel rows) */
+  int subset_collapsed;     /* how many of the plan's view subsets run on the collapsed path (tensor-product
+                               subsets, lfm_A_forward_subset); the others use the per-view path */
 } lfm_info;
 
 /* Table ids for lfm_plan_export_table (bit-exact comparison with the oracle in tests).
@@ -187,7 +191,9 @@ lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1,
 /* View-subset operators (sec,subset, eqn,subset P:366-379, reading Z19): with S_m the plan's subset m,
  *   y = (K/|S_m|) sum_{k in S_m} A_ck x           (lfm_A_forward_subset)
  *   x (+)= (K/|S_m|) sum_{k in S_m} A_ck^T y      (lfm_A_adjoint_subset)
- * evaluated on the per-view path (the K-collapse needs the full angular sum).  0 <= subset < n_subsets of the
+ * evaluated on the collapsed path when S_m is a tensor product S_s x {all k_t} (M divides K_s: the s composite is
+ * re-collapsed over S_s, the t pass is the full one; lfm_info.subset_collapsed counts these), else on the per-view
+ * path.  0 <= subset < n_subsets of the
  * plan (LFM_E_INVALID otherwise, also when the plan has no subsets).  Same buffers and workspace as
  * lfm_A_forward / lfm_A_adjoint. */
 lfm_status lfm_A_forward_subset(lfm_plan p, int cam, int subset, const float* x, float* y, void* ws, size_t ws_bytes,
@@ -203,7 +209,11 @@ lfm_status lfm_A_adjoint_subset(lfm_plan p, int cam, int subset, const float* y,
  *   LFM_STAGE_ADJ_T: Z[(vt, n)][:] = sum over i_t of C_t,n^T[vt][i_t] y[i_t][:]  (`in` = y; `out` unused,
  *                    Z is left in the workspace).
  * Status LFM_E_INVALID if the camera's collapsed path is not in its two-pass form. */
-enum { LFM_STAGE_FWD_T = 0, LFM_STAGE_ADJ_T = 1 };
+/*   LFM_STAGE_FWD_S: Z[(vt, n)][:] = sum_vx x^r_n[vt][vx] C_s,n[:][vx]  (`in` = x^r, the rotated volume;
+ *                    `out` unused, Z is left in the workspace for LFM_STAGE_FWD_T);
+ *   LFM_STAGE_ADJ_S: out_n[vt][vx] = c sum_i C_s,n^T[vx][i] Z[(vt, n)][i]  (Z from the last lfm_A_adjoint or
+ *                    LFM_STAGE_ADJ_T with this workspace; `out` = the rotated-frame volume, overwritten). */
+enum { LFM_STAGE_FWD_T = 0, LFM_STAGE_ADJ_T = 1, LFM_STAGE_FWD_S = 2, LFM_STAGE_ADJ_S = 3 };
 lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* out, void* ws, size_t ws_bytes,
                        void* stream);
 

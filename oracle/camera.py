@@ -143,6 +143,47 @@ class CameraModel:
                 g[n] += self.scale_s1 * (self.S1[1][kt][n].T @ (a @ self.S1[0][ks][n]))
         return g
 
+    # ---- single outputs, one by one (full-size parity on sampled outputs; same factored sums as above) ----
+    def forward_at(self, xr, pixels):
+        """y[i_t, i_s] = sum_k sum_n (row i of the camera factors) x^r_n for each (i_t, i_s) in `pixels`:
+        plenoptic y_i = c3 sum_k (S3t_kt[i_t] c1 S1t_kt,n) x^r_n (S3s_ks[i_s] S1s_ks,n)^T summed over n, the
+        factored chain of forward() restricted to one detector pixel."""
+        xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)
+        out = np.zeros(len(pixels))
+        for p, (it, i_s) in enumerate(pixels):
+            acc = 0.0
+            for n in range(self.nz):
+                if self.type == PLENOPTIC:
+                    rt = np.stack([np.asarray((self.S3[1][kt][it:it + 1] @ self.S1[1][kt][n]).todense()).ravel()
+                                   for kt in range(self.kt)])
+                    rs = np.stack([np.asarray((self.S3[0][ks][i_s:i_s + 1] @ self.S1[0][ks][n]).todense()).ravel()
+                                   for ks in range(self.ks)])
+                else:
+                    rt = np.stack([self.S1[1][kt][n][it].toarray().ravel() for kt in range(self.kt)])
+                    rs = np.stack([self.S1[0][ks][n][i_s].toarray().ravel() for ks in range(self.ks)])
+                acc += np.sum(rt @ xr[n] @ rs.T)
+            out[p] = acc * self.scale_s1 * (self.scale_s3 if self.type == PLENOPTIC else 1.0)
+        return out
+
+    def adjoint_at(self, y, voxels):
+        """(A^T y)[n, v_t, v_x] of the rotated frame for each (n, v_t, v_x) in `voxels`: the literal transposes
+        of adjoint(), evaluated at single voxels from the per-view array fields a_k = c3 S3t_kt^T y S3s_ks."""
+        y = np.asarray(y, np.float64).reshape(self.cam["n_t"], self.cam["n_s"])
+        fields = {}
+        for ks in range(self.ks):
+            for kt in range(self.kt):
+                fields[ks, kt] = self.scale_s3 * (self.S3[1][kt].T @ (y @ self.S3[0][ks])) \
+                    if self.type == PLENOPTIC else y
+        out = np.zeros(len(voxels))
+        for p, (n, vt, vx) in enumerate(voxels):
+            acc = 0.0
+            for (ks, kt), a in fields.items():
+                ct = self.S1[1][kt][n][:, vt].toarray().ravel()
+                cs = self.S1[0][ks][n][:, vx].toarray().ravel()
+                acc += ct @ a @ cs
+            out[p] = self.scale_s1 * acc
+        return out
+
     def array_fields(self, xr):
         """Plenoptic intermediate a_k (K, n_at, n_as) of the factored chain (for S1-stage parity)."""
         xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)

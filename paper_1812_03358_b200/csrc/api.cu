@@ -110,8 +110,22 @@ lfm_status check_cam(const lfm_plan_s* p, int cam, bool need_device = true) {
 // Rotation forward: returns the buffer holding x^r (x itself if the pose is the identity).  Stages in
 // order: the quarter-turn relabelling (if any, reading R7), then the active shear passes z, x, y;
 // intermediate results ping-pong between w.r0 and w.r1, the last one goes to final_out if given.
+// A yaw pose (only the z and x shear passes, no relabelling): both passes in one fused in-plane launch.
+static bool yaw_only(const CameraPlan& cp) { return !cp.has_perm && cp.rot[0].active && cp.rot[1].active && !cp.rot[2].active; }
+
 lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, int accumulate, const Ws& w,
                       void* stream, const float** xr) {
+  if (yaw_only(cp)) {
+    float* dst = final_out ? final_out : w.r0;
+    lfm_status st = LFM_OK;
+    std::string err;
+    if (launch_rot_zx(cp.rot[0], cp.rot[1], 0, x, dst, cp.info.nx, cp.info.ny, cp.info.nz, final_out ? accumulate : 0,
+                      stream, st, err)) {
+      if (st != LFM_OK) return fail(st, err);
+      *xr = dst;
+      return LFM_OK;
+    }
+  }
   int act[4], na = 0;
   if (cp.has_perm) act[na++] = -1;
   for (int q = 0; q < 3; ++q)
@@ -141,6 +155,12 @@ lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, in
 // Rotation adjoint E^zT E^xT E^yT, then the inverse relabelling P^T, applied to `in`, written (or
 // accumulated) into `out`.  `in` may be w.r0 or w.r1 (the ping-pong never writes the buffer it reads).
 lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int accumulate, const Ws& w, void* stream) {
+  if (yaw_only(cp)) {
+    lfm_status st = LFM_OK;
+    std::string err;
+    if (launch_rot_zx(cp.rot[0], cp.rot[1], 1, in, out, cp.info.nx, cp.info.ny, cp.info.nz, accumulate, stream, st, err))
+      return st == LFM_OK ? st : fail(st, err);
+  }
   int act[4], na = 0;
   for (int q = 2; q >= 0; --q)
     if (cp.rot[q].active) act[na++] = q;
@@ -183,7 +203,7 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
       if (cp.fwd_t == 2 || cp.fwd_t == 3) {
         // direct s pass (spass_fwd_kernel, or band_v on the tensor cores): slices -> interleaved U
         std::string err;
-        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, xr, w.z, stream, err) : k_spass_fwd(cp, xr, w.z, stream, err);
+        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err) : k_spass_fwd(cp, xr, w.z, stream, err);
         if (st != LFM_OK) return fail(st, err);
       } else if (cp.fwd_t) {
         // s pass as a t pass over the transposed slices, written back in the interleaved U layout
@@ -219,7 +239,7 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
     if (cp.adj_t == 2 || cp.adj_t == 3) {
       // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
-      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, w.z, target, acc, stream, err)
+      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err)
                                     : k_spass_adj(cp, w.z, target, acc, stream, err);
       if (st != LFM_OK) return fail(st, err);
     } else if (cp.adj_t) {
@@ -256,10 +276,22 @@ const char* lfm_version(void) { return "liblfm 0.1 (sm_100a)"; }
 int lfm_last_launch_count(void) { return g_last_launches; }
 
 // View-subset forward / adjoint (per-view path over the subset's ops, then rotation as usual).
+// A tensor-product subset (ViewOps::collapsed) runs on the collapsed two-pass path: band_v with the subset's s
+// composite (K/|S| included), then the camera's full t pass; otherwise the per-view ops of the subset.
+static bool subset_collapsed(const CameraPlan& cp, const ViewOps& vo) {
+  return vo.collapsed && vo.vf.d_img && vo.va.d_img && cp.fwd_split && cp.fwd_t == 3 && cp.adj_t == 3;
+}
+
 lfm_status forward_subset_impl(const CameraPlan& cp, int m, const float* x, float* y, const Ws& w, void* stream) {
   const ViewOps& vo = cp.subs[m];
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
+  if (subset_collapsed(cp, vo)) {
+    std::string err;
+    lfm_status st = k_vpass_fwd(cp, vo.vf, xr, w.z, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+    return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream);
+  }
   if (cp.info.type == LFM_PLENOPTIC) {
     TRY(sep(vo.fwd_s1, xr, w.f, 0, vo.n_views, 0, stream));
     return sep(vo.fwd_s3, w.f, y, 0, 1, 0, stream);
@@ -273,7 +305,12 @@ lfm_status adjoint_subset_impl(const CameraPlan& cp, int m, const float* y, floa
   const bool rot = cp.info.rot_passes != 0;
   float* target = rot ? w.r0 : x;
   const int acc = rot ? 0 : accumulate;
-  if (cp.info.type == LFM_PLENOPTIC) {
+  if (subset_collapsed(cp, vo)) {
+    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream));
+    std::string err;
+    lfm_status st = k_vpass_adj(cp, vo.va, w.z, target, acc, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+  } else if (cp.info.type == LFM_PLENOPTIC) {
     TRY(sep(vo.adj_s3, y, w.f, 0, vo.n_views, 0, stream));
     TRY(sep(vo.adj_s1, w.f, target, 0, cp.info.nz, acc, stream));
   } else {
@@ -344,6 +381,9 @@ lfm_status lfm_plan_info(lfm_plan p, int cam, lfm_info* out) {
   *out = p->cams[cam].info;
   out->kind_stage[0] = p->cams[cam].fwd_c2.kind;
   out->kind_stage[1] = p->cams[cam].adj_c1.kind;
+  out->subset_collapsed = 0;
+  if (p->device >= 0)
+    for (const ViewOps& vo : p->cams[cam].subs) out->subset_collapsed += subset_collapsed(p->cams[cam], vo) ? 1 : 0;
   return LFM_OK;
 }
 
@@ -489,6 +529,15 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
   } else if (stage == LFM_STAGE_ADJ_T) {
     if (!in) return fail(LFM_E_INVALID, "in is NULL");
     st = sep(cp.adj_c1, in, w.z, 0, 1, 0, stream);
+  } else if (stage == LFM_STAGE_FWD_S || stage == LFM_STAGE_ADJ_S) {
+    const bool fwd = stage == LFM_STAGE_FWD_S;
+    if (fwd ? !in : !out) return fail(LFM_E_INVALID, fwd ? "in is NULL" : "out is NULL");
+    if (fwd ? !(cp.fwd_split && (cp.fwd_t == 2 || cp.fwd_t == 3)) : !(cp.adj_t == 2 || cp.adj_t == 3))
+      return fail(LFM_E_INVALID, "the s pass of this camera is not a direct (band_v / spass) kernel");
+    std::string err;
+    st = fwd ? (cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, in, w.z, stream, err) : k_spass_fwd(cp, in, w.z, stream, err))
+             : (cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, out, 0, stream, err) : k_spass_adj(cp, w.z, out, 0, stream, err));
+    if (st != LFM_OK) return fail(st, err);
   } else {
     return fail(LFM_E_INVALID, "unknown stage");
   }

@@ -233,6 +233,95 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
   return dev_upload(&op.d_fp_t, vt.data(), vt.size() * sizeof(TileT), err);
 }
 
+static void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// band_v tables of one s composite (forward family f: rows = detector columns, K = vx; adjoint family a: rows = vx,
+// K = s).  Weights rounded once to fp32, then split hi = rn_tf32(w), lo = rn_tf32(w - hi); image element (row r, k)
+// at byte r*64 + k*4, bits [4,6) ^= [7,9) (64-byte swizzle) or r*128 + k*4 with bits [4,7) ^= [7,10) (128-byte).
+static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
+  T.N = N;
+  T.BK = BK;
+  T.n_nt = (f.n_rows + N - 1) / N;
+  T.off.assign((size_t)f.n_tables * T.n_nt + 1, 0);
+  T.k0.clear();
+  T.img.clear();
+  std::vector<char> any(f.n_src + 32);
+  const uint32_t smask = BK >= 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int t = 0; t < T.n_nt; ++t) {
+      T.off[(size_t)m * T.n_nt + t] = (int)T.k0.size();
+      std::fill(any.begin(), any.end(), 0);
+      const int r0 = t * N, r1 = std::min(f.n_rows, r0 + N);
+      for (int r = r0; r < r1; ++r) {
+        const size_t idx = (size_t)m * f.n_rows + r;
+        for (int e = 0; e < f.len[idx]; ++e)
+          if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e] = 1;
+      }
+      int last = -(1 << 30);
+      for (int kn = 0; kn < f.n_src; ++kn) {
+        if (!any[kn] || kn < last + BK) continue;
+        const int k = kn & ~3;  // TMA: the innermost box coordinate must sit on a 16-byte boundary
+        last = k;
+        T.k0.push_back(k);
+        const size_t base = T.img.size();
+        T.img.resize(base + (size_t)2 * BK * N, 0.f);
+        for (int r = r0; r < r1; ++r) {
+          const size_t idx = (size_t)m * f.n_rows + r;
+          for (int kk = 0; kk < BK; ++kk) {
+            const int e = k + kk - f.start[idx];
+            if (e < 0 || e >= f.len[idx]) continue;
+            const float w = (float)f.w64[idx * f.taps + e];
+            const float wh = tf32_host(w), wl = tf32_host(w - wh);
+            const int sub = BK < 32 ? BK : 32, sj = kk / sub;  // sub-images of one swizzle-atom row each
+            uint32_t o = (uint32_t)((r - r0) * sub * 4 + (kk % sub) * 4);
+            o ^= ((o >> 7) & smask) << 4;
+            const size_t so = (size_t)sj * N * sub;
+            T.img[base + so + o / 4] = wh;
+            T.img[base + (size_t)BK * N + so + o / 4] = wl;
+          }
+        }
+      }
+    }
+  T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
+}
+
+static void build_vtabs(const BandFamily& ff, const BandFamily& fa, VTab& vf, VTab& va) {
+  const int bk_f = std::getenv("LFM_VBK_F") ? std::atoi(std::getenv("LFM_VBK_F")) : 32;
+  const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
+  build_vtab(ff, 256, bk_f == 16 ? 16 : 32, vf);
+  const int vn_a = std::getenv("LFM_VN_A") ? std::atoi(std::getenv("LFM_VN_A")) : 16;
+  build_vtab(fa, vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : bk_a == 64 ? 64 : 32, va);
+  if (std::getenv("LFM_DEBUG"))
+    for (const VTab* T : {&vf, &va}) {
+      int mx = 0, mn = 1 << 30;
+      for (size_t i = 0; i + 1 < T->off.size(); ++i) {
+        mx = std::max(mx, T->off[i + 1] - T->off[i]);
+        mn = std::min(mn, T->off[i + 1] - T->off[i]);
+      }
+      std::fprintf(stderr, "[lfm] band_v N %d: items %zu blocks %zu (min %d max %d per item)\n", T->N,
+                   T->off.size() - 1, T->k0.size(), mn, mx);
+    }
+}
+
+static lfm_status upload_vtab(VTab& T, size_t& bytes, std::string& err) {
+  lfm_status st;
+  std::vector<int32_t> k0(T.k0);
+  k0.push_back(0);
+  if ((st = dev_upload(&T.d_off, T.off.data(), T.off.size() * 4, err)) != LFM_OK) return st;
+  if ((st = dev_upload(&T.d_k0, k0.data(), k0.size() * 4, err)) != LFM_OK) return st;
+  if (!T.img.empty() && (st = dev_upload(&T.d_img, T.img.data(), T.img.size() * 4, err)) != LFM_OK) return st;
+  bytes += T.off.size() * 4 + k0.size() * 4 + T.img.size() * 4;
+  std::vector<float>().swap(T.img);  // host copy not needed after upload
+  return LFM_OK;
+}
+
+static void free_vtab(VTab& T) {
+  dfree(T.d_off); dfree(T.d_k0); dfree(T.d_img);
+  T.d_off = nullptr; T.d_k0 = nullptr; T.d_img = nullptr;
+}
+
 lfm_status upload_camera(CameraPlan& cp, std::string& err) {
   size_t bytes = 0;
   lfm_status st;
@@ -259,82 +348,10 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
     }
   }
   // tcgen05 s passes (band_v.cuh): forward items (slice n, 256 detector columns), K = vx, from cf[0];
-  // adjoint items (slice n, 16 voxel columns), K = s, from ca[0].  Weights rounded once to fp32, then split
-  // hi = rn_tf32(w), lo = rn_tf32(w - hi); image element (row r, k) at byte r*64 + k*4, bits [4,6) ^= [7,9).
-  {
-    auto build = [&](const BandFamily& f, int N, int BK, CameraPlan::VTab& T) {
-      T.N = N;
-      T.BK = BK;
-      T.n_nt = (f.n_rows + N - 1) / N;
-      T.off.assign((size_t)f.n_tables * T.n_nt + 1, 0);
-      T.k0.clear();
-      T.img.clear();
-      std::vector<char> any(f.n_src + 32);
-      const uint32_t smask = BK >= 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
-      for (int m = 0; m < f.n_tables; ++m)
-        for (int t = 0; t < T.n_nt; ++t) {
-          T.off[(size_t)m * T.n_nt + t] = (int)T.k0.size();
-          std::fill(any.begin(), any.end(), 0);
-          const int r0 = t * N, r1 = std::min(f.n_rows, r0 + N);
-          for (int r = r0; r < r1; ++r) {
-            const size_t idx = (size_t)m * f.n_rows + r;
-            for (int e = 0; e < f.len[idx]; ++e)
-              if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e] = 1;
-          }
-          int last = -(1 << 30);
-          for (int kn = 0; kn < f.n_src; ++kn) {
-            if (!any[kn] || kn < last + BK) continue;
-            const int k = kn & ~3;  // TMA: the innermost box coordinate must sit on a 16-byte boundary
-            last = k;
-            T.k0.push_back(k);
-            const size_t base = T.img.size();
-            T.img.resize(base + (size_t)2 * BK * N, 0.f);
-            for (int r = r0; r < r1; ++r) {
-              const size_t idx = (size_t)m * f.n_rows + r;
-              for (int kk = 0; kk < BK; ++kk) {
-                const int e = k + kk - f.start[idx];
-                if (e < 0 || e >= f.len[idx]) continue;
-                const float w = (float)f.w64[idx * f.taps + e];
-                const float wh = tf32_host(w), wl = tf32_host(w - wh);
-                const int sub = BK < 32 ? BK : 32, sj = kk / sub;  // sub-images of one swizzle-atom row each
-                uint32_t o = (uint32_t)((r - r0) * sub * 4 + (kk % sub) * 4);
-                o ^= ((o >> 7) & smask) << 4;
-                const size_t so = (size_t)sj * N * sub;
-                T.img[base + so + o / 4] = wh;
-                T.img[base + (size_t)BK * N + so + o / 4] = wl;
-              }
-            }
-          }
-        }
-      T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
-    };
-    const int bk_f = std::getenv("LFM_VBK_F") ? std::atoi(std::getenv("LFM_VBK_F")) : 32;
-    const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
-    build(cp.cf[0], 256, bk_f == 16 ? 16 : 32, cp.vf);
-    const int vn_a = std::getenv("LFM_VN_A") ? std::atoi(std::getenv("LFM_VN_A")) : 16;
-    build(cp.ca[0], vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : bk_a == 64 ? 64 : 32, cp.va);
-    if (std::getenv("LFM_DEBUG"))
-      for (const CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
-        int mx = 0, mn = 1 << 30;
-        for (size_t i = 0; i + 1 < T->off.size(); ++i) {
-          mx = std::max(mx, T->off[i + 1] - T->off[i]);
-          mn = std::min(mn, T->off[i + 1] - T->off[i]);
-        }
-        int kmin = 1 << 30, kmax = -1;
-        for (int k : T->k0) { kmin = std::min(kmin, k); kmax = std::max(kmax, k); }
-        std::fprintf(stderr, "[lfm] band_v N %d: items %zu blocks %zu (min %d max %d per item) k0 in [%d, %d]\n", T->N,
-                     T->off.size() - 1, T->k0.size(), mn, mx, kmin, kmax);
-      }
-    for (CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
-      std::vector<int32_t> k0(T->k0);
-      k0.push_back(0);
-      if ((st = dev_upload(&T->d_off, T->off.data(), T->off.size() * 4, err)) != LFM_OK) return st;
-      if ((st = dev_upload(&T->d_k0, k0.data(), k0.size() * 4, err)) != LFM_OK) return st;
-      if (!T->img.empty() && (st = dev_upload(&T->d_img, T->img.data(), T->img.size() * 4, err)) != LFM_OK) return st;
-      bytes += T->off.size() * 4 + k0.size() * 4 + T->img.size() * 4;
-      std::vector<float>().swap(T->img);  // host copy not needed after upload
-    }
-  }
+  // adjoint items (slice n, 16 voxel columns), K = s, from ca[0]
+  build_vtabs(cp.cf[0], cp.ca[0], cp.vf, cp.va);
+  for (VTab* T : {&cp.vf, &cp.va})
+    if ((st = upload_vtab(*T, bytes, err)) != LFM_OK) return st;
   cp.info.table_bytes = bytes;
   return LFM_OK;
 }
@@ -451,7 +468,7 @@ static lfm_status encode3(CUtensorMap* map, const float* base, const long long d
 }
 
 template <int N, int DIR, int BK>
-static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
+static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err) {
   static bool attr[LFM_MAX_DEV];
   const int dv = cur_dev();
@@ -476,44 +493,40 @@ static lfm_status launch_band_v(const CameraPlan::VTab& T, const CUtensorMap& am
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
 
-lfm_status k_vpass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err) {
+lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
-  if (!cp.vf.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
+  if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
-  const int ab[3] = {cp.vf.BK, 128, 1};
-  lfm_status st = encode3(&am, x, ad, as, ab, cp.vf.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
+  const int ab[3] = {T.BK, 128, 1};
+  lfm_status st = encode3(&am, x, ad, as, ab, T.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
   const int ob[3] = {32, 1, 32};
   if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
-  return cp.vf.BK == 32 ? launch_band_v<256, 0, 32>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err)
-                        : launch_band_v<256, 0, 16>(cp.vf, am, om, nz, ny, 1.f, 0, stream, err);
+  return T.BK == 32 ? launch_band_v<256, 0, 32>(T, am, om, nz, ny, 1.f, 0, stream, err)
+                    : launch_band_v<256, 0, 16>(T, am, om, nz, ny, 1.f, 0, stream, err);
 }
 
-lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err) {
+lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
+                       std::string& err) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
-  if (!cp.va.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
+  if (!T.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const long long ad[3] = {nd, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
-  const int ab[3] = {cp.va.BK < 32 ? cp.va.BK : 32, 1, 128};
-  lfm_status st = encode3(&am, Z, ad, as, ab, cp.va.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
+  const int ab[3] = {T.BK < 32 ? T.BK : 32, 1, 128};
+  lfm_status st = encode3(&am, Z, ad, as, ab, T.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
   const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
-  const int ob[3] = {cp.va.N / 2, 32, 1};
+  const int ob[3] = {T.N / 2, 32, 1};
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
   const float sc = cp.adj_c2.out_scale;
-  if (cp.va.N == 32)
-    return cp.va.BK == 32 ? launch_band_v<32, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
-                          : launch_band_v<32, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
-  if (cp.va.BK == 64) return launch_band_v<16, 1, 64>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
-  return cp.va.BK == 32 ? launch_band_v<16, 1, 32>(cp.va, am, om, nz, ny, sc, accumulate, stream, err)
-                        : launch_band_v<16, 1, 16>(cp.va, am, om, nz, ny, sc, accumulate, stream, err);
-}
-
-
-static void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (T.N == 32)
+    return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err)
+                      : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err);
+  if (T.BK == 64) return launch_band_v<16, 1, 64>(T, am, om, nz, ny, sc, accumulate, stream, err);
+  return T.BK == 32 ? launch_band_v<16, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err)
+                    : launch_band_v<16, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err);
 }
 
 // Subset ops reuse the tile configuration the autotuner chose for the full per-view op (same tables,
@@ -521,6 +534,13 @@ static void dfree(void* p) {
 lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
   size_t bytes = 0;
   for (ViewOps& vo : cp.subs) {
+    if (vo.collapsed) {
+      build_vtabs(vo.cfs, vo.cas, vo.vf, vo.va);
+      for (VTab* T : {&vo.vf, &vo.va}) {
+        lfm_status st = upload_vtab(*T, bytes, err);
+        if (st != LFM_OK) return st;
+      }
+    }
     SepOp* pairs[][2] = {{&vo.fwd_s1, &cp.fwd_s1}, {&vo.fwd_s3, &cp.fwd_s3}, {&vo.adj_s3, &cp.adj_s3},
                          {&vo.adj_s1, &cp.adj_s1}};
     for (auto& pr : pairs) {
@@ -538,9 +558,10 @@ lfm_status prepare_subsets(CameraPlan& cp, std::string& err) {
 }
 
 void free_camera(CameraPlan& cp) {
-  for (CameraPlan::VTab* T : {&cp.vf, &cp.va}) {
-    dfree(T->d_off); dfree(T->d_k0); dfree(T->d_img);
-    T->d_off = nullptr; T->d_k0 = nullptr; T->d_img = nullptr;
+  for (VTab* T : {&cp.vf, &cp.va}) free_vtab(*T);
+  for (ViewOps& vo : cp.subs) {
+    free_vtab(vo.vf);
+    free_vtab(vo.va);
   }
 
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
@@ -2370,6 +2391,111 @@ __global__ void __launch_bounds__(256) shear_x4_kernel(const float* __restrict__
   }
 }
 
+// Fused in-plane rotation of a yaw pose (only the z and x shear passes active; both act inside the y-plane,
+// eqn,rot,decomp with D_y = 1): one CTA per y-plane holds the whole nz x nx plane in shared memory, applies the two
+// passes there and writes the plane once -- 8 B of HBM per voxel for the rotation instead of 8 B per pass, one
+// launch instead of two.  Forward (ORDER 0): E^x (E^z in); adjoint (ORDER 1): E^zT (E^xT in) with the transposed
+// tables.  Per output the taps are summed in the same ascending order with the same fp32 FMAs as shear_kernel /
+// shear_x4_kernel, so the result is bit-identical to the two-kernel path.
+constexpr int RZX_THREADS = 1024;
+template <int TZ, int TX, int ORDER>
+__global__ void __launch_bounds__(RZX_THREADS, 1) rot_zx_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                                const int32_t* __restrict__ mz, const float* __restrict__ wz,
+                                                                const int32_t* __restrict__ mx, const float* __restrict__ wx,
+                                                                int nx, int ny, int nz, int accumulate) {
+  extern __shared__ float rzx[];
+  float* A = rzx;                    // [nz][nx]: the input plane, later the result
+  float* B = rzx + (size_t)nz * nx;  // [nz][nx]: after the first pass
+  const int iy = blockIdx.x, t = threadIdx.x;
+  const size_t plane = (size_t)nx * ny;
+  const int nx4 = nx >> 2;
+  for (int e = t; e < nz * nx4; e += RZX_THREADS) {
+    const int z = e / nx4, x4 = e - z * nx4;
+    reinterpret_cast<float4*>(A)[e] = __ldg(reinterpret_cast<const float4*>(in + (size_t)z * plane + (size_t)iy * nx) + x4);
+  }
+  __syncthreads();
+  // z pass over column x (line x + nx*iy): out(x, z) = sum_k wz[k] A[z + m + k][x]; a thread keeps one column
+  // (RZX_THREADS % nx == 0, checked by the launcher), so its shift and weights are loaded once
+  auto zpass = [&](const float* S, float* D) {
+    const int x = t % nx, line = x + nx * iy, zstep = RZX_THREADS / nx;
+    const int m0 = __ldg(mz + line);
+    float wk[TZ];
+#pragma unroll
+    for (int k = 0; k < TZ; ++k) wk[k] = __ldg(wz + (size_t)line * TZ + k);
+    for (int z = t / nx; z < nz; z += zstep) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < TZ; ++k) {
+        const int j = z + m0 + k;
+        const float v = (j >= 0 && j < nz) ? S[(size_t)j * nx + x] : 0.f;
+        acc = fmaf(wk[k], v, acc);
+      }
+      D[(size_t)z * nx + x] = acc;
+    }
+  };
+  // x pass over row z (line iy + ny*z): out(x, z) = sum_k wx[k] S[z][x + m + k]
+  auto xpass = [&](const float* S, float* D) {
+    for (int e = t; e < nx * nz; e += RZX_THREADS) {
+      const int x = e % nx, z = e / nx;
+      const int line = iy + ny * z;
+      const int m0 = __ldg(mx + line);
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < TX; ++k) {
+        const int j = x + m0 + k;
+        const float v = (j >= 0 && j < nx) ? S[(size_t)z * nx + j] : 0.f;
+        acc = fmaf(__ldg(wx + (size_t)line * TX + k), v, acc);
+      }
+      D[(size_t)z * nx + x] = acc;
+    }
+  };
+  if (ORDER == 0) { zpass(A, B); __syncthreads(); xpass(B, A); }
+  else { xpass(A, B); __syncthreads(); zpass(B, A); }
+  __syncthreads();
+  for (int e = t; e < nz * nx4; e += RZX_THREADS) {
+    const int z = e / nx4, x4 = e - z * nx4;
+    float4* o = reinterpret_cast<float4*>(out + (size_t)z * plane + (size_t)iy * nx) + x4;
+    float4 r = reinterpret_cast<const float4*>(A)[e];
+    if (accumulate) {
+      const float4 p = *o;
+      r.x = p.x + r.x; r.y = p.y + r.y; r.z = p.z + r.z; r.w = p.w + r.w;
+    }
+    *o = r;
+  }
+}
+
+// Both passes of a yaw rotation in one launch when the plane fits in shared memory; returns false (nothing
+// launched) when the fused form does not apply.
+bool launch_rot_zx(const ShearPass& pz, const ShearPass& px, int dir, const float* in, float* out, int nx, int ny,
+                   int nz, int accumulate, void* stream, lfm_status& st, std::string& err) {
+  static const bool off = std::getenv("LFM_NO_ROT_FUSE") != nullptr;
+  const size_t smem = (size_t)2 * nx * nz * 4;
+  if (off || !pz.active || !px.active || pz.axis != 0 || px.axis != 1 || nx % 4 || RZX_THREADS % nx || smem > 200 * 1024 ||
+      (((uintptr_t)in | (uintptr_t)out) & 15) || pz.taps > 8 || px.taps > 8)
+    return false;
+  static bool attr[LFM_MAX_DEV][2][2][2];
+  const int dv = cur_dev(), iz_ = pz.taps == 8, ix_ = px.taps == 8;
+  cudaStream_t s = (cudaStream_t)stream;
+#define LFM_RZX(TZ_, TX_, O_)                                                                                        \
+  {                                                                                                                  \
+    if (!attr[dv][iz_][ix_][O_]) {                                                                                   \
+      cudaFuncSetAttribute(rot_zx_kernel<TZ_, TX_, O_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);    \
+      attr[dv][iz_][ix_][O_] = true;                                                                                 \
+    }                                                                                                                \
+    rot_zx_kernel<TZ_, TX_, O_><<<ny, RZX_THREADS, smem, s>>>(in, out, pz.d_mlo[dir], pz.d_w[dir], px.d_mlo[dir],    \
+                                                              px.d_w[dir], nx, ny, nz, accumulate);                  \
+  }
+  if (dir == 0) {
+    if (!iz_ && !ix_) LFM_RZX(4, 4, 0) else if (!iz_) LFM_RZX(4, 8, 0) else if (!ix_) LFM_RZX(8, 4, 0) else LFM_RZX(8, 8, 0)
+  } else {
+    if (!iz_ && !ix_) LFM_RZX(4, 4, 1) else if (!iz_) LFM_RZX(4, 8, 1) else if (!ix_) LFM_RZX(8, 4, 1) else LFM_RZX(8, 8, 1)
+  }
+#undef LFM_RZX
+  ++g_launches;
+  st = cuda_check(cudaGetLastError(), "rot_zx_kernel launch", err);
+  return true;
+}
+
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
   // z chunk per thread: the z pass reads a sliding window of ZC + TAPS - 1 values per ZC outputs, so longer
@@ -2490,28 +2616,51 @@ __device__ inline void block_sum_store(double (&v)[NV], double* part) {
   }
 }
 
-// stats: [sum w y Ax, sum w y y, sum w Ax Ax]
+// stats: [sum w y Ax, sum w y y, sum w Ax Ax] (fp64 products and sums; float4 loads when the three vectors are
+// 16-byte aligned, the n % 4 tail by the first threads)
+template <bool VEC>
 __global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float* __restrict__ Ax,
                                                                     const float* __restrict__ y,
                                                                     const float* __restrict__ w, long long n,
                                                                     double* part) {
   double v[3] = {0, 0, 0};
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double a = Ax[i], yy = y[i], ww = w[i];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+  auto acc = [&](double a, double yy, double ww) {
     v[0] += ww * yy * a;
     v[1] += ww * yy * yy;
     v[2] += ww * a * a;
+  };
+  long long i0 = t;
+  if (VEC) {
+    const long long n4 = n >> 2;
+    for (long long i = t; i < n4; i += stride) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(Ax) + i);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(y) + i);
+      const float4 c = __ldg(reinterpret_cast<const float4*>(w) + i);
+      acc(a.x, b.x, c.x); acc(a.y, b.y, c.y); acc(a.z, b.z, c.z); acc(a.w, b.w, c.w);
+    }
+    i0 = 4 * n4 + t;
   }
+  for (long long i = i0; i < n; i += stride) acc(Ax[i], y[i], w[i]);
   block_sum_store<3>(v, part);
 }
 
-__global__ void reduce_final_kernel(const double* __restrict__ part, int nblocks, int nv, double* out, int accumulate) {
-  // one thread per value, fixed order: deterministic
-  int q = threadIdx.x;
-  if (q >= nv) return;
+// final sum of nblocks block partials per value: one block of 256 threads per value q, thread t adds the partials
+// b = t, t + 256, ... in order, then a fixed-shape tree -- the same order every run (deterministic), and the
+// partial loads are spread over 256 threads instead of one dependent chain
+__global__ void __launch_bounds__(256) reduce_final_kernel(const double* __restrict__ part, int nblocks, int nv,
+                                                           double* out, int accumulate) {
+  __shared__ double sh[256];
+  const int q = blockIdx.x, t = threadIdx.x;
   double s = 0;
-  for (int b = 0; b < nblocks; ++b) s += part[(size_t)b * nv + q];
-  out[q] = accumulate ? out[q] + s : s;
+  for (int b = t; b < nblocks; b += 256) s += part[(size_t)b * nv + q];
+  sh[t] = s;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (t < h) sh[t] += sh[t + h];
+    __syncthreads();
+  }
+  if (t == 0) out[q] = accumulate ? out[q] + sh[0] : sh[0];
 }
 
 __global__ void gains_kernel(const double* __restrict__ stats, int n_cam, double* gamma, int* flag) {
@@ -2526,53 +2675,102 @@ __global__ void gains_kernel(const double* __restrict__ stats, int n_cam, double
   if (flag) *flag = bad;
 }
 
-// r = w (Ax - gamma y); partial 1/2 sum w (Ax - gamma y)^2
+// r = w (Ax - gamma y); partial 1/2 sum w (Ax - gamma y)^2 (COST only); float4 form when aligned
+template <bool VEC, bool COST>
 __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const float* __restrict__ Ax, const float* __restrict__ y,
                                                                const float* __restrict__ w,
                                                                const double* __restrict__ gamma, int cam,
                                                                float* __restrict__ r, long long n, double* part) {
   const float g = (float)gamma[cam];
   double v[1] = {0};
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float d = Ax[i] - g * y[i];
-    r[i] = w[i] * d;
-    if (part) v[0] += 0.5 * (double)w[i] * (double)d * (double)d;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x, stride = (long long)gridDim.x * blockDim.x;
+  auto one = [&](float a, float b, float c) {
+    const float d = a - g * b;
+    if (COST) v[0] += 0.5 * (double)c * (double)d * (double)d;
+    return c * d;
+  };
+  long long i0 = t;
+  if (VEC) {
+    const long long n4 = n >> 2;
+    for (long long i = t; i < n4; i += stride) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(Ax) + i);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(y) + i);
+      const float4 c = __ldg(reinterpret_cast<const float4*>(w) + i);
+      const float r0 = one(a.x, b.x, c.x), r1 = one(a.y, b.y, c.y), r2 = one(a.z, b.z, c.z), r3 = one(a.w, b.w, c.w);
+      reinterpret_cast<float4*>(r)[i] = make_float4(r0, r1, r2, r3);
+    }
+    i0 = 4 * n4 + t;
   }
-  if (part) block_sum_store<1>(v, part);
+  for (long long i = i0; i < n; i += stride) r[i] = one(Ax[i], y[i], w[i]);
+  if (COST) block_sum_store<1>(v, part);
 }
 
-// grad += beta * sum_{l in N_j, in grid} (x_j - x_l) + nu;  partial [nu*x_j + (beta/4) sum_l (x_j-x_l)^2]
-__global__ void __launch_bounds__(RED_THREADS) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad,
-                                                            int nx, int ny, int nz, float beta, float nu,
-                                                            double* part) {
-  long long n = (long long)nx * ny * nz;
-  double v[1] = {0};
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    int ix = (int)(i % nx);
-    long long r = i / nx;
-    int iy = (int)(r % ny), iz = (int)(r / ny);
-    float xj = x[i];
-    float g = 0.f;
-    double rs = 0;
-    for (int dz = -1; dz <= 1; ++dz) {
-      int zz = iz + dz;
-      if (zz < 0 || zz >= nz) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        int yy = iy + dy;
-        if (yy < 0 || yy >= ny) continue;
-        for (int dx = -1; dx <= 1; ++dx) {
-          int xx = ix + dx;
-          if (xx < 0 || xx >= nx || (dx == 0 && dy == 0 && dz == 0)) continue;
-          float d = xj - x[((long long)zz * ny + yy) * nx + xx];
-          g += d;
-          rs += (double)d * (double)d;
-        }
-      }
+// grad += beta * sum_{l in N_j, in grid} (x_j - x_l) + nu;  partial [nu*x_j + (beta/4) sum_l (x_j-x_l)^2] (COST)
+// Tiled: a block owns 32 x 8 (x, y) columns and a chunk of R26_ZC slices; the three planes z-1, z, z+1 of the
+// (32+2) x (8+2) footprint rotate through shared memory, so every x value is read from HBM/L2 about once per
+// chunk instead of 27 times through L1.  Neighbours outside the grid contribute nothing (the validity of each
+// of the 26 offsets is a per-thread select); the sum over l runs in the order dz, dy, dx ascending.
+constexpr int R26_ZC = 16;
+template <bool COST>
+__global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad, int nx,
+                                                    int ny, int nz, float beta, float nu, double* part) {
+  __shared__ float pl[3][10][36];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8, z0 = blockIdx.z * R26_ZC;
+  const int ix = x0 + tx, iy = y0 + ty;
+  const size_t plane = (size_t)nx * ny;
+  auto load = [&](int slot, int zz) {
+    for (int e = tid; e < 340; e += 256) {
+      const int ly = e / 34, lx = e % 34, gx = x0 + lx - 1, gy = y0 + ly - 1;
+      pl[slot][ly][lx] = (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
+                             ? __ldg(x + (size_t)zz * plane + (size_t)gy * nx + gx) : 0.f;
     }
-    grad[i] += beta * g + nu;
-    if (part) v[0] += (double)nu * xj + 0.25 * (double)beta * rs;
+  };
+  load(0, z0 - 1);
+  load(1, z0);
+  const bool vx[3] = {ix > 0, true, ix < nx - 1}, vy[3] = {iy > 0, true, iy < ny - 1};
+  double v = 0;
+  for (int q = 0; q < R26_ZC; ++q) {
+    const int iz = z0 + q;
+    if (iz >= nz) break;
+    load((q + 2) % 3, iz + 1);
+    __syncthreads();
+    if (ix < nx && iy < ny) {
+      const bool vz[3] = {iz > 0, true, iz < nz - 1};
+      const int sl[3] = {q % 3, (q + 1) % 3, (q + 2) % 3};   // planes z-1, z, z+1
+      const float xj = pl[sl[1]][ty + 1][tx + 1];
+      float g = 0.f;
+      double rs = 0;
+#pragma unroll
+      for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+            if (dz == 1 && dy == 1 && dx == 1) continue;
+            const float d = xj - pl[sl[dz]][ty + dy][tx + dx];
+            const bool ok = vz[dz] && vy[dy] && vx[dx];
+            g += ok ? d : 0.f;
+            if (COST) rs += ok ? (double)d * (double)d : 0.0;
+          }
+      const size_t i = (size_t)iz * plane + (size_t)iy * nx + ix;
+      grad[i] += beta * g + nu;
+      if (COST) v += (double)nu * xj + 0.25 * (double)beta * rs;
+    }
+    __syncthreads();
   }
-  if (part) block_sum_store<1>(v, part);
+  if (COST) {
+    // block partial (256 threads = 8 warps), fixed order
+    __shared__ double sh[8];
+    const double a = warp_sum(v);
+    if (tx == 0) sh[ty] = a;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0;
+      for (int w = 0; w < 8; ++w) t += sh[w];
+      part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+  }
 }
 
 __global__ void fista_kernel(float* __restrict__ x, float* __restrict__ z, const float* __restrict__ grad,
@@ -2582,6 +2780,29 @@ __global__ void fista_kernel(float* __restrict__ x, float* __restrict__ z, const
     z[i] = xn + tau * (xn - x[i]);
     x[i] = xn;
   }
+}
+
+// float4 form (all four vectors 16-byte aligned): the same per-element arithmetic, the n % 4 tail by the first threads
+__device__ __forceinline__ void fista_one(float& xv, float& zv, float gv, float dv, float tau) {
+  const float xn = fmaxf(0.f, zv - gv / dv);
+  zv = xn + tau * (xn - xv);
+  xv = xn;
+}
+__global__ void fista4_kernel(float* __restrict__ x, float* __restrict__ z, const float* __restrict__ grad,
+                              const float* __restrict__ d, long long n, float tau) {
+  const long long n4 = n >> 2, stride = (long long)gridDim.x * blockDim.x;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = t; i < n4; i += stride) {
+    float4 xv = reinterpret_cast<float4*>(x)[i], zv = reinterpret_cast<float4*>(z)[i];
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(grad) + i), dv = __ldg(reinterpret_cast<const float4*>(d) + i);
+    fista_one(xv.x, zv.x, gv.x, dv.x, tau);
+    fista_one(xv.y, zv.y, gv.y, dv.y, tau);
+    fista_one(xv.z, zv.z, gv.z, dv.z, tau);
+    fista_one(xv.w, zv.w, gv.w, dv.w, tau);
+    reinterpret_cast<float4*>(x)[i] = xv;
+    reinterpret_cast<float4*>(z)[i] = zv;
+  }
+  for (long long i = 4 * n4 + t; i < n; i += stride) fista_one(x[i], z[i], grad[i], d[i], tau);
 }
 
 __global__ void majoriser_finish_kernel(float* __restrict__ d, long long n, float add) {
@@ -2609,10 +2830,15 @@ lfm_status k_mul(const float* a, const float* b, float* out, long long n, void* 
   ++g_launches;
   return cuda_check(cudaGetLastError(), "mul", err);
 }
+static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 lfm_status k_stats(const float* Ax, const float* y, const float* w, long long n, double* part, double* out, void* s,
                    std::string& err) {
-  stats_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
-  reduce_final_kernel<<<1, 32, 0, (cudaStream_t)s>>>(part, RED_BLOCKS, 3, out, 0);
+  if (al16(Ax) && al16(y) && al16(w))
+    stats_partial_kernel<true><<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
+  else
+    stats_partial_kernel<false><<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
+  reduce_final_kernel<<<3, 256, 0, (cudaStream_t)s>>>(part, RED_BLOCKS, 3, out, 0);
   g_launches += 2;
   return cuda_check(cudaGetLastError(), "stats", err);
 }
@@ -2623,27 +2849,41 @@ lfm_status k_gains(const double* stats, int n_cam, double* gamma, int* flag, voi
 }
 lfm_status k_residual(const float* Ax, const float* y, const float* w, const double* gamma, int cam, float* r,
                       long long n, double* part, double* cost, int cost_acc, void* s, std::string& err) {
-  residual_kernel<<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, gamma, cam, r, n, cost ? part : nullptr);
-  ++g_launches;
+  const bool vec = al16(Ax) && al16(y) && al16(w) && al16(r);
+  cudaStream_t st = (cudaStream_t)s;
   if (cost) {
-    reduce_final_kernel<<<1, 32, 0, (cudaStream_t)s>>>(part, RED_BLOCKS, 1, cost, cost_acc);
+    if (vec) residual_kernel<true, true><<<RED_BLOCKS, RED_THREADS, 0, st>>>(Ax, y, w, gamma, cam, r, n, part);
+    else residual_kernel<false, true><<<RED_BLOCKS, RED_THREADS, 0, st>>>(Ax, y, w, gamma, cam, r, n, part);
+    reduce_final_kernel<<<1, 256, 0, st>>>(part, RED_BLOCKS, 1, cost, cost_acc);
+    g_launches += 2;
+  } else {
+    if (vec) residual_kernel<true, false><<<ew_grid((n + 3) / 4), RED_THREADS, 0, st>>>(Ax, y, w, gamma, cam, r, n, nullptr);
+    else residual_kernel<false, false><<<ew_grid(n), RED_THREADS, 0, st>>>(Ax, y, w, gamma, cam, r, n, nullptr);
     ++g_launches;
   }
   return cuda_check(cudaGetLastError(), "residual", err);
 }
 lfm_status k_reg26(const float* x, float* grad, int nx, int ny, int nz, float beta, float nu, double* part,
                    double* cost, void* s, std::string& err) {
-  reg26_kernel<<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, cost ? part : nullptr);
-  ++g_launches;
+  dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + R26_ZC - 1) / R26_ZC), blk(32, 8);
+  const long long nblk = (long long)grid.x * grid.y * grid.z;
+  if (cost && nblk > 4096 * 4) { err = "reg26: volume too large for the reduction partials"; return LFM_E_INVALID; }
   if (cost) {
-    reduce_final_kernel<<<1, 32, 0, (cudaStream_t)s>>>(part, RED_BLOCKS, 1, cost, 0);
+    reg26_kernel<true><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, part);
+    reduce_final_kernel<<<1, 256, 0, (cudaStream_t)s>>>(part, (int)nblk, 1, cost, 0);
+    g_launches += 2;
+  } else {
+    reg26_kernel<false><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, nullptr);
     ++g_launches;
   }
   return cuda_check(cudaGetLastError(), "reg26", err);
 }
 lfm_status k_fista(float* x, float* z, const float* grad, const float* d, long long n, float tau, void* s,
                    std::string& err) {
-  fista_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)s>>>(x, z, grad, d, n, tau);
+  if (al16(x) && al16(z) && al16(grad) && al16(d))
+    fista4_kernel<<<ew_grid((n + 3) / 4), 256, 0, (cudaStream_t)s>>>(x, z, grad, d, n, tau);
+  else
+    fista_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)s>>>(x, z, grad, d, n, tau);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "fista", err);
 }
@@ -3142,8 +3382,8 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
       cp.spa_vta = (t_sa4 > 0 && (t_sa8 <= 0 || t_sa4 < t_sa8)) ? 4 : 8;
       const float t_sa = cp.spa_vta == 4 ? t_sa4 : t_sa8;
       float adj_s = cp.adj_t ? t_z + op_best[10] : op_best[6];
-      const float t_vf = std::getenv("LFM_NO_VF") ? -1.f : time2([&] { return k_vpass_fwd(cp, sb, ob, nullptr, terr); });
-      const float t_va = std::getenv("LFM_NO_VA") ? -1.f : time2([&] { return k_vpass_adj(cp, sb, ob, 0, nullptr, terr); });
+      const float t_vf = std::getenv("LFM_NO_VF") ? -1.f : time2([&] { return k_vpass_fwd(cp, cp.vf, sb, ob, nullptr, terr); });
+      const float t_va = std::getenv("LFM_NO_VA") ? -1.f : time2([&] { return k_vpass_adj(cp, cp.va, sb, ob, 0, nullptr, terr); });
       if (dbg)
         std::fprintf(stderr, "[lfm] direct s passes: fwd %.3f / tc %.3f ms (vs %.3f), adj %.3f / tc %.3f ms (vs %.3f) x2\n",
                      t_sf, t_vf, fwd_s, t_sa, t_va, adj_s);

@@ -158,10 +158,26 @@ struct ShearPass {
   float* d_w[2] = {nullptr, nullptr};
 };
 
+// tcgen05 s-pass tables (band_v.cuh): per item (slice n, N-tile) the K blocks and the N x BK hi/lo images
+struct VTab {
+  int N = 0, n_nt = 0, BK = 16;
+  std::vector<int32_t> off, k0;
+  std::vector<float> img;
+  int32_t* d_off = nullptr;
+  int32_t* d_k0 = nullptr;
+  float* d_img = nullptr;
+};
+
 // Per-view ops restricted to one view subset (sec,subset): compact field slots j <-> views S[j].
+// When the subset is a tensor product S = S_s x {all k_t} (M | K_s, reading R5's k = k_t K_s + k_s), the
+// subset operator is also K-collapsible: C^S_{s,n} = (K/|S|) sum_{k_s in S_s} S_ks B_ks,n, the t composite being
+// the full one -- then `collapsed` is set and the subset runs on the collapsed two-pass path with these s tables.
 struct ViewOps {
   SepOp fwd_s1, fwd_s3, adj_s3, adj_s1;
   int n_views = 0;
+  int collapsed = 0;
+  BandFamily cfs, cas;   // subset s composites (forward C^S_s,n and its transpose), K/|S| included
+  VTab vf, va;           // their band_v tables
 };
 
 struct CameraPlan {
@@ -186,15 +202,9 @@ struct CameraPlan {
   std::vector<ViewOps> subs;              // view-subset ops (lfm_geometry.n_subsets > 1)
   double scal[8];                         // c1, c3, Va, Vmu_or_Vd, dz_r, V_axis..., see plan.cpp
   int spa_vta = 8;                        // voxel rows per CTA of the direct adjoint s pass (4 or 8, autotuned)
-  // tcgen05 s passes (band_v.cuh): per item (slice n, N-tile) the K blocks of 16 and the N x 16 hi/lo images
-  struct VTab {
-    int N = 0, n_nt = 0, BK = 16;
-    std::vector<int32_t> off, k0;
-    std::vector<float> img;
-    int32_t* d_off = nullptr;
-    int32_t* d_k0 = nullptr;
-    float* d_img = nullptr;
-  } vf, va;
+  // tcgen05 s passes (band_v.cuh): forward (from cf[0]) and adjoint (from ca[0]) tables
+  using VTab = lfm::VTab;
+  VTab vf, va;
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
 };
 
@@ -228,8 +238,9 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
 lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
-lfm_status k_vpass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
-lfm_status k_vpass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
+lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err);
+lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
+                       std::string& err);
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);

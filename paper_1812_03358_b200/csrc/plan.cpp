@@ -948,6 +948,82 @@ bool sep_choose_tile(SepOp& op) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Collapsed composite of one axis over the views k_axis with kmask[k] != 0, per slice n (NEXT-1):
+//   C_n = scale * sum_k S_k B_{k,n} (plenoptic, S_k the masked lenslet stage) or scale * sum_k B_{k,n} (single),
+// built in fp64 from the per-view band tables; cf = C_n (rows: detector cells), ca = C_n^T (rows: voxel cells).
+// The band of a composite row is the union of the S1 bands its non-zero S3 entries reach (structural zeros
+// between two lenslets' cells are skipped).
+static void build_composite(const CameraPlan& cp, int ax, const std::vector<char>& kmask, double scale, int nz,
+                            int nrow, int nv, bool plen, BandFamily& cf, BandFamily& ca) {
+  const BandFamily& f1 = cp.s1f[ax];
+  const int Kax = (int)kmask.size();
+  const int keep_f = cf.want_mseg, keep_a = ca.want_mseg;
+  family_init(cf, nz, nrow, nv);
+  family_init(ca, nz, nv, nrow);
+  cf.want_mseg = keep_f;
+  ca.want_mseg = keep_a;
+  FamilyBuilder bf(cf), ba(ca);
+  bf.tabs.resize(nz);
+  ba.tabs.resize(nz);
+  std::vector<double> accv(nv);
+  std::vector<char> touched(nv);
+  for (int n = 0; n < nz; ++n) {
+    auto& rows = bf.tabs[n];
+    rows.assign(nrow, Row());
+    std::vector<std::vector<std::pair<int, double>>> cols(nv);  // transpose
+    for (int i = 0; i < nrow; ++i) {
+      std::fill(accv.begin(), accv.end(), 0.0);
+      std::fill(touched.begin(), touched.end(), 0);
+      int vlo = 1 << 30, vhi = -1;
+      for (int k = 0; k < Kax; ++k) {
+        if (!kmask[k]) continue;
+        auto add_s1 = [&](int j, double w3) {
+          size_t idx = (size_t)(k * nz + n) * f1.n_rows + j;
+          for (int q = 0; q < f1.len[idx]; ++q) {
+            int v = f1.start[idx] + q;
+            accv[v] += w3 * f1.w64[idx * f1.taps + q];
+            touched[v] = 1;
+            vlo = std::min(vlo, v);
+            vhi = std::max(vhi, v);
+          }
+        };
+        if (plen) {
+          const BandFamily& f3 = cp.s3f[ax];
+          size_t i3 = (size_t)k * f3.n_rows + i;
+          for (int q = 0; q < f3.len[i3]; ++q) {
+            double w3 = f3.w64[i3 * f3.taps + q];
+            if (w3 == 0.0) continue;  // gap between two lenslets' cells (structural zero)
+            add_s1(f3.start[i3] + q, w3);
+          }
+        } else {
+          add_s1(i, 1.0);
+        }
+      }
+      if (vhi < 0) continue;
+      Row& r = rows[i];
+      r.lo = vlo;
+      r.len = vhi - vlo + 1;
+      r.w.assign(r.len, 0.0);
+      for (int v = vlo; v <= vhi; ++v) {
+        r.w[v - vlo] = scale * accv[v];
+        if (touched[v]) cols[v].push_back({i, scale * accv[v]});
+      }
+    }
+    auto& arows = ba.tabs[n];
+    arows.assign(nv, Row());
+    for (int v = 0; v < nv; ++v) {
+      if (cols[v].empty()) continue;
+      Row& r = arows[v];
+      r.lo = cols[v].front().first;
+      r.len = cols[v].back().first - r.lo + 1;
+      r.w.assign(r.len, 0.0);
+      for (auto& e : cols[v]) r.w[e.first - r.lo] = e.second;
+    }
+  }
+  bf.finish();
+  ba.finish();
+}
+
 lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subsets, CameraPlan& cp,
                         std::string& err) {
   cp.cam = cam;
@@ -1193,72 +1269,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   }
   // ---- collapsed composite per slice: C_n = sum_k S_k B_{k,n} (plenoptic) or sum_k B_{k,n} (single)
   for (int ax = 0; ax < 2; ++ax) {
-    const BandFamily& f1 = cp.s1f[ax];
-    int nrow = ndet[ax];
-    int nv = nsrc[ax];
-    family_init(cp.cf[ax], nz, nrow, nv);
-    family_init(cp.ca[ax], nz, nv, nrow);
     // s-axis composites also serve as t families of the transposed two-pass path (MSEG segments)
     cp.cf[ax].want_mseg = cp.ca[ax].want_mseg = ax == 0;
-    FamilyBuilder bf(cp.cf[ax]), ba(cp.ca[ax]);
-    bf.tabs.resize(nz);
-    ba.tabs.resize(nz);
-    std::vector<double> accv(nv);
-    std::vector<char> touched(nv);
-    for (int n = 0; n < nz; ++n) {
-      auto& rows = bf.tabs[n];
-      rows.assign(nrow, Row());
-      std::vector<std::vector<std::pair<int, double>>> cols(nv);  // transpose
-      for (int i = 0; i < nrow; ++i) {
-        std::fill(accv.begin(), accv.end(), 0.0);
-        std::fill(touched.begin(), touched.end(), 0);
-        int vlo = 1 << 30, vhi = -1;
-        for (int k = 0; k < K[ax]; ++k) {
-          auto add_s1 = [&](int j, double w3) {
-            size_t idx = (size_t)(k * nz + n) * f1.n_rows + j;
-            for (int q = 0; q < f1.len[idx]; ++q) {
-              int v = f1.start[idx] + q;
-              accv[v] += w3 * f1.w64[idx * f1.taps + q];
-              touched[v] = 1;
-              vlo = std::min(vlo, v);
-              vhi = std::max(vhi, v);
-            }
-          };
-          if (plen) {
-            const BandFamily& f3 = cp.s3f[ax];
-            size_t i3 = (size_t)k * f3.n_rows + i;
-            for (int q = 0; q < f3.len[i3]; ++q) {
-              double w3 = f3.w64[i3 * f3.taps + q];
-              if (w3 == 0.0) continue;  // gap between two lenslets' cells (structural zero)
-              add_s1(f3.start[i3] + q, w3);
-            }
-          } else {
-            add_s1(i, 1.0);
-          }
-        }
-        if (vhi < 0) continue;
-        Row& r = rows[i];
-        r.lo = vlo;
-        r.len = vhi - vlo + 1;
-        r.w.assign(r.len, 0.0);
-        for (int v = vlo; v <= vhi; ++v) {
-          r.w[v - vlo] = accv[v];
-          if (touched[v]) cols[v].push_back({i, accv[v]});
-        }
-      }
-      auto& arows = ba.tabs[n];
-      arows.assign(nv, Row());
-      for (int v = 0; v < nv; ++v) {
-        if (cols[v].empty()) continue;
-        Row& r = arows[v];
-        r.lo = cols[v].front().first;
-        r.len = cols[v].back().first - r.lo + 1;
-        r.w.assign(r.len, 0.0);
-        for (auto& e : cols[v]) r.w[e.first - r.lo] = e.second;
-      }
-    }
-    bf.finish();
-    ba.finish();
+    build_composite(cp, ax, std::vector<char>(K[ax], 1), 1.0, nz, ndet[ax], nsrc[ax], plen, cp.cf[ax], cp.ca[ax]);
   }
   info.taps_s1 = std::max(cp.s1f[0].ell, cp.s1f[1].gmax);
   info.taps_s3 = plen ? std::max(cp.s3f[0].ell, cp.s3f[1].gmax) : 0;
@@ -1323,6 +1336,18 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
       for (int k = m; k < Kv; k += n_subsets) S.push_back(k);
       vo.n_views = (int)S.size();
       const double sc = (double)Kv / S.size();
+      // tensor-product subset with every k_t: the s composite over S_s, scaled by K/|S|, on the collapsed path
+      {
+        std::vector<char> in_s(K[0], 0), in_t(K[1], 0);
+        for (int k : S) { in_s[k % K[0]] = 1; in_t[k / K[0]] = 1; }
+        int ns = 0, nt_ = 0;
+        for (char v : in_s) ns += v;
+        for (char v : in_t) nt_ += v;
+        if (nt_ == K[1] && ns * nt_ == (int)S.size() && !std::getenv("LFM_SUBSET_PER_VIEW")) {
+          vo.collapsed = 1;
+          build_composite(cp, 0, in_s, sc, nz, ndet[0], nsrc[0], plen, vo.cfs, vo.cas);
+        }
+      }
       if (plen) {
         sep_init(vo.fwd_s1, &cp.s1f[0], &cp.s1f[1], nx, ny, vo.n_views, (float)c1);
         for (int k : S) {
@@ -1550,6 +1575,11 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     info.fma_stage[1] = nnz_a * ndet[0];
     info.mma_stage[0] = 3.0 * 128 * 16 * (double)cp.cf1n.u_k0.size() * ndet[0];
     info.mma_stage[1] = 3.0 * 128 * 16 * (double)cp.ca1n.u_k0.size() * ndet[0];
+    double nnz_sf = 0, nnz_sa = 0;
+    for (int v : cp.cf[0].cnt) nnz_sf += v;
+    for (int v : cp.ca[0].cnt) nnz_sa += v;
+    info.fma_spass[0] = nnz_sf * ny;
+    info.fma_spass[1] = nnz_sa * ny;
   }
   info.bytes_alg[0] = 4.0 * info.n_vox + rot_bytes + (plen ? 8.0 * Kv * nfield : 0.0) + 4.0 * npix;
   info.bytes_alg[1] = 4.0 * info.n_vox + rot_bytes + 4.0 * npix;

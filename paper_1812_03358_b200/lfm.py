@@ -61,7 +61,8 @@ class Info(ctypes.Structure):
                 ("taps_c", ctypes.c_int), ("ws_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
                 ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
                 ("fma_stage", ctypes.c_double * 2), ("mma_stage", ctypes.c_double * 2),
-                ("kind_stage", ctypes.c_int * 2)]
+                ("kind_stage", ctypes.c_int * 2), ("fma_spass", ctypes.c_double * 2),
+                ("subset_collapsed", ctypes.c_int)]
 
     def as_dict(self):
         out = {}
@@ -249,7 +250,7 @@ def A_adjoint_subset(plan, cam, subset, y, x, ws, accumulate=False, stream=None)
                                      _stream(stream)))
 
 
-STAGE_FWD_T, STAGE_ADJ_T = 0, 1
+STAGE_FWD_T, STAGE_ADJ_T, STAGE_FWD_S, STAGE_ADJ_S = 0, 1, 2, 3
 
 
 def A_stage(plan, cam, stage, inp, out, ws, stream=None):

@@ -55,7 +55,7 @@ def test_subset_gradient_matches_oracle():
         g = host(rec.gradient(dev(x), subset=m))
         ref = pwls.gradient_subset(x.astype(np.float64), ops, [y.astype(np.float64) for y in ys],
                                    [w.astype(np.float64) for w in wts], 0.02, 0.05, 2, m)
-        assert max_rel(g, ref) <= 1e-4
+        assert max_rel(g, ref) <= TOL
 
 
 def test_ordered_subsets_fista_trajectory():

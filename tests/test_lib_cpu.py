@@ -217,3 +217,65 @@ def test_host_only_plan_rejects_apply_calls():
     with pytest.raises(lfm.LfmError) as e:
         lfm.A_forward(plan, 0, x, y, ws, stream=0)
     assert e.value.status == 1 and "host-only" in str(e.value)
+
+
+def test_tables_bit_exact_at_128():
+    """The metric's config (128^3 two-camera, 2048^2 detectors, K = 8x8): every S1 band (both directions, both
+    axes, all 8 views x 128 slices), every S3 band, the rotation factors of the 30-degree camera bit-exact;
+    weights (fp64) on every 16th slice and the collapsed composite on 3 slices (bit-exact tables were
+    checked only on tiny/small configs)."""
+    from oracle.rotation import quarter_turn
+    cfg = make_config("128^3 two-camera")
+    plan = lfm.Plan(cfg, device=-1)
+    for c, op in enumerate(build_system(cfg)):
+        cam = op.camera
+        inf = plan.info(c)
+        P, T = quarter_turn(cfg["cameras"][c]["R"])
+        dec = decompose(T.ravel())
+        assert tuple(inf["rot_D"]) == dec["D"]
+        assert tuple(inf["shear"]) == (dec["a_zx"], dec["a_zy"], dec["a_xy"], dec["a_xz"], dec["a_yx"], dec["a_yz"])
+        dst = cam.array_planes
+        for ax in range(2):
+            for k in range(len(cam.sk[ax])):
+                for n in range(cam.nz):
+                    idx = k * cam.nz + n
+                    lo, hi = band(cam.slice_planes[ax][n], dst[ax], cam.sk[ax][k], cam.d0[ax], cam.basis)
+                    _bands_equal(plan, c, "S1F", ax, idx, lo, hi)
+                    lo, hi = band(dst[ax], cam.slice_planes[ax][n], cam.sk[ax][k], cam.d0[ax], cam.basis)
+                    _bands_equal(plan, c, "S1A", ax, idx, lo, hi)
+                    if n % 16 == 5:
+                        _weights_match(plan, c, "S1F", ax, idx, cam.S1[ax][k][n].toarray())
+                st_o, ln_o = _oracle_s3_band(cam, ax, k)
+                assert np.array_equal(plan.export_table(c, "S3F_START", ax, k), st_o)
+                assert np.array_equal(plan.export_table(c, "S3F_LEN", ax, k), ln_o)
+            _weights_match(plan, c, "S3F", ax, 3, cam.S3[ax][3].toarray())
+            for n in (0, 64, 127):
+                # composite band (reading Z21): the union of the S1 bands of every array cell that a non-zero S3
+                # entry of the row reaches, over all views.  Both sides decide "non-zero" on their own fp64 S3
+                # evaluation, and at a few trapezoid edges one side leaves rounding residue (1e-24..1e-30 of the
+                # row's entries) where the other gives exactly 0.  So: the plan's band equals the oracle's on
+                # every row where the residue does not matter, and elsewhere lies between the band of the
+                # oracle's significant entries (> 1e-20 of max) and that of all its non-zero entries.
+                Cn = 0
+                n_det = cam.S3[ax][0].shape[0]
+                lo = {m: np.full(n_det, 1 << 30) for m in ("sig", "any")}
+                hi = {m: np.full(n_det, -1) for m in ("sig", "any")}
+                for k in range(len(cam.sk[ax])):
+                    Cn = Cn + cam.S3[ax][k] @ cam.S1[ax][k][n]
+                    b_lo, b_hi = band(cam.slice_planes[ax][n], dst[ax], cam.sk[ax][k], cam.d0[ax], cam.basis)
+                    s3 = cam.S3[ax][k].tocoo()
+                    for m, keep in (("sig", np.abs(s3.data) > 1e-20 * np.abs(s3.data).max()), ("any", s3.data != 0.0)):
+                        keep = keep & (b_hi[s3.col] >= b_lo[s3.col])
+                        np.minimum.at(lo[m], s3.row[keep], b_lo[s3.col[keep]])
+                        np.maximum.at(hi[m], s3.row[keep], b_hi[s3.col[keep]])
+                Cn = Cn.toarray()
+                for m in ("sig", "any"):                      # an empty row exports start 0, length 0
+                    lo[m] = np.where(hi[m] < 0, 0, lo[m])
+                st = plan.export_table(c, "CF_START", ax, n)
+                end = st + plan.export_table(c, "CF_LEN", ax, n) - 1
+                same = (lo["sig"] == lo["any"]) & (hi["sig"] == hi["any"])
+                assert same.mean() > 0.99
+                assert np.array_equal(st[same], lo["sig"][same]) and np.array_equal(end[same], hi["sig"][same])
+                assert (lo["any"] <= st).all() and (st <= lo["sig"]).all()
+                assert (hi["sig"] <= end).all() and (end <= hi["any"]).all()
+                _weights_match(plan, c, "CF", ax, n, Cn, rel=1e-12)
