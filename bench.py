@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-recon", action="store_true", help="skip the 50-iteration reconstruction timing")
     ap.add_argument("--no-per-view", action="store_true", help="skip the per-view path reference timing")
     ap.add_argument("--one-stream", action="store_true", help="run the rank's cameras one after another on one stream")
+    ap.add_argument("--shard", default="cols", choices=["cols", "rows"],
+                    help="N > n_cam: split each camera's detector into column (default) or row tiles")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed pairs eagerly instead of as a CUDA graph")
     return ap.parse_args()
 
@@ -294,22 +296,22 @@ def run_ours(args, rank, world, local_rank):
     path = lfm.COLLAPSED if args.path == "collapsed" else lfm.PER_VIEW
     plan = lfm.Plan(cfg, device=local_rank)
     ws = plan.workspace()
-    items = shard([c["n_t"] for c in cfg["cameras"]], rank, world)
+    items = shard([(c["n_t"], c["n_s"]) for c in cfg["cameras"]], rank, world, axis=args.shard, align=256)
     n_vox = plan.infos[0]["n_vox"]
     x = torch.as_tensor(flame_volume(cfg["volume"]), device=dev).reshape(-1)
-    ys = {c: torch.empty(plan.infos[c]["n_pix"], device=dev) for c, _, _ in items}
-    rs = {c: torch.as_tensor(uniform_vector(plan.infos[c]["n_pix"], 1 + c), device=dev) for c, _, _ in items}
+    ys = {c: torch.empty(plan.infos[c]["n_pix"], device=dev) for c, *_ in items}
+    rs = {c: torch.as_tensor(uniform_vector(plan.infos[c]["n_pix"], 1 + c), device=dev) for c, *_ in items}
     g = torch.empty(n_vox, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     launches = [0]
 
-    def fwd_rows(c, r0, r1, xv, y):
-        lfm.A_forward_rows(plan, c, r0, r1, xv, y, ws, path=path)
+    def fwd_win(c, win, xv, y):
+        lfm.A_forward_window(plan, c, *win, xv, y, ws, path=path)
         launches[0] += lfm.last_launch_count()
 
-    def adj_rows(c, r0, r1, r, gv, acc):
-        lfm.A_adjoint_rows(plan, c, r0, r1, r, gv, ws, accumulate=acc, path=path)
+    def adj_win(c, win, r, gv, acc):
+        lfm.A_adjoint_window(plan, c, *win, r, gv, ws, accumulate=acc, path=path)
         launches[0] += lfm.last_launch_count()
 
     def allreduce(gv):
@@ -339,19 +341,19 @@ def run_ours(args, rank, world, local_rank):
             lfm.vol_accumulate(src, dst)
             launches[0] += lfm.last_launch_count()
 
-        def fwd_i(i, c, r0, r1, xv, y):
-            lfm.A_forward_rows(plan, c, r0, r1, xv, y, wss[i], path=path)
+        def fwd_i(i, c, win, xv, y):
+            lfm.A_forward_window(plan, c, *win, xv, y, wss[i], path=path)
             launches[0] += lfm.last_launch_count()
 
-        def adj_i(i, c, r0, r1, r, gv):
-            lfm.A_adjoint_rows(plan, c, r0, r1, r, gv, wss[i], accumulate=False, path=path)
+        def adj_i(i, c, win, r, gv):
+            lfm.A_adjoint_window(plan, c, *win, r, gv, wss[i], accumulate=False, path=path)
             launches[0] += lfm.last_launch_count()
 
         runner = ConcurrentPair(items, fwd_i, adj_i, accumulate, lambda gv: gv.zero_(), run, join, private,
                                 allreduce if world > 1 else None)
     else:
         start = None
-        runner = PairRunner(items, fwd_rows, adj_rows, lambda gv: gv.zero_(), allreduce if world > 1 else None)
+        runner = PairRunner(items, fwd_win, adj_win, lambda gv: gv.zero_(), allreduce if world > 1 else None)
 
     def step(x_in, g_out, ys_=None, rs_=None):
         launches[0] = 0
@@ -360,8 +362,8 @@ def run_ours(args, rank, world, local_rank):
         runner.pair(x_in, ys if ys_ is None else ys_, rs if rs_ is None else rs_, g_out)
 
     # dominant kernel: the separable transport of an unrotated camera (one sep_kernel launch per call)
-    dom_cam = next((c for c, r0, r1 in items if plan.infos[c]["rot_passes"] == 0 and r0 == 0
-                    and r1 == plan.infos[c]["n_t"]), None)
+    dom_cam = next((c for c, r0, r1, c0, c1 in items if plan.infos[c]["rot_passes"] == 0 and r0 == 0
+                    and r1 == plan.infos[c]["n_t"] and c0 == 0 and c1 == plan.infos[c]["n_s"]), None)
 
     for _ in range(args.warmup):
         step(x, g)
@@ -378,12 +380,17 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     # the timed pair as one CUDA graph (captured once after the warm-up: the same kernels, tensor maps and
     # stream fork/join, replayed without host launch overhead); --no-graph launches it eagerly every step
+    # with several ranks the graph holds the rank's compute (every item's forward and adjoint, the camera sum)
+    # and the gradient all-reduce runs after it, eagerly on the same stream
     graph = None
-    if not args.no_graph and world == 1:  # multi-rank pairs hold an NCCL all-reduce: launched eagerly
+    if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
+        if world > 1:
+            saved, runner.allreduce = runner.allreduce, None
         with torch.cuda.graph(graph):
             step(x, g)
-        n_graph_launches = launches[0]
+        if world > 1:
+            runner.allreduce = saved
         graph.replay()
         torch.cuda.synchronize()
     for i in range(args.steps):
@@ -391,6 +398,8 @@ def run_ours(args, rank, world, local_rank):
         ev[i][0].record(stream)
         if graph is not None:
             graph.replay()
+            if world > 1:
+                allreduce(g)
         else:
             step(x, g)
         ev[i][1].record(stream)
@@ -666,10 +675,12 @@ def run_ours(args, rank, world, local_rank):
                        "cameras": len(cfg["cameras"]), "detector": "%dx%d" % (cfg["cameras"][0]["n_s"],
                                                                                 cfg["cameras"][0]["n_t"]),
                        "views": "%dx%d pillbox" % (cfg["cameras"][0]["k_s"], cfg["cameras"][0]["k_t"]),
-                       "path": args.path, "parallelism": "cameras x detector-row tiles over %d rank(s)%s" % (
-                           world, ", concurrent per-camera streams" if len(items) > 1 and not args.one_stream else ""),
+                       "path": args.path, "parallelism": "cameras x detector-%s tiles over %d rank(s)%s" % (
+                           "column" if args.shard == "cols" else "row", world,
+                           ", concurrent per-camera streams" if len(items) > 1 and not args.one_stream else ""),
                        "l2": "256 MiB write between steps, outside the per-step CUDA events",
-                       "launch": "eager" if (args.no_graph or world > 1) else "one CUDA graph per pair (captured after warm-up)"},
+                       "launch": "eager" if args.no_graph else ("one CUDA graph per pair (captured after warm-up)" if world == 1
+                                                                 else "per-rank CUDA graph + NCCL all-reduce")},
             "hbm_gbs_alg": pair_bytes / (ms_med * 1e-3) / 1e9,
             "hbm_frac_of_measured": pair_bytes / (ms_med * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6551.4),
             "pair_roofline": pair_roof,

@@ -187,6 +187,18 @@ lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1,
                               void* ws, size_t ws_bytes, void* stream);
 lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
                               int accumulate, void* ws, size_t ws_bytes, void* stream);
+/* Detector windows (rows [row0, row1) x columns [col0, col1)), the shards of the multi-GPU partition:
+ * lfm_A_forward_window writes y on the window (other entries of partially covered tiles may also be written, with
+ * their correct values); lfm_A_adjoint_window gives x (+)= A_c^T P y with P keeping only the window of y.  Summing
+ * the adjoint over a partition of the detector into windows gives lfm_A_adjoint.  On the collapsed tcgen05 path a
+ * column window restricts every kernel to the window's 256-column tiles (the s passes act column by column, the t
+ * passes tile by tile; the forward t pass splits K when the window leaves most SMs idle, with partial sums in the
+ * workspace added in a fixed order); elsewhere the column window is applied by masking y.
+ * 0 <= row0 < row1 <= n_t, 0 <= col0 < col1 <= n_s, else LFM_E_INVALID. */
+lfm_status lfm_A_forward_window(lfm_plan p, int cam, int path, int row0, int row1, int col0, int col1, const float* x,
+                                float* y, void* ws, size_t ws_bytes, void* stream);
+lfm_status lfm_A_adjoint_window(lfm_plan p, int cam, int path, int row0, int row1, int col0, int col1, const float* y,
+                                float* x, int accumulate, void* ws, size_t ws_bytes, void* stream);
 
 /* View-subset operators (sec,subset, eqn,subset P:366-379, reading Z19): with S_m the plan's subset m,
  *   y = (K/|S_m|) sum_{k in S_m} A_ck x           (lfm_A_forward_subset)

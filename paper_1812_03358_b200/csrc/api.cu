@@ -186,15 +186,32 @@ lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int acc
 }
 
 lfm_status sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int acc, void* stream,
-               int out_r0 = 0, int out_r1 = -1, int win_r0 = 0, int win_r1 = -1) {
+               int out_r0 = 0, int out_r1 = -1, int win_r0 = 0, int win_r1 = -1, int out_c0 = 0, int out_c1 = -1,
+               float* part = nullptr, size_t part_bytes = 0) {
   std::string err;
-  lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err, out_r0, out_r1, win_r0, win_r1);
+  lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err, out_r0, out_r1, win_r0, win_r1, out_c0, out_c1,
+                             part, part_bytes);
   return st == LFM_OK ? st : fail(st, err);
 }
 
-// y rows [r0, r1) of A_c x (r1 < 0: all rows).  Rows of partially covered tiles are computed as well.
+// A detector window [r0, r1) x [c0, c1) (multi-GPU shards; r1 / c1 < 0 = to the end).
+struct Win {
+  int r0 = 0, r1 = -1, c0 = 0, c1 = -1;
+  bool cols(int n_s) const { return c0 > 0 || (c1 >= 0 && c1 < n_s); }
+};
+
+// the collapsed path runs on the tcgen05 kernels end to end (band_v s passes, band_u t passes), the form whose
+// kernels restrict themselves to a column window
+static bool tc_two_pass(const CameraPlan& cp) {
+  return cp.fwd_split && cp.fwd_t == 3 && cp.adj_t == 3 && cp.fwd_c2.kind == 8 && cp.adj_c1.kind == 8;
+}
+
+// y on the window rows [r0, r1) x columns [c0, c1) of A_c x.  Other entries of partially covered tiles may be
+// written (with their correct values); the column window only saves work on the tcgen05 path (band_v items of
+// the window's 256-column tiles; band_u items of those tiles, split-K when few).
 lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y, const Ws& w, void* stream,
-                        int r0 = 0, int r1 = -1) {
+                        Win win = Win()) {
+  const int r0 = win.r0, r1 = win.r1;
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
   const bool plen = cp.info.type == LFM_PLENOPTIC;
@@ -203,7 +220,8 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
       if (cp.fwd_t == 2 || cp.fwd_t == 3) {
         // direct s pass (spass_fwd_kernel, or band_v on the tensor cores): slices -> interleaved U
         std::string err;
-        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err) : k_spass_fwd(cp, xr, w.z, stream, err);
+        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err, win.c0, win.c1)
+                                      : k_spass_fwd(cp, xr, w.z, stream, err);
         if (st != LFM_OK) return fail(st, err);
       } else if (cp.fwd_t) {
         // s pass as a t pass over the transposed slices, written back in the interleaved U layout
@@ -216,7 +234,7 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
       } else {
         TRY(sep(cp.fwd_c1, xr, w.z, 0, cp.info.nz, 0, stream));
       }
-      return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1);
+      return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z);
     }
     return sep(cp.fwd_c, xr, y, 0, 1, 0, stream, r0, r1);
   }
@@ -227,19 +245,41 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
   return sep(cp.fwd_s1, xr, y, 0, 1, 0, stream, r0, r1);
 }
 
-// x (+)= A_c^T y restricted to the detector rows [r0, r1) of y (others treated as zero).
+// y (n_t x n_s) with zeros outside the window (the generic form of a column window)
+__global__ void mask_window_kernel(const float* __restrict__ y, float* __restrict__ out, int n_t, int n_s, int r0, int r1,
+                                   int c0, int c1) {
+  const long long n = (long long)n_t * n_s;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / n_s), c = (int)(i % n_s);
+    out[i] = (r >= r0 && r < r1 && c >= c0 && c < c1) ? y[i] : 0.f;
+  }
+}
+
+// x (+)= A_c^T P y, P keeping the window rows [r0, r1) x columns [c0, c1) of y (others treated as zero).
 lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x, int accumulate, const Ws& w,
-                        void* stream, int r0 = 0, int r1 = -1) {
+                        void* stream, Win win = Win()) {
+  int r0 = win.r0, r1 = win.r1;
   const bool rot = cp.info.rot_passes != 0;
   float* target = rot ? w.r0 : x;
   int acc = rot ? 0 : accumulate;
   const bool plen = cp.info.type == LFM_PLENOPTIC;
+  const bool tc_cols = path == LFM_PATH_COLLAPSED && tc_two_pass(cp) && win.c0 % 4 == 0;
+  if (win.cols(cp.info.n_s) && !tc_cols) {
+    // kernels without column windows: mask y into scratch, then the row-windowed adjoint of the masked copy
+    const int rr1 = r1 < 0 ? cp.info.n_t : r1, cc1 = win.c1 < 0 ? cp.info.n_s : win.c1;
+    mask_window_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(y, w.s2, cp.info.n_t, cp.info.n_s, r0, rr1, win.c0, cc1);
+    ++g_launches;
+    y = w.s2;
+    win.c0 = 0;
+    win.c1 = -1;
+  }
   if (path == LFM_PATH_COLLAPSED) {
-    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1));  // one output: all (vt, n) rows
+    // one output: all (vt, n) rows; the column window selects the 256-column tiles of Z
+    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1, win.c0, win.c1));
     if (cp.adj_t == 2 || cp.adj_t == 3) {
       // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
-      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err)
+      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err, win.c0, win.c1)
                                     : k_spass_adj(cp, w.z, target, acc, stream, err);
       if (st != LFM_OK) return fail(st, err);
     } else if (cp.adj_t) {
@@ -497,20 +537,36 @@ lfm_status lfm_vol_rotate(lfm_plan p, int cam, int dir, const float* in, float* 
   return st;
 }
 
-lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* x, float* y,
-                              void* ws, size_t ws_bytes, void* stream) {
+static lfm_status check_window(const lfm_plan_s* p, int cam, int row0, int row1, int col0, int col1) {
+  const lfm_info& inf = p->cams[cam].info;
+  if (row0 < 0 || row1 > inf.n_t || row0 >= row1) return fail(LFM_E_INVALID, "bad detector row range");
+  if (col0 < 0 || col1 > inf.n_s || col0 >= col1) return fail(LFM_E_INVALID, "bad detector column range");
+  return LFM_OK;
+}
+
+lfm_status lfm_A_forward_window(lfm_plan p, int cam, int path, int row0, int row1, int col0, int col1, const float* x,
+                                float* y, void* ws, size_t ws_bytes, void* stream) {
   DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
   if ((st = check_path(path)) != LFM_OK) return st;
   if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
-  if (row0 < 0 || row1 > p->cams[cam].info.n_t || row0 >= row1) return fail(LFM_E_INVALID, "bad detector row range");
+  if ((st = check_window(p, cam, row0, row1, col0, col1)) != LFM_OK) return st;
   Ws w;
   if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
-  st = forward_impl(p->cams[cam], path, x, y, w, stream, row0, row1);
+  Win win;
+  win.r0 = row0; win.r1 = row1; win.c0 = col0; win.c1 = col1;
+  st = forward_impl(p->cams[cam], path, x, y, w, stream, win);
   g_last_launches = g_launches;
   return st;
+}
+
+lfm_status lfm_A_forward_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* x, float* y,
+                              void* ws, size_t ws_bytes, void* stream) {
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  return lfm_A_forward_window(p, cam, path, row0, row1, 0, p->cams[cam].info.n_s, x, y, ws, ws_bytes, stream);
 }
 
 lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* out, void* ws, size_t ws_bytes,
@@ -588,20 +644,30 @@ lfm_status lfm_A_forward(lfm_plan p, int cam, int path, const float* x, float* y
   return lfm_A_forward_rows(p, cam, path, 0, p->cams[cam].info.n_t, x, y, ws, ws_bytes, stream);
 }
 
-lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
-                              int accumulate, void* ws, size_t ws_bytes, void* stream) {
+lfm_status lfm_A_adjoint_window(lfm_plan p, int cam, int path, int row0, int row1, int col0, int col1, const float* y,
+                                float* x, int accumulate, void* ws, size_t ws_bytes, void* stream) {
   DevGuard dev_guard(p);
   g_launches = 0;
   lfm_status st = check_cam(p, cam);
   if (st != LFM_OK) return st;
   if ((st = check_path(path)) != LFM_OK) return st;
   if (!x || !y) return fail(LFM_E_INVALID, "x/y is NULL");
-  if (row0 < 0 || row1 > p->cams[cam].info.n_t || row0 >= row1) return fail(LFM_E_INVALID, "bad detector row range");
+  if ((st = check_window(p, cam, row0, row1, col0, col1)) != LFM_OK) return st;
   Ws w;
   if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
-  st = adjoint_impl(p->cams[cam], path, y, x, accumulate, w, stream, row0, row1);
+  Win win;
+  win.r0 = row0; win.r1 = row1; win.c0 = col0; win.c1 = col1;
+  st = adjoint_impl(p->cams[cam], path, y, x, accumulate, w, stream, win);
   g_last_launches = g_launches;
   return st;
+}
+
+lfm_status lfm_A_adjoint_rows(lfm_plan p, int cam, int path, int row0, int row1, const float* y, float* x,
+                              int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  lfm_status st = check_cam(p, cam);
+  if (st != LFM_OK) return st;
+  return lfm_A_adjoint_window(p, cam, path, row0, row1, 0, p->cams[cam].info.n_s, y, x, accumulate, ws, ws_bytes,
+                              stream);
 }
 
 lfm_status lfm_A_adjoint(lfm_plan p, int cam, int path, const float* y, float* x, int accumulate, void* ws,

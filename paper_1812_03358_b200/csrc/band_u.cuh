@@ -38,7 +38,14 @@ struct UArgs {
   int accumulate;
   int tile_mode;          // 0: tile = 128 consecutive rows; 1: 2 rows-of-slices (vt) x 64 slices, rows vt*nz + n
   int tm_nz;              // nz for tile_mode 1
+  int nt0;                // first column tile (column windows: tiles [nt0, nt0 + n_nt))
+  int ksplit;             // split-K: each (row tile, column tile) is ksplit items over consecutive thirds.. of its
+                          // live blocks; chunk kc writes its partial at output row kc * kc_rows + r (kc_rows =
+                          // row tiles x 128), summed in a fixed order by sum_chunks_kernel (deterministic)
+  int kc_rows;
 };
+
+
 
 // blocks of row tile mt whose 16 source rows intersect the row window (all of them when not windowed)
 __device__ __forceinline__ bool u_live(const UArgs& a, int b) {
@@ -52,6 +59,36 @@ __device__ __forceinline__ int u_nlive(const UArgs& a, int b0, int b1) {
   return n;
 }
 
+// item it -> (row tile, column tile, K chunk) and the chunk's live-block range [lo, hi) in producer order
+struct UItem {
+  int mt, nt, kc, b0, b1, lo, hi;
+};
+template <bool SPLIT>
+__device__ __forceinline__ UItem u_item(const UArgs& a, int it) {
+  UItem u;
+  if constexpr (!SPLIT) {  // one item per (row tile, column tile): the whole live range
+    u.mt = a.mt0 + it / a.n_nt;
+    u.nt = a.nt0 + it % a.n_nt;
+    u.kc = 0;
+    u.b0 = __ldg(a.blk_off + u.mt);
+    u.b1 = __ldg(a.blk_off + u.mt + 1);
+    u.lo = 0;
+    u.hi = u_nlive(a, u.b0, u.b1);
+    return u;
+  }
+  const int per_mt = a.n_nt * a.ksplit;
+  u.mt = a.mt0 + it / per_mt;
+  const int rem = it % per_mt;
+  u.nt = a.nt0 + rem / a.ksplit;
+  u.kc = rem % a.ksplit;
+  u.b0 = __ldg(a.blk_off + u.mt);
+  u.b1 = __ldg(a.blk_off + u.mt + 1);
+  const int nl = u_nlive(a, u.b0, u.b1);
+  u.lo = (int)((long long)nl * u.kc / a.ksplit);
+  u.hi = (int)((long long)nl * (u.kc + 1) / a.ksplit);
+  return u;
+}
+
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
 constexpr int U_THREADS = 384;
@@ -61,6 +98,7 @@ constexpr int U_THREADS = 384;
 constexpr int U_STAGE_OUT = 4096;  // per epilogue warp: 32 rows x 32 columns fp32, 128-byte swizzle (TMA store)
 constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 8 * U_STAGE_OUT + 1024 + 256;
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
                                                               const __grid_constant__ CUtensorMap out_map, UArgs a) {
   using namespace tc;
@@ -94,19 +132,25 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_items = a.n_mt * a.n_nt;
+  const int n_items = a.n_mt * a.n_nt * (SPLIT ? a.ksplit : 1);
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int mt = a.mt0 + it / a.n_nt, nt = it % a.n_nt;
-        const int b0 = __ldg(a.blk_off + mt), b1 = __ldg(a.blk_off + mt + 1);
+        const UItem ui = u_item<SPLIT>(a, it);
+        const int mt = ui.mt, nt = ui.nt, b0 = ui.b0, b1 = ui.b1;
         const bool rev = (mt & 1) != 0;
+        int li = 0;  // live-block index in producer order (split-K chunks)
         for (int j = b0; j < b1; ++j) {
           const int b = rev ? b0 + b1 - 1 - j : j;
           if (a.windowed && !u_live(a, b)) continue;
+          if constexpr (SPLIT) {
+            const int my = li++;
+            if (my < ui.lo) continue;
+            if (my >= ui.hi) break;
+          }
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * U_STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], 32768);
@@ -126,14 +170,13 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
-      uint32_t tph[2] = {0, 0};
+      uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int mt = a.mt0 + it / a.n_nt;
-        const int nl = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
-        const int b0 = 0, b1 = nl;  // live blocks in producer order
+        const UItem ui = u_item<SPLIT>(a, it);
+        const int b0 = 0, b1 = ui.hi - ui.lo;  // the chunk's live blocks in producer order
         for (int g0 = b0; g0 < b1; g0 += a.group) {
-          mbar_wait(&tempty[buf], tph[buf] ^ 1);
-          tph[buf] ^= 1;
+          mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+          tph ^= 1u << buf;
           tc_fence_after();
           const uint32_t d = tmem + buf * 256;
           const int g1 = min(b1, g0 + a.group);
@@ -168,8 +211,8 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     int s = 0;
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int mt = a.mt0 + it / a.n_nt;
-      const int nb = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
+      const UItem ui = u_item<SPLIT>(a, it);
+      const int nb = ui.hi - ui.lo;
       for (int b = 0; b < nb; ++b) {
         mbar_wait(&full[s], ph);
         const float4* src = reinterpret_cast<const float4*>(sm + s * U_STAGE_BYTES + 16384);
@@ -201,16 +244,17 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (its row quarter), columns half h
     const int q = warp & 3, h = (warp - 4) >> 2;
     int buf = 0;
-    uint32_t tph[2] = {0, 0};
+    uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int mt = a.mt0 + it / a.n_nt, nt = it % a.n_nt;
-      const int b0 = 0, b1 = u_nlive(a, __ldg(a.blk_off + mt), __ldg(a.blk_off + mt + 1));
+      const UItem ui = u_item<SPLIT>(a, it);
+      const int mt = ui.mt, nt = ui.nt;
+      const int b0 = 0, b1 = ui.hi - ui.lo;
       float acc[128];
 #pragma unroll
       for (int c = 0; c < 128; ++c) acc[c] = 0.f;
       for (int g0 = b0; g0 < b1; g0 += a.group) {
-        mbar_wait(&tfull[buf], tph[buf]);
-        tph[buf] ^= 1;
+        mbar_wait(&tfull[buf], (tph >> buf) & 1u);
+        tph ^= 1u << buf;
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + h * 128;
 #pragma unroll
@@ -228,8 +272,9 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       // output: per 32-column chunk the warp's 32 x 32 block goes through its swizzled staging buffer and one
       // TMA store (or TMA add when accumulating); rows / columns outside the output are clipped by the TMA unit
       uint8_t* stg = sout + (warp - 4) * U_STAGE_OUT;
-      const int r0 = a.tile_mode == 0 ? mt * 128 + 32 * q
-                                       : (2 * (mt / (a.tm_nz >> 6)) + (q >> 1)) * a.tm_nz + 64 * (mt % (a.tm_nz >> 6)) + 32 * (q & 1);
+      const int r0 = (a.tile_mode == 0 ? mt * 128 + 32 * q
+                                        : (2 * (mt / (a.tm_nz >> 6)) + (q >> 1)) * a.tm_nz + 64 * (mt % (a.tm_nz >> 6)) + 32 * (q & 1)) +
+                     ui.kc * a.kc_rows;
       const int c0 = nt * 256 + h * 128;
 #pragma unroll
       for (int c = 0; c < 128; c += 32) {

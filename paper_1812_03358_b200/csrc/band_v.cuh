@@ -25,11 +25,30 @@ struct VArgs {
   const float* B;          // weight images: block b at B + b * 32 * N floats (hi N x 16, then lo N x 16)
   const int32_t* blk_off;  // per item key (n * n_nt + nt): blocks [off, off+1)
   const int32_t* blk_k0;   // per block: first k (vx forward, s adjoint)
-  int nz, n_mt, n_nt;      // items = nz * n_mt * n_nt (item = (n * n_mt + mt) * n_nt + nt)
+  int nz, n_mt, n_nt;      // table N-tiles per slice; items = nz * n_mt * nt_cnt, (n, mt, nt0 + j)
+  int nt0, nt_cnt;         // the N-tiles this launch covers (column windows of the forward)
+  int k_lo, k_hi;          // K window (adjoint column windows): blocks outside [k_lo, k_hi) are skipped and the data
+                           // map starts at k_lo (TMA coordinate k - k_lo; columns outside read as zeros)
   int group;               // blocks per TMEM accumulator before it is drained
   float scale;
   int accumulate;
 };
+
+// live blocks [lb0, lb1) of item key: blocks are stored with ascending k0, so the ones meeting the K window are
+// one contiguous run
+template <bool KWIN>
+__device__ __forceinline__ void v_live(const VArgs& a, int key, int BK, int& lb0, int& lb1) {
+  const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+  if (!KWIN) {  // no K window: every block
+    lb0 = b0;
+    lb1 = b1;
+    return;
+  }
+  lb0 = b0;
+  while (lb0 < b1 && __ldg(a.blk_k0 + lb0) + BK <= a.k_lo) ++lb0;
+  lb1 = lb0;
+  while (lb1 < b1 && __ldg(a.blk_k0 + lb1) < a.k_hi) ++lb1;
+}
 
 constexpr int V_THREADS = 384;
 
@@ -66,7 +85,7 @@ struct VCfg {
   static constexpr int TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
 };
 
-template <int N, int DIR, int BK>
+template <int N, int DIR, int BK, bool KWIN = false>
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
                                                               const __grid_constant__ CUtensorMap out_map, VArgs a) {
   using namespace tc;
@@ -101,22 +120,23 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_items = a.nz * a.n_mt * a.n_nt;
+  const int n_items = a.nz * a.n_mt * a.nt_cnt;
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int nt = it % a.n_nt, mt = (it / a.n_nt) % a.n_mt, n = it / (a.n_nt * a.n_mt);
+        const int nt = a.nt0 + it % a.nt_cnt, mt = (it / a.nt_cnt) % a.n_mt, n = it / (a.nt_cnt * a.n_mt);
         const int key = n * a.n_nt + nt;
-        const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+        int b0, b1;
+        v_live<KWIN>(a, key, BK, b0, b1);
         for (int b = b0; b < b1; ++b) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
           bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
-          const int k = __ldg(a.blk_k0 + b);
+          const int k = __ldg(a.blk_k0 + b) - (KWIN ? a.k_lo : 0);
 #pragma unroll
           for (int j = 0; j < C::KS; ++j) {
             if (DIR == 0) tma_load_3d(st + j * C::SUBA, &a_map, k + j * C::SUB, mt * 128, n, &full[s]);   // (vx, vt, n)
@@ -134,14 +154,15 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
-      uint32_t tph[2] = {0, 0};
+      uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int nt = it % a.n_nt, n = it / (a.n_nt * a.n_mt);
+        const int nt = a.nt0 + it % a.nt_cnt, n = it / (a.nt_cnt * a.n_mt);
         const int key = n * a.n_nt + nt;
-        const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+        int b0, b1;
+        v_live<KWIN>(a, key, BK, b0, b1);
         for (int g0 = b0; g0 < b1; g0 += a.group) {
-          mbar_wait(&tempty[buf], tph[buf] ^ 1);
-          tph[buf] ^= 1;
+          mbar_wait(&tempty[buf], ((tph >> buf) & 1u) ^ 1u);
+          tph ^= 1u << buf;
           tc_fence_after();
           const uint32_t d = tmem + buf * C::ACC;
           const int g1 = min(b1, g0 + a.group);
@@ -181,9 +202,11 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     int s = 0;
     uint32_t ph = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int nt = it % a.n_nt, n = it / (a.n_nt * a.n_mt);
+      const int nt = a.nt0 + it % a.nt_cnt, n = it / (a.nt_cnt * a.n_mt);
       const int key = n * a.n_nt + nt;
-      const int nb = __ldg(a.blk_off + key + 1) - __ldg(a.blk_off + key);
+      int lb0, lb1;
+      v_live<KWIN>(a, key, BK, lb0, lb1);
+      const int nb = lb1 - lb0;
       for (int b = 0; b < nb; ++b) {
         mbar_wait(&full[s], ph);
         const float4* src = reinterpret_cast<const float4*>(sm + s * C::STAGE);
@@ -216,17 +239,18 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     uint8_t* stg0 = sout + (warp - 4) * C::NOB * C::OUT;
     int ob = 0;  // staging buffer of the next store
     int buf = 0;
-    uint32_t tph[2] = {0, 0};
+    uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const int nt = it % a.n_nt, mt = (it / a.n_nt) % a.n_mt, n = it / (a.n_nt * a.n_mt);
+      const int nt = a.nt0 + it % a.nt_cnt, mt = (it / a.nt_cnt) % a.n_mt, n = it / (a.nt_cnt * a.n_mt);
       const int key = n * a.n_nt + nt;
-      const int b0 = __ldg(a.blk_off + key), b1 = __ldg(a.blk_off + key + 1);
+      int b0, b1;
+      v_live<KWIN>(a, key, BK, b0, b1);
       float acc[EC];
 #pragma unroll
       for (int c = 0; c < EC; ++c) acc[c] = 0.f;
       for (int g0 = b0; g0 < b1; g0 += a.group) {
-        mbar_wait(&tfull[buf], tph[buf]);
-        tph[buf] ^= 1;
+        mbar_wait(&tfull[buf], (tph >> buf) & 1u);
+        tph ^= 1u << buf;
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * C::ACC + h * EC;
 #pragma unroll

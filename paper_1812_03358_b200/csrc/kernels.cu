@@ -469,13 +469,19 @@ static lfm_status encode3(CUtensorMap* map, const float* base, const long long d
 
 template <int N, int DIR, int BK>
 static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
-                                float scale, int accumulate, void* stream, std::string& err) {
-  static bool attr[LFM_MAX_DEV];
+                                float scale, int accumulate, void* stream, std::string& err, int nt0 = 0, int nt_cnt = -1,
+                                int k_lo = 0, int k_hi = 1 << 30) {
+  // the K-window instantiation only when a window cuts the K range (adjoint column shards)
+  const bool kwin = k_lo > 0 || k_hi < (1 << 30);
+  static bool attr[LFM_MAX_DEV][2];
   const int dv = cur_dev();
-  if (!attr[dv]) {
-    if (cudaFuncSetAttribute(band_v_kernel<N, DIR, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VCfg<N, BK>::SMEM) != cudaSuccess)
-      return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
-    attr[dv] = true;
+  if (!attr[dv][kwin]) {
+    cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)VCfg<N, BK>::SMEM)
+                         : cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)VCfg<N, BK>::SMEM);
+    if (e != cudaSuccess) return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
+    attr[dv][kwin] = true;
   }
   VArgs v;
   v.B = T.d_img;
@@ -484,16 +490,24 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   v.nz = nz;
   v.n_mt = (ny + 127) / 128;
   v.n_nt = T.n_nt;
+  v.nt0 = std::max(0, nt0);
+  v.nt_cnt = nt_cnt < 0 ? T.n_nt - v.nt0 : std::min(nt_cnt, T.n_nt - v.nt0);
+  v.k_lo = kwin ? k_lo : 0;
+  v.k_hi = k_hi;
   v.group = 4;
   v.scale = scale;
   v.accumulate = accumulate;
-  const int items = v.nz * v.n_mt * v.n_nt;
-  band_v_kernel<N, DIR, BK><<<std::min(items, g_num_sms()), V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
+  const int items = v.nz * v.n_mt * v.nt_cnt;
+  if (items <= 0) return LFM_OK;
+  const int grid = std::min(items, g_num_sms());
+  if (kwin) band_v_kernel<N, DIR, BK, true><<<grid, V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
+  else band_v_kernel<N, DIR, BK, false><<<grid, V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
 
-lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err) {
+lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
+                       int c0, int c1) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
   if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
@@ -504,16 +518,23 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
   const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
   const int ob[3] = {32, 1, 32};
   if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
-  return T.BK == 32 ? launch_band_v<256, 0, 32>(T, am, om, nz, ny, 1.f, 0, stream, err)
-                    : launch_band_v<256, 0, 16>(T, am, om, nz, ny, 1.f, 0, stream, err);
+  // column window [c0, c1): only the N-tiles (256 detector columns) that meet it
+  const int nt0 = std::max(0, c0) / T.N, nt1 = c1 < 0 ? T.n_nt : (c1 + T.N - 1) / T.N;
+  return T.BK == 32 ? launch_band_v<256, 0, 32>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0)
+                    : launch_band_v<256, 0, 16>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0);
 }
 
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
-                       std::string& err) {
+                       std::string& err, int c0, int c1) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
   if (!T.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
+  // column window [c0, c1) of Z (= of y): the data map starts at c0 and is c1 - c0 wide, so columns outside read
+  // as zeros; K blocks outside the window are skipped (items without live blocks write zeros)
+  const int k_lo = std::max(0, c0), k_hi = (c1 < 0 || c1 >= nd) ? (1 << 30) : c1;
+  if (k_lo % 4) { err = "band_v: a column window must start on a multiple of 4"; return LFM_E_INVALID; }
   CUtensorMap am, om;
-  const long long ad[3] = {nd, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+  const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+  Z += k_lo;
   const int ab[3] = {T.BK < 32 ? T.BK : 32, 1, 128};
   lfm_status st = encode3(&am, Z, ad, as, ab, T.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
@@ -522,11 +543,11 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, floa
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
   const float sc = cp.adj_c2.out_scale;
   if (T.N == 32)
-    return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err)
-                      : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err);
-  if (T.BK == 64) return launch_band_v<16, 1, 64>(T, am, om, nz, ny, sc, accumulate, stream, err);
-  return T.BK == 32 ? launch_band_v<16, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err)
-                    : launch_band_v<16, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err);
+    return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi)
+                      : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
+  if (T.BK == 64) return launch_band_v<16, 1, 64>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
+  return T.BK == 32 ? launch_band_v<16, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi)
+                    : launch_band_v<16, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
 }
 
 // Subset ops reuse the tile configuration the autotuner chose for the full per-view op (same tables,
@@ -2020,8 +2041,23 @@ static int g_num_sms() {
   return n;
 }
 
+// split-K partial sums of band_u: y[r][c] (+)= sum_kc part[kc * kc_rows + r][c] over the window, kc ascending
+__global__ void sum_chunks_kernel(const float* __restrict__ part, float* __restrict__ y, long long pitch, int r0, int r1,
+                                  int c0, int c1, int ksplit, int kc_rows, int accumulate) {
+  const int w = c1 - c0;
+  const long long n = (long long)(r1 - r0) * w;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = r0 + (int)(i / w), c = c0 + (int)(i % w);
+    float v = part[(long long)r * pitch + c];
+    for (int kc = 1; kc < ksplit; ++kc) v += part[((long long)kc * kc_rows + r) * pitch + c];
+    float* o = y + (long long)r * pitch + c;
+    *o = accumulate ? *o + v : v;
+  }
+}
+
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
-                      void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1) {
+                      void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1, int out_c0,
+                      int out_c1, float* part, size_t part_bytes) {
   if (n_out <= 0) return LFM_OK;
   SepArgs a;
   a.src = src;
@@ -2132,16 +2168,36 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
             return cuda_check(cudaGetLastError(), "band_u memset", err);
       return LFM_OK;
     }
+    // column window [c0, c1): the 256-column tiles that meet it (columns of edge tiles outside it are computed too)
+    const int cw0 = std::max(0, out_c0), cw1 = out_c1 < 0 ? op.n_os : std::min(out_c1, op.n_os);
+    if (cw1 <= cw0) return LFM_OK;
+    const int nt0 = cw0 / 256, nt1 = (cw1 + 255) / 256;
+    const int n_mt_all = op.ft->u_ntiles;
+    const int mt0 = op.ft->u_mode ? 0 : r0 / 128;
+    const int n_mt_l = op.ft->u_mode ? n_mt_all : (r1 + 127) / 128 - mt0;
+    // split-K when the window leaves most SMs idle (row / column shards of the multi-GPU partition): each item's
+    // live blocks in ksplit chunks, partial outputs in `part`, summed in a fixed order (deterministic)
+    int ksplit = 1;
+    const int items0 = n_mt_l * (nt1 - nt0);
+    const long long kc_rows = (long long)n_mt_all * 128;
+    if (part && !op.ft->u_mode && 2 * items0 <= g_num_sms() && !std::getenv("LFM_NO_SPLITK")) {
+      ksplit = std::min(4, g_num_sms() / std::max(1, items0));
+      while (ksplit > 1 && (size_t)ksplit * kc_rows * a.out_pitch * 4 > part_bytes) --ksplit;
+    }
     CUtensorMap map, omap;
     lfm_status st = encode_map(&map, base, op.n_is, win_rows, a.src_pitch, 32, 16, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, err);
     if (st != LFM_OK) return st;
-    st = encode_map(&omap, out + (long long)b0 * a.out_stride, op.n_os, op.n_ot, a.out_pitch, 32, 32,
-                    CU_TENSOR_MAP_SWIZZLE_128B, err);
+    if (ksplit > 1)
+      st = encode_map(&omap, part, op.n_os, (int)(ksplit * kc_rows), a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, err);
+    else
+      st = encode_map(&omap, out + (long long)b0 * a.out_stride, op.n_os, op.n_ot, a.out_pitch, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B, err);
     if (st != LFM_OK) return st;
     static bool smem_set[LFM_MAX_DEV];
     const int dv = cur_dev();
     if (!smem_set[dv]) {
-      if (cudaFuncSetAttribute(band_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
+      if (cudaFuncSetAttribute(band_u_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(band_u_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
         return cuda_check(cudaGetLastError(), "band_u smem attribute", err);
       smem_set[dv] = true;
     }
@@ -2154,21 +2210,33 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.out_pitch = a.out_pitch;
     u.n_rows = op.n_ot;
     u.n_cols = op.n_os;
-    u.mt0 = op.ft->u_mode ? 0 : r0 / 128;
-    u.n_mt = op.ft->u_mode ? n_mt : (r1 + 127) / 128 - u.mt0;
-    u.n_nt = (op.n_os + 255) / 256;
+    u.mt0 = mt0;
+    u.n_mt = n_mt_l;
+    u.nt0 = nt0;
+    u.n_nt = nt1 - nt0;
+    u.ksplit = ksplit;
+    u.kc_rows = (int)kc_rows;
     u.k_shift = a.win_r0;
     u.k_end = a.win_r1;
     u.windowed = a.win_r0 > 0 || a.win_r1 < op.n_it;
     u.group = op.stages > 0 ? op.stages : 4;
     u.scale = op.out_scale * term.scale;
-    u.accumulate = accumulate;
+    u.accumulate = ksplit > 1 ? 0 : accumulate;
     u.tile_mode = op.ft->u_mode;
     u.tm_nz = op.ft->u_nz;
     if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
-    const int grid_u = std::min(u.n_mt * u.n_nt, g_num_sms());
-    band_u_kernel<<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
+    const int grid_u = std::min(u.n_mt * u.n_nt * u.ksplit, g_num_sms());
+    if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
+    else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
     ++g_launches;
+    if (ksplit > 1) {
+      const int sr0 = mt0 * 128, sr1 = std::min(op.n_ot, (mt0 + n_mt_l) * 128);
+      const int sc0 = nt0 * 256, sc1 = std::min(op.n_os, nt1 * 256);
+      const long long n = (long long)(sr1 - sr0) * (sc1 - sc0);
+      sum_chunks_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, s>>>(
+          part, out + (long long)b0 * a.out_stride, a.out_pitch, sr0, sr1, sc0, sc1, ksplit, (int)kc_rows, accumulate);
+      ++g_launches;
+    }
     return cuda_check(cudaGetLastError(), "band_u_kernel launch", err);
   }
   if (op.kind == 7) {
@@ -2392,86 +2460,109 @@ __global__ void __launch_bounds__(256) shear_x4_kernel(const float* __restrict__
 }
 
 // Fused in-plane rotation of a yaw pose (only the z and x shear passes active; both act inside the y-plane,
-// eqn,rot,decomp with D_y = 1): one CTA per y-plane holds the whole nz x nx plane in shared memory, applies the two
+// eqn,rot,decomp with D_y = 1): one CTA per y-plane holds the nz x nx plane in shared memory, applies the two
 // passes there and writes the plane once -- 8 B of HBM per voxel for the rotation instead of 8 B per pass, one
 // launch instead of two.  Forward (ORDER 0): E^x (E^z in); adjoint (ORDER 1): E^zT (E^xT in) with the transposed
 // tables.  Per output the taps are summed in the same ascending order with the same fp32 FMAs as shear_kernel /
-// shear_x4_kernel, so the result is bit-identical to the two-kernel path.
+// shear_x4_kernel (out-of-range taps contribute exact zeros), so the result is bit-identical to the two-kernel path.
 constexpr int RZX_THREADS = 1024;
 template <int TZ, int TX, int ORDER>
 __global__ void __launch_bounds__(RZX_THREADS, 1) rot_zx_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                                 const int32_t* __restrict__ mz, const float* __restrict__ wz,
                                                                 const int32_t* __restrict__ mx, const float* __restrict__ wx,
                                                                 int nx, int ny, int nz, int accumulate) {
+  // plane buffers [nz][nx + 1] (the pad makes a walk across z conflict-free); nx and nz divide RZX_THREADS
   extern __shared__ float rzx[];
-  float* A = rzx;                    // [nz][nx]: the input plane, later the result
-  float* B = rzx + (size_t)nz * nx;  // [nz][nx]: after the first pass
+  const int P = nx + 1;
+  float* A = rzx;                    // the input plane, later the result
+  float* B = rzx + (size_t)nz * P;   // after the first pass
   const int iy = blockIdx.x, t = threadIdx.x;
   const size_t plane = (size_t)nx * ny;
-  const int nx4 = nx >> 2;
-  for (int e = t; e < nz * nx4; e += RZX_THREADS) {
-    const int z = e / nx4, x4 = e - z * nx4;
-    reinterpret_cast<float4*>(A)[e] = __ldg(reinterpret_cast<const float4*>(in + (size_t)z * plane + (size_t)iy * nx) + x4);
+  const int ne = nz * nx;
+  // loads issued 8 at a time before their shared-memory stores (a load followed at once by its store would
+  // wait out one DRAM latency per element)
+  for (int e0 = t; e0 < ne; e0 += 8 * RZX_THREADS) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
+      v[u] = e < ne ? __ldg(in + (size_t)z * plane + (size_t)iy * nx + x) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
+      if (e < ne) A[z * P + x] = v[u];
+    }
   }
   __syncthreads();
-  // z pass over column x (line x + nx*iy): out(x, z) = sum_k wz[k] A[z + m + k][x]; a thread keeps one column
-  // (RZX_THREADS % nx == 0, checked by the launcher), so its shift and weights are loaded once
+  // z pass: a thread owns column x (line x + nx*iy) and a run of consecutive z; out(x, z) = sum_k wz[k] S[z+m+k][x]
   auto zpass = [&](const float* S, float* D) {
-    const int x = t % nx, line = x + nx * iy, zstep = RZX_THREADS / nx;
+    const int x = t % nx, runs = RZX_THREADS / nx, run = (nz + runs - 1) / runs, z0 = (t / nx) * run;
+    const int line = x + nx * iy;
     const int m0 = __ldg(mz + line);
     float wk[TZ];
 #pragma unroll
     for (int k = 0; k < TZ; ++k) wk[k] = __ldg(wz + (size_t)line * TZ + k);
-    for (int z = t / nx; z < nz; z += zstep) {
+    for (int z = z0; z < min(nz, z0 + run); ++z) {
       float acc = 0.f;
 #pragma unroll
       for (int k = 0; k < TZ; ++k) {
         const int j = z + m0 + k;
-        const float v = (j >= 0 && j < nz) ? S[(size_t)j * nx + x] : 0.f;
-        acc = fmaf(wk[k], v, acc);
+        acc = fmaf(wk[k], (j >= 0 && j < nz) ? S[j * P + x] : 0.f, acc);
       }
-      D[(size_t)z * nx + x] = acc;
+      D[z * P + x] = acc;
     }
   };
-  // x pass over row z (line iy + ny*z): out(x, z) = sum_k wx[k] S[z][x + m + k]
+  // x pass: a thread owns row z (line iy + ny*z) and a run of consecutive x; lanes take consecutive z (padded
+  // rows: distinct banks); out(x, z) = sum_k wx[k] S[z][x+m+k]
   auto xpass = [&](const float* S, float* D) {
-    for (int e = t; e < nx * nz; e += RZX_THREADS) {
-      const int x = e % nx, z = e / nx;
-      const int line = iy + ny * z;
-      const int m0 = __ldg(mx + line);
+    const int z = t % nz, runs = RZX_THREADS / nz, run = (nx + runs - 1) / runs, x0 = (t / nz) * run;
+    const int line = iy + ny * z;
+    const int m0 = __ldg(mx + line);
+    float wk[TX];
+#pragma unroll
+    for (int k = 0; k < TX; ++k) wk[k] = __ldg(wx + (size_t)line * TX + k);
+    for (int x = x0; x < min(nx, x0 + run); ++x) {
       float acc = 0.f;
 #pragma unroll
       for (int k = 0; k < TX; ++k) {
         const int j = x + m0 + k;
-        const float v = (j >= 0 && j < nx) ? S[(size_t)z * nx + j] : 0.f;
-        acc = fmaf(__ldg(wx + (size_t)line * TX + k), v, acc);
+        acc = fmaf(wk[k], (j >= 0 && j < nx) ? S[z * P + j] : 0.f, acc);
       }
-      D[(size_t)z * nx + x] = acc;
+      D[z * P + x] = acc;
     }
   };
   if (ORDER == 0) { zpass(A, B); __syncthreads(); xpass(B, A); }
   else { xpass(A, B); __syncthreads(); zpass(B, A); }
   __syncthreads();
-  for (int e = t; e < nz * nx4; e += RZX_THREADS) {
-    const int z = e / nx4, x4 = e - z * nx4;
-    float4* o = reinterpret_cast<float4*>(out + (size_t)z * plane + (size_t)iy * nx) + x4;
-    float4 r = reinterpret_cast<const float4*>(A)[e];
+  for (int e0 = t; e0 < ne; e0 += 8 * RZX_THREADS) {
+    float p[8];
     if (accumulate) {
-      const float4 p = *o;
-      r.x = p.x + r.x; r.y = p.y + r.y; r.z = p.z + r.z; r.w = p.w + r.w;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
+        p[u] = e < ne ? out[(size_t)z * plane + (size_t)iy * nx + x] : 0.f;
+      }
     }
-    *o = r;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
+      if (e < ne) {
+        const float r = A[z * P + x];
+        out[(size_t)z * plane + (size_t)iy * nx + x] = accumulate ? p[u] + r : r;
+      }
+    }
   }
 }
 
-// Both passes of a yaw rotation in one launch when the plane fits in shared memory; returns false (nothing
-// launched) when the fused form does not apply.
+// Both passes of a yaw rotation in one launch when the plane fits in shared memory (LFM_ROT_FUSE=0 disables);
+// returns false (nothing launched) when the fused form does not apply.
 bool launch_rot_zx(const ShearPass& pz, const ShearPass& px, int dir, const float* in, float* out, int nx, int ny,
                    int nz, int accumulate, void* stream, lfm_status& st, std::string& err) {
-  static const bool off = std::getenv("LFM_NO_ROT_FUSE") != nullptr;
-  const size_t smem = (size_t)2 * nx * nz * 4;
-  if (off || !pz.active || !px.active || pz.axis != 0 || px.axis != 1 || nx % 4 || RZX_THREADS % nx || smem > 200 * 1024 ||
-      (((uintptr_t)in | (uintptr_t)out) & 15) || pz.taps > 8 || px.taps > 8)
+  static const bool off = std::getenv("LFM_ROT_FUSE") && std::getenv("LFM_ROT_FUSE")[0] == '0';
+  const size_t smem = (size_t)2 * (nx + 1) * nz * 4;
+  if (off || !pz.active || !px.active || pz.axis != 0 || px.axis != 1 || RZX_THREADS % nx || RZX_THREADS % nz ||
+      smem > 200 * 1024 || pz.taps > 8 || px.taps > 8)
     return false;
   static bool attr[LFM_MAX_DEV][2][2][2];
   const int dv = cur_dev(), iz_ = pz.taps == 8, ix_ = px.taps == 8;
@@ -2587,7 +2678,7 @@ __global__ void mul_kernel(const float* __restrict__ a, const float* __restrict_
     out[i] = a[i] * b[i];
 }
 
-constexpr int RED_BLOCKS = 592;  // 4 x 148 SMs
+constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs (partials: 3 x 1184 doubles fit the workspace's 16384)
 constexpr int RED_THREADS = 256;
 
 __device__ inline double warp_sum(double v) {
@@ -2632,8 +2723,17 @@ __global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float*
   };
   long long i0 = t;
   if (VEC) {
+    // two float4 of each vector per iteration: six 16-byte loads in flight before the fp64 sums need them
     const long long n4 = n >> 2;
-    for (long long i = t; i < n4; i += stride) {
+    long long i = t;
+    for (; i + stride < n4; i += 2 * stride) {
+      const float4 a0 = __ldg(reinterpret_cast<const float4*>(Ax) + i), a1 = __ldg(reinterpret_cast<const float4*>(Ax) + i + stride);
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(y) + i), b1 = __ldg(reinterpret_cast<const float4*>(y) + i + stride);
+      const float4 c0 = __ldg(reinterpret_cast<const float4*>(w) + i), c1 = __ldg(reinterpret_cast<const float4*>(w) + i + stride);
+      acc(a0.x, b0.x, c0.x); acc(a0.y, b0.y, c0.y); acc(a0.z, b0.z, c0.z); acc(a0.w, b0.w, c0.w);
+      acc(a1.x, b1.x, c1.x); acc(a1.y, b1.y, c1.y); acc(a1.z, b1.z, c1.z); acc(a1.w, b1.w, c1.w);
+    }
+    for (; i < n4; i += stride) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(Ax) + i);
       const float4 b = __ldg(reinterpret_cast<const float4*>(y) + i);
       const float4 c = __ldg(reinterpret_cast<const float4*>(w) + i);
@@ -2706,39 +2806,45 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const float* __re
 }
 
 // grad += beta * sum_{l in N_j, in grid} (x_j - x_l) + nu;  partial [nu*x_j + (beta/4) sum_l (x_j-x_l)^2] (COST)
-// Tiled: a block owns 32 x 8 (x, y) columns and a chunk of R26_ZC slices; the three planes z-1, z, z+1 of the
-// (32+2) x (8+2) footprint rotate through shared memory, so every x value is read from HBM/L2 about once per
-// chunk instead of 27 times through L1.  Neighbours outside the grid contribute nothing (the validity of each
-// of the 26 offsets is a per-thread select); the sum over l runs in the order dz, dy, dx ascending.
-constexpr int R26_ZC = 16;
+// Tiled: a block owns 32 x 8 (x, y) columns and a chunk of R26_ZC slices; the R26_ZC + 2 planes of the
+// (32+2) x (8+2) footprint are loaded into shared memory at once (every load in flight together, one barrier),
+// so every x value is read from HBM/L2 about once per chunk instead of 27 times through L1.  Neighbours outside
+// the grid contribute nothing (the validity of each of the 26 offsets is a per-thread select); the sum over l
+// runs in the order dz, dy, dx ascending.
+constexpr int R26_ZC = 8;
 template <bool COST>
 __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad, int nx,
                                                     int ny, int nz, float beta, float nu, double* part) {
-  __shared__ float pl[3][10][36];
+  __shared__ float pl[R26_ZC + 2][10][34];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8, z0 = blockIdx.z * R26_ZC;
   const int ix = x0 + tx, iy = y0 + ty;
   const size_t plane = (size_t)nx * ny;
-  auto load = [&](int slot, int zz) {
-    for (int e = tid; e < 340; e += 256) {
-      const int ly = e / 34, lx = e % 34, gx = x0 + lx - 1, gy = y0 + ly - 1;
-      pl[slot][ly][lx] = (zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-                             ? __ldg(x + (size_t)zz * plane + (size_t)gy * nx + gx) : 0.f;
-    }
-  };
-  load(0, z0 - 1);
-  load(1, z0);
+  // all (R26_ZC + 2) x 340 footprint loads in flight before their stores (14 per thread)
+  constexpr int NE = (R26_ZC + 2) * 340, NL = (NE + 255) / 256;
+  float v0[NL];
+#pragma unroll
+  for (int u = 0; u < NL; ++u) {
+    const int e = tid + 256 * u;
+    const int pz = e / 340, r = e - pz * 340, ly = r / 34, lx = r - ly * 34;
+    const int gx = x0 + lx - 1, gy = y0 + ly - 1, zz = z0 + pz - 1;
+    v0[u] = (e < NE && zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
+                ? __ldg(x + (size_t)zz * plane + (size_t)gy * nx + gx) : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < NL; ++u) {
+    const int e = tid + 256 * u;
+    if (e < NE) (&pl[0][0][0])[e] = v0[u];
+  }
+  __syncthreads();
   const bool vx[3] = {ix > 0, true, ix < nx - 1}, vy[3] = {iy > 0, true, iy < ny - 1};
   double v = 0;
-  for (int q = 0; q < R26_ZC; ++q) {
-    const int iz = z0 + q;
-    if (iz >= nz) break;
-    load((q + 2) % 3, iz + 1);
-    __syncthreads();
-    if (ix < nx && iy < ny) {
+  if (ix < nx && iy < ny) {
+    for (int q = 0; q < R26_ZC; ++q) {
+      const int iz = z0 + q;
+      if (iz >= nz) break;
       const bool vz[3] = {iz > 0, true, iz < nz - 1};
-      const int sl[3] = {q % 3, (q + 1) % 3, (q + 2) % 3};   // planes z-1, z, z+1
-      const float xj = pl[sl[1]][ty + 1][tx + 1];
+      const float xj = pl[q + 1][ty + 1][tx + 1];
       float g = 0.f;
       double rs = 0;
 #pragma unroll
@@ -2748,7 +2854,7 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
             if (dz == 1 && dy == 1 && dx == 1) continue;
-            const float d = xj - pl[sl[dz]][ty + dy][tx + dx];
+            const float d = xj - pl[q + dz][ty + dy][tx + dx];
             const bool ok = vz[dz] && vy[dy] && vx[dx];
             g += ok ? d : 0.f;
             if (COST) rs += ok ? (double)d * (double)d : 0.0;
@@ -2757,7 +2863,6 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
       grad[i] += beta * g + nu;
       if (COST) v += (double)nu * xj + 0.25 * (double)beta * rs;
     }
-    __syncthreads();
   }
   if (COST) {
     // block partial (256 threads = 8 warps), fixed order

@@ -234,13 +234,15 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err);
 void free_camera(CameraPlan& cp);
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0 = 0, int out_r1 = -1, int win_r0 = 0,
-                      int win_r1 = -1);
+                      int win_r1 = -1, int out_c0 = 0, int out_c1 = -1, float* part = nullptr,
+                      size_t part_bytes = 0);
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
 lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
-lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err);
+lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
+                       int c0 = 0, int c1 = -1);
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
-                       std::string& err);
+                       std::string& err, int c0 = 0, int c1 = -1);
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);

@@ -94,6 +94,8 @@ _SIGS = {
     "lfm_A_adjoint": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_forward_rows": [_P, _I, _I, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint_rows": [_P, _I, _I, _I, _I, _P, _P, _I, _P, _S, _P],
+    "lfm_A_forward_window": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _S, _P],
+    "lfm_A_adjoint_window": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _S, _P],
     "lfm_A_stage": [_P, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_forward_subset": [_P, _I, _I, _P, _P, _P, _S, _P],
     "lfm_A_adjoint_subset": [_P, _I, _I, _P, _P, _I, _P, _S, _P],
@@ -238,6 +240,16 @@ def A_adjoint(plan, cam, y, x, ws, accumulate=False, path=COLLAPSED, stream=None
 def A_forward_rows(plan, cam, row0, row1, x, y, ws, path=COLLAPSED, stream=None):
     _check(_lib.lfm_A_forward_rows(plan.handle, cam, path, row0, row1, _ptr(x), _ptr(y), _ptr(ws), ws.numel(),
                                    _stream(stream)))
+
+
+def A_forward_window(plan, cam, row0, row1, col0, col1, x, y, ws, path=COLLAPSED, stream=None):
+    _check(_lib.lfm_A_forward_window(plan.handle, cam, path, row0, row1, col0, col1, _ptr(x), _ptr(y), _ptr(ws),
+                                     ws.numel(), _stream(stream)))
+
+
+def A_adjoint_window(plan, cam, row0, row1, col0, col1, y, x, ws, accumulate=False, path=COLLAPSED, stream=None):
+    _check(_lib.lfm_A_adjoint_window(plan.handle, cam, path, row0, row1, col0, col1, _ptr(y), _ptr(x), int(accumulate),
+                                     _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def A_forward_subset(plan, cam, subset, x, y, ws, stream=None):

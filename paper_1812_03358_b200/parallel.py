@@ -1,28 +1,41 @@
-"""Multi-GPU partition of an A + A^T pair (SURVEY §8(e)): one process per GPU, NCCL over NVLink.
+"""Multi-GPU partition of an A + A^T pair (SURVEY §8(e), DESIGN.md §7): one process per GPU, NCCL over NVLink.
 
-Work items are (camera, detector rows [r0, r1)): cameras are dealt round-robin over the ranks; with
-more ranks than cameras every camera's detector rows are split into contiguous tiles.  Forward
-projection needs no communication (x is replicated; each rank produces its rows of y_c).  The adjoint
-of each rank covers only its rows (A_c^T P_rows y_c); the partial volumes are summed by ONE all-reduce
-of n_vox fp32 values -- the only data-path collective.  Orchestration only: the per-item operators
-are injected (the C-ABI calls on a GPU; any implementation in the CPU tests).
+Work items are (camera, detector window [r0, r1) x [c0, c1)).  Cameras are dealt round-robin over the ranks; with
+more ranks than cameras every camera's detector is split into contiguous tiles -- by default along the detector
+columns s, the axis the collapsed operator's s passes act on column by column, so a column shard shrinks every
+kernel of the pair (band_v items, band_u tiles; DESIGN.md §7 has the per-rank timings), or along the rows t.
+Forward projection needs no communication (x is replicated; each rank produces its window of y_c).  The adjoint
+of each rank covers only its window (A_c^T P_window y_c); the partial volumes are summed by ONE all-reduce of
+n_vox fp32 values -- the only data-path collective.  Orchestration only: the per-item operators are injected
+(the C-ABI calls on a GPU; any implementation in the CPU tests).
 """
 
 
-def shard(n_rows, rank, world):
-    """Items (camera, r0, r1) of `rank`; n_rows[c] = detector rows of camera c."""
-    n_cam = len(n_rows)
+def _split(n, k, align):
+    """k contiguous tiles of [0, n) with inner edges on multiples of `align` (empty tiles dropped)."""
+    edges = [0] + [min(n, (n * i // k + align // 2) // align * align) for i in range(1, k)] + [n]
+    return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+def shard(dims, rank, world, axis="cols", align=4):
+    """Items (camera, r0, r1, c0, c1) of `rank`; dims[c] = (n_t, n_s) of camera c.  axis "cols": tiles of
+    columns whose inner edges are multiples of `align` (band_v moves 16-byte column groups); "rows": tiles of
+    rows."""
+    n_cam = len(dims)
     if world <= n_cam:
-        return [(c, 0, n_rows[c]) for c in range(n_cam) if c % world == rank]
+        return [(c, 0, dims[c][0], 0, dims[c][1]) for c in range(n_cam) if c % world == rank]
     per = world // n_cam
     extra = world - per * n_cam                     # the first `extra` cameras get one more tile
     c, slot = 0, rank
     while c < n_cam:
         tiles = per + (1 if c < extra else 0)
         if slot < tiles:
-            r0 = n_rows[c] * slot // tiles
-            r1 = n_rows[c] * (slot + 1) // tiles
-            return [(c, r0, r1)] if r1 > r0 else []
+            n_t, n_s = dims[c]
+            if axis == "rows":
+                parts = _split(n_t, tiles, 1)
+                return [(c, parts[slot][0], parts[slot][1], 0, n_s)] if slot < len(parts) else []
+            parts = _split(n_s, tiles, align)
+            return [(c, 0, n_t, parts[slot][0], parts[slot][1])] if slot < len(parts) else []
         slot -= tiles
         c += 1
     return []
@@ -31,26 +44,26 @@ def shard(n_rows, rank, world):
 class PairRunner:
     """One A+A^T pair of this rank.
 
-    forward_rows(c, r0, r1, x, y_c) -> writes rows [r0, r1) of y_c
-    adjoint_rows(c, r0, r1, r_c, g, accumulate) -> g (+)= A_c^T P_[r0,r1) r_c
+    forward_win(c, win, x, y_c) -> writes the window win = (r0, r1, c0, c1) of y_c
+    adjoint_win(c, win, r_c, g, accumulate) -> g (+)= A_c^T P_win r_c
     zero(g); allreduce(g) (None on one rank)
     """
 
-    def __init__(self, items, forward_rows, adjoint_rows, zero, allreduce=None):
+    def __init__(self, items, forward_win, adjoint_win, zero, allreduce=None):
         self.items = items
-        self.forward_rows = forward_rows
-        self.adjoint_rows = adjoint_rows
+        self.forward_win = forward_win
+        self.adjoint_win = adjoint_win
         self.zero = zero
         self.allreduce = allreduce
 
     def forward(self, x, ys):
-        for c, r0, r1 in self.items:
-            self.forward_rows(c, r0, r1, x, ys[c])
+        for c, *win in self.items:
+            self.forward_win(c, tuple(win), x, ys[c])
 
     def adjoint(self, rs, g):
         first = True
-        for c, r0, r1 in self.items:
-            self.adjoint_rows(c, r0, r1, rs[c], g, not first)
+        for c, *win in self.items:
+            self.adjoint_win(c, tuple(win), rs[c], g, not first)
             first = False
         if first:
             self.zero(g)
@@ -73,26 +86,31 @@ class ConcurrentPair:
     accumulate(src, dst) adds on the main stream.
     """
 
-    def __init__(self, items, forward_rows, adjoint_rows, accumulate, zero, run, join, private, allreduce=None):
+    def __init__(self, items, forward_win, adjoint_win, accumulate, zero, run, join, private, allreduce=None):
         self.items = items
-        self.forward_rows = forward_rows      # (i, c, r0, r1, x, y)
-        self.adjoint_rows = adjoint_rows      # (i, c, r0, r1, r, g_target)   overwrite
-        self.accumulate = accumulate          # (src, dst)                     dst += src
+        self.forward_win = forward_win        # (i, c, win, x, y)
+        self.adjoint_win = adjoint_win        # (i, c, win, r, g_target)   overwrite
+        self.accumulate = accumulate          # (src, dst)                 dst += src
         self.zero = zero
         self.run = run                        # (i, fn)
         self.join = join                      # ()
         self.private = private                # private[i] for i >= 1: volume buffers
         self.allreduce = allreduce
 
-    def pair(self, x, ys, rs, g):
-        for i, (c, r0, r1) in enumerate(self.items):
+    def compute(self, x, ys, rs, g):
+        """Everything but the all-reduce (what a per-rank CUDA graph captures)."""
+        for i, (c, *win) in enumerate(self.items):
             tgt = g if i == 0 else self.private[i]
-            self.run(i, lambda i=i, c=c, r0=r0, r1=r1, tgt=tgt: (self.forward_rows(i, c, r0, r1, x, ys[c]),
-                                                            self.adjoint_rows(i, c, r0, r1, rs[c], tgt)))
+            w = tuple(win)
+            self.run(i, lambda i=i, c=c, w=w, tgt=tgt: (self.forward_win(i, c, w, x, ys[c]),
+                                                        self.adjoint_win(i, c, w, rs[c], tgt)))
         self.join()
         if not self.items:
             self.zero(g)
         for i in range(1, len(self.items)):
             self.accumulate(self.private[i], g)
+
+    def pair(self, x, ys, rs, g):
+        self.compute(x, ys, rs, g)
         if self.allreduce is not None:
             self.allreduce(g)

@@ -1,7 +1,7 @@
 """The rotation passes' kernel variants give bit-identical results (eqn,rot,toeplitz P:1186-1198).
 
 A yaw pose (z and x passes only) runs both passes in one in-plane kernel (`rot_zx_kernel`, the default; off with
-LFM_NO_ROT_FUSE).  Otherwise `launch_shear` picks the x-pass kernel (`shear_x4_kernel`, 4 consecutive x per thread from float4 windows, or the
+LFM_ROT_FUSE=0).  Otherwise `launch_shear` picks the x-pass kernel (`shear_x4_kernel`, 4 consecutive x per thread from float4 windows, or the
 scalar `shear_kernel`) and the z chunk per thread from LFM_SH_X4 / LFM_SH_ZC, read once per process; every
 variant keeps the same FMA order per output, so vol_rotate (forward and adjoint, store and accumulate) must
 agree bit for bit with the scalar kernel.  Each setting runs in its own process.  Parity of the default against
@@ -52,14 +52,11 @@ def _run(tmp_path, env_extra, tag):
 
 @pytest.mark.gpu
 def test_shear_variants_bit_identical(tmp_path):
-    ref = _run(tmp_path, {"LFM_SH_X4": "0", "LFM_SH_ZC": "8", "LFM_NO_ROT_FUSE": "1"}, "scalar")
+    ref = _run(tmp_path, {"LFM_SH_X4": "0", "LFM_SH_ZC": "8", "LFM_ROT_FUSE": "0"}, "scalar")
     assert any(np.abs(v).max() > 0 for v in ref.values())
-    # the default (yaw poses: both passes fused in one in-plane kernel, rot_zx_kernel) and the unfused variants
-    for x4, zc, fuse in (("4", "16", "1"), ("1", "16", ""), ("2", "32", ""), ("3", "8", ""), ("4", "16", ""),
-                         ("5", "8", "")):
-        env = {"LFM_SH_X4": x4, "LFM_SH_ZC": zc}
-        if not fuse:
-            env["LFM_NO_ROT_FUSE"] = "1"
-        got = _run(tmp_path, env, f"x4_{x4}_zc_{zc}_f{fuse}")
+    # the default (yaw poses: both passes in one in-plane kernel, rot_zx_kernel) and the unfused variants
+    for x4, zc, fuse in (("4", "16", "1"), ("1", "16", "0"), ("2", "32", "0"), ("3", "8", "0"), ("4", "16", "0"),
+                         ("5", "8", "0")):
+        got = _run(tmp_path, {"LFM_SH_X4": x4, "LFM_SH_ZC": zc, "LFM_ROT_FUSE": fuse}, f"x4_{x4}_zc_{zc}_f{fuse}")
         for k, v in ref.items():
             assert np.array_equal(got[k], v), (x4, zc, k)

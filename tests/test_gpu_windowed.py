@@ -80,3 +80,75 @@ def test_row_windows_partition(name):
             lfm.A_adjoint_rows(plan, c, r0, r1, r, g, ws, accumulate=i > 0)
         gf = host(g_full)
         assert max_rel(host(g), gf) <= TOL
+
+
+def _col_cuts(n_s):
+    # ragged, multiples of 4 (band_v's TMA column alignment) but not of the 256-column tiles
+    return [0, n_s // 6 - (n_s // 6) % 4 + 4, n_s // 2 + 4, (3 * n_s) // 4 + 8, n_s]
+
+
+@pytest.mark.parametrize("name", ["64^3 single", "128^3 two-camera"])
+def test_column_and_tile_windows_partition(name):
+    """Column windows (the multi-GPU shards of DESIGN.md §7) and 2-D tiles: windowed forwards reproduce the full
+    forward on their window; windowed adjoints over a partition sum to the full adjoint.  A 256-column window and
+    a quarter of the rows leave most SMs idle, so band_u's forward runs split-K there (partials summed in order)."""
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config(name)
+    plan = _plan(cfg)
+    ws = plan.workspace()
+    x = torch.as_tensor(uniform_volume(cfg["volume"], 0), device="cuda:0").reshape(-1)
+    for c in range(plan.n_cam):
+        inf = plan.infos[c]
+        n_t, n_s = inf["n_t"], inf["n_s"]
+        y_full = torch.empty(inf["n_pix"], device="cuda:0")
+        lfm.A_forward(plan, c, x, y_full, ws)
+        yf = host(y_full).reshape(n_t, n_s)
+        r = torch.as_tensor(uniform_vector(inf["n_pix"], 1 + c), device="cuda:0")
+        g_full = torch.empty(inf["n_vox"], device="cuda:0")
+        lfm.A_adjoint(plan, c, r, g_full, ws)
+        gf = host(g_full)
+        ccuts = _col_cuts(n_s)
+        windows = [(0, n_t, a, b) for a, b in zip(ccuts[:-1], ccuts[1:])]
+        windows_2d = [(r0, r1, c0, c1) for r0, r1 in ((0, n_t // 2 + 3), (n_t // 2 + 3, n_t))
+                      for c0, c1 in ((0, n_s // 4 + 12), (n_s // 4 + 12, n_s))]
+        windows_small = [(0, n_t // 4, 0, n_s), (0, n_t, 256, 512)]     # split-K shapes
+        for wins in (windows, windows_2d):
+            y = torch.full((inf["n_pix"],), float("nan"), device="cuda:0")
+            g = torch.empty(inf["n_vox"], device="cuda:0")
+            for i, (r0, r1, c0, c1) in enumerate(wins):
+                lfm.A_forward_window(plan, c, r0, r1, c0, c1, x, y, ws)
+                got = host(y).reshape(n_t, n_s)[r0:r1, c0:c1]
+                assert np.abs(got - yf[r0:r1, c0:c1]).max() <= TOL * np.abs(yf).max(), (c, r0, r1, c0, c1)
+                lfm.A_adjoint_window(plan, c, r0, r1, c0, c1, r, g, ws, accumulate=i > 0)
+            assert max_rel(host(g), gf) <= TOL, (c, wins)
+        for r0, r1, c0, c1 in windows_small:
+            y = torch.full((inf["n_pix"],), float("nan"), device="cuda:0")
+            lfm.A_forward_window(plan, c, r0, r1, c0, c1, x, y, ws)
+            got = host(y).reshape(n_t, n_s)[r0:r1, c0:c1]
+            assert np.abs(got - yf[r0:r1, c0:c1]).max() <= TOL * np.abs(yf).max(), (c, r0, r1, c0, c1)
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_windows_vs_oracle(path):
+    """Window entry points against the fp64 oracle: A^T P y with P the window mask, on both evaluation orders
+    (the per-view path applies a column window by masking y)."""
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config("small_two")
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    ops = build_system(cfg)
+    x = uniform_volume(cfg["volume"], 0)
+    for c, op in enumerate(ops):
+        n_t, n_s = cfg["cameras"][c]["n_t"], cfg["cameras"][c]["n_s"]
+        r = uniform_vector(op.n_pix, 1).reshape(n_t, n_s)
+        yref = op.forward(x.astype(np.float64)).reshape(n_t, n_s)
+        for r0, r1, c0, c1 in ((0, n_t, 0, 24), (0, n_t, 24, n_s), (5, 40, 8, 52)):
+            y = torch.full((op.n_pix,), float("nan"), device="cuda:0")
+            lfm.A_forward_window(plan, c, r0, r1, c0, c1, dev(x), y, ws, path=path)
+            got = host(y).reshape(n_t, n_s)[r0:r1, c0:c1]
+            assert np.abs(got - yref[r0:r1, c0:c1]).max() <= TOL * np.abs(yref).max()
+            m = np.zeros_like(r)
+            m[r0:r1, c0:c1] = r[r0:r1, c0:c1]
+            g = torch.empty(op.n_vox, device="cuda:0")
+            lfm.A_adjoint_window(plan, c, r0, r1, c0, c1, dev(r), g, ws, path=path)
+            assert max_rel(host(g), op.adjoint(m.ravel().astype(np.float64))) <= TOL

@@ -1,7 +1,7 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): the partition covers every detector row of
-every camera exactly once, and the all-reduced partial adjoints of the ranks equal the single-process
-adjoint; rank-local forward rows equal the corresponding rows of the full forward.  The per-item
-operators here are the fp64 oracle restricted to rows (tests may use the oracle)."""
+"""Multi-rank host logic on CPU (gloo, world_size 2, 3 and 4): the partition covers every detector pixel of
+every camera exactly once (column tiles, the default, and row tiles), and the all-reduced partial adjoints of the
+ranks equal the single-process adjoint; rank-local forward windows equal the corresponding window of the full
+forward.  The per-item operators here are the fp64 oracle restricted to a window (tests may use the oracle)."""
 import os
 
 import numpy as np
@@ -13,18 +13,22 @@ import torch.multiprocessing as mp
 from paper_1812_03358_b200.parallel import ConcurrentPair, PairRunner, shard
 
 
+@pytest.mark.parametrize("axis", ["cols", "rows"])
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
-@pytest.mark.parametrize("rows", [[32], [32, 32], [2048, 2048], [21, 32, 32], [2048] * 4])
-def test_partition_covers_rows_once(world, rows):
-    seen = [np.zeros(n, int) for n in rows]
+@pytest.mark.parametrize("dims", [[(32, 32)], [(32, 32), (32, 32)], [(2048, 2048)] * 2, [(21, 35), (32, 32), (32, 32)],
+                                  [(2048, 2048)] * 4])
+def test_partition_covers_pixels_once(world, dims, axis):
+    seen = [np.zeros(d, int) for d in dims]
     for r in range(world):
-        for c, r0, r1 in shard(rows, r, world):
-            seen[c][r0:r1] += 1
+        for c, r0, r1, c0, c1 in shard(dims, r, world, axis=axis):
+            seen[c][r0:r1, c0:c1] += 1
+            if axis == "cols" and 0 < c0:
+                assert c0 % 4 == 0
     for s in seen:
         assert (s == 1).all()
 
 
-def _worker(rank, world, port, out, mode="seq"):
+def _worker(rank, world, port, out, mode="seq", axis="cols"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -33,18 +37,19 @@ def _worker(rank, world, port, out, mode="seq"):
         from workloads import make_config, uniform_vector, uniform_volume
         cfg = make_config("tiny_multi")
         ops = build_system(cfg)
-        n_rows = [c["n_t"] for c in cfg["cameras"]]
+        dims = [(c["n_t"], c["n_s"]) for c in cfg["cameras"]]
         x = uniform_volume(cfg["volume"], 0).astype(np.float64).ravel()
         rs = [uniform_vector(op.n_pix, 1 + c).astype(np.float64) for c, op in enumerate(ops)]
 
-        def fwd_rows(c, r0, r1, xv, y):
-            full = ops[c].forward(xv).reshape(n_rows[c], -1)
-            y.reshape(n_rows[c], -1)[r0:r1] = full[r0:r1]
+        def fwd_win(c, win, xv, y):
+            r0, r1, c0, c1 = win
+            full = ops[c].forward(xv).reshape(dims[c])
+            y.reshape(dims[c])[r0:r1, c0:c1] = full[r0:r1, c0:c1]
 
-        def adj_rows(c, r0, r1, r, g, acc):
-            rr = r.reshape(n_rows[c], -1).copy()
-            rr[:r0] = 0.0
-            rr[r1:] = 0.0
+        def adj_win(c, win, r, g, acc):
+            r0, r1, c0, c1 = win
+            rr = np.zeros(dims[c])
+            rr[r0:r1, c0:c1] = r.reshape(dims[c])[r0:r1, c0:c1]
             v = ops[c].adjoint(rr.ravel())
             if acc:
                 g += v
@@ -56,13 +61,13 @@ def _worker(rank, world, port, out, mode="seq"):
             dist.all_reduce(t)
             g[:] = t.numpy()
 
-        items = shard(n_rows, rank, world)
+        items = shard(dims, rank, world, axis=axis)
         if mode == "seq":
-            runner = PairRunner(items, fwd_rows, adj_rows, lambda g: g.fill(0.0), allreduce)
+            runner = PairRunner(items, fwd_win, adj_win, lambda g: g.fill(0.0), allreduce)
         else:  # per-item "streams" are plain calls on CPU; private volumes for items >= 1
             private = [None] + [np.zeros(ops[0].n_vox) for _ in items[1:]]
-            runner = ConcurrentPair(items, lambda i, c, r0, r1, xv, y: fwd_rows(c, r0, r1, xv, y),
-                                    lambda i, c, r0, r1, r, tgt: adj_rows(c, r0, r1, r, tgt, False),
+            runner = ConcurrentPair(items, lambda i, c, w, xv, y: fwd_win(c, w, xv, y),
+                                    lambda i, c, w, r, tgt: adj_win(c, w, r, tgt, False),
                                     lambda src, dst: dst.__iadd__(src), lambda g: g.fill(0.0),
                                     lambda i, fn: fn(), lambda: None, private, allreduce)
         ys = [np.full(op.n_pix, np.nan) for op in ops]
@@ -71,21 +76,21 @@ def _worker(rank, world, port, out, mode="seq"):
         ref_g = sum(op.adjoint(r) for op, r in zip(ops, rs))
         ok_g = np.abs(g - ref_g).max() <= 1e-12 * np.abs(ref_g).max()
         ok_y = True
-        for c, r0, r1 in items:
-            full = ops[c].forward(x).reshape(n_rows[c], -1)
-            ok_y &= np.array_equal(ys[c].reshape(n_rows[c], -1)[r0:r1], full[r0:r1])
+        for c, r0, r1, c0, c1 in items:
+            full = ops[c].forward(x).reshape(dims[c])
+            ok_y &= np.array_equal(ys[c].reshape(dims[c])[r0:r1, c0:c1], full[r0:r1, c0:c1])
         out[rank] = bool(ok_g and ok_y)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world,axis", [(2, "cols"), (4, "cols"), (4, "rows")])
 @pytest.mark.parametrize("mode", ["seq", "conc"])
-def test_gloo_pair_equals_single_process(world, mode):
-    port = 29500 + 7 * world + (13 if mode == "conc" else 0) + os.getpid() % 200
+def test_gloo_pair_equals_single_process(world, mode, axis):
+    port = 29500 + 7 * world + (13 if mode == "conc" else 0) + (50 if axis == "rows" else 0) + os.getpid() % 200
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out, mode), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, out, mode, axis), nprocs=world, join=True)
     assert all(out[r] for r in range(world))
 
 
@@ -98,13 +103,13 @@ def test_concurrent_pair_sums_in_item_order():
     ops = build_system(cfg)
     x = uniform_volume(cfg["volume"], 0).astype(np.float64).ravel()
     rs = [uniform_vector(op.n_pix, 1 + c).astype(np.float64) for c, op in enumerate(ops)]
-    items = [(c, 0, cam["n_t"]) for c, cam in enumerate(cfg["cameras"])]
+    items = [(c, 0, cam["n_t"], 0, cam["n_s"]) for c, cam in enumerate(cfg["cameras"])]
     assert len(items) >= 2
 
-    def fwd(c, r0, r1, xv, y):
+    def fwd(c, win, xv, y):
         y[:] = ops[c].forward(xv)
 
-    def adj(c, r0, r1, r, g, acc):
+    def adj(c, win, r, g, acc):
         v = ops[c].adjoint(r)
         if acc:
             g += v
@@ -118,8 +123,8 @@ def test_concurrent_pair_sums_in_item_order():
     ys2 = [np.zeros(op.n_pix) for op in ops]
     g2 = np.full(ops[0].n_vox, np.nan)
     private = [None] + [np.full(ops[0].n_vox, np.nan) for _ in items[1:]]
-    ConcurrentPair(items, lambda i, c, r0, r1, xv, y: fwd(c, r0, r1, xv, y),
-                   lambda i, c, r0, r1, r, tgt: adj(c, r0, r1, r, tgt, False),
+    ConcurrentPair(items, lambda i, c, w, xv, y: fwd(c, w, xv, y),
+                   lambda i, c, w, r, tgt: adj(c, w, r, tgt, False),
                    lambda src, dst: (order.append(id(src)), dst.__iadd__(src)), lambda g: g.fill(0.0),
                    lambda i, fn: fn(), lambda: None, private).pair(x, ys2, rs, g2)
     assert order == [id(p) for p in private[1:]]

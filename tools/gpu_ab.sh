@@ -1,8 +1,19 @@
-# A/B of environment settings on the bench: bash tools/gpu_ab.sh "ENV1=.. ENV2=.." "ENV3=.." ...
+# A/B on one box: bench default vs the unfused rotation; shard timing; launch list of one bench pair
+set -x
 mkdir -p gpurun_out
-for e in "$@"; do
-  echo "== $e"
-  env $e LFM_DEBUG_TUNE=1 LFM_DEBUG=1 timeout 600 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-per-view --no-e2e > gpurun_out/ab.log 2> gpurun_out/ab.err
-  python -c "import json; d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]); print('pairs/s %.1f' % d['value'])"
-  grep "direct s" gpurun_out/ab.err | head -2
+timeout 900 python -m pytest tests/test_gpu_windowed.py tests/test_gpu_shear.py -q -ra -x > gpurun_out/t_win.log 2>&1; echo "T EXIT $?" >> gpurun_out/t_win.log
+tail -5 gpurun_out/t_win.log
+for i in 1 2; do
+timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --no-e2e --no-per-view --no-recon > gpurun_out/bench_a$i.log 2>&1
+LFM_NO_ROT_FUSE=1 timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --no-e2e --no-per-view --no-recon > gpurun_out/bench_b$i.log 2>&1
 done
+python - <<'PY'
+import json
+for n in ("a1","b1","a2","b2"):
+    d=json.loads(open("gpurun_out/bench_%s.log"%n).read().strip().splitlines()[-1])
+    k=d["kernels"]
+    print(n, "%.1f pairs/s"%d["value"], {kk: round(v["ms"]*1e3,1) for kk,v in k.items()})
+PY
+timeout 600 python tools/shard_timing.py 1 > gpurun_out/shard_timing.json 2> gpurun_out/shard_timing.err; echo "SHARD EXIT $?"
+cat gpurun_out/shard_timing.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-per-view --no-recon --no-graph > gpurun_out/ncu_list.log 2>&1; echo "NCU EXIT $?"
