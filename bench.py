@@ -414,12 +414,13 @@ def run_ours(args, rank, world, local_rank):
     # the slice sum over the interleaved intermediate); its adjoint counterpart is ADJ_T.  Each launch
     # is timed alone with events on the bench stream, after an L2 flush, inputs from a full call.
     def timed(fn, reps=max(5, min(21, args.steps // 4)), prep=None):
-        """Median device time (ms) of fn() alone on the bench stream, L2 flushed before every launch."""
+        """Median device time (ms) of fn() alone on the bench stream, L2 flushed before every launch by READING a
+        256 MiB buffer (a write flush would leave L2 full of dirty lines whose write-back the timed kernel pays)."""
         out = []
         for _ in range(reps):
             if prep is not None:
                 prep()
-            flush.zero_()
+            torch.sum(flush)
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_.record(stream)
             fn()
@@ -608,10 +609,29 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t_maj, t_run = e0.elapsed_time(e1), e1.elapsed_time(e2)
         rel = float((xr_ - x).norm() / x.norm())
+        # ordered subsets (sec,subset P:360-388) with M = 4 view subsets (M divides K_s = 8: tensor-product subsets,
+        # reading R9, so every subset iteration runs on the collapsed tcgen05 path): ms per subset iteration
+        plan_os = lfm.Plan(cfg, device=local_rank, n_subsets=4)
+        rec_os = PWLS(plan_os, yd, wd, rec.beta)
+        rec_os.fista(2, subsets=True)
+        torch.cuda.synchronize()
+        e3, e4, e5 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e3.record(stream)
+        rec_os.majoriser()
+        e4.record(stream)
+        rec_os.fista(iters, subsets=True)
+        e5.record(stream)
+        torch.cuda.synchronize()
+        t_os = e4.elapsed_time(e5) - e3.elapsed_time(e4)
+        os_line = {"n_subsets": 4, "ms_per_subset_iteration": t_os / iters,
+                   "ratio_to_full_iteration": (t_os / iters) / ((t_run - t_maj) / iters),
+                   "subsets_on_collapsed_path": plan_os.infos[0]["subset_collapsed"]}
+        plan_os.close()
         recon = {"workload": "recon: 128^3 two-camera, 50 FISTA iterations, gains (1, 0.7), W = 1, beta = 0.01 "
                              "median(d)", "ms_per_iteration": (t_run - t_maj) / iters, "iterations": iters,
                  "ms_majoriser": t_maj, "ms_total": t_run, "iterations_per_s": 1e3 * iters / (t_run - t_maj),
                  "rel_error_vs_truth_after_50": rel,
+                 "ordered_subsets": os_line,
                  "per_iteration": "A_c z + stats (every camera), gains, sum_c A_c^T W(A_c z - gamma y) + reg26, "
                                   "FISTA update; majoriser (one extra forward+adjoint per camera) once per run"}
 

@@ -110,22 +110,8 @@ lfm_status check_cam(const lfm_plan_s* p, int cam, bool need_device = true) {
 // Rotation forward: returns the buffer holding x^r (x itself if the pose is the identity).  Stages in
 // order: the quarter-turn relabelling (if any, reading R7), then the active shear passes z, x, y;
 // intermediate results ping-pong between w.r0 and w.r1, the last one goes to final_out if given.
-// A yaw pose (only the z and x shear passes, no relabelling): both passes in one fused in-plane launch.
-static bool yaw_only(const CameraPlan& cp) { return !cp.has_perm && cp.rot[0].active && cp.rot[1].active && !cp.rot[2].active; }
-
 lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, int accumulate, const Ws& w,
                       void* stream, const float** xr) {
-  if (yaw_only(cp)) {
-    float* dst = final_out ? final_out : w.r0;
-    lfm_status st = LFM_OK;
-    std::string err;
-    if (launch_rot_zx(cp.rot[0], cp.rot[1], 0, x, dst, cp.info.nx, cp.info.ny, cp.info.nz, final_out ? accumulate : 0,
-                      stream, st, err)) {
-      if (st != LFM_OK) return fail(st, err);
-      *xr = dst;
-      return LFM_OK;
-    }
-  }
   int act[4], na = 0;
   if (cp.has_perm) act[na++] = -1;
   for (int q = 0; q < 3; ++q)
@@ -155,12 +141,6 @@ lfm_status rotate_fwd(const CameraPlan& cp, const float* x, float* final_out, in
 // Rotation adjoint E^zT E^xT E^yT, then the inverse relabelling P^T, applied to `in`, written (or
 // accumulated) into `out`.  `in` may be w.r0 or w.r1 (the ping-pong never writes the buffer it reads).
 lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int accumulate, const Ws& w, void* stream) {
-  if (yaw_only(cp)) {
-    lfm_status st = LFM_OK;
-    std::string err;
-    if (launch_rot_zx(cp.rot[0], cp.rot[1], 1, in, out, cp.info.nx, cp.info.ny, cp.info.nz, accumulate, stream, st, err))
-      return st == LFM_OK ? st : fail(st, err);
-  }
   int act[4], na = 0;
   for (int q = 2; q >= 0; --q)
     if (cp.rot[q].active) act[na++] = q;

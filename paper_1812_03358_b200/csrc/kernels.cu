@@ -542,12 +542,35 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, floa
   const int ob[3] = {T.N / 2, 32, 1};
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
   const float sc = cp.adj_c2.out_scale;
+  // a column window reaches only the voxel-column tiles whose K blocks meet it (host copy of the block starts):
+  // launch those; the rest of the output is zero (memset first unless accumulating)
+  int nt0 = 0, nt_cnt = -1;
+  if (k_lo > 0 || k_hi < (1 << 30)) {
+    int lo = T.n_nt, hi = -1;
+    for (int nt = 0; nt < T.n_nt; ++nt)
+      for (int n = 0; n < nz && !(lo <= nt && nt <= hi); ++n) {
+        const size_t key = (size_t)n * T.n_nt + nt;
+        for (int b = T.off[key]; b < T.off[key + 1]; ++b)
+          if (T.k0[b] + T.BK > k_lo && T.k0[b] < k_hi) {
+            lo = std::min(lo, nt);
+            hi = std::max(hi, nt);
+            break;
+          }
+      }
+    nt0 = hi < 0 ? 0 : lo;
+    nt_cnt = hi < 0 ? 0 : hi - lo + 1;
+    if (!accumulate && (nt0 > 0 || nt0 + nt_cnt < T.n_nt)) {
+      if (cudaMemsetAsync(out, 0, (size_t)nx * ny * nz * 4, (cudaStream_t)stream) != cudaSuccess)
+        return cuda_check(cudaGetLastError(), "band_v window memset", err);
+    }
+    if (nt_cnt == 0) return LFM_OK;
+  }
   if (T.N == 32)
-    return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi)
-                      : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
-  if (T.BK == 64) return launch_band_v<16, 1, 64>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
-  return T.BK == 32 ? launch_band_v<16, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi)
-                    : launch_band_v<16, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, 0, -1, k_lo, k_hi);
+    return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi)
+                      : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi);
+  if (T.BK == 64) return launch_band_v<16, 1, 64>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi);
+  return T.BK == 32 ? launch_band_v<16, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi)
+                    : launch_band_v<16, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi);
 }
 
 // Subset ops reuse the tile configuration the autotuner chose for the full per-view op (same tables,
@@ -2041,17 +2064,25 @@ static int g_num_sms() {
   return n;
 }
 
-// split-K partial sums of band_u: y[r][c] (+)= sum_kc part[kc * kc_rows + r][c] over the window, kc ascending
+// split-K partial sums of band_u: y[r][c] (+)= sum_kc part[kc * kc_rows + r][c] over the window, kc ascending;
+// float4 per thread (window columns, pitch and the buffers on 16-byte boundaries, checked by the caller)
 __global__ void sum_chunks_kernel(const float* __restrict__ part, float* __restrict__ y, long long pitch, int r0, int r1,
                                   int c0, int c1, int ksplit, int kc_rows, int accumulate) {
-  const int w = c1 - c0;
-  const long long n = (long long)(r1 - r0) * w;
+  const int w4 = (c1 - c0) >> 2;
+  const long long n = (long long)(r1 - r0) * w4;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int r = r0 + (int)(i / w), c = c0 + (int)(i % w);
-    float v = part[(long long)r * pitch + c];
-    for (int kc = 1; kc < ksplit; ++kc) v += part[((long long)kc * kc_rows + r) * pitch + c];
-    float* o = y + (long long)r * pitch + c;
-    *o = accumulate ? *o + v : v;
+    const int r = r0 + (int)(i / w4), c = c0 + 4 * (int)(i % w4);
+    float4 v = __ldg(reinterpret_cast<const float4*>(part + (long long)r * pitch + c));
+    for (int kc = 1; kc < ksplit; ++kc) {
+      const float4 p = __ldg(reinterpret_cast<const float4*>(part + ((long long)kc * kc_rows + r) * pitch + c));
+      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+    }
+    float4* o = reinterpret_cast<float4*>(y + (long long)r * pitch + c);
+    if (accumulate) {
+      const float4 q = *o;
+      v.x = q.x + v.x; v.y = q.y + v.y; v.z = q.z + v.z; v.w = q.w + v.w;
+    }
+    *o = v;
   }
 }
 
@@ -2180,7 +2211,9 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     int ksplit = 1;
     const int items0 = n_mt_l * (nt1 - nt0);
     const long long kc_rows = (long long)n_mt_all * 128;
-    if (part && !op.ft->u_mode && 2 * items0 <= g_num_sms() && !std::getenv("LFM_NO_SPLITK")) {
+    const float* ob = out + (long long)b0 * a.out_stride;
+    if (part && !op.ft->u_mode && 2 * items0 <= g_num_sms() && !std::getenv("LFM_NO_SPLITK") && a.out_pitch % 4 == 0 &&
+        op.n_os % 4 == 0 && ((uintptr_t)ob & 15) == 0 && ((uintptr_t)part & 15) == 0) {
       ksplit = std::min(4, g_num_sms() / std::max(1, items0));
       while (ksplit > 1 && (size_t)ksplit * kc_rows * a.out_pitch * 4 > part_bytes) --ksplit;
     }
@@ -2232,8 +2265,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     if (ksplit > 1) {
       const int sr0 = mt0 * 128, sr1 = std::min(op.n_ot, (mt0 + n_mt_l) * 128);
       const int sc0 = nt0 * 256, sc1 = std::min(op.n_os, nt1 * 256);
-      const long long n = (long long)(sr1 - sr0) * (sc1 - sc0);
-      sum_chunks_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, s>>>(
+      const long long n = (long long)(sr1 - sr0) * ((sc1 - sc0) / 4);
+      sum_chunks_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
           part, out + (long long)b0 * a.out_stride, a.out_pitch, sr0, sr1, sc0, sc1, ksplit, (int)kc_rows, accumulate);
       ++g_launches;
     }
@@ -2406,6 +2439,42 @@ __global__ void __launch_bounds__(256) shear_kernel(const float* __restrict__ in
   }
 }
 
+// y pass (axis 2, lines (x, z) along y, stride nx): like the z pass, a thread owns one line and walks YC
+// consecutive y with a sliding window of YC + TAPS - 1 loads (each input value loaded once); lanes take consecutive
+// x, so every load and store is a coalesced row.  Same ascending-tap FMA order as shear_kernel: bit-identical.
+template <int TAPS, int YC>
+__global__ void __launch_bounds__(256) shear_y_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                      const int32_t* __restrict__ mlo, const float* __restrict__ w,
+                                                      int nx, int ny, int nz, int accumulate) {
+  const int ix = blockIdx.x * 32 + threadIdx.x, iz = blockIdx.y * 8 + threadIdx.y, y0 = blockIdx.z * YC;
+  if (ix >= nx || iz >= nz) return;
+  const int line = ix + nx * iz;
+  const int m0 = __ldg(mlo + line);
+  float wk[TAPS];
+#pragma unroll
+  for (int k = 0; k < TAPS; k += 4) {
+    const float4 w4 = __ldg(reinterpret_cast<const float4*>(w + (size_t)line * TAPS + k));
+    wk[k] = w4.x; wk[k + 1] = w4.y; wk[k + 2] = w4.z; wk[k + 3] = w4.w;
+  }
+  const size_t base = (size_t)iz * nx * ny + ix;
+  float win[YC + TAPS - 1];
+#pragma unroll
+  for (int i = 0; i < YC + TAPS - 1; ++i) {
+    const int j = y0 + m0 + i;
+    win[i] = (j >= 0 && j < ny) ? __ldg(in + base + (size_t)j * nx) : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < YC; ++q) {
+    const int iy = y0 + q;
+    if (iy >= ny) break;
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < TAPS; ++k) acc = fmaf(wk[k], win[q + k], acc);
+    float* o = out + base + (size_t)iy * nx;
+    *o = accumulate ? *o + acc : acc;
+  }
+}
+
 // x pass (axis 1, the line runs along the contiguous axis, one shift m0 and one weight row per line): each thread
 // owns 4 consecutive x of one line, loads the aligned float4 window that covers them plus the taps
 // (ceil((TAPS + 6) / 4) LDG.128 instead of 4 TAPS scalar loads) and stores one float4.  Same FMA order as
@@ -2459,134 +2528,6 @@ __global__ void __launch_bounds__(256) shear_x4_kernel(const float* __restrict__
   }
 }
 
-// Fused in-plane rotation of a yaw pose (only the z and x shear passes active; both act inside the y-plane,
-// eqn,rot,decomp with D_y = 1): one CTA per y-plane holds the nz x nx plane in shared memory, applies the two
-// passes there and writes the plane once -- 8 B of HBM per voxel for the rotation instead of 8 B per pass, one
-// launch instead of two.  Forward (ORDER 0): E^x (E^z in); adjoint (ORDER 1): E^zT (E^xT in) with the transposed
-// tables.  Per output the taps are summed in the same ascending order with the same fp32 FMAs as shear_kernel /
-// shear_x4_kernel (out-of-range taps contribute exact zeros), so the result is bit-identical to the two-kernel path.
-constexpr int RZX_THREADS = 1024;
-template <int TZ, int TX, int ORDER>
-__global__ void __launch_bounds__(RZX_THREADS, 1) rot_zx_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                                const int32_t* __restrict__ mz, const float* __restrict__ wz,
-                                                                const int32_t* __restrict__ mx, const float* __restrict__ wx,
-                                                                int nx, int ny, int nz, int accumulate) {
-  // plane buffers [nz][nx + 1] (the pad makes a walk across z conflict-free); nx and nz divide RZX_THREADS
-  extern __shared__ float rzx[];
-  const int P = nx + 1;
-  float* A = rzx;                    // the input plane, later the result
-  float* B = rzx + (size_t)nz * P;   // after the first pass
-  const int iy = blockIdx.x, t = threadIdx.x;
-  const size_t plane = (size_t)nx * ny;
-  const int ne = nz * nx;
-  // loads issued 8 at a time before their shared-memory stores (a load followed at once by its store would
-  // wait out one DRAM latency per element)
-  for (int e0 = t; e0 < ne; e0 += 8 * RZX_THREADS) {
-    float v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
-      v[u] = e < ne ? __ldg(in + (size_t)z * plane + (size_t)iy * nx + x) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
-      if (e < ne) A[z * P + x] = v[u];
-    }
-  }
-  __syncthreads();
-  // z pass: a thread owns column x (line x + nx*iy) and a run of consecutive z; out(x, z) = sum_k wz[k] S[z+m+k][x]
-  auto zpass = [&](const float* S, float* D) {
-    const int x = t % nx, runs = RZX_THREADS / nx, run = (nz + runs - 1) / runs, z0 = (t / nx) * run;
-    const int line = x + nx * iy;
-    const int m0 = __ldg(mz + line);
-    float wk[TZ];
-#pragma unroll
-    for (int k = 0; k < TZ; ++k) wk[k] = __ldg(wz + (size_t)line * TZ + k);
-    for (int z = z0; z < min(nz, z0 + run); ++z) {
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < TZ; ++k) {
-        const int j = z + m0 + k;
-        acc = fmaf(wk[k], (j >= 0 && j < nz) ? S[j * P + x] : 0.f, acc);
-      }
-      D[z * P + x] = acc;
-    }
-  };
-  // x pass: a thread owns row z (line iy + ny*z) and a run of consecutive x; lanes take consecutive z (padded
-  // rows: distinct banks); out(x, z) = sum_k wx[k] S[z][x+m+k]
-  auto xpass = [&](const float* S, float* D) {
-    const int z = t % nz, runs = RZX_THREADS / nz, run = (nx + runs - 1) / runs, x0 = (t / nz) * run;
-    const int line = iy + ny * z;
-    const int m0 = __ldg(mx + line);
-    float wk[TX];
-#pragma unroll
-    for (int k = 0; k < TX; ++k) wk[k] = __ldg(wx + (size_t)line * TX + k);
-    for (int x = x0; x < min(nx, x0 + run); ++x) {
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < TX; ++k) {
-        const int j = x + m0 + k;
-        acc = fmaf(wk[k], (j >= 0 && j < nx) ? S[z * P + j] : 0.f, acc);
-      }
-      D[z * P + x] = acc;
-    }
-  };
-  if (ORDER == 0) { zpass(A, B); __syncthreads(); xpass(B, A); }
-  else { xpass(A, B); __syncthreads(); zpass(B, A); }
-  __syncthreads();
-  for (int e0 = t; e0 < ne; e0 += 8 * RZX_THREADS) {
-    float p[8];
-    if (accumulate) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
-        p[u] = e < ne ? out[(size_t)z * plane + (size_t)iy * nx + x] : 0.f;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * RZX_THREADS, z = e / nx, x = e - z * nx;
-      if (e < ne) {
-        const float r = A[z * P + x];
-        out[(size_t)z * plane + (size_t)iy * nx + x] = accumulate ? p[u] + r : r;
-      }
-    }
-  }
-}
-
-// Both passes of a yaw rotation in one launch when the plane fits in shared memory (LFM_ROT_FUSE=0 disables);
-// returns false (nothing launched) when the fused form does not apply.
-bool launch_rot_zx(const ShearPass& pz, const ShearPass& px, int dir, const float* in, float* out, int nx, int ny,
-                   int nz, int accumulate, void* stream, lfm_status& st, std::string& err) {
-  static const bool off = std::getenv("LFM_ROT_FUSE") && std::getenv("LFM_ROT_FUSE")[0] == '0';
-  const size_t smem = (size_t)2 * (nx + 1) * nz * 4;
-  if (off || !pz.active || !px.active || pz.axis != 0 || px.axis != 1 || RZX_THREADS % nx || RZX_THREADS % nz ||
-      smem > 200 * 1024 || pz.taps > 8 || px.taps > 8)
-    return false;
-  static bool attr[LFM_MAX_DEV][2][2][2];
-  const int dv = cur_dev(), iz_ = pz.taps == 8, ix_ = px.taps == 8;
-  cudaStream_t s = (cudaStream_t)stream;
-#define LFM_RZX(TZ_, TX_, O_)                                                                                        \
-  {                                                                                                                  \
-    if (!attr[dv][iz_][ix_][O_]) {                                                                                   \
-      cudaFuncSetAttribute(rot_zx_kernel<TZ_, TX_, O_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);    \
-      attr[dv][iz_][ix_][O_] = true;                                                                                 \
-    }                                                                                                                \
-    rot_zx_kernel<TZ_, TX_, O_><<<ny, RZX_THREADS, smem, s>>>(in, out, pz.d_mlo[dir], pz.d_w[dir], px.d_mlo[dir],    \
-                                                              px.d_w[dir], nx, ny, nz, accumulate);                  \
-  }
-  if (dir == 0) {
-    if (!iz_ && !ix_) LFM_RZX(4, 4, 0) else if (!iz_) LFM_RZX(4, 8, 0) else if (!ix_) LFM_RZX(8, 4, 0) else LFM_RZX(8, 8, 0)
-  } else {
-    if (!iz_ && !ix_) LFM_RZX(4, 4, 1) else if (!iz_) LFM_RZX(4, 8, 1) else if (!ix_) LFM_RZX(8, 4, 1) else LFM_RZX(8, 8, 1)
-  }
-#undef LFM_RZX
-  ++g_launches;
-  st = cuda_check(cudaGetLastError(), "rot_zx_kernel launch", err);
-  return true;
-}
-
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err) {
   // z chunk per thread: the z pass reads a sliding window of ZC + TAPS - 1 values per ZC outputs, so longer
@@ -2613,6 +2554,15 @@ lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* ou
 #undef LFM_SHX4
     ++g_launches;
     return cuda_check(cudaGetLastError(), "shear_x4_kernel launch", err);
+  }
+  if (sp.axis == 2 && !std::getenv("LFM_SH_Y_SCALAR")) {
+    dim3 gy((nx + 31) / 32, (nz + 7) / 8, (ny + 15) / 16), by(32, 8);
+    cudaStream_t sy = (cudaStream_t)stream;
+    if (sp.taps == 4) shear_y_kernel<4, 16><<<gy, by, 0, sy>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    else if (sp.taps == 8) shear_y_kernel<8, 16><<<gy, by, 0, sy>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    else shear_y_kernel<16, 16><<<gy, by, 0, sy>>>(in, out, sp.d_mlo[dir], sp.d_w[dir], nx, ny, nz, accumulate);
+    ++g_launches;
+    return cuda_check(cudaGetLastError(), "shear_y_kernel launch", err);
   }
   dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + zc - 1) / zc), blk(32, 8);
   cudaStream_t s = (cudaStream_t)stream;
@@ -2840,6 +2790,12 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
   const bool vx[3] = {ix > 0, true, ix < nx - 1}, vy[3] = {iy > 0, true, iy < ny - 1};
   double v = 0;
   if (ix < nx && iy < ny) {
+    // the chunk's grad values loaded together (read-modify-write: one latency for the chunk, not one per voxel)
+    float gin[R26_ZC];
+#pragma unroll
+    for (int q = 0; q < R26_ZC; ++q)
+      gin[q] = z0 + q < nz ? grad[(size_t)(z0 + q) * plane + (size_t)iy * nx + ix] : 0.f;
+#pragma unroll
     for (int q = 0; q < R26_ZC; ++q) {
       const int iz = z0 + q;
       if (iz >= nz) break;
@@ -2860,7 +2816,7 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
             if (COST) rs += ok ? (double)d * (double)d : 0.0;
           }
       const size_t i = (size_t)iz * plane + (size_t)iy * nx + ix;
-      grad[i] += beta * g + nu;
+      grad[i] = gin[q] + (beta * g + nu);
       if (COST) v += (double)nu * xj + 0.25 * (double)beta * rs;
     }
   }

@@ -8,8 +8,6 @@ namespace lfm {
 extern thread_local int g_launches;
 lfm_status launch_shear(const ShearPass& sp, int dir, const float* in, float* out, int nx, int ny, int nz,
                         int accumulate, void* stream, std::string& err);
-bool launch_rot_zx(const ShearPass& pz, const ShearPass& px, int dir, const float* in, float* out, int nx, int ny,
-                   int nz, int accumulate, void* stream, lfm_status& st, std::string& err);
 lfm_status k_copy_scale(const float* in, float* out, long long n, float scale, int acc, void* s, std::string& err);
 lfm_status k_fill(float* out, long long n, float v, void* s, std::string& err);
 lfm_status k_mul(const float* a, const float* b, float* out, long long n, void* s, std::string& err);
