@@ -25,6 +25,16 @@ Conventions (readings Z1-Z13):
 The plenoptic S3 operator per axis S_k = sum_mu B^{mu a}_k M_mu is formed literally
 (one transport per lenslet) -- the oracle does not use the adjoint symmetry; its
 adjoint is the literal transpose of every factor.
+
+Non-separable lenslet stages (NEXT-4; "hexagonal microlens configuration"; occluders rasterised onto the
+array grid, eqn,occlusion P:915-927; readings R12/R13 of DESIGN.md):
+* lens_layout 1 (hexagonal): lenslet row j (along t) has its lenslets shifted by +pitch_s/2 when j is odd, and odd
+  rows hold nl_s - 1 lenslets (every lenslet inside the array);
+* aperture 1 (circular): array cell (j_s, j_t) is open for lenslet mu iff its centre is strictly inside the disk of
+  diameter fill * pitch_s about the lenslet centre; aperture 0 keeps the square rule per axis.
+Then M_mu is a 2-D mask and the lenslet stage is evaluated literally lenslet by lenslet,
+  y = sum_k sum_mu (sqrt(V^mu)/V^mu) B^{d mu}_{k,t} (M_mu .* a_k) (B^{d mu}_{k,s})^T,
+each lenslet's transport still separable (the lens is); no term decomposition in the oracle.
 """
 import math
 
@@ -42,6 +52,7 @@ class CameraModel:
 
     def __init__(self, cam, dims, vox_r, dense=False):
         self.cam = cam
+        self.nonsep = False
         self.nx, self.ny, self.nz = dims
         self.vox_r = vox_r
         self.type = cam["type"]
@@ -85,6 +96,31 @@ class CameraModel:
                     masks.append(((ac >= c_mu - half) & (ac < c_mu + half)).astype(np.float64))
                 self.lenslet_planes.append(planes)
                 self.masks.append(masks)
+            # non-separable lenslet stage (hexagonal layout and/or circular apertures): one entry per lenslet with
+            # its centre, per-axis lenslet planes and a 2-D mask over the array grid [t][s]
+            self.layout = int(cam.get("lens_layout", 0))
+            self.aperture = int(cam.get("aperture", 0))
+            self.nonsep = self.layout != 0 or self.aperture != 0 or bool(cam.get("_force_2d", False))
+            if self.nonsep:
+                ac_s, ac_t = self.array_planes[0].centres(), self.array_planes[1].centres()
+                self.lenslets2d = []
+                for j in range(nl[1]):
+                    odd = self.layout == 1 and j % 2 == 1
+                    c_t = (j - (nl[1] - 1) * 0.5) * self.pitch[1]
+                    for i in range(nl[0] - (1 if odd else 0)):
+                        c_s = (i - (nl[0] - 1) * 0.5 + (0.5 if odd else 0.0)) * self.pitch[0]
+                        if self.aperture == 1:
+                            r = 0.5 * cam["fill"] * self.pitch[0]
+                            m = ((ac_s[None, :] - c_s) ** 2 + (ac_t[:, None] - c_t) ** 2) < r * r
+                        else:
+                            hs, ht = 0.5 * cam["fill"] * self.pitch[0], 0.5 * cam["fill"] * self.pitch[1]
+                            m = ((ac_s[None, :] >= c_s - hs) & (ac_s[None, :] < c_s + hs) &
+                                 (ac_t[:, None] >= c_t - ht) & (ac_t[:, None] < c_t + ht))
+                        pls = Plane(det_n[0], det_d[0], compose(translate(-cam["d_mu_m"]),
+                                                               compose(invert(lens(cam["f_mu"], c_s)), translate(-b))))
+                        plt = Plane(det_n[1], det_d[1], compose(translate(-cam["d_mu_m"]),
+                                                               compose(invert(lens(cam["f_mu"], c_t)), translate(-b))))
+                        self.lenslets2d.append((c_s, c_t, pls, plt, m.astype(np.float64)))
             dst = self.array_planes
             va = basis_volume(dst[0], self.d0[0]) * basis_volume(dst[1], self.d0[1])
             vmu = basis_volume(self.lenslet_planes[0][0], self.d0[0]) * \
@@ -94,8 +130,18 @@ class CameraModel:
         # S1: slice n -> array (plenoptic) or detector (single), per axis, per k_axis, per n
         self.S1 = [[[build(self.slice_planes[ax][n], dst[ax], self.sk[ax][k], self.d0[ax], self.basis)
                      for n in range(self.nz)] for k in range(len(self.sk[ax]))] for ax in range(2)]
+        # non-separable lenslet stage: per view and lenslet the two 1D transports (literal, no symmetry)
+        if self.type == PLENOPTIC and self.nonsep:
+            self.S3 = None
+            self.S3_2d = {}
+            for ks in range(len(self.sk[0])):
+                for kt in range(len(self.sk[1])):
+                    self.S3_2d[ks, kt] = [
+                        (build(self.array_planes[0], pls, self.sk[0][ks], self.d0[0], self.basis),
+                         build(self.array_planes[1], plt, self.sk[1][kt], self.d0[1], self.basis), m)
+                        for (_, _, pls, plt, m) in self.lenslets2d]
         # S3: array -> detector through every lenslet, masked: S_k = sum_mu B^{mu a}_k M_mu
-        if self.type == PLENOPTIC:
+        if self.type == PLENOPTIC and not self.nonsep:
             self.S3 = []
             for ax in range(2):
                 per_k = []
@@ -125,7 +171,10 @@ class CameraModel:
             for n in range(self.nz):
                 acc += self.S1[1][kt][n] @ (xr[n] @ self.S1[0][ks][n].T)
             acc *= self.scale_s1
-            if self.type == PLENOPTIC:
+            if self.type == PLENOPTIC and self.nonsep:
+                for Bs, Bt, m in self.S3_2d[ks, kt]:
+                    y += self.scale_s3 * (Bt @ ((m * acc) @ Bs.T))
+            elif self.type == PLENOPTIC:
                 y += self.scale_s3 * (self.S3[1][kt] @ (acc @ self.S3[0][ks].T))
             else:
                 y += acc
@@ -135,7 +184,12 @@ class CameraModel:
         y = np.asarray(y, np.float64).reshape(self.cam["n_t"], self.cam["n_s"])
         g = np.zeros((self.nz, self.ny, self.nx))
         for ks, kt in self._views(views):
-            if self.type == PLENOPTIC:
+            if self.type == PLENOPTIC and self.nonsep:
+                a = 0.0
+                for Bs, Bt, m in self.S3_2d[ks, kt]:
+                    a = a + m * (Bt.T @ (y @ Bs))
+                a = self.scale_s3 * a
+            elif self.type == PLENOPTIC:
                 a = self.scale_s3 * (self.S3[1][kt].T @ (y @ self.S3[0][ks]))
             else:
                 a = y
@@ -148,6 +202,8 @@ class CameraModel:
         """y[i_t, i_s] = sum_k sum_n (row i of the camera factors) x^r_n for each (i_t, i_s) in `pixels`:
         plenoptic y_i = c3 sum_k (S3t_kt[i_t] c1 S1t_kt,n) x^r_n (S3s_ks[i_s] S1s_ks,n)^T summed over n, the
         factored chain of forward() restricted to one detector pixel."""
+        if self.type == PLENOPTIC and self.nonsep:
+            raise NotImplementedError("forward_at: separable lenslet stages only")
         xr = np.asarray(xr, np.float64).reshape(self.nz, self.ny, self.nx)
         out = np.zeros(len(pixels))
         for p, (it, i_s) in enumerate(pixels):
@@ -168,6 +224,8 @@ class CameraModel:
     def adjoint_at(self, y, voxels):
         """(A^T y)[n, v_t, v_x] of the rotated frame for each (n, v_t, v_x) in `voxels`: the literal transposes
         of adjoint(), evaluated at single voxels from the per-view array fields a_k = c3 S3t_kt^T y S3s_ks."""
+        if self.type == PLENOPTIC and self.nonsep:
+            raise NotImplementedError("adjoint_at: separable lenslet stages only")
         y = np.asarray(y, np.float64).reshape(self.cam["n_t"], self.cam["n_s"])
         fields = {}
         for ks in range(self.ks):
@@ -204,8 +262,13 @@ class CameraModel:
         A = np.zeros((self.n_pix, self.nz * n_vox_slice))
         for ks in range(self.ks):
             for kt in range(self.kt):
-                S = self.scale_s3 * np.kron(d(self.S3[1][kt]), d(self.S3[0][ks])) \
-                    if self.type == PLENOPTIC else None
+                if self.type == PLENOPTIC and self.nonsep:
+                    S = self.scale_s3 * sum(np.kron(d(Bt), d(Bs)) * m.ravel()[None, :]
+                                            for Bs, Bt, m in self.S3_2d[ks, kt])
+                elif self.type == PLENOPTIC:
+                    S = self.scale_s3 * np.kron(d(self.S3[1][kt]), d(self.S3[0][ks]))
+                else:
+                    S = None
                 for n in range(self.nz):
                     B = self.scale_s1 * np.kron(d(self.S1[1][kt][n]), d(self.S1[0][ks][n]))
                     blk = B if S is None else S @ B

@@ -47,22 +47,28 @@ IDENTITY = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
 
 
 def plenoptic_camera(n_lens, px_per_lens, pitch_mm, k, n_a, pose=IDENTITY, basis=PILLBOX,
-                     f_main=F_MAIN, aperture=APERTURE, d_scene=D_SCENE, d_mu_m=D_MU_M, fill=1.0):
+                     f_main=F_MAIN, aperture=APERTURE, d_scene=D_SCENE, d_mu_m=D_MU_M, fill=1.0, layout=0,
+                     lens_aperture=0, rows=None, px_per_row=None):
+    """rows / px_per_row: lenslet rows along t and detector pixels per row (default: square, as along s);
+    layout 1 = hexagonal (odd rows shifted by half a pitch, one lenslet fewer), lens_aperture 1 = circular."""
     lens_pitch = px_per_lens * pitch_mm
     b = lens_pitch * d_mu_m / aperture
     image = 1.0 / (1.0 / f_main - 1.0 / d_scene)          # main-lens image of the volume centre (60 mm)
     f_mu = 1.0 / (1.0 / (d_mu_m - image) + 1.0 / b)       # lenslets image that plane onto the detector
+    rows = n_lens if rows is None else rows
+    px_per_row = px_per_lens if px_per_row is None else px_per_row
     return dict(type=PLENOPTIC, basis=basis, f_main=f_main, ap_s=aperture, ap_t=aperture, d_scene=d_scene,
                 k_s=k, k_t=k, d_det=0.0, d_mu_m=d_mu_m, d_d_mu=b, f_mu=f_mu, fill=fill,
-                nl_s=n_lens, nl_t=n_lens, n_a=n_a, n_s=n_lens * px_per_lens, n_t=n_lens * px_per_lens,
-                px_s=pitch_mm, px_t=pitch_mm, R=tuple(pose))
+                nl_s=n_lens, nl_t=rows, n_a=n_a, n_s=n_lens * px_per_lens, n_t=rows * px_per_row,
+                px_s=pitch_mm, px_t=pitch_mm, R=tuple(pose), lens_layout=layout, aperture=lens_aperture)
 
 
 def single_camera(n_px, pitch_mm, k, pose=IDENTITY, basis=PILLBOX, f_main=F_MAIN, aperture=APERTURE,
                   d_scene=D_SCENE, d_det=60.0):
     return dict(type=SINGLE, basis=basis, f_main=f_main, ap_s=aperture, ap_t=aperture, d_scene=d_scene,
                 k_s=k, k_t=k, d_det=d_det, d_mu_m=0.0, d_d_mu=0.0, f_mu=0.0, fill=0.0,
-                nl_s=0, nl_t=0, n_a=0, n_s=n_px, n_t=n_px, px_s=pitch_mm, px_t=pitch_mm, R=tuple(pose))
+                nl_s=0, nl_t=0, n_a=0, n_s=n_px, n_t=n_px, px_s=pitch_mm, px_t=pitch_mm, R=tuple(pose),
+                lens_layout=0, aperture=0)
 
 
 def volume(n, d):
@@ -101,6 +107,18 @@ def make_config(name):
         return dict(name=name, volume=volume(32, 0.4),
                     cameras=[plenoptic_camera(8, 8, 0.04, 4, 4),
                              plenoptic_camera(8, 8, 0.04, 4, 4, pose=pose_yaw(30.0))])
+    if name == "tiny_hex":  # NEXT-4: hexagonal lenslet layout with circular lenslet apertures;
+        # rows of 7 px against 8 px columns (row pitch 0.875 of the column pitch, ~ sqrt(3)/2)
+        return dict(name=name, volume=volume(16, 0.4),
+                    cameras=[plenoptic_camera(4, 8, 0.04, 2, 4, layout=1, lens_aperture=1, rows=5, px_per_row=7)])
+    if name == "tiny_disk":  # rectangular lenslet grid with circular apertures (non-separable mask only)
+        return dict(name=name, volume=volume(16, 0.4),
+                    cameras=[plenoptic_camera(4, 8, 0.04, 2, 4, lens_aperture=1, fill=0.9)])
+    if name == "small_hex":  # 32^3 two-camera, hexagonal + circular, several tiles and a rotated camera
+        return dict(name=name, volume=volume(32, 0.4),
+                    cameras=[plenoptic_camera(8, 8, 0.04, 4, 4, layout=1, lens_aperture=1, rows=9, px_per_row=7),
+                             plenoptic_camera(8, 8, 0.04, 4, 4, layout=1, lens_aperture=1, rows=9, px_per_row=7,
+                                              pose=pose_yaw(30.0))])
     if name == "odd_ny":  # nz % 64 == 0 (slice-pair tcgen05 tiles) with an odd number of voxel rows, ragged edges
         return dict(name=name, volume=dict(nx=32, ny=33, nz=64, dx=0.4, dy=0.4, dz=0.4),
                     cameras=[plenoptic_camera(16, 8, 0.04, 2, 2),
@@ -122,4 +140,5 @@ def make_config(name):
 
 
 CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "odd_ny",
+           "tiny_hex", "tiny_disk", "small_hex",
            "64^3 single", "128^3 two-camera", "256^3 four-camera"]
