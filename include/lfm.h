@@ -74,6 +74,12 @@ typedef struct {
   int n_s, n_t;             /* detector pixels */
   double px_s, px_t;        /* detector pitch */
   double R[9];              /* pose Theta, row-major, p = Theta p_r, residual < 45 deg */
+  int lens_layout;          /* plenoptic: 0 rectangular lenslet grid; 1 hexagonal: odd lenslet rows (along t)
+                               shifted by pitch_s/2 along s and holding nl_s - 1 lenslets (reading R12) */
+  int aperture;             /* plenoptic: 0 square lenslet apertures (side fill*pitch per axis); 1 circular: array
+                               cells whose centres lie strictly inside the disk of diameter fill*pitch_s (the
+                               occluder rasterised onto the array grid, eqn,occlusion P:915-927; reading R13).
+                               Overlapping apertures give LFM_E_INVALID. */
 } lfm_camera;
 
 typedef struct {
@@ -119,6 +125,9 @@ typedef struct {
                                path's s passes: non-zeros of C_s,n summed over slices x ny voxel rows) */
   int subset_collapsed;     /* how many of the plan's view subsets run on the collapsed path (tensor-product
                                subsets, lfm_A_forward_subset); the others use the per-view path */
+  int s3_terms;             /* separable terms T of the lenslet stage (1 for a rectangular grid with square
+                               apertures; hexagonal layouts / circular apertures: S_k = sum_tau S^tau_ks (x) S^tau_kt,
+                               reading R12).  S3 table ids index k*T + tau; the collapsed path sums T terms. */
 } lfm_info;
 
 /* Table ids for lfm_plan_export_table (bit-exact comparison with the oracle in tests).

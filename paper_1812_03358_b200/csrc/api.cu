@@ -183,7 +183,15 @@ struct Win {
 // the collapsed path runs on the tcgen05 kernels end to end (band_v s passes, band_u t passes), the form whose
 // kernels restrict themselves to a column window
 static bool tc_two_pass(const CameraPlan& cp) {
-  return cp.fwd_split && cp.fwd_t == 3 && cp.adj_t == 3 && cp.fwd_c2.kind == 8 && cp.adj_c1.kind == 8;
+  bool ok = cp.fwd_split && cp.fwd_t == 3 && cp.adj_t == 3 && cp.fwd_c2.kind == 8 && cp.adj_c1.kind == 8;
+  for (const Component& cm : cp.comps) ok = ok && cm.fwd_c2.kind == 8 && cm.adj_c1.kind == 8 && cm.vf.d_img && cm.va.d_img;
+  return ok;
+}
+
+// The collapsed path of a non-separable lenslet stage (T > 1 terms) exists only as the tcgen05 two-pass form (a
+// sum over terms of s pass + t pass); without it such a camera's collapsed requests run on the per-view path.
+static int eff_path(const CameraPlan& cp, int path) {
+  return (path == LFM_PATH_COLLAPSED && !cp.comps.empty() && !tc_two_pass(cp)) ? LFM_PATH_PER_VIEW : path;
 }
 
 // y on the window rows [r0, r1) x columns [c0, c1) of A_c x.  Other entries of partially covered tiles may be
@@ -192,9 +200,22 @@ static bool tc_two_pass(const CameraPlan& cp) {
 lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y, const Ws& w, void* stream,
                         Win win = Win()) {
   const int r0 = win.r0, r1 = win.r1;
+  path = eff_path(cp, path);
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
   const bool plen = cp.info.type == LFM_PLENOPTIC;
+  if (path == LFM_PATH_COLLAPSED && !cp.comps.empty()) {
+    // non-separable lenslet stage: y = sum over terms of (band_v s pass, band_u t pass), terms >= 1 accumulated
+    std::string err;
+    lfm_status st = k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err, win.c0, win.c1);
+    if (st != LFM_OK) return fail(st, err);
+    TRY(sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z));
+    for (const Component& cm : cp.comps) {
+      if ((st = k_vpass_fwd(cp, cm.vf, xr, w.z, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
+      TRY(sep(cm.fwd_c2, w.z, y, 0, 1, 1, stream, r0, r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z));
+    }
+    return LFM_OK;
+  }
   if (path == LFM_PATH_COLLAPSED) {
     if (cp.fwd_split) {
       if (cp.fwd_t == 2 || cp.fwd_t == 3) {
@@ -239,6 +260,7 @@ __global__ void mask_window_kernel(const float* __restrict__ y, float* __restric
 lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x, int accumulate, const Ws& w,
                         void* stream, Win win = Win()) {
   int r0 = win.r0, r1 = win.r1;
+  path = eff_path(cp, path);
   const bool rot = cp.info.rot_passes != 0;
   float* target = rot ? w.r0 : x;
   int acc = rot ? 0 : accumulate;
@@ -262,6 +284,11 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
       lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err, win.c0, win.c1)
                                     : k_spass_adj(cp, w.z, target, acc, stream, err);
       if (st != LFM_OK) return fail(st, err);
+      // non-separable lenslet stage: the other terms' t and s passes, accumulated (tcgen05 path only, eff_path)
+      for (const Component& cm : cp.comps) {
+        TRY(sep(cm.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1, win.c0, win.c1));
+        if ((st = k_vpass_adj(cp, cm.va, w.z, target, 1, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
+      }
     } else if (cp.adj_t) {
       // Z_n -> ZT_n = [j][vt] per slice, then the s pass as a t pass with transposed output into x_n
       const int ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;

@@ -352,6 +352,16 @@ lfm_status upload_camera(CameraPlan& cp, std::string& err) {
   build_vtabs(cp.cf[0], cp.ca[0], cp.vf, cp.va);
   for (VTab* T : {&cp.vf, &cp.va})
     if ((st = upload_vtab(*T, bytes, err)) != LFM_OK) return st;
+  // terms >= 1 of a non-separable lenslet stage: t families (tcgen05 images), their ops, band_v tables
+  for (Component& cm : cp.comps) {
+    for (BandFamily* f : {&cm.ca1n, &cm.cf1n})
+      if ((st = upload_family(*f, bytes, err)) != LFM_OK) return st;
+    for (SepOp* op : {&cm.fwd_c2, &cm.adj_c1})
+      if ((st = upload_sep(*op, bytes, err)) != LFM_OK) return st;
+    build_vtabs(cm.cf[0], cm.ca[0], cm.vf, cm.va);
+    for (VTab* T : {&cm.vf, &cm.va})
+      if ((st = upload_vtab(*T, bytes, err)) != LFM_OK) return st;
+  }
   cp.info.table_bytes = bytes;
   return LFM_OK;
 }
@@ -607,8 +617,14 @@ void free_camera(CameraPlan& cp) {
     free_vtab(vo.vf);
     free_vtab(vo.va);
   }
+  for (Component& cm : cp.comps) {
+    free_vtab(cm.vf);
+    free_vtab(cm.va);
+  }
 
   std::vector<BandFamily*> fams = {&cp.id_s, &cp.id_t, &cp.id_vt, &cp.ca1n, &cp.cf1n};
+  for (Component& cm : cp.comps)
+    for (BandFamily* f : {&cm.ca1n, &cm.cf1n}) fams.push_back(f);
   for (int ax = 0; ax < 2; ++ax)
     for (BandFamily* f : {&cp.s1f[ax], &cp.s1a[ax], &cp.s3f[ax], &cp.s3a[ax], &cp.cf[ax], &cp.ca[ax]})
       fams.push_back(f);
@@ -630,6 +646,8 @@ void free_camera(CameraPlan& cp) {
   std::vector<SepOp*> all(std::begin(ops), std::end(ops));
   for (ViewOps& vo : cp.subs)
     for (SepOp* op : {&vo.fwd_s1, &vo.fwd_s3, &vo.adj_s3, &vo.adj_s1}) all.push_back(op);
+  for (Component& cm : cp.comps)
+    for (SepOp* op : {&cm.fwd_c2, &cm.adj_c1}) all.push_back(op);
   for (SepOp* op : all) {
     dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t); dfree(op->d_chunks);
     dfree(op->d_chunk_off); dfree(op->d_chunk_w);
@@ -3016,7 +3034,12 @@ static void finish_choice(CameraPlan& cp, bool dbg, float t_x, float t_z) {
 // and band_v for both s passes -- the choice the timed search makes on B200 at 64^3-256^3.
 // The other ops keep the cost model's tiles.  LFM_FORCE_<op> still wins.
 static lfm_status tc_defaults(CameraPlan& cp, std::string& err) {
-  for (auto pr : {std::make_pair(&cp.fwd_c2, "fwd_c2"), std::make_pair(&cp.adj_c1, "adj_c1")}) {
+  std::vector<std::pair<SepOp*, const char*>> ops = {{&cp.fwd_c2, "fwd_c2"}, {&cp.adj_c1, "adj_c1"}};
+  for (Component& cm : cp.comps) {
+    ops.push_back({&cm.fwd_c2, "fwd_c2"});
+    ops.push_back({&cm.adj_c1, "adj_c1"});
+  }
+  for (auto pr : ops) {
     SepOp& op = *pr.first;
     if (!op.fs || std::getenv((std::string("LFM_FORCE_") + pr.second).c_str())) continue;
     const long long sp = op.src_pitch ? op.src_pitch : op.n_is;
@@ -3038,7 +3061,7 @@ static lfm_status tc_defaults(CameraPlan& cp, std::string& err) {
 
 lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
   const char* env = std::getenv("LFM_AUTOTUNE");
-  if (!env || env[0] != '1') {
+  if (!env || env[0] != '1' || !cp.comps.empty()) {  // non-separable lenslet stages: the tcgen05 defaults
     lfm_status st = tc_defaults(cp, err);
     finish_choice(cp, std::getenv("LFM_DEBUG") != nullptr, -1.f, -1.f);
     return st;

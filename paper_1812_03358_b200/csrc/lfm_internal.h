@@ -180,6 +180,14 @@ struct ViewOps {
   VTab vf, va;           // their band_v tables
 };
 
+// Term tau >= 1 of a non-separable lenslet stage (hexagonal layout / circular apertures, reading R12): its collapsed
+// composites, the slice-interleaved t families with their tcgen05 images, the band_v tables and the two t-pass ops.
+struct Component {
+  BandFamily cf[2], ca[2], ca1n, cf1n;
+  VTab vf, va;
+  SepOp fwd_c2, adj_c1;
+};
+
 struct CameraPlan {
   lfm_camera cam;
   lfm_info info;
@@ -206,6 +214,8 @@ struct CameraPlan {
   using VTab = lfm::VTab;
   VTab vf, va;
   size_t ws_rot = 0, ws_fields = 0, ws_z = 0;
+  int n_terms = 1;                        // separable terms of the lenslet stage (1: separable geometry)
+  std::vector<Component> comps;           // terms 1 .. n_terms - 1
 };
 
 }  // namespace lfm

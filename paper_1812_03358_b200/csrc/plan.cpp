@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "lfm_internal.h"
@@ -954,7 +955,7 @@ bool sep_choose_tile(SepOp& op) {
 // The band of a composite row is the union of the S1 bands its non-zero S3 entries reach (structural zeros
 // between two lenslets' cells are skipped).
 static void build_composite(const CameraPlan& cp, int ax, const std::vector<char>& kmask, double scale, int nz,
-                            int nrow, int nv, bool plen, BandFamily& cf, BandFamily& ca) {
+                            int nrow, int nv, bool plen, BandFamily& cf, BandFamily& ca, int tau) {
   const BandFamily& f1 = cp.s1f[ax];
   const int Kax = (int)kmask.size();
   const int keep_f = cf.want_mseg, keep_a = ca.want_mseg;
@@ -989,7 +990,7 @@ static void build_composite(const CameraPlan& cp, int ax, const std::vector<char
         };
         if (plen) {
           const BandFamily& f3 = cp.s3f[ax];
-          size_t i3 = (size_t)k * f3.n_rows + i;
+          size_t i3 = (size_t)(k * cp.n_terms + tau) * f3.n_rows + i;
           for (int q = 0; q < f3.len[i3]; ++q) {
             double w3 = f3.w64[i3 * f3.taps + q];
             if (w3 == 0.0) continue;  // gap between two lenslets' cells (structural zero)
@@ -1139,33 +1140,134 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
 
   Plane dst[2];
   double V_dst[2], V_mu[2] = {0, 0};
-  std::vector<Plane> lenslets[2];
-  std::vector<std::pair<int, int>> mask_range[2];  // open array cells per lenslet [lo, hi]
   double pitch[2] = {0, 0};
   for (int ax = 0; ax < 2; ++ax) {
     if (plen) {
       pitch[ax] = ndet[ax] * pdet[ax] / nl[ax];
       dst[ax] = Plane{nl[ax] * cam.n_a, pitch[ax] / cam.n_a, translate(-cam.d_mu_m), 0.0};
-      Affine inv;
-      for (int mu = 0; mu < nl[ax]; ++mu) {
-        double c_mu = ((double)mu - (nl[ax] - 1) * 0.5) * pitch[ax];
-        if (!invert(lens(cam.f_mu, c_mu), inv)) { err = "singular lenslet block"; return LFM_E_SINGULAR; }
-        Affine X0 = compose(translate(-cam.d_mu_m), compose(inv, translate(-cam.d_d_mu)));
-        lenslets[ax].push_back(Plane{ndet[ax], pdet[ax], X0, 0.0});
-        double half = 0.5 * cam.fill * pitch[ax];
-        int lo = 1 << 30, hi = -1;
-        for (int j = 0; j < dst[ax].n; ++j) {
-          double c = centre(dst[ax], j);
-          if (c >= c_mu - half && c < c_mu + half) { lo = std::min(lo, j); hi = std::max(hi, j); }
-        }
-        mask_range[ax].push_back({lo, hi});
-      }
-      V_mu[ax] = basis_volume(lenslets[ax][0], d0[ax]);
     } else {
       dst[ax] = Plane{ndet[ax], pdet[ax], translate(-cam.d_det), 0.0};
     }
     V_dst[ax] = basis_volume(dst[ax], d0[ax]);
   }
+  // ---- lenslet stage (plenoptic) as a sum of T separable terms (readings Z9/Z10, R12, R13):
+  //   S_k = sum_mu c3 B^{d mu}_k M_mu = sum_tau c3 S^tau_{k,s} (x) S^tau_{k,t},
+  // term tau = per axis a list of items (lenslet plane along the axis, open array cells [lo, hi] along it).
+  // Rectangular grid + square apertures: one term, per axis every lenslet with its open interval.  Hexagonal layout
+  // (odd lenslet rows shifted by pitch_s / 2, one lenslet fewer) and/or circular apertures (cells whose centres lie
+  // strictly inside the disk of diameter fill * pitch_s): each (lenslet row j, array row j_t) pair contributes the
+  // row's open s-cells of row j's lenslets; pairs with the same parity of j and the same s-cells form one term
+  // (its t items: the rows j_t, each through its own lenslet row's plane).
+  struct Item { int plane, lo, hi; };
+  std::vector<Plane> lplanes[2];
+  std::vector<std::vector<Item>> terms[2];
+  int T = 1;
+  if (plen) {
+    if ((cam.lens_layout != 0 && cam.lens_layout != 1) || (cam.aperture != 0 && cam.aperture != 1)) {
+      err = "lens_layout and aperture must be 0 or 1";
+      return LFM_E_INVALID;
+    }
+    if (cam.lens_layout == 1 && cam.nl_s < 2) { err = "a hexagonal lenslet layout needs nl_s >= 2"; return LFM_E_INVALID; }
+    std::vector<double> pl_c[2];  // centre of each plane along each axis
+    auto plane_of = [&](int ax, double c, int& idx) -> lfm_status {
+      for (size_t q = 0; q < pl_c[ax].size(); ++q)
+        if (pl_c[ax][q] == c) { idx = (int)q; return LFM_OK; }
+      Affine inv;
+      if (!invert(lens(cam.f_mu, c), inv)) { err = "singular lenslet block"; return LFM_E_SINGULAR; }
+      Affine X0 = compose(translate(-cam.d_mu_m), compose(inv, translate(-cam.d_d_mu)));
+      lplanes[ax].push_back(Plane{ndet[ax], pdet[ax], X0, 0.0});
+      pl_c[ax].push_back(c);
+      idx = (int)pl_c[ax].size() - 1;
+      return LFM_OK;
+    };
+    const bool sep_geom = cam.lens_layout == 0 && cam.aperture == 0;
+    if (sep_geom) {
+      for (int ax = 0; ax < 2; ++ax) {
+        terms[ax].assign(1, {});
+        for (int mu = 0; mu < nl[ax]; ++mu) {
+          double c_mu = ((double)mu - (nl[ax] - 1) * 0.5) * pitch[ax];
+          int pi;
+          if ((st = plane_of(ax, c_mu, pi)) != LFM_OK) return st;
+          double half = 0.5 * cam.fill * pitch[ax];
+          int lo = 1 << 30, hi = -1;
+          for (int j = 0; j < dst[ax].n; ++j) {
+            double c = centre(dst[ax], j);
+            if (c >= c_mu - half && c < c_mu + half) { lo = std::min(lo, j); hi = std::max(hi, j); }
+          }
+          if (hi >= lo) terms[ax][0].push_back({pi, lo, hi});
+        }
+      }
+    } else {
+      const int nas = dst[0].n, nat = dst[1].n;
+      std::vector<int> owners((size_t)nas * nat, 0);
+      std::map<std::vector<int>, int> key_to_term;
+      for (int j = 0; j < nl[1]; ++j) {
+        const bool odd = cam.lens_layout == 1 && (j & 1);
+        const double c_t = ((double)j - (nl[1] - 1) * 0.5) * pitch[1];
+        int pt;
+        if ((st = plane_of(1, c_t, pt)) != LFM_OK) return st;
+        // per array row: the open s-interval of each lenslet of this lenslet row
+        std::vector<std::vector<int>> row_key(nat);   // [parity, plane, lo, hi, plane, lo, hi, ...]
+        for (int i = 0; i < nl[0] - (odd ? 1 : 0); ++i) {
+          const double c_s = ((double)i - (nl[0] - 1) * 0.5 + (odd ? 0.5 : 0.0)) * pitch[0];
+          int ps;
+          if ((st = plane_of(0, c_s, ps)) != LFM_OK) return st;
+          for (int jt = 0; jt < nat; ++jt) {
+            const double tt = centre(dst[1], jt);
+            int lo = 1 << 30, hi = -1;
+            for (int js = 0; js < nas; ++js) {
+              const double ss = centre(dst[0], js);
+              bool open;
+              if (cam.aperture == 1) {
+                const double r = 0.5 * cam.fill * pitch[0];
+                open = (ss - c_s) * (ss - c_s) + (tt - c_t) * (tt - c_t) < r * r;
+              } else {
+                const double hs = 0.5 * cam.fill * pitch[0], ht = 0.5 * cam.fill * pitch[1];
+                open = ss >= c_s - hs && ss < c_s + hs && tt >= c_t - ht && tt < c_t + ht;
+              }
+              if (open) {
+                lo = std::min(lo, js);
+                hi = std::max(hi, js);
+                ++owners[(size_t)jt * nas + js];
+              }
+            }
+            if (hi < 0) continue;
+            if (row_key[jt].empty()) row_key[jt].push_back(odd ? 1 : 0);
+            row_key[jt].insert(row_key[jt].end(), {ps, lo, hi});
+          }
+        }
+        for (int jt = 0; jt < nat; ++jt) {
+          if (row_key[jt].empty()) continue;
+          auto it = key_to_term.find(row_key[jt]);
+          int tau;
+          if (it == key_to_term.end()) {
+            tau = (int)terms[0].size();
+            key_to_term[row_key[jt]] = tau;
+            std::vector<Item> sitems;
+            for (size_t q = 1; q + 2 < row_key[jt].size(); q += 3)
+              sitems.push_back({row_key[jt][q], row_key[jt][q + 1], row_key[jt][q + 2]});
+            terms[0].push_back(sitems);
+            terms[1].push_back({});
+          } else {
+            tau = it->second;
+          }
+          terms[1][tau].push_back({pt, jt, jt});
+        }
+      }
+      for (int v : owners)
+        if (v > 1) { err = "lenslet apertures overlap on the array grid (reduce fill)"; return LFM_E_INVALID; }
+      for (auto& tl : terms[1]) {   // within a term every array row has one lenslet row
+        std::sort(tl.begin(), tl.end(), [](const Item& a, const Item& b) { return a.lo < b.lo; });
+        for (size_t q = 1; q < tl.size(); ++q)
+          if (tl[q].lo == tl[q - 1].lo) { err = "lenslet rows share an array row within one term"; return LFM_E_INVALID; }
+      }
+      if (terms[0].empty()) { terms[0].assign(1, {}); terms[1].assign(1, {}); }
+    }
+    T = (int)terms[0].size();
+    for (int ax = 0; ax < 2; ++ax) V_mu[ax] = basis_volume(lplanes[ax][0], d0[ax]);
+  }
+  cp.n_terms = T;
+  info.s3_terms = T;
   info.n_as = plen ? dst[0].n : 0;
   info.n_at = plen ? dst[1].n : 0;
   const double Vdst = V_dst[0] * V_dst[1];
@@ -1196,70 +1298,65 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     bf.finish();
     ba.finish();
   }
-  // ---- S3 families (plenoptic): array -> detector through every lenslet, masked (fwd),
-  //      and detector -> array through the lenslet owning each cell (adj)
+  // ---- S3 families (plenoptic), table = k*T + tau: array -> detector through the term's items, masked (fwd),
+  //      and detector -> array through the item owning each cell (adj)
   if (plen) {
     for (int ax = 0; ax < 2; ++ax) {
-      family_init(cp.s3f[ax], K[ax], ndet[ax], dst[ax].n);
-      family_init(cp.s3a[ax], K[ax], dst[ax].n, ndet[ax]);
+      family_init(cp.s3f[ax], K[ax] * T, ndet[ax], dst[ax].n);
+      family_init(cp.s3a[ax], K[ax] * T, dst[ax].n, ndet[ax]);
       FamilyBuilder bf(cp.s3f[ax]), ba(cp.s3a[ax]);
-      bf.tabs.resize(K[ax]);
-      ba.tabs.resize(K[ax]);
-      // owner lenslet of every array cell
-      std::vector<int> owner(dst[ax].n, -1);
-      for (int mu = 0; mu < nl[ax]; ++mu)
-        for (int j = mask_range[ax][mu].first; j <= mask_range[ax][mu].second; ++j) owner[j] = mu;
+      bf.tabs.resize(K[ax] * T);
+      ba.tabs.resize(K[ax] * T);
       for (int k = 0; k < K[ax]; ++k) {
         double sk = ((double)k - (K[ax] - 1) * 0.5) * d0[ax];
-        // forward: union over lenslets of band_mu(i) cap open cells of mu
-        std::vector<int> lo(ndet[ax], 1 << 30), hi(ndet[ax], -1);
-        std::vector<std::vector<std::pair<int, double>>> acc(ndet[ax]);
-        for (int mu = 0; mu < nl[ax]; ++mu) {
-          int mlo = mask_range[ax][mu].first, mhi = mask_range[ax][mu].second;
-          if (mhi < mlo) continue;
-          Kernel1D kk;
-          st = make_kernel(dst[ax], lenslets[ax][mu], sk, d0[ax], cam.basis, kk, err);
-          if (st != LFM_OK) return st;
-          for (int i = 0; i < ndet[ax]; ++i) {
-            double c;
-            int blo, bhi;
-            row_band(dst[ax], lenslets[ax][mu], kk, i, c, blo, bhi);
-            blo = std::max(blo, mlo);
-            bhi = std::min(bhi, mhi);
-            if (bhi < blo) continue;
-            for (int j = blo; j <= bhi; ++j) acc[i].push_back({j, entry(dst[ax], kk, c, j)});
-            lo[i] = std::min(lo[i], blo);
-            hi[i] = std::max(hi[i], bhi);
+        for (int tau = 0; tau < T; ++tau) {
+          const std::vector<Item>& items = terms[ax][tau];
+          // forward: union over items of band_mu(i) cap the item's open cells
+          std::vector<int> lo(ndet[ax], 1 << 30), hi(ndet[ax], -1);
+          std::vector<std::vector<std::pair<int, double>>> acc(ndet[ax]);
+          for (const Item& it : items) {
+            Kernel1D kk;
+            st = make_kernel(dst[ax], lplanes[ax][it.plane], sk, d0[ax], cam.basis, kk, err);
+            if (st != LFM_OK) return st;
+            for (int i = 0; i < ndet[ax]; ++i) {
+              double c;
+              int blo, bhi;
+              row_band(dst[ax], lplanes[ax][it.plane], kk, i, c, blo, bhi);
+              blo = std::max(blo, it.lo);
+              bhi = std::min(bhi, it.hi);
+              if (bhi < blo) continue;
+              for (int j = blo; j <= bhi; ++j) acc[i].push_back({j, entry(dst[ax], kk, c, j)});
+              lo[i] = std::min(lo[i], blo);
+              hi[i] = std::max(hi[i], bhi);
+            }
           }
-        }
-        auto& rows = bf.tabs[k];
-        rows.assign(ndet[ax], Row());
-        for (int i = 0; i < ndet[ax]; ++i) {
-          if (hi[i] < 0) continue;
-          rows[i].lo = lo[i];
-          rows[i].len = hi[i] - lo[i] + 1;
-          rows[i].w.assign(rows[i].len, 0.0);
-          for (auto& e : acc[i]) rows[i].w[e.first - lo[i]] += e.second;
-        }
-        // adjoint: row j (array cell) = B^{a mu(j)}[j, :] (transport detector(mu) -> array)
-        auto& arows = ba.tabs[k];
-        arows.assign(dst[ax].n, Row());
-        for (int mu = 0; mu < nl[ax]; ++mu) {
-          int mlo = mask_range[ax][mu].first, mhi = mask_range[ax][mu].second;
-          if (mhi < mlo) continue;
-          Kernel1D kk;
-          st = make_kernel(lenslets[ax][mu], dst[ax], sk, d0[ax], cam.basis, kk, err);
-          if (st != LFM_OK) return st;
-          for (int j = mlo; j <= mhi; ++j) {
-            double c;
-            int blo, bhi;
-            row_band(lenslets[ax][mu], dst[ax], kk, j, c, blo, bhi);
-            if (bhi < blo) continue;
-            Row& r = arows[j];
-            r.lo = blo;
-            r.len = bhi - blo + 1;
-            r.w.resize(r.len);
-            for (int i = blo; i <= bhi; ++i) r.w[i - blo] = entry(lenslets[ax][mu], kk, c, i);
+          auto& rows = bf.tabs[k * T + tau];
+          rows.assign(ndet[ax], Row());
+          for (int i = 0; i < ndet[ax]; ++i) {
+            if (hi[i] < 0) continue;
+            rows[i].lo = lo[i];
+            rows[i].len = hi[i] - lo[i] + 1;
+            rows[i].w.assign(rows[i].len, 0.0);
+            for (auto& e : acc[i]) rows[i].w[e.first - lo[i]] += e.second;
+          }
+          // adjoint: row j (array cell) = B^{a mu(j)}[j, :] (transport detector(mu) -> array)
+          auto& arows = ba.tabs[k * T + tau];
+          arows.assign(dst[ax].n, Row());
+          for (const Item& it : items) {
+            Kernel1D kk;
+            st = make_kernel(lplanes[ax][it.plane], dst[ax], sk, d0[ax], cam.basis, kk, err);
+            if (st != LFM_OK) return st;
+            for (int j = it.lo; j <= it.hi; ++j) {
+              double c;
+              int blo, bhi;
+              row_band(lplanes[ax][it.plane], dst[ax], kk, j, c, blo, bhi);
+              if (bhi < blo) continue;
+              Row& r = arows[j];
+              r.lo = blo;
+              r.len = bhi - blo + 1;
+              r.w.resize(r.len);
+              for (int i = blo; i <= bhi; ++i) r.w[i - blo] = entry(lplanes[ax][it.plane], kk, c, i);
+            }
           }
         }
       }
@@ -1267,11 +1364,16 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
       ba.finish();
     }
   }
-  // ---- collapsed composite per slice: C_n = sum_k S_k B_{k,n} (plenoptic) or sum_k B_{k,n} (single)
+  // ---- collapsed composite per slice and term: C^tau_n = sum_k S^tau_k B_{k,n} (plenoptic) or sum_k B_{k,n} (single);
+  //      term 0 in the camera's own families, terms >= 1 in cp.comps
+  cp.comps.assign(T - 1, Component());
   for (int ax = 0; ax < 2; ++ax) {
     // s-axis composites also serve as t families of the transposed two-pass path (MSEG segments)
     cp.cf[ax].want_mseg = cp.ca[ax].want_mseg = ax == 0;
-    build_composite(cp, ax, std::vector<char>(K[ax], 1), 1.0, nz, ndet[ax], nsrc[ax], plen, cp.cf[ax], cp.ca[ax]);
+    build_composite(cp, ax, std::vector<char>(K[ax], 1), 1.0, nz, ndet[ax], nsrc[ax], plen, cp.cf[ax], cp.ca[ax], 0);
+    for (int tau = 1; tau < T; ++tau)
+      build_composite(cp, ax, std::vector<char>(K[ax], 1), 1.0, nz, ndet[ax], nsrc[ax], plen, cp.comps[tau - 1].cf[ax],
+                      cp.comps[tau - 1].ca[ax], tau);
   }
   info.taps_s1 = std::max(cp.s1f[0].ell, cp.s1f[1].gmax);
   info.taps_s3 = plen ? std::max(cp.s3f[0].ell, cp.s3f[1].gmax) : 0;
@@ -1291,16 +1393,18 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
         for (int n = 0; n < nz; ++n) sep_add(cp.fwd_s1, n * nslice, tab(ks, n), tab(kt, n), 1.f);
         sep_close_output(cp.fwd_s1);
       }
-    // forward S3: y = c3 * sum_k S_k a_k
+    // forward S3: y = c3 * sum_k sum_tau (S^tau_ks (x) S^tau_kt) a_k
     sep_init(cp.fwd_s3, &cp.s3f[0], &cp.s3f[1], dst[0].n, dst[1].n, 1, (float)c3);
     for (int kt = 0; kt < K[1]; ++kt)
-      for (int ks = 0; ks < K[0]; ++ks) sep_add(cp.fwd_s3, (long long)(kt * K[0] + ks) * nfield, ks, kt, 1.f);
+      for (int ks = 0; ks < K[0]; ++ks)
+        for (int tau = 0; tau < T; ++tau)
+          sep_add(cp.fwd_s3, (long long)(kt * K[0] + ks) * nfield, ks * T + tau, kt * T + tau, 1.f);
     sep_close_output(cp.fwd_s3);
     // adjoint S3: field k = c3 * S_k^T r  (evaluated with the detector -> array transport)
     sep_init(cp.adj_s3, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], Kv, (float)c3);
     for (int kt = 0; kt < K[1]; ++kt)
       for (int ks = 0; ks < K[0]; ++ks) {
-        sep_add(cp.adj_s3, 0, ks, kt, 1.f);
+        for (int tau = 0; tau < T; ++tau) sep_add(cp.adj_s3, 0, ks * T + tau, kt * T + tau, 1.f);
         sep_close_output(cp.adj_s3);
       }
     // adjoint S1: slice n = c1 * sum_k B^{q_n a}_k field_k
@@ -1343,9 +1447,9 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
         int ns = 0, nt_ = 0;
         for (char v : in_s) ns += v;
         for (char v : in_t) nt_ += v;
-        if (nt_ == K[1] && ns * nt_ == (int)S.size() && !std::getenv("LFM_SUBSET_PER_VIEW")) {
+        if (nt_ == K[1] && ns * nt_ == (int)S.size() && T == 1 && !std::getenv("LFM_SUBSET_PER_VIEW")) {
           vo.collapsed = 1;
-          build_composite(cp, 0, in_s, sc, nz, ndet[0], nsrc[0], plen, vo.cfs, vo.cas);
+          build_composite(cp, 0, in_s, sc, nz, ndet[0], nsrc[0], plen, vo.cfs, vo.cas, 0);
         }
       }
       if (plen) {
@@ -1356,11 +1460,13 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
           sep_close_output(vo.fwd_s1);
         }
         sep_init(vo.fwd_s3, &cp.s3f[0], &cp.s3f[1], dst[0].n, dst[1].n, 1, (float)(c3 * sc));
-        for (size_t j = 0; j < S.size(); ++j) sep_add(vo.fwd_s3, (long long)j * nfield, S[j] % K[0], S[j] / K[0], 1.f);
+        for (size_t j = 0; j < S.size(); ++j)
+          for (int tau = 0; tau < T; ++tau)
+            sep_add(vo.fwd_s3, (long long)j * nfield, (S[j] % K[0]) * T + tau, (S[j] / K[0]) * T + tau, 1.f);
         sep_close_output(vo.fwd_s3);
         sep_init(vo.adj_s3, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], vo.n_views, (float)c3);
         for (int k : S) {
-          sep_add(vo.adj_s3, 0, k % K[0], k / K[0], 1.f);
+          for (int tau = 0; tau < T; ++tau) sep_add(vo.adj_s3, 0, (k % K[0]) * T + tau, (k / K[0]) * T + tau, 1.f);
           sep_close_output(vo.adj_s3);
         }
         sep_init(vo.adj_s1, &cp.s1a[0], &cp.s1a[1], dst[0].n, dst[1].n, nz, (float)(c1 * sc));
@@ -1450,6 +1556,26 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   cp.fwd_c2.s_ident = 1;
   sep_add(cp.fwd_c2, 0, 0, 0, 1.f);
   sep_close_output(cp.fwd_c2);
+  // terms >= 1 of a non-separable lenslet stage: their own interleaved t families and t-pass ops (the s passes run
+  // on their band_v tables, built at upload); the collapsed path then sums the terms (tcgen05 kernels only)
+  for (Component& cm : cp.comps) {
+    make_rows_by_slice(cm.ca1n, cm.ca[1]);
+    if (nz % 64 == 0 && !std::getenv("LFM_UMMA_ROWS128")) {
+      cm.ca1n.u_mode = 1;
+      cm.ca1n.u_nz = nz;
+    }
+    build_umma(cm.ca1n);
+    make_cols_by_slice(cm.cf1n, cm.cf[1]);
+    build_umma(cm.cf1n);
+    sep_init(cm.adj_c1, &cp.id_s, &cm.ca1n, ndet[0], ndet[1], 1, 1.f);
+    cm.adj_c1.s_ident = 1;
+    sep_add(cm.adj_c1, 0, 0, 0, 1.f);
+    sep_close_output(cm.adj_c1);
+    sep_init(cm.fwd_c2, &cp.id_s, &cm.cf1n, ndet[0], ny * nz, 1, (float)(c1 * c3));
+    cm.fwd_c2.s_ident = 1;
+    sep_add(cm.fwd_c2, 0, 0, 0, 1.f);
+    sep_close_output(cm.fwd_c2);
+  }
   // transposed variants of the s passes (t passes over transposed slices, written back transposed):
   //  fwd_p1: U[(vt,n)][i_s] = sum_vx C_s,n[i_s][vx] xT_n[vx][vt]     (xT_n = x_n transposed, [vx][vt])
   //  adj_a2: x_n[vt][vx]   = sum_j C_s,n^T[vx][j] ZT_n[j][vt]        (ZT_n = Z_n transposed, [j][vt])
@@ -1498,9 +1624,11 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
       sep_init(cp.xp_s3a, &cp.s3a[0], &cp.s3a[1], ndet[0], ndet[1], Kv, (float)(1.0 / Vdst));
       for (int kt = 0; kt < K[1]; ++kt)
         for (int ks = 0; ks < K[0]; ++ks) {
-          sep_add(cp.xp_s3f, (long long)(kt * K[0] + ks) * nfield, ks, kt, 1.f);
+          for (int tau = 0; tau < T; ++tau)
+            sep_add(cp.xp_s3f, (long long)(kt * K[0] + ks) * nfield, ks * T + tau, kt * T + tau, 1.f);
           sep_close_output(cp.xp_s3f);
-          sep_add(cp.xp_s3a, (long long)(kt * K[0] + ks) * npix, ks, kt, 1.f);
+          for (int tau = 0; tau < T; ++tau)
+            sep_add(cp.xp_s3a, (long long)(kt * K[0] + ks) * npix, ks * T + tau, kt * T + tau, 1.f);
           sep_close_output(cp.xp_s3a);
         }
     }

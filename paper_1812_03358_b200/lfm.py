@@ -43,7 +43,7 @@ class Camera(ctypes.Structure):
                 ("d_mu_m", ctypes.c_double), ("d_d_mu", ctypes.c_double), ("f_mu", ctypes.c_double),
                 ("fill", ctypes.c_double), ("nl_s", ctypes.c_int), ("nl_t", ctypes.c_int), ("n_a", ctypes.c_int),
                 ("n_s", ctypes.c_int), ("n_t", ctypes.c_int), ("px_s", ctypes.c_double), ("px_t", ctypes.c_double),
-                ("R", ctypes.c_double * 9)]
+                ("R", ctypes.c_double * 9), ("lens_layout", ctypes.c_int), ("aperture", ctypes.c_int)]
 
 
 class Geometry(ctypes.Structure):
@@ -62,7 +62,7 @@ class Info(ctypes.Structure):
                 ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
                 ("fma_stage", ctypes.c_double * 2), ("mma_stage", ctypes.c_double * 2),
                 ("kind_stage", ctypes.c_int * 2), ("fma_spass", ctypes.c_double * 2),
-                ("subset_collapsed", ctypes.c_int)]
+                ("subset_collapsed", ctypes.c_int), ("s3_terms", ctypes.c_int)]
 
     def as_dict(self):
         out = {}
@@ -152,6 +152,8 @@ def _camera_struct(c):
     for name, _ in Camera._fields_:
         if name == "R":
             cs.R = (ctypes.c_double * 9)(*[float(v) for v in c["R"]])
+        elif name in ("lens_layout", "aperture"):
+            setattr(cs, name, int(c.get(name, 0)))
         else:
             setattr(cs, name, c[name])
     return cs

@@ -12,7 +12,8 @@ from workloads import make_config, normal_vector, uniform_vector, uniform_volume
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "ragged"]
+SMALL = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "ragged",
+         "tiny_hex", "tiny_disk", "small_hex"]
 PATHS = [0, 1]  # PER_VIEW, COLLAPSED
 
 
@@ -118,14 +119,20 @@ def _xport_ref(op, dst_kind, src_kind, n, src):
                 out.append(cam.S1[1][kt][n].T @ s @ cam.S1[0][ks][n] / V)
             elif (dst_kind, src_kind) == ("d", "a"):
                 V = basis_volume(cam.lenslet_planes[0][0], cam.d0[0]) * basis_volume(cam.lenslet_planes[1][0], cam.d0[1])
-                out.append(cam.S3[1][kt] @ s @ cam.S3[0][ks].T / V)
+                if cam.nonsep:   # literal per-lenslet 2-D masks (R12/R13)
+                    out.append(sum(Bt @ (m * s) @ Bs.T for Bs, Bt, m in cam.S3_2d[ks, kt]) / V)
+                else:
+                    out.append(cam.S3[1][kt] @ s @ cam.S3[0][ks].T / V)
             elif (dst_kind, src_kind) == ("a", "d"):
                 V = basis_volume(cam.array_planes[0], cam.d0[0]) * basis_volume(cam.array_planes[1], cam.d0[1])
-                out.append(cam.S3[1][kt].T @ s @ cam.S3[0][ks] / V)
+                if cam.nonsep:
+                    out.append(sum(m * (Bt.T @ s @ Bs) for Bs, Bt, m in cam.S3_2d[ks, kt]) / V)
+                else:
+                    out.append(cam.S3[1][kt].T @ s @ cam.S3[0][ks] / V)
     return np.stack(out)
 
 
-@pytest.mark.parametrize("name", ["tiny", "tiny_single", "ragged"])
+@pytest.mark.parametrize("name", ["tiny", "tiny_single", "ragged", "tiny_hex"])
 def test_lf_transport_parity(name):
     from paper_1812_03358_b200 import lfm
     cfg, plan, ops, ws = _setup(name)

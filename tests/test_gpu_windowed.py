@@ -128,12 +128,13 @@ def test_column_and_tile_windows_partition(name):
             assert np.abs(got - yf[r0:r1, c0:c1]).max() <= TOL * np.abs(yf).max(), (c, r0, r1, c0, c1)
 
 
+@pytest.mark.parametrize("name", ["small_two", "small_hex"])
 @pytest.mark.parametrize("path", [0, 1])
-def test_windows_vs_oracle(path):
+def test_windows_vs_oracle(path, name):
     """Window entry points against the fp64 oracle: A^T P y with P the window mask, on both evaluation orders
-    (the per-view path applies a column window by masking y)."""
+    (the per-view path applies a column window by masking y); small_hex sums T > 1 lenslet-stage terms."""
     from paper_1812_03358_b200 import lfm
-    cfg = make_config("small_two")
+    cfg = make_config(name)
     plan = lfm.Plan(cfg, device=0)
     ws = plan.workspace()
     ops = build_system(cfg)
