@@ -92,3 +92,34 @@ def test_256_four_camera_sampled_oracle_parity():
             err = np.abs(gg[cam["g"]["idx"]] - np.array(cam["g"]["val"])).max() / cam["g"]["max_abs"]
             assert err <= TOL, (c, path, "adjoint", err)
             assert abs(np.abs(gg).max() - cam["g"]["max_abs"]) <= TOL * cam["g"]["max_abs"]
+
+
+def test_128_hex_properties():
+    """NEXT-4 at the metric's scale (hexagonal layout + circular apertures, T = 2 lenslet-stage terms): the per-view
+    and collapsed evaluation orders agree element by element, and the fp32 adjoint identity holds (the oracle's
+    literal per-lenslet model would take hours at 128 x 146 lenslets; its parity is at tiny/small sizes)."""
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config("128^3 hex two-camera")
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    n_vox = plan.infos[0]["n_vox"]
+    xf = dev(flame_volume(cfg["volume"])).reshape(-1)
+    x = dev(normal_vector(n_vox, 2))
+    for c in range(plan.n_cam):
+        assert plan.infos[c]["s3_terms"] > 1
+        n_pix = plan.infos[c]["n_pix"]
+        y0 = torch.empty(n_pix, device="cuda:0")
+        y1 = torch.empty(n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, xf, y0, ws, path=lfm.PER_VIEW)
+        lfm.A_forward(plan, c, xf, y1, ws, path=lfm.COLLAPSED)
+        assert max_rel(host(y0), host(y1)) <= TOL
+        r = dev(normal_vector(n_pix, 3))
+        g0 = torch.empty(n_vox, device="cuda:0")
+        g1 = torch.empty(n_vox, device="cuda:0")
+        lfm.A_adjoint(plan, c, r, g0, ws, path=lfm.PER_VIEW)
+        lfm.A_adjoint(plan, c, r, g1, ws, path=lfm.COLLAPSED)
+        assert max_rel(host(g0), host(g1)) <= TOL
+        lfm.A_forward(plan, c, x, y1, ws)
+        lhs = float((y1.double() * r.double()).sum())
+        rhs = float((x.double() * g1.double()).sum())
+        assert abs(lhs - rhs) / (float(y1.double().norm()) * float(r.double().norm())) <= 1e-5

@@ -130,6 +130,11 @@ def make_config(name):
         return dict(name=name, volume=volume(128, 0.4),
                     cameras=[plenoptic_camera(128, 16, 0.005, 8, 4),
                              plenoptic_camera(128, 16, 0.005, 8, 4, pose=pose_yaw(30.0))])
+    if name == "128^3 hex two-camera":  # NEXT-4 at the metric's scale: hexagonal layout, circular apertures
+        return dict(name=name, volume=volume(128, 0.4),
+                    cameras=[plenoptic_camera(128, 16, 0.005, 8, 4, layout=1, lens_aperture=1, rows=146, px_per_row=14),
+                             plenoptic_camera(128, 16, 0.005, 8, 4, layout=1, lens_aperture=1, rows=146, px_per_row=14,
+                                              pose=pose_yaw(30.0))])
     if name == "256^3 four-camera":  # configs[3]
         return dict(name=name, volume=volume(256, 0.2),
                     cameras=[plenoptic_camera(128, 16, 0.005, 8, 4, pose=pose_yaw(-30.0)),
@@ -140,5 +145,5 @@ def make_config(name):
 
 
 CONFIGS = ["tiny", "tiny_k4", "tiny_single", "tiny_yaw15", "tiny_multi", "tiny_dirac", "tiny_turn", "small_two", "odd_ny",
-           "tiny_hex", "tiny_disk", "small_hex",
+           "tiny_hex", "tiny_disk", "small_hex", "128^3 hex two-camera",
            "64^3 single", "128^3 two-camera", "256^3 four-camera"]
