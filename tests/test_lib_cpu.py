@@ -149,24 +149,27 @@ def test_rotation_factors_and_shear_tables(name):
         vox_r = tuple(v / d for v, d in zip(vox, dec["D"]))
         assert tuple(inf["vox_r"]) == vox_r
         coeffs = [(dec["a_zx"], dec["a_zy"]), (dec["a_xy"], dec["a_xz"]), (dec["a_yx"], dec["a_yz"])]
+        import scipy.sparse as sp
         for p, axis in enumerate("zxy"):
-            E = shear_matrix(dims, vox_r, axis, *coeffs[p]).toarray()
+            E = shear_matrix(dims, vox_r, axis, *coeffs[p]).tocsr()
             mlo = plan.export_table(c, "ROT_MLO", 0, p)
             if len(mlo) == 0:                                        # identity pass skipped
                 assert coeffs[p] == (0.0, 0.0)
                 continue
             w = plan.export_table(c, "ROT_W64", 0, p).reshape(len(mlo), -1)
-            rec = np.zeros_like(E)
             nx, ny, nz = dims
-            for flat in range(nx * ny * nz):
-                ix, iy, iz = flat % nx, (flat // nx) % ny, flat // (nx * ny)
-                line, pos, n, stride = {"z": (ix + nx * iy, iz, nz, nx * ny), "x": (iy + ny * iz, ix, nx, 1),
-                                        "y": (ix + nx * iz, iy, ny, nx)}[axis]
-                for q in range(w.shape[1]):
-                    j = pos + mlo[line] + q
-                    if 0 <= j < n and w[line, q] != 0.0:
-                        rec[flat, flat + (j - pos) * stride] = w[line, q]
-            assert np.abs(rec - E).max() <= 1e-12
+            flat = np.arange(nx * ny * nz)
+            ix, iy, iz = flat % nx, (flat // nx) % ny, flat // (nx * ny)
+            line, pos, n, stride = {"z": (ix + nx * iy, iz, nz, nx * ny), "x": (iy + ny * iz, ix, nx, 1),
+                                    "y": (ix + nx * iz, iy, ny, nx)}[axis]
+            rows, cols, vals = [], [], []
+            for q in range(w.shape[1]):                              # the plan's line tables as a sparse matrix
+                j = pos + mlo[line] + q
+                ok = (j >= 0) & (j < n) & (w[line, q] != 0.0)
+                rows.append(flat[ok]); cols.append((flat + (j - pos) * stride)[ok]); vals.append(w[line, q][ok])
+            N = nx * ny * nz
+            rec = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N))
+            assert abs(rec - E).max() <= 1e-12
 
 
 @pytest.mark.parametrize("name", CONFIGS)
