@@ -117,16 +117,7 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_fw, fw.data(), fw.size() * 4, err)) != LFM_OK) return st;
     bytes += f.f_off.size() * 4 + fr.size() * 4 + fw.size() * 4;
   }
-  if (!f.x_off.empty()) {
-    std::vector<int32_t> xk(f.x_k);
-    xk.push_back(0);
-    std::vector<float> xa(f.x_a);
-    xa.resize(xa.size() + 256, 0.f);
-    if ((st = dev_upload(&f.d_xoff, f.x_off.data(), f.x_off.size() * 4, err)) != LFM_OK) return st;
-    if ((st = dev_upload(&f.d_xk, xk.data(), xk.size() * 4, err)) != LFM_OK) return st;
-    if ((st = dev_upload(&f.d_xa, xa.data(), xa.size() * 4, err)) != LFM_OK) return st;
-    bytes += f.x_off.size() * 4 + xk.size() * 4 + xa.size() * 4;
-  }
+
   if (!f.u_off.empty()) {
     std::vector<int32_t> uk(f.u_k0);
     uk.push_back(0);
@@ -172,64 +163,7 @@ static lfm_status upload_sep(SepOp& op, size_t& bytes, std::string& err) {
   st = dev_upload(&op.d_fp_s, vs.data(), vs.size() * sizeof(TileT), err);
   if (st != LFM_OK) return st;
   bytes += op.terms.size() * sizeof(Term) + (vs.size() + vt.size()) * sizeof(TileT);
-  if (op.kind == 4) {
-    // band_s chunk lists: per (t-table, tile_y) the union of the tile's MSEG segments (gaps <= 2 rows
-    // merged), cut into chunks of <= op.chunk source rows, in increasing row order
-    const int ng = ft.n_groups, NG = op.tt / 4;
-    std::vector<int2> ch;
-    std::vector<int32_t> off((size_t)ft.n_tables * op.nty + 1, 0);
-    std::vector<std::pair<int, int>> iv;
-    for (int m = 0; m < ft.n_tables; ++m)
-      for (int y = 0; y < op.nty; ++y) {
-        off[(size_t)m * op.nty + y] = (int)ch.size();
-        iv.clear();
-        for (int g = y * NG; g < std::min(ng, y * NG + NG); ++g) {
-          size_t gi = (size_t)m * ng + g;
-          for (int sg = ft.m_off[gi]; sg < ft.m_off[gi + 1]; ++sg)
-            iv.push_back({ft.m_seg[4 * (size_t)sg], ft.m_seg[4 * (size_t)sg] + ft.m_seg[4 * (size_t)sg + 1]});
-        }
-        std::sort(iv.begin(), iv.end());
-        int a = -1, b = -1;
-        auto flush = [&]() {
-          for (int lo = a; lo < b; lo += op.chunk) ch.push_back(make_int2(lo, std::min(op.chunk, b - lo)));
-        };
-        for (auto& v : iv) {
-          if (a < 0) { a = v.first; b = v.second; continue; }
-          if (v.first <= b + 2) { b = std::max(b, v.second); continue; }
-          flush();
-          a = v.first; b = v.second;
-        }
-        if (a >= 0) flush();
-      }
-    off.back() = (int)ch.size();
-    // per (chunk, group): the range [e_lo, e_hi) of the group's flat entries whose source rows fall in the
-    // chunk (flat entries are in increasing row order within a group)
-    std::vector<int2> cw(ch.size() * NG + 1, make_int2(0, 0));
-    for (int m = 0; m < ft.n_tables; ++m)
-      for (int y = 0; y < op.nty; ++y)
-        for (int k = 0; k < NG; ++k) {
-          const int g = y * NG + k;
-          if (g >= ng) continue;
-          const size_t gi = (size_t)m * ng + g;
-          int e = ft.f_off[gi];
-          const int e_end = ft.f_off[gi + 1];
-          for (int c = off[(size_t)m * op.nty + y]; c < off[(size_t)m * op.nty + y + 1]; ++c) {
-            const int cs = ch[c].x, ce = ch[c].x + ch[c].y;
-            while (e < e_end && ft.f_row[e] < cs) ++e;
-            int e2 = e;
-            while (e2 < e_end && ft.f_row[e2] < ce) ++e2;
-            cw[(size_t)c * NG + k] = make_int2(e, e2);
-            e = e2;
-          }
-        }
-    ch.push_back(make_int2(0, 0));
-    if ((st = dev_upload(&op.d_chunks, reinterpret_cast<int32_t*>(ch.data()), ch.size() * sizeof(int2), err)) != LFM_OK)
-      return st;
-    if ((st = dev_upload(&op.d_chunk_w, reinterpret_cast<int32_t*>(cw.data()), cw.size() * sizeof(int2), err)) != LFM_OK)
-      return st;
-    if ((st = dev_upload(&op.d_chunk_off, off.data(), off.size() * 4, err)) != LFM_OK) return st;
-    bytes += ch.size() * sizeof(int2) + off.size() * 4;
-  }
+
   return dev_upload(&op.d_fp_t, vt.data(), vt.size() * sizeof(TileT), err);
 }
 
@@ -634,8 +568,6 @@ void free_camera(CameraPlan& cp) {
     f->d_m8off = nullptr; f->d_m8seg = nullptr; f->d_m8w = nullptr;
     dfree(f->d_foff); dfree(f->d_frow); dfree(f->d_fw);
     f->d_foff = nullptr; f->d_frow = nullptr; f->d_fw = nullptr;
-    dfree(f->d_xoff); dfree(f->d_xk); dfree(f->d_xa);
-    f->d_xoff = nullptr; f->d_xk = nullptr; f->d_xa = nullptr;
     dfree(f->d_uoff); dfree(f->d_uk0); dfree(f->d_ua);
     f->d_uoff = nullptr; f->d_uk0 = nullptr; f->d_ua = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
@@ -649,10 +581,8 @@ void free_camera(CameraPlan& cp) {
   for (Component& cm : cp.comps)
     for (SepOp* op : {&cm.fwd_c2, &cm.adj_c1}) all.push_back(op);
   for (SepOp* op : all) {
-    dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t); dfree(op->d_chunks);
-    dfree(op->d_chunk_off); dfree(op->d_chunk_w);
+    dfree(op->d_terms); dfree(op->d_offs); dfree(op->d_fp_s); dfree(op->d_fp_t);
     op->d_terms = nullptr; op->d_offs = nullptr; op->d_fp_s = nullptr; op->d_fp_t = nullptr;
-    op->d_chunks = nullptr; op->d_chunk_off = nullptr; op->d_chunk_w = nullptr;
   }
   for (int p = 0; p < 3; ++p)
     for (int d = 0; d < 2; ++d) {
@@ -680,12 +610,6 @@ struct SepArgs {
   long long out_stride;
   long long src_pitch;  // floats between source rows
   long long out_pitch;  // floats between output rows
-  const int2* chunks;     // band_s_kernel chunk lists
-  const int32_t* chunk_off;
-  const int2* chunk_w;
-  const int32_t* t_xoff;  // tensor-core blocks (band_x_kernel)
-  const int32_t* t_xk;
-  const float4* t_xa;
   const int32_t* t_foff;  // flat MSEG entries (band_f_kernel)
   const int4* t_frow;
   const float4* t_fw;
@@ -1047,235 +971,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-struct StreamHdr {
-  float scale;
-  int ft_lo, ft_w, wt_off, live;
-};
-
-template <int TS, int TT, int NCW, int STAGES>
-__global__ void __launch_bounds__((NCW + 1) * 32) band_t_kernel(SepArgs a) {
-  constexpr int NCT = NCW * 32;        // consumer threads
-  constexpr int NQ = TS / 4;
-  constexpr int GSTEP = NCT / NQ;
-  constexpr int NG = TT / 4;
-  constexpr int GP = NG / GSTEP;
-  static_assert(GP >= 1 && NG % GSTEP == 0 && NCT % NQ == 0, "tile/thread mismatch");
-  extern __shared__ __align__(16) float smem[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  __shared__ StreamHdr hdr[STAGES];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
-  const int os0 = tx * TS, ot0 = ty * TT;
-  const int ustride = a.ftm * TS;                      // floats of the U slot
-  const int wstride = (a.wtm + 3) / 4 * 4;
-  const int slot_floats = ustride + wstride + 8 * NG;  // U | weights | 2 int4 descriptors per group
-  const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == NCW) {
-    // ---------------- producer warp
-    const int ncol = min(TS, a.n_is - os0);
-    const uint32_t row_bytes = (uint32_t)ncol * 4;
-    for (int i = 0; i < e1 - e0; ++i) {
-      const int s = i % STAGES;
-      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-      const Term term = a.terms[e0 + i];
-      const TileT ft = a.fp_t[(size_t)term.t_tab * a.nty + ty];
-      float* slot = smem + (size_t)s * slot_floats;
-      // source rows outside [win_r0, win_r1) count as zero (adjoint detector-row sharding)
-      const int wlo = max(ft.lo, a.win_r0), whi = min(ft.lo + ft.width, a.win_r1);
-      const bool live = ft.width != 0 && whi > wlo;
-      const int ngt = min(NG, a.t_ngroups - ty * NG);  // descriptors that exist for this tile
-      const uint32_t bytes =
-          live ? (uint32_t)(whi - wlo) * row_bytes + (uint32_t)ft.wlen * 4 + 32u * ngt : 0u;
-      if (live && (wlo > ft.lo || whi < ft.lo + ft.width)) {
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = ft.lo; r < ft.lo + ft.width; ++r) {
-          if (r >= wlo && r < whi) continue;
-          for (int c = lane; c < TS / 4; c += 32) reinterpret_cast<float4*>(slot + (r - ft.lo) * TS)[c] = z;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      }
-      __syncwarp();
-      if (lane == 0) {
-        hdr[s] = StreamHdr{term.scale, ft.lo, ft.width, ft.woff, live ? 1 : 0};
-        mbar_arrive_expect_tx(&full[s], bytes);
-      }
-      __syncwarp();
-      if (live) {
-        const float* src = a.src + term.src_off + (size_t)wlo * a.src_pitch + os0;
-        float* dst = slot + (wlo - ft.lo) * TS;
-        for (int r = lane; r < whi - wlo; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.src_pitch, row_bytes, &full[s]);
-        if (lane == 0) {
-          bulk_g2s(slot + ustride, a.t_gw + ft.woff, (uint32_t)ft.wlen * 4, &full[s]);
-          bulk_g2s(slot + ustride + wstride, a.t_g + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG), 32u * ngt,
-                   &full[s]);
-        }
-      }
-    }
-    return;
-  }
-  // ---------------- consumer warps
-  const int quad = tid % NQ, gsub = tid / NQ;
-  float acc[GP][4][4];
-#pragma unroll
-  for (int j = 0; j < GP; ++j)
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
-  for (int i = 0; i < e1 - e0; ++i) {
-    const int s = i % STAGES;
-    mbar_wait(&full[s], (i / STAGES) & 1);
-    const StreamHdr h = hdr[s];
-    if (h.live) {
-      const float* slot = smem + (size_t)s * slot_floats;
-      const float* W = slot + ustride;
-      const int4* GD = reinterpret_cast<const int4*>(slot + ustride + wstride);
-#pragma unroll
-      for (int j = 0; j < GP; ++j) {
-        const int gl = gsub + j * GSTEP;
-        if (ty * NG + gl >= a.t_ngroups) continue;
-        float part[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) part[r][c] = 0.f;
-#pragma unroll
-        for (int sg = 0; sg < 2; ++sg) {
-          const int4 gd = GD[2 * gl + sg];
-          const float4* wp = reinterpret_cast<const float4*>(W + (gd.z - h.wt_off));
-          const float4* up = reinterpret_cast<const float4*>(slot + (gd.x - h.ft_lo) * TS + quad * 4);
-#pragma unroll 4
-          for (int p = 0; p < gd.y; ++p) fma4x4(part, wp[p], up[p * (TS / 4)]);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[j][r][c] = fmaf(h.scale, part[r][c], acc[j][r][c]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  float* outb = a.out + (size_t)b * a.out_stride;
-  const int col = os0 + quad * 4;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
-#pragma unroll
-  for (int j = 0; j < GP; ++j) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
-      if (row >= a.n_ot) continue;
-      float* p = outb + (size_t)row * a.out_pitch + col;
-      float v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
-      if (vec) {
-        float4 o = make_float4(v[0], v[1], v[2], v[3]);
-        if (a.accumulate) {
-          const float4 q = *reinterpret_cast<float4*>(p);
-          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-        }
-        *reinterpret_cast<float4*>(p) = o;
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (col + c >= a.n_os) continue;
-          p[c] = a.accumulate ? p[c] + v[c] : v[c];
-        }
-      }
-    }
-  }
-}
-
-// L2-gather t-pass for identity-s ops: no shared memory and no barriers.  Thread = (4 source columns,
-// GP groups of 4 output rows); per term and segment a branch-free loop over the segment's source rows
-// [gd.x, gd.x + gd.y) clipped once to the row window, loading u (16 B) and the 4 weights (16 B, L1-resident)
-// per row with a deep unroll so that many L2 requests are in flight per warp.
-template <int TS, int TT, int NT, int UNR>
-__global__ void __launch_bounds__(NT, 1024 / NT) band_g_kernel(SepArgs a) {
-  constexpr int NQ = TS / 4;
-  constexpr int GSTEP = NT / NQ;
-  constexpr int NG = TT / 4;
-  constexpr int GP = NG / GSTEP;
-  static_assert(GP >= 1 && NG % GSTEP == 0 && NT % NQ == 0, "tile/thread mismatch");
-  const int tid = threadIdx.x;
-  const int quad = tid % NQ, gsub = tid / NQ;
-  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
-  const int os0 = tx * TS, ot0 = ty * TT;
-  const int col = os0 + quad * 4;
-  const bool col_ok = col < a.n_is;  // n_is % 4 == 0 (checked at tuning time): whole quads in or out
-  const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  float acc[GP][4][4];
-#pragma unroll
-  for (int j = 0; j < GP; ++j)
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[j][r][c] = 0.f;
-  if (col_ok) {
-    for (int e = e0; e < e1; ++e) {
-      const Term term = a.terms[e];
-      const float* src = a.src + term.src_off + col;
-      const int4* GD = reinterpret_cast<const int4*>(a.t_g) + 2 * ((size_t)term.t_tab * a.t_ngroups + ty * NG);
-#pragma unroll
-      for (int j = 0; j < GP; ++j) {
-        const int gl = gsub + j * GSTEP;
-        if (ty * NG + gl >= a.t_ngroups) continue;
-#pragma unroll
-        for (int sg = 0; sg < 2; ++sg) {
-          const int4 gd = __ldg(GD + 2 * gl + sg);
-          const int p0 = max(0, a.win_r0 - gd.x), p1 = min(gd.y, a.win_r1 - gd.x);
-          const float4* wp = reinterpret_cast<const float4*>(a.t_gw + gd.z);
-          const float* up = src + (size_t)gd.x * a.src_pitch;
-#pragma unroll UNR
-          for (int p = p0; p < p1; ++p)
-            fma4x4(acc[j], __ldg(wp + p), __ldg(reinterpret_cast<const float4*>(up + (size_t)p * a.src_pitch)));
-        }
-      }
-    }
-  }
-  if (!col_ok) return;
-  float* outb = a.out + (size_t)b * a.out_stride;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
-#pragma unroll
-  for (int j = 0; j < GP; ++j) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int row = ot0 + 4 * (gsub + j * GSTEP) + r;
-      if (row >= a.n_ot) continue;
-      float* p = outb + (size_t)row * a.out_pitch + col;
-      float v[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[j][r][c];
-      if (vec) {
-        float4 o = make_float4(v[0], v[1], v[2], v[3]);
-        if (a.accumulate) {
-          const float4 q = *reinterpret_cast<float4*>(p);
-          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-        }
-        *reinterpret_cast<float4*>(p) = o;
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (col + c >= a.n_os) continue;
-          p[c] = a.accumulate ? p[c] + v[c] : v[c];
-        }
-      }
-    }
-  }
-}
-
 // L2-gather t-pass over the MSEG form of the t family (identity s): per group a CSR list of dense
 // segments (one per cluster of source rows), so the FMA slots follow the non-zeros (~95% for the
-// slice-interleaved adjoint family, vs ~36-52% with two segments).  Otherwise as band_g_kernel.
+// slice-interleaved adjoint family, vs ~36-52% with two segments).  L2 gather, no shared memory.
 template <int GR>
 __device__ __forceinline__ void fma_gr(float (&acc)[GR][4], const float* __restrict__ w, float4 u) {
 #pragma unroll
@@ -1399,136 +1097,6 @@ __global__ void __launch_bounds__(NT, (GR == 8 ? 512 : 1024) / NT) band_m_kernel
       }
     }
   }
-}
-
-// Streaming MSEG t-pass for identity-s ops (TS = 128 columns, one consumer warp per group of 4 output
-// rows, NG groups per CTA, plus one producer warp).  The producer streams the union of the tile's
-// segment rows, chunk by chunk (cp.async.bulk per source row, completion on an mbarrier), into a
-// STAGES-deep ring; every consumer warp walks its own sorted segment list alongside the chunks, so each
-// source row is read from L2 once per CTA and shared by all NG groups through shared memory.
-template <int NG, int K, int STAGES>
-__global__ void __launch_bounds__((NG + 1) * 32) band_s_kernel(SepArgs a) {
-  constexpr int TS = 128;
-  constexpr int SLOT = K * TS;  // the chunk's source rows
-  extern __shared__ __align__(16) float smem[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tx = blockIdx.x, ty = blockIdx.y + a.ty0, b = blockIdx.z;
-  const int os0 = tx * TS;
-  const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NG);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == NG) {
-    // ---------------- producer warp: all chunks of all terms, in order
-    const int ncol = min(TS, a.n_is - os0);
-    const uint32_t row_bytes = (uint32_t)ncol * 4;
-    int it = 0;
-    for (int e = e0; e < e1; ++e) {
-      const Term term = a.terms[e];
-      const int c0 = a.chunk_off[(size_t)term.t_tab * a.nty + ty], c1 = a.chunk_off[(size_t)term.t_tab * a.nty + ty + 1];
-      for (int c = c0; c < c1; ++c, ++it) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        const int2 ck = a.chunks[c];
-        float* slot = smem + (size_t)s * SLOT;
-        const int wlo = max(ck.x, a.win_r0), whi = min(ck.x + ck.y, a.win_r1);
-        const int nrow = max(0, whi - wlo);
-
-        if (nrow < ck.y) {  // rows outside the source window read as zero
-          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int r = 0; r < ck.y; ++r) {
-            const int row = ck.x + r;
-            if (row >= wlo && row < whi) continue;
-            for (int q = lane; q < TS / 4; q += 32) reinterpret_cast<float4*>(slot + r * TS)[q] = z;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * row_bytes);
-        __syncwarp();
-        const float* src = a.src + term.src_off + (size_t)wlo * a.src_pitch + os0;
-        float* dst = slot + (wlo - ck.x) * TS;
-        for (int r = lane; r < nrow; r += 32) bulk_g2s(dst + r * TS, src + (size_t)r * a.src_pitch, row_bytes, &full[s]);
-      }
-    }
-    return;
-  }
-  // ---------------- consumer warp `warp` = group ty*NG + warp: its flat entries of each chunk
-  const int g = ty * NG + warp;
-  const bool gvalid = g < a.t_ngroups;
-  const int* frow = reinterpret_cast<const int*>(a.t_frow);
-  float acc[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
-  int it = 0;
-  for (int e = e0; e < e1; ++e) {
-    const Term term = a.terms[e];
-    const int c0 = a.chunk_off[(size_t)term.t_tab * a.nty + ty], c1 = a.chunk_off[(size_t)term.t_tab * a.nty + ty + 1];
-    for (int c = c0; c < c1; ++c, ++it) {
-      const int s = it % STAGES;
-      const int2 ck = a.chunks[c];
-      const int2 er = a.chunk_w[(size_t)c * NG + warp];
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      const float* up = smem + (size_t)s * SLOT + lane * 4 - ck.x * TS;
-#pragma unroll 4
-      for (int q = er.x; q < er.y; ++q)
-        fma4x4(acc, __ldg(a.t_fw + q), *reinterpret_cast<const float4*>(up + __ldg(frow + q) * TS));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-  }
-  if (!gvalid) return;
-  const int col = os0 + lane * 4;
-  if (col >= a.n_os) return;
-  float* outb = a.out + (size_t)b * a.out_stride;
-  const bool vec = (col + 3 < a.n_os) && ((a.n_os & 3) == 0) && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int row = 4 * g + r;
-    if (row >= a.n_ot) continue;
-    float* p = outb + (size_t)row * a.out_pitch + col;
-    float v[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = a.out_scale * acc[r][c];
-    if (vec) {
-      float4 o = make_float4(v[0], v[1], v[2], v[3]);
-      if (a.accumulate) {
-        const float4 q = *reinterpret_cast<float4*>(p);
-        o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-      }
-      *reinterpret_cast<float4*>(p) = o;
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (col + c >= a.n_os) continue;
-        p[c] = a.accumulate ? p[c] + v[c] : v[c];
-      }
-    }
-  }
-}
-
-template <int NG, int K, int STAGES>
-static lfm_status launch_band_s(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err) {
-  auto kern = band_s_kernel<NG, K, STAGES>;
-  const size_t smem = (size_t)STAGES * K * 128 * 4;
-  static bool configured_dev[LFM_MAX_DEV];
-  bool& configured = configured_dev[cur_dev()];
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_s_kernel)", err);
-    configured = true;
-  }
-  kern<<<grid, (NG + 1) * 32, smem, s>>>(a);
-  ++g_launches;
-  return cuda_check(cudaGetLastError(), "band_s_kernel launch", err);
 }
 
 // Flat L2-gather t-pass (identity s): per group of 4 output rows a padded list of entries
@@ -1672,170 +1240,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) band_f_kernel(SepArgs a) {
   }
 }
 
-// Tensor-core t pass (identity s, one output row tile of 16 rows per warp-group): out = C U with C sparse,
-// evaluated as block-sparse dense products on the legacy tensor path (mma.sync m16n8k8, tf32 in, fp32
-// accumulate) in 3xTF32 form, C U = C_hi U_hi + C_hi U_lo + C_lo U_hi (+ O(2^-22)), which keeps fp32-level
-// accuracy.  The weights arrive pre-split in fragment order (build_mma); the source values are split in
-// registers (cvt.rna.tf32).  CTA = NW warps on one 16-row tile, each warp 64 columns (8 n8 tiles).
-__device__ __forceinline__ uint32_t tf32_rna(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return r;
-}
-__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <int NW, int NJ, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB) band_x_kernel(SepArgs a) {
-  // Column map: n-index g of n8 tile j is column c0 + NJ g + j, so a lane's B values of one source row are
-  // NJ consecutive floats and its accumulators cover 2 NJ consecutive columns.
-  constexpr int WC = 8 * NJ;  // columns per warp
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  const int ty = blockIdx.y + a.ty0, b = blockIdx.z;
-  const int c0 = (blockIdx.x * NW + warp) * WC;  // this warp's first column
-  if (c0 >= a.n_is) return;
-  const int e0 = a.offs[b], e1 = a.offs[b + 1];
-  const int ntile = (a.n_ot + 15) / 16;
-  // The tensor-core accumulator adds with truncation, so a long chain of MMAs into one accumulator drifts
-  // (~N ulp for N MMAs, all in one direction for same-sign data).  The MMAs therefore accumulate only
-  // XBLK blocks at a time (1: every block, with fresh accumulators); each partial sum is then added to `acc`
-  // with a round-to-nearest FADD.
-  constexpr int XBLK = 1;
-  float acc[NJ][4], part[NJ][4];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q] = part[j][q] = 0.f;
-  int nblk = 0;
-  const int cl = c0 + NJ * g;                              // this lane's NJ source columns
-  const bool cfull = cl + NJ <= a.n_is && ((a.src_pitch & 3) == 0);
-  for (int e = e0; e < e1; ++e) {
-    const Term term = a.terms[e];
-    const float* src = a.src + term.src_off + cl;
-    const bool vec = cfull && ((term.src_off & 3) == 0);
-    const size_t ti = (size_t)term.t_tab * ntile + ty;
-    const int q0 = __ldg(a.t_xoff + ti), q1 = __ldg(a.t_xoff + ti + 1);
-#pragma unroll 2
-    for (int q = q0; q < q1; ++q) {
-      const int k0 = __ldg(a.t_xk + q);
-      const float4 ah = __ldg(a.t_xa + 2 * ((size_t)q * 32 + lane));
-      const float4 al = __ldg(a.t_xa + 2 * ((size_t)q * 32 + lane) + 1);
-      const uint32_t Ah[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z), __float_as_uint(ah.w)};
-      const uint32_t Al[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z), __float_as_uint(al.w)};
-      const int ka = k0 + tq, kb = k0 + tq + 4;
-      const bool ina = ka >= a.win_r0 && ka < a.win_r1, inb = kb >= a.win_r0 && kb < a.win_r1;
-      const float* pa = src + (size_t)ka * a.src_pitch;
-      const float* pb = src + (size_t)kb * a.src_pitch;
-      float bv0[NJ], bv1[NJ];
-      if (vec) {
-#pragma unroll
-        for (int v = 0; v < NJ / 4; ++v) {
-          const float4 u0 = ina ? __ldg(reinterpret_cast<const float4*>(pa) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float4 u1 = inb ? __ldg(reinterpret_cast<const float4*>(pb) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-          bv0[4 * v] = u0.x; bv0[4 * v + 1] = u0.y; bv0[4 * v + 2] = u0.z; bv0[4 * v + 3] = u0.w;
-          bv1[4 * v] = u1.x; bv1[4 * v + 1] = u1.y; bv1[4 * v + 2] = u1.z; bv1[4 * v + 3] = u1.w;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const bool cin = cl + j < a.n_is;
-          bv0[j] = (ina && cin) ? __ldg(pa + j) : 0.f;
-          bv1[j] = (inb && cin) ? __ldg(pb + j) : 0.f;
-        }
-      }
-      // 3xTF32 split of the source: hi = truncation to tf32 (exact), lo = the exact fp32 remainder; the three
-      // products are issued tile-interleaved so consecutive MMAs never share an accumulator
-      uint32_t h0[NJ], h1[NJ], l0[NJ], l1[NJ];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        h0[j] = __float_as_uint(bv0[j]) & 0xffffe000u;
-        h1[j] = __float_as_uint(bv1[j]) & 0xffffe000u;
-        l0[j] = __float_as_uint(bv0[j] - __uint_as_float(h0[j]));
-        l1[j] = __float_as_uint(bv1[j] - __uint_as_float(h1[j]));
-      }
-      if (XBLK == 1) {
-        // fresh tensor-core accumulators per block, in groups of 4 tiles (few live registers), then RN adds
-#pragma unroll
-        for (int j0 = 0; j0 < NJ; j0 += 4) {
-          float pp[4][4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) pp[j][c] = 0.f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Al, h0[j0 + j], h1[j0 + j]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Ah, l0[j0 + j], l1[j0 + j]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) mma_tf32(pp[j], Ah, h0[j0 + j], h1[j0 + j]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[j0 + j][c] += pp[j][c];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Al, h0[j], h1[j]);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Ah, l0[j], l1[j]);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) mma_tf32(part[j], Ah, h0[j], h1[j]);
-        if (++nblk == XBLK) {
-          nblk = 0;
-#pragma unroll
-          for (int j = 0; j < NJ; ++j)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              acc[j][c] += part[j][c];
-              part[j][c] = 0.f;
-            }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NJ; ++j)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[j][c] += part[j][c];
-  // C fragment of tile j: (row g, n 2tq / 2tq+1) and (row g+8, ...) -> columns c0 + 2 NJ tq + j and
-  // c0 + 2 NJ tq + NJ + j: a lane's 2 NJ consecutive columns per row
-  float* outb = a.out + (size_t)b * a.out_stride;
-  const int r0 = 16 * ty + g;
-  const int cw = c0 + 2 * NJ * tq;
-  const bool ovec = cw + 2 * NJ <= a.n_os && ((a.out_pitch & 3) == 0) && ((a.out_stride & 3) == 0);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int row = r0 + 8 * h;
-    if (row >= a.n_ot) continue;
-    float v[2 * NJ];
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      v[j] = a.out_scale * acc[j][2 * h];
-      v[NJ + j] = a.out_scale * acc[j][2 * h + 1];
-    }
-    float* p = outb + (size_t)row * a.out_pitch + cw;
-    if (ovec) {
-#pragma unroll
-      for (int k = 0; k < NJ / 2; ++k) {
-        float4 o = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-        if (a.accumulate) {
-          const float4 qv = reinterpret_cast<float4*>(p)[k];
-          o.x += qv.x; o.y += qv.y; o.z += qv.z; o.w += qv.w;
-        }
-        reinterpret_cast<float4*>(p)[k] = o;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 2 * NJ; ++k)
-        if (cw + k < a.n_os) p[k] = a.accumulate ? p[k] + v[k] : v[k];
-    }
-  }
-}
-
 template <int TS, int TT, int NT>
 static lfm_status launch_band_f(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr, int tout) {
   if (tout) {
@@ -1884,40 +1288,6 @@ static lfm_status launch_band_m(const SepArgs& a, dim3 grid, cudaStream_t s, std
   return cuda_check(cudaGetLastError(), "band_m_kernel launch", err);
 }
 
-template <int TS, int TT, int NT>
-static lfm_status launch_band_g(const SepArgs& a, dim3 grid, cudaStream_t s, std::string& err, int unr) {
-  if (unr == 8)
-    band_g_kernel<TS, TT, NT, 8><<<grid, NT, 0, s>>>(a);
-  else
-    band_g_kernel<TS, TT, NT, 4><<<grid, NT, 0, s>>>(a);
-  ++g_launches;
-  return cuda_check(cudaGetLastError(), "band_g_kernel launch", err);
-}
-
-template <int TS, int TT, int NCW, int STAGES>
-static lfm_status launch_band_t(const SepArgs& a, dim3 grid, size_t smem, cudaStream_t s, std::string& err) {
-  auto kern = band_t_kernel<TS, TT, NCW, STAGES>;
-  static bool configured_dev[LFM_MAX_DEV];
-  bool& configured = configured_dev[cur_dev()];
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(band_t_kernel)", err);
-    configured = true;
-  }
-  kern<<<grid, (NCW + 1) * 32, smem, s>>>(a);
-  ++g_launches;
-  return cuda_check(cudaGetLastError(), "band_t_kernel launch", err);
-}
-
-// shared memory of the streaming kernel (must match band_t_kernel's slot layout)
-size_t band_t_smem(const SepOp& op) {
-  size_t slot = (size_t)op.ft_max * op.ts + ((size_t)op.wt_max + 3) / 4 * 4 + 8 * (size_t)(op.tt / 4);
-  return slot * 4 * op.stages;
-}
-
-// Batched transpose: out[b][c][r] = in[b][r][c] (r < R, c < C), 32x32 tiles through shared memory
-// (padded against bank conflicts), coalesced on both sides.  Used to move the collapsed path's
-// intermediates between row-major orders (pure data movement, no arithmetic).
 __global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int R,
                                                         int C, long long in_bs, long long in_pitch, long long out_bs,
                                                         long long out_pitch) {
@@ -2118,12 +1488,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   a.out_stride = op.out_stride ? op.out_stride : (long long)op.n_os * op.n_ot;
   a.src_pitch = op.src_pitch ? op.src_pitch : op.n_is;
   a.out_pitch = op.out_pitch ? op.out_pitch : op.n_os;
-  a.chunks = reinterpret_cast<const int2*>(op.d_chunks);
-  a.chunk_w = reinterpret_cast<const int2*>(op.d_chunk_w);
-  a.chunk_off = op.d_chunk_off;
-  a.t_xoff = op.ft->d_xoff;
-  a.t_xk = op.ft->d_xk;
-  a.t_xa = reinterpret_cast<const float4*>(op.ft->d_xa);
   a.t_foff = op.ft->d_foff;
   a.t_frow = reinterpret_cast<const int4*>(op.ft->d_frow);
   a.t_fw = reinterpret_cast<const float4*>(op.ft->d_fw);
@@ -2168,40 +1532,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
   cudaStream_t s = (cudaStream_t)stream;
   if (op.tout && op.kind != 3 && op.kind != 5) {
     err = "transposed output needs the band_m or band_f kernel";
-    return LFM_E_INVALID;
-  }
-  if (op.kind == 1) {
-    // streaming t-pass: identity s, whole windows, 16-byte aligned rows (checked at tuning time)
-    const size_t smem = band_t_smem(op);
-#define LFM_BT_CASE(TS_, TT_, NCW_)                                                                  \
-    if (op.ts == TS_ && op.tt == TT_) {                                                              \
-      switch (op.stages) {                                                                           \
-        case 2: return launch_band_t<TS_, TT_, NCW_, 2>(a, grid, smem, s, err);                      \
-        case 3: return launch_band_t<TS_, TT_, NCW_, 3>(a, grid, smem, s, err);                      \
-        default: return launch_band_t<TS_, TT_, NCW_, 4>(a, grid, smem, s, err);                     \
-      }                                                                                              \
-    }
-    LFM_BT_CASE(128, 64, 8)
-    LFM_BT_CASE(128, 32, 8)
-    LFM_BT_CASE(64, 64, 8)
-    LFM_BT_CASE(64, 32, 4)
-    LFM_BT_CASE(32, 32, 2)
-#undef LFM_BT_CASE
-    err = "unsupported band_t tile";
-    return LFM_E_INVALID;
-  }
-  if (op.kind == 2) {
-    // L2-gather t-pass: identity s, no shared memory
-#define LFM_BG_CASE(TS_, TT_, NT_) \
-    if (op.ts == TS_ && op.tt == TT_ && op.nt == NT_) return launch_band_g<TS_, TT_, NT_>(a, grid, s, err, op.stages);
-    LFM_BG_CASE(128, 32, 256)
-    LFM_BG_CASE(128, 64, 256)
-    LFM_BG_CASE(128, 16, 128)
-    LFM_BG_CASE(64, 32, 128)
-    LFM_BG_CASE(64, 64, 256)
-    LFM_BG_CASE(32, 32, 64)
-#undef LFM_BG_CASE
-    err = "unsupported band_g tile";
     return LFM_E_INVALID;
   }
   if (op.kind == 8) {
@@ -2290,23 +1620,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     }
     return cuda_check(cudaGetLastError(), "band_u_kernel launch", err);
   }
-  if (op.kind == 7) {
-    if (!op.ft->d_xoff || op.tout) { err = "band_x: needs the tensor-core form and normal output"; return LFM_E_INVALID; }
-    // grid: x = column groups of ts (= warps x 8 NJ), y = 16-row tiles; op.stages = NJ (n8 tiles per warp)
-    const int nw = op.nt / 32;
-    dim3 gx((op.n_is + op.ts - 1) / op.ts, (r1 + 15) / 16 - r0 / 16, n_out);
-    a.ty0 = r0 / 16;
-    if (op.ts != nw * 8 * op.stages) { err = "band_x: ts must be warps x 8 x NJ"; return LFM_E_INVALID; }
-    // minimum resident CTAs per SM: ~128 registers per thread for NJ 8, ~80 for NJ 4
-    if (op.stages == 8 && nw == 4) band_x_kernel<4, 8, 4><<<gx, 128, 0, s>>>(a);
-    else if (op.stages == 8 && nw == 2) band_x_kernel<2, 8, 8><<<gx, 64, 0, s>>>(a);
-    else if (op.stages == 4 && nw == 4) band_x_kernel<4, 4, 6><<<gx, 128, 0, s>>>(a);
-    else if (op.stages == 4 && nw == 8) band_x_kernel<8, 4, 3><<<gx, 256, 0, s>>>(a);
-    else if (op.stages == 4 && nw == 2) band_x_kernel<2, 4, 12><<<gx, 64, 0, s>>>(a);
-    else { err = "unsupported band_x configuration"; return LFM_E_INVALID; }
-    ++g_launches;
-    return cuda_check(cudaGetLastError(), "band_x_kernel launch", err);
-  }
   if (op.kind == 5) {
     if (!op.ft->d_foff) { err = "band_f: t family has no flat MSEG form"; return LFM_E_INVALID; }
 #define LFM_BF_CASE(TS_, TT_, NT_) \
@@ -2318,21 +1631,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     LFM_BF_CASE(64, 16, 64)
 #undef LFM_BF_CASE
     err = "unsupported band_f tile";
-    return LFM_E_INVALID;
-  }
-  if (op.kind == 4) {
-    // streamed MSEG t-pass: TS = 128, tt = 4 * NG; unit term scales (checked at tuning time)
-    if (!op.d_chunks) { err = "band_s: chunk lists missing"; return LFM_E_INVALID; }
-#define LFM_BS_CASE(NG_, K_, ST_) \
-    if (op.tt == 4 * NG_ && op.chunk == K_ && op.stages == ST_) return launch_band_s<NG_, K_, ST_>(a, grid, s, err);
-    LFM_BS_CASE(4, 32, 4)
-    LFM_BS_CASE(8, 32, 4)
-    LFM_BS_CASE(4, 64, 3)
-    LFM_BS_CASE(8, 64, 3)
-    LFM_BS_CASE(16, 32, 4)
-    LFM_BS_CASE(8, 16, 6)
-#undef LFM_BS_CASE
-    err = "unsupported band_s configuration";
     return LFM_E_INVALID;
   }
   if (op.kind == 3) {
@@ -2981,10 +2279,8 @@ namespace lfm {
 // zero-filled scratch buffers with CUDA events and keeps the fastest.  It runs only with LFM_AUTOTUNE=1; the
 // default is the fixed tcgen05 choice of tc_defaults (no timed launches at plan creation).
 static void free_sep_dev(SepOp& op) {
-  dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t); dfree(op.d_chunks); dfree(op.d_chunk_off);
-  dfree(op.d_chunk_w);
+  dfree(op.d_terms); dfree(op.d_offs); dfree(op.d_fp_s); dfree(op.d_fp_t);
   op.d_terms = nullptr; op.d_offs = nullptr; op.d_fp_s = nullptr; op.d_fp_t = nullptr;
-  op.d_chunks = nullptr; op.d_chunk_off = nullptr; op.d_chunk_w = nullptr;
 }
 
 // Optional result cache (LFM_TUNE_FILE): lines "<key> <op> ts tt nt nb stage"; a hit skips the timing
@@ -3141,60 +2437,6 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     float best = 1e30f;
     int bkind = keep.kind, bstages = keep.stages, bmgrp = keep.mgrp, bchunk = keep.chunk;
     if (op.s_ident && (op.n_is % 4) == 0) {
-      for (auto& c : cand) {
-        if (op.tout) break;  // transposed output: band_m only
-        for (int stages : {2, 3, 4}) {
-          op.kind = 1; op.ts = c[0]; op.tt = c[1]; op.stages = stages; op.nb = 1; op.stage = 1;
-          op.nt = c[0] == 32 ? 96 : (c[0] == 64 && c[1] == 32 ? 160 : 288);
-          fill_sep_geometry(op);
-          bool aligned = true;
-          for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
-          if (!aligned || band_t_smem(op) > (size_t)200 * 1024) continue;
-          free_sep_dev(op);
-          size_t bytes = 0;
-          if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
-          float ms = 0, tot = 0;
-          bool ok = true;
-          for (int rep = 0; rep < 3 && ok; ++rep) {
-            cudaEventRecord(e0, 0);
-            ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
-            cudaEventRecord(e1, 0);
-            cudaEventSynchronize(e1);
-            cudaEventElapsedTime(&ms, e0, e1);
-            if (rep > 0) tot += ms;
-          }
-          if (!ok || cudaGetLastError() != cudaSuccess) continue;
-          if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = op.nt; bnb = 1; bst = 1; bkind = 1; bstages = stages; }
-        }
-        if (st != LFM_OK) break;
-      }
-      op.kind = 0;
-      const int gcand[][3] = {{128, 32, 256}, {128, 64, 256}, {128, 16, 128}, {64, 32, 128}, {64, 64, 256}, {32, 32, 64}};
-      for (auto& c : gcand) {
-        if (st != LFM_OK || op.tout) break;
-        bool aligned = true;
-        for (const Term& t : op.terms) aligned &= (t.src_off % 4) == 0;
-        if (!aligned) break;
-        for (int unr : {4, 8}) {
-        op.kind = 2; op.ts = c[0]; op.tt = c[1]; op.nt = c[2]; op.nb = 1; op.stage = 0; op.stages = unr;
-        fill_sep_geometry(op);
-        free_sep_dev(op);
-        size_t bytes = 0;
-        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
-        float ms = 0, tot = 0;
-        bool ok = true;
-        for (int rep = 0; rep < 3 && ok; ++rep) {
-          cudaEventRecord(e0, 0);
-          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
-          cudaEventRecord(e1, 0);
-          cudaEventSynchronize(e1);
-          cudaEventElapsedTime(&ms, e0, e1);
-          if (rep > 0) tot += ms;
-        }
-        if (!ok || cudaGetLastError() != cudaSuccess) continue;
-        if (tot < best) { best = tot; bts = c[0]; btt = c[1]; bnt = c[2]; bnb = 1; bst = 0; bkind = 2; bstages = unr; }
-        }
-      }
       op.kind = 0;
       const int mcand[][4] = {{128, 32, 256, 4}, {128, 16, 128, 4}, {128, 8, 64, 4},  {64, 32, 128, 4},
                               {64, 16, 64, 4},   {32, 32, 64, 4},   {128, 32, 128, 8}, {128, 16, 64, 8},
@@ -3259,35 +2501,6 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         }
       }
       op.kind = 0;
-      // band_x: tensor cores (one-table MMA form, unit scales, normal output)
-      const int xcand[][2] = {{128, 8}, {64, 8}, {128, 4}, {256, 4}, {64, 4}};  // threads, NJ
-      for (auto& xc : xcand) {
-        const int nt = xc[0], nj = xc[1];
-        if (st != LFM_OK || op.ft->x_off.empty() || op.tout) break;
-        bool unit = true;
-        for (const Term& t : op.terms) unit &= t.scale == 1.f;
-        if (!unit) break;
-        op.kind = 7; op.ts = (nt / 32) * 8 * nj; op.tt = 16; op.nt = nt; op.nb = 1; op.stage = 0; op.stages = nj;
-        op.mgrp = 4;
-        fill_sep_geometry(op);
-        free_sep_dev(op);
-        size_t bytes = 0;
-        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
-        float ms = 0, tot = 0;
-        bool ok = true;
-        for (int rep = 0; rep < 3 && ok; ++rep) {
-          cudaEventRecord(e0, 0);
-          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
-          cudaEventRecord(e1, 0);
-          cudaEventSynchronize(e1);
-          cudaEventElapsedTime(&ms, e0, e1);
-          if (rep > 0) tot += ms;
-        }
-        if (!ok || cudaGetLastError() != cudaSuccess) continue;
-        if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_x nt %3d NJ %d: %.3f ms\n", names[q], nt, nj, tot / 2);
-        if (tot < best) { best = tot; bts = op.ts; btt = 16; bnt = nt; bnb = 1; bst = 0; bkind = 7; bstages = nj; bmgrp = 4; }
-      }
-      op.kind = 0;
       // band_u: tcgen05 (one output, one term, normal output, 16-byte source rows); stages = drain group
       for (int grp : {4, 8}) {
         const long long sp = op.src_pitch ? op.src_pitch : op.n_is;
@@ -3313,37 +2526,6 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
         if (dbg_all) std::fprintf(stderr, "[lfm]   %-7s band_u group %d: %.3f ms\n", names[q], grp, tot / 2);
         // the second drain group must win by 2 % (ties otherwise flip between runs)
         if (tot < (grp == 4 ? best : 0.98f * best)) { best = tot; bts = 256; btt = 128; bnt = U_THREADS; bnb = 1; bst = 0; bkind = 8; bstages = grp; bmgrp = 4; }
-      }
-      op.kind = 0;
-      // band_s: streamed MSEG (TS 128, unit term scales, MSEG t family, normal output)
-      bool unit = true;
-      for (const Term& t : op.terms) unit &= t.scale == 1.f && (t.src_off % 4) == 0;
-      const int scand[][3] = {{4, 32, 4}, {8, 32, 4}, {4, 64, 3}, {8, 64, 3}, {16, 32, 4}, {8, 16, 6}};
-      for (auto& c : scand) {
-        if (st != LFM_OK || !op.ft->want_mseg || op.tout || !unit) break;
-        op.kind = 4; op.ts = 128; op.tt = 4 * c[0]; op.nt = (c[0] + 1) * 32; op.chunk = c[1]; op.stages = c[2];
-        op.nb = 1; op.stage = 0; op.mgrp = 4;
-        fill_sep_geometry(op);
-        free_sep_dev(op);
-        size_t bytes = 0;
-        if ((st = upload_sep(op, bytes, err)) != LFM_OK) break;
-        float ms = 0, tot = 0;
-        bool ok = true;
-        for (int rep = 0; rep < 3 && ok; ++rep) {
-          cudaEventRecord(e0, 0);
-          ok = launch_sep(op, src, out, 0, n_out, 0, nullptr, err) == LFM_OK;
-          cudaEventRecord(e1, 0);
-          cudaEventSynchronize(e1);
-          cudaEventElapsedTime(&ms, e0, e1);
-          if (rep > 0) tot += ms;
-        }
-        if (!ok || cudaGetLastError() != cudaSuccess) continue;
-        if (dbg_all)
-          std::fprintf(stderr, "[lfm]   %-7s band_s NG %2d chunk %2d stages %d: %.3f ms\n", names[q], c[0], c[1], c[2], tot / 2);
-        if (tot < best) {
-          best = tot; bts = 128; btt = 4 * c[0]; bnt = (c[0] + 1) * 32; bnb = 1; bst = 0; bkind = 4; bstages = c[2];
-          bmgrp = 4; bchunk = c[1];
-        }
       }
       op.kind = 0;
     }
@@ -3384,7 +2566,7 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err) {
     op_best[q] = best * (float)op.n_out / (float)n_out;  // per launch over all outputs
     if (dbg)
       std::fprintf(stderr, "[lfm] autotune %-7s -> %s tile %3dx%-3d nt %3d nb %d stage %d stages %d grp %d (%.3f ms for %d outputs)\n",
-                   names[q], op.kind == 1 ? "band_t" : op.kind == 2 ? "band_g" : op.kind == 3 ? "band_m" : op.kind == 4 ? "band_s" : op.kind == 5 ? "band_f" : op.kind == 7 ? "band_x" : op.kind == 8 ? "band_u" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
+                   names[q], op.kind == 3 ? "band_m" : op.kind == 5 ? "band_f" : op.kind == 8 ? "band_u" : "sep   ", op.ts, op.tt, op.nt, op.nb, op.stage, op.stages, op.mgrp, best / 2, n_out);
     if (tfile && st == LFM_OK) {
       if (FILE* f = std::fopen(tfile, "a")) {
         std::fprintf(f, "%s %s %d %d %d %d %d %d %d %.6f %d %d\n", key.c_str(), names[q], op.ts, op.tt, op.nt, op.nb,

@@ -61,14 +61,6 @@ struct BandFamily {
   int32_t* d_foff = nullptr;
   int32_t* d_frow = nullptr;
   float* d_fw = nullptr;
-  // tensor-core form (band_x): per tile of 16 rows, the union of the rows' supports cut into blocks of 8
-  // source cells; per block the 16x8 weights split into tf32 hi + lo parts in mma.m16n8k8 A-fragment order
-  // (per lane: hi[4], lo[4])
-  std::vector<int32_t> x_off, x_k;         // x_off[tile] .. +1 into blocks; x_k[block] = first source cell
-  std::vector<float> x_a;                  // 256 floats per block
-  int32_t* d_xoff = nullptr;
-  int32_t* d_xk = nullptr;
-  float* d_xa = nullptr;
   // tcgen05 form (band_u): per tile of 128 rows the union of the rows' supports cut into blocks of 16 source
   // cells; per block two 128 x 16 tf32 weight images (hi, lo) in the shared-memory layout the MMA reads
   std::vector<int32_t> u_off, u_k0;        // u_off[table * n_tiles + tile] .. +1 into blocks; u_k0[block]
@@ -122,22 +114,17 @@ struct SepOp {
   int nb = 1;                      // terms staged per barrier
   int stage = 1;                   // stage the source footprint in smem (0: pass 1 reads L1/L2)
   int s_ident = 0;                 // the s family is the identity (pass 1 = copy into U)
-  int kind = 0;                    // 0: sep_kernel, 1: band_t_kernel (streaming t-pass, identity s), 2: band_g_kernel (L2 gather),
+  int kind = 0;                    // 0: sep_kernel,
                                    // 3: band_m_kernel (L2 gather over MSEG segments of ft)
-                                   // 4: band_s_kernel (MSEG segments, source rows streamed through smem)
                                    // 5: band_f_kernel (flat MSEG entry lists, L2 gather, deep unroll)
-                                   // 7: band_x_kernel (tensor cores: mma.sync m16n8k8 3xTF32 over 16-row blocks)
                                    // 8: band_u_kernel (tcgen05 kind::tf32 3xTF32, 128-row tiles, TMA, TMEM)
   long long src_pitch = 0;         // floats between source rows (0: n_is)
   long long out_pitch = 0;         // floats between output rows (0: n_os)
   long long out_stride = 0;        // floats between outputs b (0: n_os * n_ot)
   int tout = 0;                    // band_m only: write element (row, col) at col * out_pitch + row
   int mgrp = 4;                    // band_m only: rows per MSEG group (4 or 8)
-  int chunk = 32;                  // band_s only: source rows per streamed chunk
-  int32_t* d_chunks = nullptr;     // band_s: per (t-table, tile_y) list of {first row, rows} chunk pairs
-  int32_t* d_chunk_off = nullptr;  //         offsets into d_chunks, size n_tables * nty + 1
-  int32_t* d_chunk_w = nullptr;    //         per (chunk, group of the tile): {first weight float4, count}
-  int stages = 2;                  // band_t pipeline depth
+  int chunk = 32;                  // (unused, kept in the tune-cache line format)
+  int stages = 2;                  // band_m / band_f unroll; band_u drain group
   int wt_max = 0;                  // max G4 weight floats of one t tile
   int ws_max = 0;                  // max G4 weight floats of one s tile
   int nbuf = 2;                    // 2: double-buffered chunks, 1: one chunk per output
@@ -232,7 +219,6 @@ namespace lfm {
 void ell_footprint(const BandFamily& f, int tab, int tile, int t, int& lo, int& width);
 void g4_tile(const BandFamily& f, int tab, int tile, int t, int& lo, int& width, int& woff, int& wlen);
 size_t sep_smem(const SepOp& op, int nb);
-size_t band_t_smem(const SepOp& op);
 void fill_sep_geometry(SepOp& op);
 bool sep_choose_tile(SepOp& op);
 lfm_status autotune_camera(CameraPlan& cp, std::string& err);

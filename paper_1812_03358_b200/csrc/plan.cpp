@@ -377,65 +377,6 @@ static float tf32_round(float v) {
   return r;
 }
 
-// Tensor-core form of a one-table family (band_x): tiles of 16 rows; the union of the rows' non-zero
-// source cells covered by the fewest blocks of 8 consecutive cells; per block the
-// fp32 weights (one rounding from fp64) split as w = hi + lo + O(2^-22 w) with hi, lo tf32, laid out per
-// lane of mma.m16n8k8 (row-major A: a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]).
-static void build_mma(BandFamily& f) {
-  const int nt = (f.n_rows + 15) / 16;
-  f.x_off.assign((size_t)f.n_tables * nt + 1, 0);
-  f.x_k.clear();
-  f.x_a.clear();
-  std::vector<char> any;
-  std::vector<float> A;
-  for (int m = 0; m < f.n_tables; ++m)
-    for (int t = 0; t < nt; ++t) {
-      f.x_off[(size_t)m * nt + t] = (int)f.x_k.size();
-      const int r0 = 16 * t, r1 = std::min(f.n_rows, r0 + 16);
-      int lo = 1 << 30, hi = -1;
-      for (int r = r0; r < r1; ++r) {
-        size_t idx = (size_t)m * f.n_rows + r;
-        if (!f.len[idx]) continue;
-        lo = std::min(lo, (int)f.start[idx]);
-        hi = std::max(hi, (int)(f.start[idx] + f.len[idx]));
-      }
-      if (hi < 0) continue;
-      any.assign(hi - lo, 0);
-      for (int r = r0; r < r1; ++r) {
-        size_t idx = (size_t)m * f.n_rows + r;
-        for (int e = 0; e < f.len[idx]; ++e)
-          if (f.w64[idx * f.taps + e] != 0.0) any[f.start[idx] + e - lo] = 1;
-      }
-      auto weight = [&](int r, int k) -> float {  // fp32 weight of row r at source k (0 outside the band)
-        if (r >= r1) return 0.f;
-        size_t idx = (size_t)m * f.n_rows + r;
-        const int e = k - f.start[idx];
-        if (e < 0 || e >= f.len[idx]) return 0.f;
-        return (float)f.w64[idx * f.taps + e];
-      };
-      // fewest blocks of 8 consecutive source cells covering every non-zero column: greedy interval cover
-      // (a block starts at the first non-zero column not yet covered)
-      const int W = hi - lo;
-      std::vector<int> starts;
-      for (int p = 0; p < W; ++p)
-        if (any[p] && (starts.empty() || p >= starts.back() + 8)) starts.push_back(p);
-      for (int a0 : starts) {
-        {
-          const int k0 = lo + a0;
-          f.x_k.push_back(k0);
-          for (int lane = 0; lane < 32; ++lane) {
-            const int g = lane / 4, tq = lane % 4;
-            const float v[4] = {weight(r0 + g, k0 + tq), weight(r0 + g + 8, k0 + tq), weight(r0 + g, k0 + tq + 4),
-                                weight(r0 + g + 8, k0 + tq + 4)};
-            for (int q = 0; q < 4; ++q) f.x_a.push_back(tf32_round(v[q]));
-            for (int q = 0; q < 4; ++q) f.x_a.push_back(tf32_round(v[q] - tf32_round(v[q])));
-          }
-        }
-      }
-    }
-  f.x_off[(size_t)f.n_tables * nt] = (int)f.x_k.size();
-}
-
 // tcgen05 form of a one-table family (band_u, band_u.cuh): tiles of 128 rows; the union of the rows'
 // non-zero source cells covered by the fewest blocks of 16 consecutive cells (greedy); per block the fp32
 // weights (one rounding from fp64) split as w = hi + lo + O(2^-22 w), hi = rn_tf32(w), lo = rn_tf32(w - hi),
@@ -1492,7 +1433,6 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   cp.ca1n.want_mseg = 1;
   make_rows_by_slice(cp.ca1n, cp.ca[1]);
   build_mseg8(cp.ca1n);
-  build_mma(cp.ca1n);
   if (nz % 64 == 0 && !std::getenv("LFM_UMMA_ROWS128")) {
     cp.ca1n.u_mode = 1;
     cp.ca1n.u_nz = nz;
@@ -1501,7 +1441,6 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
   cp.cf1n.want_mseg = 1;
   make_cols_by_slice(cp.cf1n, cp.cf[1]);
   build_mseg8(cp.cf1n);
-  build_mma(cp.cf1n);
   build_umma(cp.cf1n);
   if (std::getenv("LFM_DEBUG")) {
     const BandFamily* fs[] = {&cp.ca1n, &cp.cf1n, &cp.ca[1], &cp.cf[1], &cp.ca[0], &cp.cf[0]};
@@ -1514,8 +1453,8 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     for (const BandFamily* f : {&cp.ca1n, &cp.cf1n}) {
       double nnz = 0;
       for (int v : f->cnt) nnz += v;
-      std::fprintf(stderr, "[lfm] tensor-core form: %zu blocks of 16x8, density %.3f\n", f->x_k.size(),
-                   nnz / (128.0 * f->x_k.size()));
+      std::fprintf(stderr, "[lfm] tcgen05 form: %zu blocks of 128x16, density %.3f\n", f->u_k0.size(),
+                   nnz / (2048.0 * f->u_k0.size()));
     }
     for (int G : {4, 8, 16})
       std::fprintf(stderr, "[lfm] MSEG density with %2d-row groups: ca1n %.3f  cf1n %.3f  ca0 %.3f  cf0 %.3f\n", G,
@@ -1661,20 +1600,18 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     // tuning hook: LFM_FORCE_<op>=ts,tt,nt,nb,stage overrides the cost model (sweeps, tools/)
     std::string env = std::string("LFM_FORCE_") + names[q];
     if (const char* f = std::getenv(env.c_str())) {
-      // optional 6th/7th fields: kind (1 = streaming band_t kernel, identity-s ops only), stages
+      // optional 6th/7th fields: kind (3 = band_m L2 gather over MSEG segments, 5 = band_f flat entries, 8 = band_u
+      // tcgen05; identity-s ops only), stages (unroll, or band_u's drain group), MSEG group rows
       int ts, tt, nt, nb, stg, kind = 0, stages = 2, mg = 4, chk = 32;
       if (std::sscanf(f, "%d,%d,%d,%d,%d,%d,%d,%d,%d", &ts, &tt, &nt, &nb, &stg, &kind, &stages, &mg, &chk) >= 5) {
         SepOp& op = *ops[q];
         op.ts = ts; op.tt = tt; op.nt = nt; op.nb = nb; op.stage = stg; op.kind = kind; op.stages = stages; op.mgrp = mg;
-        op.chunk = chk;
         fill_sep_geometry(op);
         if (kind >= 1) {
-          bool ok = op.s_ident && op.n_is % 4 == 0 && (kind != 1 || band_t_smem(op) <= (size_t)200 * 1024) &&
-                    (kind < 3 || op.ft->want_mseg) && (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty())) &&
-                    (kind != 4 || (ts == 128 && !op.tout)) && (kind != 5 || !op.ft->f_off.empty()) &&
-                    (kind != 7 || (!op.ft->x_off.empty() && !op.tout)) &&
+          bool ok = (kind == 3 || kind == 5 || kind == 8) && op.s_ident && op.n_is % 4 == 0 && op.ft->want_mseg &&
+                    (mg == 4 || (kind == 3 && mg == 8 && !op.ft->m8_off.empty())) &&
+                    (kind != 5 || !op.ft->f_off.empty()) &&
                     (kind != 8 || (!op.ft->u_off.empty() && !op.tout && op.n_out == 1 && op.terms.size() == 1));
-          for (const Term& t : op.terms) ok &= (kind != 4 && kind != 7) || t.scale == 1.f;
           for (const Term& t : op.terms) ok &= (t.src_off % 4) == 0;
           if (!ok) { err = env + ": kernel kind not applicable"; return LFM_E_INVALID; }
         } else if (sep_smem(op, nb) > (size_t)220 * 1024) {

@@ -45,9 +45,9 @@ def test_rows_entry_points(name, path):
         assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL
 
 
-# band_t: ts,tt,nt,nb,stage,kind=1,stages ; band_g (2-segment G4) kind=2 / band_m (MSEG) kind=3 with
-# unroll and MSEG group rows ; band_s (streamed MSEG) kind=4 with stages, 4, chunk rows ; band_f (flat
-# MSEG entries) kind=5 with unroll ; band_u (tcgen05 3xTF32, 128-row tiles) kind=8, stages = drain group ; band_x (tensor cores, 3xTF32) kind=7, stages = NJ n8 tiles per warp, ts = warps x 8 NJ, tt = 16 ; sep: MODE variants (stage 1 = staged U, 0 = U from L2)
+# ts,tt,nt,nb,stage,kind,stages[,mseg rows]: band_m (MSEG L2 gather) kind=3 with unroll and MSEG group rows ;
+# band_f (flat MSEG entries) kind=5 with unroll ; band_u (tcgen05 3xTF32, 128-row tiles) kind=8, stages = drain
+# group ; sep: MODE variants (stage 1 = staged U, 0 = U from L2)
 VARIANTS = {
     "band_m_128x16_u4": "128,16,128,1,0,3,4",
     "band_m_128x32_u8": "128,32,256,1,0,3,8",
@@ -55,22 +55,11 @@ VARIANTS = {
     "band_m_32x32_u4": "32,32,64,1,0,3,4",
     "band_m8_128x32_u4": "128,32,128,1,0,3,4,8",
     "band_m8_64x32_u8": "64,32,64,1,0,3,8,8",
-    "band_s_ng4_k32": "128,16,160,1,0,4,4,4,32",
     "band_f_128x16_u1": "128,16,128,1,0,5,1",
     "band_f_64x32_u2": "64,32,128,1,0,5,2",
-    "band_x_nt64_nj8": "128,16,64,1,0,7,8",
-    "band_x_nt128_nj8": "256,16,128,1,0,7,8",
-    "band_x_nt128_nj4": "128,16,128,1,0,7,4",
-    "band_x_nt256_nj4": "256,16,256,1,0,7,4",
     "band_u_g4": "256,128,384,1,0,8,4",
     "band_u_g1": "256,128,384,1,0,8,1",
     "band_u_g8": "256,128,384,1,0,8,8",
-    "band_s_ng8_k64": "128,32,288,1,0,4,3,4,64",
-    "band_s_ng8_k16": "128,32,288,1,0,4,6,4,16",
-    "band_g_128x32_u8": "128,32,256,1,0,2,8",
-    "band_g_64x32_u4": "64,32,128,1,0,2,4",
-    "band_t_128x32_s2": "128,32,288,1,1,1,2",
-    "band_t_32x32_s4": "32,32,96,1,1,1,4",
     "sep_64x32_l2": "64,32,128,1,0",
     "sep_32x32_staged": "32,32,64,1,1",
 }
