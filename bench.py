@@ -543,25 +543,34 @@ def run_ours(args, rank, world, local_rank):
                     h["y"][c].copy_(b["y"][c], non_blocking=True)
             h["g"].copy_(b["g"], non_blocking=True)
 
+        # uploads and downloads on two copy streams, so the two PCIe directions overlap each other and the compute
+        cs_out = torch.cuda.Stream()
         up = [torch.cuda.Event() for _ in range(n + 1)]
         done = [torch.cuda.Event() for _ in range(n)]
+        dl = [torch.cuda.Event() for _ in range(n)]
         cs.wait_stream(stream)
+        cs_out.wait_stream(stream)
         with torch.cuda.stream(cs):
             upload(0)
             up[0].record(cs)
         for i in range(n):
             stream.wait_event(up[i])
+            if i >= 2:
+                stream.wait_event(dl[i - 2])          # step i - 2's outputs in these buffers have been read
             b = dv[i % 2]
             step(b["x"], b["g"], b["y"], b["r"])
             done[i].record(stream)
             with torch.cuda.stream(cs):
                 if i + 1 < n:
                     if i >= 1:
-                        cs.wait_event(done[i - 1])     # buffers (i+1)%2 were step i-1's
+                        cs.wait_event(done[i - 1])     # inputs (i+1)%2 were step i-1's
                     upload(i + 1)
                     up[i + 1].record(cs)
-                cs.wait_event(done[i])
+            with torch.cuda.stream(cs_out):
+                cs_out.wait_event(done[i])
                 download(i)
+                dl[i].record(cs_out)
+        stream.wait_stream(cs_out)
         stream.wait_stream(cs)
         full_in = x.numel() * 4 + (sum(rs[c].numel() for c in cams_) * 4 if full else 0)
         full_out = n_vox * 4 + (sum(ys[c].numel() for c in cams_) * 4 if full else 0)

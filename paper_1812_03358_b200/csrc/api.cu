@@ -588,7 +588,7 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
   if (stage == LFM_STAGE_FWD_T) {
     if (!cp.fwd_split) return fail(LFM_E_INVALID, "collapsed forward of this camera is not in two-pass form");
     if (!out) return fail(LFM_E_INVALID, "out is NULL");
-    st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream);
+    st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream, 0, -1, 0, -1, 0, -1, w.zt, cp.ws_z);  // as in A_forward
   } else if (stage == LFM_STAGE_ADJ_T) {
     if (!in) return fail(LFM_E_INVALID, "in is NULL");
     st = sep(cp.adj_c1, in, w.z, 0, 1, 0, stream);

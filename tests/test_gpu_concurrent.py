@@ -36,15 +36,15 @@ def test_concurrent_pair_matches_sequential(name):
     cfg = make_config(name)
     plan = lfm.Plan(cfg, device=0)
     ops = build_system(cfg)
-    items = [(c, 0, cam["n_t"]) for c, cam in enumerate(cfg["cameras"])]
+    items = [(c, 0, cam["n_t"], 0, cam["n_s"]) for c, cam in enumerate(cfg["cameras"])]
     x = dev(uniform_volume(cfg["volume"], 0)).reshape(-1)
     rs = [dev(uniform_vector(op.n_pix, 1 + c)) for c, op in enumerate(ops)]
     n_vox = ops[0].n_vox
     ws0 = plan.workspace()
     ys_a = [torch.empty(op.n_pix, device="cuda:0") for op in ops]
     g_a = torch.empty(n_vox, device="cuda:0")
-    PairRunner(items, lambda c, r0, r1, xv, y: lfm.A_forward_rows(plan, c, r0, r1, xv, y, ws0),
-               lambda c, r0, r1, r, g, acc: lfm.A_adjoint_rows(plan, c, r0, r1, r, g, ws0, accumulate=acc),
+    PairRunner(items, lambda c, w, xv, y: lfm.A_forward_window(plan, c, *w, xv, y, ws0),
+               lambda c, w, r, g, acc: lfm.A_adjoint_window(plan, c, *w, r, g, ws0, accumulate=acc),
                lambda g: g.zero_()).pair(x, ys_a, rs, g_a)
     streams = [torch.cuda.Stream() for _ in items]
     wss = [plan.workspace() for _ in items]
@@ -60,8 +60,8 @@ def test_concurrent_pair_matches_sequential(name):
 
     ys_b = [torch.full((op.n_pix,), float("nan"), device="cuda:0") for op in ops]
     g_b = torch.full((n_vox,), float("nan"), device="cuda:0")
-    ConcurrentPair(items, lambda i, c, r0, r1, xv, y: lfm.A_forward_rows(plan, c, r0, r1, xv, y, wss[i]),
-                   lambda i, c, r0, r1, r, g: lfm.A_adjoint_rows(plan, c, r0, r1, r, g, wss[i]),
+    ConcurrentPair(items, lambda i, c, w, xv, y: lfm.A_forward_window(plan, c, *w, xv, y, wss[i]),
+                   lambda i, c, w, r, g: lfm.A_adjoint_window(plan, c, *w, r, g, wss[i]),
                    lambda src, dst: lfm.vol_accumulate(src, dst), lambda g: g.zero_(), run,
                    lambda: [main.wait_stream(s) for s in streams], private).pair(x, ys_b, rs, g_b)
     torch.cuda.synchronize()
