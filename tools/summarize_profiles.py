@@ -61,11 +61,18 @@ def main():
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 agg[d["Kernel Name"][:90]][0] += 1
                 agg[d["Kernel Name"][:90]][1] += float(d["Metric Value"].replace(",", ""))
-    tot = sum(v[1] for v in agg.values())
+    ours = {k: v for k, v in agg.items() if "lfm::" in k}
+    tot = sum(v[1] for v in ours.values())
+    cmd = os.environ.get("LAUNCH_CMD", "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e")
     lines.append("# launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised:")
-    lines.append("# compare shares, not absolutes) of `python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e`")
-    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    lines.append(f"# compare shares, not absolutes) of `{cmd}`")
+    lines.append("# share = of the lfm:: kernels' total; other launches (torch fills / reductions: the L2 flush between")
+    lines.append("# steps, input init) are listed after, without a share")
+    for k, (n, t) in sorted(ours.items(), key=lambda x: -x[1][1]):
         lines.append(f"{n:4d} launches {t / 1e3:10.1f} us {100 * t / tot:5.1f}%  {k}")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        if k not in ours:
+            lines.append(f"{n:4d} launches {t / 1e3:10.1f} us     -   {k}")
     open(os.path.join(pdir, f"{rnd}_launches.txt"), "w").write("\n".join(lines) + "\n")
     summary = {}
     for rep in reps:
