@@ -44,12 +44,13 @@ struct DevGuard {
 };
 
 struct WsLayout {
-  size_t r0, r1, xt, f, s, s2, z, zt, p, total;
+  size_t r0, r1, xt, f, s, s2, z, zt, p, am, h16, total;
 };
 
 WsLayout layout(const lfm_plan_s* p) {
-  size_t V = 0, F = 0, S = 0, Z = 0;
+  size_t V = 0, F = 0, S = 0, Z = 0, P = 0;
   for (const CameraPlan& c : p->cams) {
+    P = std::max(P, (size_t)c.info.n_pix * 4);
     V = std::max(V, (size_t)c.info.n_vox * 4);
     F = std::max(F, c.ws_fields);
     Z = std::max(Z, c.ws_z);
@@ -65,13 +66,17 @@ WsLayout layout(const lfm_plan_s* p) {
   L.z = L.s2 + al256(S);
   L.zt = L.z + al256(Z);
   L.p = L.zt + al256(Z);
-  L.total = L.p + al256(4096 * 8 * 4);
+  L.am = L.p + al256(4096 * 8 * 4);
+  L.h16 = L.am + al256(LFM_AMAX_SLOTS * 4);
+  L.total = L.h16 + al256(P);
   return L;
 }
 
 struct Ws {
   float *r0, *r1, *xt, *f, *s, *s2, *z, *zt;
   double* p;
+  float* am;      // partial maxima of the 2xFP16 t-pass input's source: of x^r (forward), of y (adjoint)
+  uint16_t* h16;  // fp16 hi (n_pix) then lo (n_pix) of 2^e y: the adjoint t pass input in the 2xFP16 form
 };
 
 lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
@@ -89,6 +94,8 @@ lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
   w.xt = (float*)(b + L.xt);
   w.zt = (float*)(b + L.zt);
   w.p = (double*)(b + L.p);
+  w.am = (float*)(b + L.am);
+  w.h16 = (uint16_t*)(b + L.h16);
   return LFM_OK;
 }
 
@@ -167,10 +174,10 @@ lfm_status rotate_adj(const CameraPlan& cp, const float* in, float* out, int acc
 
 lfm_status sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int acc, void* stream,
                int out_r0 = 0, int out_r1 = -1, int win_r0 = 0, int win_r1 = -1, int out_c0 = 0, int out_c1 = -1,
-               float* part = nullptr, size_t part_bytes = 0) {
+               float* part = nullptr, size_t part_bytes = 0, F16Src amx = F16Src()) {
   std::string err;
   lfm_status st = launch_sep(op, src, out, b0, n_out, acc, stream, err, out_r0, out_r1, win_r0, win_r1, out_c0, out_c1,
-                             part, part_bytes);
+                             part, part_bytes, amx);
   return st == LFM_OK ? st : fail(st, err);
 }
 
@@ -179,6 +186,64 @@ struct Win {
   int r0 = 0, r1 = -1, c0 = 0, c1 = -1;
   bool cols(int n_s) const { return c0 > 0 || (c1 >= 0 && c1 < n_s); }
 };
+
+// 2xFP16 form of the tcgen05 t passes (band_u_kernel<., true>): the t-pass input is written pre-split into fp16
+// hi + lo by its producer (band_v forward / split16_kernel), scaled by 2^e from the maxima of its source (DESIGN
+// §6).  Default wherever the plan has the fp16 images and the detector rows are 16-byte aligned in fp16;
+// LFM_UMMA_TF32=1 selects the 3xTF32 form (A/B, tests).
+static bool f16_env() {
+  static const bool off = std::getenv("LFM_UMMA_TF32") != nullptr;
+  return !off;
+}
+static bool f16_fwd(const CameraPlan& cp, const SepOp& c2) {
+  return f16_env() && cp.fwd_split && cp.fwd_t == 3 && c2.kind == 8 && c2.ft->d_uh && cp.info.n_s % 8 == 0;
+}
+static bool f16_adj(const CameraPlan& cp, const SepOp& c1) {
+  return f16_env() && c1.kind == 8 && c1.ft->d_uh && cp.info.n_s % 8 == 0;
+}
+
+// One term of the collapsed forward: band_v s pass (T) into U, band_u t pass (c2) into y.  2xFP16: the maxima of
+// x^r (computed once per call, `amax_done`) set the scale with which band_v writes U as fp16 hi / lo.
+static lfm_status vt_forward(const CameraPlan& cp, const VTab& T, const SepOp& c2, const float* xr, float* y, int acc,
+                             const Ws& w, void* stream, Win win, bool& amax_done) {
+  std::string err;
+  lfm_status st;
+  if (f16_fwd(cp, c2)) {
+    if (!amax_done && (st = k_amax(xr, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
+    amax_done = true;
+    if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1, w.am)) != LFM_OK) return fail(st, err);
+    F16Src h;
+    h.hi = reinterpret_cast<const uint16_t*>(w.z);
+    h.lo = h.hi + (size_t)cp.cf[0].n_rows * cp.info.nz * cp.info.ny;
+    h.amax = w.am;
+    h.amax_scale = T.lsum;
+    return sep(c2, w.z, y, 0, 1, acc, stream, win.r0, win.r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z, h);
+  }
+  if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
+  return sep(c2, w.z, y, 0, 1, acc, stream, win.r0, win.r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z);
+}
+
+// The adjoint t pass (c1) of y's rows [r0, r1): 2xFP16 = maxima of those rows, fp16 hi / lo of 2^e y into w.h16
+// (done once per call, `split_done`), then band_u from them.
+static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* y, const Ws& w, void* stream, Win win,
+                            bool& split_done) {
+  if (!f16_adj(cp, c1)) return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1);
+  const int n_s = cp.info.n_s, r0 = std::max(0, win.r0), r1 = win.r1 < 0 ? cp.info.n_t : std::min(win.r1, cp.info.n_t);
+  const size_t np = (size_t)cp.info.n_pix;
+  if (!split_done && r1 > r0) {
+    std::string err;
+    const long long off = (long long)r0 * n_s, n = (long long)(r1 - r0) * n_s;
+    lfm_status st = k_amax(y + off, n, w.am, stream, err);
+    if (st == LFM_OK) st = k_split16(y + off, n, w.am, w.h16 + off, w.h16 + np + off, stream, err);
+    if (st != LFM_OK) return fail(st, err);
+  }
+  split_done = true;
+  F16Src h;
+  h.hi = w.h16;
+  h.lo = w.h16 + np;
+  h.amax = w.am;
+  return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1, nullptr, 0, h);
+}
 
 // the collapsed path runs on the tcgen05 kernels end to end (band_v s passes, band_u t passes), the form whose
 // kernels restrict themselves to a column window
@@ -206,23 +271,20 @@ lfm_status forward_impl(const CameraPlan& cp, int path, const float* x, float* y
   const bool plen = cp.info.type == LFM_PLENOPTIC;
   if (path == LFM_PATH_COLLAPSED && !cp.comps.empty()) {
     // non-separable lenslet stage: y = sum over terms of (band_v s pass, band_u t pass), terms >= 1 accumulated
-    std::string err;
-    lfm_status st = k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err, win.c0, win.c1);
-    if (st != LFM_OK) return fail(st, err);
-    TRY(sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream, r0, r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z));
-    for (const Component& cm : cp.comps) {
-      if ((st = k_vpass_fwd(cp, cm.vf, xr, w.z, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
-      TRY(sep(cm.fwd_c2, w.z, y, 0, 1, 1, stream, r0, r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z));
-    }
+    bool amax_done = false;
+    TRY(vt_forward(cp, cp.vf, cp.fwd_c2, xr, y, 0, w, stream, win, amax_done));
+    for (const Component& cm : cp.comps) TRY(vt_forward(cp, cm.vf, cm.fwd_c2, xr, y, 1, w, stream, win, amax_done));
     return LFM_OK;
   }
   if (path == LFM_PATH_COLLAPSED) {
     if (cp.fwd_split) {
-      if (cp.fwd_t == 2 || cp.fwd_t == 3) {
-        // direct s pass (spass_fwd_kernel, or band_v on the tensor cores): slices -> interleaved U
+      if (cp.fwd_t == 3) {  // band_v on the tensor cores: slices -> interleaved U, then band_u
+        bool amax_done = false;
+        return vt_forward(cp, cp.vf, cp.fwd_c2, xr, y, 0, w, stream, win, amax_done);
+      } else if (cp.fwd_t == 2) {
+        // direct s pass (spass_fwd_kernel): slices -> interleaved U
         std::string err;
-        lfm_status st = cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, xr, w.z, stream, err, win.c0, win.c1)
-                                      : k_spass_fwd(cp, xr, w.z, stream, err);
+        lfm_status st = k_spass_fwd(cp, xr, w.z, stream, err);
         if (st != LFM_OK) return fail(st, err);
       } else if (cp.fwd_t) {
         // s pass as a t pass over the transposed slices, written back in the interleaved U layout
@@ -277,7 +339,8 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   }
   if (path == LFM_PATH_COLLAPSED) {
     // one output: all (vt, n) rows; the column window selects the 256-column tiles of Z
-    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1, win.c0, win.c1));
+    bool split_done = false;
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, win, split_done));
     if (cp.adj_t == 2 || cp.adj_t == 3) {
       // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
@@ -286,7 +349,7 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
       if (st != LFM_OK) return fail(st, err);
       // non-separable lenslet stage: the other terms' t and s passes, accumulated (tcgen05 path only, eff_path)
       for (const Component& cm : cp.comps) {
-        TRY(sep(cm.adj_c1, y, w.z, 0, 1, 0, stream, 0, -1, r0, r1, win.c0, win.c1));
+        TRY(t_adjoint(cp, cm.adj_c1, y, w, stream, win, split_done));
         if ((st = k_vpass_adj(cp, cm.va, w.z, target, 1, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
       }
     } else if (cp.adj_t) {
@@ -334,10 +397,8 @@ lfm_status forward_subset_impl(const CameraPlan& cp, int m, const float* x, floa
   const float* xr;
   TRY(rotate_fwd(cp, x, nullptr, 0, w, stream, &xr));
   if (subset_collapsed(cp, vo)) {
-    std::string err;
-    lfm_status st = k_vpass_fwd(cp, vo.vf, xr, w.z, stream, err);
-    if (st != LFM_OK) return fail(st, err);
-    return sep(cp.fwd_c2, w.z, y, 0, 1, 0, stream);
+    bool amax_done = false;
+    return vt_forward(cp, vo.vf, cp.fwd_c2, xr, y, 0, w, stream, Win(), amax_done);
   }
   if (cp.info.type == LFM_PLENOPTIC) {
     TRY(sep(vo.fwd_s1, xr, w.f, 0, vo.n_views, 0, stream));
@@ -353,7 +414,8 @@ lfm_status adjoint_subset_impl(const CameraPlan& cp, int m, const float* y, floa
   float* target = rot ? w.r0 : x;
   const int acc = rot ? 0 : accumulate;
   if (subset_collapsed(cp, vo)) {
-    TRY(sep(cp.adj_c1, y, w.z, 0, 1, 0, stream));
+    bool split_done = false;
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, Win(), split_done));
     std::string err;
     lfm_status st = k_vpass_adj(cp, vo.va, w.z, target, acc, stream, err);
     if (st != LFM_OK) return fail(st, err);
@@ -588,17 +650,28 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
   if (stage == LFM_STAGE_FWD_T) {
     if (!cp.fwd_split) return fail(LFM_E_INVALID, "collapsed forward of this camera is not in two-pass form");
     if (!out) return fail(LFM_E_INVALID, "out is NULL");
-    st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream, 0, -1, 0, -1, 0, -1, w.zt, cp.ws_z);  // as in A_forward
+    // as in A_forward, on the U (and, 2xFP16, its fp16 split and the maxima of x^r) the last forward or FWD_S left
+    F16Src h;
+    if (f16_fwd(cp, cp.fwd_c2)) {
+      h.hi = reinterpret_cast<const uint16_t*>(w.z);
+      h.lo = h.hi + (size_t)cp.cf[0].n_rows * cp.info.nz * cp.info.ny;
+      h.amax = w.am;
+      h.amax_scale = cp.vf.lsum;
+    }
+    st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream, 0, -1, 0, -1, 0, -1, w.zt, cp.ws_z, h);
   } else if (stage == LFM_STAGE_ADJ_T) {
     if (!in) return fail(LFM_E_INVALID, "in is NULL");
-    st = sep(cp.adj_c1, in, w.z, 0, 1, 0, stream);
+    bool split_done = false;  // 2xFP16: includes the maxima and split of `in` (part of the t pass's cost)
+    st = t_adjoint(cp, cp.adj_c1, in, w, stream, Win(), split_done);
   } else if (stage == LFM_STAGE_FWD_S || stage == LFM_STAGE_ADJ_S) {
     const bool fwd = stage == LFM_STAGE_FWD_S;
     if (fwd ? !in : !out) return fail(LFM_E_INVALID, fwd ? "in is NULL" : "out is NULL");
     if (fwd ? !(cp.fwd_split && (cp.fwd_t == 2 || cp.fwd_t == 3)) : !(cp.adj_t == 2 || cp.adj_t == 3))
       return fail(LFM_E_INVALID, "the s pass of this camera is not a direct (band_v / spass) kernel");
     std::string err;
-    st = fwd ? (cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, in, w.z, stream, err) : k_spass_fwd(cp, in, w.z, stream, err))
+    const bool h = fwd && cp.fwd_t == 3 && f16_fwd(cp, cp.fwd_c2);  // U as fp16 hi / lo (the FWD_T input), maxima of `in`
+    if (h && (st = k_amax(in, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
+    st = fwd ? (cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, in, w.z, stream, err, 0, -1, h ? w.am : nullptr) : k_spass_fwd(cp, in, w.z, stream, err))
              : (cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, out, 0, stream, err) : k_spass_adj(cp, w.z, out, 0, stream, err));
     if (st != LFM_OK) return fail(st, err);
   } else {

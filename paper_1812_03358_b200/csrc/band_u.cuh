@@ -24,6 +24,11 @@ namespace lfm {
 
 struct UArgs {
   const float* A;         // weight images: block b at A + 4096 b (hi 2048 floats, then lo 2048 floats)
+  const uint16_t* H;      // 2xFP16 form (F16 instances): block b at H + 4096 b (hi 2048 halves, then lo), weights
+                          // scaled by 2^wexp (the host folds 2^-wexp into `scale`)
+  const float* amax;      // F16: n_amax partial maxima m_i; the source was written as fp16 hi + lo of 2^e src with
+  int n_amax;             // e = u_data_exp(max m_i * amax_scale) by its producer (band_v / split16_kernel), so the
+  float amax_scale;       // epilogue takes 2^-e back out
   const int32_t* blk_off; // per row tile: first block .. (row tiles of the table, n_tiles + 1 entries)
   const int32_t* blk_k0;  // per block: first source row (plan coordinates)
   float* out;
@@ -91,17 +96,26 @@ __device__ __forceinline__ UItem u_item(const UArgs& a, int it) {
 
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
+// 2xFP16: A hi+lo (8 KB) | src tile fp32 (16 KB), overwritten in place by the fp16 src hi (8 KB) | src lo (8 KB)
+template <bool F16> struct UStage {
+  static constexpr int STAGES = F16 ? 8 : U_STAGES;
+  static constexpr int BYTES = F16 ? 24576 : U_STAGE_BYTES;
+};
 constexpr int U_THREADS = 384;
+
 #ifndef U_SPLIT_BATCH
 #define U_SPLIT_BATCH 8  // float4 loads issued together by each split thread (16 per block)
 #endif
 constexpr int U_STAGE_OUT = 4096;  // per epilogue warp: 32 rows x 32 columns fp32, 128-byte swizzle (TMA store)
 constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 8 * U_STAGE_OUT + 1024 + 256;
 
-template <bool SPLIT>
+template <bool SPLIT, bool F16 = false>
 __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
-                                                              const __grid_constant__ CUtensorMap out_map, UArgs a) {
+                                                              const __grid_constant__ CUtensorMap out_map,
+                                                              const __grid_constant__ CUtensorMap lo_map, UArgs a) {
   using namespace tc;
+  constexpr int U_STAGES = UStage<F16>::STAGES, U_STAGE_BYTES = UStage<F16>::BYTES;
+  static_assert(UStage<true>::STAGES * UStage<true>::BYTES == 4 * 49152, "same ring size");
   extern __shared__ uint8_t u_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)u_smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sout = sm + U_STAGES * U_STAGE_BYTES;  // epilogue staging, 8 x 4 KB
@@ -153,20 +167,33 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
           }
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * U_STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[s], 32768);
-          bulk_g2s(st, a.A + (size_t)b * 4096, 16384, &full[s]);
           const int k = __ldg(a.blk_k0 + b) - a.k_shift;
+          if constexpr (F16) {  // fp16 weight images (8 KB); pre-split fp16 source hi and lo, 4 boxes of 16 rows x 64
+                                // columns each with the 128-byte swizzle = the MN-major operand layout
+            mbar_arrive_expect_tx(&full[s], 8192 + 16384);
+            bulk_g2s(st, a.H + (size_t)b * 4096, 8192, &full[s]);
 #pragma unroll
-          for (int g = 0; g < 8; ++g) tma_load_2d(st + 16384 + g * 2048, &src_map, nt * 256 + g * 32, k, &full[s]);
+            for (int g = 0; g < 4; ++g) {
+              tma_load_2d(st + 8192 + g * 2048, &src_map, nt * 256 + g * 64, k, &full[s]);
+              tma_load_2d(st + 16384 + g * 2048, &lo_map, nt * 256 + g * 64, k, &full[s]);
+            }
+          } else {
+            mbar_arrive_expect_tx(&full[s], 32768);
+            bulk_g2s(st, a.A + (size_t)b * 4096, 16384, &full[s]);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) tma_load_2d(st + 16384 + g * 2048, &src_map, nt * 256 + g * 32, k, &full[s]);
+          }
           if (++s == U_STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_tf32(128, 256, 0, 1);
-      const uint64_t dA0 = smem_desc(smem_u32(sm), 16, 512, 4);            // weights, K-major 64-byte swizzle
-      const uint64_t dB0 = smem_desc(smem_u32(sm) + 16384, 2048, 512, 1);  // source, MN-major 128B/32B-atom
+      constexpr uint32_t IDESC = F16 ? idesc_f16(128, 256, 0, 1) : idesc_tf32(128, 256, 0, 1);
+      // tf32: weights K-major 64-byte swizzle, source MN-major 128B/32B-atom; fp16: weights K-major 32-byte
+      // swizzle, source MN-major 128-byte swizzle (atoms of 64 columns x 8 rows, 2048 bytes apart along N)
+      const uint64_t dA0 = F16 ? smem_desc(smem_u32(sm), 16, 256, 6) : smem_desc(smem_u32(sm), 16, 512, 4);
+      const uint64_t dB0 = F16 ? smem_desc(smem_u32(sm) + 8192, 2048, 1024, 2) : smem_desc(smem_u32(sm) + 16384, 2048, 512, 1);
       int s = 0;
       uint32_t ph = 0;
       int buf = 0;
@@ -181,10 +208,17 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
           const uint32_t d = tmem + buf * 256;
           const int g1 = min(b1, g0 + a.group);
           for (int j = g0; j < g1; ++j) {
-            mbar_wait(&conv[s], ph);
+            mbar_wait(F16 ? &full[s] : &conv[s], ph);  // 2xFP16: the source arrives split, no split warps
             tc_fence_after();
             // descriptors = the stage-0 ones plus the start-address offset (16-byte units, low field; no carry)
             const uint64_t so = (uint64_t)((s * U_STAGE_BYTES) >> 4);
+            if constexpr (F16) {  // one K = 16 step: D += C_lo S_hi + C_hi S_lo + C_hi S_hi
+              const uint64_t ahi = dA0 + so, alo = dA0 + so + (4096 >> 4);
+              const uint64_t bhi = dB0 + so, blo = dB0 + so + (8192 >> 4);
+              mma_bf16_ss(d, alo, bhi, IDESC, j != g0 ? 1u : 0u);
+              mma_bf16_ss(d, ahi, blo, IDESC, 1u);
+              mma_bf16_ss(d, ahi, bhi, IDESC, 1u);
+            } else
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
               const uint64_t ahi = dA0 + so + 2 * kk;
@@ -206,6 +240,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       }
     }
   } else if (warp < 4) {
+    if constexpr (!F16) {  // (2xFP16: nothing to split)
     // lo split: 16 KB source tile = 1024 float4, 64 threads x 16
     const int t = threadIdx.x - 64;
     int s = 0;
@@ -240,11 +275,14 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         if (++s == U_STAGES) { s = 0; ph ^= 1; }
       }
     }
+    }
   } else {
     // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (its row quarter), columns half h
     const int q = warp & 3, h = (warp - 4) >> 2;
     int buf = 0;
     uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
+    float inv_sig = 1.f;  // 2xFP16: the data scale 2^-e (exact), applied before `scale`
+    if constexpr (F16) inv_sig = pow2f(-u_data_exp(a.amax, a.n_amax, a.amax_scale));
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const UItem ui = u_item<SPLIT>(a, it);
       const int mt = ui.mt, nt = ui.nt;
@@ -282,8 +320,13 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float4 v = make_float4(a.scale * acc[c + 4 * j], a.scale * acc[c + 4 * j + 1], a.scale * acc[c + 4 * j + 2],
-                                       a.scale * acc[c + 4 * j + 3]);
+          float4 v;
+          if constexpr (F16)
+            v = make_float4(a.scale * (inv_sig * acc[c + 4 * j]), a.scale * (inv_sig * acc[c + 4 * j + 1]),
+                            a.scale * (inv_sig * acc[c + 4 * j + 2]), a.scale * (inv_sig * acc[c + 4 * j + 3]));
+          else
+            v = make_float4(a.scale * acc[c + 4 * j], a.scale * acc[c + 4 * j + 1], a.scale * acc[c + 4 * j + 2],
+                            a.scale * acc[c + 4 * j + 3]);
           *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
         }
         fence_proxy_async_smem();

@@ -17,6 +17,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cuda_fp16.h>
+
 #include "tc_sm100.h"
 
 namespace lfm {
@@ -32,7 +34,10 @@ struct VArgs {
   int group;               // blocks per TMEM accumulator before it is drained
   float scale;
   int accumulate;
+  const float* amax;       // OUT16 (forward): LFM_AMAX_SLOTS partial maxima of |x^r| and a bound on the row sums of
+  float amax_scale;        // the s composite: U is written as fp16 hi + lo of 2^e U, e = u_data_exp(.) (tc_sm100.h)
 };
+
 
 // live blocks [lb0, lb1) of item key: blocks are stored with ascending k0, so the ones meeting the K window are
 // one contiguous run
@@ -52,11 +57,12 @@ __device__ __forceinline__ void v_live(const VArgs& a, int key, int BK, int& lb0
 
 constexpr int V_THREADS = 384;
 
-template <int N, int BK>
+template <int N, int BK, bool H = false>
 struct VCfg {
   static constexpr int A_BYTES = 128 * BK * 4;        // data tile [128][BK] fp32
   static constexpr int B_BYTES = N * BK * 4;          // one weight image [N][BK]
   static constexpr int EC0 = N >= 256 ? 128 : N / 2;
+  // staging per store: 32 rows x 32 fp32 columns, or (H: fp16 hi + lo output) 32 rows x 32 fp16 columns, twice
   static constexpr int OUT0 = 32 * (EC0 >= 32 ? 32 : EC0) * 4;
   // staging buffers per epilogue warp: 2 (store i+1 overlaps store i) when the ring keeps >= 2 stages, else 1
   static constexpr int NOB = (230912 - 16 * OUT0) / (2 * A_BYTES + 2 * B_BYTES) >= 2 ? 2 : 1;
@@ -71,7 +77,7 @@ struct VCfg {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
   static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
-  static constexpr int OUT = 32 * OC * 4;             // staging per warp
+  static constexpr int OUT = OUT0;                    // staging per warp and buffer
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * NOB * OUT + 1024 + 512;
   static_assert(STAGES >= 2, "band_v: stage too large");
 #ifndef BAND_V_NO_MERGE
@@ -85,11 +91,13 @@ struct VCfg {
   static constexpr int TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
 };
 
-template <int N, int DIR, int BK, bool KWIN = false>
+template <int N, int DIR, int BK, bool KWIN = false, bool OUT16 = false>
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
-                                                              const __grid_constant__ CUtensorMap out_map, VArgs a) {
+                                                              const __grid_constant__ CUtensorMap out_map,
+                                                              const __grid_constant__ CUtensorMap lo_map, VArgs a) {
   using namespace tc;
-  using C = VCfg<N, BK>;
+  using C = VCfg<N, BK, OUT16>;
+  static_assert(!OUT16 || (DIR == 0 && N == 256), "fp16 output: forward, 256-column tiles");
   extern __shared__ uint8_t v_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sout = sm + C::STAGES * C::STAGE;
@@ -240,6 +248,8 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     int ob = 0;  // staging buffer of the next store
     int buf = 0;
     uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
+    float sig = 1.f;  // OUT16: the data scale 2^e of the 2xFP16 t pass that reads U
+    if constexpr (OUT16) sig = pow2f(u_data_exp(a.amax, LFM_AMAX_SLOTS, a.amax_scale));
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int nt = a.nt0 + it % a.nt_cnt, mt = (it / a.nt_cnt) % a.n_mt, n = it / (a.nt_cnt * a.n_mt);
       const int key = n * a.n_nt + nt;
@@ -281,7 +291,24 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         uint8_t* stg = stg0 + ob * C::OUT;
         if (lane == 0) bulk_wait_read<C::NOB - 1>();  // the store that last used this buffer has read it
         __syncwarp();
-        if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
+        if constexpr (OUT16) {  // fp16 hi / lo of 2^e U: two 32 x 32 tiles, 64-byte rows, 64-byte swizzle
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float x0 = sig * (a.scale * acc[c + 8 * jj + 2 * i]), x1 = sig * (a.scale * acc[c + 8 * jj + 2 * i + 1]);
+              const __half2 hh = __floats2half2_rn(x0, x1);
+              const float2 hf = __half22float2(hh);
+              const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+              hw[i] = *reinterpret_cast<const uint32_t*>(&hh);
+              lw[i] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+            const int o = lane * 64 + ((jj ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(stg + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(stg + 2048 + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+        } else if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             const float4 v = make_float4(a.scale * acc[c + 4 * jj], a.scale * acc[c + 4 * jj + 1],
@@ -299,7 +326,10 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (DIR == 0) {  // U map (s, n, vt)
+          if (OUT16) {  // U hi / lo maps (s, n, vt), fp16
+            tma_store_3d(&out_map, c0 + c, n, vt0, stg);
+            tma_store_3d(&lo_map, c0 + c, n, vt0, stg + 2048);
+          } else if (DIR == 0) {  // U map (s, n, vt)
             if (a.accumulate) tma_add_3d(&out_map, c0 + c, n, vt0, stg);
             else tma_store_3d(&out_map, c0 + c, n, vt0, stg);
           } else {  // x map (vx, vt, n)

@@ -21,10 +21,10 @@
 #include <string>
 #include <vector>
 
+#include "lfm_internal.h"
 #include "band_u.cuh"
 #include "band_v.cuh"
 #include "spass.cuh"
-#include "lfm_internal.h"
 #include "lfm_kernels.h"
 
 namespace lfm {
@@ -124,7 +124,8 @@ static lfm_status upload_family(BandFamily& f, size_t& bytes, std::string& err) 
     if ((st = dev_upload(&f.d_uoff, f.u_off.data(), f.u_off.size() * 4, err)) != LFM_OK) return st;
     if ((st = dev_upload(&f.d_uk0, uk.data(), uk.size() * 4, err)) != LFM_OK) return st;
     if ((st = dev_upload(&f.d_ua, f.u_a.data(), f.u_a.size() * 4, err)) != LFM_OK) return st;
-    bytes += f.u_off.size() * 4 + uk.size() * 4 + f.u_a.size() * 4;
+    if ((st = dev_upload(&f.d_uh, f.u_h.data(), f.u_h.size() * 2, err)) != LFM_OK) return st;
+    bytes += f.u_off.size() * 4 + uk.size() * 4 + f.u_a.size() * 4 + f.u_h.size() * 2;
   }
   if (!f.m8_off.empty()) {
     std::vector<float> mw(f.m8_w64.size() + 8);
@@ -181,6 +182,13 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
   T.off.assign((size_t)f.n_tables * T.n_nt + 1, 0);
   T.k0.clear();
   T.img.clear();
+  double lsum = 0;
+  for (size_t idx = 0; idx < (size_t)f.n_tables * f.n_rows; ++idx) {
+    double r = 0;
+    for (int e = 0; e < f.len[idx]; ++e) r += std::fabs((double)(float)f.w64[idx * f.taps + e]);
+    lsum = std::max(lsum, r);
+  }
+  T.lsum = (float)(lsum * (1.0 + 1e-6));
   std::vector<char> any(f.n_src + 32);
   const uint32_t smask = BK >= 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
   for (int m = 0; m < f.n_tables; ++m)
@@ -375,8 +383,8 @@ static void tmap_insert(const TmapKey& k, const CUtensorMap& m) {
 typedef CUresult (*EncodeTiledFnV)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static lfm_status encode3_raw(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
-                          const int box[3], CUtensorMapSwizzle swz, std::string& err) {
+static lfm_status encode3_raw(CUtensorMap* map, const void* base, const long long dims[3], const long long strides[2],
+                          const int box[3], CUtensorMapSwizzle swz, std::string& err, bool f16 = false) {
   static EncodeTiledFnV encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -393,7 +401,7 @@ static lfm_status encode3_raw(CUtensorMap* map, const float* base, const long lo
   cuuint64_t gd[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
   cuuint64_t gs[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
   cuuint32_t bx[3] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2]}, es[3] = {1, 1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gd, gs, bx, es,
+  CUresult r = encode(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gd, gs, bx, es,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     err = "band_v: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
@@ -402,28 +410,30 @@ static lfm_status encode3_raw(CUtensorMap* map, const float* base, const long lo
   return LFM_OK;
 }
 
-static lfm_status encode3(CUtensorMap* map, const float* base, const long long dims[3], const long long strides[2],
-                          const int box[3], CUtensorMapSwizzle swz, std::string& err) {
-  const TmapKey k = {base, {3, dims[0], dims[1], dims[2], strides[0], strides[1], box[0], box[1], box[2], (long long)swz, 0}};
+static lfm_status encode3(CUtensorMap* map, const void* base, const long long dims[3], const long long strides[2],
+                          const int box[3], CUtensorMapSwizzle swz, std::string& err, bool f16 = false) {
+  const TmapKey k = {base, {3, dims[0], dims[1], dims[2], strides[0], strides[1], box[0], box[1], box[2], (long long)swz, f16}};
   if (tmap_lookup(k, map)) return LFM_OK;
-  lfm_status st = encode3_raw(map, base, dims, strides, box, swz, err);
+  lfm_status st = encode3_raw(map, base, dims, strides, box, swz, err, f16);
   if (st == LFM_OK) tmap_insert(k, *map);
   return st;
 }
 
-template <int N, int DIR, int BK>
+template <int N, int DIR, int BK, bool OUT16 = false>
 static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err, int nt0 = 0, int nt_cnt = -1,
-                                int k_lo = 0, int k_hi = 1 << 30) {
+                                int k_lo = 0, int k_hi = 1 << 30, const CUtensorMap* lom = nullptr,
+                                const float* amax = nullptr) {
   // the K-window instantiation only when a window cuts the K range (adjoint column shards)
   const bool kwin = k_lo > 0 || k_hi < (1 << 30);
   static bool attr[LFM_MAX_DEV][2];
   const int dv = cur_dev();
+  constexpr size_t SMEM = VCfg<N, BK, OUT16>::SMEM;
   if (!attr[dv][kwin]) {
-    cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)VCfg<N, BK>::SMEM)
-                         : cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)VCfg<N, BK>::SMEM);
+    cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true, OUT16>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)
+                         : cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, false, OUT16>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
     attr[dv][kwin] = true;
   }
@@ -441,17 +451,20 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   v.group = 4;
   v.scale = scale;
   v.accumulate = accumulate;
+  v.amax = amax;
+  v.amax_scale = T.lsum;
   const int items = v.nz * v.n_mt * v.nt_cnt;
   if (items <= 0) return LFM_OK;
   const int grid = std::min(items, g_num_sms());
-  if (kwin) band_v_kernel<N, DIR, BK, true><<<grid, V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
-  else band_v_kernel<N, DIR, BK, false><<<grid, V_THREADS, VCfg<N, BK>::SMEM, (cudaStream_t)stream>>>(am, om, v);
+  const CUtensorMap& lm = lom ? *lom : om;
+  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, v);
+  else band_v_kernel<N, DIR, BK, false, OUT16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
 
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0, int c1) {
+                       int c0, int c1, const float* amax) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
   if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
@@ -459,11 +472,21 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
   const int ab[3] = {T.BK, 128, 1};
   lfm_status st = encode3(&am, x, ad, as, ab, T.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
   if (st != LFM_OK) return st;
-  const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
   const int ob[3] = {32, 1, 32};
-  if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
   // column window [c0, c1): only the N-tiles (256 detector columns) that meet it
   const int nt0 = std::max(0, c0) / T.N, nt1 = c1 < 0 ? T.n_nt : (c1 + T.N - 1) / T.N;
+  if (amax) {  // fp16 hi / lo of 2^e U (the 2xFP16 t pass input): two [vt][n][s] half arrays
+    const uint16_t* hi = reinterpret_cast<const uint16_t*>(U);
+    const uint16_t* lo = hi + (size_t)nd * nz * ny;
+    const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 2, (long long)nz * nd * 2};
+    CUtensorMap lm;
+    if ((st = encode3(&om, hi, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK) return st;
+    if ((st = encode3(&lm, lo, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK) return st;
+    return T.BK == 32 ? launch_band_v<256, 0, 32, true>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0, 0, 1 << 30, &lm, amax)
+                      : launch_band_v<256, 0, 16, true>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0, 0, 1 << 30, &lm, amax);
+  }
+  const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+  if ((st = encode3(&om, U, od, os, ob, CU_TENSOR_MAP_SWIZZLE_128B, err)) != LFM_OK) return st;
   return T.BK == 32 ? launch_band_v<256, 0, 32>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0)
                     : launch_band_v<256, 0, 16>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0);
 }
@@ -568,8 +591,8 @@ void free_camera(CameraPlan& cp) {
     f->d_m8off = nullptr; f->d_m8seg = nullptr; f->d_m8w = nullptr;
     dfree(f->d_foff); dfree(f->d_frow); dfree(f->d_fw);
     f->d_foff = nullptr; f->d_frow = nullptr; f->d_fw = nullptr;
-    dfree(f->d_uoff); dfree(f->d_uk0); dfree(f->d_ua);
-    f->d_uoff = nullptr; f->d_uk0 = nullptr; f->d_ua = nullptr;
+    dfree(f->d_uoff); dfree(f->d_uk0); dfree(f->d_ua); dfree(f->d_uh);
+    f->d_uoff = nullptr; f->d_uk0 = nullptr; f->d_ua = nullptr; f->d_uh = nullptr;
     f->d_cnt = nullptr; f->d_idx = nullptr; f->d_w = nullptr; f->d_g = nullptr; f->d_gw = nullptr;
     f->d_moff = nullptr; f->d_mseg = nullptr; f->d_mw = nullptr;
   }
@@ -1403,18 +1426,19 @@ lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
-                                 int box_r, CUtensorMapSwizzle swz, std::string& err);
-static lfm_status encode_map(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
-                             int box_r, CUtensorMapSwizzle swz, std::string& err) {
-  const TmapKey k = {base, {2, cols, rows, pitch, box_c, box_r, (long long)swz, 0, 0, 0, 0}};
+static lfm_status encode_map_raw(CUtensorMap* map, const void* base, int cols, int rows, long long pitch, int box_c,
+                                 int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16);
+// (pitch in elements; f16: 2-byte elements)
+static lfm_status encode_map(CUtensorMap* map, const void* base, int cols, int rows, long long pitch, int box_c,
+                             int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16 = false) {
+  const TmapKey k = {base, {2, cols, rows, pitch, box_c, box_r, (long long)swz, f16, 0, 0, 0}};
   if (tmap_lookup(k, map)) return LFM_OK;
-  lfm_status st = encode_map_raw(map, base, cols, rows, pitch, box_c, box_r, swz, err);
+  lfm_status st = encode_map_raw(map, base, cols, rows, pitch, box_c, box_r, swz, err, f16);
   if (st == LFM_OK) tmap_insert(k, *map);
   return st;
 }
-static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, int rows, long long pitch, int box_c,
-                                 int box_r, CUtensorMapSwizzle swz, std::string& err) {
+static lfm_status encode_map_raw(CUtensorMap* map, const void* base, int cols, int rows, long long pitch, int box_c,
+                                 int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -1425,14 +1449,15 @@ static lfm_status encode_map_raw(CUtensorMap* map, const float* base, int cols, 
       return LFM_E_CUDA;
     }
   }
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 3)) {
+  const int esz = f16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((pitch * esz) & 15)) {
     err = "band_u: buffers and their rows must be 16-byte aligned";
     return LFM_E_INVALID;
   }
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t gstr[1] = {(cuuint64_t)pitch * 4};
+  cuuint64_t gstr[1] = {(cuuint64_t)pitch * esz};
   cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r}, es[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, es,
+  CUresult r = encode(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstr, box, es,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -1474,9 +1499,100 @@ __global__ void sum_chunks_kernel(const float* __restrict__ part, float* __restr
   }
 }
 
+// per-CTA maxima of |src[0, n)| at part[blockIdx.x]; CTA 0 zero-fills the other LFM_AMAX_SLOTS (the data scale of
+// the 2xFP16 band_u form: of x^r for the forward, of y for the adjoint)
+__global__ void amax_kernel(const float* __restrict__ src, long long n, float* __restrict__ part) {
+  uint32_t m = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const long long n4 = n >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    long long i = i0;
+    for (; i + 3 * stride < n4; i += 4 * stride) {  // four independent loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldg(s4 + i + j * stride);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        m = max(max(max(m, __float_as_uint(v[j].x) & 0x7fffffffu), max(__float_as_uint(v[j].y) & 0x7fffffffu,
+                __float_as_uint(v[j].z) & 0x7fffffffu)), __float_as_uint(v[j].w) & 0x7fffffffu);
+    }
+    for (; i < n4; i += stride) {
+      const float4 v = __ldg(s4 + i);
+      m = max(max(max(m, __float_as_uint(v.x) & 0x7fffffffu), max(__float_as_uint(v.y) & 0x7fffffffu,
+              __float_as_uint(v.z) & 0x7fffffffu)), __float_as_uint(v.w) & 0x7fffffffu);
+    }
+    for (long long i = 4 * n4 + i0; i < n; i += stride) m = max(m, __float_as_uint(__ldg(src + i)) & 0x7fffffffu);
+  } else {
+    for (long long i = i0; i < n; i += stride) m = max(m, __float_as_uint(__ldg(src + i)) & 0x7fffffffu);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ uint32_t red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) part[blockIdx.x] = __uint_as_float(m);
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + threadIdx.x; i < LFM_AMAX_SLOTS; i += 32) part[i] = 0.f;
+  }
+}
+
+lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err) {
+  const int g = std::min(std::min(g_num_sms(), LFM_AMAX_SLOTS), (int)std::max<long long>(1, n / 8192));
+  amax_kernel<<<g, 1024, 0, (cudaStream_t)stream>>>(src, n, part);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "amax_kernel launch", err);
+}
+
+// fp16 hi / lo of 2^e src (e from the partial maxima of |src|, as band_u computes it); float4 path when aligned
+__global__ void split16_kernel(const float* __restrict__ src, long long n, const float* __restrict__ amax,
+                               uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+  const float sig = pow2f(u_data_exp(amax, LFM_AMAX_SLOTS, 1.f));
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
+  const long long n4 = vec ? n >> 2 : 0;
+  auto one = [&](long long i, const float4 v) {
+    const float x0 = sig * v.x, x1 = sig * v.y, x2 = sig * v.z, x3 = sig * v.w;
+    const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+    const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+    reinterpret_cast<uint2*>(hi)[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+    reinterpret_cast<uint2*>(lo)[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+  };
+  long long i = i0;
+  for (; i + 3 * stride < n4; i += 4 * stride) {  // four independent loads in flight
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(src) + i + j * stride);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) one(i + j * stride, v[j]);
+  }
+  for (; i < n4; i += stride) one(i, __ldg(reinterpret_cast<const float4*>(src) + i));
+  for (long long i = 4 * n4 + i0; i < n; i += stride) {
+    const float x = sig * __ldg(src + i);
+    const __half h = __float2half_rn(x), l = __float2half_rn(x - __half2float(h));
+    hi[i] = *reinterpret_cast<const uint16_t*>(&h);
+    lo[i] = *reinterpret_cast<const uint16_t*>(&l);
+  }
+}
+
+lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t* hi, uint16_t* lo, void* stream,
+                     std::string& err) {
+  split16_kernel<<<(unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, (long long)g_num_sms() * 4), 256, 0,
+                   (cudaStream_t)stream>>>(src, n, amax, hi, lo);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "split16_kernel launch", err);
+}
+
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0, int out_r1, int win_r0, int win_r1, int out_c0,
-                      int out_c1, float* part, size_t part_bytes) {
+                      int out_c1, float* part, size_t part_bytes, F16Src h16) {
   if (n_out <= 0) return LFM_OK;
   SepArgs a;
   a.src = src;
@@ -1565,9 +1681,20 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
       ksplit = std::min(4, g_num_sms() / std::max(1, items0));
       while (ksplit > 1 && (size_t)ksplit * kc_rows * a.out_pitch * 4 > part_bytes) --ksplit;
     }
-    CUtensorMap map, omap;
-    lfm_status st = encode_map(&map, base, op.n_is, win_rows, a.src_pitch, 32, 16, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, err);
-    if (st != LFM_OK) return st;
+    // 2xFP16 form when the caller passes the pre-split source (api.cu decides, f16_ok) and the plan has the images
+    const bool f16 = h16.hi && op.ft->d_uh;
+    CUtensorMap map, omap, lmap;
+    lfm_status st;
+    if (f16) {  // fp16 hi / lo maps of the source window, 64-column x 16-row boxes, 128-byte swizzle
+      const long long wo = (long long)a.win_r0 * a.src_pitch + term.src_off;
+      if ((st = encode_map(&map, h16.hi + wo, op.n_is, win_rows, a.src_pitch, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
+          (st = encode_map(&lmap, h16.lo + wo, op.n_is, win_rows, a.src_pitch, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK)
+        return st;
+    } else {
+      st = encode_map(&map, base, op.n_is, win_rows, a.src_pitch, 32, 16, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, err);
+      if (st != LFM_OK) return st;
+      lmap = map;
+    }
     if (ksplit > 1)
       st = encode_map(&omap, part, op.n_os, (int)(ksplit * kc_rows), a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, err);
     else
@@ -1578,13 +1705,19 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     const int dv = cur_dev();
     if (!smem_set[dv]) {
       if (cudaFuncSetAttribute(band_u_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
-          cudaFuncSetAttribute(band_u_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
+          cudaFuncSetAttribute(band_u_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(band_u_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(band_u_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
         return cuda_check(cudaGetLastError(), "band_u smem attribute", err);
       smem_set[dv] = true;
     }
     UArgs u;
     const int n_mt = op.ft->u_ntiles;
     u.A = op.ft->d_ua;
+    u.H = op.ft->d_uh;
+    u.amax = h16.amax;
+    u.n_amax = LFM_AMAX_SLOTS;
+    u.amax_scale = h16.amax_scale;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
     u.blk_k0 = op.ft->d_uk0;
     u.out = out + (long long)b0 * a.out_stride;
@@ -1601,14 +1734,24 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.k_end = a.win_r1;
     u.windowed = a.win_r0 > 0 || a.win_r1 < op.n_it;
     u.group = op.stages > 0 ? op.stages : 4;
-    u.scale = op.out_scale * term.scale;
+    if (f16) {  // 2xFP16: 3 MMAs per block instead of 6, so twice the blocks per drain (same MMAs per accumulator
+                // chain, and a drain -- 128 KB of TMEM reads -- no longer outlasts the group's MMAs)
+      static const int g16 = std::getenv("LFM_U16_GROUP") ? std::atoi(std::getenv("LFM_U16_GROUP")) : 0;
+      u.group = g16 > 0 ? g16 : 2 * u.group;
+    }
+    u.scale = f16 ? (float)std::ldexp((double)(op.out_scale * term.scale), -op.ft->u_wexp) : op.out_scale * term.scale;
     u.accumulate = ksplit > 1 ? 0 : accumulate;
     u.tile_mode = op.ft->u_mode;
     u.tm_nz = op.ft->u_nz;
     if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
     const int grid_u = std::min(u.n_mt * u.n_nt * u.ksplit, g_num_sms());
-    if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
-    else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, u);
+    if (f16) {
+      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+    } else {
+      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+    }
     ++g_launches;
     if (ksplit > 1) {
       const int sr0 = mt0 * 128, sr1 = std::min(op.n_ot, (mt0 + n_mt_l) * 128);

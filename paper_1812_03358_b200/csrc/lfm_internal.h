@@ -70,6 +70,12 @@ struct BandFamily {
   int32_t* d_uoff = nullptr;
   int32_t* d_uk0 = nullptr;
   float* d_ua = nullptr;
+  // 2xFP16 form of the same blocks (band_u_kernel<.., true>): per block the weights scaled by 2^u_wexp (exact) and
+  // split w 2^e = hi + lo + O(2^-22 w 2^e), hi = rn_fp16(w 2^e), lo = rn_fp16(w 2^e - hi), each a 128 x 16 fp16 image
+  // in the K-major 32-byte-swizzled layout (element (m, k) at byte m*32 + k*2 with bit 4 ^= bit 7): 4096 halves
+  std::vector<uint16_t> u_h;
+  int u_wexp = 0;                          // max |w| 2^u_wexp in [2^14, 2^15)
+  uint16_t* d_uh = nullptr;
   // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
   std::vector<int32_t> m8_off, m8_seg;
   std::vector<double> m8_w64;
@@ -148,6 +154,7 @@ struct ShearPass {
 // tcgen05 s-pass tables (band_v.cuh): per item (slice n, N-tile) the K blocks and the N x BK hi/lo images
 struct VTab {
   int N = 0, n_nt = 0, BK = 16;
+  float lsum = 0.f;  // max over rows (output columns) of sum |w|: |U| <= lsum max |x| (the 2xFP16 data scale)
   std::vector<int32_t> off, k0;
   std::vector<float> img;
   int32_t* d_off = nullptr;
@@ -228,15 +235,33 @@ lfm_status prepare_subsets(CameraPlan& cp, std::string& err);
 // kernels.cu
 lfm_status upload_camera(CameraPlan& cp, std::string& err);
 void free_camera(CameraPlan& cp);
+// Pre-split source of the 2xFP16 band_u form: fp16 arrays hi, lo (same shape and pitch as the fp32 source) holding
+// 2^e src = hi + lo, e = u_data_exp(max of the LFM_AMAX_SLOTS partial maxima `amax` x amax_scale) as their producer
+// computed it (band_v forward: maxima of x^r times the s composite's row-sum bound; split16_kernel: maxima of the
+// source itself).  hi == nullptr: the 3xTF32 form on the fp32 source.
+constexpr int LFM_AMAX_SLOTS = 256;  // partial maxima slots in the workspace (>= CTAs of any launch writing them)
+struct F16Src {
+  const uint16_t* hi = nullptr;
+  const uint16_t* lo = nullptr;
+  const float* amax = nullptr;
+  float amax_scale = 1.f;
+};
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0 = 0, int out_r1 = -1, int win_r0 = 0,
                       int win_r1 = -1, int out_c0 = 0, int out_c1 = -1, float* part = nullptr,
-                      size_t part_bytes = 0);
+                      size_t part_bytes = 0, F16Src h16 = F16Src());
 lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long long in_bs, long long in_pitch,
                        long long out_bs, long long out_pitch, void* stream, std::string& err);
 lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
+// amax != nullptr: U is written as fp16 hi (U reinterpreted as uint16_t*, nd*nz*ny halves) then lo (the next
+// nd*nz*ny halves) of 2^e U with e from the partial maxima of |x| (amax_kernel) and T.lsum -- the 2xFP16 t pass input
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0 = 0, int c1 = -1);
+                       int c0 = 0, int c1 = -1, const float* amax = nullptr);
+// LFM_AMAX_SLOTS partial maxima of |src[0, n)| into part (one kernel)
+lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err);
+// fp16 hi / lo of 2^e src over n floats (e from the partial maxima `amax` of src), for the 2xFP16 band_u form
+lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t* hi, uint16_t* lo, void* stream,
+                     std::string& err);
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
                        std::string& err, int c0 = 0, int c1 = -1);
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);

@@ -396,6 +396,27 @@ static int umma_row(const BandFamily& f, int t, int m) {
   return r < f.n_rows ? r : -1;
 }
 
+// fp32 -> fp16 bits, round to nearest even (normal and subnormal; |x| < 65520 assumed, as the callers scale to
+// below 2^15), and back
+static uint16_t f2h_rn(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  const uint32_t sign = (u >> 16) & 0x8000u;
+  u &= 0x7fffffffu;
+  if (u < 0x38800000u) {  // below 2^-14: subnormal fp16, value m 2^-24 with m = rn_even(|x| 2^24) (exact product)
+    float a;
+    std::memcpy(&a, &u, 4);
+    return (uint16_t)(sign | (uint32_t)std::nearbyint((double)a * 16777216.0));
+  }
+  const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) >> 13;  // mantissa rounded to 10 bits (carry into exponent)
+  return (uint16_t)(sign | (r - ((127u - 15u) << 10)));
+}
+static float h2f(uint16_t h) {
+  const int e = (h >> 10) & 31, m = h & 1023;
+  const double v = e == 0 ? std::ldexp((double)m, -24) : std::ldexp(1.0 + m / 1024.0, e - 15);
+  return (float)((h & 0x8000) ? -v : v);
+}
+
 static void build_umma(BandFamily& f) {
   // mode 1 pairs voxel rows: an odd ny leaves a last tile with one voxel row (its other half reads as none)
   const int nt = f.u_mode == 0 ? (f.n_rows + 127) / 128 : ((f.n_rows / f.u_nz + 1) / 2) * (f.u_nz / 64);
@@ -451,6 +472,35 @@ static void build_umma(BandFamily& f) {
       }
     }
   f.u_off[(size_t)f.n_tables * nt] = (int)f.u_k0.size();
+  // 2xFP16 images: w 2^e split into fp16 hi + lo, e so that max |w| 2^e lies in [2^14, 2^15)
+  float wmax = 0.f;
+  for (size_t idx = 0; idx < (size_t)f.n_tables * f.n_rows; ++idx)
+    for (int e = 0; e < f.len[idx]; ++e) wmax = std::max(wmax, std::fabs((float)f.w64[idx * f.taps + e]));
+  int ex = 0;
+  if (wmax > 0.f) std::frexp((double)wmax * (1.0 + 1e-6), &ex);
+  f.u_wexp = wmax > 0.f ? 15 - ex : 0;
+  const size_t nb = f.u_k0.size();
+  f.u_h.assign(nb * 4096, 0);
+  for (int m = 0; m < f.n_tables; ++m)
+    for (int t = 0; t < nt; ++t)
+      for (int b = f.u_off[(size_t)m * nt + t]; b < f.u_off[(size_t)m * nt + t + 1]; ++b) {
+        const int k0 = f.u_k0[b];
+        for (int mm = 0; mm < 128; ++mm) {
+          const int r = umma_row(f, t, mm);
+          if (r < 0) continue;
+          const size_t idx = (size_t)m * f.n_rows + r;
+          for (int k = 0; k < 16; ++k) {
+            const int e = k0 + k - f.start[idx];
+            if (e < 0 || e >= f.len[idx]) continue;
+            const float w = (float)std::ldexp((double)(float)f.w64[idx * f.taps + e], f.u_wexp);  // exact
+            const uint16_t wh = f2h_rn(w), wl = f2h_rn(w - h2f(wh));
+            uint32_t off = (uint32_t)(mm * 32 + k * 2);
+            off ^= ((off >> 7) & 1u) << 4;
+            f.u_h[(size_t)b * 4096 + off / 2] = wh;
+            f.u_h[(size_t)b * 4096 + 2048 + off / 2] = wl;
+          }
+        }
+      }
 }
 
 // MSEG form with groups of 8 rows (segments split at zero runs >= 2 source cells, weights 8 per cell).

@@ -178,6 +178,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// Instruction descriptor, kind::f16 with fp16 A and B, fp32 accumulator (a_mn / b_mn = 1 for MN-major operands).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
 // Instruction descriptor, kind::tf32, fp32 accumulator; a_mn / b_mn = 1 for MN-major operands.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
   return (1u << 4)                      // D format f32
@@ -187,4 +192,23 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_
 }
 
 }  // namespace tc
+
+// Data scale exponent of the 2xFP16 form (whole warp, the same value in every kernel that reads the same partial
+// maxima): e with B 2^e in [2^14, 2^15), B = max_i m_i * mult >= max |data| (mult: a bound on the operator's row
+// sums when the maxima are those of its input); 0 when B is 0 or not finite (the data is then 0 or not finite).
+// With max |2^e data| < 2^15 the fp16 hi cannot overflow, and values far below the maximum only lose precision
+// below 2^-24 absolute (2^-39 of the maximum) -- the split is as exact as the 3xTF32 one (tools/microbench/f16_probe.cu).
+__device__ __forceinline__ int u_data_exp(const float* amax, int n, float mult) {
+  uint32_t m = 0;
+  for (int i = threadIdx.x & 31; i < n; i += 32) m = max(m, __float_as_uint(__ldg(amax + i)) & 0x7fffffffu);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float b = __uint_as_float(m) * mult;
+  if (!(b > 0.f) || !(b < 3.0e38f)) return 0;
+  int ex;
+  frexpf(b, &ex);  // b < 2^ex
+  return min(100, max(-100, 15 - ex));
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }  // |e| <= 126
+
 }  // namespace lfm

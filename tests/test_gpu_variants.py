@@ -133,7 +133,7 @@ def test_s_pass_orders(name, transposed, monkeypatch):
 
 def test_stage_entry_points():
     """lfm_A_stage runs the forward / adjoint t pass alone on the workspace intermediate (one band_u launch, plus the
-    ordered split-K sum on small outputs, as in A_forward):
+    ordered split-K sum on small outputs, as in A_forward; the adjoint's 2xFP16 form also splits its input):
     FWD_T after a forward reproduces that forward's y bit for bit; bad stage ids and NULLs fail."""
     from paper_1812_03358_b200 import lfm
     cfg, plan, ops, ws = setup("small_two")
@@ -150,7 +150,7 @@ def test_stage_entry_points():
         assert lfm.last_launch_count() in (1, 2)     # band_u, plus the ordered chunk sum when it splits K
         assert torch.equal(y, y2)
         lfm.A_stage(plan, c, lfm.STAGE_ADJ_T, dev(uniform_vector(op.n_pix, 1)), None, ws)
-        assert lfm.last_launch_count() == 1
+        assert lfm.last_launch_count() in (1, 3)     # band_u (3xTF32), or maxima + fp16 split + band_u (2xFP16)
         with pytest.raises(lfm.LfmError):
             lfm.A_stage(plan, c, 7, None, y2, ws)
         with pytest.raises(lfm.LfmError):
