@@ -209,9 +209,16 @@ static lfm_status vt_forward(const CameraPlan& cp, const VTab& T, const SepOp& c
   std::string err;
   lfm_status st;
   if (f16_fwd(cp, c2)) {
-    if (!amax_done && (st = k_amax(xr, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
+    // x^r pre-split into fp16 hi / lo (w.xt) when band_v has its fp16 images: no split warps in either kernel
+    static const bool no_x16 = std::getenv("LFM_NO_X16") != nullptr;  // A/B: band_v splits x^r itself
+    uint16_t* x16 = T.d_h16 && T.BK == 32 && !no_x16 ? reinterpret_cast<uint16_t*>(w.xt) : nullptr;
+    if (!amax_done) {
+      if ((st = k_amax(xr, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
+      if (x16 && (st = k_split16(xr, cp.info.n_vox, w.am, x16, x16 + cp.info.n_vox, stream, err)) != LFM_OK)
+        return fail(st, err);
+    }
     amax_done = true;
-    if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1, w.am)) != LFM_OK) return fail(st, err);
+    if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1, w.am, x16)) != LFM_OK) return fail(st, err);
     F16Src h;
     h.hi = reinterpret_cast<const uint16_t*>(w.z);
     h.lo = h.hi + (size_t)cp.cf[0].n_rows * cp.info.nz * cp.info.ny;
@@ -226,7 +233,7 @@ static lfm_status vt_forward(const CameraPlan& cp, const VTab& T, const SepOp& c
 // The adjoint t pass (c1) of y's rows [r0, r1): 2xFP16 = maxima of those rows, fp16 hi / lo of 2^e y into w.h16
 // (done once per call, `split_done`), then band_u from them.
 static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* y, const Ws& w, void* stream, Win win,
-                            bool& split_done) {
+                            bool& split_done, bool z16 = false) {
   if (!f16_adj(cp, c1)) return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1);
   const int n_s = cp.info.n_s, r0 = std::max(0, win.r0), r1 = win.r1 < 0 ? cp.info.n_t : std::min(win.r1, cp.info.n_t);
   const size_t np = (size_t)cp.info.n_pix;
@@ -242,7 +249,18 @@ static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* 
   h.hi = w.h16;
   h.lo = w.h16 + np;
   h.amax = w.am;
+  if (z16) {  // Z as fp16 hi / lo of 2^e' Z for band_v's 2xFP16 form (k_vpass_adj with in_scale = u_lsum)
+    h.out_hi = reinterpret_cast<uint16_t*>(w.z);
+    h.out_lo = h.out_hi + (size_t)c1.n_ot * c1.n_os;
+    h.out_scale16 = c1.ft->u_lsum;
+  }
   return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1, nullptr, 0, h);
+}
+
+// the adjoint's t pass can hand band_v an fp16 Z (every term's tables have the 2xFP16 forms)
+static bool z16_ok(const CameraPlan& cp, const SepOp& c1, const VTab& va) {
+  static const bool no_z16 = std::getenv("LFM_NO_Z16") != nullptr;  // A/B: fp32 Z, band_v splits it
+  return f16_adj(cp, c1) && cp.adj_t == 3 && vpass_adj_in16(va) && !no_z16;
 }
 
 // the collapsed path runs on the tcgen05 kernels end to end (band_v s passes, band_u t passes), the form whose
@@ -340,17 +358,22 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   if (path == LFM_PATH_COLLAPSED) {
     // one output: all (vt, n) rows; the column window selects the 256-column tiles of Z
     bool split_done = false;
-    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, win, split_done));
+    const bool z16 = z16_ok(cp, cp.adj_c1, cp.va) && win.c0 % 8 == 0;  // fp16 Z maps start on 16-byte boundaries
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, win, split_done, z16));
     if (cp.adj_t == 2 || cp.adj_t == 3) {
       // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
-      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err, win.c0, win.c1)
+      lfm_status st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, target, acc, stream, err, win.c0, win.c1,
+                                                  z16 ? w.am : nullptr, cp.adj_c1.ft->u_lsum)
                                     : k_spass_adj(cp, w.z, target, acc, stream, err);
       if (st != LFM_OK) return fail(st, err);
       // non-separable lenslet stage: the other terms' t and s passes, accumulated (tcgen05 path only, eff_path)
       for (const Component& cm : cp.comps) {
-        TRY(t_adjoint(cp, cm.adj_c1, y, w, stream, win, split_done));
-        if ((st = k_vpass_adj(cp, cm.va, w.z, target, 1, stream, err, win.c0, win.c1)) != LFM_OK) return fail(st, err);
+        const bool zc = z16_ok(cp, cm.adj_c1, cm.va) && win.c0 % 8 == 0;
+        TRY(t_adjoint(cp, cm.adj_c1, y, w, stream, win, split_done, zc));
+        if ((st = k_vpass_adj(cp, cm.va, w.z, target, 1, stream, err, win.c0, win.c1, zc ? w.am : nullptr,
+                              cm.adj_c1.ft->u_lsum)) != LFM_OK)
+          return fail(st, err);
       }
     } else if (cp.adj_t) {
       // Z_n -> ZT_n = [j][vt] per slice, then the s pass as a t pass with transposed output into x_n
@@ -415,9 +438,11 @@ lfm_status adjoint_subset_impl(const CameraPlan& cp, int m, const float* y, floa
   const int acc = rot ? 0 : accumulate;
   if (subset_collapsed(cp, vo)) {
     bool split_done = false;
-    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, Win(), split_done));
+    const bool z16 = z16_ok(cp, cp.adj_c1, vo.va);
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, Win(), split_done, z16));
     std::string err;
-    lfm_status st = k_vpass_adj(cp, vo.va, w.z, target, acc, stream, err);
+    lfm_status st = k_vpass_adj(cp, vo.va, w.z, target, acc, stream, err, 0, -1, z16 ? w.am : nullptr,
+                                cp.adj_c1.ft->u_lsum);
     if (st != LFM_OK) return fail(st, err);
   } else if (cp.info.type == LFM_PLENOPTIC) {
     TRY(sep(vo.adj_s3, y, w.f, 0, vo.n_views, 0, stream));
@@ -661,18 +686,30 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
     st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream, 0, -1, 0, -1, 0, -1, w.zt, cp.ws_z, h);
   } else if (stage == LFM_STAGE_ADJ_T) {
     if (!in) return fail(LFM_E_INVALID, "in is NULL");
-    bool split_done = false;  // 2xFP16: includes the maxima and split of `in` (part of the t pass's cost)
-    st = t_adjoint(cp, cp.adj_c1, in, w, stream, Win(), split_done);
+    bool split_done = false;  // 2xFP16: includes the maxima and split of `in` (part of the t pass's cost); Z in fp16
+    st = t_adjoint(cp, cp.adj_c1, in, w, stream, Win(), split_done, z16_ok(cp, cp.adj_c1, cp.va));
   } else if (stage == LFM_STAGE_FWD_S || stage == LFM_STAGE_ADJ_S) {
     const bool fwd = stage == LFM_STAGE_FWD_S;
     if (fwd ? !in : !out) return fail(LFM_E_INVALID, fwd ? "in is NULL" : "out is NULL");
     if (fwd ? !(cp.fwd_split && (cp.fwd_t == 2 || cp.fwd_t == 3)) : !(cp.adj_t == 2 || cp.adj_t == 3))
       return fail(LFM_E_INVALID, "the s pass of this camera is not a direct (band_v / spass) kernel");
     std::string err;
-    const bool h = fwd && cp.fwd_t == 3 && f16_fwd(cp, cp.fwd_c2);  // U as fp16 hi / lo (the FWD_T input), maxima of `in`
-    if (h && (st = k_amax(in, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
-    st = fwd ? (cp.fwd_t == 3 ? k_vpass_fwd(cp, cp.vf, in, w.z, stream, err, 0, -1, h ? w.am : nullptr) : k_spass_fwd(cp, in, w.z, stream, err))
-             : (cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, out, 0, stream, err) : k_spass_adj(cp, w.z, out, 0, stream, err));
+    if (fwd && cp.fwd_t == 3) {  // as in A_forward (2xFP16: maxima and split of `in`, U as fp16 hi / lo)
+      if (f16_fwd(cp, cp.fwd_c2)) {
+        uint16_t* x16 = cp.vf.d_h16 && cp.vf.BK == 32 ? reinterpret_cast<uint16_t*>(w.xt) : nullptr;
+        st = k_amax(in, cp.info.n_vox, w.am, stream, err);
+        if (st == LFM_OK && x16) st = k_split16(in, cp.info.n_vox, w.am, x16, x16 + cp.info.n_vox, stream, err);
+        if (st == LFM_OK) st = k_vpass_fwd(cp, cp.vf, in, w.z, stream, err, 0, -1, w.am, x16);
+      } else {
+        st = k_vpass_fwd(cp, cp.vf, in, w.z, stream, err);
+      }
+    } else if (fwd) {
+      st = k_spass_fwd(cp, in, w.z, stream, err);
+    } else {  // on the Z (fp16 when the t pass wrote it so) and maxima the last ADJ_T / adjoint left
+      const bool z16 = z16_ok(cp, cp.adj_c1, cp.va);
+      st = cp.adj_t == 3 ? k_vpass_adj(cp, cp.va, w.z, out, 0, stream, err, 0, -1, z16 ? w.am : nullptr, cp.adj_c1.ft->u_lsum)
+                         : k_spass_adj(cp, w.z, out, 0, stream, err);
+    }
     if (st != LFM_OK) return fail(st, err);
   } else {
     return fail(LFM_E_INVALID, "unknown stage");

@@ -18,6 +18,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cuda_fp16.h>
+
 #include "tc_sm100.h"
 
 namespace lfm {
@@ -29,6 +31,8 @@ struct UArgs {
   const float* amax;      // F16: n_amax partial maxima m_i; the source was written as fp16 hi + lo of 2^e src with
   int n_amax;             // e = u_data_exp(max m_i * amax_scale) by its producer (band_v / split16_kernel), so the
   float amax_scale;       // epilogue takes 2^-e back out
+  float out_scale16;      // OUT16 instances: the output is written as fp16 hi + lo of 2^e' out, e' =
+                          // u_data_exp(max m_i * out_scale16) (a bound on |out| over max |src| m_i: the row sums)
   const int32_t* blk_off; // per row tile: first block .. (row tiles of the table, n_tiles + 1 entries)
   const int32_t* blk_k0;  // per block: first source row (plan coordinates)
   float* out;
@@ -109,10 +113,12 @@ constexpr int U_THREADS = 384;
 constexpr int U_STAGE_OUT = 4096;  // per epilogue warp: 32 rows x 32 columns fp32, 128-byte swizzle (TMA store)
 constexpr size_t U_SMEM = (size_t)U_STAGES * U_STAGE_BYTES + 8 * U_STAGE_OUT + 1024 + 256;
 
-template <bool SPLIT, bool F16 = false>
+template <bool SPLIT, bool F16 = false, bool OUT16 = false>
 __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
                                                               const __grid_constant__ CUtensorMap out_map,
-                                                              const __grid_constant__ CUtensorMap lo_map, UArgs a) {
+                                                              const __grid_constant__ CUtensorMap lo_map,
+                                                              const __grid_constant__ CUtensorMap out_lo_map, UArgs a) {
+  static_assert(!OUT16 || (F16 && !SPLIT), "fp16 output: 2xFP16 form, no split-K");
   using namespace tc;
   constexpr int U_STAGES = UStage<F16>::STAGES, U_STAGE_BYTES = UStage<F16>::BYTES;
   static_assert(UStage<true>::STAGES * UStage<true>::BYTES == 4 * 49152, "same ring size");
@@ -283,6 +289,8 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
     uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
     float inv_sig = 1.f;  // 2xFP16: the data scale 2^-e (exact), applied before `scale`
     if constexpr (F16) inv_sig = pow2f(-u_data_exp(a.amax, a.n_amax, a.amax_scale));
+    float osig = 1.f;  // OUT16: the output's scale 2^e'
+    if constexpr (OUT16) osig = pow2f(u_data_exp(a.amax, a.n_amax, a.out_scale16));
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const UItem ui = u_item<SPLIT>(a, it);
       const int mt = ui.mt, nt = ui.nt;
@@ -318,6 +326,33 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       for (int c = 0; c < 128; c += 32) {
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
+        if constexpr (OUT16) {  // fp16 hi / lo of 2^e' out: two 32 x 32 tiles, 64-byte rows, 64-byte swizzle
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float x0 = osig * (a.scale * (inv_sig * acc[c + 8 * jj + 2 * i]));
+              const float x1 = osig * (a.scale * (inv_sig * acc[c + 8 * jj + 2 * i + 1]));
+              const __half2 hh = __floats2half2_rn(x0, x1);
+              const float2 hf = __half22float2(hh);
+              const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+              hw[i] = *reinterpret_cast<const uint32_t*>(&hh);
+              lw[i] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+            const int o = lane * 64 + ((jj ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(stg + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(stg + 2048 + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&out_map, c0 + c, r0, stg);
+            tma_store_2d(&out_lo_map, c0 + c, r0, stg + 2048);
+            bulk_commit();
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float4 v;

@@ -25,6 +25,7 @@ namespace lfm {
 
 struct VArgs {
   const float* B;          // weight images: block b at B + b * 32 * N floats (hi N x 16, then lo N x 16)
+  const uint16_t* H;       // IN16: fp16 weight images (2^wexp w split into hi + lo), block b at H + 2 b BK N
   const int32_t* blk_off;  // per item key (n * n_nt + nt): blocks [off, off+1)
   const int32_t* blk_k0;   // per block: first k (vx forward, s adjoint)
   int nz, n_mt, n_nt;      // table N-tiles per slice; items = nz * n_mt * nt_cnt, (n, mt, nt0 + j)
@@ -34,8 +35,10 @@ struct VArgs {
   int group;               // blocks per TMEM accumulator before it is drained
   float scale;
   int accumulate;
-  const float* amax;       // OUT16 (forward): LFM_AMAX_SLOTS partial maxima of |x^r| and a bound on the row sums of
-  float amax_scale;        // the s composite: U is written as fp16 hi + lo of 2^e U, e = u_data_exp(.) (tc_sm100.h)
+  const float* amax;       // LFM_AMAX_SLOTS partial maxima of the source of the data (x^r forward, y adjoint)
+  float amax_scale;        // OUT16 (forward): bound on the s composite's row sums -- U is written as fp16 hi + lo of
+                           // 2^e U, e = u_data_exp(amax, amax_scale) (tc_sm100.h)
+  float in_scale;          // IN16: the data arrives as fp16 hi + lo of 2^e data, e = u_data_exp(amax, in_scale)
 };
 
 
@@ -57,10 +60,11 @@ __device__ __forceinline__ void v_live(const VArgs& a, int key, int BK, int& lb0
 
 constexpr int V_THREADS = 384;
 
-template <int N, int BK, bool H = false>
+template <int N, int BK, bool H = false>  // H: 2xFP16 operands (data and weights pre-split into fp16 hi / lo)
 struct VCfg {
-  static constexpr int A_BYTES = 128 * BK * 4;        // data tile [128][BK] fp32
-  static constexpr int B_BYTES = N * BK * 4;          // one weight image [N][BK]
+  static constexpr int ES = H ? 2 : 4;                // operand element bytes
+  static constexpr int A_BYTES = 128 * BK * ES;       // data tile [128][BK] (hi, or lo)
+  static constexpr int B_BYTES = N * BK * ES;         // one weight image [N][BK]
   static constexpr int EC0 = N >= 256 ? 128 : N / 2;
   // staging per store: 32 rows x 32 fp32 columns, or (H: fp16 hi + lo output) 32 rows x 32 fp16 columns, twice
   static constexpr int OUT0 = 32 * (EC0 >= 32 ? 32 : EC0) * 4;
@@ -68,12 +72,13 @@ struct VCfg {
   static constexpr int NOB = (230912 - 16 * OUT0) / (2 * A_BYTES + 2 * B_BYTES) >= 2 ? 2 : 1;
   static constexpr int RING = 230912 - 8 * NOB * OUT0;  // 227 KB minus alignment slack and barriers
   static constexpr int STAGES = RING / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : RING / (2 * A_BYTES + 2 * B_BYTES);
-  static constexpr int SUB = BK < 32 ? BK : 32;      // sub-block width: one swizzle atom row (BK 64 = 2 sub-blocks)
+  static constexpr int SUB = BK * ES <= 128 ? BK : 128 / ES;  // sub-block width: one swizzle atom row (<= 128 B)
   static constexpr int KS = BK / SUB;
-  static constexpr int SUBA = 128 * SUB * 4;          // bytes of one data sub-tile [128][SUB]
-  static constexpr int SUBB = N * SUB * 4;            // bytes of one weight sub-image [N][SUB]
-  static constexpr int LAYOUT = SUB == 32 ? 2 : 4;    // UMMA K-major 128-byte (SUB 32) or 64-byte (SUB 16) swizzle
-  static constexpr int SBO = 8 * SUB * 4;             // 8-row core-matrix group stride
+  static constexpr int SUBA = 128 * SUB * ES;         // bytes of one data sub-tile [128][SUB]
+  static constexpr int SUBB = N * SUB * ES;           // bytes of one weight sub-image [N][SUB]
+  static constexpr int LAYOUT = SUB * ES == 128 ? 2 : 4;  // UMMA K-major 128-byte or 64-byte swizzle
+  static constexpr int SBO = 8 * SUB * ES;            // 8-row core-matrix group stride
+  static constexpr int KSTEP = 32 / ES;               // K per MMA (8 tf32, 16 fp16): 32 bytes of a row
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
   static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
@@ -91,12 +96,13 @@ struct VCfg {
   static constexpr int TCOLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
 };
 
-template <int N, int DIR, int BK, bool KWIN = false, bool OUT16 = false>
+template <int N, int DIR, int BK, bool KWIN = false, bool OUT16 = false, bool IN16 = false>
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
                                                               const __grid_constant__ CUtensorMap out_map,
-                                                              const __grid_constant__ CUtensorMap lo_map, VArgs a) {
+                                                              const __grid_constant__ CUtensorMap lo_map,
+                                                              const __grid_constant__ CUtensorMap a_lo_map, VArgs a) {
   using namespace tc;
-  using C = VCfg<N, BK, OUT16>;
+  using C = VCfg<N, BK, IN16>;
   static_assert(!OUT16 || (DIR == 0 && N == 256), "fp16 output: forward, 256-column tiles");
   extern __shared__ uint8_t v_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
@@ -142,13 +148,18 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         for (int b = b0; b < b1; ++b) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * C::STAGE;
-          mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
-          bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
+          mbar_arrive_expect_tx(&full[s], (IN16 ? 2 : 1) * C::A_BYTES + 2 * C::B_BYTES);
+          if constexpr (IN16) bulk_g2s(st + 2 * C::A_BYTES, a.H + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
+          else bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           const int k = __ldg(a.blk_k0 + b) - (KWIN ? a.k_lo : 0);
 #pragma unroll
           for (int j = 0; j < C::KS; ++j) {
             if (DIR == 0) tma_load_3d(st + j * C::SUBA, &a_map, k + j * C::SUB, mt * 128, n, &full[s]);   // (vx, vt, n)
             else tma_load_3d(st + j * C::SUBA, &a_map, k + j * C::SUB, n, mt * 128, &full[s]);            // (s, n, vt)
+            if constexpr (IN16) {  // the pre-split lo tile beside it
+              if (DIR == 0) tma_load_3d(st + C::A_BYTES + j * C::SUBA, &a_lo_map, k + j * C::SUB, mt * 128, n, &full[s]);
+              else tma_load_3d(st + C::A_BYTES + j * C::SUBA, &a_lo_map, k + j * C::SUB, n, mt * 128, &full[s]);
+            }
           }
           if (++s == C::STAGES) { s = 0; ph ^= 1; }
         }
@@ -156,8 +167,8 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
-      constexpr uint32_t IDESC2 = idesc_tf32(128, C::MERGE ? 2 * N : N, 0, 0);
+      constexpr uint32_t IDESC = IN16 ? idesc_f16(128, N, 0, 0) : idesc_tf32(128, N, 0, 0);
+      constexpr uint32_t IDESC2 = IN16 ? idesc_f16(128, C::MERGE ? 2 * N : N, 0, 0) : idesc_tf32(128, C::MERGE ? 2 * N : N, 0, 0);
       const uint64_t d0 = smem_desc(smem_u32(sm), 16, C::SBO, C::LAYOUT);  // all operands K-major, same swizzle
       int s = 0;
       uint32_t ph = 0;
@@ -175,18 +186,27 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           const uint32_t d = tmem + buf * C::ACC;
           const int g1 = min(b1, g0 + a.group);
           for (int j = g0; j < g1; ++j) {
-            mbar_wait(&conv[s], ph);
+            mbar_wait(IN16 ? &full[s] : &conv[s], ph);  // 2xFP16: the data arrives split
             tc_fence_after();
             const uint64_t so = (uint64_t)((s * C::STAGE) >> 4);  // stage offset in the descriptors' address field
 #pragma unroll
-            for (int kq = 0; kq < BK / 8; ++kq) {
-              const int sj = kq / (C::SUB / 8), kk = kq % (C::SUB / 8);
+            for (int kq = 0; kq < BK / C::KSTEP; ++kq) {
+              const int sj = kq / (C::SUB / C::KSTEP), kk = kq % (C::SUB / C::KSTEP);
               const uint64_t ao = (uint64_t)((sj * C::SUBA + 32 * kk) >> 4), bo = (uint64_t)((sj * C::SUBB + 32 * kk) >> 4);
               const uint64_t ahi = d0 + so + ao;
               const uint64_t alo = d0 + so + (C::A_BYTES >> 4) + ao;
               const uint64_t bhi = d0 + so + ((2 * C::A_BYTES) >> 4) + bo;
               const uint64_t blo = d0 + so + ((2 * C::A_BYTES + C::B_BYTES) >> 4) + bo;
-              if constexpr (C::MERGE) {
+              if constexpr (IN16) {
+                if constexpr (C::MERGE) {
+                  mma_bf16_ss(d, ahi, bhi, IDESC2, (j != g0 || kq != 0) ? 1u : 0u);
+                  mma_bf16_ss(d, alo, bhi, IDESC, 1u);
+                } else {
+                  mma_bf16_ss(d, ahi, blo, IDESC, (j != g0 || kq != 0) ? 1u : 0u);
+                  mma_bf16_ss(d, alo, bhi, IDESC, 1u);
+                  mma_bf16_ss(d, ahi, bhi, IDESC, 1u);
+                }
+              } else if constexpr (C::MERGE) {
                 // D[:, 0:N] += A_hi B_hi, D[:, N:2N] += A_hi B_lo (one MMA), then D[:, 0:N] += A_lo B_hi
                 mma_tf32_ss(d, ahi, bhi, IDESC2, (j != g0 || kq != 0) ? 1u : 0u);
                 mma_tf32_ss(d, alo, bhi, IDESC, 1u);
@@ -205,6 +225,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
       }
     }
   } else if (warp < 4) {
+    if constexpr (!IN16) {  // (2xFP16: nothing to split)
     // lo split of the data tile: 128 x BK floats, 64 threads
     const int t = threadIdx.x - 64;
     int s = 0;
@@ -240,6 +261,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         if (++s == C::STAGES) { s = 0; ph ^= 1; }
       }
     }
+    }
   } else {
     // drain + epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (voxel rows), columns [h EC, (h+1) EC)
     constexpr int EC = C::EC, OC = C::OC;
@@ -250,6 +272,8 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
     uint32_t tph = 0;  // phase bit of accumulator buffer b at bit b
     float sig = 1.f;  // OUT16: the data scale 2^e of the 2xFP16 t pass that reads U
     if constexpr (OUT16) sig = pow2f(u_data_exp(a.amax, LFM_AMAX_SLOTS, a.amax_scale));
+    float in_inv = 1.f;  // IN16: 2^-e of the data's scale (the weights' 2^-wexp is folded into a.scale)
+    if constexpr (IN16) in_inv = pow2f(-u_data_exp(a.amax, LFM_AMAX_SLOTS, a.in_scale));
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int nt = a.nt0 + it % a.nt_cnt, mt = (it / a.nt_cnt) % a.n_mt, n = it / (a.nt_cnt * a.n_mt);
       const int key = n * a.n_nt + nt;
@@ -284,6 +308,10 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         buf ^= 1;
+      }
+      if constexpr (IN16) {
+#pragma unroll
+        for (int c = 0; c < EC; ++c) acc[c] *= in_inv;  // exact
       }
       const int vt0 = mt * 128 + 32 * q, c0 = nt * N + h * EC;
 #pragma unroll

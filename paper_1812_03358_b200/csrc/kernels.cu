@@ -189,6 +189,7 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
     lsum = std::max(lsum, r);
   }
   T.lsum = (float)(lsum * (1.0 + 1e-6));
+  std::vector<float> raw;  // the fp32 weights in the hi image's positions (source of the fp16 split)
   std::vector<char> any(f.n_src + 32);
   const uint32_t smask = BK >= 32 ? 7u : 3u;  // Swizzle<3,4,3> (128 B) or Swizzle<2,4,3> (64 B)
   for (int m = 0; m < f.n_tables; ++m)
@@ -204,11 +205,12 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
       int last = -(1 << 30);
       for (int kn = 0; kn < f.n_src; ++kn) {
         if (!any[kn] || kn < last + BK) continue;
-        const int k = kn & ~3;  // TMA: the innermost box coordinate must sit on a 16-byte boundary
+        const int k = kn & ~7;  // TMA: the innermost box coordinate must sit on a 16-byte boundary (fp16: 8 elements)
         last = k;
         T.k0.push_back(k);
         const size_t base = T.img.size();
         T.img.resize(base + (size_t)2 * BK * N, 0.f);
+        raw.resize(base / 2 + (size_t)BK * N, 0.f);
         for (int r = r0; r < r1; ++r) {
           const size_t idx = (size_t)m * f.n_rows + r;
           for (int kk = 0; kk < BK; ++kk) {
@@ -222,11 +224,37 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
             const size_t so = (size_t)sj * N * sub;
             T.img[base + so + o / 4] = wh;
             T.img[base + (size_t)BK * N + so + o / 4] = wl;
+            raw[base / 2 + so + o / 4] = w;
           }
         }
       }
     }
   T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
+  // 2xFP16 images: the fp32 weights w (one rounding from fp64), 2^wexp w -> fp16 hi + lo in the same (row, k)
+  // positions, 64-byte rows with the 64-byte swizzle
+  T.h16.clear();
+  if (BK == 32) {
+    float wmax = 0.f;
+    for (size_t i = 0; i < raw.size(); ++i) wmax = std::max(wmax, std::fabs(raw[i]));
+    int ex = 0;
+    if (wmax > 0.f) std::frexp((double)wmax * 1.01, &ex);
+    T.wexp = wmax > 0.f ? 15 - ex : 0;
+    const size_t nb = T.k0.size();
+    T.h16.assign(nb * 2 * BK * N, 0);
+    for (size_t b = 0; b < nb; ++b)
+      for (int r = 0; r < N; ++r)
+        for (int kk = 0; kk < BK; ++kk) {
+          uint32_t o32 = (uint32_t)(r * 128 + kk * 4);  // fp32 image: 128-byte rows, 128-byte swizzle
+          o32 ^= ((o32 >> 7) & 7u) << 4;
+          const float w = raw[b * BK * N + o32 / 4];
+          const float ws = (float)std::ldexp((double)w, T.wexp);
+          const uint16_t wh = f2h_rn(ws), wl = f2h_rn(ws - h2f(wh));
+          uint32_t o16 = (uint32_t)(r * 64 + kk * 2);
+          o16 ^= ((o16 >> 7) & 3u) << 4;
+          T.h16[b * 2 * BK * N + o16 / 2] = wh;
+          T.h16[b * 2 * BK * N + (size_t)BK * N + o16 / 2] = wl;
+        }
+  }
 }
 
 static void build_vtabs(const BandFamily& ff, const BandFamily& fa, VTab& vf, VTab& va) {
@@ -254,14 +282,16 @@ static lfm_status upload_vtab(VTab& T, size_t& bytes, std::string& err) {
   if ((st = dev_upload(&T.d_off, T.off.data(), T.off.size() * 4, err)) != LFM_OK) return st;
   if ((st = dev_upload(&T.d_k0, k0.data(), k0.size() * 4, err)) != LFM_OK) return st;
   if (!T.img.empty() && (st = dev_upload(&T.d_img, T.img.data(), T.img.size() * 4, err)) != LFM_OK) return st;
-  bytes += T.off.size() * 4 + k0.size() * 4 + T.img.size() * 4;
-  std::vector<float>().swap(T.img);  // host copy not needed after upload
+  if (!T.h16.empty() && (st = dev_upload(&T.d_h16, T.h16.data(), T.h16.size() * 2, err)) != LFM_OK) return st;
+  bytes += T.off.size() * 4 + k0.size() * 4 + T.img.size() * 4 + T.h16.size() * 2;
+  std::vector<float>().swap(T.img);  // host copies not needed after upload
+  std::vector<uint16_t>().swap(T.h16);
   return LFM_OK;
 }
 
 static void free_vtab(VTab& T) {
-  dfree(T.d_off); dfree(T.d_k0); dfree(T.d_img);
-  T.d_off = nullptr; T.d_k0 = nullptr; T.d_img = nullptr;
+  dfree(T.d_off); dfree(T.d_k0); dfree(T.d_img); dfree(T.d_h16);
+  T.d_off = nullptr; T.d_k0 = nullptr; T.d_img = nullptr; T.d_h16 = nullptr;
 }
 
 lfm_status upload_camera(CameraPlan& cp, std::string& err) {
@@ -419,26 +449,27 @@ static lfm_status encode3(CUtensorMap* map, const void* base, const long long di
   return st;
 }
 
-template <int N, int DIR, int BK, bool OUT16 = false>
+template <int N, int DIR, int BK, bool OUT16 = false, bool IN16 = false>
 static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err, int nt0 = 0, int nt_cnt = -1,
                                 int k_lo = 0, int k_hi = 1 << 30, const CUtensorMap* lom = nullptr,
-                                const float* amax = nullptr) {
+                                const float* amax = nullptr, const CUtensorMap* alom = nullptr, float in_scale = 1.f) {
   // the K-window instantiation only when a window cuts the K range (adjoint column shards)
   const bool kwin = k_lo > 0 || k_hi < (1 << 30);
   static bool attr[LFM_MAX_DEV][2];
   const int dv = cur_dev();
-  constexpr size_t SMEM = VCfg<N, BK, OUT16>::SMEM;
+  constexpr size_t SMEM = VCfg<N, BK, IN16>::SMEM;
   if (!attr[dv][kwin]) {
-    cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true, OUT16>,
+    cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true, OUT16, IN16>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)
-                         : cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, false, OUT16>,
+                         : cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, false, OUT16, IN16>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
     if (e != cudaSuccess) return cuda_check(cudaGetLastError(), "band_v smem attribute", err);
     attr[dv][kwin] = true;
   }
   VArgs v;
   v.B = T.d_img;
+  v.H = T.d_h16;
   v.blk_off = T.d_off;
   v.blk_k0 = T.d_k0;
   v.nz = nz;
@@ -449,32 +480,50 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   v.k_lo = kwin ? k_lo : 0;
   v.k_hi = k_hi;
   v.group = 4;
-  v.scale = scale;
+  v.scale = IN16 ? (float)std::ldexp((double)scale, -T.wexp) : scale;
   v.accumulate = accumulate;
   v.amax = amax;
   v.amax_scale = T.lsum;
+  v.in_scale = in_scale;
   const int items = v.nz * v.n_mt * v.nt_cnt;
   if (items <= 0) return LFM_OK;
   const int grid = std::min(items, g_num_sms());
   const CUtensorMap& lm = lom ? *lom : om;
-  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, v);
-  else band_v_kernel<N, DIR, BK, false, OUT16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, v);
+  const CUtensorMap& alm = alom ? *alom : am;
+  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
+  else band_v_kernel<N, DIR, BK, false, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
 
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0, int c1, const float* amax) {
+                       int c0, int c1, const float* amax, const uint16_t* x16) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
   if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
-  const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
-  const int ab[3] = {T.BK, 128, 1};
-  lfm_status st = encode3(&am, x, ad, as, ab, T.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
-  if (st != LFM_OK) return st;
   const int ob[3] = {32, 1, 32};
   // column window [c0, c1): only the N-tiles (256 detector columns) that meet it
   const int nt0 = std::max(0, c0) / T.N, nt1 = c1 < 0 ? T.n_nt : (c1 + T.N - 1) / T.N;
+  lfm_status st;
+  if (amax && x16 && T.d_h16 && T.BK == 32) {  // 2xFP16 in and out: x^r pre-split (fp16 hi, lo = hi + n_vox)
+    const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 2, (long long)nx * ny * 2};
+    const int ab[3] = {32, 128, 1};
+    CUtensorMap alm, lm;
+    const uint16_t* hi = reinterpret_cast<const uint16_t*>(U);
+    const uint16_t* lo = hi + (size_t)nd * nz * ny;
+    const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 2, (long long)nz * nd * 2};
+    if ((st = encode3(&am, x16, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
+        (st = encode3(&alm, x16 + cp.info.n_vox, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
+        (st = encode3(&om, hi, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
+        (st = encode3(&lm, lo, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+      return st;
+    return launch_band_v<256, 0, 32, true, true>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0, 0, 1 << 30, &lm,
+                                                 amax, &alm, 1.f);
+  }
+  const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
+  const int ab[3] = {T.BK, 128, 1};
+  st = encode3(&am, x, ad, as, ab, T.BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
+  if (st != LFM_OK) return st;
   if (amax) {  // fp16 hi / lo of 2^e U (the 2xFP16 t pass input): two [vt][n][s] half arrays
     const uint16_t* hi = reinterpret_cast<const uint16_t*>(U);
     const uint16_t* lo = hi + (size_t)nd * nz * ny;
@@ -492,19 +541,31 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
 }
 
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
-                       std::string& err, int c0, int c1) {
+                       std::string& err, int c0, int c1, const float* amax, float in_scale) {
+  const bool in16 = amax && T.d_h16 && T.BK == 32 && T.N == 16;
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
   if (!T.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
   // column window [c0, c1) of Z (= of y): the data map starts at c0 and is c1 - c0 wide, so columns outside read
   // as zeros; K blocks outside the window are skipped (items without live blocks write zeros)
   const int k_lo = std::max(0, c0), k_hi = (c1 < 0 || c1 >= nd) ? (1 << 30) : c1;
   if (k_lo % 4) { err = "band_v: a column window must start on a multiple of 4"; return LFM_E_INVALID; }
-  CUtensorMap am, om;
-  const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
-  Z += k_lo;
-  const int ab[3] = {T.BK < 32 ? T.BK : 32, 1, 128};
-  lfm_status st = encode3(&am, Z, ad, as, ab, T.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
-  if (st != LFM_OK) return st;
+  CUtensorMap am, om, alm;
+  lfm_status st;
+  if (in16) {  // Z as fp16 hi (Z reinterpreted) and lo (the next nd nz ny halves) of 2^e Z
+    const uint16_t* zh = reinterpret_cast<const uint16_t*>(Z);
+    const uint16_t* zl = zh + (size_t)nd * nz * ny;
+    const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 2, (long long)nz * nd * 2};
+    const int ab[3] = {32, 1, 128};
+    if ((st = encode3(&am, zh + k_lo, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
+        (st = encode3(&alm, zl + k_lo, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+      return st;
+  } else {
+    const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
+    Z += k_lo;
+    const int ab[3] = {T.BK < 32 ? T.BK : 32, 1, 128};
+    st = encode3(&am, Z, ad, as, ab, T.BK >= 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, err);
+    if (st != LFM_OK) return st;
+  }
   const long long od[3] = {nx, ny, nz}, os[2] = {(long long)nx * 4, (long long)nx * ny * 4};
   const int ob[3] = {T.N / 2, 32, 1};
   if ((st = encode3(&om, out, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE, err)) != LFM_OK) return st;
@@ -532,6 +593,9 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, floa
     }
     if (nt_cnt == 0) return LFM_OK;
   }
+  if (in16)
+    return launch_band_v<16, 1, 32, false, true>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi,
+                                                 nullptr, amax, &alm, in_scale);
   if (T.N == 32)
     return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi)
                       : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi);
@@ -1695,7 +1759,15 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
       if (st != LFM_OK) return st;
       lmap = map;
     }
-    if (ksplit > 1)
+    const bool out16 = f16 && h16.out_hi;
+    CUtensorMap olmap;
+    if (out16) {
+      if (ksplit > 1 || accumulate) { err = "band_u: fp16 output without split-K or accumulation"; return LFM_E_INVALID; }
+      const long long oo = (long long)b0 * a.out_stride;
+      if ((st = encode_map(&omap, h16.out_hi + oo, op.n_os, op.n_ot, a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
+          (st = encode_map(&olmap, h16.out_lo + oo, op.n_os, op.n_ot, a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+        return st;
+    } else if (ksplit > 1)
       st = encode_map(&omap, part, op.n_os, (int)(ksplit * kc_rows), a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, err);
     else
       st = encode_map(&omap, out + (long long)b0 * a.out_stride, op.n_os, op.n_ot, a.out_pitch, 32, 32,
@@ -1707,7 +1779,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
       if (cudaFuncSetAttribute(band_u_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
           cudaFuncSetAttribute(band_u_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
           cudaFuncSetAttribute(band_u_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
-          cudaFuncSetAttribute(band_u_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
+          cudaFuncSetAttribute(band_u_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(band_u_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM) != cudaSuccess)
         return cuda_check(cudaGetLastError(), "band_u smem attribute", err);
       smem_set[dv] = true;
     }
@@ -1718,6 +1791,7 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.amax = h16.amax;
     u.n_amax = LFM_AMAX_SLOTS;
     u.amax_scale = h16.amax_scale;
+    u.out_scale16 = h16.out_scale16;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
     u.blk_k0 = op.ft->d_uk0;
     u.out = out + (long long)b0 * a.out_stride;
@@ -1745,12 +1819,13 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.tm_nz = op.ft->u_nz;
     if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
     const int grid_u = std::min(u.n_mt * u.n_nt * u.ksplit, g_num_sms());
-    if (f16) {
-      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
-      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+    if (out16) band_u_kernel<false, true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, olmap, u);
+    else if (f16) {
+      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
     } else {
-      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
-      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, u);
+      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
     }
     ++g_launches;
     if (ksplit > 1) {

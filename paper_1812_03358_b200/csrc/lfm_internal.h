@@ -75,6 +75,7 @@ struct BandFamily {
   // in the K-major 32-byte-swizzled layout (element (m, k) at byte m*32 + k*2 with bit 4 ^= bit 7): 4096 halves
   std::vector<uint16_t> u_h;
   int u_wexp = 0;                          // max |w| 2^u_wexp in [2^14, 2^15)
+  float u_lsum = 0.f;                      // max over rows of sum |w| (fp32 weights): |out| <= u_lsum max |src|
   uint16_t* d_uh = nullptr;
   // the same with groups of 8 rows (weights 8 per source cell): half the source loads per FMA
   std::vector<int32_t> m8_off, m8_seg;
@@ -155,6 +156,11 @@ struct ShearPass {
 struct VTab {
   int N = 0, n_nt = 0, BK = 16;
   float lsum = 0.f;  // max over rows (output columns) of sum |w|: |U| <= lsum max |x| (the 2xFP16 data scale)
+  // 2xFP16 images (BK 32 only): 2^wexp w split into fp16 hi + lo, same K-major layout with 64-byte rows (64-byte
+  // swizzle), hi N x BK then lo N x BK per block
+  std::vector<uint16_t> h16;
+  int wexp = 0;
+  uint16_t* d_h16 = nullptr;
   std::vector<int32_t> off, k0;
   std::vector<float> img;
   int32_t* d_off = nullptr;
@@ -232,6 +238,8 @@ lfm_status autotune_camera(CameraPlan& cp, std::string& err);
 lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subsets, CameraPlan& out,
                         std::string& err);
 lfm_status prepare_subsets(CameraPlan& cp, std::string& err);
+uint16_t f2h_rn(float x);  // fp32 -> fp16 bits, round to nearest even (|x| < 65520)
+float h2f(uint16_t h);
 // kernels.cu
 lfm_status upload_camera(CameraPlan& cp, std::string& err);
 void free_camera(CameraPlan& cp);
@@ -245,6 +253,11 @@ struct F16Src {
   const uint16_t* lo = nullptr;
   const float* amax = nullptr;
   float amax_scale = 1.f;
+  // optional fp16 output (the adjoint's Z for band_v's 2xFP16 form): hi / lo arrays shaped like the fp32 output,
+  // 2^e' out with e' = u_data_exp(amax, out_scale16); not with split-K or accumulation
+  uint16_t* out_hi = nullptr;
+  uint16_t* out_lo = nullptr;
+  float out_scale16 = 1.f;
 };
 lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int n_out, int accumulate,
                       void* stream, std::string& err, int out_r0 = 0, int out_r1 = -1, int win_r0 = 0,
@@ -255,15 +268,21 @@ lfm_status k_transpose(const float* in, float* out, int B, int R, int C, long lo
 lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* stream, std::string& err);
 // amax != nullptr: U is written as fp16 hi (U reinterpreted as uint16_t*, nd*nz*ny halves) then lo (the next
 // nd*nz*ny halves) of 2^e U with e from the partial maxima of |x| (amax_kernel) and T.lsum -- the 2xFP16 t pass input
+// x16 != nullptr too (and BK 32 fp16 tables): 2xFP16 input, x16 = fp16 hi (n_vox) then lo of 2^e x (split16_kernel
+// with the same maxima)
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0 = 0, int c1 = -1, const float* amax = nullptr);
+                       int c0 = 0, int c1 = -1, const float* amax = nullptr, const uint16_t* x16 = nullptr);
 // LFM_AMAX_SLOTS partial maxima of |src[0, n)| into part (one kernel)
 lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err);
 // fp16 hi / lo of 2^e src over n floats (e from the partial maxima `amax` of src), for the 2xFP16 band_u form
 lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t* hi, uint16_t* lo, void* stream,
                      std::string& err);
+// amax != nullptr (and BK 32, N 16 fp16 tables): Z is fp16 hi then lo of 2^e Z, e = u_data_exp(amax, in_scale)
+// (band_u adjoint's fp16 output); otherwise fp32 Z
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
-                       std::string& err, int c0 = 0, int c1 = -1);
+                       std::string& err, int c0 = 0, int c1 = -1, const float* amax = nullptr, float in_scale = 1.f);
+// whether k_vpass_adj can take an fp16 Z for table T
+inline bool vpass_adj_in16(const VTab& T) { return T.d_h16 && T.BK == 32 && T.N == 16; }
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);

@@ -398,7 +398,7 @@ static int umma_row(const BandFamily& f, int t, int m) {
 
 // fp32 -> fp16 bits, round to nearest even (normal and subnormal; |x| < 65520 assumed, as the callers scale to
 // below 2^15), and back
-static uint16_t f2h_rn(float x) {
+uint16_t f2h_rn(float x) {
   uint32_t u;
   std::memcpy(&u, &x, 4);
   const uint32_t sign = (u >> 16) & 0x8000u;
@@ -411,7 +411,7 @@ static uint16_t f2h_rn(float x) {
   const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) >> 13;  // mantissa rounded to 10 bits (carry into exponent)
   return (uint16_t)(sign | (r - ((127u - 15u) << 10)));
 }
-static float h2f(uint16_t h) {
+float h2f(uint16_t h) {
   const int e = (h >> 10) & 31, m = h & 1023;
   const double v = e == 0 ? std::ldexp((double)m, -24) : std::ldexp(1.0 + m / 1024.0, e - 15);
   return (float)((h & 0x8000) ? -v : v);
@@ -474,8 +474,16 @@ static void build_umma(BandFamily& f) {
   f.u_off[(size_t)f.n_tables * nt] = (int)f.u_k0.size();
   // 2xFP16 images: w 2^e split into fp16 hi + lo, e so that max |w| 2^e lies in [2^14, 2^15)
   float wmax = 0.f;
-  for (size_t idx = 0; idx < (size_t)f.n_tables * f.n_rows; ++idx)
-    for (int e = 0; e < f.len[idx]; ++e) wmax = std::max(wmax, std::fabs((float)f.w64[idx * f.taps + e]));
+  double lsum = 0;
+  for (size_t idx = 0; idx < (size_t)f.n_tables * f.n_rows; ++idx) {
+    double r = 0;
+    for (int e = 0; e < f.len[idx]; ++e) {
+      wmax = std::max(wmax, std::fabs((float)f.w64[idx * f.taps + e]));
+      r += std::fabs((double)(float)f.w64[idx * f.taps + e]);
+    }
+    lsum = std::max(lsum, r);
+  }
+  f.u_lsum = (float)(lsum * (1.0 + 1e-6));
   int ex = 0;
   if (wmax > 0.f) std::frexp((double)wmax * (1.0 + 1e-6), &ex);
   f.u_wexp = wmax > 0.f ? 15 - ex : 0;
