@@ -44,13 +44,14 @@ struct DevGuard {
 };
 
 struct WsLayout {
-  size_t r0, r1, xt, f, s, s2, z, zt, p, am, h16, total;
+  size_t r0, r1, xt, f, s, s2, z, zt, p, am, h16, rs, total;
 };
 
 WsLayout layout(const lfm_plan_s* p) {
-  size_t V = 0, F = 0, S = 0, Z = 0, P = 0;
+  size_t V = 0, F = 0, S = 0, Z = 0, P = 0, R = 0;
   for (const CameraPlan& c : p->cams) {
     P = std::max(P, (size_t)c.info.n_pix * 4);
+    R = std::max(R, (size_t)c.info.ny * c.info.nz * 4);
     V = std::max(V, (size_t)c.info.n_vox * 4);
     F = std::max(F, c.ws_fields);
     Z = std::max(Z, c.ws_z);
@@ -68,7 +69,8 @@ WsLayout layout(const lfm_plan_s* p) {
   L.p = L.zt + al256(Z);
   L.am = L.p + al256(4096 * 8 * 4);
   L.h16 = L.am + al256(LFM_AMAX_SLOTS * 4);
-  L.total = L.h16 + al256(P);
+  L.rs = L.h16 + al256(P);
+  L.total = L.rs + al256(R);
   return L;
 }
 
@@ -77,6 +79,7 @@ struct Ws {
   double* p;
   float* am;      // partial maxima of the 2xFP16 t-pass input's source: of x^r (forward), of y (adjoint)
   uint16_t* h16;  // fp16 hi (n_pix) then lo (n_pix) of 2^e y: the adjoint t pass input in the 2xFP16 form
+  float* rs;      // per-row inverse scales of the row-scaled fp16 split of x^r (nz ny)
 };
 
 lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
@@ -96,6 +99,7 @@ lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
   w.p = (double*)(b + L.p);
   w.am = (float*)(b + L.am);
   w.h16 = (uint16_t*)(b + L.h16);
+  w.rs = (float*)(b + L.rs);
   return LFM_OK;
 }
 
@@ -212,13 +216,14 @@ static lfm_status vt_forward(const CameraPlan& cp, const VTab& T, const SepOp& c
     // x^r pre-split into fp16 hi / lo (w.xt) when band_v has its fp16 images: no split warps in either kernel
     static const bool no_x16 = std::getenv("LFM_NO_X16") != nullptr;  // A/B: band_v splits x^r itself
     uint16_t* x16 = T.d_h16 && T.BK == 32 && !no_x16 ? reinterpret_cast<uint16_t*>(w.xt) : nullptr;
-    if (!amax_done) {
-      if ((st = k_amax(xr, cp.info.n_vox, w.am, stream, err)) != LFM_OK) return fail(st, err);
-      if (x16 && (st = k_split16(xr, cp.info.n_vox, w.am, x16, x16 + cp.info.n_vox, stream, err)) != LFM_OK)
-        return fail(st, err);
+    if (x16 && cp.info.nx % 8) x16 = nullptr;  // fp16 rows of x^r must start on 16-byte boundaries
+    if (!amax_done) {  // one pass: row-scaled split (x16) and the maxima of x^r, or the maxima alone
+      st = x16 ? k_split16_rows(xr, cp.info.ny * cp.info.nz, cp.info.nx, w.am, w.rs, x16, x16 + cp.info.n_vox, stream, err)
+               : k_amax(xr, cp.info.n_vox, w.am, stream, err);
+      if (st != LFM_OK) return fail(st, err);
     }
     amax_done = true;
-    if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1, w.am, x16)) != LFM_OK) return fail(st, err);
+    if ((st = k_vpass_fwd(cp, T, xr, w.z, stream, err, win.c0, win.c1, w.am, x16, w.rs)) != LFM_OK) return fail(st, err);
     F16Src h;
     h.hi = reinterpret_cast<const uint16_t*>(w.z);
     h.lo = h.hi + (size_t)cp.cf[0].n_rows * cp.info.nz * cp.info.ny;
@@ -696,10 +701,10 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
     std::string err;
     if (fwd && cp.fwd_t == 3) {  // as in A_forward (2xFP16: maxima and split of `in`, U as fp16 hi / lo)
       if (f16_fwd(cp, cp.fwd_c2)) {
-        uint16_t* x16 = cp.vf.d_h16 && cp.vf.BK == 32 ? reinterpret_cast<uint16_t*>(w.xt) : nullptr;
-        st = k_amax(in, cp.info.n_vox, w.am, stream, err);
-        if (st == LFM_OK && x16) st = k_split16(in, cp.info.n_vox, w.am, x16, x16 + cp.info.n_vox, stream, err);
-        if (st == LFM_OK) st = k_vpass_fwd(cp, cp.vf, in, w.z, stream, err, 0, -1, w.am, x16);
+        uint16_t* x16 = cp.vf.d_h16 && cp.vf.BK == 32 && cp.info.nx % 8 == 0 ? reinterpret_cast<uint16_t*>(w.xt) : nullptr;
+        st = x16 ? k_split16_rows(in, cp.info.ny * cp.info.nz, cp.info.nx, w.am, w.rs, x16, x16 + cp.info.n_vox, stream, err)
+                 : k_amax(in, cp.info.n_vox, w.am, stream, err);
+        if (st == LFM_OK) st = k_vpass_fwd(cp, cp.vf, in, w.z, stream, err, 0, -1, w.am, x16, w.rs);
       } else {
         st = k_vpass_fwd(cp, cp.vf, in, w.z, stream, err);
       }

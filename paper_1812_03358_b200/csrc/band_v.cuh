@@ -39,6 +39,8 @@ struct VArgs {
   float amax_scale;        // OUT16 (forward): bound on the s composite's row sums -- U is written as fp16 hi + lo of
                            // 2^e U, e = u_data_exp(amax, amax_scale) (tc_sm100.h)
   float in_scale;          // IN16: the data arrives as fp16 hi + lo of 2^e data, e = u_data_exp(amax, in_scale)
+  const float* rinv;       // IN16 forward: per data row (n ny + vt) scales instead: the row was split as 2^e_row x,
+  int ny;                  // rinv[row] = 2^-e_row (split16_rows_kernel)
 };
 
 
@@ -310,8 +312,13 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         buf ^= 1;
       }
       if constexpr (IN16) {
+        float f = in_inv;
+        if (a.rinv) {  // this lane's voxel row of slice n
+          const int vt = mt * 128 + 32 * q + lane;
+          f = vt < a.ny ? __ldg(a.rinv + (size_t)n * a.ny + vt) : 1.f;
+        }
 #pragma unroll
-        for (int c = 0; c < EC; ++c) acc[c] *= in_inv;  // exact
+        for (int c = 0; c < EC; ++c) acc[c] *= f;  // exact
       }
       const int vt0 = mt * 128 + 32 * q, c0 = nt * N + h * EC;
 #pragma unroll

@@ -453,7 +453,8 @@ template <int N, int DIR, int BK, bool OUT16 = false, bool IN16 = false>
 static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err, int nt0 = 0, int nt_cnt = -1,
                                 int k_lo = 0, int k_hi = 1 << 30, const CUtensorMap* lom = nullptr,
-                                const float* amax = nullptr, const CUtensorMap* alom = nullptr, float in_scale = 1.f) {
+                                const float* amax = nullptr, const CUtensorMap* alom = nullptr, float in_scale = 1.f,
+                                const float* rinv = nullptr) {
   // the K-window instantiation only when a window cuts the K range (adjoint column shards)
   const bool kwin = k_lo > 0 || k_hi < (1 << 30);
   static bool attr[LFM_MAX_DEV][2];
@@ -485,6 +486,8 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   v.amax = amax;
   v.amax_scale = T.lsum;
   v.in_scale = in_scale;
+  v.rinv = rinv;
+  v.ny = ny;
   const int items = v.nz * v.n_mt * v.nt_cnt;
   if (items <= 0) return LFM_OK;
   const int grid = std::min(items, g_num_sms());
@@ -497,7 +500,7 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
 }
 
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0, int c1, const float* amax, const uint16_t* x16) {
+                       int c0, int c1, const float* amax, const uint16_t* x16, const float* rinv) {
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.cf[0].n_rows;
   if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
@@ -518,7 +521,7 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
         (st = encode3(&lm, lo, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
       return st;
     return launch_band_v<256, 0, 32, true, true>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0, 0, 1 << 30, &lm,
-                                                 amax, &alm, 1.f);
+                                                 amax, &alm, 1.f, rinv);
   }
   const long long ad[3] = {nx, ny, nz}, as[2] = {(long long)nx * 4, (long long)nx * ny * 4};
   const int ab[3] = {T.BK, 128, 1};
@@ -1644,6 +1647,75 @@ __global__ void split16_kernel(const float* __restrict__ src, long long n, const
     hi[i] = *reinterpret_cast<const uint16_t*>(&h);
     lo[i] = *reinterpret_cast<const uint16_t*>(&l);
   }
+}
+
+// Row-scaled fp16 split in one pass (the A operand of band_v's 2xFP16 forward, whose rows are the MMA's M rows, so a
+// scale per row is undone per output row): one warp per row of `len` floats, e_row from the row's maximum
+// (u_data_exp), hi / lo of 2^e_row src, rinv[row] = 2^-e_row; the per-CTA maxima of |src| go to part (CTA 0
+// zero-fills the other LFM_AMAX_SLOTS) for the global scale of the next stage.
+__global__ void split16_rows_kernel(const float* __restrict__ src, int rows, int len, float* __restrict__ part,
+                                    float* __restrict__ rinv, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const bool vec = (len & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (len & 7) == 0;
+  uint32_t cmax = 0;
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    const float* r = src + (long long)row * len;
+    uint32_t m = 0;
+    if (vec) {
+      for (int c = 4 * lane; c < len; c += 128) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(r + c));
+        m = max(max(max(m, __float_as_uint(v.x) & 0x7fffffffu), max(__float_as_uint(v.y) & 0x7fffffffu,
+                __float_as_uint(v.z) & 0x7fffffffu)), __float_as_uint(v.w) & 0x7fffffffu);
+      }
+    } else {
+      for (int c = lane; c < len; c += 32) m = max(m, __float_as_uint(__ldg(r + c)) & 0x7fffffffu);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    cmax = max(cmax, m);
+    const int e = data_exp(__uint_as_float(m));
+    const float sig = pow2f(e);
+    if (lane == 0) rinv[row] = pow2f(-e);
+    uint16_t* h = hi + (long long)row * len;
+    uint16_t* l = lo + (long long)row * len;
+    if (vec) {
+      for (int c = 4 * lane; c < len; c += 128) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(r + c));
+        const float x0 = sig * v.x, x1 = sig * v.y, x2 = sig * v.z, x3 = sig * v.w;
+        const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+        *reinterpret_cast<uint2*>(h + c) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+        *reinterpret_cast<uint2*>(l + c) = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+      }
+    } else {
+      for (int c = lane; c < len; c += 32) {
+        const float x = sig * __ldg(r + c);
+        const __half hh = __float2half_rn(x), ll = __float2half_rn(x - __half2float(hh));
+        h[c] = *reinterpret_cast<const uint16_t*>(&hh);
+        l[c] = *reinterpret_cast<const uint16_t*>(&ll);
+      }
+    }
+  }
+  __shared__ uint32_t red[32];
+  if (lane == 0) red[threadIdx.x >> 5] = cmax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t m = threadIdx.x < (unsigned)wpb ? red[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) part[blockIdx.x] = __uint_as_float(m);
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + threadIdx.x; i < LFM_AMAX_SLOTS; i += 32) part[i] = 0.f;
+  }
+}
+
+lfm_status k_split16_rows(const float* src, int rows, int len, float* part, float* rinv, uint16_t* hi, uint16_t* lo,
+                          void* stream, std::string& err) {
+  const int g = std::min(std::min(g_num_sms() * 2, LFM_AMAX_SLOTS), std::max(1, (rows + 15) / 16));
+  split16_rows_kernel<<<g, 512, 0, (cudaStream_t)stream>>>(src, rows, len, part, rinv, hi, lo);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "split16_rows_kernel launch", err);
 }
 
 lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t* hi, uint16_t* lo, void* stream,

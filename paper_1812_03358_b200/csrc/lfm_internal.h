@@ -270,8 +270,12 @@ lfm_status k_spass_fwd(const CameraPlan& cp, const float* x, float* U, void* str
 // nd*nz*ny halves) of 2^e U with e from the partial maxima of |x| (amax_kernel) and T.lsum -- the 2xFP16 t pass input
 // x16 != nullptr too (and BK 32 fp16 tables): 2xFP16 input, x16 = fp16 hi (n_vox) then lo of 2^e x (split16_kernel
 // with the same maxima)
+// rinv != nullptr: x16 was split with per-row scales (split16_rows_kernel), rinv[n ny + vt] = 2^-e_row
 lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, float* U, void* stream, std::string& err,
-                       int c0 = 0, int c1 = -1, const float* amax = nullptr, const uint16_t* x16 = nullptr);
+                       int c0 = 0, int c1 = -1, const float* amax = nullptr, const uint16_t* x16 = nullptr,
+                       const float* rinv = nullptr);
+lfm_status k_split16_rows(const float* src, int rows, int len, float* part, float* rinv, uint16_t* hi, uint16_t* lo,
+                          void* stream, std::string& err);
 // LFM_AMAX_SLOTS partial maxima of |src[0, n)| into part (one kernel)
 lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err);
 // fp16 hi / lo of 2^e src over n floats (e from the partial maxima `amax` of src), for the 2xFP16 band_u form

@@ -209,6 +209,13 @@ __device__ __forceinline__ int u_data_exp(const float* amax, int n, float mult) 
   frexpf(b, &ex);  // b < 2^ex
   return min(100, max(-100, 15 - ex));
 }
+// e with b 2^e in [2^14, 2^15) for a maximum b (0 when b is 0 or not finite)
+__device__ __forceinline__ int data_exp(float b) {
+  if (!(b > 0.f) || !(b < 3.0e38f)) return 0;
+  int ex;
+  frexpf(b, &ex);
+  return min(100, max(-100, 15 - ex));
+}
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }  // |e| <= 126
 
 }  // namespace lfm
