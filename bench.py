@@ -457,7 +457,8 @@ def run_ours(args, rank, world, local_rank):
         else:
             fma_f = fma_a = inf["fma_alg"][1 if path == lfm.COLLAPSED else 0]
             kname = "%s A_forward, camera %d" % (args.path, dom_cam)
-        dom = dict(fwd_ms=fwd_ms, adj_ms=adj_ms, fma=fma_f, fma_adj=fma_a, name=kname, kind=kind, mma=inf["mma_stage"][0])
+        dom = dict(fwd_ms=fwd_ms, adj_ms=adj_ms, fma=fma_f, fma_adj=fma_a, name=kname, kind=kind, mma=inf["mma_stage"][0],
+                   f16=bool(inf["f16_stage"][0]))
 
     # every kernel of the pair timed alone (CUDA events, L2 flushed, median): device time, algorithmic HBM bytes
     # -> GB/s and the fraction of the measured copy peak / the 8 TB/s spec, FMA rate where it counts
@@ -672,7 +673,31 @@ def run_ours(args, rank, world, local_rank):
                 "adjoint_achieved": 2.0 * dom["fma_adj"] / (dom["adj_ms"] * 1e-3) / 1e12,
                 "peak_note": "FP32 FMA: 148 SM x 128 lanes x 2 flop x %.0f MHz (sm_max_mhz, MEASURED_PEAKS.json)"
                              % sm_max}
-        if dom.get("kind") == 8:
+        if dom.get("kind") == 8 and dom.get("f16"):
+            # the stage runs on the tcgen05 tensor cores in the 2xFP16 form (band_u, kind::f16, 3 fp16 products of
+            # pre-split hi/lo operands): its roof is the fp16 dense tensor peak = measured bf16 peak (same rate).
+            # `achieved` is the algorithmic (non-zero) work; `issued` the dense block MMAs it runs; `l2_feed` the
+            # bytes its TMA brings into shared memory (weights 8 KB + source 16 KB per 16-row block and 256 columns
+            # = issued MACs / 64) against the measured TMA fill rate of all SMs (tools/microbench/tma_rate.cu:
+            # ~36 B/cycle/SM), the bound it actually runs into.
+            f16_peak = peaks.get("bf16_tflops", 1653.4)
+            issued = 2.0 * dom["mma"] / (dom["fwd_ms"] * 1e-3) / 1e12
+            staged = dom["mma"] / 64.0
+            feed_peak = 36.0 * 148 * sm_max * 1e6 / 1e9  # GB/s
+            feed = staged / (dom["fwd_ms"] * 1e-3) / 1e9
+            roof.update({"bound": "tensor", "peak": f16_peak, "frac": achieved / f16_peak,
+                         "peak_note": "fp16 dense tensor peak = MEASURED_PEAKS bf16_tflops %.1f (fp16 and bf16 share "
+                                      "the kind::f16 rate)" % f16_peak,
+                         "issued": {"achieved": issued, "frac": issued / f16_peak,
+                                    "what": "2xFP16 dense 128x16-block MACs (3 products) x 2 per launch / time"},
+                         "l2_feed": {"achieved_gbs": feed, "peak_gbs": feed_peak, "frac": feed / feed_peak,
+                                     "bytes_per_launch": staged,
+                                     "what": "TMA L2->shared bytes per launch / time vs 36 B/cycle/SM x 148 SMs "
+                                             "(measured, tools/microbench/tma_rate.cu)"},
+                         "alu_equiv": {"peak": fp32_peak, "frac": achieved / fp32_peak,
+                                       "what": "algorithmic flops / time vs the FP32 FMA roof the plain kernels face"},
+                         "kernel": dom["name"] + " on tcgen05 (band_u, 2xFP16)"})
+        elif dom.get("kind") == 8:
             # the stage runs on the tcgen05 tensor cores (band_u, 3xTF32): its roof is the tf32 tensor peak =
             # measured bf16 peak x nominal tf32/bf16 ratio (1.1 / 2.25, B200_PROFILING.md).  `achieved` stays the
             # algorithmic (non-zero) work; `issued` is the dense 3xTF32 MMA work the kernel actually runs

@@ -128,6 +128,8 @@ typedef struct {
   int s3_terms;             /* separable terms T of the lenslet stage (1 for a rectangular grid with square
                                apertures; hexagonal layouts / circular apertures: S_k = sum_tau S^tau_ks (x) S^tau_kt,
                                reading R12).  S3 table ids index k*T + tau; the collapsed path sums T terms. */
+  int f16_stage[2];         /* 1 when the collapsed path's forward / adjoint t pass runs in the 2xFP16 form
+                               (fp16 hi + lo operands, kind::f16 MMAs), 0 for 3xTF32 */
 } lfm_info;
 
 /* Table ids for lfm_plan_export_table (bit-exact comparison with the oracle in tests).

@@ -521,6 +521,8 @@ lfm_status lfm_plan_info(lfm_plan p, int cam, lfm_info* out) {
   out->kind_stage[0] = p->cams[cam].fwd_c2.kind;
   out->kind_stage[1] = p->cams[cam].adj_c1.kind;
   out->subset_collapsed = 0;
+  out->f16_stage[0] = p->device >= 0 && f16_fwd(p->cams[cam], p->cams[cam].fwd_c2) ? 1 : 0;
+  out->f16_stage[1] = p->device >= 0 && f16_adj(p->cams[cam], p->cams[cam].adj_c1) ? 1 : 0;
   if (p->device >= 0)
     for (const ViewOps& vo : p->cams[cam].subs) out->subset_collapsed += subset_collapsed(p->cams[cam], vo) ? 1 : 0;
   return LFM_OK;

@@ -1576,12 +1576,12 @@ __global__ void amax_kernel(const float* __restrict__ src, long long n, float* _
     const long long n4 = n >> 2;
     const float4* s4 = reinterpret_cast<const float4*>(src);
     long long i = i0;
-    for (; i + 3 * stride < n4; i += 4 * stride) {  // four independent loads in flight
-      float4 v[4];
+    for (; i + 7 * stride < n4; i += 8 * stride) {  // eight independent loads in flight
+      float4 v[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = __ldg(s4 + i + j * stride);
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(s4 + i + j * stride);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 8; ++j)
         m = max(max(max(m, __float_as_uint(v[j].x) & 0x7fffffffu), max(__float_as_uint(v[j].y) & 0x7fffffffu,
                 __float_as_uint(v[j].z) & 0x7fffffffu)), __float_as_uint(v[j].w) & 0x7fffffffu);
     }
@@ -1610,7 +1610,8 @@ __global__ void amax_kernel(const float* __restrict__ src, long long n, float* _
 }
 
 lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err) {
-  const int g = std::min(std::min(g_num_sms(), LFM_AMAX_SLOTS), (int)std::max<long long>(1, n / 8192));
+  // enough threads that every load of a 16 MiB source is in flight at once (8 float4 per thread)
+  const int g = std::min(LFM_AMAX_SLOTS, (int)std::max<long long>(1, (n / 4 + 1023) / 1024));
   amax_kernel<<<g, 1024, 0, (cudaStream_t)stream>>>(src, n, part);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "amax_kernel launch", err);
@@ -1720,7 +1721,7 @@ lfm_status k_split16_rows(const float* src, int rows, int len, float* part, floa
 
 lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t* hi, uint16_t* lo, void* stream,
                      std::string& err) {
-  split16_kernel<<<(unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, (long long)g_num_sms() * 4), 256, 0,
+  split16_kernel<<<(unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, (long long)g_num_sms() * 8), 256, 0,
                    (cudaStream_t)stream>>>(src, n, amax, hi, lo);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "split16_kernel launch", err);

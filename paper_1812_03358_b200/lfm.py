@@ -62,7 +62,8 @@ class Info(ctypes.Structure):
                 ("fma_alg", ctypes.c_double * 2), ("bytes_alg", ctypes.c_double * 2),
                 ("fma_stage", ctypes.c_double * 2), ("mma_stage", ctypes.c_double * 2),
                 ("kind_stage", ctypes.c_int * 2), ("fma_spass", ctypes.c_double * 2),
-                ("subset_collapsed", ctypes.c_int), ("s3_terms", ctypes.c_int)]
+                ("subset_collapsed", ctypes.c_int), ("s3_terms", ctypes.c_int),
+                ("f16_stage", ctypes.c_int * 2)]
 
     def as_dict(self):
         out = {}
