@@ -57,13 +57,15 @@ def build(force=False, verbose=False, ptxas_verbose=False):
     for f in SOURCES_CU:
         o = os.path.join(bdir, f + ".o")
         extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+        extra += os.environ.get("LFM_NVCC_DEFS", "").split()  # experiments only (e.g. -DBAND_U_NO_MMA)
         _run([NVCC, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off"]
              + ARCH + extra + inc + ["-c", os.path.join(CSRC, f), "-o", o], verbose or ptxas_verbose)
         objs.append(o)
-    tmp = LIB + ".tmp"
+    out = os.environ.get("LFM_BUILD_OUT", LIB)  # experiments: build a variant library beside the product one
+    tmp = out + ".tmp"
     _run([NVCC, "-shared", "-cudart", "static"] + ARCH + objs + ["-o", tmp], verbose)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

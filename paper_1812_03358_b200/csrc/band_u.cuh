@@ -171,9 +171,9 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
             if (my < ui.lo) continue;
             if (my >= ui.hi) break;
           }
-          mbar_wait(&empty[s], ph ^ 1);
+          const int k = __ldg(a.blk_k0 + b) - a.k_shift;  // before the wait: off the issue path
           uint8_t* st = sm + s * U_STAGE_BYTES;
-          const int k = __ldg(a.blk_k0 + b) - a.k_shift;
+          mbar_wait(&empty[s], ph ^ 1);
           if constexpr (F16) {  // fp16 weight images (8 KB); pre-split fp16 source hi and lo, 4 boxes of 16 rows x 64
                                 // columns each with the 128-byte swizzle = the MN-major operand layout
             mbar_arrive_expect_tx(&full[s], 8192 + 16384);
@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
             if constexpr (F16) {  // one K = 16 step: D += C_lo S_hi + C_hi S_lo + C_hi S_hi
               const uint64_t ahi = dA0 + so, alo = dA0 + so + (4096 >> 4);
               const uint64_t bhi = dB0 + so, blo = dB0 + so + (8192 >> 4);
+#ifndef BAND_U_NO_MMA
               mma_bf16_ss(d, alo, bhi, IDESC, j != g0 ? 1u : 0u);
               mma_bf16_ss(d, ahi, blo, IDESC, 1u);
               mma_bf16_ss(d, ahi, bhi, IDESC, 1u);
+#endif
             } else
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {

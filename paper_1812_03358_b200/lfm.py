@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblfm.so")
+LIB_PATH = os.environ.get("LFM_LIB") or os.path.join(_HERE, "liblfm.so")  # LFM_LIB: experiment variants
 
 PILLBOX, DIRAC = 0, 1
 SINGLE, PLENOPTIC = 0, 1
