@@ -421,12 +421,15 @@ def run_ours(args, rank, world, local_rank):
     # is timed alone with events on the bench stream, after an L2 flush, inputs from a full call.
     def timed(fn, reps=max(5, min(21, args.steps // 4)), prep=None):
         """Median device time (ms) of fn() alone on the bench stream, L2 flushed before every launch by READING a
-        256 MiB buffer (a write flush would leave L2 full of dirty lines whose write-back the timed kernel pays)."""
+        256 MiB buffer (a write flush would leave L2 full of dirty lines whose write-back the timed kernel pays).
+        A ~50 us sleep kernel after the flush keeps the stream busy while the host enqueues fn(), so the events
+        bracket device time only (not the ctypes call and launch latency of a short kernel)."""
         out = []
         for _ in range(reps):
             if prep is not None:
                 prep()
             torch.sum(flush)
+            torch.cuda._sleep(100000)
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_.record(stream)
             fn()

@@ -2236,6 +2236,7 @@ __global__ void mul_kernel(const float* __restrict__ a, const float* __restrict_
 }
 
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs (partials: 3 x 1184 doubles fit the workspace's 16384)
+constexpr int STATS_BLOCKS = 592; // 4 x 148: the stats kernel's blocks all resident at once (64 registers x 256)
 constexpr int RED_THREADS = 256;
 
 __device__ inline double warp_sum(double v) {
@@ -2280,21 +2281,27 @@ __global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float*
   };
   long long i0 = t;
   if (VEC) {
-    // two float4 of each vector per iteration: six 16-byte loads in flight before the fp64 sums need them
+    // four float4 of each vector per iteration: twelve 16-byte loads in flight before the fp64 sums need them
+    // (one round covers a 2048^2 detector with the 1184 x 256 threads)
     const long long n4 = n >> 2;
-    long long i = t;
-    for (; i + stride < n4; i += 2 * stride) {
-      const float4 a0 = __ldg(reinterpret_cast<const float4*>(Ax) + i), a1 = __ldg(reinterpret_cast<const float4*>(Ax) + i + stride);
-      const float4 b0 = __ldg(reinterpret_cast<const float4*>(y) + i), b1 = __ldg(reinterpret_cast<const float4*>(y) + i + stride);
-      const float4 c0 = __ldg(reinterpret_cast<const float4*>(w) + i), c1 = __ldg(reinterpret_cast<const float4*>(w) + i + stride);
-      acc(a0.x, b0.x, c0.x); acc(a0.y, b0.y, c0.y); acc(a0.z, b0.z, c0.z); acc(a0.w, b0.w, c0.w);
-      acc(a1.x, b1.x, c1.x); acc(a1.y, b1.y, c1.y); acc(a1.z, b1.z, c1.z); acc(a1.w, b1.w, c1.w);
-    }
-    for (; i < n4; i += stride) {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(Ax) + i);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(y) + i);
-      const float4 c = __ldg(reinterpret_cast<const float4*>(w) + i);
-      acc(a.x, b.x, c.x); acc(a.y, b.y, c.y); acc(a.z, b.z, c.z); acc(a.w, b.w, c.w);
+    const float4* A4 = reinterpret_cast<const float4*>(Ax);
+    const float4* Y4 = reinterpret_cast<const float4*>(y);
+    const float4* W4 = reinterpret_cast<const float4*>(w);
+    for (long long i = t; i < n4; i += 4 * stride) {  // every lane's 4 x 3 loads issued before any sum
+      float4 a[4], b[4], c[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long k = i + j * stride;
+        const bool ok = k < n4;
+        a[j] = ok ? __ldg(A4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        b[j] = ok ? __ldg(Y4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        c[j] = ok ? __ldg(W4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i + j * stride < n4) {
+          acc(a[j].x, b[j].x, c[j].x); acc(a[j].y, b[j].y, c[j].y); acc(a[j].z, b[j].z, c[j].z); acc(a[j].w, b[j].w, c[j].w);
+        }
     }
     i0 = 4 * n4 + t;
   }
@@ -2310,6 +2317,7 @@ __global__ void __launch_bounds__(256) reduce_final_kernel(const double* __restr
   __shared__ double sh[256];
   const int q = blockIdx.x, t = threadIdx.x;
   double s = 0;
+#pragma unroll 8
   for (int b = t; b < nblocks; b += 256) s += part[(size_t)b * nv + q];
   sh[t] = s;
   __syncthreads();
@@ -2363,38 +2371,36 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const float* __re
 }
 
 // grad += beta * sum_{l in N_j, in grid} (x_j - x_l) + nu;  partial [nu*x_j + (beta/4) sum_l (x_j-x_l)^2] (COST)
-// Tiled: a block owns 32 x 8 (x, y) columns and a chunk of R26_ZC slices; the R26_ZC + 2 planes of the
-// (32+2) x (8+2) footprint are loaded into shared memory at once (every load in flight together, one barrier),
-// so every x value is read from HBM/L2 about once per chunk instead of 27 times through L1.  Neighbours outside
-// the grid contribute nothing (the validity of each of the 26 offsets is a per-thread select); the sum over l
-// runs in the order dz, dy, dx ascending.
-constexpr int R26_ZC = 8;
+// Tiled: a block of 32 x 8 threads owns 32 x 8 (x, y) columns and a chunk of R26_ZC slices; the R26_ZC + 2 planes
+// of the (32+2) x (16+2) footprint are loaded into shared memory at once (every load in flight together, one
+// barrier; x is read from HBM/L2 about 1.4 times).  Each thread walks its column up the chunk keeping the 3 x 3
+// neighbourhoods of planes z-1, z, z+1 in registers, so every shared value is loaded once per plane (9 loads per
+// voxel instead of 26).  Neighbours outside the grid contribute nothing: their shared values are 0, so their terms
+// are x_j, taken back out after the sum (n_out x_j); the sum runs in the order dz, dy, dx ascending.
+constexpr int R26_ZC = 16, R26_TY = 8, R26_NT = 32 * R26_TY;
 template <bool COST>
-__global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad, int nx,
+__global__ void __launch_bounds__(R26_NT) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad, int nx,
                                                     int ny, int nz, float beta, float nu, double* part) {
-  __shared__ float pl[R26_ZC + 2][10][34];
+  constexpr int PX = 34, PY = R26_TY + 2, PP = PX * PY;
+  __shared__ float pl[R26_ZC + 2][PY][PX];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8, z0 = blockIdx.z * R26_ZC;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * R26_TY, z0 = blockIdx.z * R26_ZC;
   const int ix = x0 + tx, iy = y0 + ty;
   const size_t plane = (size_t)nx * ny;
-  // all (R26_ZC + 2) x 340 footprint loads in flight before their stores (14 per thread)
-  constexpr int NE = (R26_ZC + 2) * 340, NL = (NE + 255) / 256;
-  float v0[NL];
-#pragma unroll
-  for (int u = 0; u < NL; ++u) {
-    const int e = tid + 256 * u;
-    const int pz = e / 340, r = e - pz * 340, ly = r / 34, lx = r - ly * 34;
+  constexpr int NE = (R26_ZC + 2) * PP;
+  // the footprint straight into shared memory (cp.async, 4 bytes; zero-filled outside the grid): every load in
+  // flight at once without holding registers, so two blocks fit an SM and one's loads overlap the other's sums
+  for (int e = tid; e < NE; e += R26_NT) {
+    const int pz = e / PP, r = e - pz * PP, ly = r / PX, lx = r - ly * PX;
     const int gx = x0 + lx - 1, gy = y0 + ly - 1, zz = z0 + pz - 1;
-    v0[u] = (e < NE && zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny)
-                ? __ldg(x + (size_t)zz * plane + (size_t)gy * nx + gx) : 0.f;
+    const bool ok = zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+    const float* src = ok ? x + (size_t)zz * plane + (size_t)gy * nx + gx : x;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(&pl[0][0][0] + e)),
+                 "l"(src), "r"(ok ? 4 : 0) : "memory");
   }
-#pragma unroll
-  for (int u = 0; u < NL; ++u) {
-    const int e = tid + 256 * u;
-    if (e < NE) (&pl[0][0][0])[e] = v0[u];
-  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  const bool vx[3] = {ix > 0, true, ix < nx - 1}, vy[3] = {iy > 0, true, iy < ny - 1};
+  const int cxy = (1 + (ix > 0) + (ix < nx - 1)) * (1 + (iy > 0) + (iy < ny - 1));  // in-grid x, y neighbours (+self)
   double v = 0;
   if (ix < nx && iy < ny) {
     // the chunk's grad values loaded together (read-modify-write: one latency for the chunk, not one per voxel)
@@ -2402,12 +2408,20 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
 #pragma unroll
     for (int q = 0; q < R26_ZC; ++q)
       gin[q] = z0 + q < nz ? grad[(size_t)(z0 + q) * plane + (size_t)iy * nx + ix] : 0.f;
+    float P[3][9];  // 3 x 3 neighbourhoods of planes q, q+1, q+2 (z-1, z, z+1) of the footprint
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+#pragma unroll
+      for (int k = 0; k < 9; ++k) P[d][k] = pl[d][ty + k / 3][tx + k % 3];
 #pragma unroll
     for (int q = 0; q < R26_ZC; ++q) {
       const int iz = z0 + q;
       if (iz >= nz) break;
-      const bool vz[3] = {iz > 0, true, iz < nz - 1};
-      const float xj = pl[q + 1][ty + 1][tx + 1];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) P[(q + 2) % 3][k] = pl[q + 2][ty + k / 3][tx + k % 3];
+      const float xj = P[(q + 1) % 3][4];
+      // all 26 differences in the order dz, dy, dx (outside the grid the shared value is 0, so such a term is x_j);
+      // the n_out of them are taken back out after the sum (interior voxels: n_out = 0, the plain sum)
       float g = 0.f;
       double rs = 0;
 #pragma unroll
@@ -2417,25 +2431,29 @@ __global__ void __launch_bounds__(256) reg26_kernel(const float* __restrict__ x,
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
             if (dz == 1 && dy == 1 && dx == 1) continue;
-            const float d = xj - pl[q + dz][ty + dy][tx + dx];
-            const bool ok = vz[dz] && vy[dy] && vx[dx];
-            g += ok ? d : 0.f;
-            if (COST) rs += ok ? (double)d * (double)d : 0.0;
+            const float d = xj - P[(q + dz) % 3][dy * 3 + dx];
+            g += d;
+            if (COST) rs += (double)d * (double)d;
           }
+      const int n_out = 27 - (1 + (iz > 0) + (iz < nz - 1)) * cxy;
+      if (n_out) {
+        g -= (float)n_out * xj;
+        if (COST) rs -= (double)n_out * (double)xj * (double)xj;
+      }
       const size_t i = (size_t)iz * plane + (size_t)iy * nx + ix;
       grad[i] = gin[q] + (beta * g + nu);
       if (COST) v += (double)nu * xj + 0.25 * (double)beta * rs;
     }
   }
   if (COST) {
-    // block partial (256 threads = 8 warps), fixed order
-    __shared__ double sh[8];
+    // block partial (R26_TY warps), fixed order
+    __shared__ double sh[R26_TY];
     const double a = warp_sum(v);
     if (tx == 0) sh[ty] = a;
     __syncthreads();
     if (tid == 0) {
       double t = 0;
-      for (int w = 0; w < 8; ++w) t += sh[w];
+      for (int w = 0; w < R26_TY; ++w) t += sh[w];
       part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
   }
@@ -2503,10 +2521,10 @@ static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 lfm_status k_stats(const float* Ax, const float* y, const float* w, long long n, double* part, double* out, void* s,
                    std::string& err) {
   if (al16(Ax) && al16(y) && al16(w))
-    stats_partial_kernel<true><<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
+    stats_partial_kernel<true><<<STATS_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
   else
-    stats_partial_kernel<false><<<RED_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
-  reduce_final_kernel<<<3, 256, 0, (cudaStream_t)s>>>(part, RED_BLOCKS, 3, out, 0);
+    stats_partial_kernel<false><<<STATS_BLOCKS, RED_THREADS, 0, (cudaStream_t)s>>>(Ax, y, w, n, part);
+  reduce_final_kernel<<<3, 256, 0, (cudaStream_t)s>>>(part, STATS_BLOCKS, 3, out, 0);
   g_launches += 2;
   return cuda_check(cudaGetLastError(), "stats", err);
 }
@@ -2533,7 +2551,7 @@ lfm_status k_residual(const float* Ax, const float* y, const float* w, const dou
 }
 lfm_status k_reg26(const float* x, float* grad, int nx, int ny, int nz, float beta, float nu, double* part,
                    double* cost, void* s, std::string& err) {
-  dim3 grid((nx + 31) / 32, (ny + 7) / 8, (nz + R26_ZC - 1) / R26_ZC), blk(32, 8);
+  dim3 grid((nx + 31) / 32, (ny + R26_TY - 1) / R26_TY, (nz + R26_ZC - 1) / R26_ZC), blk(32, R26_TY);
   const long long nblk = (long long)grid.x * grid.y * grid.z;
   if (cost && nblk > 4096 * 4) { err = "reg26: volume too large for the reduction partials"; return LFM_E_INVALID; }
   if (cost) {

@@ -36,6 +36,7 @@ def main():
         ts = []
         for _ in range(reps):
             torch.sum(flush)
+            torch.cuda._sleep(100000)  # the stream stays busy while the host enqueues fn (device time only)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()

@@ -23,6 +23,7 @@ torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
 torch.cuda.profiler.start()
 for i in range(reps):
+    torch.cuda._sleep(100000)  # keep the stream busy while the host enqueues (device time only)
     ev[2 * i].record()
     if which == "fwd":
         lfm.A_stage(plan, cam, lfm.STAGE_FWD_T, None, y, ws)
