@@ -44,12 +44,13 @@ struct DevGuard {
 };
 
 struct WsLayout {
-  size_t r0, r1, xt, f, s, s2, z, zt, p, am, h16, rs, total;
+  size_t r0, r1, xt, f, s, s2, z, zt, p, am, h16, rs, cs, total;
 };
 
 WsLayout layout(const lfm_plan_s* p) {
-  size_t V = 0, F = 0, S = 0, Z = 0, P = 0, R = 0;
+  size_t V = 0, F = 0, S = 0, Z = 0, P = 0, R = 0, C = 0;
   for (const CameraPlan& c : p->cams) {
+    C = std::max(C, (size_t)((c.info.n_s + 255) / 256 * 256) * 4);
     P = std::max(P, (size_t)c.info.n_pix * 4);
     R = std::max(R, (size_t)c.info.ny * c.info.nz * 4);
     V = std::max(V, (size_t)c.info.n_vox * 4);
@@ -70,7 +71,8 @@ WsLayout layout(const lfm_plan_s* p) {
   L.am = L.p + al256(4096 * 8 * 4);
   L.h16 = L.am + al256(LFM_AMAX_SLOTS * 4);
   L.rs = L.h16 + al256(P);
-  L.total = L.rs + al256(R);
+  L.cs = L.rs + al256(R);
+  L.total = L.cs + al256(C);
   return L;
 }
 
@@ -80,6 +82,7 @@ struct Ws {
   float* am;      // partial maxima of the 2xFP16 t-pass input's source: of x^r (forward), of y (adjoint)
   uint16_t* h16;  // fp16 hi (n_pix) then lo (n_pix) of 2^e y: the adjoint t pass input in the 2xFP16 form
   float* rs;      // per-row inverse scales of the row-scaled fp16 split of x^r (nz ny)
+  float* cs;      // per-column inverse scales of the column-scaled fp16 split of y (n_s rounded up to 256)
 };
 
 lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
@@ -100,6 +103,7 @@ lfm_status get_ws(const lfm_plan_s* p, void* ws, size_t ws_bytes, Ws& w) {
   w.am = (float*)(b + L.am);
   w.h16 = (uint16_t*)(b + L.h16);
   w.rs = (float*)(b + L.rs);
+  w.cs = (float*)(b + L.cs);
   return LFM_OK;
 }
 
@@ -235,6 +239,13 @@ static lfm_status vt_forward(const CameraPlan& cp, const VTab& T, const SepOp& c
   return sep(c2, w.z, y, 0, 1, acc, stream, win.r0, win.r1, 0, -1, win.c0, win.c1, w.zt, cp.ws_z);
 }
 
+// the adjoint t pass's input split with a scale per detector column in one kernel (k_split16_cols) instead of
+// the global maxima + split (two kernels); LFM_SPLIT_GLOBAL=1 keeps the latter (A/B)
+static bool cols_split() {
+  static const bool off = std::getenv("LFM_SPLIT_GLOBAL") != nullptr;
+  return !off;
+}
+
 // The adjoint t pass (c1) of y's rows [r0, r1): 2xFP16 = maxima of those rows, fp16 hi / lo of 2^e y into w.h16
 // (done once per call, `split_done`), then band_u from them.
 static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* y, const Ws& w, void* stream, Win win,
@@ -242,11 +253,20 @@ static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* 
   if (!f16_adj(cp, c1)) return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1);
   const int n_s = cp.info.n_s, r0 = std::max(0, win.r0), r1 = win.r1 < 0 ? cp.info.n_t : std::min(win.r1, cp.info.n_t);
   const size_t np = (size_t)cp.info.n_pix;
+  // column scales: with the fp16 Z output only (band_u's OUT16 epilogue applies them), 16-byte aligned rows of y
+  // (n_s % 8 == 0 already holds for the 2xFP16 form)
+  const bool cs = cols_split() && z16 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
   if (!split_done && r1 > r0) {
     std::string err;
     const long long off = (long long)r0 * n_s, n = (long long)(r1 - r0) * n_s;
-    lfm_status st = k_amax(y + off, n, w.am, stream, err);
-    if (st == LFM_OK) st = k_split16(y + off, n, w.am, w.h16 + off, w.h16 + np + off, stream, err);
+    lfm_status st;
+    if (cs) {
+      st = k_split16_cols(y + off, r1 - r0, n_s, (n_s + 255) / 256 * 256, w.am, w.cs, w.h16 + off, w.h16 + np + off,
+                          stream, err);
+    } else {
+      st = k_amax(y + off, n, w.am, stream, err);
+      if (st == LFM_OK) st = k_split16(y + off, n, w.am, w.h16 + off, w.h16 + np + off, stream, err);
+    }
     if (st != LFM_OK) return fail(st, err);
   }
   split_done = true;
@@ -254,6 +274,7 @@ static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* 
   h.hi = w.h16;
   h.lo = w.h16 + np;
   h.amax = w.am;
+  if (cs) h.cinv = w.cs;
   if (z16) {  // Z as fp16 hi / lo of 2^e' Z for band_v's 2xFP16 form (k_vpass_adj with in_scale = u_lsum)
     h.out_hi = reinterpret_cast<uint16_t*>(w.z);
     h.out_lo = h.out_hi + (size_t)c1.n_ot * c1.n_os;

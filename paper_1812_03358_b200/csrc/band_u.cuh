@@ -31,6 +31,8 @@ struct UArgs {
   const float* amax;      // F16: n_amax partial maxima m_i; the source was written as fp16 hi + lo of 2^e src with
   int n_amax;             // e = u_data_exp(max m_i * amax_scale) by its producer (band_v / split16_kernel), so the
   float amax_scale;       // epilogue takes 2^-e back out
+  const float* cinv;      // OUT16, optional: the source was split with a scale per column (split16_cols_kernel), the
+                          // epilogue takes cinv[c] = 2^-e_c back out per output column (the t pass never mixes columns)
   float out_scale16;      // OUT16 instances: the output is written as fp16 hi + lo of 2^e' out, e' =
                           // u_data_exp(max m_i * out_scale16) (a bound on |out| over max |src| m_i: the row sums)
   const int32_t* blk_off; // per row tile: first block .. (row tiles of the table, n_tiles + 1 entries)
@@ -300,6 +302,11 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       float acc[128];
 #pragma unroll
       for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+      // OUT16 with per-column source scales: lane l holds the factors of its half's columns 4l..4l+3 (loaded while
+      // the MMAs run; the epilogue broadcasts them with shuffles)
+      float4 cv = make_float4(1.f, 1.f, 1.f, 1.f);
+      if constexpr (OUT16)
+        if (a.cinv) cv = __ldg(reinterpret_cast<const float4*>(a.cinv + ui.nt * 256 + h * 128) + lane);
       for (int g0 = b0; g0 < b1; g0 += a.group) {
         mbar_wait(&tfull[buf], (tph >> buf) & 1u);
         tph ^= 1u << buf;
@@ -332,10 +339,21 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             uint32_t hw[4], lw[4];
+            float ci[8];
+            if (a.cinv) {
+              const int sl = (c + 8 * jj) >> 2;  // lanes sl, sl + 1 hold these 8 columns
+              ci[0] = __shfl_sync(0xffffffffu, cv.x, sl); ci[1] = __shfl_sync(0xffffffffu, cv.y, sl);
+              ci[2] = __shfl_sync(0xffffffffu, cv.z, sl); ci[3] = __shfl_sync(0xffffffffu, cv.w, sl);
+              ci[4] = __shfl_sync(0xffffffffu, cv.x, sl + 1); ci[5] = __shfl_sync(0xffffffffu, cv.y, sl + 1);
+              ci[6] = __shfl_sync(0xffffffffu, cv.z, sl + 1); ci[7] = __shfl_sync(0xffffffffu, cv.w, sl + 1);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) ci[i] = inv_sig;
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float x0 = osig * (a.scale * (inv_sig * acc[c + 8 * jj + 2 * i]));
-              const float x1 = osig * (a.scale * (inv_sig * acc[c + 8 * jj + 2 * i + 1]));
+              const float x0 = osig * (a.scale * (ci[2 * i] * acc[c + 8 * jj + 2 * i]));
+              const float x1 = osig * (a.scale * (ci[2 * i + 1] * acc[c + 8 * jj + 2 * i + 1]));
               const __half2 hh = __floats2half2_rn(x0, x1);
               const float2 hf = __half22float2(hh);
               const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);

@@ -1711,6 +1711,109 @@ __global__ void split16_rows_kernel(const float* __restrict__ src, int rows, int
   }
 }
 
+// Column-scaled fp16 split in one pass (the adjoint t pass's input y: the t pass mixes rows, never columns, so a
+// scale per column is undone per output column by band_u's epilogue): a CTA owns strips of 16 columns over all
+// `rows` rows; pass 1 takes the column maxima (8 float4 loads in flight per thread), e_c = data_exp(max_c),
+// cinv[c] = 2^-e_c; pass 2 re-reads the strip (L1 / L2) and writes fp16 hi / lo of 2^e_c src.  The per-CTA maxima
+// go to part (CTA 0 zero-fills the other LFM_AMAX_SLOTS) for the global scale of the t pass's fp16 output.
+// Needs cols % 4 == 0 and 16-byte aligned src / hi / lo rows (pitch = cols); cinv is padded with 1 up to cols_pad.
+constexpr int SPLITC_THREADS = 1024;
+__global__ void __launch_bounds__(SPLITC_THREADS) split16_cols_kernel(const float* __restrict__ src, int rows, int cols,
+                                                                      int cols_pad, float* __restrict__ part,
+                                                                      float* __restrict__ cinv, uint16_t* __restrict__ hi,
+                                                                      uint16_t* __restrict__ lo) {
+  __shared__ float4 red[SPLITC_THREADS / 32][4];
+  __shared__ float4 csig[4];
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5, q = t & 3, r_first = t >> 2;
+  constexpr int RSTEP = SPLITC_THREADS / 4;
+  const int nstrips = (cols + 15) / 16;
+  uint32_t cmax = 0;
+  for (int strip = blockIdx.x; strip < nstrips; strip += gridDim.x) {
+    const int c = strip * 16 + 4 * q;  // this thread's 4 columns
+    const bool live = c < cols;
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    int r = r_first;
+    for (; r + 7 * RSTEP < rows; r += 8 * RSTEP) {
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = live ? __ldg(reinterpret_cast<const float4*>(src + (long long)(r + j * RSTEP) * cols + c)) : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        m0 = max(m0, __float_as_uint(v[j].x) & 0x7fffffffu);
+        m1 = max(m1, __float_as_uint(v[j].y) & 0x7fffffffu);
+        m2 = max(m2, __float_as_uint(v[j].z) & 0x7fffffffu);
+        m3 = max(m3, __float_as_uint(v[j].w) & 0x7fffffffu);
+      }
+    }
+    for (; r < rows; r += RSTEP) {
+      const float4 v = live ? __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)) : make_float4(0, 0, 0, 0);
+      m0 = max(m0, __float_as_uint(v.x) & 0x7fffffffu);
+      m1 = max(m1, __float_as_uint(v.y) & 0x7fffffffu);
+      m2 = max(m2, __float_as_uint(v.z) & 0x7fffffffu);
+      m3 = max(m3, __float_as_uint(v.w) & 0x7fffffffu);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {  // lanes of the same column quad
+      m0 = max(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+      m1 = max(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+      m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+      m3 = max(m3, __shfl_xor_sync(0xffffffffu, m3, o));
+    }
+    if (lane < 4) red[wp][lane] = make_float4(__uint_as_float(m0), __uint_as_float(m1), __uint_as_float(m2), __uint_as_float(m3));
+    __syncthreads();
+    if (t < 16) {  // column strip*16 + t
+      uint32_t m = 0;
+      for (int w = 0; w < SPLITC_THREADS / 32; ++w) {
+        const float4 v = red[w][t >> 2];
+        const float x = (t & 3) == 0 ? v.x : (t & 3) == 1 ? v.y : (t & 3) == 2 ? v.z : v.w;
+        m = max(m, __float_as_uint(x));
+      }
+      cmax = max(cmax, m);
+      const int e = data_exp(__uint_as_float(m));
+      reinterpret_cast<float*>(csig)[t] = pow2f(e);
+      const int col = strip * 16 + t;
+      if (col < cols_pad) cinv[col] = col < cols ? pow2f(-e) : 1.f;
+    }
+    __syncthreads();
+    if (live) {
+      const float4 sg = csig[q];
+      for (int r = r_first; r < rows; r += RSTEP) {
+        const long long o = (long long)r * cols + c;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src + o));
+        const float x0 = sg.x * v.x, x1 = sg.y * v.y, x2 = sg.z * v.z, x3 = sg.w * v.w;
+        const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+        *reinterpret_cast<uint2*>(hi + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+        *reinterpret_cast<uint2*>(lo + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+      }
+    }
+  }
+  // strip padding past the last strip (cols_pad may exceed the strips' columns)
+  for (int col = nstrips * 16 + (int)(blockIdx.x * SPLITC_THREADS + t); col < cols_pad; col += gridDim.x * SPLITC_THREADS)
+    cinv[col] = 1.f;
+  if (t < 16) {
+#pragma unroll
+    for (int o = 8; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0x0000ffffu, cmax, o));
+    if (t == 0) part[blockIdx.x] = __uint_as_float(cmax);
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + t; i < LFM_AMAX_SLOTS; i += 16) part[i] = 0.f;
+  }
+}
+
+lfm_status k_split16_cols(const float* src, int rows, int cols, int cols_pad, float* part, float* cinv, uint16_t* hi,
+                          uint16_t* lo, void* stream, std::string& err) {
+  if (cols % 4 || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)) {
+    err = "split16_cols: columns must be a multiple of 4 and rows 16-byte aligned";
+    return LFM_E_INVALID;
+  }
+  const int g = std::max(1, std::min(LFM_AMAX_SLOTS, (cols + 15) / 16));
+  split16_cols_kernel<<<g, SPLITC_THREADS, 0, (cudaStream_t)stream>>>(src, rows, cols, cols_pad, part, cinv, hi, lo);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "split16_cols_kernel launch", err);
+}
+
 lfm_status k_split16_rows(const float* src, int rows, int len, float* part, float* rinv, uint16_t* hi, uint16_t* lo,
                           void* stream, std::string& err) {
   const int g = std::min(std::min(g_num_sms() * 2, LFM_AMAX_SLOTS), std::max(1, (rows + 15) / 16));
@@ -1864,6 +1967,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.amax = h16.amax;
     u.n_amax = LFM_AMAX_SLOTS;
     u.amax_scale = h16.amax_scale;
+    u.cinv = h16.cinv;
+    if (u.cinv && !out16) { err = "band_u: per-column source scales need the fp16 output form"; return LFM_E_INVALID; }
     u.out_scale16 = h16.out_scale16;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
     u.blk_k0 = op.ft->d_uk0;

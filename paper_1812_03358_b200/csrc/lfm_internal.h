@@ -253,6 +253,7 @@ struct F16Src {
   const uint16_t* lo = nullptr;
   const float* amax = nullptr;
   float amax_scale = 1.f;
+  const float* cinv = nullptr;  // per-column data scales 2^-e_c (k_split16_cols) instead of the global 2^-e
   // optional fp16 output (the adjoint's Z for band_v's 2xFP16 form): hi / lo arrays shaped like the fp32 output,
   // 2^e' out with e' = u_data_exp(amax, out_scale16); not with split-K or accumulation
   uint16_t* out_hi = nullptr;
@@ -276,6 +277,10 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
                        const float* rinv = nullptr);
 lfm_status k_split16_rows(const float* src, int rows, int len, float* part, float* rinv, uint16_t* hi, uint16_t* lo,
                           void* stream, std::string& err);
+// column-scaled split of a rows x cols source (pitch cols): hi / lo of 2^e_c src, cinv[c] = 2^-e_c (1 for the padding
+// columns [cols, cols_pad)), per-CTA maxima of |src| into part -- the adjoint t pass's input (one kernel)
+lfm_status k_split16_cols(const float* src, int rows, int cols, int cols_pad, float* part, float* cinv, uint16_t* hi,
+                          uint16_t* lo, void* stream, std::string& err);
 // LFM_AMAX_SLOTS partial maxima of |src[0, n)| into part (one kernel)
 lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err);
 // fp16 hi / lo of 2^e src over n floats (e from the partial maxima `amax` of src), for the 2xFP16 band_u form

@@ -1511,8 +1511,13 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
     for (const BandFamily* f : {&cp.ca1n, &cp.cf1n}) {
       double nnz = 0;
       for (int v : f->cnt) nnz += v;
-      std::fprintf(stderr, "[lfm] tcgen05 form: %zu blocks of 128x16, density %.3f\n", f->u_k0.size(),
-                   nnz / (2048.0 * f->u_k0.size()));
+      int bmin = 1 << 30, bmax = 0;
+      for (size_t t = 0; t + 1 < f->u_off.size(); ++t) {
+        bmin = std::min(bmin, f->u_off[t + 1] - f->u_off[t]);
+        bmax = std::max(bmax, f->u_off[t + 1] - f->u_off[t]);
+      }
+      std::fprintf(stderr, "[lfm] tcgen05 form: %zu blocks of 128x16, density %.3f, %d tiles, blocks per tile %d..%d\n",
+                   f->u_k0.size(), nnz / (2048.0 * f->u_k0.size()), (int)f->u_off.size() - 1, bmin, bmax);
     }
     for (int G : {4, 8, 16})
       std::fprintf(stderr, "[lfm] MSEG density with %2d-row groups: ca1n %.3f  cf1n %.3f  ca0 %.3f  cf0 %.3f\n", G,

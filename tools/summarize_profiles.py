@@ -77,7 +77,7 @@ def main():
     summary = {}
     for rep in reps:
         name = os.path.splitext(os.path.basename(rep))[0]
-        res = raw(rep)
+        res = [d for d in raw(rep) if "lfm::" in d["kernel"] or "band_" in d["kernel"]]  # not the spin / flush kernels
         txt = [f"# ncu --set full --clock-control none capture: {os.path.basename(rep)}"]
         for d in res:
             txt.append(d["kernel"])
@@ -89,7 +89,7 @@ def main():
                           "dram_bytes": to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"]),
                           "duration_us": float(d["gpu__time_duration.sum"][0].replace(",", ""))} for d in res]
     js = {"round": rnd, "captures": summary}
-    fwd = summary.get("prof_fwd", [])
+    fwd = [d for d in summary.get("prof_fwd", []) if "band_u" in d["kernel"]] or summary.get("prof_fwd", [])
     if fwd:
         js["dominant_kernel_dram_bytes_per_launch"] = fwd[0]["dram_bytes"]
         js["dominant_kernel"] = fwd[0]["kernel"]
