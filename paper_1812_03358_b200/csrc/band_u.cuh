@@ -54,6 +54,8 @@ struct UArgs {
                           // live blocks; chunk kc writes its partial at output row kc * kc_rows + r (kc_rows =
                           // row tiles x 128), summed in a fixed order by sum_chunks_kernel (deterministic)
   int kc_rows;
+  int src3d;              // 2xFP16: the source maps are 3D (64 columns, rows, 64-column groups), one box per part
+  int wtma;               // 2xFP16: the weight images come through w_map (rows of 128 B, one 64-row box per block)
 };
 
 
@@ -119,7 +121,8 @@ template <bool SPLIT, bool F16 = false, bool OUT16 = false>
 __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
                                                               const __grid_constant__ CUtensorMap out_map,
                                                               const __grid_constant__ CUtensorMap lo_map,
-                                                              const __grid_constant__ CUtensorMap out_lo_map, UArgs a) {
+                                                              const __grid_constant__ CUtensorMap out_lo_map,
+                                                              const __grid_constant__ CUtensorMap w_map, UArgs a) {
   static_assert(!OUT16 || (F16 && !SPLIT), "fp16 output: 2xFP16 form, no split-K");
   using namespace tc;
   constexpr int U_STAGES = UStage<F16>::STAGES, U_STAGE_BYTES = UStage<F16>::BYTES;
@@ -179,11 +182,17 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
           if constexpr (F16) {  // fp16 weight images (8 KB); pre-split fp16 source hi and lo, 4 boxes of 16 rows x 64
                                 // columns each with the 128-byte swizzle = the MN-major operand layout
             mbar_arrive_expect_tx(&full[s], 8192 + 16384);
-            bulk_g2s(st, a.H + (size_t)b * 4096, 8192, &full[s]);
+            if (a.wtma) tma_load_2d(st, &w_map, 0, b * 64, &full[s]);  // a verbatim 8 KB copy (no swizzle)
+            else bulk_g2s(st, a.H + (size_t)b * 4096, 8192, &full[s]);
+            if (a.src3d) {  // 4 column groups x 16 rows x 64 columns = the same [g][row][64] layout in one box
+              tma_load_3d(st + 8192, &src_map, 0, k, nt * 4, &full[s]);
+              tma_load_3d(st + 16384, &lo_map, 0, k, nt * 4, &full[s]);
+            } else {
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              tma_load_2d(st + 8192 + g * 2048, &src_map, nt * 256 + g * 64, k, &full[s]);
-              tma_load_2d(st + 16384 + g * 2048, &lo_map, nt * 256 + g * 64, k, &full[s]);
+              for (int g = 0; g < 4; ++g) {
+                tma_load_2d(st + 8192 + g * 2048, &src_map, nt * 256 + g * 64, k, &full[s]);
+                tma_load_2d(st + 16384 + g * 2048, &lo_map, nt * 256 + g * 64, k, &full[s]);
+              }
             }
           } else {
             mbar_arrive_expect_tx(&full[s], 32768);

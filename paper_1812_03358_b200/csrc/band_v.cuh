@@ -41,6 +41,7 @@ struct VArgs {
   float in_scale;          // IN16: the data arrives as fp16 hi + lo of 2^e data, e = u_data_exp(amax, in_scale)
   const float* rinv;       // IN16 forward: per data row (n ny + vt) scales instead: the row was split as 2^e_row x,
   int ny;                  // rinv[row] = 2^-e_row (split16_rows_kernel)
+  int wtma;                // IN16: the weight images come through w_map (rows of 128 B, one box per block)
 };
 
 
@@ -62,16 +63,19 @@ __device__ __forceinline__ void v_live(const VArgs& a, int key, int BK, int& lb0
 
 constexpr int V_THREADS = 384;
 
-template <int N, int BK, bool H = false>  // H: 2xFP16 operands (data and weights pre-split into fp16 hi / lo)
+// H: 2xFP16 operands (data and weights pre-split into fp16 hi / lo); O16: fp16 hi / lo output (the forward's U),
+// stored in boxes of 64 columns (128-byte rows, whole cache lines) from one staging buffer per warp
+template <int N, int BK, bool H = false, bool O16 = false>
 struct VCfg {
+  static constexpr bool W64 = O16 && H;               // 64-column fp16 store boxes (2xFP16 in and out)
   static constexpr int ES = H ? 2 : 4;                // operand element bytes
   static constexpr int A_BYTES = 128 * BK * ES;       // data tile [128][BK] (hi, or lo)
   static constexpr int B_BYTES = N * BK * ES;         // one weight image [N][BK]
   static constexpr int EC0 = N >= 256 ? 128 : N / 2;
   // staging per store: 32 rows x 32 fp32 columns, or (H: fp16 hi + lo output) 32 rows x 32 fp16 columns, twice
-  static constexpr int OUT0 = 32 * (EC0 >= 32 ? 32 : EC0) * 4;
+  static constexpr int OUT0 = W64 ? 2 * 32 * 64 * 2 : 32 * (EC0 >= 32 ? 32 : EC0) * 4;
   // staging buffers per epilogue warp: 2 (store i+1 overlaps store i) when the ring keeps >= 2 stages, else 1
-  static constexpr int NOB = (230912 - 16 * OUT0) / (2 * A_BYTES + 2 * B_BYTES) >= 2 ? 2 : 1;
+  static constexpr int NOB = W64 ? 1 : (230912 - 16 * OUT0) / (2 * A_BYTES + 2 * B_BYTES) >= 2 ? 2 : 1;
   static constexpr int RING = 230912 - 8 * NOB * OUT0;  // 227 KB minus alignment slack and barriers
   static constexpr int STAGES = RING / (2 * A_BYTES + 2 * B_BYTES) > 10 ? 10 : RING / (2 * A_BYTES + 2 * B_BYTES);
   static constexpr int SUB = BK * ES <= 128 ? BK : 128 / ES;  // sub-block width: one swizzle atom row (<= 128 B)
@@ -83,7 +87,7 @@ struct VCfg {
   static constexpr int KSTEP = 32 / ES;               // K per MMA (8 tf32, 16 fp16): 32 bytes of a row
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A | A_lo | B_hi | B_lo
   static constexpr int EC = N >= 256 ? 128 : N / 2;   // epilogue columns per warp (8 warps: 4 quarters x 2 halves)
-  static constexpr int OC = EC >= 32 ? 32 : EC;       // columns per TMA store box
+  static constexpr int OC = W64 ? 64 : EC >= 32 ? 32 : EC;  // columns per TMA store box
   static constexpr int OUT = OUT0;                    // staging per warp and buffer
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 8 * NOB * OUT + 1024 + 512;
   static_assert(STAGES >= 2, "band_v: stage too large");
@@ -102,9 +106,10 @@ template <int N, int DIR, int BK, bool KWIN = false, bool OUT16 = false, bool IN
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
                                                               const __grid_constant__ CUtensorMap out_map,
                                                               const __grid_constant__ CUtensorMap lo_map,
-                                                              const __grid_constant__ CUtensorMap a_lo_map, VArgs a) {
+                                                              const __grid_constant__ CUtensorMap a_lo_map,
+                                                              const __grid_constant__ CUtensorMap w_map, VArgs a) {
   using namespace tc;
-  using C = VCfg<N, BK, IN16>;
+  using C = VCfg<N, BK, IN16, OUT16>;
   static_assert(!OUT16 || (DIR == 0 && N == 256), "fp16 output: forward, 256-column tiles");
   extern __shared__ uint8_t v_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)v_smem_raw + 1023) & ~(uintptr_t)1023);
@@ -151,7 +156,10 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], (IN16 ? 2 : 1) * C::A_BYTES + 2 * C::B_BYTES);
-          if constexpr (IN16) bulk_g2s(st + 2 * C::A_BYTES, a.H + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
+          if constexpr (IN16) {
+            if (a.wtma) tma_load_2d(st + 2 * C::A_BYTES, &w_map, 0, b * (2 * C::B_BYTES / 128), &full[s]);
+            else bulk_g2s(st + 2 * C::A_BYTES, a.H + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
+          }
           else bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           const int k = __ldg(a.blk_k0 + b) - (KWIN ? a.k_lo : 0);
 #pragma unroll
@@ -326,9 +334,10 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         uint8_t* stg = stg0 + ob * C::OUT;
         if (lane == 0) bulk_wait_read<C::NOB - 1>();  // the store that last used this buffer has read it
         __syncwarp();
-        if constexpr (OUT16) {  // fp16 hi / lo of 2^e U: two 32 x 32 tiles, 64-byte rows, 64-byte swizzle
+        if constexpr (OUT16) {  // fp16 hi / lo of 2^e U: two 32 x OC tiles, 2 OC-byte rows, 2 OC-byte swizzle
+          constexpr int RB = 2 * OC, HB = 32 * RB;  // row bytes, bytes of one half (hi or lo)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
+          for (int jj = 0; jj < OC / 8; ++jj) {
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -339,9 +348,9 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
               hw[i] = *reinterpret_cast<const uint32_t*>(&hh);
               lw[i] = *reinterpret_cast<const uint32_t*>(&ll);
             }
-            const int o = lane * 64 + ((jj ^ ((lane >> 1) & 3)) << 4);
+            const int o = RB == 128 ? lane * 128 + ((jj ^ (lane & 7)) << 4) : lane * 64 + ((jj ^ ((lane >> 1) & 3)) << 4);
             *reinterpret_cast<uint4*>(stg + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(stg + 2048 + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(stg + HB + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
         } else if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
 #pragma unroll
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         if (lane == 0) {
           if (OUT16) {  // U hi / lo maps (s, n, vt), fp16
             tma_store_3d(&out_map, c0 + c, n, vt0, stg);
-            tma_store_3d(&lo_map, c0 + c, n, vt0, stg + 2048);
+            tma_store_3d(&lo_map, c0 + c, n, vt0, stg + 32 * 2 * OC);
           } else if (DIR == 0) {  // U map (s, n, vt)
             if (a.accumulate) tma_add_3d(&out_map, c0 + c, n, vt0, stg);
             else tma_store_3d(&out_map, c0 + c, n, vt0, stg);

@@ -231,9 +231,10 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
     }
   T.off[(size_t)f.n_tables * T.n_nt] = (int)T.k0.size();
   // 2xFP16 images: the fp32 weights w (one rounding from fp64), 2^wexp w -> fp16 hi + lo in the same (row, k)
-  // positions, 64-byte rows with the 64-byte swizzle
+  // positions, BK-half rows: 64-byte rows with the 64-byte swizzle (BK 32) or 128-byte rows with the 128-byte
+  // swizzle (BK 64)
   T.h16.clear();
-  if (BK == 32) {
+  if (BK == 32 || BK == 64) {
     float wmax = 0.f;
     for (size_t i = 0; i < raw.size(); ++i) wmax = std::max(wmax, std::fabs(raw[i]));
     int ex = 0;
@@ -244,13 +245,14 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
     for (size_t b = 0; b < nb; ++b)
       for (int r = 0; r < N; ++r)
         for (int kk = 0; kk < BK; ++kk) {
-          uint32_t o32 = (uint32_t)(r * 128 + kk * 4);  // fp32 image: 128-byte rows, 128-byte swizzle
+          // fp32 image: sub-images of 32 columns, 128-byte rows, 128-byte swizzle
+          uint32_t o32 = (uint32_t)(r * 128 + (kk % 32) * 4);
           o32 ^= ((o32 >> 7) & 7u) << 4;
-          const float w = raw[b * BK * N + o32 / 4];
+          const float w = raw[b * BK * N + (size_t)(kk / 32) * N * 32 + o32 / 4];
           const float ws = (float)std::ldexp((double)w, T.wexp);
           const uint16_t wh = f2h_rn(ws), wl = f2h_rn(ws - h2f(wh));
-          uint32_t o16 = (uint32_t)(r * 64 + kk * 2);
-          o16 ^= ((o16 >> 7) & 3u) << 4;
+          uint32_t o16 = (uint32_t)(r * BK * 2 + kk * 2);
+          o16 ^= ((o16 >> 7) & (BK == 64 ? 7u : 3u)) << 4;
           T.h16[b * 2 * BK * N + o16 / 2] = wh;
           T.h16[b * 2 * BK * N + (size_t)BK * N + o16 / 2] = wl;
         }
@@ -259,7 +261,9 @@ static void build_vtab(const BandFamily& f, int N, int BK, VTab& T) {
 
 static void build_vtabs(const BandFamily& ff, const BandFamily& fa, VTab& vf, VTab& va) {
   const int bk_f = std::getenv("LFM_VBK_F") ? std::atoi(std::getenv("LFM_VBK_F")) : 32;
-  const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 32;
+  // adjoint K blocks of 64 detector columns: with the 2xFP16 Z (fp16) that is 128-byte rows per TMA row, which
+  // measured 45.1 -> 36.9 us per camera against 32 (LFM_VBK_A selects 16 / 32 / 64)
+  const int bk_a = std::getenv("LFM_VBK_A") ? std::atoi(std::getenv("LFM_VBK_A")) : 64;
   build_vtab(ff, 256, bk_f == 16 ? 16 : 32, vf);
   const int vn_a = std::getenv("LFM_VN_A") ? std::atoi(std::getenv("LFM_VN_A")) : 16;
   build_vtab(fa, vn_a == 32 ? 32 : 16, bk_a == 16 ? 16 : bk_a == 64 ? 64 : 32, va);
@@ -449,6 +453,10 @@ static lfm_status encode3(CUtensorMap* map, const void* base, const long long di
   return st;
 }
 
+// 2D tensor map of a row-major matrix (rows x cols, pitch in elements; cached per host thread), defined below
+static lfm_status encode_map(CUtensorMap* map, const void* base, int cols, int rows, long long pitch, int box_c,
+                             int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16 = false);
+
 template <int N, int DIR, int BK, bool OUT16 = false, bool IN16 = false>
 static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUtensorMap& om, int nz, int ny,
                                 float scale, int accumulate, void* stream, std::string& err, int nt0 = 0, int nt_cnt = -1,
@@ -459,7 +467,7 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   const bool kwin = k_lo > 0 || k_hi < (1 << 30);
   static bool attr[LFM_MAX_DEV][2];
   const int dv = cur_dev();
-  constexpr size_t SMEM = VCfg<N, BK, IN16>::SMEM;
+  constexpr size_t SMEM = VCfg<N, BK, IN16, OUT16>::SMEM;
   if (!attr[dv][kwin]) {
     cudaError_t e = kwin ? cudaFuncSetAttribute(band_v_kernel<N, DIR, BK, true, OUT16, IN16>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)
@@ -493,8 +501,18 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   const int grid = std::min(items, g_num_sms());
   const CUtensorMap& lm = lom ? *lom : om;
   const CUtensorMap& alm = alom ? *alom : am;
-  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
-  else band_v_kernel<N, DIR, BK, false, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
+  // IN16: the weight images as a tensor of 128-byte rows, one box (2 B_BYTES / 128 <= 256 rows) per block
+  CUtensorMap wm = am;
+  v.wtma = 0;
+  static const bool wtma_env = std::getenv("LFM_V_WTMA") && std::atoi(std::getenv("LFM_V_WTMA")) != 0;
+  constexpr int WROWS = 2 * VCfg<N, BK, IN16, OUT16>::B_BYTES / 128;
+  if (IN16 && wtma_env && WROWS <= 256 && WROWS * 128 == 2 * VCfg<N, BK, IN16, OUT16>::B_BYTES && !T.k0.empty()) {
+    lfm_status st = encode_map(&wm, T.d_h16, 64, (int)(T.k0.size() * WROWS), 64, 64, WROWS, CU_TENSOR_MAP_SWIZZLE_NONE, err, true);
+    if (st != LFM_OK) return st;
+    v.wtma = 1;
+  }
+  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, wm, v);
+  else band_v_kernel<N, DIR, BK, false, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, wm, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
@@ -505,6 +523,7 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
   if (!T.d_img) { err = "band_v: no forward tables"; return LFM_E_INVALID; }
   CUtensorMap am, om;
   const int ob[3] = {32, 1, 32};
+  const int ob16[3] = {64, 1, 32};  // fp16 U: 64-column boxes (VCfg O16)
   // column window [c0, c1): only the N-tiles (256 detector columns) that meet it
   const int nt0 = std::max(0, c0) / T.N, nt1 = c1 < 0 ? T.n_nt : (c1 + T.N - 1) / T.N;
   lfm_status st;
@@ -517,8 +536,8 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
     const long long od[3] = {nd, nz, ny}, os[2] = {(long long)nd * 2, (long long)nz * nd * 2};
     if ((st = encode3(&am, x16, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
         (st = encode3(&alm, x16 + cp.info.n_vox, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
-        (st = encode3(&om, hi, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
-        (st = encode3(&lm, lo, od, os, ob, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+        (st = encode3(&om, hi, od, os, ob16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
+        (st = encode3(&lm, lo, od, os, ob16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK)
       return st;
     return launch_band_v<256, 0, 32, true, true>(T, am, om, nz, ny, 1.f, 0, stream, err, nt0, nt1 - nt0, 0, 1 << 30, &lm,
                                                  amax, &alm, 1.f, rinv);
@@ -545,7 +564,7 @@ lfm_status k_vpass_fwd(const CameraPlan& cp, const VTab& T, const float* x, floa
 
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
                        std::string& err, int c0, int c1, const float* amax, float in_scale) {
-  const bool in16 = amax && T.d_h16 && T.BK == 32 && T.N == 16;
+  const bool in16 = amax && vpass_adj_in16(T);
   const int nx = cp.info.nx, ny = cp.info.ny, nz = cp.info.nz, nd = cp.adj_c1.n_os;
   if (!T.d_img) { err = "band_v: no adjoint tables"; return LFM_E_INVALID; }
   // column window [c0, c1) of Z (= of y): the data map starts at c0 and is c1 - c0 wide, so columns outside read
@@ -558,9 +577,10 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, floa
     const uint16_t* zh = reinterpret_cast<const uint16_t*>(Z);
     const uint16_t* zl = zh + (size_t)nd * nz * ny;
     const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 2, (long long)nz * nd * 2};
-    const int ab[3] = {32, 1, 128};
-    if ((st = encode3(&am, zh + k_lo, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
-        (st = encode3(&alm, zl + k_lo, ad, as, ab, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+    const int ab[3] = {T.BK, 1, 128};
+    const CUtensorMapSwizzle sw = T.BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if ((st = encode3(&am, zh + k_lo, ad, as, ab, sw, err, true)) != LFM_OK ||
+        (st = encode3(&alm, zl + k_lo, ad, as, ab, sw, err, true)) != LFM_OK)
       return st;
   } else {
     const long long ad[3] = {std::min(k_hi, nd) - k_lo, nz, ny}, as[2] = {(long long)nd * 4, (long long)nz * nd * 4};
@@ -597,8 +617,10 @@ lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, floa
     if (nt_cnt == 0) return LFM_OK;
   }
   if (in16)
-    return launch_band_v<16, 1, 32, false, true>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi,
-                                                 nullptr, amax, &alm, in_scale);
+    return T.BK == 64 ? launch_band_v<16, 1, 64, false, true>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt,
+                                                              k_lo, k_hi, nullptr, amax, &alm, in_scale)
+                      : launch_band_v<16, 1, 32, false, true>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt,
+                                                              k_lo, k_hi, nullptr, amax, &alm, in_scale);
   if (T.N == 32)
     return T.BK == 32 ? launch_band_v<32, 1, 32>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi)
                       : launch_band_v<32, 1, 16>(T, am, om, nz, ny, sc, accumulate, stream, err, nt0, nt_cnt, k_lo, k_hi);
@@ -1497,7 +1519,7 @@ static lfm_status encode_map_raw(CUtensorMap* map, const void* base, int cols, i
                                  int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16);
 // (pitch in elements; f16: 2-byte elements)
 static lfm_status encode_map(CUtensorMap* map, const void* base, int cols, int rows, long long pitch, int box_c,
-                             int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16 = false) {
+                             int box_r, CUtensorMapSwizzle swz, std::string& err, bool f16) {
   const TmapKey k = {base, {2, cols, rows, pitch, box_c, box_r, (long long)swz, f16, 0, 0, 0}};
   if (tmap_lookup(k, map)) return LFM_OK;
   lfm_status st = encode_map_raw(map, base, cols, rows, pitch, box_c, box_r, swz, err, f16);
@@ -1925,9 +1947,21 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     const bool f16 = h16.hi && op.ft->d_uh;
     CUtensorMap map, omap, lmap;
     lfm_status st;
+    bool src3d = false;
     if (f16) {  // fp16 hi / lo maps of the source window, 64-column x 16-row boxes, 128-byte swizzle
       const long long wo = (long long)a.win_r0 * a.src_pitch + term.src_off;
-      if ((st = encode_map(&map, h16.hi + wo, op.n_is, win_rows, a.src_pitch, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
+      // one 8 KB 3D box per source part instead of four 2 KB boxes: the TMA unit's rate grows with the box
+      // (tools/microbench/tma_rate.cu on B200: 82 vs 36 B/cycle/SM); forward t pass 64.5 -> 50.2 us, adjoint
+      // 72.7 -> 62.5 us, 2500 -> 2748 pairs/s.  LFM_U_SRC3D=0 keeps the 2D boxes (A/B).
+      static const bool src3d_env = !std::getenv("LFM_U_SRC3D") || std::atoi(std::getenv("LFM_U_SRC3D")) != 0;
+      src3d = src3d_env && op.n_is % 256 == 0;  // every column group inside the row (no reads past a row's end)
+      if (src3d) {  // (64 columns, rows, column groups of 64): the group stride (128 B) overlaps the row stride
+        const long long d3[3] = {64, win_rows, op.n_is / 64}, s3[2] = {a.src_pitch * 2, 128};
+        const int b3[3] = {64, 16, 4};
+        if ((st = encode3(&map, h16.hi + wo, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
+            (st = encode3(&lmap, h16.lo + wo, d3, s3, b3, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK)
+          return st;
+      } else if ((st = encode_map(&map, h16.hi + wo, op.n_is, win_rows, a.src_pitch, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
           (st = encode_map(&lmap, h16.lo + wo, op.n_is, win_rows, a.src_pitch, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK)
         return st;
     } else {
@@ -1968,6 +2002,18 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.n_amax = LFM_AMAX_SLOTS;
     u.amax_scale = h16.amax_scale;
     u.cinv = h16.cinv;
+    u.src3d = src3d ? 1 : 0;
+    // the weight images as a tensor of 128-byte rows, one 64-row box (8 KB) per block, instead of a bulk copy
+    CUtensorMap wmap = map;
+    static const bool wtma_env = std::getenv("LFM_U_WTMA") && std::atoi(std::getenv("LFM_U_WTMA")) != 0;
+    u.wtma = 0;
+    if (f16 && wtma_env) {
+      const long long nb = (long long)op.ft->u_k0.size();
+      if (nb > 0 && nb * 64 < (1ll << 31) &&
+          (st = encode_map(&wmap, op.ft->d_uh, 64, (int)(nb * 64), 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_NONE, err, true)) != LFM_OK)
+        return st;
+      u.wtma = nb > 0 ? 1 : 0;
+    }
     if (u.cinv && !out16) { err = "band_u: per-column source scales need the fp16 output form"; return LFM_E_INVALID; }
     u.out_scale16 = h16.out_scale16;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
@@ -1997,13 +2043,13 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.tm_nz = op.ft->u_nz;
     if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
     const int grid_u = std::min(u.n_mt * u.n_nt * u.ksplit, g_num_sms());
-    if (out16) band_u_kernel<false, true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, olmap, u);
+    if (out16) band_u_kernel<false, true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, olmap, wmap, u);
     else if (f16) {
-      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
-      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
+      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
     } else {
-      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
-      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
+      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
     }
     ++g_launches;
     if (ksplit > 1) {

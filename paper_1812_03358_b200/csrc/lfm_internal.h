@@ -291,7 +291,7 @@ lfm_status k_split16(const float* src, long long n, const float* amax, uint16_t*
 lfm_status k_vpass_adj(const CameraPlan& cp, const VTab& T, const float* Z, float* out, int accumulate, void* stream,
                        std::string& err, int c0 = 0, int c1 = -1, const float* amax = nullptr, float in_scale = 1.f);
 // whether k_vpass_adj can take an fp16 Z for table T
-inline bool vpass_adj_in16(const VTab& T) { return T.d_h16 && T.BK == 32 && T.N == 16; }
+inline bool vpass_adj_in16(const VTab& T) { return T.d_h16 && (T.BK == 32 || T.BK == 64) && T.N == 16; }
 lfm_status k_spass_adj(const CameraPlan& cp, const float* Z, float* out, int accumulate, void* stream, std::string& err);
 lfm_status k_permute(const float* in, float* out, int nx, int ny, int nz, const int* axis, const int* sign,
                      int accumulate, void* stream, std::string& err);

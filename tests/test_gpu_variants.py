@@ -131,6 +131,33 @@ def test_s_pass_orders(name, transposed, monkeypatch):
         assert max_rel(host(g), op.adjoint(_masked_rows(r, n_t, r0, r1).astype(np.float64))) <= TOL, (name, c)
 
 
+@pytest.mark.parametrize("name", ["small_two", "small_hex"])
+@pytest.mark.parametrize("bk", ["16", "32", "64"])
+def test_band_v_adjoint_block_width(name, bk, monkeypatch):
+    """band_v's adjoint s pass with K blocks of 16 / 32 / 64 detector columns (LFM_VBK_A; 32 and 64 have 2xFP16
+    images, so the fp16 Z of the t pass feeds them directly, 64 with 128-byte rows) against the oracle, also on a
+    column window (the K-window instance)."""
+    from paper_1812_03358_b200 import lfm
+    cfg = make_config(name)
+    monkeypatch.setenv("LFM_VBK_A", bk)
+    monkeypatch.delenv("LFM_TUNE_FILE", raising=False)
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    ops = build_system(cfg)
+    for c, op in enumerate(ops):
+        r = uniform_vector(op.n_pix, 1)
+        g = torch.empty(op.n_vox, device="cuda:0")
+        lfm.A_adjoint(plan, c, dev(r), g, ws, path=1)
+        assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL, (name, bk, c)
+        n_s, n_t = cfg["cameras"][c]["n_s"], cfg["cameras"][c]["n_t"]
+        c0, c1 = 8, n_s - 5
+        lfm.A_adjoint_window(plan, c, 0, n_t, c0, c1, dev(r), g, ws, path=1)
+        rm = r.reshape(n_t, n_s).copy()
+        rm[:, :c0] = 0
+        rm[:, c1:] = 0
+        assert max_rel(host(g), op.adjoint(rm.reshape(-1).astype(np.float64))) <= TOL, (name, bk, c, "window")
+
+
 def test_stage_entry_points():
     """lfm_A_stage runs the forward / adjoint t pass alone on the workspace intermediate (one band_u launch, plus the
     ordered split-K sum on small outputs, as in A_forward; the adjoint's 2xFP16 form also splits its input):

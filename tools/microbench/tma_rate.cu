@@ -16,8 +16,12 @@ using namespace lfm::tc;
 constexpr int STAGES = 8, STAGE = 24576, ITERS = 2000;
 
 // mode 0: 12 tensor boxes (64 x 16 fp16) per stage from the strided map; 1: same from the contiguous map;
-// 2: 3 bulk copies of 8 KB
+// 2: 3 bulk copies of 8 KB; 3: 3 3D boxes (64 x 16 x 4: 4 column groups of 64 in one box, the group stride 128 B
+// overlapping the row stride) from the strided data; 4: 3 2D boxes of 64 rows x 128 B (8 KB contiguous, no
+// swizzle: a verbatim copy of a pre-laid-out image, as band_u's weight images)
 __global__ void __launch_bounds__(128, 1) rate(const __grid_constant__ CUtensorMap m_str, const __grid_constant__ CUtensorMap m_con,
+                                               const __grid_constant__ CUtensorMap m_3d,
+                                               const __grid_constant__ CUtensorMap m_img,
                                                const uint8_t* src, long long src_bytes, int mode, long long* clk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem + 1023) & ~(uintptr_t)1023);
@@ -36,7 +40,11 @@ __global__ void __launch_bounds__(128, 1) rate(const __grid_constant__ CUtensorM
     uint8_t* st = base + s * STAGE;
     mbar_arrive_expect_tx(&full[s], STAGE);
     const int blk = (blockIdx.x * 7919 + it * 104729) & 1023;  // pseudo-random block of rows / images
-    if (mode == 2) {
+    if (mode == 4) {
+      for (int j = 0; j < 3; ++j) tma_load_2d(st + j * 8192, &m_img, 0, ((blk * 3 + j) * 64) % (16384 * 32), &full[s]);
+    } else if (mode == 3) {
+      for (int j = 0; j < 3; ++j) tma_load_3d(st + j * 8192, &m_3d, 0, (blk * 48 + j * 16) % 16384, 0, &full[s]);
+    } else if (mode == 2) {
       for (int j = 0; j < 3; ++j)
         bulk_g2s(st + j * 8192, src + ((long long)(blk * 3 + j) * 8192) % (src_bytes - 8192), 8192, &full[s]);
     } else {
@@ -75,12 +83,29 @@ int main() {
     enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, d, gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
+  CUtensorMap m3;
+  {  // the strided data as (64 columns, rows, column groups): box 64 x 16 x 4 = 8 KB, [group][row][64] in shared memory
+    cuuint64_t gd[3] = {64, 16384, 32}, gs[2] = {4096, 128};
+    cuuint32_t b3[3] = {64, 16, 4}, e3[3] = {1, 1, 1};
+    CUresult r = enc(&m3, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d, gd, gs, b3, e3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    printf("3D map with overlapping group stride: encode %s (%d)\n", r == CUDA_SUCCESS ? "ok" : "FAILED", (int)r);
+    if (r != CUDA_SUCCESS) m3 = ms;
+  }
+  CUtensorMap mi;
+  {  // 8 KB images as rows of 128 B, box 64 rows, no swizzle
+    cuuint64_t gd[2] = {64, 16384 * 32}, gs[1] = {128};
+    cuuint32_t bi[2] = {64, 64}, ei[2] = {1, 1};
+    enc(&mi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, d, gd, gs, bi, ei, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   const int smem = STAGES * STAGE + 1024;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[3] = {"tensor boxes 16 x 128 B, rows 4 KB apart", "tensor boxes 16 x 128 B, contiguous", "bulk 8 KB"};
+  const char* names[5] = {"tensor boxes 16 x 128 B, rows 4 KB apart", "tensor boxes 16 x 128 B, contiguous", "bulk 8 KB",
+                          "3D boxes 4 x 16 x 128 B, rows 4 KB apart", "2D boxes 64 x 128 B (8 KB image), no swizzle"};
   for (int rep = 0; rep < 2; ++rep)
-    for (int mode = 0; mode < 3; ++mode) {
-      rate<<<148, 128, smem>>>(ms, mc, d, bytes, mode, dclk);
+    for (int mode = 0; mode < 5; ++mode) {
+      rate<<<148, 128, smem>>>(ms, mc, m3, mi, d, bytes, mode, dclk);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
       std::vector<long long> c(148);
