@@ -55,7 +55,6 @@ struct UArgs {
                           // row tiles x 128), summed in a fixed order by sum_chunks_kernel (deterministic)
   int kc_rows;
   int src3d;              // 2xFP16: the source maps are 3D (64 columns, rows, 64-column groups), one box per part
-  int wtma;               // 2xFP16: the weight images come through w_map (rows of 128 B, one 64-row box per block)
 };
 
 
@@ -105,8 +104,11 @@ __device__ __forceinline__ UItem u_item(const UArgs& a, int it) {
 constexpr int U_STAGES = 4;
 constexpr int U_STAGE_BYTES = 49152;  // A hi+lo (16 KB) | src tile (16 KB) | src lo (16 KB)
 // 2xFP16: A hi+lo (8 KB) | src tile fp32 (16 KB), overwritten in place by the fp16 src hi (8 KB) | src lo (8 KB)
-template <bool F16> struct UStage {
-  static constexpr int STAGES = F16 ? 8 : U_STAGES;
+// OUT16 (the adjoint's fp16 Z): 6 stages and 8 KB of epilogue staging per warp, so Z goes out in 64-column boxes
+// (whole 128-byte lines of its fp16 rows) -- the source (the split y) is L2-resident, so fewer stages suffice
+template <bool F16, bool OUT16 = false> struct UStage {
+  static constexpr int STAGES = OUT16 ? 6 : F16 ? 8 : U_STAGES;
+  static constexpr int OUT = OUT16 ? 8192 : 4096;  // epilogue staging per warp
   static constexpr int BYTES = F16 ? 24576 : U_STAGE_BYTES;
 };
 constexpr int U_THREADS = 384;
@@ -121,15 +123,17 @@ template <bool SPLIT, bool F16 = false, bool OUT16 = false>
 __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_constant__ CUtensorMap src_map,
                                                               const __grid_constant__ CUtensorMap out_map,
                                                               const __grid_constant__ CUtensorMap lo_map,
-                                                              const __grid_constant__ CUtensorMap out_lo_map,
-                                                              const __grid_constant__ CUtensorMap w_map, UArgs a) {
+                                                              const __grid_constant__ CUtensorMap out_lo_map, UArgs a) {
   static_assert(!OUT16 || (F16 && !SPLIT), "fp16 output: 2xFP16 form, no split-K");
   using namespace tc;
-  constexpr int U_STAGES = UStage<F16>::STAGES, U_STAGE_BYTES = UStage<F16>::BYTES;
+  constexpr int U_STAGES = UStage<F16, OUT16>::STAGES, U_STAGE_BYTES = UStage<F16, OUT16>::BYTES;
+  constexpr int U_STAGE_OUT = UStage<F16, OUT16>::OUT;
   static_assert(UStage<true>::STAGES * UStage<true>::BYTES == 4 * 49152, "same ring size");
+  static_assert(UStage<F16, OUT16>::STAGES * UStage<F16, OUT16>::BYTES + 8 * U_STAGE_OUT + 1024 + 256 <= U_SMEM,
+                "shared memory");
   extern __shared__ uint8_t u_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)u_smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sout = sm + U_STAGES * U_STAGE_BYTES;  // epilogue staging, 8 x 4 KB
+  uint8_t* sout = sm + U_STAGES * U_STAGE_BYTES;  // epilogue staging, 8 x 4 KB (OUT16: 8 x 8 KB)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sout + 8 * U_STAGE_OUT);
   uint64_t* full = bars;                  // TMA landed (tx count)
   uint64_t* conv = bars + U_STAGES;       // lo split written (64 arrivals)
@@ -182,8 +186,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
           if constexpr (F16) {  // fp16 weight images (8 KB); pre-split fp16 source hi and lo, 4 boxes of 16 rows x 64
                                 // columns each with the 128-byte swizzle = the MN-major operand layout
             mbar_arrive_expect_tx(&full[s], 8192 + 16384);
-            if (a.wtma) tma_load_2d(st, &w_map, 0, b * 64, &full[s]);  // a verbatim 8 KB copy (no swizzle)
-            else bulk_g2s(st, a.H + (size_t)b * 4096, 8192, &full[s]);
+            bulk_g2s(st, a.H + (size_t)b * 4096, 8192, &full[s]);
             if (a.src3d) {  // 4 column groups x 16 rows x 64 columns = the same [g][row][64] layout in one box
               tma_load_3d(st + 8192, &src_map, 0, k, nt * 4, &full[s]);
               tma_load_3d(st + 16384, &lo_map, 0, k, nt * 4, &full[s]);
@@ -340,13 +343,14 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
                                         : (2 * (mt / (a.tm_nz >> 6)) + (q >> 1)) * a.tm_nz + 64 * (mt % (a.tm_nz >> 6)) + 32 * (q & 1)) +
                      ui.kc * a.kc_rows;
       const int c0 = nt * 256 + h * 128;
+      constexpr int CW = OUT16 ? 64 : 32;  // columns per store
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < 128; c += CW) {
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
-        if constexpr (OUT16) {  // fp16 hi / lo of 2^e' out: two 32 x 32 tiles, 64-byte rows, 64-byte swizzle
+        if constexpr (OUT16) {  // fp16 hi / lo of 2^e' out: two 32 x 64 tiles, 128-byte rows, 128-byte swizzle
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
+          for (int jj = 0; jj < 8; ++jj) {
             uint32_t hw[4], lw[4];
             float ci[8];
             if (a.cinv) {
@@ -369,15 +373,15 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
               hw[i] = *reinterpret_cast<const uint32_t*>(&hh);
               lw[i] = *reinterpret_cast<const uint32_t*>(&ll);
             }
-            const int o = lane * 64 + ((jj ^ ((lane >> 1) & 3)) << 4);
+            const int o = lane * 128 + ((jj ^ (lane & 7)) << 4);
             *reinterpret_cast<uint4*>(stg + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(stg + 2048 + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(stg + 4096 + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&out_map, c0 + c, r0, stg);
-            tma_store_2d(&out_lo_map, c0 + c, r0, stg + 2048);
+            tma_store_2d(&out_lo_map, c0 + c, r0, stg + 4096);
             bulk_commit();
           }
           continue;

@@ -41,7 +41,6 @@ struct VArgs {
   float in_scale;          // IN16: the data arrives as fp16 hi + lo of 2^e data, e = u_data_exp(amax, in_scale)
   const float* rinv;       // IN16 forward: per data row (n ny + vt) scales instead: the row was split as 2^e_row x,
   int ny;                  // rinv[row] = 2^-e_row (split16_rows_kernel)
-  int wtma;                // IN16: the weight images come through w_map (rows of 128 B, one box per block)
 };
 
 
@@ -106,8 +105,7 @@ template <int N, int DIR, int BK, bool KWIN = false, bool OUT16 = false, bool IN
 __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_constant__ CUtensorMap a_map,
                                                               const __grid_constant__ CUtensorMap out_map,
                                                               const __grid_constant__ CUtensorMap lo_map,
-                                                              const __grid_constant__ CUtensorMap a_lo_map,
-                                                              const __grid_constant__ CUtensorMap w_map, VArgs a) {
+                                                              const __grid_constant__ CUtensorMap a_lo_map, VArgs a) {
   using namespace tc;
   using C = VCfg<N, BK, IN16, OUT16>;
   static_assert(!OUT16 || (DIR == 0 && N == 256), "fp16 output: forward, 256-column tiles");
@@ -156,10 +154,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = sm + s * C::STAGE;
           mbar_arrive_expect_tx(&full[s], (IN16 ? 2 : 1) * C::A_BYTES + 2 * C::B_BYTES);
-          if constexpr (IN16) {
-            if (a.wtma) tma_load_2d(st + 2 * C::A_BYTES, &w_map, 0, b * (2 * C::B_BYTES / 128), &full[s]);
-            else bulk_g2s(st + 2 * C::A_BYTES, a.H + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
-          }
+          if constexpr (IN16) bulk_g2s(st + 2 * C::A_BYTES, a.H + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           else bulk_g2s(st + 2 * C::A_BYTES, a.B + (size_t)b * 2 * BK * N, 2 * C::B_BYTES, &full[s]);
           const int k = __ldg(a.blk_k0 + b) - (KWIN ? a.k_lo : 0);
 #pragma unroll

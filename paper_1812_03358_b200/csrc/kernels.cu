@@ -501,18 +501,8 @@ static lfm_status launch_band_v(const VTab& T, const CUtensorMap& am, const CUte
   const int grid = std::min(items, g_num_sms());
   const CUtensorMap& lm = lom ? *lom : om;
   const CUtensorMap& alm = alom ? *alom : am;
-  // IN16: the weight images as a tensor of 128-byte rows, one box (2 B_BYTES / 128 <= 256 rows) per block
-  CUtensorMap wm = am;
-  v.wtma = 0;
-  static const bool wtma_env = std::getenv("LFM_V_WTMA") && std::atoi(std::getenv("LFM_V_WTMA")) != 0;
-  constexpr int WROWS = 2 * VCfg<N, BK, IN16, OUT16>::B_BYTES / 128;
-  if (IN16 && wtma_env && WROWS <= 256 && WROWS * 128 == 2 * VCfg<N, BK, IN16, OUT16>::B_BYTES && !T.k0.empty()) {
-    lfm_status st = encode_map(&wm, T.d_h16, 64, (int)(T.k0.size() * WROWS), 64, 64, WROWS, CU_TENSOR_MAP_SWIZZLE_NONE, err, true);
-    if (st != LFM_OK) return st;
-    v.wtma = 1;
-  }
-  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, wm, v);
-  else band_v_kernel<N, DIR, BK, false, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, wm, v);
+  if (kwin) band_v_kernel<N, DIR, BK, true, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
+  else band_v_kernel<N, DIR, BK, false, OUT16, IN16><<<grid, V_THREADS, SMEM, (cudaStream_t)stream>>>(am, om, lm, alm, v);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "band_v_kernel launch", err);
 }
@@ -1681,6 +1671,40 @@ __global__ void split16_rows_kernel(const float* __restrict__ src, int rows, int
   const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   const bool vec = (len & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (len & 7) == 0;
   uint32_t cmax = 0;
+  if (vec && len <= 128) {  // one float4 per lane and row: 4 rows per warp with their loads in flight together
+    constexpr int RB = 4;
+    const int nw = gridDim.x * wpb;
+    for (int r0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * RB; r0 < rows; r0 += nw * RB) {
+      float4 v[RB];
+      const bool on = 4 * lane < len;
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        v[i] = on && r0 + i < rows ? __ldg(reinterpret_cast<const float4*>(src + (long long)(r0 + i) * len) + lane)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int row = r0 + i;
+        uint32_t m = max(max(__float_as_uint(v[i].x) & 0x7fffffffu, __float_as_uint(v[i].y) & 0x7fffffffu),
+                         max(__float_as_uint(v[i].z) & 0x7fffffffu, __float_as_uint(v[i].w) & 0x7fffffffu));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (row >= rows) continue;  // (uniform across the warp)
+        cmax = max(cmax, m);
+        const int e = data_exp(__uint_as_float(m));
+        const float sig = pow2f(e);
+        if (lane == 0) rinv[row] = pow2f(-e);
+        if (on) {
+          const float x0 = sig * v[i].x, x1 = sig * v[i].y, x2 = sig * v[i].z, x3 = sig * v[i].w;
+          const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+          const long long o4 = (long long)row * len + 4 * lane;
+          *reinterpret_cast<uint2*>(hi + o4) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+          *reinterpret_cast<uint2*>(lo + o4) = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+        }
+      }
+    }
+  } else
   for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
     const float* r = src + (long long)row * len;
     uint32_t m = 0;
@@ -1734,93 +1758,89 @@ __global__ void split16_rows_kernel(const float* __restrict__ src, int rows, int
 }
 
 // Column-scaled fp16 split in one pass (the adjoint t pass's input y: the t pass mixes rows, never columns, so a
-// scale per column is undone per output column by band_u's epilogue): a CTA owns strips of 16 columns over all
-// `rows` rows; pass 1 takes the column maxima (8 float4 loads in flight per thread), e_c = data_exp(max_c),
-// cinv[c] = 2^-e_c; pass 2 re-reads the strip (L1 / L2) and writes fp16 hi / lo of 2^e_c src.  The per-CTA maxima
-// go to part (CTA 0 zero-fills the other LFM_AMAX_SLOTS) for the global scale of the t pass's fp16 output.
-// Needs cols % 4 == 0 and 16-byte aligned src / hi / lo rows (pitch = cols); cinv is padded with 1 up to cols_pad.
-constexpr int SPLITC_THREADS = 1024;
+// scale per column is undone per output column by band_u's epilogue): a CTA owns strips of SPLITC_SC columns over
+// all `rows` rows; the first SPLITC_KEEP float4 of each thread stay in registers (the whole strip for rows <=
+// SPLITC_KEEP * SPLITC_RSTEP, so y is read once), e_c = data_exp(max_c), cinv[c] = 2^-e_c, then fp16 hi / lo of
+// 2^e_c src.  The per-CTA maxima go to part (CTA 0 zero-fills the other LFM_AMAX_SLOTS) for the global scale of
+// the t pass's fp16 output.  Needs cols % 4 == 0 and 16-byte aligned src / hi / lo rows (pitch = cols); cinv is
+// padded with 1 up to cols_pad.
+constexpr int SPLITC_THREADS = 512, SPLITC_SC = 16, SPLITC_QN = SPLITC_SC / 4, SPLITC_RSTEP = SPLITC_THREADS / SPLITC_QN,
+              SPLITC_KEEP = 16;
+__device__ __forceinline__ void split_store(uint16_t* hi, uint16_t* lo, long long o, float4 v, float4 sg) {
+  const float x0 = sg.x * v.x, x1 = sg.y * v.y, x2 = sg.z * v.z, x3 = sg.w * v.w;
+  const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+  *reinterpret_cast<uint2*>(hi + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  *reinterpret_cast<uint2*>(lo + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+__device__ __forceinline__ void amax4(uint32_t (&m)[4], float4 v) {
+  m[0] = max(m[0], __float_as_uint(v.x) & 0x7fffffffu);
+  m[1] = max(m[1], __float_as_uint(v.y) & 0x7fffffffu);
+  m[2] = max(m[2], __float_as_uint(v.z) & 0x7fffffffu);
+  m[3] = max(m[3], __float_as_uint(v.w) & 0x7fffffffu);
+}
 __global__ void __launch_bounds__(SPLITC_THREADS) split16_cols_kernel(const float* __restrict__ src, int rows, int cols,
                                                                       int cols_pad, float* __restrict__ part,
                                                                       float* __restrict__ cinv, uint16_t* __restrict__ hi,
                                                                       uint16_t* __restrict__ lo) {
-  __shared__ float4 red[SPLITC_THREADS / 32][4];
-  __shared__ float4 csig[4];
-  const int t = threadIdx.x, lane = t & 31, wp = t >> 5, q = t & 3, r_first = t >> 2;
-  constexpr int RSTEP = SPLITC_THREADS / 4;
-  const int nstrips = (cols + 15) / 16;
+  __shared__ uint32_t red[SPLITC_THREADS / 32][SPLITC_SC];
+  __shared__ float csig[SPLITC_SC];
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5, q = t % SPLITC_QN, r_first = t / SPLITC_QN;
+  const int nstrips = (cols + SPLITC_SC - 1) / SPLITC_SC;
   uint32_t cmax = 0;
   for (int strip = blockIdx.x; strip < nstrips; strip += gridDim.x) {
-    const int c = strip * 16 + 4 * q;  // this thread's 4 columns
+    const int c = strip * SPLITC_SC + 4 * q;  // this thread's 4 columns
     const bool live = c < cols;
-    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    int r = r_first;
-    for (; r + 7 * RSTEP < rows; r += 8 * RSTEP) {
-      float4 v[8];
+    uint32_t m[4] = {0, 0, 0, 0};
+    float4 keep[SPLITC_KEEP];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        v[j] = live ? __ldg(reinterpret_cast<const float4*>(src + (long long)(r + j * RSTEP) * cols + c)) : make_float4(0, 0, 0, 0);
+    for (int j = 0; j < SPLITC_KEEP; ++j) {
+      const int r = r_first + j * SPLITC_RSTEP;
+      keep[j] = live && r < rows ? __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)) : make_float4(0, 0, 0, 0);
+      amax4(m, keep[j]);
+    }
+    for (int r = r_first + SPLITC_KEEP * SPLITC_RSTEP; r < rows; r += SPLITC_RSTEP)  // taller strips
+      if (live) amax4(m, __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        m0 = max(m0, __float_as_uint(v[j].x) & 0x7fffffffu);
-        m1 = max(m1, __float_as_uint(v[j].y) & 0x7fffffffu);
-        m2 = max(m2, __float_as_uint(v[j].z) & 0x7fffffffu);
-        m3 = max(m3, __float_as_uint(v[j].w) & 0x7fffffffu);
-      }
-    }
-    for (; r < rows; r += RSTEP) {
-      const float4 v = live ? __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)) : make_float4(0, 0, 0, 0);
-      m0 = max(m0, __float_as_uint(v.x) & 0x7fffffffu);
-      m1 = max(m1, __float_as_uint(v.y) & 0x7fffffffu);
-      m2 = max(m2, __float_as_uint(v.z) & 0x7fffffffu);
-      m3 = max(m3, __float_as_uint(v.w) & 0x7fffffffu);
-    }
+    for (int o = SPLITC_QN; o < 32; o <<= 1)  // lanes of the same column quad
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {  // lanes of the same column quad
-      m0 = max(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-      m1 = max(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-      m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, o));
-      m3 = max(m3, __shfl_xor_sync(0xffffffffu, m3, o));
-    }
-    if (lane < 4) red[wp][lane] = make_float4(__uint_as_float(m0), __uint_as_float(m1), __uint_as_float(m2), __uint_as_float(m3));
+      for (int i = 0; i < 4; ++i) m[i] = max(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+    if (lane < SPLITC_QN)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) red[wp][4 * lane + i] = m[i];
     __syncthreads();
-    if (t < 16) {  // column strip*16 + t
-      uint32_t m = 0;
-      for (int w = 0; w < SPLITC_THREADS / 32; ++w) {
-        const float4 v = red[w][t >> 2];
-        const float x = (t & 3) == 0 ? v.x : (t & 3) == 1 ? v.y : (t & 3) == 2 ? v.z : v.w;
-        m = max(m, __float_as_uint(x));
-      }
-      cmax = max(cmax, m);
-      const int e = data_exp(__uint_as_float(m));
-      reinterpret_cast<float*>(csig)[t] = pow2f(e);
-      const int col = strip * 16 + t;
+    if (t < SPLITC_SC) {  // column strip * SC + t
+      uint32_t mc = 0;
+      for (int w = 0; w < SPLITC_THREADS / 32; ++w) mc = max(mc, red[w][t]);
+      cmax = max(cmax, mc);
+      const int e = data_exp(__uint_as_float(mc));
+      csig[t] = pow2f(e);
+      const int col = strip * SPLITC_SC + t;
       if (col < cols_pad) cinv[col] = col < cols ? pow2f(-e) : 1.f;
     }
     __syncthreads();
     if (live) {
-      const float4 sg = csig[q];
-      for (int r = r_first; r < rows; r += RSTEP) {
-        const long long o = (long long)r * cols + c;
-        const float4 v = __ldg(reinterpret_cast<const float4*>(src + o));
-        const float x0 = sg.x * v.x, x1 = sg.y * v.y, x2 = sg.z * v.z, x3 = sg.w * v.w;
-        const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
-        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-        const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
-        *reinterpret_cast<uint2*>(hi + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
-        *reinterpret_cast<uint2*>(lo + o) = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+      const float4 sg = make_float4(csig[4 * q], csig[4 * q + 1], csig[4 * q + 2], csig[4 * q + 3]);
+#pragma unroll
+      for (int j = 0; j < SPLITC_KEEP; ++j) {
+        const int r = r_first + j * SPLITC_RSTEP;
+        if (r < rows) split_store(hi, lo, (long long)r * cols + c, keep[j], sg);
       }
+      for (int r = r_first + SPLITC_KEEP * SPLITC_RSTEP; r < rows; r += SPLITC_RSTEP)
+        split_store(hi, lo, (long long)r * cols + c, __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)), sg);
     }
   }
   // strip padding past the last strip (cols_pad may exceed the strips' columns)
-  for (int col = nstrips * 16 + (int)(blockIdx.x * SPLITC_THREADS + t); col < cols_pad; col += gridDim.x * SPLITC_THREADS)
+  for (int col = nstrips * SPLITC_SC + (int)(blockIdx.x * SPLITC_THREADS + t); col < cols_pad; col += gridDim.x * SPLITC_THREADS)
     cinv[col] = 1.f;
-  if (t < 16) {
+  if (t < 32) {
+    uint32_t mm = t < SPLITC_SC ? cmax : 0u;
 #pragma unroll
-    for (int o = 8; o; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0x0000ffffu, cmax, o));
-    if (t == 0) part[blockIdx.x] = __uint_as_float(cmax);
+    for (int o = 16; o; o >>= 1) mm = max(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+    if (t == 0) part[blockIdx.x] = __uint_as_float(mm);
     if (blockIdx.x == 0)
-      for (int i = gridDim.x + t; i < LFM_AMAX_SLOTS; i += 16) part[i] = 0.f;
+      for (int i = gridDim.x + t; i < LFM_AMAX_SLOTS; i += 32) part[i] = 0.f;
   }
 }
 
@@ -1830,7 +1850,7 @@ lfm_status k_split16_cols(const float* src, int rows, int cols, int cols_pad, fl
     err = "split16_cols: columns must be a multiple of 4 and rows 16-byte aligned";
     return LFM_E_INVALID;
   }
-  const int g = std::max(1, std::min(LFM_AMAX_SLOTS, (cols + 15) / 16));
+  const int g = std::max(1, std::min(LFM_AMAX_SLOTS, (cols + SPLITC_SC - 1) / SPLITC_SC));
   split16_cols_kernel<<<g, SPLITC_THREADS, 0, (cudaStream_t)stream>>>(src, rows, cols, cols_pad, part, cinv, hi, lo);
   ++g_launches;
   return cuda_check(cudaGetLastError(), "split16_cols_kernel launch", err);
@@ -1974,8 +1994,8 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     if (out16) {
       if (ksplit > 1 || accumulate) { err = "band_u: fp16 output without split-K or accumulation"; return LFM_E_INVALID; }
       const long long oo = (long long)b0 * a.out_stride;
-      if ((st = encode_map(&omap, h16.out_hi + oo, op.n_os, op.n_ot, a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK ||
-          (st = encode_map(&olmap, h16.out_lo + oo, op.n_os, op.n_ot, a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, err, true)) != LFM_OK)
+      if ((st = encode_map(&omap, h16.out_hi + oo, op.n_os, op.n_ot, a.out_pitch, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK ||
+          (st = encode_map(&olmap, h16.out_lo + oo, op.n_os, op.n_ot, a.out_pitch, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B, err, true)) != LFM_OK)
         return st;
     } else if (ksplit > 1)
       st = encode_map(&omap, part, op.n_os, (int)(ksplit * kc_rows), a.out_pitch, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B, err);
@@ -2003,17 +2023,6 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.amax_scale = h16.amax_scale;
     u.cinv = h16.cinv;
     u.src3d = src3d ? 1 : 0;
-    // the weight images as a tensor of 128-byte rows, one 64-row box (8 KB) per block, instead of a bulk copy
-    CUtensorMap wmap = map;
-    static const bool wtma_env = std::getenv("LFM_U_WTMA") && std::atoi(std::getenv("LFM_U_WTMA")) != 0;
-    u.wtma = 0;
-    if (f16 && wtma_env) {
-      const long long nb = (long long)op.ft->u_k0.size();
-      if (nb > 0 && nb * 64 < (1ll << 31) &&
-          (st = encode_map(&wmap, op.ft->d_uh, 64, (int)(nb * 64), 64, 64, 64, CU_TENSOR_MAP_SWIZZLE_NONE, err, true)) != LFM_OK)
-        return st;
-      u.wtma = nb > 0 ? 1 : 0;
-    }
     if (u.cinv && !out16) { err = "band_u: per-column source scales need the fp16 output form"; return LFM_E_INVALID; }
     u.out_scale16 = h16.out_scale16;
     u.blk_off = op.ft->d_uoff + (size_t)term.t_tab * n_mt;
@@ -2043,13 +2052,13 @@ lfm_status launch_sep(const SepOp& op, const float* src, float* out, int b0, int
     u.tm_nz = op.ft->u_nz;
     if (u.tile_mode && (r0 != 0 || r1 != op.n_ot)) { err = "band_u: slice-pair tiles need the full output row range"; return LFM_E_INVALID; }
     const int grid_u = std::min(u.n_mt * u.n_nt * u.ksplit, g_num_sms());
-    if (out16) band_u_kernel<false, true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, olmap, wmap, u);
+    if (out16) band_u_kernel<false, true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, olmap, u);
     else if (f16) {
-      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
-      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
+      if (ksplit > 1) band_u_kernel<true, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      else band_u_kernel<false, true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
     } else {
-      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
-      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, wmap, u);
+      if (ksplit > 1) band_u_kernel<true><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
+      else band_u_kernel<false><<<grid_u, U_THREADS, U_SMEM, s>>>(map, omap, lmap, omap, u);
     }
     ++g_launches;
     if (ksplit > 1) {
