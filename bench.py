@@ -46,8 +46,6 @@ def parse():
     ap.add_argument("--profile-timed", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (for ncu --profile-from-start off)")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed pairs eagerly instead of as a CUDA graph")
-    ap.add_argument("--no-chain", action="store_true",
-                    help="concurrent items: private volumes summed after the join instead of chained accumulating adjoints")
     return ap.parse_args()
 
 
@@ -353,20 +351,8 @@ def run_ours(args, rank, world, local_rank):
             lfm.A_adjoint_window(plan, c, *win, r, gv, wss[i], accumulate=False, path=path)
             launches[0] += lfm.last_launch_count()
 
-        done = [torch.cuda.Event() for _ in items]
-
-        def chain(i, j):  # item i's stream waits for what item j has issued so far (its adjoint)
-            done[j].record(streams[j])
-            streams[i].wait_event(done[j])
-
-        def adj_acc_i(i, c, win, r, gv):
-            lfm.A_adjoint_window(plan, c, *win, r, gv, wss[i], accumulate=True, path=path)
-            launches[0] += lfm.last_launch_count()
-
-        chained = not args.no_chain
         runner = ConcurrentPair(items, fwd_i, adj_i, accumulate, lambda gv: gv.zero_(), run, join, private,
-                                allreduce if world > 1 else None, chain=chain if chained else None,
-                                accumulate_adjoint=adj_acc_i)
+                                allreduce if world > 1 else None)
     else:
         start = None
         runner = PairRunner(items, fwd_win, adj_win, lambda gv: gv.zero_(), allreduce if world > 1 else None)

@@ -84,15 +84,9 @@ class ConcurrentPair:
     run(i, fn) runs fn on item i's stream after the previous call's inputs are visible (injected: CUDA
     streams on a GPU, plain calls on CPU); join() makes the main stream wait for every item;
     accumulate(src, dst) adds on the main stream.
-
-    With `chain` (chain(i, j): item i's later work waits for the work item j has issued so far) the adjoints are
-    chained instead: item 0's writes g, item i > 0 waits for item i - 1's adjoint and accumulates into g inside
-    its own last kernel (accumulate_adjoint(i, c, win, r, g)), so no private volume and no separate sum -- the
-    same summation order, g = ((A_0^T r_0) + A_1^T r_1) + ..., hence the same bits.  The forwards still overlap.
     """
 
-    def __init__(self, items, forward_win, adjoint_win, accumulate, zero, run, join, private, allreduce=None,
-                 chain=None, accumulate_adjoint=None):
+    def __init__(self, items, forward_win, adjoint_win, accumulate, zero, run, join, private, allreduce=None):
         self.items = items
         self.forward_win = forward_win        # (i, c, win, x, y)
         self.adjoint_win = adjoint_win        # (i, c, win, r, g_target)   overwrite
@@ -102,26 +96,9 @@ class ConcurrentPair:
         self.join = join                      # ()
         self.private = private                # private[i] for i >= 1: volume buffers
         self.allreduce = allreduce
-        self.chain = chain                    # (i, j) or None
-        self.accumulate_adjoint = accumulate_adjoint  # (i, c, win, r, g)  g += A_c^T P_win r
 
     def compute(self, x, ys, rs, g):
         """Everything but the all-reduce (what a per-rank CUDA graph captures)."""
-        if self.chain is not None:
-            for i, (c, *win) in enumerate(self.items):
-                w = tuple(win)
-                self.run(i, lambda i=i, c=c, w=w: self.forward_win(i, c, w, x, ys[c]))
-            for i, (c, *win) in enumerate(self.items):
-                w = tuple(win)
-                if i == 0:
-                    self.run(i, lambda i=i, c=c, w=w: self.adjoint_win(i, c, w, rs[c], g))
-                else:
-                    self.chain(i, i - 1)
-                    self.run(i, lambda i=i, c=c, w=w: self.accumulate_adjoint(i, c, w, rs[c], g))
-            self.join()
-            if not self.items:
-                self.zero(g)
-            return
         for i, (c, *win) in enumerate(self.items):
             tgt = g if i == 0 else self.private[i]
             w = tuple(win)

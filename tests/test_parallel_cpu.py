@@ -131,57 +131,3 @@ def test_concurrent_pair_sums_in_item_order():
     assert np.array_equal(g1, g2)
     for a, b in zip(ys1, ys2):
         assert np.array_equal(a, b)
-
-
-def test_concurrent_pair_chained_adjoints():
-    """ConcurrentPair with chained adjoints: every item's forward first, item 0's adjoint writes g, item i > 0
-    waits for item i - 1 (chain) and accumulates -- bitwise the sequential PairRunner result, each wait issued
-    after the adjoint it waits for, no private volume and no separate sum."""
-    from oracle.system import build_system
-    from workloads import make_config, uniform_vector, uniform_volume
-    cfg = make_config("tiny_multi")
-    ops = build_system(cfg)
-    x = uniform_volume(cfg["volume"], 0).astype(np.float64).ravel()
-    rs = [uniform_vector(op.n_pix, 1 + c).astype(np.float64) for c, op in enumerate(ops)]
-    items = [(c, 0, cam["n_t"], 0, cam["n_s"]) for c, cam in enumerate(cfg["cameras"])]
-    assert len(items) >= 3
-
-    def adj(c, r, g, acc):
-        v = ops[c].adjoint(r)
-        if acc:
-            g += v
-        else:
-            g[:] = v
-
-    ys1 = [np.zeros(op.n_pix) for op in ops]
-    g1 = np.zeros(ops[0].n_vox)
-    PairRunner(items, lambda c, w, xv, y: y.__setitem__(slice(None), ops[c].forward(xv)),
-               lambda c, w, r, g, acc: adj(c, r, g, acc), lambda g: g.fill(0.0)).pair(x, ys1, rs, g1)
-    log = []
-    ys2 = [np.zeros(op.n_pix) for op in ops]
-    g2 = np.full(ops[0].n_vox, np.nan)
-
-    def fwd(i, c, w, xv, y):
-        log.append(("fwd", i))
-        y[:] = ops[c].forward(xv)
-
-    def adj_over(i, c, w, r, g):
-        log.append(("adj", i))
-        adj(c, r, g, False)
-
-    def adj_acc(i, c, w, r, g):
-        log.append(("adj+", i))
-        adj(c, r, g, True)
-
-    ConcurrentPair(items, fwd, adj_over, lambda src, dst: log.append(("sum",)), lambda g: g.fill(0.0),
-                   lambda i, fn: fn(), lambda: None, [None] * len(items),
-                   chain=lambda i, j: log.append(("wait", i, j)), accumulate_adjoint=adj_acc).pair(x, ys2, rs, g2)
-    n = len(items)
-    assert log[:n] == [("fwd", i) for i in range(n)]
-    expect = [("adj", 0)]
-    for i in range(1, n):
-        expect += [("wait", i, i - 1), ("adj+", i)]
-    assert log[n:] == expect
-    assert np.array_equal(g1, g2)
-    for a, b in zip(ys1, ys2):
-        assert np.array_equal(a, b)
