@@ -702,12 +702,12 @@ def run_ours(args, rank, world, local_rank):
             # pre-split hi/lo operands): its roof is the fp16 dense tensor peak = measured bf16 peak (same rate).
             # `achieved` is the algorithmic (non-zero) work; `issued` the dense block MMAs it runs; `l2_feed` the
             # bytes its TMA brings into shared memory (weights 8 KB + source 16 KB per 16-row block and 256 columns
-            # = issued MACs / 64) against the measured TMA fill rate of all SMs (tools/microbench/tma_rate.cu:
-            # ~36 B/cycle/SM), the bound it actually runs into.
+            # = issued MACs / 64) against the measured TMA fill rate of all SMs for the 8 KB 3D boxes it issues
+            # (tools/microbench/tma_rate.cu: 82-88 B/cycle/SM from L2).
             f16_peak = peaks.get("bf16_tflops", 1653.4)
             issued = 2.0 * dom["mma"] / (dom["fwd_ms"] * 1e-3) / 1e12
             staged = dom["mma"] / 64.0
-            feed_peak = 36.0 * 148 * sm_max * 1e6 / 1e9  # GB/s
+            feed_peak = 85.0 * 148 * sm_max * 1e6 / 1e9  # GB/s
             feed = staged / (dom["fwd_ms"] * 1e-3) / 1e9
             roof.update({"bound": "tensor", "peak": f16_peak, "frac": achieved / f16_peak,
                          "peak_note": "fp16 dense tensor peak = MEASURED_PEAKS bf16_tflops %.1f (fp16 and bf16 share "
@@ -716,8 +716,8 @@ def run_ours(args, rank, world, local_rank):
                                     "what": "2xFP16 dense 128x16-block MACs (3 products) x 2 per launch / time"},
                          "l2_feed": {"achieved_gbs": feed, "peak_gbs": feed_peak, "frac": feed / feed_peak,
                                      "bytes_per_launch": staged,
-                                     "what": "TMA L2->shared bytes per launch / time vs 36 B/cycle/SM x 148 SMs "
-                                             "(measured, tools/microbench/tma_rate.cu)"},
+                                     "what": "TMA L2->shared bytes per launch / time vs 85 B/cycle/SM x 148 SMs "
+                                             "(8 KB 3D boxes from L2, measured: tools/microbench/tma_rate.cu)"},
                          "alu_equiv": {"peak": fp32_peak, "frac": achieved / fp32_peak,
                                        "what": "algorithmic flops / time vs the FP32 FMA roof the plain kernels face"},
                          "kernel": dom["name"] + " on tcgen05 (band_u, 2xFP16)"})

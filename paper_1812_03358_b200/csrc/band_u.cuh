@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
   constexpr int U_STAGES = UStage<F16, OUT16>::STAGES, U_STAGE_BYTES = UStage<F16, OUT16>::BYTES;
   constexpr int U_STAGE_OUT = UStage<F16, OUT16>::OUT;
   static_assert(UStage<true>::STAGES * UStage<true>::BYTES == 4 * 49152, "same ring size");
-  static_assert(UStage<F16, OUT16>::STAGES * UStage<F16, OUT16>::BYTES + 8 * U_STAGE_OUT + 1024 + 256 <= U_SMEM,
+  static_assert(UStage<F16, OUT16>::STAGES * UStage<F16, OUT16>::BYTES + 8 * U_STAGE_OUT + 1024 + 256 +
+                    (OUT16 ? 4096 : 0) <= U_SMEM,
                 "shared memory");
   extern __shared__ uint8_t u_smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)u_smem_raw + 1023) & ~(uintptr_t)1023);
@@ -172,15 +173,19 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         const int mt = ui.mt, nt = ui.nt, b0 = ui.b0, b1 = ui.b1;
         const bool rev = (mt & 1) != 0;
         int li = 0;  // live-block index in producer order (split-K chunks)
+        // block starts read one block ahead, so the load's latency overlaps the previous block's wait and issue
+        int k_next = b0 < b1 ? __ldg(a.blk_k0 + (rev ? b1 - 1 : b0)) : 0;
         for (int j = b0; j < b1; ++j) {
           const int b = rev ? b0 + b1 - 1 - j : j;
-          if (a.windowed && !u_live(a, b)) continue;
+          const int k_raw = k_next;
+          if (j + 1 < b1) k_next = __ldg(a.blk_k0 + (rev ? b0 + b1 - 2 - j : j + 1));
+          if (a.windowed && !(k_raw + 16 > a.k_shift && k_raw < a.k_end)) continue;  // (u_live)
           if constexpr (SPLIT) {
             const int my = li++;
             if (my < ui.lo) continue;
             if (my >= ui.hi) break;
           }
-          const int k = __ldg(a.blk_k0 + b) - a.k_shift;  // before the wait: off the issue path
+          const int k = k_raw - a.k_shift;
           uint8_t* st = sm + s * U_STAGE_BYTES;
           mbar_wait(&empty[s], ph ^ 1);
           if constexpr (F16) {  // fp16 weight images (8 KB); pre-split fp16 source hi and lo, 4 boxes of 16 rows x 64
@@ -314,11 +319,17 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       float acc[128];
 #pragma unroll
       for (int c = 0; c < 128; ++c) acc[c] = 0.f;
-      // OUT16 with per-column source scales: lane l holds the factors of its half's columns 4l..4l+3 (loaded while
-      // the MMAs run; the epilogue broadcasts them with shuffles)
+      // OUT16: the multiplier of each of the warp's 128 columns, osig * scale * 2^-e_c (per-column source scales,
+      // or the global 2^-e), loaded while the MMAs run and kept in the warp's shared-memory table (all lanes read
+      // the same entry: broadcast).  Powers of two commute with the rounding, so (osig scale 2^-e) acc is
+      // bit-identical to osig (scale (2^-e acc)).
       float4 cv = make_float4(1.f, 1.f, 1.f, 1.f);
-      if constexpr (OUT16)
-        if (a.cinv) cv = __ldg(reinterpret_cast<const float4*>(a.cinv + ui.nt * 256 + h * 128) + lane);
+      if constexpr (OUT16) {
+        cv = a.cinv ? __ldg(reinterpret_cast<const float4*>(a.cinv + ui.nt * 256 + h * 128) + lane)
+                    : make_float4(inv_sig, inv_sig, inv_sig, inv_sig);
+        const float m = osig * a.scale;
+        cv = make_float4(m * cv.x, m * cv.y, m * cv.z, m * cv.w);
+      }
       for (int g0 = b0; g0 < b1; g0 += a.group) {
         mbar_wait(&tfull[buf], (tph >> buf) & 1u);
         tph ^= 1u << buf;
@@ -339,6 +350,7 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
       // output: per 32-column chunk the warp's 32 x 32 block goes through its swizzled staging buffer and one
       // TMA store (or TMA add when accumulating); rows / columns outside the output are clipped by the TMA unit
       uint8_t* stg = sout + (warp - 4) * U_STAGE_OUT;
+      float* mtab = reinterpret_cast<float*>(bars + 4 * U_STAGES + 8) + 128 * (warp - 4);  // OUT16: 512 B per warp
       const int r0 = (a.tile_mode == 0 ? mt * 128 + 32 * q
                                         : (2 * (mt / (a.tm_nz >> 6)) + (q >> 1)) * a.tm_nz + 64 * (mt % (a.tm_nz >> 6)) + 32 * (q & 1)) +
                      ui.kc * a.kc_rows;
@@ -349,24 +361,20 @@ __global__ void __launch_bounds__(U_THREADS, 1) band_u_kernel(const __grid_const
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
         if constexpr (OUT16) {  // fp16 hi / lo of 2^e' out: two 32 x 64 tiles, 128-byte rows, 128-byte swizzle
+          if (c == 0) {  // the warp's multiplier table, written once per item (the previous item's reads are done)
+            reinterpret_cast<float4*>(mtab)[lane] = cv;
+            __syncwarp();
+          }
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             uint32_t hw[4], lw[4];
-            float ci[8];
-            if (a.cinv) {
-              const int sl = (c + 8 * jj) >> 2;  // lanes sl, sl + 1 hold these 8 columns
-              ci[0] = __shfl_sync(0xffffffffu, cv.x, sl); ci[1] = __shfl_sync(0xffffffffu, cv.y, sl);
-              ci[2] = __shfl_sync(0xffffffffu, cv.z, sl); ci[3] = __shfl_sync(0xffffffffu, cv.w, sl);
-              ci[4] = __shfl_sync(0xffffffffu, cv.x, sl + 1); ci[5] = __shfl_sync(0xffffffffu, cv.y, sl + 1);
-              ci[6] = __shfl_sync(0xffffffffu, cv.z, sl + 1); ci[7] = __shfl_sync(0xffffffffu, cv.w, sl + 1);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) ci[i] = inv_sig;
-            }
+            const float4 m0 = reinterpret_cast<const float4*>(mtab)[(c >> 2) + 2 * jj];
+            const float4 m1 = reinterpret_cast<const float4*>(mtab)[(c >> 2) + 2 * jj + 1];
+            const float ci[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float x0 = osig * (a.scale * (ci[2 * i] * acc[c + 8 * jj + 2 * i]));
-              const float x1 = osig * (a.scale * (ci[2 * i + 1] * acc[c + 8 * jj + 2 * i + 1]));
+              const float x0 = ci[2 * i] * acc[c + 8 * jj + 2 * i];
+              const float x1 = ci[2 * i + 1] * acc[c + 8 * jj + 2 * i + 1];
               const __half2 hh = __floats2half2_rn(x0, x1);
               const float2 hf = __half22float2(hh);
               const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);

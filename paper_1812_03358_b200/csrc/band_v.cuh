@@ -287,6 +287,13 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
       float acc[EC];
 #pragma unroll
       for (int c = 0; c < EC; ++c) acc[c] = 0.f;
+      // IN16 forward: this lane's voxel-row scale 2^-e_row, loaded before the MMAs are waited for
+      float f_row = in_inv;
+      if constexpr (IN16)
+        if (a.rinv) {
+          const int vt = mt * 128 + 32 * q + lane;
+          f_row = vt < a.ny ? __ldg(a.rinv + (size_t)n * a.ny + vt) : 1.f;
+        }
       for (int g0 = b0; g0 < b1; g0 += a.group) {
         mbar_wait(&tfull[buf], (tph >> buf) & 1u);
         tph ^= 1u << buf;
@@ -314,15 +321,9 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         if (lane == 0) mbar_arrive(&tempty[buf]);
         buf ^= 1;
       }
-      if constexpr (IN16) {
-        float f = in_inv;
-        if (a.rinv) {  // this lane's voxel row of slice n
-          const int vt = mt * 128 + 32 * q + lane;
-          f = vt < a.ny ? __ldg(a.rinv + (size_t)n * a.ny + vt) : 1.f;
-        }
-#pragma unroll
-        for (int c = 0; c < EC; ++c) acc[c] *= f;  // exact
-      }
+      // one multiplier per value: the data scale (a power of two: 2^-e_row or 2^-e) times scale, times the U scale
+      // 2^e (OUT16) -- bit-identical to applying them one after another (powers of two commute with the rounding)
+      const float mul = (IN16 ? f_row : 1.f) * a.scale * (OUT16 ? sig : 1.f);
       const int vt0 = mt * 128 + 32 * q, c0 = nt * N + h * EC;
 #pragma unroll
       for (int c = 0; c < EC; c += OC) {
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float x0 = sig * (a.scale * acc[c + 8 * jj + 2 * i]), x1 = sig * (a.scale * acc[c + 8 * jj + 2 * i + 1]);
+              const float x0 = mul * acc[c + 8 * jj + 2 * i], x1 = mul * acc[c + 8 * jj + 2 * i + 1];
               const __half2 hh = __floats2half2_rn(x0, x1);
               const float2 hf = __half22float2(hh);
               const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
@@ -350,15 +351,15 @@ __global__ void __launch_bounds__(V_THREADS, 1) band_v_kernel(const __grid_const
         } else if constexpr (OC == 32) {  // 128-byte rows, 128-byte swizzle
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
-            const float4 v = make_float4(a.scale * acc[c + 4 * jj], a.scale * acc[c + 4 * jj + 1],
-                                         a.scale * acc[c + 4 * jj + 2], a.scale * acc[c + 4 * jj + 3]);
+            const float4 v = make_float4(mul * acc[c + 4 * jj], mul * acc[c + 4 * jj + 1], mul * acc[c + 4 * jj + 2],
+                                         mul * acc[c + 4 * jj + 3]);
             *reinterpret_cast<float4*>(stg + lane * 128 + ((jj ^ (lane & 7)) << 4)) = v;
           }
         } else {  // OC-float rows, no swizzle
 #pragma unroll
           for (int jj = 0; jj < OC; jj += 4) {
-            const float4 v = make_float4(a.scale * acc[c + jj], a.scale * acc[c + jj + 1], a.scale * acc[c + jj + 2],
-                                         a.scale * acc[c + jj + 3]);
+            const float4 v = make_float4(mul * acc[c + jj], mul * acc[c + jj + 1], mul * acc[c + jj + 2],
+                                         mul * acc[c + jj + 3]);
             *reinterpret_cast<float4*>(stg + lane * OC * 4 + jj * 4) = v;
           }
         }
