@@ -2428,7 +2428,7 @@ __device__ inline void block_sum_store(double (&v)[NV], double* part) {
 // stats: [sum w y Ax, sum w y y, sum w Ax Ax] (fp64 products and sums; float4 loads when the three vectors are
 // 16-byte aligned, the n % 4 tail by the first threads)
 template <bool VEC>
-__global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float* __restrict__ Ax,
+__global__ void __launch_bounds__(RED_THREADS, STATS_BLOCKS / 148) stats_partial_kernel(const float* __restrict__ Ax,
                                                                     const float* __restrict__ y,
                                                                     const float* __restrict__ w, long long n,
                                                                     double* part) {
@@ -2441,16 +2441,18 @@ __global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float*
   };
   long long i0 = t;
   if (VEC) {
-    // four float4 of each vector per iteration: twelve 16-byte loads in flight before the fp64 sums need them
-    // (one round covers a 2048^2 detector with the 1184 x 256 threads)
+    // LD float4 of each vector per iteration: 3 LD 16-byte loads in flight before the fp64 sums need them; LD = 2
+    // keeps the kernel at 64 registers, so all STATS_BLOCKS (4 per SM) are resident in one wave (with LD = 4 it took
+    // 124 registers: 2 blocks per SM, two waves)
+    constexpr int LD = 2;
     const long long n4 = n >> 2;
     const float4* A4 = reinterpret_cast<const float4*>(Ax);
     const float4* Y4 = reinterpret_cast<const float4*>(y);
     const float4* W4 = reinterpret_cast<const float4*>(w);
-    for (long long i = t; i < n4; i += 4 * stride) {  // every lane's 4 x 3 loads issued before any sum
-      float4 a[4], b[4], c[4];
+    for (long long i = t; i < n4; i += LD * stride) {  // every lane's LD x 3 loads issued before any sum
+      float4 a[LD], b[LD], c[LD];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < LD; ++j) {
         const long long k = i + j * stride;
         const bool ok = k < n4;
         a[j] = ok ? __ldg(A4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -2458,7 +2460,7 @@ __global__ void __launch_bounds__(RED_THREADS) stats_partial_kernel(const float*
         c[j] = ok ? __ldg(W4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < LD; ++j)
         if (i + j * stride < n4) {
           acc(a[j].x, b[j].x, c[j].x); acc(a[j].y, b[j].y, c[j].y); acc(a[j].z, b[j].z, c[j].z); acc(a[j].w, b[j].w, c[j].w);
         }
@@ -2538,25 +2540,41 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const float* __re
 // voxel instead of 26).  Neighbours outside the grid contribute nothing: their shared values are 0, so their terms
 // are x_j, taken back out after the sum (n_out x_j); the sum runs in the order dz, dy, dx ascending.
 constexpr int R26_ZC = 16, R26_TY = 8, R26_NT = 32 * R26_TY;
-template <bool COST>
+// VEC (nx % 4 == 0): the footprint rows are loaded as 10 aligned float4 [x0 - 4, x0 + 36) (16-byte cp.async, whole
+// float4s in or out of the grid), so the load loop issues 1800 instead of 6120 copies per block with cheaper index
+// arithmetic -- the kernel is issue-bound (ncu: 79 % issue-active, integer pipe 65 %), not DRAM-bound.
+template <bool COST, bool VEC>
 __global__ void __launch_bounds__(R26_NT) reg26_kernel(const float* __restrict__ x, float* __restrict__ grad, int nx,
                                                     int ny, int nz, float beta, float nu, double* part) {
-  constexpr int PX = 34, PY = R26_TY + 2, PP = PX * PY;
-  __shared__ float pl[R26_ZC + 2][PY][PX];
+  constexpr int PX = VEC ? 40 : 34, XO = VEC ? 3 : 0, PY = R26_TY + 2, PP = PX * PY;
+  __shared__ __align__(16) float pl[R26_ZC + 2][PY][PX];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * R26_TY, z0 = blockIdx.z * R26_ZC;
   const int ix = x0 + tx, iy = y0 + ty;
   const size_t plane = (size_t)nx * ny;
-  constexpr int NE = (R26_ZC + 2) * PP;
-  // the footprint straight into shared memory (cp.async, 4 bytes; zero-filled outside the grid): every load in
-  // flight at once without holding registers, so two blocks fit an SM and one's loads overlap the other's sums
-  for (int e = tid; e < NE; e += R26_NT) {
-    const int pz = e / PP, r = e - pz * PP, ly = r / PX, lx = r - ly * PX;
-    const int gx = x0 + lx - 1, gy = y0 + ly - 1, zz = z0 + pz - 1;
-    const bool ok = zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
-    const float* src = ok ? x + (size_t)zz * plane + (size_t)gy * nx + gx : x;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(&pl[0][0][0] + e)),
-                 "l"(src), "r"(ok ? 4 : 0) : "memory");
+  if constexpr (VEC) {
+    constexpr int NV = (R26_ZC + 2) * PY * 10;  // float4 per block
+    for (int e = tid; e < NV; e += R26_NT) {
+      const int row = e / 10, lv = e - row * 10;  // row = pz * PY + ly
+      const int pz = row / PY, ly = row - pz * PY;
+      const int gx = x0 - 4 + 4 * lv, gy = y0 + ly - 1, zz = z0 + pz - 1;
+      const bool ok = zz >= 0 && zz < nz && gy >= 0 && gy < ny && gx >= 0 && gx < nx;
+      const float* src = ok ? x + (size_t)zz * plane + (size_t)gy * nx + gx : x;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(&pl[0][0][0] + 4 * e)),
+                   "l"(src), "r"(ok ? 16 : 0) : "memory");
+    }
+  } else {
+    constexpr int NE = (R26_ZC + 2) * PP;
+    // the footprint straight into shared memory (cp.async, 4 bytes; zero-filled outside the grid): every load in
+    // flight at once without holding registers, so two blocks fit an SM and one's loads overlap the other's sums
+    for (int e = tid; e < NE; e += R26_NT) {
+      const int pz = e / PP, r = e - pz * PP, ly = r / PX, lx = r - ly * PX;
+      const int gx = x0 + lx - 1, gy = y0 + ly - 1, zz = z0 + pz - 1;
+      const bool ok = zz >= 0 && zz < nz && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+      const float* src = ok ? x + (size_t)zz * plane + (size_t)gy * nx + gx : x;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(&pl[0][0][0] + e)),
+                   "l"(src), "r"(ok ? 4 : 0) : "memory");
+    }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -2568,17 +2586,51 @@ __global__ void __launch_bounds__(R26_NT) reg26_kernel(const float* __restrict__
 #pragma unroll
     for (int q = 0; q < R26_ZC; ++q)
       gin[q] = z0 + q < nz ? grad[(size_t)(z0 + q) * plane + (size_t)iy * nx + ix] : 0.f;
+    if constexpr (VEC && !COST) {
+      // gradient only (the FISTA loop): sum_{l in N_j} (x_j - x_l) = n_in x_j - sum_{l in N_j} x_l, with the
+      // neighbour sum taken as 3 x 3 plane sums that slide along z (each plane summed once, not three times) and
+      // the out-of-grid neighbours zero in the footprint: (27 - n_out) x_j - (S_{z-1} + S_z + S_{z+1}).  About a
+      // third of the instructions of the literal 26-difference order (which the cost path keeps); the two differ
+      // by fp32 summation order only.
+      float S[3], xc[3];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        float r[3];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+          r[dy] = (pl[d][ty + dy][tx + XO] + pl[d][ty + dy][tx + XO + 1]) + pl[d][ty + dy][tx + XO + 2];
+        S[d] = (r[0] + r[1]) + r[2];
+        xc[d] = pl[d][ty + 1][tx + XO + 1];
+      }
+#pragma unroll
+      for (int q = 0; q < R26_ZC; ++q) {
+        const int iz = z0 + q;
+        if (iz >= nz) break;
+        {
+          float r[3];
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+            r[dy] = (pl[q + 2][ty + dy][tx + XO] + pl[q + 2][ty + dy][tx + XO + 1]) + pl[q + 2][ty + dy][tx + XO + 2];
+          S[(q + 2) % 3] = (r[0] + r[1]) + r[2];
+          xc[(q + 2) % 3] = pl[q + 2][ty + 1][tx + XO + 1];
+        }
+        const float xj = xc[(q + 1) % 3];
+        const int n_out = 27 - (1 + (iz > 0) + (iz < nz - 1)) * cxy;
+        const float g = (float)(27 - n_out) * xj - ((S[q % 3] + S[(q + 1) % 3]) + S[(q + 2) % 3]);
+        grad[(size_t)iz * plane + (size_t)iy * nx + ix] = gin[q] + (beta * g + nu);
+      }
+    } else {
     float P[3][9];  // 3 x 3 neighbourhoods of planes q, q+1, q+2 (z-1, z, z+1) of the footprint
 #pragma unroll
     for (int d = 0; d < 2; ++d)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) P[d][k] = pl[d][ty + k / 3][tx + k % 3];
+      for (int k = 0; k < 9; ++k) P[d][k] = pl[d][ty + k / 3][tx + XO + k % 3];
 #pragma unroll
     for (int q = 0; q < R26_ZC; ++q) {
       const int iz = z0 + q;
       if (iz >= nz) break;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) P[(q + 2) % 3][k] = pl[q + 2][ty + k / 3][tx + k % 3];
+      for (int k = 0; k < 9; ++k) P[(q + 2) % 3][k] = pl[q + 2][ty + k / 3][tx + XO + k % 3];
       const float xj = P[(q + 1) % 3][4];
       // all 26 differences in the order dz, dy, dx (outside the grid the shared value is 0, so such a term is x_j);
       // the n_out of them are taken back out after the sum (interior voxels: n_out = 0, the plain sum)
@@ -2603,6 +2655,7 @@ __global__ void __launch_bounds__(R26_NT) reg26_kernel(const float* __restrict__
       const size_t i = (size_t)iz * plane + (size_t)iy * nx + ix;
       grad[i] = gin[q] + (beta * g + nu);
       if (COST) v += (double)nu * xj + 0.25 * (double)beta * rs;
+    }
     }
   }
   if (COST) {
@@ -2714,12 +2767,15 @@ lfm_status k_reg26(const float* x, float* grad, int nx, int ny, int nz, float be
   dim3 grid((nx + 31) / 32, (ny + R26_TY - 1) / R26_TY, (nz + R26_ZC - 1) / R26_ZC), blk(32, R26_TY);
   const long long nblk = (long long)grid.x * grid.y * grid.z;
   if (cost && nblk > 4096 * 4) { err = "reg26: volume too large for the reduction partials"; return LFM_E_INVALID; }
+  const bool vec = nx % 4 == 0 && ((uintptr_t)x & 15) == 0 && !std::getenv("LFM_R26_SCALAR");
   if (cost) {
-    reg26_kernel<true><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, part);
+    if (vec) reg26_kernel<true, true><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, part);
+    else reg26_kernel<true, false><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, part);
     reduce_final_kernel<<<1, 256, 0, (cudaStream_t)s>>>(part, (int)nblk, 1, cost, 0);
     g_launches += 2;
   } else {
-    reg26_kernel<false><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, nullptr);
+    if (vec) reg26_kernel<false, true><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, nullptr);
+    else reg26_kernel<false, false><<<grid, blk, 0, (cudaStream_t)s>>>(x, grad, nx, ny, nz, beta, nu, nullptr);
     ++g_launches;
   }
   return cuda_check(cudaGetLastError(), "reg26", err);

@@ -80,3 +80,47 @@ def test_nonfinite_cost_status():
     rec.gradient(dev(x), with_cost=False)   # no cost requested: no check, no error
     torch.cuda.synchronize()
     assert np.isnan(host(rec.grad)).any()
+
+
+@pytest.mark.parametrize("n", [64, 96])
+def test_reg26_vector_and_scalar_footprints_agree(n, monkeypatch):
+    """The regulariser gradient (+ cost) with the float4 footprint loads (nx % 4 == 0) and with the scalar loads
+    (LFM_R26_SCALAR, read per call) is the same arithmetic on the same values: bit-identical, several blocks in
+    every direction and a partial 16-slice z chunk (nz = n - 24)."""
+    import torch
+    from paper_1812_03358_b200 import lfm
+    from workloads import normal_vector
+    from workloads.geometry import plenoptic_camera, volume
+    cfg = dict(volume=volume(n, 0.4), cameras=[plenoptic_camera(4, 8, 0.04, 2, 2)])
+    cfg["volume"]["nz"] = n - 24   # a partial 16-slice chunk
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    nv = plan.infos[0]["n_vox"]
+    x = torch.as_tensor(normal_vector(nv, 7), device="cuda:0")
+    outs = []
+    for scalar in (False, True):
+        if scalar:
+            monkeypatch.setenv("LFM_R26_SCALAR", "1")
+        else:
+            monkeypatch.delenv("LFM_R26_SCALAR", raising=False)
+        g = torch.empty(nv, device="cuda:0")
+        cost = torch.zeros(2, dtype=torch.float64, device="cuda:0")
+        lfm.pwls_grad(plan, x, [], [], [], None, 0.05, 0.01, g, ws, cost=cost, cam0=0, cam1=0, include_reg=True)
+        torch.cuda.synchronize()
+        outs.append((g.cpu(), cost.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    # gradient only (the FISTA loop's call): the float4 path sums the neighbours as sliding 3 x 3 plane sums, the
+    # scalar one as the literal 26 differences -- the same value up to fp32 summation order
+    gs = []
+    for scalar in (False, True):
+        if scalar:
+            monkeypatch.setenv("LFM_R26_SCALAR", "1")
+        else:
+            monkeypatch.delenv("LFM_R26_SCALAR", raising=False)
+        g = torch.empty(nv, device="cuda:0")
+        lfm.pwls_grad(plan, x, [], [], [], None, 0.05, 0.01, g, ws, cam0=0, cam1=0, include_reg=True)
+        torch.cuda.synchronize()
+        gs.append(g.cpu().double())
+    assert torch.equal(gs[1], outs[1][0].double())   # the scalar gradient is the same with and without the cost
+    assert float((gs[0] - gs[1]).abs().max() / gs[1].abs().max()) <= 1e-6
