@@ -210,3 +210,35 @@ def test_zero_input_and_errors():
     assert e.value.status == 1
     with pytest.raises(lfm.LfmError):
         lfm.A_forward(plan, 5, torch.zeros(op.n_vox, device="cuda:0"), y, ws)
+
+
+@pytest.mark.parametrize("n_lens,dynamic", [(5, False), (5, True), (7, True)])
+def test_collapsed_f16_column_strips(n_lens, dynamic):
+    """The 2xFP16 collapsed path on detectors whose width is a multiple of 8 but not of 16 (40 and 56 columns: the
+    column-scaled split's last 16-column strip is half empty, band_u's last 256-column tile ragged) against the
+    oracle; `dynamic`: detector columns scaled by 10^(-6 .. 0) and voxel rows by 10^(-4 .. 0), so the per-column
+    (adjoint input) and per-row (x^r) fp16 scales differ by orders of magnitude across the data."""
+    from paper_1812_03358_b200 import lfm
+    from oracle.system import build_system
+    from workloads.geometry import plenoptic_camera, pose_yaw, volume
+    cfg = dict(volume=volume(16, 0.4), cameras=[plenoptic_camera(n_lens, 8, 0.04, 2, 2),
+                                                plenoptic_camera(n_lens, 8, 0.04, 2, 2, pose=pose_yaw(20.0))])
+    plan = lfm.Plan(cfg, device=0)
+    assert plan.infos[0]["f16_stage"] == [1, 1], plan.infos[0]["f16_stage"]
+    ws = plan.workspace()
+    ops = build_system(cfg)
+    x = uniform_volume(cfg["volume"], 0)
+    if dynamic:
+        x = (x * (10.0 ** np.linspace(-4, 0, x.shape[1]))[None, :, None]).astype(np.float32)
+    for c, op in enumerate(ops):
+        n_s = cfg["cameras"][c]["n_s"]
+        y = torch.empty(op.n_pix, device="cuda:0")
+        lfm.A_forward(plan, c, dev(x).reshape(-1), y, ws, path=1)
+        assert max_rel(host(y), op.forward(x.astype(np.float64).ravel())) <= TOL, (n_lens, dynamic, c, "forward")
+        r = uniform_vector(op.n_pix, 1).reshape(-1, n_s)
+        if dynamic:
+            r = (r * 10.0 ** np.linspace(-6, 0, n_s)[None, :]).astype(np.float32)
+        r = r.ravel()
+        g = torch.empty(op.n_vox, device="cuda:0")
+        lfm.A_adjoint(plan, c, dev(r), g, ws, path=1)
+        assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL, (n_lens, dynamic, c, "adjoint")
