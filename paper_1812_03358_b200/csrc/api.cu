@@ -246,21 +246,41 @@ static bool cols_split() {
   return !off;
 }
 
-// The adjoint t pass (c1) of y's rows [r0, r1): 2xFP16 = maxima of those rows, fp16 hi / lo of 2^e y into w.h16
-// (done once per call, `split_done`), then band_u from them.
+// The PWLS residual r = w (Ax - gamma[cam] y) as the adjoint's input, computed inside the t pass's input split
+// (lfm_pwls_grad passes it instead of a materialised r when that split is the column-scaled one, see res_fusable)
+struct ResSrc {
+  const float* Ax;
+  const float* y;
+  const float* w;
+  const double* gamma;
+  int cam;
+};
+static bool al16p(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// The adjoint t pass (c1) of y's rows [r0, r1): 2xFP16 = fp16 hi / lo of y (scaled per column, or by 2^e from the
+// maxima of those rows) into w.h16 -- done once per call and kind (`split_state`: 0 none, 1 global scale, 2 column
+// scales), then band_u from them.  res != nullptr: y is the residual of *res (only with column scales).
 static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* y, const Ws& w, void* stream, Win win,
-                            bool& split_done, bool z16 = false) {
-  if (!f16_adj(cp, c1)) return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1);
+                            int& split_state, bool z16 = false, const ResSrc* res = nullptr) {
+  if (!f16_adj(cp, c1)) {
+    if (res) return fail(LFM_E_INVALID, "internal: fused residual without the 2xFP16 t pass");
+    return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1);
+  }
   const int n_s = cp.info.n_s, r0 = std::max(0, win.r0), r1 = win.r1 < 0 ? cp.info.n_t : std::min(win.r1, cp.info.n_t);
   const size_t np = (size_t)cp.info.n_pix;
   // column scales: with the fp16 Z output only (band_u's OUT16 epilogue applies them), 16-byte aligned rows of y
   // (n_s % 8 == 0 already holds for the 2xFP16 form)
-  const bool cs = cols_split() && z16 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
-  if (!split_done && r1 > r0) {
+  const bool cs = cols_split() && z16 && (res ? al16p(res->Ax) && al16p(res->y) && al16p(res->w) : al16p(y));
+  if (res && !cs) return fail(LFM_E_INVALID, "internal: fused residual without the column-scaled split");
+  const int need = cs ? 2 : 1;
+  if (split_state != need && r1 > r0) {
     std::string err;
     const long long off = (long long)r0 * n_s, n = (long long)(r1 - r0) * n_s;
     lfm_status st;
-    if (cs) {
+    if (cs && res) {
+      st = k_split16_cols_residual(res->Ax + off, res->y + off, res->w + off, res->gamma, res->cam, r1 - r0, n_s,
+                                   (n_s + 255) / 256 * 256, w.am, w.cs, w.h16 + off, w.h16 + np + off, stream, err);
+    } else if (cs) {
       st = k_split16_cols(y + off, r1 - r0, n_s, (n_s + 255) / 256 * 256, w.am, w.cs, w.h16 + off, w.h16 + np + off,
                           stream, err);
     } else {
@@ -269,7 +289,7 @@ static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* 
     }
     if (st != LFM_OK) return fail(st, err);
   }
-  split_done = true;
+  split_state = need;
   F16Src h;
   h.hi = w.h16;
   h.lo = w.h16 + np;
@@ -281,6 +301,20 @@ static lfm_status t_adjoint(const CameraPlan& cp, const SepOp& c1, const float* 
     h.out_scale16 = c1.ft->u_lsum;
   }
   return sep(c1, y, w.z, 0, 1, 0, stream, 0, -1, win.r0, win.r1, win.c0, win.c1, nullptr, 0, h);
+}
+
+// the adjoint's t pass can hand band_v an fp16 Z (every term's tables have the 2xFP16 forms)
+static bool z16_ok(const CameraPlan& cp, const SepOp& c1, const VTab& va);
+static int eff_path(const CameraPlan& cp, int path);
+// lfm_pwls_grad may fuse the residual into the adjoint's input split: the camera's whole adjoint runs the
+// collapsed tcgen05 path with the column-scaled split in every term (LFM_NO_FUSED_RES=1: the residual kernel first)
+static bool res_fusable(const CameraPlan& cp, int path, const float* Ax, const float* y, const float* wv) {
+  if (std::getenv("LFM_NO_FUSED_RES") || eff_path(cp, path) != LFM_PATH_COLLAPSED || !cols_split()) return false;
+  if (!(al16p(Ax) && al16p(y) && al16p(wv))) return false;
+  if (!f16_adj(cp, cp.adj_c1) || !z16_ok(cp, cp.adj_c1, cp.va)) return false;
+  for (const Component& cm : cp.comps)
+    if (!f16_adj(cp, cm.adj_c1) || !z16_ok(cp, cm.adj_c1, cm.va)) return false;
+  return true;
 }
 
 // the adjoint's t pass can hand band_v an fp16 Z (every term's tables have the 2xFP16 forms)
@@ -364,7 +398,7 @@ __global__ void mask_window_kernel(const float* __restrict__ y, float* __restric
 
 // x (+)= A_c^T P y, P keeping the window rows [r0, r1) x columns [c0, c1) of y (others treated as zero).
 lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x, int accumulate, const Ws& w,
-                        void* stream, Win win = Win()) {
+                        void* stream, Win win = Win(), const ResSrc* res = nullptr) {
   int r0 = win.r0, r1 = win.r1;
   path = eff_path(cp, path);
   const bool rot = cp.info.rot_passes != 0;
@@ -383,9 +417,9 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
   }
   if (path == LFM_PATH_COLLAPSED) {
     // one output: all (vt, n) rows; the column window selects the 256-column tiles of Z
-    bool split_done = false;
+    int split_state = 0;
     const bool z16 = z16_ok(cp, cp.adj_c1, cp.va) && win.c0 % 8 == 0;  // fp16 Z maps start on 16-byte boundaries
-    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, win, split_done, z16));
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, win, split_state, z16, res));
     if (cp.adj_t == 2 || cp.adj_t == 3) {
       // direct s pass (spass_adj_kernel, or band_v on the tensor cores) on Z
       std::string err;
@@ -396,7 +430,7 @@ lfm_status adjoint_impl(const CameraPlan& cp, int path, const float* y, float* x
       // non-separable lenslet stage: the other terms' t and s passes, accumulated (tcgen05 path only, eff_path)
       for (const Component& cm : cp.comps) {
         const bool zc = z16_ok(cp, cm.adj_c1, cm.va) && win.c0 % 8 == 0;
-        TRY(t_adjoint(cp, cm.adj_c1, y, w, stream, win, split_done, zc));
+        TRY(t_adjoint(cp, cm.adj_c1, y, w, stream, win, split_state, zc, res));
         if ((st = k_vpass_adj(cp, cm.va, w.z, target, 1, stream, err, win.c0, win.c1, zc ? w.am : nullptr,
                               cm.adj_c1.ft->u_lsum)) != LFM_OK)
           return fail(st, err);
@@ -463,9 +497,9 @@ lfm_status adjoint_subset_impl(const CameraPlan& cp, int m, const float* y, floa
   float* target = rot ? w.r0 : x;
   const int acc = rot ? 0 : accumulate;
   if (subset_collapsed(cp, vo)) {
-    bool split_done = false;
+    int split_state = 0;
     const bool z16 = z16_ok(cp, cp.adj_c1, vo.va);
-    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, Win(), split_done, z16));
+    TRY(t_adjoint(cp, cp.adj_c1, y, w, stream, Win(), split_state, z16));
     std::string err;
     lfm_status st = k_vpass_adj(cp, vo.va, w.z, target, acc, stream, err, 0, -1, z16 ? w.am : nullptr,
                                 cp.adj_c1.ft->u_lsum);
@@ -714,8 +748,8 @@ lfm_status lfm_A_stage(lfm_plan p, int cam, int stage, const float* in, float* o
     st = sep(cp.fwd_c2, w.z, out, 0, 1, 0, stream, 0, -1, 0, -1, 0, -1, w.zt, cp.ws_z, h);
   } else if (stage == LFM_STAGE_ADJ_T) {
     if (!in) return fail(LFM_E_INVALID, "in is NULL");
-    bool split_done = false;  // 2xFP16: includes the maxima and split of `in` (part of the t pass's cost); Z in fp16
-    st = t_adjoint(cp, cp.adj_c1, in, w, stream, Win(), split_done, z16_ok(cp, cp.adj_c1, cp.va));
+    int split_state = 0;  // 2xFP16: includes the split of `in` (part of the t pass's cost); Z in fp16
+    st = t_adjoint(cp, cp.adj_c1, in, w, stream, Win(), split_state, z16_ok(cp, cp.adj_c1, cp.va));
   } else if (stage == LFM_STAGE_FWD_S || stage == LFM_STAGE_ADJ_S) {
     const bool fwd = stage == LFM_STAGE_FWD_S;
     if (fwd ? !in : !out) return fail(LFM_E_INVALID, fwd ? "in is NULL" : "out is NULL");
@@ -870,6 +904,12 @@ lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, c
   for (int c = cam0; c < cam1; ++c) {
     const CameraPlan& cp = p->cams[c];
     if (!y[c] || !wts[c] || !Ax[c]) return fail(LFM_E_INVALID, "NULL per-camera pointer");
+    if (!cost && subset < 0 && res_fusable(cp, path, Ax[c], y[c], wts[c])) {
+      // r never stored: the adjoint's column-scaled input split computes it from Ax, y, w
+      const ResSrc rs = {Ax[c], y[c], wts[c], gamma, c};
+      if ((st = adjoint_impl(cp, path, nullptr, grad, c > cam0, w, stream, Win(), &rs)) != LFM_OK) return st;
+      continue;
+    }
     st = k_residual(Ax[c], y[c], wts[c], gamma, c, w.s, cp.info.n_pix, w.p, cost, c > cam0, stream, err);
     if (st != LFM_OK) return fail(st, err);
     st = subset < 0 ? adjoint_impl(cp, path, w.s, grad, c > cam0, w, stream)

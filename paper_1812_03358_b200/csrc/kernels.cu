@@ -1780,10 +1780,37 @@ __device__ __forceinline__ void amax4(uint32_t (&m)[4], float4 v) {
   m[2] = max(m[2], __float_as_uint(v.z) & 0x7fffffffu);
   m[3] = max(m[3], __float_as_uint(v.w) & 0x7fffffffu);
 }
+// RES: the source is the PWLS residual r = w (Ax - gamma_cam y), computed from its three inputs on the load (the
+// arithmetic of residual_kernel), so r is never written and re-read (the residual fused into the
+// adjoint's input load).
+struct ResIn {
+  const float* Ax = nullptr;
+  const float* y = nullptr;
+  const float* w = nullptr;
+  const double* gamma = nullptr;
+  int cam = 0;
+};
+template <bool RES>
+__device__ __forceinline__ float4 split_src(const float* __restrict__ src, const ResIn& ri, float gm, long long o) {
+  if constexpr (!RES) {
+    return __ldg(reinterpret_cast<const float4*>(src + o));
+  } else {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(ri.Ax + o));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(ri.y + o));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(ri.w + o));
+    auto one = [&](float av, float bv, float cv) {
+      const float d = av - gm * bv;
+      return cv * d;
+    };
+    return make_float4(one(a.x, b.x, c.x), one(a.y, b.y, c.y), one(a.z, b.z, c.z), one(a.w, b.w, c.w));
+  }
+}
+template <bool RES>
 __global__ void __launch_bounds__(SPLITC_THREADS) split16_cols_kernel(const float* __restrict__ src, int rows, int cols,
                                                                       int cols_pad, float* __restrict__ part,
                                                                       float* __restrict__ cinv, uint16_t* __restrict__ hi,
-                                                                      uint16_t* __restrict__ lo) {
+                                                                      uint16_t* __restrict__ lo, ResIn ri) {
+  const float gm = RES ? (float)ri.gamma[ri.cam] : 0.f;
   __shared__ uint32_t red[SPLITC_THREADS / 32][SPLITC_SC];
   __shared__ float csig[SPLITC_SC];
   const int t = threadIdx.x, lane = t & 31, wp = t >> 5, q = t % SPLITC_QN, r_first = t / SPLITC_QN;
@@ -1797,11 +1824,11 @@ __global__ void __launch_bounds__(SPLITC_THREADS) split16_cols_kernel(const floa
 #pragma unroll
     for (int j = 0; j < SPLITC_KEEP; ++j) {
       const int r = r_first + j * SPLITC_RSTEP;
-      keep[j] = live && r < rows ? __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)) : make_float4(0, 0, 0, 0);
+      keep[j] = live && r < rows ? split_src<RES>(src, ri, gm, (long long)r * cols + c) : make_float4(0, 0, 0, 0);
       amax4(m, keep[j]);
     }
     for (int r = r_first + SPLITC_KEEP * SPLITC_RSTEP; r < rows; r += SPLITC_RSTEP)  // taller strips
-      if (live) amax4(m, __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)));
+      if (live) amax4(m, split_src<RES>(src, ri, gm, (long long)r * cols + c));
 #pragma unroll
     for (int o = SPLITC_QN; o < 32; o <<= 1)  // lanes of the same column quad
 #pragma unroll
@@ -1828,7 +1855,7 @@ __global__ void __launch_bounds__(SPLITC_THREADS) split16_cols_kernel(const floa
         if (r < rows) split_store(hi, lo, (long long)r * cols + c, keep[j], sg);
       }
       for (int r = r_first + SPLITC_KEEP * SPLITC_RSTEP; r < rows; r += SPLITC_RSTEP)
-        split_store(hi, lo, (long long)r * cols + c, __ldg(reinterpret_cast<const float4*>(src + (long long)r * cols + c)), sg);
+        split_store(hi, lo, (long long)r * cols + c, split_src<RES>(src, ri, gm, (long long)r * cols + c), sg);
     }
   }
   // strip padding past the last strip (cols_pad may exceed the strips' columns)
@@ -1851,9 +1878,30 @@ lfm_status k_split16_cols(const float* src, int rows, int cols, int cols_pad, fl
     return LFM_E_INVALID;
   }
   const int g = std::max(1, std::min(LFM_AMAX_SLOTS, (cols + SPLITC_SC - 1) / SPLITC_SC));
-  split16_cols_kernel<<<g, SPLITC_THREADS, 0, (cudaStream_t)stream>>>(src, rows, cols, cols_pad, part, cinv, hi, lo);
+  split16_cols_kernel<false><<<g, SPLITC_THREADS, 0, (cudaStream_t)stream>>>(src, rows, cols, cols_pad, part, cinv, hi, lo,
+                                                                             ResIn());
   ++g_launches;
   return cuda_check(cudaGetLastError(), "split16_cols_kernel launch", err);
+}
+
+lfm_status k_split16_cols_residual(const float* Ax, const float* y, const float* w, const double* gamma, int cam,
+                                   int rows, int cols, int cols_pad, float* part, float* cinv, uint16_t* hi, uint16_t* lo,
+                                   void* stream, std::string& err) {
+  if (cols % 4 || ((reinterpret_cast<uintptr_t>(Ax) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(w) |
+                    reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo)) & 15)) {
+    err = "split16_cols (residual): columns must be a multiple of 4 and rows 16-byte aligned";
+    return LFM_E_INVALID;
+  }
+  ResIn ri;
+  ri.Ax = Ax;
+  ri.y = y;
+  ri.w = w;
+  ri.gamma = gamma;
+  ri.cam = cam;
+  const int g = std::max(1, std::min(LFM_AMAX_SLOTS, (cols + SPLITC_SC - 1) / SPLITC_SC));
+  split16_cols_kernel<true><<<g, SPLITC_THREADS, 0, (cudaStream_t)stream>>>(nullptr, rows, cols, cols_pad, part, cinv, hi, lo, ri);
+  ++g_launches;
+  return cuda_check(cudaGetLastError(), "split16_cols_kernel (residual) launch", err);
 }
 
 lfm_status k_split16_rows(const float* src, int rows, int len, float* part, float* rinv, uint16_t* hi, uint16_t* lo,

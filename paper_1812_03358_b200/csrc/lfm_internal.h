@@ -281,6 +281,10 @@ lfm_status k_split16_rows(const float* src, int rows, int len, float* part, floa
 // columns [cols, cols_pad)), per-CTA maxima of |src| into part -- the adjoint t pass's input (one kernel)
 lfm_status k_split16_cols(const float* src, int rows, int cols, int cols_pad, float* part, float* cinv, uint16_t* hi,
                           uint16_t* lo, void* stream, std::string& err);
+// the same split of the PWLS residual r = w (Ax - gamma[cam] y) computed on the load (r itself never stored)
+lfm_status k_split16_cols_residual(const float* Ax, const float* y, const float* w, const double* gamma, int cam,
+                                   int rows, int cols, int cols_pad, float* part, float* cinv, uint16_t* hi, uint16_t* lo,
+                                   void* stream, std::string& err);
 // LFM_AMAX_SLOTS partial maxima of |src[0, n)| into part (one kernel)
 lfm_status k_amax(const float* src, long long n, float* part, void* stream, std::string& err);
 // fp16 hi / lo of 2^e src over n floats (e from the partial maxima `amax` of src), for the 2xFP16 band_u form

@@ -1518,6 +1518,22 @@ lfm_status build_camera(const lfm_volume& vol, const lfm_camera& cam, int n_subs
       }
       std::fprintf(stderr, "[lfm] tcgen05 form: %zu blocks of 128x16, density %.3f, %d tiles, blocks per tile %d..%d\n",
                    f->u_k0.size(), nnz / (2048.0 * f->u_k0.size()), (int)f->u_off.size() - 1, bmin, bmax);
+      {  // persistent-CTA load balance of 8 column tiles per row tile on 148 CTAs: round robin vs LPT
+        const int nt_ = (int)f->u_off.size() - 1, items = nt_ * 8, G = 148;
+        std::vector<double> rr(G, 0.0), lpt(G, 0.0);
+        std::vector<std::pair<int, int>> it;
+        for (int i = 0; i < items; ++i) {
+          const int c = f->u_off[i / 8 + 1] - f->u_off[i / 8] + 2;  // + ~2 blocks of per-item drain / epilogue
+          rr[i % G] += c;
+          it.push_back({c, i});
+        }
+        std::sort(it.begin(), it.end(), [](auto& a, auto& b) { return a.first > b.first; });
+        for (auto& p : it) *std::min_element(lpt.begin(), lpt.end()) += p.first;
+        double tot = 0;
+        for (double v : rr) tot += v;
+        std::fprintf(stderr, "[lfm]   148 CTAs: mean %.1f, round-robin max %.1f, LPT max %.1f (block units)\n", tot / G,
+                     *std::max_element(rr.begin(), rr.end()), *std::max_element(lpt.begin(), lpt.end()));
+      }
     }
     for (int G : {4, 8, 16})
       std::fprintf(stderr, "[lfm] MSEG density with %2d-row groups: ca1n %.3f  cf1n %.3f  ca0 %.3f  cf0 %.3f\n", G,

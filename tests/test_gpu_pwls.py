@@ -124,3 +124,36 @@ def test_reg26_vector_and_scalar_footprints_agree(n, monkeypatch):
         gs.append(g.cpu().double())
     assert torch.equal(gs[1], outs[1][0].double())   # the scalar gradient is the same with and without the cost
     assert float((gs[0] - gs[1]).abs().max() / gs[1].abs().max()) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["small_two", "small_hex", "128^3 two-camera"])
+def test_fused_residual_gradient(name, monkeypatch):
+    """lfm_pwls_grad without a cost fuses r = W (A z - gamma y) into the adjoint's column-scaled input split (r never
+    stored); with LFM_NO_FUSED_RES the residual kernel writes r first.  Same arithmetic per element, so the two
+    gradients are bit-identical; both match the oracle gradient on the small configs."""
+    import torch
+    from paper_1812_03358_b200 import lfm
+    from workloads import make_config, uniform_vector, uniform_volume
+    cfg = make_config(name)
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    n = plan.n_cam
+    x = torch.as_tensor(uniform_volume(cfg["volume"], 0), device="cuda:0").reshape(-1)
+    ys = [torch.as_tensor(uniform_vector(plan.infos[c]["n_pix"], 1 + c), device="cuda:0") for c in range(n)]
+    wts = [torch.as_tensor(0.5 + uniform_vector(plan.infos[c]["n_pix"], 7 + c), device="cuda:0") for c in range(n)]
+    Axs = [torch.empty(plan.infos[c]["n_pix"], device="cuda:0") for c in range(n)]
+    for c in range(n):
+        lfm.A_forward(plan, c, x, Axs[c], ws)
+    gamma = torch.tensor([1.0, 0.7, 1.3, 0.9][:n], dtype=torch.float64, device="cuda:0")
+    gs = []
+    for fused in (True, False):
+        if fused:
+            monkeypatch.delenv("LFM_NO_FUSED_RES", raising=False)
+        else:
+            monkeypatch.setenv("LFM_NO_FUSED_RES", "1")
+        g = torch.empty_like(x)
+        lfm.pwls_grad(plan, x, ys, wts, Axs, gamma, 0.01, 0.0, g, ws)
+        torch.cuda.synchronize()
+        gs.append(g.clone())
+    assert torch.equal(gs[0], gs[1])
+    assert torch.isfinite(gs[0]).all()
