@@ -242,3 +242,25 @@ def test_collapsed_f16_column_strips(n_lens, dynamic):
         g = torch.empty(op.n_vox, device="cuda:0")
         lfm.A_adjoint(plan, c, dev(r), g, ws, path=1)
         assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL, (n_lens, dynamic, c, "adjoint")
+
+
+def test_collapsed_tall_detector():
+    """A detector taller than the column-scaled split keeps in registers (2112 > 16 x 128 rows: the strip's extra
+    rows take the split's second pass) and wider than 8 band_u column tiles, on the collapsed path, against the
+    oracle (single-lens camera, 16^3 volume, pixel pitch matched to the voxels' image)."""
+    from paper_1812_03358_b200 import lfm
+    from oracle.system import build_system
+    from workloads.geometry import single_camera, volume
+    cfg = dict(volume=volume(16, 0.4), cameras=[single_camera(2112, 0.004, 2)])
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    op = build_system(cfg)[0]
+    r = uniform_vector(op.n_pix, 1)
+    g = torch.empty(op.n_vox, device="cuda:0")
+    lfm.A_adjoint(plan, 0, dev(r), g, ws, path=1)
+    assert max_rel(host(g), op.adjoint(r.astype(np.float64))) <= TOL
+    x = uniform_volume(cfg["volume"], 0)
+    y = torch.empty(op.n_pix, device="cuda:0")
+    lfm.A_forward(plan, 0, dev(x).reshape(-1), y, ws, path=1)
+    assert max_rel(host(y), op.forward(x.astype(np.float64).ravel())) <= TOL
+    assert plan.infos[0]["f16_stage"] == [1, 1], plan.infos[0]["f16_stage"]   # the 2xFP16 tcgen05 path ran
