@@ -260,7 +260,13 @@ lfm_status lfm_pwls_gains(lfm_plan p, const double* stats_dev, double* gamma_dev
  * is then ignored.  subset < 0: the exact gradient on `path`.
  * Non-finite cost: when cost_dev is non-NULL (and `stream` is not capturing a graph) the call
  * waits for the stream, reads the cost and returns LFM_E_NONFINITE if either part is NaN or infinite (grad and
- * cost_dev are still written).  Pass cost_dev = NULL for a call that never synchronises. */
+ * cost_dev are still written).  Pass cost_dev = NULL for a call that never synchronises.
+ * include_reg bit 0: add the regulariser term; bit 1 (LFM_GRAD_ACCUMULATE): grad already holds a partial
+ * gradient (other cameras' terms, computed concurrently on other streams): every term of this call is added to
+ * it and nothing is zeroed -- so cameras split over streams and summed in camera order, then a call with
+ * cam0 == cam1 and include_reg = 3, give the same sums in the same order as one call over all cameras.
+ * LFM_GRAD_ACCUMULATE with cost_dev != NULL is LFM_E_INVALID. */
+#define LFM_GRAD_ACCUMULATE 2
 lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, const float* x,
                          const float* const* y, const float* const* w, const float* const* Ax,
                          const double* gamma_dev, float beta, float nu, int include_reg,

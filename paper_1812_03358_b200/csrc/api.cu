@@ -897,7 +897,10 @@ lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, c
   if ((st = get_ws(p, ws, ws_bytes, w)) != LFM_OK) return st;
   std::string err;
   const long long nvox = (long long)p->vol.nx * p->vol.ny * p->vol.nz;
-  if (cam1 == cam0) {
+  const bool acc_in = (include_reg & LFM_GRAD_ACCUMULATE) != 0;  // grad holds a partial gradient: add to it
+  if (acc_in && cost) return fail(LFM_E_INVALID, "LFM_GRAD_ACCUMULATE with a cost");
+  include_reg &= 1;
+  if (cam1 == cam0 && !acc_in) {
     if ((st = k_fill(grad, nvox, 0.f, stream, err)) != LFM_OK) return fail(st, err);
     if (cost) cudaMemsetAsync(cost, 0, sizeof(double), (cudaStream_t)stream);
   }
@@ -907,13 +910,13 @@ lfm_status lfm_pwls_grad(lfm_plan p, int path, int subset, int cam0, int cam1, c
     if (!cost && subset < 0 && res_fusable(cp, path, Ax[c], y[c], wts[c])) {
       // r never stored: the adjoint's column-scaled input split computes it from Ax, y, w
       const ResSrc rs = {Ax[c], y[c], wts[c], gamma, c};
-      if ((st = adjoint_impl(cp, path, nullptr, grad, c > cam0, w, stream, Win(), &rs)) != LFM_OK) return st;
+      if ((st = adjoint_impl(cp, path, nullptr, grad, acc_in || c > cam0, w, stream, Win(), &rs)) != LFM_OK) return st;
       continue;
     }
     st = k_residual(Ax[c], y[c], wts[c], gamma, c, w.s, cp.info.n_pix, w.p, cost, c > cam0, stream, err);
     if (st != LFM_OK) return fail(st, err);
-    st = subset < 0 ? adjoint_impl(cp, path, w.s, grad, c > cam0, w, stream)
-                    : adjoint_subset_impl(cp, subset, w.s, grad, c > cam0, w, stream);
+    st = subset < 0 ? adjoint_impl(cp, path, w.s, grad, acc_in || c > cam0, w, stream)
+                    : adjoint_subset_impl(cp, subset, w.s, grad, acc_in || c > cam0, w, stream);
     if (st != LFM_OK) return st;
   }
   if (include_reg) {

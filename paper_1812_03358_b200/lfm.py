@@ -18,6 +18,7 @@ SINGLE, PLENOPTIC = 0, 1
 FWD, ADJ = 0, 1
 PER_VIEW, COLLAPSED = 0, 1
 MAJ_SUM, MAJ_FINISH = 1, 2
+GRAD_ACCUMULATE = 2  # lfm_pwls_grad include_reg bit 1 (include/lfm.h)
 STATUS = {0: "LFM_OK", 1: "LFM_E_INVALID", 2: "LFM_E_SINGULAR", 3: "LFM_E_DEGENERATE", 4: "LFM_E_MISMATCH",
           5: "LFM_E_ZERO_DATA", 6: "LFM_E_NONFINITE", 7: "LFM_E_CUDA", 8: "LFM_E_NOMEM"}
 TAB = dict(S1F_START=0, S1F_LEN=1, S1F_W64=2, S1A_START=3, S1A_LEN=4, S1A_W64=5, S3F_START=6, S3F_LEN=7,
