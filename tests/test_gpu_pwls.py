@@ -157,3 +157,32 @@ def test_fused_residual_gradient(name, monkeypatch):
         gs.append(g.clone())
     assert torch.equal(gs[0], gs[1])
     assert torch.isfinite(gs[0]).all()
+
+
+def test_grad_accumulate_contract():
+    """LFM_GRAD_ACCUMULATE: a call over no cameras with the regulariser adds R's gradient to grad (no zero fill),
+    so grad(cam 0..n) == grad(cameras, no reg) then (+reg, accumulate); with a cost it is rejected."""
+    import torch
+    from paper_1812_03358_b200 import lfm
+    from workloads import make_config, uniform_vector, uniform_volume
+    cfg = make_config("small_two")
+    plan = lfm.Plan(cfg, device=0)
+    ws = plan.workspace()
+    n = plan.n_cam
+    x = torch.as_tensor(uniform_volume(cfg["volume"], 0), device="cuda:0").reshape(-1)
+    ys = [torch.as_tensor(uniform_vector(plan.infos[c]["n_pix"], 1 + c), device="cuda:0") for c in range(n)]
+    wts = [torch.ones(plan.infos[c]["n_pix"], device="cuda:0") for c in range(n)]
+    Axs = [torch.empty(plan.infos[c]["n_pix"], device="cuda:0") for c in range(n)]
+    for c in range(n):
+        lfm.A_forward(plan, c, x, Axs[c], ws)
+    gamma = torch.tensor([1.0, 0.8], dtype=torch.float64, device="cuda:0")
+    g1 = torch.empty_like(x)
+    lfm.pwls_grad(plan, x, ys, wts, Axs, gamma, 0.02, 0.001, g1, ws)
+    g2 = torch.empty_like(x)
+    lfm.pwls_grad(plan, x, ys, wts, Axs, gamma, 0.02, 0.001, g2, ws, include_reg=False)
+    lfm.pwls_grad(plan, x, ys, wts, Axs, gamma, 0.02, 0.001, g2, ws, cam0=0, cam1=0, include_reg=1 | lfm.GRAD_ACCUMULATE)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2)
+    cost = torch.zeros(2, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(lfm.LfmError):
+        lfm.pwls_grad(plan, x, ys, wts, Axs, gamma, 0.02, 0.001, g2, ws, include_reg=1 | lfm.GRAD_ACCUMULATE, cost=cost)

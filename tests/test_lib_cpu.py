@@ -44,6 +44,15 @@ def test_exports_every_header_symbol():
     assert lfm.version().startswith("liblfm")
 
 
+def test_binding_constants_match_header():
+    """Every #define LFM_<NAME> <int> of include/lfm.h that the binding mirrors has the same value there."""
+    header = open(lfm.os.path.join(lfm._HERE, "..", "include", "lfm.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"^#define\s+LFM_(\w+)\s+(-?\d+)\s*$", header, re.M)}
+    mirrored = {"MAJ_SUM": lfm.MAJ_SUM, "MAJ_FINISH": lfm.MAJ_FINISH, "GRAD_ACCUMULATE": lfm.GRAD_ACCUMULATE}
+    for k, v in mirrored.items():
+        assert defs[k] == v, k
+
+
 def _oracle_s3_band(cam, ax, k):
     """Union over lenslets of band_mu(i) cap open cells of mu (reading Z9/Z10)."""
     n_det = cam.lenslet_planes[ax][0].n
